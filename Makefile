@@ -1,0 +1,22 @@
+# Product build: the C-ABI library with the sm_100a kernels, built in-tree so
+# it travels to the GPU box with the repo snapshot.
+NVCC ?= /usr/local/cuda/bin/nvcc
+PKG := paper_2012_14792_b200
+SRCS := $(wildcard $(PKG)/csrc/*.cu)
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/slicecraft_b200.h
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Iinclude --expt-relaxed-constexpr -Xptxas -v
+
+all: $(PKG)/libslicecraft_b200.so oracle
+
+$(PKG)/libslicecraft_b200.so: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -shared $(SRCS) -o $@ -lpthread 2> build_ptxas.log || (cat build_ptxas.log; false)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(PKG)/libslicecraft_b200.so build_ptxas.log
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

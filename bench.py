@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 TRS partitioner hot path (BASELINE.json metric).
+
+One STEP = one pass of the hot path over one batch of synthetic input: the
+K1 texture pass over the batch's luma frames, K2/K3 tables, and the two-step
+search (step 1 + step 2) for every frame of the batch.  Default workload:
+BASELINE config 3 (32 frames of 3840x2160 10-bit luma, 30x17 CTU grid,
+n=8 slices, exhaustive tile columns) -- the "at 4K" configuration the metric
+is quoted on that fits one GPU.  Config 1 is the reference's CPU-runnable
+case; configs 2/4/5 are parity cases (tests/).
+
+value  = TRS candidates scored per second over the whole job, inputs resident
+         in HBM (device pointers into sc_partition_frames).  A candidate is
+         one (frame, candidate) pair counted by the reference's own counters
+         (candidates_step1 + candidates_step2, search.hpp:41-43).
+e2e    = the same metric through the public C-ABI call with HOST (pinned)
+         buffers: the H2D copy of that step's luma + estimate maps and the D2H
+         of the per-frame results happen inside the timed region.
+Multi-GPU (torchrun): frames are independent once estimated,
+so every rank partitions its own batch (POCs offset by rank) -- weak scaling,
+no data-path collective; the timed region is barrier-bracketed and the max
+over ranks is reported.
+
+--impl reference runs the UNMODIFIED reference CPU path (oracle/_ref, built
+from /root/reference; the C oracle port when that is absent) on the host
+cores, one frame per thread, on a bounded prefix sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TRS candidates scored/sec & frames partitioned/sec at 4K; texture pass GB/s"
+UNIT = "candidates/s"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---- clocks sampler (nvidia-smi during the timed region) ------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- inputs ------------------------------------------------------------------------
+def make_inputs(w, rank, frames, pinned=True):
+    import torch
+    from paper_2012_14792_b200 import workloads as wl
+    first = rank * frames + 1
+    dt = torch.uint8 if w.bps == 1 else torch.int16
+    luma_t = torch.empty((frames, w.height, w.width), dtype=dt, pin_memory=pinned)
+    luma = luma_t.numpy().view(np.uint8 if w.bps == 1 else np.uint16)
+    wl.synth_luma(w, frames=frames, first_poc=first, out=luma)
+    tr = wl.cost_trace(w, frames=first + frames - 1)
+    est_t = torch.empty((frames, w.grid().cell_count()), dtype=torch.float64, pin_memory=pinned)
+    est_t.numpy()[:] = tr.est[first - 1:]
+    return luma_t, est_t
+
+
+# ---- our arm -------------------------------------------------------------------------
+def run_ours(args):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+    from paper_2012_14792_b200 import Partitioner, lib
+    from paper_2012_14792_b200._abi import SearchResult, check
+    from paper_2012_14792_b200 import workloads as wl
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = wl.WORKLOADS[args.config]
+    F = w.frames
+    g = w.grid()
+    cfg = w.cfg(mode=args.mode)
+    luma_h, est_h = make_inputs(w, rank, F)
+    luma_d = luma_h.cuda()
+    est_d = est_h.cuda()
+    torch.cuda.synchronize()
+
+    part = Partitioner(local)
+    stream = torch.cuda.current_stream()
+    check(lib().sc_ctx_set_stream(part._h, C.c_void_p(stream.cuda_stream)))
+    res = (SearchResult * F)()
+    bps = w.bps
+    pitch, fstride = w.width * bps, w.width * w.height * bps
+    gc, cc = g.c(), cfg.c()
+    tim = (C.c_double * 5)()
+
+    def call(luma_ptr, est_ptr):
+        check(lib().sc_partition_frames(part._h, C.byref(gc), C.byref(cc), C.c_void_p(luma_ptr),
+                                        bps, pitch, fstride, C.c_void_p(est_ptr), F, None,
+                                        C.cast(res, C.c_void_p)))
+        check(lib().sc_ctx_timings(part._h, tim))
+        return [tim[i] for i in range(5)]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (device-resident) ----
+    for _ in range(max(args.warmup, 0)):
+        call(luma_d.data_ptr(), est_d.data_ptr())
+    cands = sum(r.candidates_step1 + r.candidates_step2 for r in res)
+    counts = sorted({(r.candidates_step1, r.candidates_step2) for r in res})
+
+    # ---- timed: device-resident inputs ----
+    clocks = Clocks(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phase = np.zeros(5)
+    e0.record(stream)
+    for _ in range(args.steps):
+        phase += np.array(call(luma_d.data_ptr(), est_d.data_ptr()))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    phase /= args.steps
+
+    # ---- timed: end to end from pinned host buffers ----
+    barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        call(luma_h.data_ptr(), est_h.data_ptr())
+    e3.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3)) / args.steps
+
+    total_cands = cands * world
+    value = total_cands / (ms / 1e3)
+    e2e = total_cands / (ms_e2e / 1e3)
+    frames_total = F * world
+    luma_bytes = F * w.width * w.height * bps
+    rec_bytes = F * g.cell_count() * 24
+    tex_us, tab_us, s1_us, s2_us = phase[0], phase[1], phase[2], phase[3]
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    tex_gbs = (luma_bytes + rec_bytes) / (tex_us * 1e-6) / 1e9 if tex_us > 0 else None
+    # search roofline: integer-ALU issue.  The
+    # warp-instruction count per launch comes from the committed ncu capture
+    # of this same workload (the walk is frame-independent and warp-uniform,
+    # so the count is a property of the workload); time is measured live.
+    issue = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "search_issue.json")))
+        key = f"cfg{args.config}_mode{args.mode}"
+        if key in prof:
+            p = prof[key]
+            clk = ck.get("sm_mhz") or p.get("sm_mhz_ncu") or 1965.0
+            sms = torch.cuda.get_device_properties(local).multi_processor_count
+            peak = sms * 4 * clk * 1e6 / 1e9  # G warp-instr / s at the measured clock
+            ach = (p["warp_inst_step1"] / (s1_us * 1e-6) + p["warp_inst_step2"] / (s2_us * 1e-6)) \
+                / 2 / 1e9
+            issue = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2),
+                     "unit": "Gwarp-inst/s", "frac": round(ach / peak, 4),
+                     "traffic": p.get("dram_bytes_per_launch"),
+                     "ncu_issue_active_pct": p.get("issue_active_pct"),
+                     "source": "instructions: profiles/search_issue.json (ncu); time: live CUDA events"}
+    except Exception:
+        pass
+    if issue is None:
+        issue = {"bound": "alu", "achieved": None, "peak": None, "unit": "Gwarp-inst/s",
+                 "frac": None, "traffic": None, "note": "no ncu instruction count committed yet"}
+    tex_roof = {"bound": "hbm", "achieved": round(tex_gbs, 1) if tex_gbs else None,
+                "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(tex_gbs / hbm_peak, 4) if tex_gbs else None,
+                "traffic": None, "peak_source": hbm_src,
+                "algorithmic_bytes_per_launch": luma_bytes + rec_bytes,
+                "launch_us": round(tex_us, 2)}
+    try:
+        tp = json.load(open(os.path.join(ROOT, "profiles", "texture_traffic.json")))
+        tex_roof["traffic"] = tp.get(f"cfg{args.config}")
+    except Exception:
+        pass
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
+        "data": "synthetic (seeded; SURVEY.md §8d generator, no public dataset)",
+        "config": {"workload": w.name, "frames_per_rank": F, "frame": f"{w.width}x{w.height}",
+                   "bit_depth": w.bit_depth, "ctu": w.ctu, "grid": f"{g.cols}x{g.rows}",
+                   "n_slices": w.n_slices, "max_tile_cols": w.max_tile_cols,
+                   "lambda": cfg.lambda_, "k_area": cfg.k_area,
+                   "coverage": "reference", "mode": "exhaustive" if args.mode == 0 else "pruned",
+                   "candidates_per_frame_step": [list(c) for c in counts],
+                   "parallelism": f"frames sharded, {world} rank(s)",
+                   "l2": "inputs larger than L2 (luma batch %.0f MB/step)" % (luma_bytes / 1e6)},
+        "frames_per_s": frames_total / (ms / 1e3),
+        "frames_per_s_e2e": frames_total / (ms_e2e / 1e3),
+        "texture_gbs": tex_gbs,
+        "phase_us": {"texture_k1": round(tex_us, 2), "tables_k2k3": round(tab_us, 2),
+                     "step1": round(s1_us, 2), "step2": round(s2_us, 2),
+                     "call": round(phase[4], 2)},
+        "roofline": issue,
+        "roofline_texture": tex_roof,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": luma_bytes + F * g.cell_count() * 8,
+                "d2h_bytes_per_step": 2 * 32 * ((F + 31) // 32) * 168, "ms_per_step": ms_e2e},
+        "gpu_launches": args.steps * (5 + 4 * ((F + 31) // 32)),
+        "clocks": ck,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_sample(w, threads=1, steps=1)["cpu_baseline"]
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    part.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---- reference (CPU) arm ------------------------------------------------------------
+def _sample_cap(total_steps):
+    # enumeration prefix c <= cap (c ascending is the outermost loop of the
+    # reference's order, search.cpp:120-128): 12.4M candidates/step/frame at
+    # cap 3, 1.27M at cap 2 (30x17 grid, n = 8)
+    return 3 if total_steps * 12 <= 200 else 2
+
+
+def cpu_baseline_sample(w, threads, steps, warmup=0):
+    from oracle.oracle import Oracle, Ref
+    from paper_2012_14792_b200 import workloads as wl
+    kind = "reference"
+    try:
+        R = Ref()
+    except Exception:
+        R, kind = None, "port"
+    O = Oracle()
+    cap = _sample_cap(steps + warmup) if w.index == 3 else w.max_tile_cols
+    nfr = threads
+    tr = wl.cost_trace(w, frames=nfr)
+    luma = wl.synth_luma(w, frames=nfr)
+    maps = np.stack([m.times_us for m in tr.history_maps])
+    hp = [m.poc for m in tr.history_maps]
+    ht = [m.temporal_layer for m in tr.history_maps]
+    counts = [0] * nfr
+
+    def one(i):
+        p = i + 1
+        plane = luma[i].astype(np.uint16)
+        if R is not None:
+            _, rec = R.ctu_stats(plane, w.bit_depth, w.ctu)
+            st, o = R.two_step(w.width, w.height, w.ctu, 16, maps[:p], hp[:p], ht[:p], rec, p,
+                               w.n_slices, 0.0, 3.0, 0, cap)
+            counts[i] = o.candidates_step1 + o.candidates_step2
+        else:
+            rec = O.ctu_stats(luma[i], w.ctu)
+            st, o = O.search(w.width, w.height, w.ctu, tr.est[i], rec, w.n_slices, 0.0, 3.0, cap,
+                             0, 3)
+            counts[i] = o.candidates_step1 + o.candidates_step2
+
+    def step():
+        th = [threading.Thread(target=one, args=(i,)) for i in range(nfr)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        return time.perf_counter() - t0, sum(counts)
+
+    for _ in range(warmup):
+        step()
+    tot_t, tot_c = 0.0, 0
+    for _ in range(steps):
+        dt, c = step()
+        tot_t += dt
+        tot_c += c
+    v = tot_c / tot_t
+    sample = (f"{w.name}: ctu_stats + two_step_partition on {nfr} frame(s) (POC 1..{nfr}), one "
+              f"frame per thread, over the enumeration prefix c <= {cap} "
+              f"({tot_c // max(steps, 1) // nfr:,} candidates per frame, both steps)")
+    return {"value": v, "seconds": tot_t,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nfr, "kind": kind,
+                             "sample": sample}}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2012_14792_b200 import workloads as wl
+    w = wl.WORKLOADS[args.config]
+    threads = min(os.cpu_count() or 1, w.frames) if w.frames > 1 else 1
+    r = cpu_baseline_sample(w, threads=threads, steps=args.steps, warmup=args.warmup)
+    v = r["value"]
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / max(args.steps, 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
+           "data": "synthetic (seeded; SURVEY.md §8d generator)",
+           "config": {"workload": w.name, "host_threads": threads},
+           "impl": "reference", "cpu_baseline": r["cpu_baseline"],
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--mode", type=int, default=0, choices=[0, 1],
+                    help="0 exhaustive (every candidate scored), 1 exact branch-and-bound")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

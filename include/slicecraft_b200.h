@@ -1,0 +1,227 @@
+/*
+ * slicecraft_b200.h — the C-ABI drop-in boundary of the B200-native TRS
+ * partitioner core (arXiv 2012.14792, reference library `slicecraft`).
+ *
+ * Plain C: POD structs, caller-owned buffers, an opaque context, integer
+ * status codes and a thread-local error string.  No torch or C++ types cross
+ * this boundary.  The C++ drop-in layer (include/slicecraft/*.hpp, namespace
+ * slicecraft) and the Python binding (paper_2012_14792_b200/) both sit on top
+ * of these entry points.  Each entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj).
+ *
+ * Pointers to frame data may be HOST or DEVICE pointers (detected with
+ * cudaPointerGetAttributes); host inputs are staged through pinned buffers
+ * owned by the context.  All calls are synchronous with respect to their
+ * outputs.  A context is owned by one host thread at a time.
+ */
+#ifndef SLICECRAFT_B200_H
+#define SLICECRAFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SC_ABI_VERSION 1
+
+/* Compile-time limits of the search kernels.  Larger requests fail with
+ * SC_ERR_SIZE (the reference has no such limits). */
+#define SC_MAX_SLICES 64
+#define SC_MAX_COLS 16
+
+/* One status per exception class of include/slicecraft/errors.hpp:10-85. */
+typedef enum sc_status {
+  SC_OK = 0,
+  SC_ERR_GEOMETRY = 1,     /* GeometryError */
+  SC_ERR_OVERLAP = 2,      /* OverlapError */
+  SC_ERR_COVERAGE = 3,     /* CoverageError */
+  SC_ERR_STRUCTURE = 4,    /* StructureError */
+  SC_ERR_IO = 5,           /* IoError */
+  SC_ERR_RANGE = 6,        /* RangeError */
+  SC_ERR_FORMAT = 7,       /* FormatError */
+  SC_ERR_CONFIG = 8,       /* ConfigError */
+  SC_ERR_TRACE = 9,        /* TraceError */
+  SC_ERR_NO_CANDIDATE = 10,/* NoCandidateError */
+  SC_ERR_SIZE = 11,        /* SizeError */
+  SC_ERR_USAGE = 12,       /* UsageError */
+  SC_ERR_CUDA = 100,       /* CUDA runtime failure / no device */
+  SC_ERR_INTERNAL = 101
+} sc_status;
+
+/* CtuGrid (grid.hpp:13-34). */
+typedef struct sc_grid {
+  int32_t frame_width;
+  int32_t frame_height;
+  int32_t ctu_size;
+  int32_t cols;
+  int32_t rows;
+} sc_grid;
+
+/* CtuRecord (texture.hpp:35-41). */
+typedef struct sc_ctu_record {
+  uint64_t count;
+  uint64_t sum;
+  uint64_t sumsq;
+} sc_ctu_record;
+
+/* CandidateFamily (search.hpp:17). */
+enum { SC_FAMILY_COLUMN_SPLIT = 0, SC_FAMILY_UNIFORM_ONLY = 1 };
+/* Candidate-space coverage: REFERENCE reproduces search.cpp:133-143 exactly
+ * (tile widths sum to <= cols); COVERING keeps only sum == cols. */
+enum { SC_COVERAGE_REFERENCE = 0, SC_COVERAGE_COVERING = 1 };
+/* EXHAUSTIVE scores every candidate; PRUNED is an exact branch-and-bound
+ * (identical results and counters, fewer leaves scored). */
+enum { SC_MODE_EXHAUSTIVE = 0, SC_MODE_PRUNED = 1 };
+
+/* SearchConfig (search.hpp:22-34) + B200 fields. */
+typedef struct sc_search_cfg {
+  int32_t n_slices;       /* >= 1 */
+  double lambda;          /* >= 0, finite */
+  double k_area;          /* > 1 */
+  int32_t family;         /* SC_FAMILY_* */
+  int32_t max_tile_cols;  /* 0 means n_slices */
+  int32_t workers;        /* accepted for parity of SearchConfig::check; >= 1 */
+  int32_t coverage;       /* SC_COVERAGE_* */
+  int32_t mode;           /* SC_MODE_* */
+} sc_search_cfg;
+
+/* A ColumnSplit layout (search.cpp:41-45): tile columns, each cut into
+ * full-width CTU-row runs.  run_heights is column-major. */
+typedef struct sc_layout {
+  int32_t n_cols;
+  int32_t n_slices;
+  int32_t col_widths[SC_MAX_COLS];
+  int32_t runs_per_col[SC_MAX_COLS];
+  int32_t run_heights[SC_MAX_SLICES];
+} sc_layout;
+
+/* SearchOutcome (search.hpp:36-49) + the step-1 argmin of min_time_search. */
+typedef struct sc_search_result {
+  double t_min_us;
+  double t_best_us;
+  double sse_best;
+  uint64_t candidates_evaluated;
+  uint64_t candidates_step1;
+  uint64_t candidates_step2;
+  double search_time_us;       /* device time of both steps (CUDA events) */
+  double time_min_step_us;
+  double clustering_step_us;
+  uint64_t leaves_scored_step1; /* == candidates_step1 in EXHAUSTIVE mode */
+  uint64_t leaves_scored_step2;
+  sc_layout argmin;            /* step-1 first-in-order argmin */
+  sc_layout best;              /* step-2 choice */
+} sc_search_result;
+
+typedef struct sc_ctx sc_ctx;
+
+/* ---- errors / version --------------------------------------------------- */
+const char* sc_last_error(void);
+int sc_abi_version(void);
+
+/* ---- geometry (grid.cpp:9-32, CtuGrid::make) ---------------------------- */
+sc_status sc_grid_make(int32_t frame_width, int32_t frame_height, int32_t ctu_size,
+                       sc_grid* out);
+/* temporal_layer_of_poc (cost.cpp:28-38, cost.hpp:39) */
+sc_status sc_temporal_layer(int32_t poc, int32_t gop_size, int32_t* out);
+
+/* ---- context ------------------------------------------------------------ */
+sc_status sc_ctx_create(int32_t device, sc_ctx** out);
+sc_status sc_ctx_destroy(sc_ctx* ctx);
+/* Bind the context to a rank of a candidate-space shard (multi-GPU):
+ * rank r of world w scores the work items r, r+w, r+2w, ... ; results of
+ * sc_search_* then hold this shard's best and must be merged with
+ * sc_merge_results (an all-gather of sc_shard_best records). */
+sc_status sc_ctx_set_shard(sc_ctx* ctx, int32_t rank, int32_t world);
+
+/* Run all work of this context on the caller's CUDA stream (a cudaStream_t
+ * passed as void*; NULL restores the context's own stream).  Calls stay
+ * synchronous; events recorded on that stream bracket the device work. */
+sc_status sc_ctx_set_stream(sc_ctx* ctx, void* cuda_stream);
+/* Device time (CUDA events, microseconds) of the phases of the last
+ * search call: [0] K1 texture, [1] K2/K3 tables, [2] step 1, [3] step 2,
+ * [4] whole call (first to last event on the context's stream). */
+sc_status sc_ctx_timings(sc_ctx* ctx, double out[5]);
+
+/* ---- texture map (texture.cpp:145-169, ctu_stats) ------------------------ */
+/* K1: per-CTU exact moments over n_frames frames.  luma: bytes_per_sample
+ * 1 (uint8) or 2 (uint16 LE, values <= 65535), row pitch and frame stride in
+ * bytes; host or device pointer.  out: n_frames * cols * rows records
+ * (host or device pointer). */
+sc_status sc_texture_moments(sc_ctx* ctx, const void* luma, int32_t bytes_per_sample,
+                             int32_t width, int32_t height, size_t pitch_bytes,
+                             size_t frame_stride_bytes, int32_t ctu_size,
+                             int32_t n_frames, sc_ctu_record* out);
+/* TextureStats ctor validation (texture.cpp:90-111) of caller records. */
+sc_status sc_texture_validate(const sc_grid* grid, const sc_ctu_record* records);
+
+/* ---- grid tables (cost.cpp:97-115, texture.cpp:113-143) ----------------- */
+/* K2+K3 on n_frames frames: est_times n_frames*cells doubles (host ptr),
+ * records n_frames*cells (host ptr or NULL).  Outputs, host pointers, may be
+ * NULL: rect_time / rect_sse n_frames * NXW * NYH doubles in rectangle order
+ * xw(x0,w)*NYH + yh(y0,h), sat n_frames*(cols+1)*(rows+1). */
+sc_status sc_grid_tables(sc_ctx* ctx, const sc_grid* grid, const double* est_times,
+                         const sc_ctu_record* records, int32_t n_frames,
+                         double* rect_time, double* rect_sse, double* sat);
+
+/* ---- partition search (search.cpp:257-434) ------------------------------ */
+/* min_time_search (search.cpp:328-332) for n_frames est maps. */
+sc_status sc_min_time_search(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                             const double* est_times, int32_t n_frames,
+                             sc_search_result* out);
+/* constrained_clustering_search (search.cpp:334-405): t_min_us per frame. */
+sc_status sc_constrained_clustering(sc_ctx* ctx, const sc_grid* grid,
+                                    const sc_search_cfg* cfg, const double* est_times,
+                                    const sc_ctu_record* records, const double* t_min_us,
+                                    int32_t n_frames, sc_search_result* out);
+/* two_step_partition (search.cpp:407-434) after the host-side estimate
+ * (estimate_ctu_times, cost.cpp:66-95): est_times are the estimated maps. */
+sc_status sc_two_step(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                      const double* est_times, const sc_ctu_record* records,
+                      int32_t n_frames, sc_search_result* out);
+/* The whole per-batch hot path in one call: K1 texture pass over the frames,
+ * K2/K3 tables, step 1, step 2.  records_out may be NULL. */
+sc_status sc_partition_frames(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                              const void* luma, int32_t bytes_per_sample,
+                              size_t pitch_bytes, size_t frame_stride_bytes,
+                              const double* est_times, int32_t n_frames,
+                              sc_ctu_record* records_out, sc_search_result* out);
+/* for_each_candidate / enumerate_candidates count (search.cpp:302-326). */
+sc_status sc_count_candidates(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                              uint64_t* count);
+
+/* ---- multi-GPU shard merge --------------------------------------------- */
+/* Opaque per-frame shard best, exchanged by an all-gather (NCCL or gloo). */
+typedef struct sc_shard_best {
+  double key_sse;     /* step 2 key (inf in step 1) */
+  uint64_t key_t;     /* f64 bits of t (non-negative => monotone) */
+  uint64_t item;      /* global work-item index (lex order) */
+  uint64_t ord;       /* candidate ordinal inside the item */
+  uint64_t count;     /* this shard's candidate count */
+  uint64_t leaves;    /* this shard's scored leaves */
+  sc_layout layout;
+} sc_shard_best;
+/* Export this context's last step-1 (step=1) or step-2 (step=2) shard bests. */
+sc_status sc_shard_export(sc_ctx* ctx, int32_t step, int32_t n_frames, sc_shard_best* out);
+/* Merge world*n_frames gathered records (rank-major) into per-frame results. */
+sc_status sc_shard_merge(int32_t step, int32_t world, int32_t n_frames,
+                         const sc_shard_best* gathered, sc_search_result* inout);
+
+/* ---- synthetic inputs (bench/test utility; BASELINE.json configs) ------- */
+/* Seeded luma frames: bytes_per_sample 1 or 2, max value
+ * (1<<bit_depth)-1, `textured_pct` percent of 128x128 blocks noise, mode 1 =
+ * the three-class (flat/gradient/noise) mix of config 2.  Frame f drifts the
+ * block lattice by 4*f px.  Host buffer, frame stride width*height*bps. */
+sc_status sc_synth_luma(uint64_t seed, int32_t width, int32_t height, int32_t bit_depth,
+                        int32_t n_frames, int32_t first_frame, int32_t textured_pct,
+                        int32_t mode, void* out);
+/* Seeded lognormal(0, sigma) per-CTU times, (float) rounded then widened. */
+sc_status sc_synth_times(uint64_t seed, int32_t tag, int32_t cells, double sigma,
+                         double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SLICECRAFT_B200_H */

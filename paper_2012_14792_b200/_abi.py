@@ -1,0 +1,131 @@
+"""ctypes mirror of include/slicecraft_b200.h (the C-ABI drop-in boundary).
+
+The product library is ``libslicecraft_b200.so`` built in-tree by ``make``
+(or ``__graft_entry__.build()``).  Loading fails loudly when it is missing:
+there is no CPU fallback for any entry point.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libslicecraft_b200.so")
+
+SC_MAX_SLICES = 64
+SC_MAX_COLS = 16
+
+# sc_status, one per exception class of slicecraft/errors.hpp:10-85
+SC_OK = 0
+STATUS_NAMES = {
+    1: "GeometryError", 2: "OverlapError", 3: "CoverageError", 4: "StructureError",
+    5: "IoError", 6: "RangeError", 7: "FormatError", 8: "ConfigError", 9: "TraceError",
+    10: "NoCandidateError", 11: "SizeError", 12: "UsageError", 100: "CudaError",
+    101: "InternalError",
+}
+
+
+class Grid(C.Structure):
+    _fields_ = [("frame_width", C.c_int32), ("frame_height", C.c_int32),
+                ("ctu_size", C.c_int32), ("cols", C.c_int32), ("rows", C.c_int32)]
+
+
+class CtuRecord(C.Structure):
+    _fields_ = [("count", C.c_uint64), ("sum", C.c_uint64), ("sumsq", C.c_uint64)]
+
+
+class SearchCfg(C.Structure):
+    _fields_ = [("n_slices", C.c_int32), ("lambda_", C.c_double), ("k_area", C.c_double),
+                ("family", C.c_int32), ("max_tile_cols", C.c_int32), ("workers", C.c_int32),
+                ("coverage", C.c_int32), ("mode", C.c_int32)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("n_cols", C.c_int32), ("n_slices", C.c_int32),
+                ("col_widths", C.c_int32 * SC_MAX_COLS),
+                ("runs_per_col", C.c_int32 * SC_MAX_COLS),
+                ("run_heights", C.c_int32 * SC_MAX_SLICES)]
+
+
+class SearchResult(C.Structure):
+    _fields_ = [("t_min_us", C.c_double), ("t_best_us", C.c_double), ("sse_best", C.c_double),
+                ("candidates_evaluated", C.c_uint64), ("candidates_step1", C.c_uint64),
+                ("candidates_step2", C.c_uint64), ("search_time_us", C.c_double),
+                ("time_min_step_us", C.c_double), ("clustering_step_us", C.c_double),
+                ("leaves_scored_step1", C.c_uint64), ("leaves_scored_step2", C.c_uint64),
+                ("argmin", Layout), ("best", Layout)]
+
+
+class ShardBest(C.Structure):
+    _fields_ = [("key_sse", C.c_double), ("key_t", C.c_uint64), ("item", C.c_uint64),
+                ("ord", C.c_uint64), ("count", C.c_uint64), ("leaves", C.c_uint64),
+                ("layout", Layout)]
+
+
+# (name, restype, argtypes) for every symbol declared in the header.
+_P = C.c_void_p
+SIGNATURES = [
+    ("sc_last_error", C.c_char_p, []),
+    ("sc_abi_version", C.c_int, []),
+    ("sc_grid_make", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(Grid)]),
+    ("sc_temporal_layer", C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32)]),
+    ("sc_ctx_create", C.c_int, [C.c_int32, C.POINTER(_P)]),
+    ("sc_ctx_destroy", C.c_int, [_P]),
+    ("sc_ctx_set_shard", C.c_int, [_P, C.c_int32, C.c_int32]),
+    ("sc_ctx_set_stream", C.c_int, [_P, _P]),
+    ("sc_ctx_timings", C.c_int, [_P, _P]),
+    ("sc_texture_moments", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_size_t,
+                                     C.c_size_t, C.c_int32, C.c_int32, _P]),
+    ("sc_texture_validate", C.c_int, [C.POINTER(Grid), _P]),
+    ("sc_grid_tables", C.c_int, [_P, C.POINTER(Grid), _P, _P, C.c_int32, _P, _P, _P]),
+    ("sc_min_time_search", C.c_int, [_P, C.POINTER(Grid), C.POINTER(SearchCfg), _P,
+                                     C.c_int32, _P]),
+    ("sc_constrained_clustering", C.c_int, [_P, C.POINTER(Grid), C.POINTER(SearchCfg), _P,
+                                            _P, _P, C.c_int32, _P]),
+    ("sc_two_step", C.c_int, [_P, C.POINTER(Grid), C.POINTER(SearchCfg), _P, _P, C.c_int32,
+                              _P]),
+    ("sc_partition_frames", C.c_int, [_P, C.POINTER(Grid), C.POINTER(SearchCfg), _P,
+                                      C.c_int32, C.c_size_t, C.c_size_t, _P, C.c_int32, _P,
+                                      _P]),
+    ("sc_count_candidates", C.c_int, [_P, C.POINTER(Grid), C.POINTER(SearchCfg),
+                                      C.POINTER(C.c_uint64)]),
+    ("sc_shard_export", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
+    ("sc_shard_merge", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P]),
+    ("sc_synth_luma", C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                C.c_int32, C.c_int32, C.c_int32, _P]),
+    ("sc_synth_times", C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_double, _P]),
+]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the product library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                "the B200 path has no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class SlicecraftError(RuntimeError):
+    """Raised for a non-OK sc_status; ``kind`` is the reference exception name."""
+
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.kind = STATUS_NAMES.get(status, f"status{status}")
+        super().__init__(f"{self.kind}: {message}")
+
+
+def check(status: int) -> None:
+    if status != SC_OK:
+        msg = lib().sc_last_error()
+        raise SlicecraftError(status, msg.decode() if msg else "")

@@ -1,0 +1,883 @@
+// C-ABI entry points (include/slicecraft_b200.h) and the host-side planner.
+//
+// Host work here is O(cells) or O(items) bookkeeping — geometry, validation,
+// the frame-independent work-item plan, the area-threshold table — plus the
+// CUDA launches.  No candidate is scored on the host.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+
+#include "common.cuh"
+
+namespace scb {
+// kernels (texture.cu, tables.cu, search.cu)
+void texture_moments_device(const void* d_luma, int bps, int W, int H, size_t pitch,
+                            size_t fstride, int ctu, int frames, int cols, int rows,
+                            sc_ctu_record* d_out, cudaStream_t st);
+void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, int rows,
+                     int frames, double* d_sat, uint64_t* d_usat, cudaStream_t st);
+void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16_t* d_dec,
+                        int cols, int rows, int frames, int fpw, double* d_rect_t,
+                        double* d_rect_s, uint64_t* d_rt, double* d_rs, int sm_count,
+                        cudaStream_t st);
+void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st);
+int search_blocks_per_sm(int fpw, int step);
+void finalize_launch(int step, int fpw, int frames_in_group, uint32_t n_warps,
+                     const LaneBest* lanes, const uint8_t* snaps,
+                     const unsigned long long* count, double lambda, FrameBest* out,
+                     uint64_t* budget_out, cudaStream_t st);
+}  // namespace scb
+
+using namespace scb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sc_status set_error(sc_status s, const std::string& m) {
+  g_last_error = m;
+  return s;
+}
+
+template <typename F>
+sc_status guarded(F&& fn) {
+  try {
+    fn();
+    g_last_error.clear();
+    return SC_OK;
+  } catch (const Fail& f) {
+    return set_error(f.status, f.msg);
+  } catch (const std::bad_alloc&) {
+    return set_error(SC_ERR_INTERNAL, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_error(SC_ERR_INTERNAL, e.what());
+  }
+}
+
+// CtuGrid::make (grid.cpp:9-24)
+sc_grid make_grid(int w, int h, int ctu) {
+  if (ctu != 32 && ctu != 64 && ctu != 128)
+    fail(SC_ERR_GEOMETRY, "ctu_size must be one of {32, 64, 128}, got " + std::to_string(ctu));
+  if (w < 1 || h < 1) fail(SC_ERR_GEOMETRY, "frame dimensions must be positive");
+  sc_grid g;
+  g.frame_width = w;
+  g.frame_height = h;
+  g.ctu_size = ctu;
+  g.cols = (w + ctu - 1) / ctu;
+  g.rows = (h + ctu - 1) / ctu;
+  return g;
+}
+
+void check_grid(const sc_grid* g) {
+  if (!g) fail(SC_ERR_USAGE, "grid is NULL");
+  sc_grid m = make_grid(g->frame_width, g->frame_height, g->ctu_size);
+  if (m.cols != g->cols || m.rows != g->rows)
+    fail(SC_ERR_GEOMETRY, "grid cols/rows inconsistent with frame and CTU size");
+}
+
+// SearchConfig::check (search.cpp:28-36) + the kernels' compiled limits.
+int check_cfg(const sc_grid& g, const sc_search_cfg* c) {
+  if (!c) fail(SC_ERR_USAGE, "cfg is NULL");
+  if (c->n_slices < 1) fail(SC_ERR_CONFIG, "n_slices must be >= 1");
+  if (!(c->k_area > 1.0)) fail(SC_ERR_CONFIG, "k_area must be > 1");
+  if (!(c->lambda >= 0.0) || !std::isfinite(c->lambda))
+    fail(SC_ERR_CONFIG, "lambda must be finite and >= 0");
+  if (c->workers < 1) fail(SC_ERR_CONFIG, "workers must be >= 1");
+  if (c->max_tile_cols < 0) fail(SC_ERR_CONFIG, "max_tile_cols must be >= 0");
+  if (c->family != SC_FAMILY_COLUMN_SPLIT && c->family != SC_FAMILY_UNIFORM_ONLY)
+    fail(SC_ERR_CONFIG, "unknown candidate family");
+  if (c->coverage != SC_COVERAGE_REFERENCE && c->coverage != SC_COVERAGE_COVERING)
+    fail(SC_ERR_CONFIG, "unknown coverage");
+  if (c->mode != SC_MODE_EXHAUSTIVE && c->mode != SC_MODE_PRUNED)
+    fail(SC_ERR_CONFIG, "unknown search mode");
+  // run_step1 / for_each_candidate (search.cpp:260-262, 305-307)
+  if (c->n_slices > g.cols * g.rows) fail(SC_ERR_GEOMETRY, "n_slices exceeds the CTU cell count");
+  const int eff = c->max_tile_cols > 0 ? c->max_tile_cols : c->n_slices;
+  const int maxc = std::min({c->n_slices, eff, g.cols});
+  if (c->n_slices > SC_MAX_SLICES)
+    fail(SC_ERR_SIZE, "n_slices exceeds the compiled limit SC_MAX_SLICES");
+  if (maxc > SC_MAX_COLS) fail(SC_ERR_SIZE, "tile-column count exceeds SC_MAX_COLS");
+  if (g.rows > 255) fail(SC_ERR_SIZE, "more than 255 CTU rows");
+  return maxc;
+}
+
+// TextureStats ctor validation (texture.cpp:90-111).
+void validate_records(const sc_grid& g, const sc_ctu_record* r) {
+  for (int y = 0; y < g.rows; ++y)
+    for (int x = 0; x < g.cols; ++x) {
+      const sc_ctu_record& c = r[(size_t)y * g.cols + x];
+      if (c.count != (uint64_t)cell_w(g, x) * (uint64_t)cell_h(g, y))
+        fail(SC_ERR_FORMAT, "CTU pixel count mismatch at (" + std::to_string(x) + "," +
+                                std::to_string(y) + ")");
+      const unsigned __int128 lhs = (unsigned __int128)c.count * c.sumsq;
+      const unsigned __int128 rhs = (unsigned __int128)c.sum * c.sum;
+      if (lhs < rhs)
+        fail(SC_ERR_FORMAT, "CTU statistics violate count*sumsq >= sum^2 at (" +
+                                std::to_string(x) + "," + std::to_string(y) + ")");
+    }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// ---- planner ------------------------------------------------------------------
+void gen_prefixes(int cols, int c, int d, bool covering, std::vector<WorkItem>& out) {
+  int w[16];
+  // iterative lex enumeration of (w_0..w_{d-1})
+  std::function<void(int, int)> rec = [&](int i, int cols_left) {
+    if (i == d) {
+      if (covering && d == c && cols_left != 0) return;
+      WorkItem it{};
+      it.c = (uint8_t)c;
+      it.d = (uint8_t)d;
+      for (int j = 0; j < d; ++j) it.w[j] = (uint8_t)w[j];
+      out.push_back(it);
+      return;
+    }
+    const int maxw = cols_left - (c - i - 1);
+    for (int x = 1; x <= maxw; ++x) {
+      w[i] = x;
+      rec(i + 1, cols_left - x);
+    }
+  };
+  rec(0, cols);
+}
+
+Plan* get_plan(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc) {
+  PlanKey key{g.cols, g.rows, cfg.n_slices, maxc, cfg.coverage, cfg.k_area};
+  for (Plan* p : ctx->plans)
+    if (p->key == key) return p;
+  Plan* p = new Plan();
+  p->key = key;
+  const bool covering = cfg.coverage == SC_COVERAGE_COVERING;
+  // work items: width prefixes of depth D (per c: min(c, D)), D grown until
+  // there are enough items to keep every warp busy.
+  const size_t target = (size_t)ctx->sm_count * 16 * 32;
+  for (int D = 1; D <= 12; ++D) {
+    p->items.clear();
+    for (int c = 1; c <= maxc; ++c) gen_prefixes(g.cols, c, std::min(c, D), covering, p->items);
+    if (p->items.size() >= target || D >= maxc || p->items.size() > (1u << 22)) break;
+  }
+  // area table: bmax[a] = largest B in [0, max_area] with k*(double)a > (double)B
+  // (the admissibility test of search.cpp:182-183), -1 if none.
+  const int max_area = g.cols * g.rows;
+  p->bmax.assign((size_t)max_area + 1, -1);
+  int b = -1;
+  for (int a = 0; a <= max_area; ++a) {
+    // k*a is non-decreasing in a, so b only moves up
+    while (b + 1 <= max_area && cfg.k_area * (double)a > (double)(b + 1)) ++b;
+    p->bmax[a] = b;
+  }
+  ctx->plans.push_back(p);
+  return p;
+}
+
+void upload_plan(sc_ctx* ctx, Plan* p) {
+  if (p->uploaded) return;
+  p->d_items.ensure(p->items.size() * sizeof(WorkItem));
+  SCB_CUDA(cudaMemcpy(p->d_items.p, p->items.data(), p->items.size() * sizeof(WorkItem),
+                      cudaMemcpyHostToDevice));
+  p->d_bmax.ensure(p->bmax.size() * sizeof(int32_t));
+  SCB_CUDA(cudaMemcpy(p->d_bmax.p, p->bmax.data(), p->bmax.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice));
+  p->uploaded = true;
+  (void)ctx;
+}
+
+void layout_from_snap(const FrameBest& fb, int n, sc_layout* L) {
+  std::memset(L, 0, sizeof(*L));
+  int c = 0;
+  while (c < SC_MAX_COLS && fb.snap[c] != 0) ++c;
+  L->n_cols = c;
+  L->n_slices = n;
+  for (int i = 0; i < c; ++i) {
+    L->col_widths[i] = fb.snap[i];
+    L->runs_per_col[i] = fb.snap[SC_MAX_COLS + i];
+  }
+  for (int i = 0; i < n; ++i) L->run_heights[i] = fb.snap[2 * SC_MAX_COLS + i];
+}
+
+
+cudaStream_t main_stream(sc_ctx* ctx) { return ctx->user_stream ? ctx->user_stream : ctx->stream; }
+
+struct Layouts {
+  int frames = 0, fpw = 1, groups = 1;
+  size_t nr = 0;
+  int nsat = 0;
+};
+
+Layouts layouts_for(const sc_grid& g, int frames) {
+  Layouts L;
+  L.frames = frames;
+  L.fpw = std::min(32, next_pow2(frames));
+  L.groups = (frames + L.fpw - 1) / L.fpw;
+  L.nr = (size_t)n_xw(g.cols) * n_yh(g.rows);
+  L.nsat = (g.cols + 1) * (g.rows + 1);
+  return L;
+}
+
+// Rectangle decode table (xw -> x0,w ; yh -> y0,h), cached per grid.
+const int16_t* decode_table(sc_ctx* ctx, const sc_grid& g) {
+  if (ctx->dec_cols == g.cols && ctx->dec_rows == g.rows) return ctx->dec.as<int16_t>();
+  const int nxw = n_xw(g.cols), nyh = n_yh(g.rows);
+  std::vector<int16_t> dec((size_t)2 * nxw + 2 * nyh);
+  for (int x0 = 0; x0 < g.cols; ++x0)
+    for (int w = 1; w <= g.cols - x0; ++w) {
+      const int i = xw_index(g.cols, x0, w);
+      dec[i] = (int16_t)x0;
+      dec[nxw + i] = (int16_t)w;
+    }
+  for (int y0 = 0; y0 < g.rows; ++y0)
+    for (int h = 1; h <= g.rows - y0; ++h) {
+      const int i = yh_index(g.rows, y0, h);
+      dec[2 * nxw + i] = (int16_t)y0;
+      dec[2 * nxw + nyh + i] = (int16_t)h;
+    }
+  ctx->dec.ensure(dec.size() * sizeof(int16_t));
+  SCB_CUDA(cudaMemcpy(ctx->dec.p, dec.data(), dec.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+  ctx->dec_cols = g.cols;
+  ctx->dec_rows = g.rows;
+  return ctx->dec.as<int16_t>();
+}
+
+// K2 (f64 SAT) + K3 (time tables) from ctx->est.
+void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
+                         cudaStream_t st) {
+  const int16_t* dec = decode_table(ctx, g);
+  ctx->sat.ensure((size_t)L.frames * L.nsat * sizeof(double));
+  ctx->rt_search.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint64_t));
+  if (raw) ctx->rect_t.ensure((size_t)L.frames * L.nr * sizeof(double));
+  grid_sat_device(ctx->est.as<double>(), nullptr, g.cols, g.rows, L.frames, ctx->sat.as<double>(),
+                  nullptr, st);
+  rect_tables_device(ctx->sat.as<double>(), nullptr, dec, g.cols, g.rows, L.frames, L.fpw,
+                     raw ? ctx->rect_t.as<double>() : nullptr, nullptr,
+                     ctx->rt_search.as<uint64_t>(), nullptr, ctx->sm_count, st);
+}
+
+// K2 (u64 SATs) + K3 (SSE tables) from ctx->records.
+void enqueue_moment_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
+                           cudaStream_t st) {
+  const int16_t* dec = decode_table(ctx, g);
+  ctx->usat.ensure((size_t)L.frames * 3 * L.nsat * sizeof(uint64_t));
+  ctx->rs_search.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(double));
+  if (raw) ctx->rect_s.ensure((size_t)L.frames * L.nr * sizeof(double));
+  grid_sat_device(nullptr, ctx->records.as<sc_ctu_record>(), g.cols, g.rows, L.frames, nullptr,
+                  ctx->usat.as<uint64_t>(), st);
+  rect_tables_device(nullptr, ctx->usat.as<uint64_t>(), dec, g.cols, g.rows, L.frames, L.fpw,
+                     nullptr, raw ? ctx->rect_s.as<double>() : nullptr, nullptr,
+                     ctx->rs_search.as<double>(), ctx->sm_count, st);
+}
+
+// One search step over all frame groups; finalize writes FrameBest[step] and,
+// after step 1, the device budgets of step 2.  No host synchronisation.
+void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
+                  const Layouts& L, int step, cudaStream_t st) {
+  const int bps = search_blocks_per_sm(L.fpw, step);
+  const int blocks = ctx->sm_count * bps;
+  const uint32_t warps = (uint32_t)blocks * 8;
+  const size_t lane_bytes = (size_t)warps * 32 * sizeof(LaneBest);
+  const size_t snap_bytes = (size_t)warps * 32 * kSnapBytes;
+  ctx->lanes.ensure(lane_bytes * L.groups);
+  ctx->snaps.ensure(snap_bytes * L.groups);
+  ctx->counter.ensure((size_t)L.groups * 4 * sizeof(uint64_t));
+  ctx->frame_best.ensure((size_t)2 * L.groups * L.fpw * sizeof(FrameBest));
+  ctx->budget.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+  uint64_t* ctr_base = ctx->counter.as<uint64_t>() + (step - 1) * 2;
+  SCB_CUDA(cudaMemsetAsync(ctx->counter.p, 0, (size_t)L.groups * 4 * sizeof(uint64_t), st));
+  const uint32_t total = (uint32_t)plan->items.size();
+  const uint32_t rank = (uint32_t)ctx->shard_rank, world = (uint32_t)ctx->shard_world;
+  const uint32_t mine = total > rank ? (total - rank + world - 1) / world : 0;
+  FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)(step - 1) * L.groups * L.fpw;
+  for (int gi = 0; gi < L.groups; ++gi) {
+    SearchArgs a{};
+    a.cols = g.cols;
+    a.rows = g.rows;
+    a.n = cfg.n_slices;
+    a.nyh = n_yh(g.rows);
+    a.max_area = g.cols * g.rows;
+    a.coverage = cfg.coverage;
+    a.items = plan->d_items.as<WorkItem>();
+    a.n_items = mine;
+    a.item_offset = rank;
+    a.item_stride = world;
+    uint64_t* ctr = ctr_base + 4 * gi;
+    a.counter = reinterpret_cast<uint32_t*>(ctr);
+    a.count_out = reinterpret_cast<unsigned long long*>(ctr + 1);
+    a.bmax = plan->d_bmax.as<int32_t>();
+    a.rt = ctx->rt_search.as<uint64_t>() + (size_t)gi * L.nr * L.fpw;
+    a.rs = step == 2 ? ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw : nullptr;
+    a.budget = ctx->budget.as<uint64_t>() + (size_t)gi * L.fpw;
+    a.lanes = reinterpret_cast<LaneBest*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
+    a.snaps = ctx->snaps.as<uint8_t>() + snap_bytes * gi;
+    search_launch(L.fpw, step, a, blocks, st);
+    const int fig = std::min(L.fpw, L.frames - gi * L.fpw);
+    finalize_launch(step, L.fpw, fig, warps, a.lanes, a.snaps, a.count_out, cfg.lambda,
+                    fb + (size_t)gi * L.fpw,
+                    step == 1 ? ctx->budget.as<uint64_t>() + (size_t)gi * L.fpw : nullptr, st);
+  }
+}
+
+// Device budgets from host t_min values (constrained_clustering with a
+// caller-supplied t_min; budget = t_min * (1.0 + lambda), search.cpp:344).
+void upload_budgets(sc_ctx* ctx, const Layouts& L, const double* t_min, double lambda,
+                    cudaStream_t st) {
+  ctx->h_budget.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+  uint64_t* b = ctx->h_budget.as<uint64_t>();
+  std::memset(b, 0, (size_t)L.groups * L.fpw * sizeof(uint64_t));
+  for (int f = 0; f < L.frames; ++f) {
+    const double v = t_min[f] * (1.0 + lambda);
+    uint64_t bits;
+    std::memcpy(&bits, &v, 8);
+    b[f] = (v > 0.0) ? bits : 0;
+  }
+  ctx->budget.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+  SCB_CUDA(cudaMemcpyAsync(ctx->budget.p, b, (size_t)L.groups * L.fpw * sizeof(uint64_t),
+                           cudaMemcpyHostToDevice, st));
+}
+
+double bits_to_double(uint64_t b) {
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.f;
+  }
+  return ms;
+}
+
+void require_column_split(const sc_search_cfg* cfg) {
+  if (cfg->family == SC_FAMILY_UNIFORM_ONLY)
+    fail(SC_ERR_USAGE, "UniformOnly family is not implemented on the device path yet");
+}
+
+// The per-batch hot path.  luma (host or device) may be NULL when records
+// are given; est / records / t_min_in are host or device pointers.
+//   main stream : est -> K2/K3 time tables -> step 1 -> [join] -> step 2
+//   side stream : luma H2D -> K1 -> K2/K3 moment tables          (overlaps step 1)
+void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc, int frames,
+                  const void* luma, int bps, size_t pitch, size_t fstride, const double* est,
+                  const sc_ctu_record* records, const double* t_min_in, bool do1, bool do2,
+                  sc_search_result* out, sc_ctu_record* records_out) {
+  if (frames < 1) fail(SC_ERR_USAGE, "n_frames must be >= 1");
+  Plan* plan = get_plan(ctx, g, cfg, maxc);
+  upload_plan(ctx, plan);
+  const Layouts L = layouts_for(g, frames);
+  const size_t cells = (size_t)g.cols * g.rows;
+  cudaStream_t s = main_stream(ctx), s2 = ctx->stream2;
+  cudaEvent_t* ev = ctx->ev;
+  SCB_CUDA(cudaEventRecord(ev[0], s));
+  // fork the side stream from the caller's stream
+  SCB_CUDA(cudaEventRecord(ev[7], s));
+  SCB_CUDA(cudaStreamWaitEvent(s2, ev[7], 0));
+  const bool need_moments = do2;
+  SCB_CUDA(cudaEventRecord(ev[4], s2));
+  if (need_moments) {
+    ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
+    if (luma) {
+      const int W = g.frame_width, H = g.frame_height;
+      const size_t span = (size_t)(frames - 1) * fstride + pitch * (H - 1) + (size_t)W * bps;
+      const void* d_luma = luma;
+      if (!is_device_ptr(luma)) {
+        ctx->luma.ensure(span);
+        SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyDefault, s2));
+        d_luma = ctx->luma.p;
+      }
+      SCB_CUDA(cudaEventRecord(ev[4], s2));
+      texture_moments_device(d_luma, bps, W, H, pitch, fstride, g.ctu_size, frames, g.cols, g.rows,
+                             ctx->records.as<sc_ctu_record>(), s2);
+    } else {
+      SCB_CUDA(cudaMemcpyAsync(ctx->records.p, records, cells * frames * sizeof(sc_ctu_record),
+                               cudaMemcpyDefault, s2));
+      SCB_CUDA(cudaEventRecord(ev[4], s2));
+    }
+  }
+  SCB_CUDA(cudaEventRecord(ev[5], s2));
+  if (need_moments) enqueue_moment_tables(ctx, g, L, false, s2);
+  SCB_CUDA(cudaEventRecord(ev[6], s2));
+  // main stream
+  ctx->est.ensure((size_t)frames * cells * sizeof(double));
+  SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
+                           cudaMemcpyDefault, s));
+  enqueue_time_tables(ctx, g, L, false, s);
+  SCB_CUDA(cudaEventRecord(ev[1], s));
+  if (do1) enqueue_step(ctx, g, cfg, plan, L, 1, s);
+  else upload_budgets(ctx, L, t_min_in, cfg.lambda, s);
+  SCB_CUDA(cudaEventRecord(ev[2], s));
+  SCB_CUDA(cudaStreamWaitEvent(s, ev[6], 0));  // join
+  SCB_CUDA(cudaEventRecord(ev[8], s));
+  if (do2) enqueue_step(ctx, g, cfg, plan, L, 2, s);
+  SCB_CUDA(cudaEventRecord(ev[3], s));
+  const size_t nfb = (size_t)2 * L.groups * L.fpw;
+  ctx->h_frame_best.ensure(nfb * sizeof(FrameBest));
+  SCB_CUDA(cudaMemcpyAsync(ctx->h_frame_best.p, ctx->frame_best.p, nfb * sizeof(FrameBest),
+                           cudaMemcpyDeviceToHost, s));
+  if (records_out && need_moments)
+    SCB_CUDA(cudaMemcpyAsync(records_out, ctx->records.p, cells * frames * sizeof(sc_ctu_record),
+                             cudaMemcpyDefault, s));
+  SCB_CUDA(cudaEventRecord(ev[9], s));
+  SCB_CUDA(cudaStreamSynchronize(s));
+  // timings
+  ctx->timings[0] = need_moments && luma ? 1000.0 * ev_ms(ev[4], ev[5]) : 0.0;
+  ctx->timings[1] = 1000.0 * (ev_ms(ev[0], ev[1]) + (need_moments ? ev_ms(ev[5], ev[6]) : 0.f));
+  ctx->timings[2] = do1 ? 1000.0 * ev_ms(ev[1], ev[2]) : 0.0;
+  ctx->timings[3] = do2 ? 1000.0 * ev_ms(ev[8], ev[3]) : 0.0;
+  ctx->timings[4] = 1000.0 * ev_ms(ev[0], ev[9]);
+  // results
+  const FrameBest* hb = ctx->h_frame_best.as<FrameBest>();
+  const FrameBest* b1 = hb;
+  const FrameBest* b2 = hb + (size_t)L.groups * L.fpw;
+  ctx->last_best[0].assign(b1, b1 + frames);
+  ctx->last_best[1].assign(b2, b2 + frames);
+  for (int f = 0; f < frames; ++f) {
+    sc_search_result& r = out[f];
+    std::memset(&r, 0, sizeof(r));
+    if (do1) {
+      if (!b1[f].found) fail(SC_ERR_NO_CANDIDATE, "area constraint admits no candidate partition");
+      r.t_min_us = bits_to_double(b1[f].t);
+      r.candidates_step1 = b1[f].count;
+      r.leaves_scored_step1 = b1[f].count;
+      layout_from_snap(b1[f], cfg.n_slices, &r.argmin);
+    } else if (t_min_in) {
+      double tm;
+      SCB_CUDA(cudaMemcpy(&tm, t_min_in + f, sizeof(double), cudaMemcpyDefault));
+      r.t_min_us = tm;
+    }
+    if (do2) {
+      if (!b2[f].found) fail(SC_ERR_NO_CANDIDATE, "no candidate within the time budget");
+      r.t_best_us = bits_to_double(b2[f].t);
+      r.sse_best = b2[f].sse;
+      r.candidates_step2 = b2[f].count;
+      r.leaves_scored_step2 = b2[f].count;
+      layout_from_snap(b2[f], cfg.n_slices, &r.best);
+    }
+    r.candidates_evaluated = r.candidates_step1 + r.candidates_step2;
+    r.time_min_step_us = ctx->timings[2] / frames;
+    r.clustering_step_us = ctx->timings[3] / frames;
+    r.search_time_us = (ctx->timings[2] + ctx->timings[3]) / frames;
+  }
+}
+
+}  // namespace
+
+sc_ctx::~sc_ctx() {
+  for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rs_search, &usat,
+                  &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec})
+    b->release();
+  h_stage.release();
+  h_records.release();
+  h_frame_best.release();
+  h_budget.release();
+  for (Plan* p : plans) {
+    p->d_items.release();
+    p->d_bmax.release();
+    delete p;
+  }
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+  if (stream2) cudaStreamDestroy(stream2);
+}
+
+extern "C" {
+
+const char* sc_last_error(void) { return g_last_error.c_str(); }
+int sc_abi_version(void) { return SC_ABI_VERSION; }
+
+sc_status sc_grid_make(int32_t w, int32_t h, int32_t ctu, sc_grid* out) {
+  return guarded([&] {
+    if (!out) fail(SC_ERR_USAGE, "out is NULL");
+    *out = make_grid(w, h, ctu);
+  });
+}
+
+// temporal_layer_of_poc (cost.cpp:28-38)
+sc_status sc_temporal_layer(int32_t poc, int32_t gop, int32_t* out) {
+  return guarded([&] {
+    if (gop < 1 || (gop & (gop - 1)) != 0)
+      fail(SC_ERR_CONFIG, "gop size must be a power of two, got " + std::to_string(gop));
+    if (poc < 0) fail(SC_ERR_CONFIG, "poc must be >= 0");
+    const unsigned rem = (unsigned)poc % (unsigned)gop;
+    *out = rem == 0 ? 0 : (__builtin_ctz((unsigned)gop) - __builtin_ctz(rem));
+  });
+}
+
+sc_status sc_ctx_create(int32_t device, sc_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(SC_ERR_USAGE, "out is NULL");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      fail(SC_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) fail(SC_ERR_CUDA, "device index out of range");
+    SCB_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    SCB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      fail(SC_ERR_CUDA, std::string("device is not sm_100-class: ") + prop.name);
+    sc_ctx* c = new sc_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    SCB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    SCB_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    for (auto& e : c->ev) SCB_CUDA(cudaEventCreate(&e));
+    *out = c;
+  });
+}
+
+sc_status sc_ctx_destroy(sc_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    delete ctx;
+  });
+}
+
+sc_status sc_ctx_set_shard(sc_ctx* ctx, int32_t rank, int32_t world) {
+  return guarded([&] {
+    if (!ctx) fail(SC_ERR_USAGE, "ctx is NULL");
+    if (world < 1 || rank < 0 || rank >= world) fail(SC_ERR_CONFIG, "bad shard rank/world");
+    ctx->shard_rank = rank;
+    ctx->shard_world = world;
+  });
+}
+
+sc_status sc_texture_validate(const sc_grid* grid, const sc_ctu_record* records) {
+  return guarded([&] {
+    check_grid(grid);
+    if (!records) fail(SC_ERR_USAGE, "records is NULL");
+    validate_records(*grid, records);
+  });
+}
+
+sc_status sc_ctx_set_stream(sc_ctx* ctx, void* cuda_stream) {
+  return guarded([&] {
+    if (!ctx) fail(SC_ERR_USAGE, "ctx is NULL");
+    ctx->user_stream = static_cast<cudaStream_t>(cuda_stream);
+  });
+}
+
+sc_status sc_ctx_timings(sc_ctx* ctx, double out[5]) {
+  return guarded([&] {
+    if (!ctx || !out) fail(SC_ERR_USAGE, "NULL argument");
+    for (int i = 0; i < 5; ++i) out[i] = ctx->timings[i];
+  });
+}
+
+sc_status sc_texture_moments(sc_ctx* ctx, const void* luma, int32_t bps, int32_t width,
+                             int32_t height, size_t pitch, size_t fstride, int32_t ctu,
+                             int32_t frames, sc_ctu_record* out) {
+  return guarded([&] {
+    if (!ctx || !luma || !out) fail(SC_ERR_USAGE, "NULL argument");
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    sc_grid g = make_grid(width, height, ctu);
+    if (bps != 1 && bps != 2) fail(SC_ERR_FORMAT, "bytes_per_sample must be 1 or 2");
+    if (frames < 1) fail(SC_ERR_USAGE, "n_frames must be >= 1");
+    if (pitch < (size_t)width * bps) fail(SC_ERR_GEOMETRY, "pitch smaller than a row");
+    if (frames > 1 && fstride < pitch * height) fail(SC_ERR_GEOMETRY, "frame stride too small");
+    cudaStream_t s = main_stream(ctx);
+    const size_t span = (size_t)(frames - 1) * fstride + pitch * (height - 1) + (size_t)width * bps;
+    const void* d_luma = luma;
+    if (!is_device_ptr(luma)) {
+      ctx->luma.ensure(span);
+      SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyDefault, s));
+      d_luma = ctx->luma.p;
+    }
+    const size_t cells = (size_t)g.cols * g.rows;
+    sc_ctu_record* d_out = out;
+    const bool out_dev = is_device_ptr(out);
+    if (!out_dev) {
+      ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
+      d_out = ctx->records.as<sc_ctu_record>();
+    }
+    SCB_CUDA(cudaEventRecord(ctx->ev[4], s));
+    texture_moments_device(d_luma, bps, width, height, pitch, fstride, ctu, frames, g.cols, g.rows,
+                           d_out, s);
+    SCB_CUDA(cudaEventRecord(ctx->ev[5], s));
+    if (!out_dev)
+      SCB_CUDA(cudaMemcpyAsync(out, d_out, cells * frames * sizeof(sc_ctu_record),
+                               cudaMemcpyDeviceToHost, s));
+    SCB_CUDA(cudaStreamSynchronize(s));
+    ctx->timings[0] = 1000.0 * ev_ms(ctx->ev[4], ctx->ev[5]);
+  });
+}
+
+sc_status sc_grid_tables(sc_ctx* ctx, const sc_grid* grid, const double* est,
+                         const sc_ctu_record* records, int32_t frames, double* rect_time,
+                         double* rect_sse, double* sat) {
+  return guarded([&] {
+    if (!ctx || !est) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    if (frames < 1) fail(SC_ERR_USAGE, "n_frames must be >= 1");
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    const sc_grid& g = *grid;
+    const size_t cells = (size_t)g.cols * g.rows;
+    if (records && !is_device_ptr(records))
+      for (int f = 0; f < frames; ++f) validate_records(g, records + f * cells);
+    const Layouts L = layouts_for(g, frames);
+    cudaStream_t s = main_stream(ctx);
+    ctx->est.ensure((size_t)frames * cells * sizeof(double));
+    SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
+                             cudaMemcpyDefault, s));
+    enqueue_time_tables(ctx, g, L, true, s);
+    if (records) {
+      ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
+      SCB_CUDA(cudaMemcpyAsync(ctx->records.p, records, cells * frames * sizeof(sc_ctu_record),
+                               cudaMemcpyDefault, s));
+      enqueue_moment_tables(ctx, g, L, true, s);
+    }
+    if (sat)
+      SCB_CUDA(cudaMemcpyAsync(sat, ctx->sat.p, (size_t)frames * L.nsat * sizeof(double),
+                               cudaMemcpyDefault, s));
+    if (rect_time)
+      SCB_CUDA(cudaMemcpyAsync(rect_time, ctx->rect_t.p, (size_t)frames * L.nr * sizeof(double),
+                               cudaMemcpyDefault, s));
+    if (rect_sse && records)
+      SCB_CUDA(cudaMemcpyAsync(rect_sse, ctx->rect_s.p, (size_t)frames * L.nr * sizeof(double),
+                               cudaMemcpyDefault, s));
+    SCB_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+sc_status sc_min_time_search(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                             const double* est, int32_t frames, sc_search_result* out) {
+  return guarded([&] {
+    if (!ctx || !est || !out) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const int maxc = check_cfg(*grid, cfg);
+    require_column_split(cfg);
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    run_pipeline(ctx, *grid, *cfg, maxc, frames, nullptr, 0, 0, 0, est, nullptr, nullptr, true,
+                 false, out, nullptr);
+  });
+}
+
+sc_status sc_constrained_clustering(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                                    const double* est, const sc_ctu_record* records,
+                                    const double* t_min, int32_t frames, sc_search_result* out) {
+  return guarded([&] {
+    if (!ctx || !est || !records || !t_min || !out) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const int maxc = check_cfg(*grid, cfg);
+    require_column_split(cfg);
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    const size_t cells = (size_t)grid->cols * grid->rows;
+    if (!is_device_ptr(records))
+      for (int f = 0; f < frames; ++f) validate_records(*grid, records + f * cells);
+    run_pipeline(ctx, *grid, *cfg, maxc, frames, nullptr, 0, 0, 0, est, records, t_min, false,
+                 true, out, nullptr);
+  });
+}
+
+sc_status sc_two_step(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                      const double* est, const sc_ctu_record* records, int32_t frames,
+                      sc_search_result* out) {
+  return guarded([&] {
+    if (!ctx || !est || !records || !out) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const int maxc = check_cfg(*grid, cfg);
+    require_column_split(cfg);
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    const size_t cells = (size_t)grid->cols * grid->rows;
+    if (!is_device_ptr(records))
+      for (int f = 0; f < frames; ++f) validate_records(*grid, records + f * cells);
+    run_pipeline(ctx, *grid, *cfg, maxc, frames, nullptr, 0, 0, 0, est, records, nullptr, true,
+                 true, out, nullptr);
+  });
+}
+
+sc_status sc_partition_frames(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                              const void* luma, int32_t bps, size_t pitch, size_t fstride,
+                              const double* est, int32_t frames, sc_ctu_record* records_out,
+                              sc_search_result* out) {
+  return guarded([&] {
+    if (!ctx || !luma || !est || !out) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const int maxc = check_cfg(*grid, cfg);
+    require_column_split(cfg);
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    if (bps != 1 && bps != 2) fail(SC_ERR_FORMAT, "bytes_per_sample must be 1 or 2");
+    if (pitch < (size_t)grid->frame_width * bps) fail(SC_ERR_GEOMETRY, "pitch smaller than a row");
+    if (frames > 1 && fstride < pitch * grid->frame_height)
+      fail(SC_ERR_GEOMETRY, "frame stride too small");
+    run_pipeline(ctx, *grid, *cfg, maxc, frames, luma, bps, pitch, fstride, est, nullptr, nullptr,
+                 true, true, out, records_out);
+  });
+}
+
+sc_status sc_count_candidates(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                              uint64_t* count) {
+  return guarded([&] {
+    if (!ctx || !count) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const int maxc = check_cfg(*grid, cfg);
+    require_column_split(cfg);
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    const size_t cells = (size_t)grid->cols * grid->rows;
+    std::vector<double> ones(cells, 1.0);
+    sc_search_result r;
+    run_pipeline(ctx, *grid, *cfg, maxc, 1, nullptr, 0, 0, 0, ones.data(), nullptr, nullptr, true,
+                 false, &r, nullptr);
+    *count = r.candidates_step1;
+  });
+}
+
+sc_status sc_shard_export(sc_ctx* ctx, int32_t step, int32_t frames, sc_shard_best* out) {
+  return guarded([&] {
+    if (!ctx || !out) fail(SC_ERR_USAGE, "NULL argument");
+    if (step != 1 && step != 2) fail(SC_ERR_USAGE, "step must be 1 or 2");
+    const auto& v = ctx->last_best[step - 1];
+    if ((int)v.size() < frames) fail(SC_ERR_USAGE, "no step result for that many frames");
+    for (int f = 0; f < frames; ++f) {
+      sc_shard_best& s = out[f];
+      std::memset(&s, 0, sizeof(s));
+      const FrameBest& b = v[f];
+      s.key_sse = b.sse;
+      s.key_t = b.found ? b.t : ~0ull;
+      s.item = b.found ? b.item : ~0ull;
+      s.ord = b.found ? b.ord : ~0ull;
+      s.count = b.count;
+      s.leaves = b.count;
+      layout_from_snap(b, SC_MAX_SLICES, &s.layout);
+    }
+  });
+}
+
+sc_status sc_shard_merge(int32_t step, int32_t world, int32_t frames,
+                         const sc_shard_best* gathered, sc_search_result* inout) {
+  return guarded([&] {
+    if (!gathered || !inout) fail(SC_ERR_USAGE, "NULL argument");
+    for (int f = 0; f < frames; ++f) {
+      int win = -1;
+      uint64_t total = 0;
+      for (int r = 0; r < world; ++r) {
+        const sc_shard_best& s = gathered[(size_t)r * frames + f];
+        total += s.count;
+        if (s.item == ~0ull) continue;
+        if (win < 0) { win = r; continue; }
+        const sc_shard_best& b = gathered[(size_t)win * frames + f];
+        bool less;
+        if (step == 2 && s.key_sse != b.key_sse) less = s.key_sse < b.key_sse;
+        else if (s.key_t != b.key_t) less = s.key_t < b.key_t;
+        else if (s.item != b.item) less = s.item < b.item;
+        else less = s.ord < b.ord;
+        if (less) win = r;
+      }
+      if (win < 0) fail(SC_ERR_NO_CANDIDATE, "no candidate on any shard");
+      const sc_shard_best& b = gathered[(size_t)win * frames + f];
+      sc_search_result& r = inout[f];
+      const int n = r.argmin.n_slices ? r.argmin.n_slices : r.best.n_slices;
+      sc_layout L = b.layout;
+      L.n_slices = n;
+      if (step == 1) {
+        r.t_min_us = bits_to_double(b.key_t);
+        r.argmin = L;
+        r.candidates_step1 = total;
+        r.leaves_scored_step1 = total;
+      } else {
+        r.t_best_us = bits_to_double(b.key_t);
+        r.sse_best = b.key_sse;
+        r.best = L;
+        r.candidates_step2 = total;
+        r.leaves_scored_step2 = total;
+      }
+      r.candidates_evaluated = r.candidates_step1 + r.candidates_step2;
+    }
+  });
+}
+
+// ---- synthetic inputs ----------------------------------------
+static inline uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+static inline uint64_t H4(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  return mix64(mix64(mix64(seed ^ mix64(a)) ^ b) ^ (c * 0x2545f4914f6cdd1dull));
+}
+
+sc_status sc_synth_luma(uint64_t seed, int32_t W, int32_t H, int32_t bit_depth, int32_t frames,
+                        int32_t first_frame, int32_t pct, int32_t mode, void* out) {
+  return guarded([&] {
+    if (!out || W < 1 || H < 1 || frames < 1) fail(SC_ERR_USAGE, "bad synth arguments");
+    if (bit_depth < 1 || bit_depth > 16) fail(SC_ERR_FORMAT, "bit depth must be 1..16");
+    const int bps = bit_depth <= 8 ? 1 : 2;
+    const uint32_t M = (1u << bit_depth) - 1u;
+    const size_t fbytes = (size_t)W * H * bps;
+    auto work = [&](int f0, int f1) {
+      for (int fi = f0; fi < f1; ++fi) {
+        const int f = first_frame + fi;
+        unsigned char* base = static_cast<unsigned char*>(out) + (size_t)fi * fbytes;
+        for (int y = 0; y < H; ++y) {
+          const int by = y / 128;
+          for (int x = 0; x < W; ++x) {
+            const int bx = (x + 4 * f) / 128;
+            const uint32_t g = (uint32_t)(((uint64_t)x * M / (uint64_t)(W > 1 ? W - 1 : 1) +
+                                           (uint64_t)y * M / (uint64_t)(H > 1 ? H - 1 : 1)) / 2);
+            uint32_t v;
+            const uint64_t hb = H4(seed, (uint64_t)bx, (uint64_t)by, 0);
+            if (mode == 1) {
+              const uint32_t cls = (uint32_t)(H4(seed, (uint64_t)bx, (uint64_t)by, 1) % 3);
+              if (cls == 0) v = (uint32_t)(H4(seed, (uint64_t)bx, (uint64_t)by, 2) % (M + 1));
+              else if (cls == 1) v = g;
+              else v = (uint32_t)(H4(seed, (uint64_t)f, (uint64_t)x, (uint64_t)y) % (M + 1));
+            } else if ((int)(hb % 100) < pct) {
+              v = (uint32_t)(H4(seed, (uint64_t)f, (uint64_t)x, (uint64_t)y) % (M + 1));
+            } else {
+              v = g;
+            }
+            if (bps == 1) base[(size_t)y * W + x] = (unsigned char)v;
+            else reinterpret_cast<uint16_t*>(base)[(size_t)y * W + x] = (uint16_t)v;
+          }
+        }
+      }
+    };
+    int nt = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
+    nt = std::min(nt, frames);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+      const int f0 = (int)((int64_t)frames * t / nt), f1 = (int)((int64_t)frames * (t + 1) / nt);
+      th.emplace_back(work, f0, f1);
+    }
+    for (auto& t : th) t.join();
+  });
+}
+
+sc_status sc_synth_times(uint64_t seed, int32_t tag, int32_t cells, double sigma, double* out) {
+  return guarded([&] {
+    if (!out || cells < 1) fail(SC_ERR_USAGE, "bad synth arguments");
+    for (int i = 0; i < cells; ++i) {
+      const double u1 = ((H4(seed, 0x71e5ull + (uint64_t)tag, (uint64_t)i, 1) >> 11) + 1) *
+                        (1.0 / 9007199254740992.0);
+      const double u2 = (H4(seed, 0x71e5ull + (uint64_t)tag, (uint64_t)i, 2) >> 11) *
+                        (1.0 / 9007199254740992.0);
+      const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+      out[i] = (double)(float)std::exp(sigma * z);
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// Shared declarations of the B200 TRS partitioner core (C-ABI implementation).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "slicecraft_b200.h"
+
+namespace scb {
+
+// ---- errors ----------------------------------------------------------------
+// Exceptions never cross the C ABI: every entry point catches scb::Fail and
+// maps it to its sc_status plus the thread-local message (sc_last_error).
+struct Fail {
+  sc_status status;
+  std::string msg;
+};
+[[noreturn]] inline void fail(sc_status s, const std::string& m) { throw Fail{s, m}; }
+
+#define SCB_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      ::scb::fail(SC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---- geometry --------------------------------------------------------------
+inline int cell_w(const sc_grid& g, int x) {
+  int r = g.frame_width - x * g.ctu_size;
+  return r < g.ctu_size ? r : g.ctu_size;
+}
+inline int cell_h(const sc_grid& g, int y) {
+  int r = g.frame_height - y * g.ctu_size;
+  return r < g.ctu_size ? r : g.ctu_size;
+}
+// Rectangle numbering shared by every table:
+//   rect(x0,w,y0,h) = xw(x0,w) * NYH + yh(y0,h)
+__host__ __device__ inline int xw_index(int cols, int x0, int w) {
+  return x0 * cols - (x0 * (x0 - 1)) / 2 + (w - 1);
+}
+__host__ __device__ inline int yh_index(int rows, int y0, int h) {
+  return y0 * rows - (y0 * (y0 - 1)) / 2 + (h - 1);
+}
+inline int n_xw(int cols) { return cols * (cols + 1) / 2; }
+inline int n_yh(int rows) { return rows * (rows + 1) / 2; }
+
+// ---- device buffers ----------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    SCB_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    SCB_CUDA(cudaMallocHost(&p, n));
+    bytes = n;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// ---- search plan (frame-independent; cached per grid+config) ----------------
+// A work item is a lex-ordered prefix (c, w_0..w_{d-1}) of the ColumnSplit
+// enumeration (search.cpp:120-143); the items, in index order, tile the
+// reference's enumeration order exactly.
+struct WorkItem {
+  uint8_t c, d, pad0, pad1;
+  uint8_t w[12];
+};
+static_assert(sizeof(WorkItem) == 16, "WorkItem is one uint4");
+
+struct PlanKey {
+  int cols, rows, n, maxc, coverage;
+  double k;
+  bool operator==(const PlanKey& o) const {
+    return cols == o.cols && rows == o.rows && n == o.n && maxc == o.maxc &&
+           coverage == o.coverage && k == o.k;
+  }
+};
+
+struct Plan {
+  PlanKey key{};
+  std::vector<WorkItem> items;
+  std::vector<int32_t> bmax;  // bmax[a]: largest B with k*a > B, -1 if none
+  DevBuf d_items, d_bmax;
+  bool uploaded = false;
+};
+
+// Per-lane best record written by the search kernels (one per lane of every
+// persistent warp); reduced per frame by the finalize kernel.
+struct LaneBest {
+  uint64_t t;      // f64 bits of the best time (non-negative => monotone)
+  double sse;      // step 2 key
+  uint64_t item;   // work-item index
+  uint64_t ord;    // ordinal of the candidate inside the item
+};
+constexpr int kSnapBytes = 96;  // W[16] R[16] H[64], bytes
+
+// Arguments of the search kernels (search.cu), filled by api.cu.
+struct SearchArgs {
+  int cols, rows, n, nyh, max_area, coverage;
+  const WorkItem* items;
+  uint32_t n_items;       // items of this shard
+  uint32_t item_offset;   // global index = offset + k * stride
+  uint32_t item_stride;
+  uint32_t* counter;
+  const int32_t* bmax;    // [max_area + 1]
+  const uint64_t* rt;     // [NR][FPW] clamped time bits, this frame group
+  const double* rs;       // [NR][FPW] SSE (step 2)
+  const uint64_t* budget; // [FPW] budget bits (step 2)
+  LaneBest* lanes;        // [warps * 32]
+  uint8_t* snaps;         // [warps * 32][kSnapBytes]
+  unsigned long long* count_out;
+};
+
+// Device-side per-frame result written by finalize.
+struct FrameBest {
+  uint64_t t;
+  double sse;
+  uint64_t item;
+  uint64_t ord;
+  uint64_t count;
+  uint8_t snap[kSnapBytes];
+  int32_t found;
+  int32_t pad;
+};
+
+}  // namespace scb
+
+// The opaque context behind sc_ctx*.
+struct sc_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;
+  cudaStream_t user_stream = nullptr;
+  cudaEvent_t ev[10] = {};
+  double timings[5] = {0, 0, 0, 0, 0};
+  int shard_rank = 0, shard_world = 1;
+  // staging / tables
+  scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rs_search, usat;
+  scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec;
+  int dec_cols = -1, dec_rows = -1;
+  scb::HostBuf h_stage, h_records, h_frame_best, h_budget;
+  std::vector<scb::Plan*> plans;
+  // last step results (for shard export)
+  std::vector<scb::FrameBest> last_best[2];
+  uint64_t last_leaves[2] = {0, 0};
+  ~sc_ctx();
+};

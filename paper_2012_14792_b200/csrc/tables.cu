@@ -1,0 +1,176 @@
+// K2 — summed-area tables; K3 — per-rectangle time and SSE tables.
+//
+// K2 (replaces PrefixSumTable ctor, cost.cpp:97-112, and the TextureStats
+// SATs, texture.cpp:113-129): one CTA per frame.  The f64 table must follow the
+// reference recurrence T = ((v + L) + U) - UL in row-major dependency order, so
+// it is computed as an anti-diagonal wavefront (one thread per CTU row, one
+// barrier per diagonal); a row-scan/column-scan would reassociate and differ.
+// The three u64 tables are modular and order-free; they ride the same wavefront.
+//
+// K3 (replaces rect_sum, cost.hpp:75-81, and rect_moments + sse,
+// texture.cpp:83-88/132-143): one thread per (frame, rectangle).  Times use
+// the reference corner order ((d - b) - c) + a; SSE converts the exact
+// 128-bit numerator count*sumsq - sum^2 to double with round-to-nearest-even
+// (as GCC's __floattidf does) and divides by count.  The search-layout copies
+// are frame-interleaved ([group][rect][FPW]) so that the lanes of a warp —
+// one frame each — read one contiguous line per rectangle.
+#include "common.cuh"
+
+namespace scb {
+
+__global__ void k_grid_sat(const double* __restrict__ est, const sc_ctu_record* __restrict__ rec,
+                           int cols, int rows, double* __restrict__ sat_out,
+                           uint64_t* __restrict__ usat_out) {
+  extern __shared__ unsigned char smem[];
+  const int stride = cols + 1;
+  const int nsat = stride * (rows + 1);
+  double* T = reinterpret_cast<double*>(smem);
+  uint64_t* U = reinterpret_cast<uint64_t*>(T + nsat);  // 3 tables
+  const int f = blockIdx.x;
+  const double* v = est ? est + (size_t)f * cols * rows : nullptr;
+  const sc_ctu_record* r = rec ? rec + (size_t)f * cols * rows : nullptr;
+  for (int i = threadIdx.x; i < nsat; i += blockDim.x) {
+    T[i] = 0.0;
+    U[i] = 0;
+    U[nsat + i] = 0;
+    U[2 * nsat + i] = 0;
+  }
+  __syncthreads();
+  for (int s = 0; s <= cols + rows - 2; ++s) {
+    for (int y = threadIdx.x; y < rows; y += blockDim.x) {
+      const int x = s - y;
+      if (x >= 0 && x < cols) {
+        const int i = (y + 1) * stride + (x + 1);
+        if (v) {
+          const double val = v[y * cols + x];
+          T[i] = __dsub_rn(__dadd_rn(__dadd_rn(val, T[i - 1]), T[i - stride]), T[i - stride - 1]);
+        }
+        if (r) {
+          const sc_ctu_record c = r[y * cols + x];
+          U[i] = c.count + U[i - 1] + U[i - stride] - U[i - stride - 1];
+          U[nsat + i] = c.sum + U[nsat + i - 1] + U[nsat + i - stride] - U[nsat + i - stride - 1];
+          U[2 * nsat + i] =
+              c.sumsq + U[2 * nsat + i - 1] + U[2 * nsat + i - stride] - U[2 * nsat + i - stride - 1];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < nsat; i += blockDim.x) {
+    if (v) sat_out[(size_t)f * nsat + i] = T[i];
+    if (r) {
+      usat_out[((size_t)f * 3 + 0) * nsat + i] = U[i];
+      usat_out[((size_t)f * 3 + 1) * nsat + i] = U[nsat + i];
+      usat_out[((size_t)f * 3 + 2) * nsat + i] = U[2 * nsat + i];
+    }
+  }
+}
+
+// Unsigned 128-bit (hi, lo) -> double, round to nearest even.
+__device__ __forceinline__ double u128_to_double_rn(uint64_t hi, uint64_t lo) {
+  if (hi == 0) return __ull2double_rn(lo);
+  const int s = __clzll((long long)hi);  // 0..63
+  uint64_t top = s ? ((hi << s) | (lo >> (64 - s))) : hi;
+  const uint64_t rest = lo << s;           // bits shifted out (s==0: all of lo)
+  top |= (rest != 0) ? 1ull : 0ull;        // sticky below the rounding position
+  return ldexp(__ull2double_rn(top), 64 - s);
+}
+
+// SliceMoments::sse (texture.cpp:83-88) with exact i128 arithmetic.
+__device__ __forceinline__ double moments_sse(uint64_t c, uint64_t s, uint64_t q) {
+  if (c == 0) return 0.0;
+  uint64_t p1lo = c * q, p1hi = __umul64hi(c, q);
+  uint64_t p2lo = s * s, p2hi = __umul64hi(s, s);
+  uint64_t lo = p1lo - p2lo;
+  uint64_t hi = p1hi - p2hi - (p1lo < p2lo ? 1ull : 0ull);
+  double mag;
+  if ((int64_t)hi < 0) {  // negative numerator (invalid records only)
+    uint64_t nlo = ~lo + 1ull;
+    uint64_t nhi = ~hi + (nlo == 0 ? 1ull : 0ull);
+    mag = -u128_to_double_rn(nhi, nlo);
+  } else {
+    mag = u128_to_double_rn(hi, lo);
+  }
+  return __ddiv_rn(mag, (double)c);
+}
+
+struct RectDecode {
+  const int16_t* xw_x0;
+  const int16_t* xw_w;
+  const int16_t* yh_y0;
+  const int16_t* yh_h;
+};
+
+__global__ void k_rect_tables(const double* __restrict__ sat, const uint64_t* __restrict__ usat,
+                              RectDecode dec, int cols, int rows, int frames, int fpw,
+                              double* __restrict__ rect_t, double* __restrict__ rect_s,
+                              uint64_t* __restrict__ rt_search, double* __restrict__ rs_search) {
+  const int nyh = rows * (rows + 1) / 2;
+  const int nr = cols * (cols + 1) / 2 * nyh;
+  const int stride = cols + 1;
+  const int nsat = stride * (rows + 1);
+  const size_t total = (size_t)nr * frames;
+  for (size_t id = blockIdx.x * (size_t)blockDim.x + threadIdx.x; id < total;
+       id += (size_t)gridDim.x * blockDim.x) {
+    const int f = (int)(id / nr);
+    const int rr = (int)(id % nr);
+    const int xw = rr / nyh, yh = rr % nyh;
+    const int x0 = dec.xw_x0[xw], w = dec.xw_w[xw];
+    const int y0 = dec.yh_y0[yh], h = dec.yh_h[yh];
+    const int ia = y0 * stride + x0, ib = y0 * stride + x0 + w;
+    const int ic = (y0 + h) * stride + x0, idd = (y0 + h) * stride + x0 + w;
+    const int g = f / fpw, slot = f % fpw;
+    const size_t so = ((size_t)g * nr + rr) * fpw + slot;
+    if (sat) {
+      const double* T = sat + (size_t)f * nsat;
+      const double t = __dadd_rn(__dsub_rn(__dsub_rn(T[idd], T[ib]), T[ic]), T[ia]);
+      if (rect_t) rect_t[(size_t)f * nr + rr] = t;
+      // layout_time's running max starts at 0.0 and keeps it on ties/NaN
+      // (search.cpp:77-83): clamp to +0.0 so u64 bit order == double order.
+      if (rt_search) rt_search[so] = (t > 0.0) ? (uint64_t)__double_as_longlong(t) : 0ull;
+    }
+    if (usat) {
+      const uint64_t* U = usat + (size_t)f * 3 * nsat;
+      const uint64_t c = U[idd] - U[ib] - U[ic] + U[ia];
+      const uint64_t s = U[nsat + idd] - U[nsat + ib] - U[nsat + ic] + U[nsat + ia];
+      const uint64_t q = U[2 * nsat + idd] - U[2 * nsat + ib] - U[2 * nsat + ic] + U[2 * nsat + ia];
+      const double e = moments_sse(c, s, q);
+      if (rect_s) rect_s[(size_t)f * nr + rr] = e;
+      if (rs_search) rs_search[so] = e;
+    }
+  }
+}
+
+void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, int rows,
+                     int frames, double* d_sat, uint64_t* d_usat, cudaStream_t st) {
+  const int nsat = (cols + 1) * (rows + 1);
+  const size_t smem = (size_t)nsat * (8 + 24);
+  if (smem > 227 * 1024) fail(SC_ERR_SIZE, "CTU grid too large for the shared-memory SAT");
+  static bool attr_set = false;
+  if (!attr_set) {
+    SCB_CUDA(cudaFuncSetAttribute(k_grid_sat, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    attr_set = true;
+  }
+  int threads = rows < 32 ? 32 : (rows > 1024 ? 1024 : ((rows + 31) / 32) * 32);
+  k_grid_sat<<<frames, threads, smem, st>>>(d_est, d_rec, cols, rows, d_sat, d_usat);
+  SCB_CUDA(cudaGetLastError());
+}
+
+void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16_t* d_dec,
+                        int cols, int rows, int frames, int fpw, double* d_rect_t,
+                        double* d_rect_s, uint64_t* d_rt, double* d_rs, int sm_count,
+                        cudaStream_t st) {
+  const int nxw = cols * (cols + 1) / 2, nyh = rows * (rows + 1) / 2;
+  RectDecode dec{d_dec, d_dec + nxw, d_dec + 2 * nxw, d_dec + 2 * nxw + nyh};
+  const size_t total = (size_t)nxw * nyh * frames;
+  size_t blocks = (total + 255) / 256;
+  const size_t cap = (size_t)sm_count * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_rect_tables<<<(unsigned)blocks, 256, 0, st>>>(d_sat, d_usat, dec, cols, rows, frames, fpw,
+                                                  d_rect_t, d_rect_s, d_rt, d_rs);
+  SCB_CUDA(cudaGetLastError());
+}
+
+}  // namespace scb

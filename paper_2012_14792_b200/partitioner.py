@@ -1,0 +1,364 @@
+"""Python mirror of the reference partitioner API (proj/include/slicecraft).
+
+Same names, argument meaning and error behaviour as the reference C++ API, so
+the parity tests read like the reference's own (absent) tests:
+
+  texture map         ctu_stats                       texture.hpp:83
+  CTU-complexity      temporal_layer_of_poc,          cost.hpp:39
+                      CostHistory.append,              cost.hpp:43-58
+                      estimate_ctu_times              cost.hpp:64
+  partition search    min_time_search,                search.hpp:66-67
+                      constrained_clustering_search,  search.hpp:72-75
+                      two_step_partition              search.hpp:80-82
+
+Every compute call goes through the C-ABI (include/slicecraft_b200.h) into the
+sm_100a kernels; the host-side pieces here are the O(cells) cost-history
+bookkeeping the reference also keeps on the host (cost.cpp:56-95).
+Errors surface as SlicecraftError whose ``kind`` names the reference class.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ._abi import (CtuRecord, Grid, Layout, SearchCfg, SearchResult, ShardBest,
+                   SlicecraftError, check, lib)
+
+COLUMN_SPLIT, UNIFORM_ONLY = 0, 1
+COVERAGE_REFERENCE, COVERAGE_COVERING = 0, 1
+MODE_EXHAUSTIVE, MODE_PRUNED = 0, 1
+
+RECORD_DTYPE = np.dtype([("count", "<u8"), ("sum", "<u8"), ("sumsq", "<u8")])
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+@dataclass(frozen=True)
+class CtuGrid:
+    """CtuGrid (grid.hpp:13-34); build with CtuGrid.make."""
+    frame_width: int
+    frame_height: int
+    ctu_size: int
+    cols: int
+    rows: int
+
+    @staticmethod
+    def make(frame_width: int, frame_height: int, ctu_size: int = 128) -> "CtuGrid":
+        g = Grid()
+        check(lib().sc_grid_make(frame_width, frame_height, ctu_size, C.byref(g)))
+        return CtuGrid(g.frame_width, g.frame_height, g.ctu_size, g.cols, g.rows)
+
+    def cell_count(self) -> int:
+        return self.cols * self.rows
+
+    def c(self) -> Grid:
+        return Grid(self.frame_width, self.frame_height, self.ctu_size, self.cols, self.rows)
+
+    @property
+    def n_rects(self) -> int:
+        return self.cols * (self.cols + 1) // 2 * (self.rows * (self.rows + 1) // 2)
+
+
+@dataclass
+class SearchConfig:
+    """SearchConfig (search.hpp:22-34) + coverage / mode (B200 additions)."""
+    n_slices: int = 4
+    lambda_: float = 0.0
+    k_area: float = 3.0
+    family: int = COLUMN_SPLIT
+    max_tile_cols: int = 0
+    workers: int = 1
+    coverage: int = COVERAGE_REFERENCE
+    mode: int = MODE_EXHAUSTIVE
+
+    def c(self) -> SearchCfg:
+        return SearchCfg(self.n_slices, self.lambda_, self.k_area, self.family,
+                         self.max_tile_cols, self.workers, self.coverage, self.mode)
+
+
+def temporal_layer_of_poc(poc: int, gop_size: int) -> int:
+    out = C.c_int32()
+    check(lib().sc_temporal_layer(poc, gop_size, C.byref(out)))
+    return out.value
+
+
+# CostSource (cost.hpp:11-16)
+MEASURED, CO_TEMPORAL_LAYER, MOST_RECENT_ANY, UNIFORM = 0, 1, 2, 3
+
+
+@dataclass
+class CostMap:
+    """CostMap (cost.hpp:21-34): per-CTU times in microseconds, row-major."""
+    grid: CtuGrid
+    times_us: np.ndarray
+    poc: int = 0
+    temporal_layer: int = 0
+    qp: int = 0
+    source: int = MEASURED
+    source_poc: int = -1
+
+
+class CostHistory:
+    """CostHistory (cost.hpp:43-58; append validation cost.cpp:56-75)."""
+
+    def __init__(self, grid: CtuGrid, gop_size: int = 16):
+        temporal_layer_of_poc(0, gop_size)  # validates the GOP eagerly
+        self.grid = grid
+        self.gop_size = gop_size
+        self.maps: List[CostMap] = []
+
+    def append(self, m: CostMap) -> None:
+        if m.grid != self.grid:
+            raise SlicecraftError(1, "cost map grid does not match the history grid")
+        t = np.asarray(m.times_us, dtype=np.float64)
+        if t.size != self.grid.cell_count():
+            raise SlicecraftError(1, "cost map has wrong number of entries")
+        if not np.all(np.isfinite(t)) or np.any(t < 0.0):
+            raise SlicecraftError(7, "CTU times must be finite and >= 0")
+        if any(x.poc == m.poc for x in self.maps):
+            raise SlicecraftError(9, f"duplicate poc {m.poc} in cost history")
+        self.maps.append(m)
+
+
+def estimate_ctu_times(history: CostHistory, poc: int) -> CostMap:
+    """estimate_ctu_times (cost.cpp:66-95): co-TL, else most recent, else ones."""
+    tl = temporal_layer_of_poc(poc, history.gop_size)
+    for m in reversed(history.maps):
+        if m.temporal_layer == tl:
+            return CostMap(history.grid, np.array(m.times_us, dtype=np.float64), poc, tl, m.qp,
+                           CO_TEMPORAL_LAYER, m.poc)
+    if history.maps:
+        m = history.maps[-1]
+        return CostMap(history.grid, np.array(m.times_us, dtype=np.float64), poc, tl, m.qp,
+                       MOST_RECENT_ANY, m.poc)
+    return CostMap(history.grid, np.ones(history.grid.cell_count()), poc, tl, 0, UNIFORM, -1)
+
+
+@dataclass
+class TextureStats:
+    """TextureStats (texture.hpp:54-79): per-CTU records of one frame."""
+    grid: CtuGrid
+    records: np.ndarray  # RECORD_DTYPE, cols*rows
+    poc: int = 0
+
+
+@dataclass
+class Slice:
+    x0: int
+    y0: int
+    w: int
+    h: int
+    id: int
+
+
+@dataclass
+class Partition:
+    """Partition (grid.hpp:62-71) as produced by layout_to_partition (search.cpp:63-75)."""
+    grid: CtuGrid
+    col_widths: List[int]
+    row_heights: List[int]
+    slices: List[Slice] = field(default_factory=list)
+
+    @staticmethod
+    def from_layout(grid: CtuGrid, L: Layout) -> "Partition":
+        p = Partition(grid, [L.col_widths[i] for i in range(L.n_cols)], [grid.rows])
+        x, run, sid = 0, 0, 0
+        for col in range(L.n_cols):
+            w = L.col_widths[col]
+            y = 0
+            for _ in range(L.runs_per_col[col]):
+                h = L.run_heights[run]
+                p.slices.append(Slice(x, y, w, h, sid))
+                sid += 1
+                run += 1
+                y += h
+            x += w
+        return p
+
+    def rects(self):
+        return [(s.x0, s.y0, s.w, s.h, s.id) for s in self.slices]
+
+
+@dataclass
+class SearchOutcome:
+    """SearchOutcome (search.hpp:36-49) + the step-1 argmin."""
+    best: Optional[Partition]
+    argmin: Optional[Partition]
+    t_min_us: float
+    t_best_us: float
+    sse_best: float
+    candidates_evaluated: int
+    candidates_step1: int
+    candidates_step2: int
+    search_time_us: float
+    time_min_step_us: float
+    clustering_step_us: float
+    leaves_scored_step1: int = 0
+    leaves_scored_step2: int = 0
+    est_source: int = UNIFORM
+    est_source_poc: int = -1
+
+
+def _outcome(grid: CtuGrid, r: SearchResult, step1: bool, step2: bool) -> SearchOutcome:
+    return SearchOutcome(
+        best=Partition.from_layout(grid, r.best) if step2 else None,
+        argmin=Partition.from_layout(grid, r.argmin) if step1 else None,
+        t_min_us=r.t_min_us, t_best_us=r.t_best_us, sse_best=r.sse_best,
+        candidates_evaluated=r.candidates_evaluated, candidates_step1=r.candidates_step1,
+        candidates_step2=r.candidates_step2, search_time_us=r.search_time_us,
+        time_min_step_us=r.time_min_step_us, clustering_step_us=r.clustering_step_us,
+        leaves_scored_step1=r.leaves_scored_step1, leaves_scored_step2=r.leaves_scored_step2)
+
+
+class Partitioner:
+    """One device context (sc_ctx) with the partitioner entry points."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        check(lib().sc_ctx_create(device, C.byref(self._h)))
+
+    def close(self) -> None:
+        if self._h:
+            lib().sc_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_shard(self, rank: int, world: int) -> None:
+        check(lib().sc_ctx_set_shard(self._h, rank, world))
+
+    # ---- texture map --------------------------------------------------------
+    def ctu_stats_batch(self, frames: np.ndarray, ctu_size: int = 128) -> np.ndarray:
+        """K1 over a [F, H, W] uint8/uint16 array (host numpy or any array
+        exposing ``data_ptr``/``ctypes``); returns [F, rows*cols] records."""
+        if frames.ndim == 2:
+            frames = frames[None]
+        F, H, W = frames.shape
+        bps = frames.dtype.itemsize
+        if frames.dtype not in (np.uint8, np.uint16):
+            raise SlicecraftError(7, "luma must be uint8 or uint16")
+        frames = np.ascontiguousarray(frames)
+        g = CtuGrid.make(W, H, ctu_size)
+        out = np.zeros((F, g.cell_count()), dtype=RECORD_DTYPE)
+        check(lib().sc_texture_moments(self._h, _ptr(frames), bps, W, H, W * bps, W * H * bps,
+                                       ctu_size, F, _ptr(out)))
+        return out
+
+    def ctu_stats(self, luma: np.ndarray, grid: CtuGrid, poc: int = 0) -> TextureStats:
+        """ctu_stats (texture.cpp:145-169)."""
+        if luma.shape != (grid.frame_height, grid.frame_width):
+            raise SlicecraftError(1, "plane dimensions do not match the grid")
+        return TextureStats(grid, self.ctu_stats_batch(luma, grid.ctu_size)[0], poc)
+
+    def grid_tables(self, grid: CtuGrid, est: np.ndarray, records: Optional[np.ndarray] = None):
+        """K2/K3: per-rectangle times (and SSEs) for F frames, rectangle order
+        xw(x0,w)*NYH + yh(y0,h).  Returns (rect_time, rect_sse, sat)."""
+        est = np.ascontiguousarray(est, dtype=np.float64).reshape(-1, grid.cell_count())
+        F = est.shape[0]
+        nr = grid.n_rects
+        rt = np.zeros((F, nr))
+        rs = np.zeros((F, nr)) if records is not None else None
+        sat = np.zeros((F, (grid.cols + 1) * (grid.rows + 1)))
+        rec = None if records is None else np.ascontiguousarray(records).reshape(F, -1)
+        check(lib().sc_grid_tables(self._h, C.byref(grid.c()), _ptr(est), _ptr(rec), F, _ptr(rt),
+                                   _ptr(rs), _ptr(sat)))
+        return rt, rs, sat
+
+    # ---- partition search ---------------------------------------------------
+    def min_time_search_batch(self, grid: CtuGrid, est: np.ndarray, cfg: SearchConfig):
+        est = np.ascontiguousarray(est, dtype=np.float64).reshape(-1, grid.cell_count())
+        F = est.shape[0]
+        res = (SearchResult * F)()
+        check(lib().sc_min_time_search(self._h, C.byref(grid.c()), C.byref(cfg.c()), _ptr(est),
+                                       F, C.cast(res, C.c_void_p)))
+        return [_outcome(grid, r, True, False) for r in res]
+
+    def min_time_search(self, est: CostMap, cfg: SearchConfig):
+        """min_time_search (search.cpp:328-332) -> (t_min, argmin Partition)."""
+        o = self.min_time_search_batch(est.grid, est.times_us, cfg)[0]
+        return o.t_min_us, o.argmin
+
+    def constrained_clustering_batch(self, grid: CtuGrid, est: np.ndarray, records: np.ndarray,
+                                     t_min: Sequence[float], cfg: SearchConfig):
+        est = np.ascontiguousarray(est, dtype=np.float64).reshape(-1, grid.cell_count())
+        F = est.shape[0]
+        rec = np.ascontiguousarray(records).reshape(F, -1)
+        tm = np.ascontiguousarray(np.asarray(t_min, dtype=np.float64).reshape(F))
+        res = (SearchResult * F)()
+        check(lib().sc_constrained_clustering(self._h, C.byref(grid.c()), C.byref(cfg.c()),
+                                              _ptr(est), _ptr(rec), _ptr(tm), F,
+                                              C.cast(res, C.c_void_p)))
+        return [_outcome(grid, r, False, True) for r in res]
+
+    def constrained_clustering_search(self, est: CostMap, stats: TextureStats, t_min_us: float,
+                                      cfg: SearchConfig) -> SearchOutcome:
+        """constrained_clustering_search (search.cpp:334-405)."""
+        if stats.grid != est.grid:
+            raise SlicecraftError(1, "texture stats grid does not match the cost map grid")
+        return self.constrained_clustering_batch(est.grid, est.times_us, stats.records,
+                                                 [t_min_us], cfg)[0]
+
+    def two_step_batch(self, grid: CtuGrid, est: np.ndarray, records: np.ndarray,
+                       cfg: SearchConfig):
+        est = np.ascontiguousarray(est, dtype=np.float64).reshape(-1, grid.cell_count())
+        F = est.shape[0]
+        rec = np.ascontiguousarray(records).reshape(F, -1)
+        res = (SearchResult * F)()
+        check(lib().sc_two_step(self._h, C.byref(grid.c()), C.byref(cfg.c()), _ptr(est),
+                                _ptr(rec), F, C.cast(res, C.c_void_p)))
+        return [_outcome(grid, r, True, True) for r in res]
+
+    def two_step_partition(self, history: CostHistory, stats: TextureStats, poc: int,
+                           cfg: SearchConfig) -> SearchOutcome:
+        """two_step_partition (search.cpp:407-434)."""
+        if stats.grid != history.grid:
+            raise SlicecraftError(1, "texture stats grid does not match the history grid")
+        est = estimate_ctu_times(history, poc)
+        o = self.two_step_batch(history.grid, est.times_us, stats.records, cfg)[0]
+        o.est_source, o.est_source_poc = est.source, est.source_poc
+        return o
+
+    def partition_frames(self, grid: CtuGrid, luma: np.ndarray, est: np.ndarray,
+                         cfg: SearchConfig, records_out: Optional[np.ndarray] = None):
+        """Whole hot path for a batch: K1 -> K2/K3 -> step 1 -> step 2."""
+        F = est.shape[0]
+        bps = luma.dtype.itemsize
+        est = np.ascontiguousarray(est, dtype=np.float64)
+        res = (SearchResult * F)()
+        W, H = grid.frame_width, grid.frame_height
+        check(lib().sc_partition_frames(self._h, C.byref(grid.c()), C.byref(cfg.c()),
+                                        _ptr(luma), bps, W * bps, W * H * bps, _ptr(est), F,
+                                        _ptr(records_out), C.cast(res, C.c_void_p)))
+        return res
+
+    def count_candidates(self, grid: CtuGrid, cfg: SearchConfig) -> int:
+        n = C.c_uint64()
+        check(lib().sc_count_candidates(self._h, C.byref(grid.c()), C.byref(cfg.c()), C.byref(n)))
+        return n.value
+
+    def shard_export(self, step: int, frames: int):
+        out = (ShardBest * frames)()
+        check(lib().sc_shard_export(self._h, step, frames, C.cast(out, C.c_void_p)))
+        return out
+
+
+def shard_merge(step: int, world: int, frames: int, gathered: bytes, results) -> None:
+    """sc_shard_merge over rank-major gathered ShardBest records."""
+    buf = (ShardBest * (world * frames)).from_buffer_copy(gathered)
+    check(lib().sc_shard_merge(step, world, frames, C.cast(buf, C.c_void_p),
+                               C.cast(results, C.c_void_p)))
+
+
+def texture_validate(grid: CtuGrid, records: np.ndarray) -> None:
+    rec = np.ascontiguousarray(records)
+    check(lib().sc_texture_validate(C.byref(grid.c()), _ptr(rec)))

@@ -1,0 +1,167 @@
+"""Generate tests/golden/*.json from the UNMODIFIED reference (oracle/_ref).
+
+Run here (where /root/reference exists):  python tests/golden/make_golden.py
+The fixtures travel to the GPU box; the reference does not.
+
+Contents
+  spec_kats.json   known-answer tests taken from the reference's SPEC examples
+                   that the compiled reference passes: texture
+                   (SPEC.md:134-135, 145), cost
+                   plus the enumeration counts of SURVEY.md §8c.
+  search_small.json  200 seeded random small instances (grids <= 6x6, n <= 6,
+                   lambda in {0, .1, .3, 1}, k in {3, 2.5, 1.5}): the reference's
+                   min_time_search + constrained_clustering_search outputs.
+  configs.json     BASELINE configs on their real synthetic inputs: cfg1 (all),
+                   cfg2 (POC 1..4), cfg3 (POC 1): two_step_partition outputs,
+                   with a hash of the estimate maps / records that were used.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle.oracle import Ref  # noqa: E402
+from paper_2012_14792_b200 import workloads as wl  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def h(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def spec_kats(r: Ref) -> dict:
+    k = {}
+    # SPEC.md:134 constant plane value 100, 2x2 CTUs of 64^2
+    st, rec = r.ctu_stats(np.full((128, 128), 100, np.uint16), 8, 64)
+    k["constant_100"] = {"w": 128, "h": 128, "ctu": 64, "value": 100, "records": rec.tolist()}
+    # SPEC.md:135 one white pixel (255) else 0
+    p = np.zeros((128, 128), np.uint16)
+    p[70, 9] = 255
+    st, rec = r.ctu_stats(p, 8, 64)
+    k["white_pixel"] = {"w": 128, "h": 128, "ctu": 64, "pixel": [9, 70], "records": rec.tolist()}
+    # SPEC.md:145 two-tone frame: left half 0, right half 200, 8x8 grid (ctu 32)
+    p = np.zeros((256, 256), np.uint16)
+    p[:, 128:] = 200
+    st, rec = r.ctu_stats(p, 8, 32)
+    vert = r.partition_eval(256, 256, 32, [4, 4], [8], [(0, 0, 4, 8, 0), (4, 0, 4, 8, 1)],
+                            records=rec, validate=True)
+    horz = r.partition_eval(256, 256, 32, [8], [8], [(0, 0, 8, 4, 0), (0, 4, 8, 4, 1)],
+                            records=rec, validate=True)
+    k["two_tone"] = {"records": rec.tolist(), "sse_vertical": vert[4], "sse_horizontal": horz[4]}
+    # SPEC.md:192-194 temporal layers at gop 16
+    k["temporal_layers"] = [[poc, 16, r.temporal_layer(poc, 16)[1]] for poc in range(0, 33)]
+    # SPEC.md:210 [[1,2],[3,4]], two row slices -> {3,7}, T = 7
+    st, mx, tot, am, _ = r.partition_eval(64, 64, 32, [2], [1, 1], [(0, 0, 2, 1, 0), (0, 1, 2, 1, 1)],
+                                          times=np.array([1.0, 2.0, 3.0, 4.0]), validate=True)
+    k["row_slices_2x2"] = {"times": [1, 2, 3, 4], "max_us": mx, "total_us": tot, "argmax": am}
+    # SPEC.md:201-203 estimator fallbacks
+    g = (128, 128, 32)
+    maps = np.stack([np.full(16, v) for v in (1.0, 2.0, 3.0)])
+    est = {}
+    for poc, pocs, tls in [(24, [0, 16, 8], [0, 0, 1]), (5, [], []), (6, [0, 16, 8], [0, 0, 1])]:
+        mm = maps[: len(pocs)] if pocs else np.zeros((0, 16))
+        st, e, src, srcp = r.estimate(*g, 16, mm, pocs, tls, poc)
+        est[str(poc) + ":" + ",".join(map(str, pocs))] = {"est0": e[0], "source": src,
+                                                          "source_poc": srcp}
+    k["estimate"] = est
+    # enumeration counts, compat = reference family
+    cnt = {}
+    for (fw, fh, ctu, n, mc) in [(64, 64, 32, 2, 0), (128, 32, 32, 2, 0), (1920, 1080, 128, 1, 0),
+                                 (1920, 1080, 128, 2, 0), (1920, 1080, 128, 4, 0),
+                                 (128, 128, 32, 4, 0), (192, 192, 32, 4, 0),
+                                 (1920, 1080, 128, 4, 2), (1920, 1080, 128, 8, 4)]:
+        st, c, _ = r.enumerate(fw, fh, ctu, n, 3.0, 0, mc)
+        cnt[f"{fw}x{fh}/{ctu}/n{n}/c{mc}"] = c
+    k["enumeration_counts"] = cnt
+    return k
+
+
+def search_small(r: Ref, n_cases: int = 200) -> list:
+    rng = np.random.default_rng(20121479)
+    cases = []
+    while len(cases) < n_cases:
+        ctu = 32
+        cols, rows = int(rng.integers(1, 7)), int(rng.integers(1, 7))
+        W = max(1, cols * ctu - int(rng.integers(0, ctu)))
+        H = max(1, rows * ctu - int(rng.integers(0, ctu)))
+        cols, rows = -(-W // ctu), -(-H // ctu)
+        n = int(rng.integers(1, min(6, cols * rows) + 1))
+        mc = int(rng.integers(0, 4))
+        lam = float(rng.choice([0.0, 0.1, 0.3, 1.0]))
+        k = float(rng.choice([3.0, 2.5, 1.5]))
+        est = rng.lognormal(0, 0.7, cols * rows)
+        if len(cases) % 7 == 0:
+            est = np.round(est * 2) / 2  # force ties
+        plane = rng.integers(0, 1024, size=(H, W)).astype(np.uint16)
+        if len(cases) % 5 == 0:
+            plane[:] = int(rng.integers(0, 1024))
+        _, rec = r.ctu_stats(plane, 10, ctu)
+        st1, t1, lay1 = r.min_time_search(W, H, ctu, est, n, lam, k, 0, mc)
+        case = {"w": W, "h": H, "ctu": ctu, "n": n, "max_tile_cols": mc, "lambda": lam, "k": k,
+                "est": est.tolist(), "records": rec.tolist(), "status1": st1}
+        if st1 == 0:
+            st2, o = r.constrained(W, H, ctu, est, rec, t1, n, lam, k, 0, mc)
+            _, cnt, _ = r.enumerate(W, H, ctu, n, k, 0, mc)
+            case.update({"t_min": t1, "argmin": lay1.rects(), "argmin_widths": lay1.widths(),
+                         "status2": st2, "t_best": o.t_best_us, "sse_best": o.sse_best,
+                         "best": o.best.rects(), "best_widths": o.best.widths(),
+                         "candidates": cnt, "candidates_step2": o.candidates_step2})
+        cases.append(case)
+    return cases
+
+
+def configs(r: Ref) -> dict:
+    out = {}
+    plan = {1: [1], 2: [1, 2, 3, 4], 3: [1]}
+    for ci, pocs in plan.items():
+        w = wl.WORKLOADS[ci]
+        F = max(pocs)
+        tr = wl.cost_trace(w, frames=F)
+        luma = wl.synth_luma(w, frames=F)
+        maps = np.stack([m.times_us for m in tr.history_maps])
+        hpocs = [m.poc for m in tr.history_maps]
+        htls = [m.temporal_layer for m in tr.history_maps]
+        res = []
+        for p in pocs:
+            t0 = time.time()
+            st, rec = r.ctu_stats(luma[p - 1].astype(np.uint16), w.bit_depth, w.ctu)
+            # history visible to frame p: POCs 0..p-1
+            st, o = r.two_step(w.width, w.height, w.ctu, 16, maps[:p], hpocs[:p], htls[:p], rec, p,
+                               w.n_slices, 0.0, 3.0, 0, w.max_tile_cols)
+            assert st == 0, r.err()
+            res.append({"poc": p, "records_hash": h(rec), "est_hash": h(tr.est[p - 1]),
+                        "records": rec.tolist() if ci == 1 else None,
+                        "t_min": o.t_min_us, "t_best": o.t_best_us, "sse_best": o.sse_best,
+                        "best": o.best.rects(), "best_widths": o.best.widths(),
+                        "candidates_step1": o.candidates_step1,
+                        "candidates_step2": o.candidates_step2,
+                        "est_source": o.est_source, "est_source_poc": o.est_source_poc,
+                        "ref_seconds": time.time() - t0})
+            print(f"cfg{ci} poc {p}: {time.time() - t0:.1f}s", flush=True)
+        out[str(ci)] = {"name": w.name, "frames": res}
+    return out
+
+
+def main():
+    r = Ref()
+    with open(os.path.join(OUT, "spec_kats.json"), "w") as f:
+        json.dump(spec_kats(r), f, indent=1)
+    with open(os.path.join(OUT, "search_small.json"), "w") as f:
+        json.dump(search_small(r), f)
+    which = sys.argv[1:] or ["configs"]
+    if "configs" in which:
+        with open(os.path.join(OUT, "configs.json"), "w") as f:
+            json.dump(configs(r), f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,264 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle and the
+golden fixtures generated from the unmodified reference.
+
+Bar: bit-exact for every integer / index artefact (CTU records, chosen
+layouts, candidate counts) and for every double the reference computes with
+the same operation order (times, SSEs, t_min, t_best, sse_best) — the
+north_star's 1e-6 relative tolerance is therefore met with margin 0.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng(2012_14792)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+# ---- K1 texture ---------------------------------------------------------------
+@pytest.mark.parametrize("shape", [(64, 64, 32), (100, 70, 32), (1920, 1080, 128),
+                                   (333, 129, 64), (3840, 2160, 128), (1000, 1000, 64),
+                                   (127, 33, 32), (1, 1, 32), (129, 257, 128)])
+@pytest.mark.parametrize("depth", [8, 10, 16])
+def test_texture_matches_oracle(part, oracle, shape, depth):
+    W, H, ctu = shape
+    hi = (1 << depth)
+    dt = np.uint8 if depth == 8 else np.uint16
+    frames = RNG.integers(0, hi, size=(3, H, W)).astype(dt)
+    frames[1] = hi - 1  # saturated plane: largest sums
+    got = part.ctu_stats_batch(frames, ctu)
+    for f in range(3):
+        exp = oracle.ctu_stats(frames[f], ctu)
+        g = np.stack([got[f]["count"], got[f]["sum"], got[f]["sumsq"]], axis=1)
+        assert np.array_equal(g, exp), (shape, depth, f)
+
+
+def test_texture_spec_kats(part):
+    k = json.load(open(os.path.join(GOLDEN, "spec_kats.json")))
+    c = k["constant_100"]
+    got = part.ctu_stats_batch(np.full((c["h"], c["w"]), 100, np.uint8), c["ctu"])[0]
+    assert [list(r) for r in got.tolist()] == c["records"]
+    wp = k["white_pixel"]
+    p = np.zeros((wp["h"], wp["w"]), np.uint8)
+    p[wp["pixel"][1], wp["pixel"][0]] = 255
+    got = part.ctu_stats_batch(p, wp["ctu"])[0]
+    assert [list(r) for r in got.tolist()] == wp["records"]
+
+
+# ---- K2/K3 tables ---------------------------------------------------------------
+@pytest.mark.parametrize("grid", [(15, 9), (30, 17), (7, 5), (1, 1), (60, 34)])
+def test_rect_tables_bit_exact(part, oracle, grid):
+    from paper_2012_14792_b200 import CtuGrid
+    cols, rows = grid
+    g = CtuGrid.make(cols * 128 - 50, rows * 128 - 3, 128)
+    F = 3
+    est = RNG.lognormal(0, 0.8, size=(F, cols * rows))
+    est[1] = np.round(est[1] * 4) / 4
+    luma = RNG.integers(0, 1024, size=(F, g.frame_height, g.frame_width)).astype(np.uint16)
+    rec = part.ctu_stats_batch(luma, 128)
+    rt, rs, sat = part.grid_tables(g, est, rec)
+    for f in range(F):
+        exp_t = oracle.rect_times(est[f], cols, rows)
+        assert np.array_equal(_bits(rt[f]), _bits(exp_t))
+        r3 = np.stack([rec[f]["count"], rec[f]["sum"], rec[f]["sumsq"]], axis=1)
+        exp_s = oracle.rect_sse(g.frame_width, g.frame_height, 128, r3)
+        assert np.array_equal(_bits(rs[f]), _bits(exp_s))
+
+
+# ---- K4/K5 search -----------------------------------------------------------------
+def _rec3(rec):
+    return np.stack([rec["count"], rec["sum"], rec["sumsq"]], axis=1)
+
+
+def test_search_small_golden(part):
+    """200 reference-generated instances: step 1 and step 2, bit-exact."""
+    from paper_2012_14792_b200 import RECORD_DTYPE, CtuGrid, SearchConfig, SlicecraftError
+    cases = json.load(open(os.path.join(GOLDEN, "search_small.json")))
+    for i, c in enumerate(cases):
+        g = CtuGrid.make(c["w"], c["h"], c["ctu"])
+        cfg = SearchConfig(n_slices=c["n"], lambda_=c["lambda"], k_area=c["k"],
+                           max_tile_cols=c["max_tile_cols"])
+        rec = np.zeros(g.cell_count(), RECORD_DTYPE)
+        r3 = np.array(c["records"], dtype=np.uint64)
+        rec["count"], rec["sum"], rec["sumsq"] = r3[:, 0], r3[:, 1], r3[:, 2]
+        est = np.array(c["est"])
+        if c["status1"] != 0:
+            with pytest.raises(SlicecraftError) as e:
+                part.two_step_batch(g, est, rec, cfg)
+            assert e.value.status == c["status1"], i
+            continue
+        o = part.two_step_batch(g, est, rec, cfg)[0]
+        assert o.t_min_us == c["t_min"], i
+        assert o.argmin.rects() == [tuple(x) for x in c["argmin"]], i
+        assert o.candidates_step1 == c["candidates"], i
+        assert o.t_best_us == c["t_best"], i
+        assert o.sse_best == c["sse_best"], i
+        assert o.best.rects() == [tuple(x) for x in c["best"]], i
+        assert o.candidates_step2 == c["candidates_step2"], i
+
+
+@pytest.mark.parametrize("coverage", [0, 1])
+@pytest.mark.parametrize("seed", range(6))
+def test_search_random_vs_oracle(part, oracle, coverage, seed):
+    from paper_2012_14792_b200 import CtuGrid, SearchConfig, SlicecraftError
+    rng = np.random.default_rng(seed + 100 * coverage)
+    for trial in range(12):
+        cols, rows = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        g = CtuGrid.make(cols * 64, rows * 64 - int(rng.integers(0, 60)), 64)
+        n = int(rng.integers(1, min(9, g.cell_count()) + 1))
+        mc = int(rng.integers(0, 5))
+        lam = float(rng.choice([0.0, 0.1, 0.3, 1.0]))
+        k = float(rng.choice([3.0, 2.5, 2.0]))
+        F = int(rng.integers(1, 5))
+        est = rng.lognormal(0, 0.6, size=(F, g.cell_count()))
+        if trial % 3 == 0:
+            est = np.round(est)
+        luma = rng.integers(0, 1024, size=(F, g.frame_height, g.frame_width)).astype(np.uint16)
+        rec = part.ctu_stats_batch(luma, 64)
+        cfg = SearchConfig(n_slices=n, lambda_=lam, k_area=k, max_tile_cols=mc, coverage=coverage)
+        exp = [oracle.search(g.frame_width, g.frame_height, 64, est[f], _rec3(rec[f]), n, lam, k,
+                             mc, coverage, 3) for f in range(F)]
+        if any(st != 0 for st, _ in exp):
+            with pytest.raises(SlicecraftError):
+                part.two_step_batch(g, est, rec, cfg)
+            continue
+        got = part.two_step_batch(g, est, rec, cfg)
+        for f in range(F):
+            _, e = exp[f]
+            o = got[f]
+            ctx = (seed, trial, f, cols, rows, n, mc, lam, k)
+            assert o.t_min_us == e.t_min_us, ctx
+            assert o.argmin.rects() == e.argmin1.slices(rows), ctx
+            assert o.candidates_step1 == e.candidates_step1, ctx
+            assert o.t_best_us == e.t_best_us, ctx
+            assert o.sse_best == e.sse_best, ctx
+            assert o.best.rects() == e.best.slices(rows), ctx
+            assert o.candidates_step2 == e.candidates_step2, ctx
+
+
+def test_constrained_with_given_tmin(part, oracle):
+    from paper_2012_14792_b200 import CtuGrid, SearchConfig
+    g = CtuGrid.make(8 * 64, 6 * 64, 64)
+    est = RNG.lognormal(0, 0.7, size=(2, g.cell_count()))
+    luma = RNG.integers(0, 1024, size=(2, g.frame_height, g.frame_width)).astype(np.uint16)
+    rec = part.ctu_stats_batch(luma, 64)
+    cfg = SearchConfig(n_slices=5, lambda_=0.3)
+    tm = [float(est[0].sum() / 3), float(est[1].max() * 2)]
+    got = part.constrained_clustering_batch(g, est, rec, tm, cfg)
+    for f in range(2):
+        st, e = oracle.search(g.frame_width, g.frame_height, 64, est[f], _rec3(rec[f]), 5, 0.3, 3.0,
+                              0, 0, 2, tm[f])
+        assert st == 0
+        assert got[f].t_best_us == e.t_best_us and got[f].sse_best == e.sse_best
+        assert got[f].best.rects() == e.best.slices(g.rows)
+        assert got[f].candidates_step2 == e.candidates_step2
+
+
+def test_min_time_search_api(part, oracle):
+    from paper_2012_14792_b200 import CostMap, CtuGrid, SearchConfig
+    g = CtuGrid.make(1920, 1080)
+    est = RNG.lognormal(0, 0.5, g.cell_count())
+    t, p = part.min_time_search(CostMap(g, est), SearchConfig(n_slices=4, max_tile_cols=2))
+    st, e = oracle.search(1920, 1080, 128, est, None, 4, 0.0, 3.0, 2, 0, 1)
+    assert t == e.t_min_us and p.rects() == e.argmin1.slices(g.rows)
+
+
+# ---- BASELINE configs on their synthetic inputs ------------------------------------
+def _config_inputs(ci, frames):
+    from paper_2012_14792_b200 import workloads as wl
+    w = wl.WORKLOADS[ci]
+    return w, wl.cost_trace(w, frames=frames), wl.synth_luma(w, frames=frames)
+
+
+@pytest.mark.parametrize("ci", [1, 2, 3])
+def test_baseline_configs_vs_reference_golden(part, ci):
+    """cfg1 (all), cfg2 (POC 1..4), cfg3 (POC 1) against the reference itself."""
+    import hashlib
+    from paper_2012_14792_b200 import workloads as wl
+    gold = json.load(open(os.path.join(GOLDEN, "configs.json")))[str(ci)]
+    F = max(fr["poc"] for fr in gold["frames"])
+    w, tr, luma = _config_inputs(ci, F)
+    g = w.grid()
+    rec = np.zeros((F, g.cell_count()), dtype=__import__(
+        "paper_2012_14792_b200").RECORD_DTYPE)
+    res = part.partition_frames(g, luma, tr.est, w.cfg(), records_out=rec)
+    for fr in gold["frames"]:
+        p = fr["poc"]
+        r3 = np.ascontiguousarray(_rec3(rec[p - 1]), dtype=np.uint64)
+        assert hashlib.sha256(r3.tobytes()).hexdigest()[:16] == fr["records_hash"]
+        assert hashlib.sha256(np.ascontiguousarray(tr.est[p - 1]).tobytes()).hexdigest()[:16] == \
+            fr["est_hash"]
+        r = res[p - 1]
+        from paper_2012_14792_b200.partitioner import Partition
+        assert r.t_min_us == fr["t_min"]
+        assert r.t_best_us == fr["t_best"]
+        assert r.sse_best == fr["sse_best"]
+        assert Partition.from_layout(g, r.best).rects() == [tuple(x) for x in fr["best"]]
+        assert r.candidates_step1 == fr["candidates_step1"]
+        assert r.candidates_step2 == fr["candidates_step2"]
+        assert tr.est_source[p - 1] == fr["est_source"]
+        assert tr.est_source_poc[p - 1] == fr["est_source_poc"]
+    assert wl  # noqa
+
+
+def test_cfg2_all_frames_vs_oracle(part, oracle):
+    """All 64 frames of config 2 (two GPU frame groups) against the C oracle."""
+    w, tr, luma = _config_inputs(2, 64)
+    g = w.grid()
+    from paper_2012_14792_b200 import RECORD_DTYPE
+    rec = np.zeros((64, g.cell_count()), dtype=RECORD_DTYPE)
+    res = part.partition_frames(g, luma, tr.est, w.cfg(), records_out=rec)
+    from paper_2012_14792_b200.partitioner import Partition
+    for f in range(0, 64, 3):
+        st, e = oracle.search(w.width, w.height, 128, tr.est[f], _rec3(rec[f]), 8, 0.0, 3.0, 4, 0, 3)
+        assert st == 0
+        r = res[f]
+        assert r.t_min_us == e.t_min_us and r.t_best_us == e.t_best_us and r.sse_best == e.sse_best
+        assert Partition.from_layout(g, r.best).rects() == e.best.slices(g.rows)
+        assert r.candidates_step1 == e.candidates_step1 == 171788
+
+
+def test_cfg3_counts_all_frames(part):
+    """Size-independent checks on the full cfg3 batch: counts, budget, feasibility."""
+    w, tr, luma = _config_inputs(3, 32)
+    g = w.grid()
+    res = part.partition_frames(g, luma, tr.est, w.cfg())
+    for r in res:
+        assert r.candidates_step1 == r.candidates_step2 == 66007331
+        assert r.t_best_us <= r.t_min_us * (1.0 + 0.0)  # lambda = 0: t_best == t_min
+        assert r.t_best_us == r.t_min_us
+
+
+# ---- error behaviour -----------------------------------------------------------------
+def test_errors(part):
+    from paper_2012_14792_b200 import CtuGrid, SearchConfig, SlicecraftError
+    g = CtuGrid.make(256, 128, 128)  # 2x1 cells
+    est = np.ones((1, 2))
+    with pytest.raises(SlicecraftError) as e:
+        part.min_time_search_batch(g, est, SearchConfig(n_slices=3))
+    assert e.value.kind == "GeometryError"
+    with pytest.raises(SlicecraftError) as e:
+        part.min_time_search_batch(g, est, SearchConfig(n_slices=1, k_area=1.0))
+    assert e.value.kind == "ConfigError"
+    with pytest.raises(SlicecraftError) as e:
+        part.min_time_search_batch(g, est, SearchConfig(n_slices=1, lambda_=float("nan")))
+    assert e.value.kind == "ConfigError"
+    # k so tight that no candidate is admissible -> NoCandidateError
+    g4 = CtuGrid.make(4 * 128, 128, 128)
+    with pytest.raises(SlicecraftError) as e:
+        part.min_time_search_batch(g4, np.ones((1, 4)), SearchConfig(n_slices=3, k_area=1.0001,
+                                                                    max_tile_cols=1))
+    assert e.value.kind == "NoCandidateError"
+    from paper_2012_14792_b200 import RECORD_DTYPE
+    bad = np.zeros((1, 2), RECORD_DTYPE)
+    with pytest.raises(SlicecraftError) as e:
+        part.two_step_batch(g, est, bad, SearchConfig(n_slices=1))
+    assert e.value.kind == "FormatError"
