@@ -174,16 +174,37 @@ Plan* get_plan(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc
     for (int c = 1; c <= maxc; ++c) gen_prefixes(g.cols, c, std::min(c, D), covering, p->items);
     if (p->items.size() >= target || D >= maxc || p->items.size() > (1u << 22)) break;
   }
-  // area table: bmax[a] = largest B in [0, max_area] with k*(double)a > (double)B
-  // (the admissibility test of search.cpp:182-183), -1 if none.
+  // Area tables (the admissibility test k*(double)amin > (double)amax of
+  // search.cpp:182-183, tabulated so the kernels compare integers only):
+  //   bmax[a]      largest B in [0, max_area] with k*(double)a > (double)B (-1: none)
+  //   aneed[B]     smallest a >= 1 with bmax[a] >= B (max_area+1: none)
+  //   mstar[w][rl] smallest m in [1, rl/2] with w*(rl-m) <= bmax[w*m]
+  //                (rl/2+1: none) -- the two-run split admissibility bound
   const int max_area = g.cols * g.rows;
-  p->bmax.assign((size_t)max_area + 1, -1);
+  const int A = max_area + 1;
+  p->bmax.assign((size_t)2 * A + (size_t)(g.cols + 1) * (g.rows + 1), 0);
+  int32_t* bm = p->bmax.data();
+  int32_t* an = bm + A;
+  int32_t* ms = an + A;
   int b = -1;
+  p->pathological = false;
   for (int a = 0; a <= max_area; ++a) {
     // k*a is non-decreasing in a, so b only moves up
     while (b + 1 <= max_area && cfg.k_area * (double)a > (double)(b + 1)) ++b;
-    p->bmax[a] = b;
+    bm[a] = b;
+    if (a >= 1 && b < a) p->pathological = true;  // a single slice of area a is inadmissible
   }
+  int a_cur = 1;
+  for (int B = 0; B <= max_area; ++B) {
+    while (a_cur <= max_area && bm[a_cur] < B) ++a_cur;
+    an[B] = a_cur;
+  }
+  for (int w = 1; w <= g.cols; ++w)
+    for (int rl = 0; rl <= g.rows; ++rl) {
+      int m = 1;
+      while (m <= rl / 2 && !((int64_t)w * (rl - m) <= bm[w * m])) ++m;
+      ms[w * (g.rows + 1) + rl] = (rl >= 2) ? m : rl / 2 + 1;
+    }
   ctx->plans.push_back(p);
   return p;
 }
@@ -320,6 +341,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     a.counter = reinterpret_cast<uint32_t*>(ctr);
     a.count_out = reinterpret_cast<unsigned long long*>(ctr + 1);
     a.bmax = plan->d_bmax.as<int32_t>();
+    a.pathological = plan->pathological ? 1 : 0;
     a.rt = ctx->rt_search.as<uint64_t>() + (size_t)gi * L.nr * L.fpw;
     a.rs = step == 2 ? ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw : nullptr;
     a.budget = ctx->budget.as<uint64_t>() + (size_t)gi * L.fpw;

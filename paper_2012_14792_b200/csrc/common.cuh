@@ -110,7 +110,8 @@ struct PlanKey {
 struct Plan {
   PlanKey key{};
   std::vector<WorkItem> items;
-  std::vector<int32_t> bmax;  // bmax[a]: largest B with k*a > B, -1 if none
+  std::vector<int32_t> bmax;  // bmax | aneed | mstar tables (api.cu get_plan)
+  bool pathological = false;  // some single area fails the test (k ~ 1)
   DevBuf d_items, d_bmax;
   bool uploaded = false;
 };
@@ -127,13 +128,13 @@ constexpr int kSnapBytes = 96;  // W[16] R[16] H[64], bytes
 
 // Arguments of the search kernels (search.cu), filled by api.cu.
 struct SearchArgs {
-  int cols, rows, n, nyh, max_area, coverage;
+  int cols, rows, n, nyh, max_area, coverage, pathological;
   const WorkItem* items;
   uint32_t n_items;       // items of this shard
   uint32_t item_offset;   // global index = offset + k * stride
   uint32_t item_stride;
   uint32_t* counter;
-  const int32_t* bmax;    // [max_area + 1]
+  const int32_t* bmax;    // bmax[A] | aneed[A] | mstar[(cols+1)*(rows+1)], A = max_area+1
   const uint64_t* rt;     // [NR][FPW] clamped time bits, this frame group
   const double* rs;       // [NR][FPW] SSE (step 2)
   const uint64_t* budget; // [FPW] budget bits (step 2)
