@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libslicecraft_b200.so")
+LIB_PATH = os.environ.get("SLICECRAFT_B200_LIB", os.path.join(HERE, "libslicecraft_b200.so"))
 
 SC_MAX_SLICES = 64
 SC_MAX_COLS = 16

@@ -136,29 +136,7 @@ int next_pow2(int v) {
   return p;
 }
 
-// ---- planner ------------------------------------------------------------------
-void gen_prefixes(int cols, int c, int d, bool covering, std::vector<WorkItem>& out) {
-  int w[16];
-  // iterative lex enumeration of (w_0..w_{d-1})
-  std::function<void(int, int)> rec = [&](int i, int cols_left) {
-    if (i == d) {
-      if (covering && d == c && cols_left != 0) return;
-      WorkItem it{};
-      it.c = (uint8_t)c;
-      it.d = (uint8_t)d;
-      for (int j = 0; j < d; ++j) it.w[j] = (uint8_t)w[j];
-      out.push_back(it);
-      return;
-    }
-    const int maxw = cols_left - (c - i - 1);
-    for (int x = 1; x <= maxw; ++x) {
-      w[i] = x;
-      rec(i + 1, cols_left - x);
-    }
-  };
-  rec(0, cols);
-}
-
+// ---- planner (plan.h) ------------------------------------------------------
 Plan* get_plan(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc) {
   PlanKey key{g.cols, g.rows, cfg.n_slices, maxc, cfg.coverage, cfg.k_area};
   for (Plan* p : ctx->plans)
@@ -166,45 +144,8 @@ Plan* get_plan(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc
   Plan* p = new Plan();
   p->key = key;
   const bool covering = cfg.coverage == SC_COVERAGE_COVERING;
-  // work items: width prefixes of depth D (per c: min(c, D)), D grown until
-  // there are enough items to keep every warp busy.
-  const size_t target = (size_t)ctx->sm_count * 16 * 32;
-  for (int D = 1; D <= 12; ++D) {
-    p->items.clear();
-    for (int c = 1; c <= maxc; ++c) gen_prefixes(g.cols, c, std::min(c, D), covering, p->items);
-    if (p->items.size() >= target || D >= maxc || p->items.size() > (1u << 22)) break;
-  }
-  // Area tables (the admissibility test k*(double)amin > (double)amax of
-  // search.cpp:182-183, tabulated so the kernels compare integers only):
-  //   bmax[a]      largest B in [0, max_area] with k*(double)a > (double)B (-1: none)
-  //   aneed[B]     smallest a >= 1 with bmax[a] >= B (max_area+1: none)
-  //   mstar[w][rl] smallest m in [1, rl/2] with w*(rl-m) <= bmax[w*m]
-  //                (rl/2+1: none) -- the two-run split admissibility bound
-  const int max_area = g.cols * g.rows;
-  const int A = max_area + 1;
-  p->bmax.assign((size_t)2 * A + (size_t)(g.cols + 1) * (g.rows + 1), 0);
-  int32_t* bm = p->bmax.data();
-  int32_t* an = bm + A;
-  int32_t* ms = an + A;
-  int b = -1;
-  p->pathological = false;
-  for (int a = 0; a <= max_area; ++a) {
-    // k*a is non-decreasing in a, so b only moves up
-    while (b + 1 <= max_area && cfg.k_area * (double)a > (double)(b + 1)) ++b;
-    bm[a] = b;
-    if (a >= 1 && b < a) p->pathological = true;  // a single slice of area a is inadmissible
-  }
-  int a_cur = 1;
-  for (int B = 0; B <= max_area; ++B) {
-    while (a_cur <= max_area && bm[a_cur] < B) ++a_cur;
-    an[B] = a_cur;
-  }
-  for (int w = 1; w <= g.cols; ++w)
-    for (int rl = 0; rl <= g.rows; ++rl) {
-      int m = 1;
-      while (m <= rl / 2 && !((int64_t)w * (rl - m) <= bm[w * m])) ++m;
-      ms[w * (g.rows + 1) + rl] = (rl >= 2) ? m : rl / 2 + 1;
-    }
+  p->items = make_items(g.cols, maxc, covering, (size_t)ctx->sm_count * 16 * 32);
+  p->pathological = make_area_tables(g.cols, g.rows, cfg.k_area, p->bmax);
   ctx->plans.push_back(p);
   return p;
 }

@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "plan.h"
 #include "slicecraft_b200.h"
 
 namespace scb {
@@ -89,14 +90,6 @@ struct HostBuf {
 };
 
 // ---- search plan (frame-independent; cached per grid+config) ----------------
-// A work item is a lex-ordered prefix (c, w_0..w_{d-1}) of the ColumnSplit
-// enumeration (search.cpp:120-143); the items, in index order, tile the
-// reference's enumeration order exactly.
-struct WorkItem {
-  uint8_t c, d, pad0, pad1;
-  uint8_t w[12];
-};
-static_assert(sizeof(WorkItem) == 16, "WorkItem is one uint4");
 
 struct PlanKey {
   int cols, rows, n, maxc, coverage;

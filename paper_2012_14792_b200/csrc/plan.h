@@ -1,0 +1,106 @@
+// Frame-independent search plan (host C++, no CUDA): the work items that tile
+// the reference's enumeration order and the integer area tables.  Shared by
+// api.cu and the test-only host emulator (tests/emu).
+#pragma once
+
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+namespace scb {
+
+// A work item is a lex-ordered prefix (c, w_0..w_{d-1}) of the ColumnSplit
+// enumeration (search.cpp:120-143); the items, in index order, tile the
+// reference's enumeration order exactly.
+struct WorkItem {
+  uint8_t c, d, pad0, pad1;
+  uint8_t w[12];
+};
+static_assert(sizeof(WorkItem) == 16, "WorkItem is one uint4");
+
+// All width prefixes of depth d for c columns, in lex order (rec_widths,
+// search.cpp:133-143: w_i in [1, cols_left - (c - i - 1)]).
+inline void gen_prefixes(int cols, int c, int d, bool covering, std::vector<WorkItem>& out) {
+  int w[16] = {0};
+  int cl[17];
+  int i = 0;
+  cl[0] = cols;
+  w[0] = 0;
+  if (d == 0) {
+    WorkItem it{};
+    it.c = (uint8_t)c;
+    out.push_back(it);
+    return;
+  }
+  while (i >= 0) {
+    const int maxw = cl[i] - (c - i - 1);
+    if (++w[i] > maxw) {
+      --i;
+      continue;
+    }
+    if (i == d - 1) {
+      if (covering && d == c && cl[i] - w[i] != 0) continue;
+      WorkItem it{};
+      it.c = (uint8_t)c;
+      it.d = (uint8_t)d;
+      for (int j = 0; j < d; ++j) it.w[j] = (uint8_t)w[j];
+      out.push_back(it);
+      continue;
+    }
+    cl[i + 1] = cl[i] - w[i];
+    ++i;
+    w[i] = 0;
+  }
+}
+
+// Work items: width prefixes of depth min(c, D), D grown until there are at
+// least `target` items (or every width is fixed).
+inline std::vector<WorkItem> make_items(int cols, int maxc, bool covering, size_t target) {
+  std::vector<WorkItem> items;
+  for (int D = 1; D <= 12; ++D) {
+    items.clear();
+    for (int c = 1; c <= maxc; ++c) gen_prefixes(cols, c, std::min(c, D), covering, items);
+    if (items.size() >= target || D >= maxc || items.size() > (1u << 22)) break;
+  }
+  return items;
+}
+
+// Area tables (the admissibility test k*(double)amin > (double)amax of
+// search.cpp:182-183, tabulated so the kernels compare integers only), laid
+// out bmax[A] | aneed[A] | mstar[(cols+1)*(rows+1)], A = cols*rows + 1:
+//   bmax[a]      largest B in [0, max_area] with k*(double)a > (double)B (-1: none)
+//   aneed[B]     smallest a >= 1 with bmax[a] >= B (max_area+1: none)
+//   mstar[w][rl] smallest m in [1, rl/2] with w*(rl-m) <= bmax[w*m]
+//                (rl/2+1: none) -- the two-run split admissibility bound
+// Returns true when some single area a fails the test (k barely above 1).
+inline bool make_area_tables(int cols, int rows, double k, std::vector<int32_t>& t) {
+  const int max_area = cols * rows;
+  const int A = max_area + 1;
+  t.assign((size_t)2 * A + (size_t)(cols + 1) * (rows + 1), 0);
+  int32_t* bm = t.data();
+  int32_t* an = bm + A;
+  int32_t* ms = an + A;
+  int b = -1;
+  bool pathological = false;
+  for (int a = 0; a <= max_area; ++a) {
+    // k*a is non-decreasing in a, so b only moves up
+    while (b + 1 <= max_area && k * (double)a > (double)(b + 1)) ++b;
+    bm[a] = b;
+    if (a >= 1 && b < a) pathological = true;
+  }
+  int a_cur = 1;
+  for (int B = 0; B <= max_area; ++B) {
+    while (a_cur <= max_area && bm[a_cur] < B) ++a_cur;
+    an[B] = a_cur;
+  }
+  for (int w = 1; w <= cols; ++w)
+    for (int rl = 0; rl <= rows; ++rl) {
+      int m = 1;
+      while (m <= rl / 2 && !((int64_t)w * (rl - m) <= bm[w * m])) ++m;
+      ms[w * (rows + 1) + rl] = (rl >= 2) ? m : rl / 2 + 1;
+    }
+  return pathological;
+}
+
+}  // namespace scb

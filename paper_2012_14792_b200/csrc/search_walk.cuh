@@ -1,0 +1,444 @@
+// The warp-uniform walk of one work item — the body of the K4/K5 search
+// kernels (search.cu).  Written as a __host__ __device__ function so that
+// the test-only host emulator (tests/emu) executes the very same code lane
+// by lane on the CPU; the product path only ever runs it on the GPU.
+//
+// Replaces ColumnSplitGenerator + layout_time/layout_sse + the step-1/step-2
+// reductions (search.cpp:77-91, 110-196, 280-289, 375-394).
+#pragma once
+
+#include <stdint.h>
+#include <stdio.h>
+
+#include "plan.h"
+#include "slicecraft_b200.h"
+
+#ifdef __CUDACC__
+#define SCB_HD __host__ __device__ __forceinline__
+#else
+#define SCB_HD inline
+#endif
+
+namespace scb {
+
+// ---- portable intrinsics -------------------------------------------------------
+SCB_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+SCB_HD double dadd_rn(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  volatile double r = a + b;  // no contraction possible: a plain add
+  return r;
+#endif
+}
+SCB_HD int imin(int a, int b) { return a < b ? a : b; }
+SCB_HD int imax(int a, int b) { return a > b ? a : b; }
+SCB_HD uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+SCB_HD int xw_of(int cols, int x0, int w) { return x0 * cols - (x0 * (x0 - 1)) / 2 + (w - 1); }
+SCB_HD int yh_of(int rows, int y0, int h) { return y0 * rows - (y0 * (y0 - 1)) / 2 + (h - 1); }
+
+constexpr int kMaxLevels = SC_MAX_SLICES;
+constexpr int kBigArea = 1 << 20;  // "no slice yet" sentinel for amin
+constexpr int kSnap = 96;          // snapshot bytes: W[16] R[16] H[64]
+
+// Read-only walk environment (tables live in shared memory on the GPU).
+struct WalkEnv {
+  int cols, rows, n, nyh, max_area, coverage, patho, rstride;
+  const int32_t* bmax;    // [max_area + 1]
+  const int32_t* aneed;   // [max_area + 1]
+  const int32_t* mstar;   // [(cols+1) * (rows+1)]
+  const int32_t* ilo;     // [(cols+1) * rstride]: lower end of window I(w, r)
+  const uint64_t* magic;  // [cols+1]: division by w (div_magic)
+  const uint64_t* rt;     // [NR][FPW] clamped f64 time bits of every rectangle
+  const double* rs;       // [NR][FPW] SSE of every rectangle (step 2)
+};
+
+// One lane's running first-in-order best and its candidate snapshot.
+struct LaneState {
+  uint64_t best_t, best_item, best_ord;
+  double best_sse;
+  uint64_t budget;  // step 2: t_min * (1 + lambda) as f64 bits
+  uint64_t count;   // candidates enumerated (uniform over the warp)
+  uint8_t* snap;
+};
+
+// Area thresholds of a partial candidate: a further slice of area x keeps it
+// admissible iff T2 <= x <= T1 (and x <= bmax[x]); T1 = bmax[amin] (+inf
+// before the first slice), T2 = aneed[amax].
+struct Thr {
+  int t1, t2;
+};
+
+// floor(x / w) for 0 <= x <= 2^20, 1 <= w <= 2^11 with the 33-bit magic
+// floor(2^32/w)+1: one wide multiply, exact because x * w < 2^32.
+SCB_HD int div_w(int x, uint64_t magic) { return (int)(((uint64_t)(uint32_t)x * magic) >> 32); }
+SCB_HD uint64_t div_magic(int w) { return 0x100000000ull / (uint64_t)w + 1ull; }
+
+// Admissible heights of a run of width w with rl rows left in its column and
+// runs_left runs (this one included).  runs_left == 2: the next run is forced
+// to rl - h, both areas must pass -> symmetric [m, rl - m] with
+// m = max(ceil(T2/w), rl - floor(T1/w), mstar[w][rl]).  Otherwise the
+// interval includes a look-ahead: rl - h rows must still split into
+// runs_left - 1 runs of admissible height (thresholds only tighten).
+SCB_HD void height_interval(const WalkEnv& e, Thr t, int w, int rl, int runs_left, int& lo,
+                            int& hi) {
+  const uint64_t mg = e.magic[w];
+  const int hmin_a = imax(1, div_w(t.t2 + w - 1, mg));
+  const int hmax_a = t.t1 < 0 ? 0 : div_w(t.t1, mg);
+  if (runs_left == 2) {
+    int m = imax(hmin_a, rl - hmax_a);
+    m = imax(m, e.mstar[w * (e.rows + 1) + rl]);
+    lo = m;
+    hi = rl - m;
+    return;
+  }
+  const int k = runs_left - 1;
+  lo = imax(hmin_a, rl - k * hmax_a);
+  hi = imin(rl - k * hmin_a, hmax_a);
+}
+
+// Walk work item `item` (prefix wi) for frame slot f and leaf slot `slot`
+// (J = 32 / FPW lanes share a frame and split the innermost height loop).
+template <int FPW, int STEP>
+SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f, int slot,
+                      LaneState& st) {
+  constexpr int J = 32 / FPW;
+  const int rows = e.rows, cols = e.cols, nyh = e.nyh;
+  const uint64_t* rt = e.rt;
+  const double* rs = e.rs;
+  const int c = wi.c, d = wi.d;
+  uint64_t ord = 0;  // ordinal of the next candidate inside this item
+
+  // warp-uniform DFS state (identical in every lane of the warp)
+  int W[SC_MAX_COLS], R[SC_MAX_COLS], X0[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
+  uint8_t curH[SC_MAX_SLICES];
+  uint8_t Lcol[kMaxLevels], Lrun[kMaxLevels], Ly0[kMaxLevels], Lh[kMaxLevels], Lhi[kMaxLevels];
+  int32_t Amin[kMaxLevels], Amax[kMaxLevels];
+  uint64_t Pin[kMaxLevels];
+
+  auto thresholds = [&](int amin, int amax, int win_lo, int win_hi) -> Thr {
+    Thr t;
+    t.t1 = amin >= kBigArea ? kBigArea : e.bmax[amin];
+    t.t2 = e.aneed[amax];
+    t.t2 = imax(t.t2, win_lo);
+    t.t1 = imin(t.t1, win_hi);
+    return t;
+  };
+  auto rt_at = [&](int x0, int w, int y0, int h) -> uint64_t {
+    return rt[(size_t)(xw_of(cols, x0, w) * nyh + yh_of(rows, y0, h)) * FPW + f];
+  };
+  // Every multi-run column from `from` on can still be filled with runs of
+  // admissible height (necessary condition; prunes dead subtrees early).
+  auto columns_feasible = [&](int from, Thr t) -> bool {
+    for (int i = from; i < c; ++i) {
+      if (R[i] < 2) continue;
+      const int w = W[i];
+      const uint64_t mg = e.magic[w];
+      const int hmin_a = imax(1, div_w(t.t2 + w - 1, mg));
+      const int hmax_a = t.t1 < 0 ? 0 : div_w(t.t1, mg);
+      if (R[i] * hmin_a > rows || R[i] * hmax_a < rows) return false;
+    }
+    return true;
+  };
+  // snapshot of the current candidate; run `lr` takes height lh and the
+  // forced run lr+1 the rest of its column (lr < 0: no leaf loop).
+  auto take_snapshot = [&](int lr, int lh, int lrest) {
+    for (int i = 0; i < SC_MAX_COLS; ++i) {
+      st.snap[i] = (uint8_t)(i < c ? W[i] : 0);
+      st.snap[SC_MAX_COLS + i] = (uint8_t)(i < c ? R[i] : 0);
+    }
+    for (int i = 0; i < e.n; ++i) {
+      uint8_t v = curH[i];
+      if (i == lr) v = (uint8_t)lh;
+      if (i == lr + 1 && lr >= 0) v = (uint8_t)lrest;
+      st.snap[2 * SC_MAX_COLS + i] = v;
+    }
+  };
+  // step-2 objective: slice SSEs summed in slice order (search.cpp:85-91)
+  auto layout_sse = [&](int lr, int lh, int lrest) -> double {
+    double tot = 0.0;
+    int run = 0;
+    for (int i = 0; i < c; ++i) {
+      int y = 0;
+      const int base = xw_of(cols, X0[i], W[i]) * nyh;
+      for (int j = 0; j < R[i]; ++j, ++run) {
+        int hh = curH[run];
+        if (run == lr) hh = lh;
+        else if (lr >= 0 && run == lr + 1) hh = lrest;
+        tot = dadd_rn(tot, rs[(size_t)(base + yh_of(rows, y, hh)) * FPW + f]);
+        y += hh;
+      }
+    }
+    return tot;
+  };
+  // score one candidate (strict comparisons keep the first in order)
+  auto score = [&](uint64_t t, uint64_t o, int lr, int lh, int lrest) {
+    if (STEP == 1) {
+      if (t < st.best_t) {
+        st.best_t = t;
+        st.best_item = item;
+        st.best_ord = o;
+        take_snapshot(lr, lh, lrest);
+      }
+    } else if (t <= st.budget) {
+      const double s = layout_sse(lr, lh, lrest);
+      if (s < st.best_sse || (s == st.best_sse && t < st.best_t)) {
+        st.best_sse = s;
+        st.best_t = t;
+        st.best_item = item;
+        st.best_ord = o;
+        take_snapshot(lr, lh, lrest);
+      }
+    }
+  };
+
+  // ---- widths DFS over positions d..c-1 (lex, search.cpp:133-143).  A width
+  //      w can only host windows a in the hull [ilo(w, r_max), w*rows] of its
+  //      column windows (r <= n-c+1): prefixes whose hulls do not intersect
+  //      cannot complete and are skipped.
+  const int rmax_c = imin(e.n - c + 1, rows);
+  int WL[SC_MAX_COLS + 1], WH[SC_MAX_COLS + 1];
+  X0[0] = 0;
+  WL[0] = 1;
+  WH[0] = e.max_area;
+  bool ok = (e.n >= c) && (e.n <= c * rows);
+  for (int i = 0; i < d && ok; ++i) {
+    W[i] = wi.w[i];
+    X0[i + 1] = X0[i] + W[i];
+    WL[i + 1] = imax(WL[i], e.ilo[W[i] * e.rstride + rmax_c]);
+    WH[i + 1] = imin(WH[i], W[i] * rows);
+    ok = WL[i + 1] <= WH[i + 1];
+  }
+  int pos = d;
+  const bool fixed_widths = d == c;
+  if (ok && !fixed_widths) W[pos] = 0;
+  while (ok) {
+    if (!fixed_widths) {
+      bool got = false;
+      while (true) {
+        const int maxw = cols - X0[pos] - (c - pos - 1);
+        int wv;
+        if (e.coverage && pos == c - 1) wv = (W[pos] == 0) ? maxw : maxw + 1;
+        else wv = W[pos] + 1;
+        if (wv > maxw) {
+          if (pos == d) break;
+          --pos;
+          continue;
+        }
+        W[pos] = wv;
+        const int nL = imax(WL[pos], e.ilo[wv * e.rstride + rmax_c]);
+        const int nH = imin(WH[pos], wv * rows);
+        if (nL > nH) continue;
+        X0[pos + 1] = X0[pos] + wv;
+        WL[pos + 1] = nL;
+        WH[pos + 1] = nH;
+        if (pos == c - 1) {
+          got = true;
+          break;
+        }
+        ++pos;
+        W[pos] = 0;
+      }
+      if (!got) break;
+    }
+    // ---- runs DFS (lex, search.cpp:145-161).  The skeleton (widths, runs)
+    //      has an admissible completion iff the column windows
+    //      I(w, r) = [aneed[w*ceil(rows/r)], w*floor(rows/r)] intersect; I
+    //      slides down as r grows, so the feasible r of a position form one
+    //      contiguous range.
+    int RL[SC_MAX_COLS], RH[SC_MAX_COLS], SL[SC_MAX_COLS];
+    int rp = 0;
+    RL[0] = 1;
+    RH[0] = e.max_area;
+    SL[0] = e.n;
+    R[0] = imax(1, e.n - (c - 1) * rows) - 1;
+    while (true) {
+      const int after = c - 1 - rp;
+      const int rhi = imin(rows, SL[rp] - after);
+      const int w = W[rp];
+      int r = R[rp] + 1, lo = 0, hi = 0;
+      bool found = false;
+      for (; r <= rhi; ++r) {
+        lo = e.ilo[w * e.rstride + r];
+        hi = w * (rows / r);
+        if (hi < RL[rp]) break;  // every larger r is lower still
+        if (lo <= RH[rp]) {
+          found = true;
+          break;
+        }
+      }
+      if (!found) {
+        if (rp == 0) break;
+        --rp;
+        continue;
+      }
+      R[rp] = r;
+      const int nL = imax(RL[rp], lo), nH = imin(RH[rp], hi);
+      if (nL > nH) continue;
+      if (rp < c - 1) {
+        SL[rp + 1] = SL[rp] - r;
+        RL[rp + 1] = nL;
+        RH[rp + 1] = nH;
+        ++rp;
+        R[rp] = imax(1, SL[rp] - (c - 1 - rp) * rows) - 1;
+        continue;
+      }
+      // ---- one live skeleton (c, widths, runs); every area lies in
+      //      [win_lo, bmax[nH]] for a window a in [nL, nH]
+      const int win_lo = nL, win_hi = e.bmax[nH];
+      int amin = kBigArea, amax = 0;
+      int run = 0, nl = 0;
+      for (int i = 0; i < c; ++i) {
+        RS0[i] = run;
+        if (R[i] == 1) {  // one-run columns are fixed by the skeleton
+          const int ar = W[i] * rows;
+          amin = imin(amin, ar);
+          amax = imax(amax, ar);
+          curH[run] = (uint8_t)rows;
+        } else {
+          for (int j = 0; j < R[i] - 1; ++j, ++nl) {
+            Lcol[nl] = (uint8_t)i;
+            Lrun[nl] = (uint8_t)j;
+          }
+        }
+        run += R[i];
+      }
+      uint64_t P = 0;
+      for (int i = 0; i < c; ++i)
+        if (R[i] == 1) P = umax64(P, rt_at(X0[i], W[i], 0, rows));
+      if (nl == 0) {  // the skeleton is a single candidate
+        if (slot == 0) score(P, ord, -1, 0, 0);
+        ord += 1;
+        continue;
+      }
+      // ---- heights DFS over the multi-run columns (search.cpp:163-190)
+      int l = 0;
+      const bool leaf_now = (nl == 1);
+      if (!leaf_now) {
+        const int i = Lcol[0];
+        int lo0, hi0;
+        height_interval(e, thresholds(amin, amax, win_lo, win_hi), W[i], rows, R[i], lo0, hi0);
+        Lh[0] = (uint8_t)(lo0 - 1);
+        Lhi[0] = (uint8_t)imax(hi0, 0);
+        Pin[0] = P;
+        Amin[0] = amin;
+        Amax[0] = amax;
+        Ly0[0] = 0;
+      }
+      while (true) {
+        int lv;  // level whose state feeds the leaf loop
+        uint64_t Pl;
+        int amin_l, amax_l, y0l;
+        if (leaf_now) {
+          lv = 0;
+          Pl = P;
+          amin_l = amin;
+          amax_l = amax;
+          y0l = 0;
+        } else {
+          // advance level l to its next admissible height
+          const int i = Lcol[l], j = Lrun[l];
+          const int w = W[i], y0 = Ly0[l];
+          const int rows_left = rows - y0;
+          const bool forced = (R[i] - j) == 2;
+          int h = Lh[l] + 1;
+          const int hhi = Lhi[l];
+          if (e.patho && !forced)
+            while (h <= hhi && !(w * h <= e.bmax[w * h])) ++h;
+          if (h > hhi) {
+            if (l == 0) break;
+            --l;
+            continue;
+          }
+          Lh[l] = (uint8_t)h;
+          const int a1 = w * h;
+          int na = imin(Amin[l], a1), nx = imax(Amax[l], a1);
+          const int ridx = RS0[i] + j;
+          curH[ridx] = (uint8_t)h;
+          uint64_t Pn = umax64(Pin[l], rt_at(X0[i], w, y0, h));
+          if (forced) {
+            const int a2 = w * (rows_left - h);
+            na = imin(na, a2);
+            nx = imax(nx, a2);
+            curH[ridx + 1] = (uint8_t)(rows_left - h);
+            Pn = umax64(Pn, rt_at(X0[i], w, y0 + h, rows_left - h));
+          }
+          const int nxt = l + 1;
+          const bool new_col = Lrun[nxt] == 0;
+          const int y0n = new_col ? 0 : y0 + h;
+          const Thr tn = thresholds(na, nx, win_lo, win_hi);
+          if (new_col && !columns_feasible(Lcol[nxt], tn)) continue;
+          if (nxt < nl - 1) {
+            const int i2 = Lcol[nxt];
+            int lo2, hi2;
+            height_interval(e, tn, W[i2], rows - y0n, R[i2] - Lrun[nxt], lo2, hi2);
+            if (lo2 > hi2) continue;
+            l = nxt;
+            Lh[l] = (uint8_t)(lo2 - 1);
+            Lhi[l] = (uint8_t)hi2;
+            Pin[l] = Pn;
+            Amin[l] = na;
+            Amax[l] = nx;
+            Ly0[l] = (uint8_t)y0n;
+            continue;
+          }
+          lv = nxt;
+          Pl = Pn;
+          amin_l = na;
+          amax_l = nx;
+          y0l = y0n;
+        }
+        // ---- leaf loop: run Lrun[lv] of column Lcol[lv] takes every
+        //      admissible height; the column's last run is forced.
+        {
+          const int i = Lcol[lv];
+          const int w = W[i];
+          const int rows_left = rows - y0l;
+          int lo, hi;
+          height_interval(e, thresholds(amin_l, amax_l, win_lo, win_hi), w, rows_left, 2, lo, hi);
+          const int lr = RS0[i] + Lrun[lv];
+          const int xwb = xw_of(cols, X0[i], w) * nyh;
+          if (lo + slot <= hi) {
+            // rect 1 = (y0l, h) advances by +1 per h; rect 2 = (y0l+h,
+            // rows_left-h) by rows_left-h-1 (yh numbering); lanes step h by J.
+            int h = lo + slot;
+            const uint64_t* p1 = rt + (size_t)(xwb + yh_of(rows, y0l, h)) * FPW + f;
+            int i2 = xwb + yh_of(rows, y0l + h, rows_left - h);
+            uint64_t v1 = *p1, v2 = rt[(size_t)i2 * FPW + f];
+            while (true) {
+              const int hn = h + J;
+              const bool more = hn <= hi;
+              const uint64_t* p1n = p1 + J * FPW;
+              const int i2n = i2 + J * (rows_left - h - 1) - (J * (J - 1)) / 2;
+              uint64_t v1n = 0, v2n = 0;
+              if (more) {  // prefetch the next height before scoring this one
+                v1n = *p1n;
+                v2n = rt[(size_t)i2n * FPW + f];
+              }
+              score(umax64(Pl, umax64(v1, v2)), ord + (uint64_t)(h - lo), lr, h, rows_left - h);
+              if (!more) break;
+              h = hn;
+              p1 = p1n;
+              i2 = i2n;
+              v1 = v1n;
+              v2 = v2n;
+            }
+          }
+          if (hi >= lo) ord += (uint64_t)(hi - lo + 1);
+        }
+        if (leaf_now) break;
+      }
+    }
+    if (fixed_widths) break;
+  }
+  st.count += ord;
+}
+
+}  // namespace scb

@@ -1,0 +1,56 @@
+"""TEST-ONLY ctypes wrapper of the host emulator of the search kernels."""
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libsearch_emu.so")
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+class Emu:
+    def __init__(self):
+        if not os.path.exists(SO):
+            raise RuntimeError(f"{SO} missing: make -C tests/emu")
+        self.L = C.CDLL(SO)
+        I, D, P = C.c_int, C.c_double, C.c_void_p
+        self.L.emu_search.argtypes = [I, I, I, D, I, I, I, I, P, P, P, I, C.c_size_t, P, P, P, P, P]
+
+    def search(self, cols, rows, n, k, max_cols, coverage, step, rect_time, rect_sse=None,
+               budget=None, warps=3, item_target=16):
+        rt = np.ascontiguousarray(rect_time, dtype=np.float64)
+        F = rt.shape[0]
+        rs = None if rect_sse is None else np.ascontiguousarray(rect_sse, dtype=np.float64)
+        b = None if budget is None else np.ascontiguousarray(budget, dtype=np.float64)
+        t = np.zeros(F)
+        sse = np.zeros(F)
+        cnt = np.zeros(F, dtype=np.uint64)
+        snap = np.zeros((F, 96), dtype=np.uint8)
+        found = np.zeros(F, dtype=np.int32)
+        st = self.L.emu_search(cols, rows, n, k, max_cols, coverage, step, F, _p(rt), _p(rs), _p(b),
+                               warps, item_target, _p(t), _p(sse), _p(cnt), _p(snap), _p(found))
+        assert st == 0
+        return t, sse, cnt, snap, found
+
+    @staticmethod
+    def slices(snap_row, n, rows):
+        W = [int(x) for x in snap_row[:16]]
+        R = [int(x) for x in snap_row[16:32]]
+        H = [int(x) for x in snap_row[32:32 + n]]
+        out, x, run, sid = [], 0, 0, 0
+        c = 0
+        while c < 16 and W[c]:
+            c += 1
+        for i in range(c):
+            y = 0
+            for _ in range(R[i]):
+                out.append((x, y, W[i], H[run], sid))
+                y += H[run]
+                run += 1
+                sid += 1
+            x += W[i]
+        return out

@@ -1,0 +1,127 @@
+// TEST-ONLY host emulator of the K4/K5 search kernels.
+//
+// Compiles the very same walk code the GPU runs (csrc/search_walk.cuh, the
+// body of k_search) for the host and executes it lane by lane: `warps`
+// emulated warps take the work items round-robin (increasing per warp, like
+// the kernel's atomic counter), every lane keeps its first-in-order best, and
+// the per-frame reduction mirrors k_finalize.  Used by the CPU test suite to
+// check the kernel LOGIC against the oracle without a GPU; never part of the
+// product library.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "search_walk.cuh"
+
+using namespace scb;
+
+extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols, int coverage,
+                          int step, int frames, const double* rect_time /*[F][NR]*/,
+                          const double* rect_sse /*[F][NR] or NULL*/, const double* budget,
+                          int warps, size_t item_target, double* out_t, double* out_sse,
+                          uint64_t* out_count, uint8_t* out_snap /*[F][96]*/, int* out_found) {
+  if (frames < 1 || frames > 32) return 1;
+  int fpw = 1;
+  while (fpw < frames) fpw <<= 1;
+  const int eff = max_tile_cols > 0 ? max_tile_cols : n;
+  const int maxc = std::min(std::min(n, eff), cols);
+  const std::vector<WorkItem> items = make_items(cols, maxc, coverage == 1, item_target);
+  std::vector<int32_t> tab;
+  const bool patho = make_area_tables(cols, rows, k, tab);
+  const int A = cols * rows + 1;
+  const int rstride = std::min(n, rows) + 1;
+  std::vector<int32_t> ilo((size_t)(cols + 1) * rstride, 0);
+  std::vector<uint64_t> magic(cols + 1, 0);
+  for (int w = 1; w <= cols; ++w) {
+    for (int r = 1; r < rstride; ++r) ilo[w * rstride + r] = tab[A + w * ((rows + r - 1) / r)];
+    magic[w] = div_magic(w);
+  }
+  const int nyh = rows * (rows + 1) / 2;
+  const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
+  std::vector<uint64_t> rt(nr * fpw, 0);
+  std::vector<double> rs(nr * fpw, 0.0);
+  for (int f = 0; f < frames; ++f)
+    for (size_t r = 0; r < nr; ++r) {
+      const double t = rect_time[(size_t)f * nr + r];
+      uint64_t bits;
+      std::memcpy(&bits, &t, 8);
+      rt[r * fpw + f] = (t > 0.0) ? bits : 0;
+      if (rect_sse) rs[r * fpw + f] = rect_sse[(size_t)f * nr + r];
+    }
+  WalkEnv e;
+  e.cols = cols;
+  e.rows = rows;
+  e.n = n;
+  e.nyh = nyh;
+  e.max_area = cols * rows;
+  e.coverage = coverage;
+  e.patho = patho ? 1 : 0;
+  e.rstride = rstride;
+  e.bmax = tab.data();
+  e.aneed = tab.data() + A;
+  e.mstar = tab.data() + 2 * A;
+  e.ilo = ilo.data();
+  e.magic = magic.data();
+  e.rt = rt.data();
+  e.rs = rs.data();
+
+  std::vector<LaneState> st((size_t)warps * 32);
+  std::vector<uint8_t> snaps((size_t)warps * 32 * kSnap, 0);
+  for (int wp = 0; wp < warps; ++wp)
+    for (int l = 0; l < 32; ++l) {
+      LaneState& s = st[(size_t)wp * 32 + l];
+      s.best_t = ~0ull;
+      s.best_item = ~0ull;
+      s.best_ord = ~0ull;
+      s.best_sse = INFINITY;
+      s.count = 0;
+      s.snap = &snaps[((size_t)wp * 32 + l) * kSnap];
+      s.budget = 0;
+      if (step == 2 && (l % fpw) < frames) {
+        const double b = budget[l % fpw];
+        uint64_t bits;
+        std::memcpy(&bits, &b, 8);
+        s.budget = (b > 0.0) ? bits : 0;
+      }
+    }
+  for (size_t it = 0; it < items.size(); ++it) {
+    const int wp = (int)(it % (size_t)warps);
+    for (int l = 0; l < 32; ++l) {
+      LaneState& s = st[(size_t)wp * 32 + l];
+      switch (fpw * 10 + step) {
+#define CASE(F)                                                                   \
+  case F * 10 + 1: walk_item<F, 1>(e, it, items[it], l % F, l / F, s); break;    \
+  case F * 10 + 2: walk_item<F, 2>(e, it, items[it], l % F, l / F, s); break;
+        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
+#undef CASE
+        default: return 2;
+      }
+    }
+  }
+  for (int f = 0; f < frames; ++f) {
+    int win = -1;
+    for (int i = 0; i < warps * 32; ++i) {
+      if (i % 32 % fpw != f) continue;
+      const LaneState& s = st[i];
+      if (s.best_item == ~0ull) continue;
+      if (win < 0) { win = i; continue; }
+      const LaneState& b = st[win];
+      bool less;
+      if (step == 2 && s.best_sse != b.best_sse) less = s.best_sse < b.best_sse;
+      else if (s.best_t != b.best_t) less = s.best_t < b.best_t;
+      else if (s.best_item != b.best_item) less = s.best_item < b.best_item;
+      else less = s.best_ord < b.best_ord;
+      if (less) win = i;
+    }
+    out_found[f] = win >= 0;
+    uint64_t cnt = 0;
+    for (int wp = 0; wp < warps; ++wp) cnt += st[(size_t)wp * 32].count;
+    out_count[f] = cnt;
+    if (win >= 0) {
+      std::memcpy(&out_t[f], &st[win].best_t, 8);
+      out_sse[f] = st[win].best_sse;
+      std::memcpy(out_snap + (size_t)f * kSnap, st[win].snap, kSnap);
+    }
+  }
+  return 0;
+}
