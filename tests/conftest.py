@@ -27,3 +27,12 @@ def part():
     p = Partitioner(0)
     yield p
     p.close()
+
+
+@pytest.fixture(scope="session")
+def emu():
+    """Test-only host build of the search walk (tests/emu)."""
+    import subprocess
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "emu")], check=True)
+    from emu.emu import Emu
+    return Emu()

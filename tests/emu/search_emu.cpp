@@ -18,8 +18,10 @@ using namespace scb;
 extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols, int coverage,
                           int step, int frames, const double* rect_time /*[F][NR]*/,
                           const double* rect_sse /*[F][NR] or NULL*/, const double* budget,
-                          int warps, size_t item_target, double* out_t, double* out_sse,
-                          uint64_t* out_count, uint8_t* out_snap /*[F][96]*/, int* out_found) {
+                          int warps, size_t item_target, int item_offset, int item_stride,
+                          double* out_t, double* out_sse, uint64_t* out_count,
+                          uint8_t* out_snap /*[F][96]*/, int* out_found, uint64_t* out_item,
+                          uint64_t* out_ord) {
   if (frames < 1 || frames > 32) return 1;
   int fpw = 1;
   while (fpw < frames) fpw <<= 1;
@@ -84,8 +86,9 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
         s.budget = (b > 0.0) ? bits : 0;
       }
     }
-  for (size_t it = 0; it < items.size(); ++it) {
-    const int wp = (int)(it % (size_t)warps);
+  size_t kk = 0;
+  for (size_t it = (size_t)item_offset; it < items.size(); it += (size_t)item_stride, ++kk) {
+    const int wp = (int)(kk % (size_t)warps);
     for (int l = 0; l < 32; ++l) {
       LaneState& s = st[(size_t)wp * 32 + l];
       switch (fpw * 10 + step) {
@@ -121,6 +124,8 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       std::memcpy(&out_t[f], &st[win].best_t, 8);
       out_sse[f] = st[win].best_sse;
       std::memcpy(out_snap + (size_t)f * kSnap, st[win].snap, kSnap);
+      out_item[f] = st[win].best_item;
+      out_ord[f] = st[win].best_ord;
     }
   }
   return 0;

@@ -1,0 +1,86 @@
+"""CPU check of the search-kernel LOGIC: the very walk code the GPU runs
+(csrc/search_walk.cuh), compiled for the host by the test-only emulator in
+tests/emu and executed lane by lane, against the C oracle on seeded random
+instances -- both steps, both coverage modes, every frames-per-warp width
+(hence every leaf-loop split J = 32 / FPW), several work-item granularities.
+The GPU parity tests (test_gpu_parity.py) then check the compiled kernels."""
+import numpy as np
+import pytest
+
+
+def _case(rng, max_cells=9):
+    cols, rows = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+    n = int(rng.integers(1, min(max_cells, cols * rows) + 1))
+    return cols, rows, n
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_step1_vs_oracle(emu, oracle, seed):
+    from emu.emu import Emu
+    rng = np.random.default_rng(seed)
+    for trial in range(60):
+        cols, rows, n = _case(rng, 10)
+        mc = int(rng.integers(0, 5))
+        k = float(rng.choice([3.0, 2.5, 2.0, 1.5]))
+        cov = int(rng.integers(0, 2))
+        F = int(rng.choice([1, 2, 3, 4, 8, 32]))
+        est = rng.lognormal(0, 0.6, size=(F, cols * rows))
+        if trial % 3 == 0:
+            est = np.round(est)
+        rt = np.stack([oracle.rect_times(est[f], cols, rows) for f in range(F)])
+        tgt = int(rng.choice([1, 16, 100000]))
+        t, _, cnt, snap, found = emu.search(cols, rows, n, k, mc, cov, 1, rt, item_target=tgt,
+                                            warps=int(rng.integers(1, 5)))
+        for f in range(F):
+            st, r = oracle.search(cols * 64, rows * 64, 64, est[f], None, n, 0.0, k, mc, cov, 1)
+            if st:
+                assert not found[f]
+                continue
+            ctx = (seed, trial, f, cols, rows, n, mc, k, cov, F)
+            assert t[f] == r.t_min_us, ctx
+            assert cnt[f] == r.candidates_step1, ctx
+            assert Emu.slices(snap[f], n, rows) == r.argmin1.slices(rows), ctx
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_step2_vs_oracle(emu, oracle, seed):
+    from emu.emu import Emu
+    rng = np.random.default_rng(100 + seed)
+    for trial in range(40):
+        cols, rows, n = _case(rng, 9)
+        mc = int(rng.integers(0, 5))
+        k = float(rng.choice([3.0, 2.5, 2.0]))
+        cov = int(rng.integers(0, 2))
+        lam = float(rng.choice([0.0, 0.1, 0.3, 1.0]))
+        F = int(rng.choice([1, 2, 3, 4, 8]))
+        W, H = cols * 64, rows * 64 - int(rng.integers(0, 60))
+        est = rng.lognormal(0, 0.6, size=(F, cols * rows))
+        if trial % 3 == 0:
+            est = np.round(est)
+        luma = rng.integers(0, 1024, size=(F, H, W)).astype(np.uint16)
+        if trial % 4 == 0:
+            luma[:] = 7  # flat frames: SSE ties at 0
+        recs = [oracle.ctu_stats(luma[f], 64) for f in range(F)]
+        rt = np.stack([oracle.rect_times(est[f], cols, rows) for f in range(F)])
+        rs = np.stack([oracle.rect_sse(W, H, 64, recs[f]) for f in range(F)])
+        res = [oracle.search(W, H, 64, est[f], recs[f], n, lam, k, mc, cov, 3) for f in range(F)]
+        if any(st != 0 for st, _ in res):
+            continue
+        budget = np.array([r.t_min_us * (1.0 + lam) for _, r in res])
+        t, sse, cnt, snap, found = emu.search(cols, rows, n, k, mc, cov, 2, rt, rs, budget)
+        for f in range(F):
+            r = res[f][1]
+            ctx = (seed, trial, f, cols, rows, n, mc, k, cov, lam, F)
+            assert t[f] == r.t_best_us and sse[f] == r.sse_best, ctx
+            assert cnt[f] == r.candidates_step2, ctx
+            assert Emu.slices(snap[f], n, rows) == r.best.slices(rows), ctx
+
+
+def test_baseline_grid_counts(emu, oracle):
+    """cfg1 / cfg2 grids: counts of both families equal the oracle's."""
+    for (cols, rows, n, mc) in [(15, 9, 4, 2), (15, 9, 8, 4)]:
+        est = np.ones((1, cols * rows))
+        rt = np.stack([oracle.rect_times(est[0], cols, rows)])
+        for cov in (0, 1):
+            _, _, cnt, _, _ = emu.search(cols, rows, n, 3.0, mc, cov, 1, rt, item_target=512)
+            assert cnt[0] == oracle.count(cols, rows, n, 3.0, mc, cov)
