@@ -65,9 +65,17 @@ __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
   }
   for (int w = threadIdx.x; w <= a.cols; w += blockDim.x)
     s_magic[w] = w >= 1 ? div_magic(w) : 0ull;
+  int32_t* s_ybase = reinterpret_cast<int32_t*>(s_magic + a.cols + 1);
+  int32_t* s_sfx = s_ybase + a.rows + 1;
+  for (int y = threadIdx.x; y <= a.rows; y += blockDim.x) {
+    s_ybase[y] = yh_of(a.rows, y, 1);
+    s_sfx[y] = y < a.rows ? yh_of(a.rows, y, a.rows - y) : 0;
+  }
   __syncthreads();
   e.ilo = s_ilo;
   e.magic = s_magic;
+  e.ybase = s_ybase;
+  e.sfx = s_sfx;
   e.rt = a.rt;
   e.rs = a.rs;
 
@@ -197,7 +205,7 @@ int search_blocks_per_sm(int fpw, int step) {
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st) {
   const size_t smem = ((size_t)2 * (a.max_area + 1) + (size_t)(a.cols + 1) * (a.rows + 1) +
                        (size_t)(a.cols + 1) * (std::min(a.n, a.rows) + 1) + 2 +
-                       (size_t)(a.cols + 1) * 2) *
+                       (size_t)(a.cols + 1) * 2 + (size_t)(a.rows + 1) * 2) *
                       sizeof(int32_t);
   if (smem > 64 * 1024) fail(SC_ERR_SIZE, "CTU grid too large for the area tables");
   switch (fpw * 10 + step) {

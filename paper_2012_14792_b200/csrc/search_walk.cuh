@@ -21,6 +21,16 @@
 
 namespace scb {
 
+#if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
+struct WalkStats {
+  uint64_t widths, runs_steps, skeletons, levels, leaf_calls, leaves, levels_leafcol, leafr[65];
+};
+inline WalkStats g_stats;
+#define SCB_STAT(x) (++g_stats.x)
+#else
+#define SCB_STAT(x) ((void)0)
+#endif
+
 // ---- portable intrinsics -------------------------------------------------------
 SCB_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
 #ifdef __CUDA_ARCH__
@@ -56,6 +66,8 @@ struct WalkEnv {
   const int32_t* mstar;   // [(cols+1) * (rows+1)]
   const int32_t* ilo;     // [(cols+1) * rstride]: lower end of window I(w, r)
   const uint64_t* magic;  // [cols+1]: division by w (div_magic)
+  const int32_t* ybase;   // [rows+1]: yh(y, 1), the first rectangle starting at row y
+  const int32_t* sfx;     // [rows+1]: yh(y, rows - y), the rectangle from row y to the bottom
   const uint64_t* rt;     // [NR][FPW] clamped f64 time bits of every rectangle
   const double* rs;       // [NR][FPW] SSE of every rectangle (step 2)
 };
@@ -120,7 +132,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   int W[SC_MAX_COLS], R[SC_MAX_COLS], X0[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
   uint8_t curH[SC_MAX_SLICES];
   uint8_t Lcol[kMaxLevels], Lrun[kMaxLevels], Ly0[kMaxLevels], Lh[kMaxLevels], Lhi[kMaxLevels];
-  int32_t Amin[kMaxLevels], Amax[kMaxLevels];
+  int32_t Amin[kMaxLevels], Amax[kMaxLevels], Lbase[kMaxLevels];
   uint64_t Pin[kMaxLevels];
 
   auto thresholds = [&](int amin, int amax, int win_lo, int win_hi) -> Thr {
@@ -248,6 +260,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       }
       if (!got) break;
     }
+    SCB_STAT(widths);
     // ---- runs DFS (lex, search.cpp:145-161).  The skeleton (widths, runs)
     //      has an admissible completion iff the column windows
     //      I(w, r) = [aneed[w*ceil(rows/r)], w*floor(rows/r)] intersect; I
@@ -260,6 +273,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     SL[0] = e.n;
     R[0] = imax(1, e.n - (c - 1) * rows) - 1;
     while (true) {
+      SCB_STAT(runs_steps);
       const int after = c - 1 - rp;
       const int rhi = imin(rows, SL[rp] - after);
       const int w = W[rp];
@@ -293,6 +307,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       // ---- one live skeleton (c, widths, runs); every area lies in
       //      [win_lo, bmax[nH]] for a window a in [nL, nH]
       const int win_lo = nL, win_hi = e.bmax[nH];
+      SCB_STAT(skeletons);
       int amin = kBigArea, amax = 0;
       int run = 0, nl = 0;
       for (int i = 0; i < c; ++i) {
@@ -303,9 +318,11 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           amax = imax(amax, ar);
           curH[run] = (uint8_t)rows;
         } else {
+          const int base = xw_of(cols, X0[i], W[i]) * nyh;
           for (int j = 0; j < R[i] - 1; ++j, ++nl) {
             Lcol[nl] = (uint8_t)i;
             Lrun[nl] = (uint8_t)j;
+            Lbase[nl] = base;
           }
         }
         run += R[i];
@@ -344,7 +361,11 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           y0l = 0;
         } else {
           // advance level l to its next admissible height
+          SCB_STAT(levels);
           const int i = Lcol[l], j = Lrun[l];
+#if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
+          if (i == Lcol[nl - 1]) ++g_stats.levels_leafcol;
+#endif
           const int w = W[i], y0 = Ly0[l];
           const int rows_left = rows - y0;
           const bool forced = (R[i] - j) == 2;
@@ -362,13 +383,14 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           int na = imin(Amin[l], a1), nx = imax(Amax[l], a1);
           const int ridx = RS0[i] + j;
           curH[ridx] = (uint8_t)h;
-          uint64_t Pn = umax64(Pin[l], rt_at(X0[i], w, y0, h));
+          const int lb = Lbase[l];
+          uint64_t Pn = umax64(Pin[l], rt[(size_t)(lb + e.ybase[y0] + h - 1) * FPW + f]);
           if (forced) {
             const int a2 = w * (rows_left - h);
             na = imin(na, a2);
             nx = imax(nx, a2);
             curH[ridx + 1] = (uint8_t)(rows_left - h);
-            Pn = umax64(Pn, rt_at(X0[i], w, y0 + h, rows_left - h));
+            Pn = umax64(Pn, rt[(size_t)(lb + e.sfx[y0 + h]) * FPW + f]);
           }
           const int nxt = l + 1;
           const bool new_col = Lrun[nxt] == 0;
@@ -404,13 +426,17 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           int lo, hi;
           height_interval(e, thresholds(amin_l, amax_l, win_lo, win_hi), w, rows_left, 2, lo, hi);
           const int lr = RS0[i] + Lrun[lv];
-          const int xwb = xw_of(cols, X0[i], w) * nyh;
+          const int xwb = Lbase[lv];
+          SCB_STAT(leaf_calls);
+#if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
+          ++g_stats.leafr[R[i]];
+#endif
           if (lo + slot <= hi) {
             // rect 1 = (y0l, h) advances by +1 per h; rect 2 = (y0l+h,
             // rows_left-h) by rows_left-h-1 (yh numbering); lanes step h by J.
             int h = lo + slot;
-            const uint64_t* p1 = rt + (size_t)(xwb + yh_of(rows, y0l, h)) * FPW + f;
-            int i2 = xwb + yh_of(rows, y0l + h, rows_left - h);
+            const uint64_t* p1 = rt + (size_t)(xwb + e.ybase[y0l] + h - 1) * FPW + f;
+            int i2 = xwb + e.sfx[y0l + h];
             uint64_t v1 = *p1, v2 = rt[(size_t)i2 * FPW + f];
             while (true) {
               const int hn = h + J;

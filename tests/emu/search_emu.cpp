@@ -39,6 +39,11 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
     magic[w] = div_magic(w);
   }
   const int nyh = rows * (rows + 1) / 2;
+  std::vector<int32_t> ybase(rows + 1), sfx(rows + 1);
+  for (int y = 0; y <= rows; ++y) {
+    ybase[y] = yh_of(rows, y, 1);
+    sfx[y] = y < rows ? yh_of(rows, y, rows - y) : 0;
+  }
   const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
   std::vector<uint64_t> rt(nr * fpw, 0);
   std::vector<double> rs(nr * fpw, 0.0);
@@ -64,6 +69,8 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.mstar = tab.data() + 2 * A;
   e.ilo = ilo.data();
   e.magic = magic.data();
+  e.ybase = ybase.data();
+  e.sfx = sfx.data();
   e.rt = rt.data();
   e.rs = rs.data();
 
