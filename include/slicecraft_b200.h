@@ -112,6 +112,11 @@ typedef struct sc_search_result {
   uint64_t leaves_scored_step2;
   sc_layout argmin;            /* step-1 first-in-order argmin */
   sc_layout best;              /* step-2 choice */
+  /* bits 64..127 of the exact candidate counts (the low 64 bits are
+   * candidates_step1/2, the reference's own uint64 counters): non-zero only
+   * for spaces beyond 2^64 such as config 5 (~6.1e29). */
+  uint64_t candidates_step1_hi;
+  uint64_t candidates_step2_hi;
 } sc_search_result;
 
 typedef struct sc_ctx sc_ctx;

@@ -53,7 +53,8 @@ class SearchResult(C.Structure):
                 ("candidates_step2", C.c_uint64), ("search_time_us", C.c_double),
                 ("time_min_step_us", C.c_double), ("clustering_step_us", C.c_double),
                 ("leaves_scored_step1", C.c_uint64), ("leaves_scored_step2", C.c_uint64),
-                ("argmin", Layout), ("best", Layout)]
+                ("argmin", Layout), ("best", Layout),
+                ("candidates_step1_hi", C.c_uint64), ("candidates_step2_hi", C.c_uint64)]
 
 
 class ShardBest(C.Structure):

@@ -26,10 +26,12 @@ void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16
                         cudaStream_t st);
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st);
 int search_blocks_per_sm(int fpw, int step);
-void finalize_launch(int step, int fpw, int frames_in_group, uint32_t n_warps,
+void column_bounds_launch(const uint64_t* rt, int fpw, int frames_in_group, int cols, int rows,
+                          int rmax, int rstride, uint64_t* lbr, uint64_t* lbm, cudaStream_t st);
+void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
                      const LaneBest* lanes, const uint8_t* snaps,
-                     const unsigned long long* count, double lambda, FrameBest* out,
-                     uint64_t* budget_out, cudaStream_t st);
+                     const unsigned long long* count, const unsigned long long* scored,
+                     double lambda, FrameBest* out, uint64_t* budget_out, cudaStream_t st);
 }  // namespace scb
 
 using namespace scb;
@@ -137,6 +139,16 @@ int next_pow2(int v) {
 }
 
 // ---- planner (plan.h) ------------------------------------------------------
+// Exact candidate count of the plan's family (computed once, cached).
+unsigned __int128 plan_count(Plan* p, const sc_grid& g, const sc_search_cfg& cfg) {
+  if (!p->have_count) {
+    p->count = count_candidates_dp(g.cols, g.rows, cfg.n_slices, p->key.maxc,
+                                   cfg.coverage == SC_COVERAGE_COVERING, p->bmax);
+    p->have_count = true;
+  }
+  return p->count;
+}
+
 Plan* get_plan(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc) {
   PlanKey key{g.cols, g.rows, cfg.n_slices, maxc, cfg.coverage, cfg.k_area};
   for (Plan* p : ctx->plans)
@@ -145,6 +157,12 @@ Plan* get_plan(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc
   p->key = key;
   const bool covering = cfg.coverage == SC_COVERAGE_COVERING;
   p->items = make_items(g.cols, maxc, covering, (size_t)ctx->sm_count * 16 * 32);
+  // seed phase of the pruned mode: the items of the smallest column count(s)
+  p->seed_items = 0;
+  for (const WorkItem& it : p->items) {
+    if (it.c > 1) break;
+    ++p->seed_items;
+  }
   p->pathological = make_area_tables(g.cols, g.rows, cfg.k_area, p->bmax);
   ctx->plans.push_back(p);
   return p;
@@ -249,7 +267,7 @@ void enqueue_moment_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool
 // One search step over all frame groups; finalize writes FrameBest[step] and,
 // after step 1, the device budgets of step 2.  No host synchronisation.
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
-                  const Layouts& L, int step, cudaStream_t st) {
+                  const Layouts& L, int step, bool compute_bounds, cudaStream_t st) {
   const int bps = search_blocks_per_sm(L.fpw, step);
   const int blocks = ctx->sm_count * bps;
   const uint32_t warps = (uint32_t)blocks * 8;
@@ -257,15 +275,36 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
   const size_t snap_bytes = (size_t)warps * 32 * kSnapBytes;
   ctx->lanes.ensure(lane_bytes * L.groups);
   ctx->snaps.ensure(snap_bytes * L.groups);
-  ctx->counter.ensure((size_t)L.groups * 4 * sizeof(uint64_t));
+  ctx->counter.ensure((size_t)L.groups * 8 * sizeof(uint64_t));
   ctx->frame_best.ensure((size_t)2 * L.groups * L.fpw * sizeof(FrameBest));
   ctx->budget.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
-  uint64_t* ctr_base = ctx->counter.as<uint64_t>() + (step - 1) * 2;
-  SCB_CUDA(cudaMemsetAsync(ctx->counter.p, 0, (size_t)L.groups * 4 * sizeof(uint64_t), st));
+  // per group: 4 u64 per step = {item counter, candidates, scored, pad}
+  uint64_t* ctr_base = ctx->counter.as<uint64_t>() + (step - 1) * 4;
+  SCB_CUDA(cudaMemsetAsync(ctr_base, 0, sizeof(uint64_t) * 4, st));
+  for (int gi = 1; gi < L.groups; ++gi)
+    SCB_CUDA(cudaMemsetAsync(ctr_base + 8 * gi, 0, sizeof(uint64_t) * 4, st));
   const uint32_t total = (uint32_t)plan->items.size();
   const uint32_t rank = (uint32_t)ctx->shard_rank, world = (uint32_t)ctx->shard_world;
   const uint32_t mine = total > rank ? (total - rank + world - 1) / world : 0;
   FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)(step - 1) * L.groups * L.fpw;
+  const bool prune = cfg.mode == SC_MODE_PRUNED;
+  const int rstride = std::min(cfg.n_slices, g.rows) + 1;
+  const size_t lb_per_group = (size_t)n_xw(g.cols) * rstride * L.fpw;
+  if (prune) {
+    ctx->inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+    ctx->seed_inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+    if (compute_bounds) {
+      // column lower bounds from the time tables; shared incumbents to +inf
+      ctx->lbr.ensure(lb_per_group * L.groups * sizeof(uint64_t));
+      ctx->lbm.ensure(lb_per_group * L.groups * sizeof(uint64_t));
+      for (int gi = 0; gi < L.groups; ++gi)
+        column_bounds_launch(ctx->rt_search.as<uint64_t>() + (size_t)gi * L.nr * L.fpw, L.fpw,
+                             std::min(L.fpw, L.frames - gi * L.fpw), g.cols, g.rows,
+                             rstride - 1, rstride, ctx->lbr.as<uint64_t>() + gi * lb_per_group,
+                             ctx->lbm.as<uint64_t>() + gi * lb_per_group, st);
+    }
+    SCB_CUDA(cudaMemsetAsync(ctx->inc.p, 0xff, (size_t)L.groups * L.fpw * sizeof(uint64_t), st));
+  }
   for (int gi = 0; gi < L.groups; ++gi) {
     SearchArgs a{};
     a.cols = g.cols;
@@ -278,9 +317,16 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     a.n_items = mine;
     a.item_offset = rank;
     a.item_stride = world;
-    uint64_t* ctr = ctr_base + 4 * gi;
+    uint64_t* ctr = ctr_base + 8 * gi;
     a.counter = reinterpret_cast<uint32_t*>(ctr);
     a.count_out = reinterpret_cast<unsigned long long*>(ctr + 1);
+    a.scored_out = reinterpret_cast<unsigned long long*>(ctr + 2);
+    a.prune = prune ? 1 : 0;
+    if (prune) {
+      a.lbr = ctx->lbr.as<uint64_t>() + gi * lb_per_group;
+      a.lbm = ctx->lbm.as<uint64_t>() + gi * lb_per_group;
+      a.inc = ctx->inc.as<uint64_t>() + (size_t)gi * L.fpw;
+    }
     a.bmax = plan->d_bmax.as<int32_t>();
     a.pathological = plan->pathological ? 1 : 0;
     a.rt = ctx->rt_search.as<uint64_t>() + (size_t)gi * L.nr * L.fpw;
@@ -288,9 +334,30 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     a.budget = ctx->budget.as<uint64_t>() + (size_t)gi * L.fpw;
     a.lanes = reinterpret_cast<LaneBest*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
     a.snaps = ctx->snaps.as<uint8_t>() + snap_bytes * gi;
-    search_launch(L.fpw, step, a, blocks, st);
+    if (prune && step == 1 && mine > 1) {
+      // Seeded branch-and-bound: phase A walks the first items (the smallest
+      // column counts, which hold the fast candidates of the family) so every
+      // frame has a shared incumbent before phase B spreads the rest of the
+      // space over all warps.  Both phases keep each lane's items increasing.
+      const uint32_t seed_items = std::min<uint32_t>(mine, plan->seed_items);
+      a.k_begin = 0;
+      a.n_items = seed_items;
+      search_launch(L.fpw, step, a, blocks, st);
+      uint64_t* frozen = ctx->seed_inc.as<uint64_t>() + (size_t)gi * L.fpw;
+      SCB_CUDA(cudaMemcpyAsync(frozen, a.inc, L.fpw * sizeof(uint64_t),
+                               cudaMemcpyDeviceToDevice, st));
+      a.seed_inc = frozen;
+      a.k_begin = seed_items;
+      a.n_items = mine;
+      a.resume = 1;
+      a.counter = reinterpret_cast<uint32_t*>(ctr + 3);
+      search_launch(L.fpw, step, a, blocks, st);
+    } else {
+      search_launch(L.fpw, step, a, blocks, st);
+    }
     const int fig = std::min(L.fpw, L.frames - gi * L.fpw);
-    finalize_launch(step, L.fpw, fig, warps, a.lanes, a.snaps, a.count_out, cfg.lambda,
+    finalize_launch(step, cfg.n_slices, L.fpw, fig, warps, a.lanes, a.snaps, a.count_out,
+                    a.scored_out, cfg.lambda,
                     fb + (size_t)gi * L.fpw,
                     step == 1 ? ctx->budget.as<uint64_t>() + (size_t)gi * L.fpw : nullptr, st);
   }
@@ -384,12 +451,12 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
                            cudaMemcpyDefault, s));
   enqueue_time_tables(ctx, g, L, false, s);
   SCB_CUDA(cudaEventRecord(ev[1], s));
-  if (do1) enqueue_step(ctx, g, cfg, plan, L, 1, s);
+  if (do1) enqueue_step(ctx, g, cfg, plan, L, 1, true, s);
   else upload_budgets(ctx, L, t_min_in, cfg.lambda, s);
   SCB_CUDA(cudaEventRecord(ev[2], s));
   SCB_CUDA(cudaStreamWaitEvent(s, ev[6], 0));  // join
   SCB_CUDA(cudaEventRecord(ev[8], s));
-  if (do2) enqueue_step(ctx, g, cfg, plan, L, 2, s);
+  if (do2) enqueue_step(ctx, g, cfg, plan, L, 2, !do1, s);
   SCB_CUDA(cudaEventRecord(ev[3], s));
   const size_t nfb = (size_t)2 * L.groups * L.fpw;
   ctx->h_frame_best.ensure(nfb * sizeof(FrameBest));
@@ -412,6 +479,12 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   const FrameBest* b2 = hb + (size_t)L.groups * L.fpw;
   ctx->last_best[0].assign(b1, b1 + frames);
   ctx->last_best[1].assign(b2, b2 + frames);
+  ctx->last_pruned = cfg.mode == SC_MODE_PRUNED;
+  if (ctx->last_pruned) {  // shards export the global DP count from rank 0 only
+    const unsigned __int128 cnt = plan_count(plan, g, cfg);
+    for (int s2 = 0; s2 < 2; ++s2)
+      for (auto& fbv : ctx->last_best[s2]) fbv.count = ctx->shard_rank == 0 ? (uint64_t)cnt : 0;
+  }
   for (int f = 0; f < frames; ++f) {
     sc_search_result& r = out[f];
     std::memset(&r, 0, sizeof(r));
@@ -419,7 +492,7 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
       if (!b1[f].found) fail(SC_ERR_NO_CANDIDATE, "area constraint admits no candidate partition");
       r.t_min_us = bits_to_double(b1[f].t);
       r.candidates_step1 = b1[f].count;
-      r.leaves_scored_step1 = b1[f].count;
+      r.leaves_scored_step1 = b1[f].scored / (uint64_t)L.fpw;
       layout_from_snap(b1[f], cfg.n_slices, &r.argmin);
     } else if (t_min_in) {
       double tm;
@@ -431,8 +504,21 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
       r.t_best_us = bits_to_double(b2[f].t);
       r.sse_best = b2[f].sse;
       r.candidates_step2 = b2[f].count;
-      r.leaves_scored_step2 = b2[f].count;
+      r.leaves_scored_step2 = b2[f].scored / (uint64_t)L.fpw;
       layout_from_snap(b2[f], cfg.n_slices, &r.best);
+    }
+    if (cfg.mode == SC_MODE_PRUNED) {
+      // pruned walks do not enumerate every candidate: the counters come from
+      // the exact DP (plan.h count_candidates_dp) -- the reference's values
+      const unsigned __int128 cnt = plan_count(plan, g, cfg);
+      if (do1) {
+        r.candidates_step1 = (uint64_t)cnt;
+        r.candidates_step1_hi = (uint64_t)(cnt >> 64);
+      }
+      if (do2) {
+        r.candidates_step2 = (uint64_t)cnt;
+        r.candidates_step2_hi = (uint64_t)(cnt >> 64);
+      }
     }
     r.candidates_evaluated = r.candidates_step1 + r.candidates_step2;
     r.time_min_step_us = ctx->timings[2] / frames;
@@ -445,7 +531,7 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
 
 sc_ctx::~sc_ctx() {
   for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rs_search, &usat,
-                  &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec})
+                  &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc})
     b->release();
   h_stage.release();
   h_records.release();
@@ -460,6 +546,18 @@ sc_ctx::~sc_ctx() {
     if (e) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);
   if (stream2) cudaStreamDestroy(stream2);
+}
+
+// Lexicographic (widths, runs, heights) order of two layouts of one work
+// item: the reference's enumeration order (search.cpp:120-190).
+bool layout_less(const sc_layout& a, const sc_layout& b) {
+  for (int i = 0; i < SC_MAX_COLS; ++i)
+    if (a.col_widths[i] != b.col_widths[i]) return a.col_widths[i] < b.col_widths[i];
+  for (int i = 0; i < SC_MAX_COLS; ++i)
+    if (a.runs_per_col[i] != b.runs_per_col[i]) return a.runs_per_col[i] < b.runs_per_col[i];
+  for (int i = 0; i < SC_MAX_SLICES; ++i)
+    if (a.run_heights[i] != b.run_heights[i]) return a.run_heights[i] < b.run_heights[i];
+  return false;
 }
 
 extern "C" {
@@ -745,7 +843,7 @@ sc_status sc_shard_merge(int32_t step, int32_t world, int32_t frames,
         if (step == 2 && s.key_sse != b.key_sse) less = s.key_sse < b.key_sse;
         else if (s.key_t != b.key_t) less = s.key_t < b.key_t;
         else if (s.item != b.item) less = s.item < b.item;
-        else less = s.ord < b.ord;
+        else less = layout_less(s.layout, b.layout);
         if (less) win = r;
       }
       if (win < 0) fail(SC_ERR_NO_CANDIDATE, "no candidate on any shard");

@@ -105,6 +105,9 @@ struct Plan {
   std::vector<WorkItem> items;
   std::vector<int32_t> bmax;  // bmax | aneed | mstar tables (api.cu get_plan)
   bool pathological = false;  // some single area fails the test (k ~ 1)
+  uint32_t seed_items = 0;    // pruned mode: items of the seeding phase
+  bool have_count = false;    // exact DP count computed (pruned mode)
+  unsigned __int128 count = 0;
   DevBuf d_items, d_bmax;
   bool uploaded = false;
 };
@@ -121,9 +124,11 @@ constexpr int kSnapBytes = 96;  // W[16] R[16] H[64], bytes
 
 // Arguments of the search kernels (search.cu), filled by api.cu.
 struct SearchArgs {
-  int cols, rows, n, nyh, max_area, coverage, pathological;
+  int cols, rows, n, nyh, max_area, coverage, pathological, prune;
   const WorkItem* items;
-  uint32_t n_items;       // items of this shard
+  uint32_t n_items;       // items of this shard: k in [k_begin, n_items)
+  uint32_t k_begin;       // first local item index of this launch
+  int resume;             // lanes continue from the LaneBest left by a previous launch
   uint32_t item_offset;   // global index = offset + k * stride
   uint32_t item_stride;
   uint32_t* counter;
@@ -134,6 +139,11 @@ struct SearchArgs {
   LaneBest* lanes;        // [warps * 32]
   uint8_t* snaps;         // [warps * 32][kSnapBytes]
   unsigned long long* count_out;
+  unsigned long long* scored_out;  // candidate-frame scores actually evaluated
+  const uint64_t* lbr;             // pruned mode: column lower bounds (search_walk.cuh)
+  const uint64_t* lbm;
+  uint64_t* inc;                   // pruned mode: shared step-1 incumbent [FPW]
+  const uint64_t* seed_inc;        // pruned mode, phase B: incumbent frozen after phase A
 };
 
 // Device-side per-frame result written by finalize.
@@ -143,6 +153,7 @@ struct FrameBest {
   uint64_t item;
   uint64_t ord;
   uint64_t count;
+  uint64_t scored;
   uint8_t snap[kSnapBytes];
   int32_t found;
   int32_t pad;
@@ -162,12 +173,13 @@ struct sc_ctx {
   int shard_rank = 0, shard_world = 1;
   // staging / tables
   scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rs_search, usat;
-  scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec;
+  scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec, lbr, lbm, inc, seed_inc;
   int dec_cols = -1, dec_rows = -1;
   scb::HostBuf h_stage, h_records, h_frame_best, h_budget;
   std::vector<scb::Plan*> plans;
   // last step results (for shard export)
   std::vector<scb::FrameBest> last_best[2];
   uint64_t last_leaves[2] = {0, 0};
+  bool last_pruned = false;  // last search ran in SC_MODE_PRUNED (DP counts)
   ~sc_ctx();
 };

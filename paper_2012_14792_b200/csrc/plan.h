@@ -104,3 +104,96 @@ inline bool make_area_tables(int cols, int rows, double k, std::vector<int32_t>&
 }
 
 }  // namespace scb
+
+#include <thread>
+
+namespace scb {
+
+// Exact candidate count of the ColumnSplit family (what for_each_candidate
+// would enumerate, search.cpp:302-319) without enumerating it.
+//
+// A candidate is admissible iff all its slice areas lie in one window
+// [a, bmax[a]] (a = its smallest area).  So
+//     count = sum_a  N(a, bmax[a]) - N(a+1, bmax[a])
+// where N(lo, hi) counts candidates whose areas all lie in [lo, hi].  N
+// factorises over columns: a column of width w with r runs contributes the
+// number of compositions of `rows` into r parts in [ceil(lo/w), floor(hi/w)],
+// and a DP over (columns, width used, runs used) sums the products.  Only
+// a <= cells / n can be a smallest area (n disjoint slices of area >= a).
+// Counts are exact in 128 bits (cfg5: ~6.1e29 < 2^100).
+using u128 = unsigned __int128;
+
+inline u128 count_candidates_dp(int cols, int rows, int n, int maxc, bool covering,
+                                const std::vector<int32_t>& tab, int threads = 0) {
+  const int max_area = cols * rows;
+  const int32_t* bm = tab.data();
+  const int rmax = std::min(n, rows);
+  // comp[hl][hh][r]: compositions of rows into r parts, each in [hl, hh]
+  const int R1 = rows + 1;
+  std::vector<u128> comp((size_t)R1 * R1 * (rmax + 1), 0);
+  for (int hl = 1; hl <= rows; ++hl)
+    for (int hh = hl; hh <= rows; ++hh) {
+      std::vector<u128> f((size_t)(rmax + 1) * R1, 0);  // f[r][sum]
+      f[0] = 1;
+      for (int r = 1; r <= rmax; ++r)
+        for (int sum = 0; sum <= rows; ++sum) {
+          u128 v = 0;
+          for (int h = hl; h <= hh && h <= sum; ++h) v += f[(size_t)(r - 1) * R1 + sum - h];
+          f[(size_t)r * R1 + sum] = v;
+        }
+      for (int r = 1; r <= rmax; ++r) comp[((size_t)hl * R1 + hh) * (rmax + 1) + r] = f[(size_t)r * R1 + rows];
+    }
+  auto N = [&](int lo, int hi) -> u128 {
+    if (lo > hi) return 0;
+    // nonzero column options (w, r, ways)
+    struct Opt { int w, r; u128 ways; };
+    std::vector<Opt> opts;
+    for (int w = 1; w <= cols; ++w) {
+      const int hl = std::max(1, (lo + w - 1) / w), hh = std::min(rows, hi / w);
+      if (hl > hh) continue;
+      for (int r = 1; r <= rmax; ++r) {
+        const u128 v = comp[((size_t)hl * R1 + hh) * (rmax + 1) + r];
+        if (v) opts.push_back({w, r, v});
+      }
+    }
+    if (opts.empty()) return 0;
+    // D[x][s] for j columns, rolled over j
+    const size_t S = (size_t)n + 1;
+    std::vector<u128> D((size_t)(cols + 1) * S, 0), E((size_t)(cols + 1) * S, 0);
+    D[0] = 1;
+    u128 total = 0;
+    for (int j = 1; j <= maxc; ++j) {
+      std::fill(E.begin(), E.end(), (u128)0);
+      for (int x = 0; x < cols; ++x)
+        for (int s = 0; s < n; ++s) {
+          const u128 d = D[(size_t)x * S + s];
+          if (!d) continue;
+          for (const Opt& o : opts) {
+            if (x + o.w > cols || s + o.r > n) continue;
+            E[(size_t)(x + o.w) * S + s + o.r] += d * o.ways;
+          }
+        }
+      std::swap(D, E);
+      for (int x = covering ? cols : 1; x <= cols; ++x) total += D[(size_t)x * S + n];
+    }
+    return total;
+  };
+  const int amax_min = max_area / std::max(n, 1);
+  if (threads <= 0) threads = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<u128> part((size_t)threads, 0);
+  std::vector<std::thread> th;
+  for (int t = 0; t < threads; ++t)
+    th.emplace_back([&, t] {
+      for (int a = 1 + t; a <= amax_min; a += threads) {
+        const int B = bm[a];
+        if (B < a) continue;
+        part[t] += N(a, B) - N(a + 1, B);
+      }
+    });
+  for (auto& x : th) x.join();
+  u128 tot = 0;
+  for (u128 v : part) tot += v;
+  return tot;
+}
+
+}  // namespace scb

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
   e.max_area = a.max_area;
   e.coverage = a.coverage;
   e.patho = a.pathological;
+  e.prune = a.prune;
   e.rstride = min(a.n, a.rows) + 1;
   e.bmax = s_tab;
   e.aneed = s_tab + A;
@@ -78,6 +79,10 @@ __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
   e.sfx = s_sfx;
   e.rt = a.rt;
   e.rs = a.rs;
+  e.lbr = a.lbr;
+  e.lbm = a.lbm;
+  e.inc = a.inc;
+  e.seed_inc = a.seed_inc;
 
   const int lane = threadIdx.x & 31;
   const int f = lane % FPW;
@@ -88,12 +93,21 @@ __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
   st.best_item = ~0ull;
   st.best_ord = ~0ull;
   st.best_sse = __longlong_as_double(0x7ff0000000000000ll);
+  if (a.resume) {  // second phase of a seeded launch: keep this lane's best
+    const LaneBest prev = a.lanes[(size_t)gwarp * 32 + lane];
+    st.best_t = prev.t;
+    st.best_item = prev.item;
+    st.best_ord = prev.ord;
+    st.best_sse = prev.sse;
+  }
   st.budget = STEP == 2 ? a.budget[f] : 0;
   st.count = 0;
+  st.scored = 0;
+  st.inc = ~0ull;
   st.snap = a.snaps + ((size_t)gwarp * 32 + lane) * kSnapBytes;
   for (;;) {
     uint32_t k = 0;
-    if (lane == 0) k = atomicAdd(a.counter, 1u);
+    if (lane == 0) k = a.k_begin + atomicAdd(a.counter, 1u);
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= a.n_items) break;
     const uint64_t item = (uint64_t)a.item_offset + (uint64_t)k * a.item_stride;
@@ -108,23 +122,61 @@ __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
   lb.ord = st.best_ord;
   a.lanes[(size_t)gwarp * 32 + lane] = lb;
   if (lane == 0 && st.count) atomicAdd(a.count_out, (unsigned long long)st.count);
+  unsigned long long sc = st.scored;
+  for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+  if (lane == 0 && sc) atomicAdd(a.scored_out, sc);
+}
+
+// ---- pruned mode: per-frame column lower bounds (search_walk.cuh) -------------
+__global__ void k_column_bounds(const uint64_t* __restrict__ rt, int fpw, int frames_in_group,
+                                int cols, int rows, int rmax, int rstride, uint64_t* lbr,
+                                uint64_t* lbm) {
+  const int nxw = cols * (cols + 1) / 2;
+  const int nyh = rows * (rows + 1) / 2;
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nxw * fpw) return;
+  const int xw = id / fpw, f = id % fpw;
+  if (f >= frames_in_group) return;
+  const size_t off = (size_t)xw * rstride * fpw + f;
+  column_bounds(rt, fpw, f, rows, xw * nyh, rmax, lbr + off, lbm + off, (size_t)fpw);
+}
+
+void column_bounds_launch(const uint64_t* rt, int fpw, int frames_in_group, int cols, int rows,
+                          int rmax, int rstride, uint64_t* lbr, uint64_t* lbm, cudaStream_t st) {
+  const int nxw = cols * (cols + 1) / 2;
+  const int threads = 128, total = nxw * fpw;
+  k_column_bounds<<<(total + threads - 1) / threads, threads, 0, st>>>(
+      rt, fpw, frames_in_group, cols, rows, rmax, rstride, lbr, lbm);
+  SCB_CUDA(cudaGetLastError());
 }
 
 // ---- finalize: per frame, reduce all lanes of that frame ---------------------
-__device__ __forceinline__ bool key_less(int step, const LaneBest& x, const LaneBest& y) {
+// Order: step key ((t) or (sse, t)), then work item, then the candidate's
+// position inside the item, read from the snapshots: widths, runs, heights
+// compared lexicographically -- the reference's enumeration order.  (Ordinals
+// are not dense under pruning, so the layout itself is the position.)
+__device__ __forceinline__ bool lane_less(int step, int n, const LaneBest& x, uint32_t xi,
+                                          const LaneBest& y, uint32_t yi,
+                                          const uint8_t* __restrict__ snaps) {
   if (step == 2) {
     if (x.sse < y.sse) return true;
     if (x.sse > y.sse) return false;
   }
   if (x.t != y.t) return x.t < y.t;
   if (x.item != y.item) return x.item < y.item;
-  return x.ord < y.ord;
+  const uint8_t* a = snaps + (size_t)xi * kSnapBytes;
+  const uint8_t* b = snaps + (size_t)yi * kSnapBytes;
+  const int len = 2 * SC_MAX_COLS + n;
+  for (int i = 0; i < len; ++i)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return xi < yi;
 }
 
-__global__ void k_finalize(int step, int fpw, int frames_in_group, uint32_t n_warps,
+__global__ void k_finalize(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
                            const LaneBest* __restrict__ lanes, const uint8_t* __restrict__ snaps,
-                           const unsigned long long* count, double lambda,
-                           FrameBest* __restrict__ out, uint64_t* __restrict__ budget_out) {
+                           const unsigned long long* count, const unsigned long long* scored,
+                           double lambda, FrameBest* __restrict__ out,
+                           uint64_t* __restrict__ budget_out) {
   const int f = blockIdx.x;
   if (f >= frames_in_group) return;
   __shared__ LaneBest sb[256];
@@ -136,18 +188,20 @@ __global__ void k_finalize(int step, int fpw, int frames_in_group, uint32_t n_wa
   const uint32_t n_lanes = n_warps * 32;
   for (uint32_t li = threadIdx.x * fpw + f; li < n_lanes; li += blockDim.x * fpw) {
     const LaneBest x = lanes[li];
-    if (x.item != ~0ull && key_less(step, x, best)) { best = x; bi = li; }
+    if (x.item == ~0ull) continue;
+    if (bi == 0xffffffffu || lane_less(step, n, x, li, best, bi, snaps)) { best = x; bi = li; }
   }
   sb[threadIdx.x] = best;
   si[threadIdx.x] = bi;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
     if (threadIdx.x < o) {
-      const LaneBest y = sb[threadIdx.x + o];
-      if (si[threadIdx.x + o] != 0xffffffffu &&
-          (si[threadIdx.x] == 0xffffffffu || key_less(step, y, sb[threadIdx.x]))) {
-        sb[threadIdx.x] = y;
-        si[threadIdx.x] = si[threadIdx.x + o];
+      const uint32_t yi = si[threadIdx.x + o];
+      if (yi != 0xffffffffu &&
+          (si[threadIdx.x] == 0xffffffffu ||
+           lane_less(step, n, sb[threadIdx.x + o], yi, sb[threadIdx.x], si[threadIdx.x], snaps))) {
+        sb[threadIdx.x] = sb[threadIdx.x + o];
+        si[threadIdx.x] = yi;
       }
     }
     __syncthreads();
@@ -162,6 +216,7 @@ __global__ void k_finalize(int step, int fpw, int frames_in_group, uint32_t n_wa
     o->item = sb[0].item;
     o->ord = sb[0].ord;
     o->count = *count;
+    o->scored = *scored;
     o->found = (win == 0xffffffffu) ? 0 : 1;
     if (budget_out && step == 1) {
       // budget = t_min * (1.0 + lambda)   (search.cpp:344)
@@ -226,12 +281,12 @@ void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStrea
   SCB_CUDA(cudaGetLastError());
 }
 
-void finalize_launch(int step, int fpw, int frames_in_group, uint32_t n_warps,
+void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
                      const LaneBest* lanes, const uint8_t* snaps,
-                     const unsigned long long* count, double lambda, FrameBest* out,
-                     uint64_t* budget_out, cudaStream_t st) {
-  k_finalize<<<frames_in_group, 256, 0, st>>>(step, fpw, frames_in_group, n_warps, lanes, snaps,
-                                              count, lambda, out, budget_out);
+                     const unsigned long long* count, const unsigned long long* scored,
+                     double lambda, FrameBest* out, uint64_t* budget_out, cudaStream_t st) {
+  k_finalize<<<frames_in_group, 256, 0, st>>>(step, n, fpw, frames_in_group, n_warps, lanes, snaps,
+                                              count, scored, lambda, out, budget_out);
   SCB_CUDA(cudaGetLastError());
 }
 

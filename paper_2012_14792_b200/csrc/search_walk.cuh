@@ -61,6 +61,9 @@ constexpr int kSnap = 96;          // snapshot bytes: W[16] R[16] H[64]
 // Read-only walk environment (tables live in shared memory on the GPU).
 struct WalkEnv {
   int cols, rows, n, nyh, max_area, coverage, patho, rstride;
+  int prune;  // exact branch-and-bound (SC_MODE_PRUNED): skip subtrees that
+              // cannot strictly improve this lane's best (step 1) or that
+              // exceed the budget (step 2); ordinals are then not dense
   const int32_t* bmax;    // [max_area + 1]
   const int32_t* aneed;   // [max_area + 1]
   const int32_t* mstar;   // [(cols+1) * (rows+1)]
@@ -70,6 +73,15 @@ struct WalkEnv {
   const int32_t* sfx;     // [rows+1]: yh(y, rows - y), the rectangle from row y to the bottom
   const uint64_t* rt;     // [NR][FPW] clamped f64 time bits of every rectangle
   const double* rs;       // [NR][FPW] SSE of every rectangle (step 2)
+  // pruned mode only: per-frame lower bounds on a column's slowest slice,
+  // lbr[(xw*rstride + r)*FPW + f] for exactly r runs and lbm[...] for any
+  // r' <= r (prefix minimum); inc[f] is the shared step-1 incumbent.
+  const uint64_t* lbr;
+  const uint64_t* lbm;
+  uint64_t* inc;
+  // incumbent frozen after the seed phase (or nullptr): its candidate precedes
+  // every item still to walk, so a tie with it can never win -> prune P >= it
+  const uint64_t* seed_inc;
 };
 
 // One lane's running first-in-order best and its candidate snapshot.
@@ -78,8 +90,57 @@ struct LaneState {
   double best_sse;
   uint64_t budget;  // step 2: t_min * (1 + lambda) as f64 bits
   uint64_t count;   // candidates enumerated (uniform over the warp)
+  uint64_t scored;  // candidates this lane actually scored
+  uint64_t inc;     // last seen shared incumbent (pruned step 1)
   uint8_t* snap;
 };
+
+// Shared incumbent: a candidate with time t exists for this frame, so no
+// candidate slower than t can win (equal ones still can: first in order).
+SCB_HD uint64_t incumbent_load(uint64_t* p) {
+#ifdef __CUDA_ARCH__
+  return *(volatile uint64_t*)p;
+#else
+  return *p;
+#endif
+}
+SCB_HD void incumbent_offer(uint64_t* p, uint64_t t) {
+#ifdef __CUDA_ARCH__
+  atomicMin((unsigned long long*)p, (unsigned long long)t);
+#else
+  if (t < *p) *p = t;
+#endif
+}
+
+// Lower bound on the slowest slice of a column (x0, w) cut into exactly r
+// runs, for every r <= rmax: min over all compositions (area constraint
+// relaxed) of the max run time, by a DP over rows.  lbr/lbm are written at
+// [r * stride] (lbm: prefix minimum over r).  Times are clamped f64 bits.
+SCB_HD void column_bounds(const uint64_t* rt, int fpw, int f, int rows, int base, int rmax,
+                          uint64_t* lbr, uint64_t* lbm, size_t stride) {
+  uint64_t prev[256], cur[256];
+  const uint64_t INF = ~0ull;
+  for (int y = 0; y <= rows; ++y) prev[y] = y == 0 ? 0 : INF;
+  uint64_t run_min = INF;
+  lbr[0] = INF;
+  lbm[0] = INF;
+  for (int r = 1; r <= rmax; ++r) {
+    for (int y = 0; y <= rows; ++y) {
+      uint64_t best = INF;
+      for (int y0 = r - 1; y0 < y; ++y0) {
+        if (prev[y0] == INF) continue;
+        const uint64_t v = rt[(size_t)(base + yh_of(rows, y0, y - y0)) * fpw + f];
+        const uint64_t m = prev[y0] > v ? prev[y0] : v;
+        if (m < best) best = m;
+      }
+      cur[y] = best;
+    }
+    lbr[(size_t)r * stride] = cur[rows];
+    run_min = cur[rows] < run_min ? cur[rows] : run_min;
+    lbm[(size_t)r * stride] = run_min;
+    for (int y = 0; y <= rows; ++y) prev[y] = cur[y];
+  }
+}
 
 // Area thresholds of a partial candidate: a further slice of area x keeps it
 // admissible iff T2 <= x <= T1 (and x <= bmax[x]); T1 = bmax[amin] (+inf
@@ -190,14 +251,30 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     }
     return tot;
   };
+  // can a subtree whose fixed slices already reach time P still win?
+  const uint64_t seed_inc = (STEP == 1 && e.prune && e.seed_inc) ? e.seed_inc[f] : ~0ull;
+  auto viable = [&](uint64_t P) -> bool {
+    return !e.prune ||
+           (STEP == 1 ? (P < st.best_t && P <= st.inc && P < seed_inc) : (P <= st.budget));
+  };
+  if (STEP == 1 && e.prune) st.inc = incumbent_load(e.inc + f);
+  // lower bound of column (x0, w) with r runs (exact r) / any r' <= r
+  auto lb_r = [&](int x0, int w, int r) -> uint64_t {
+    return e.lbr[((size_t)xw_of(cols, x0, w) * e.rstride + r) * FPW + f];
+  };
+  auto lb_m = [&](int x0, int w, int r) -> uint64_t {
+    return e.lbm[((size_t)xw_of(cols, x0, w) * e.rstride + r) * FPW + f];
+  };
   // score one candidate (strict comparisons keep the first in order)
   auto score = [&](uint64_t t, uint64_t o, int lr, int lh, int lrest) {
+    ++st.scored;
     if (STEP == 1) {
       if (t < st.best_t) {
         st.best_t = t;
         st.best_item = item;
         st.best_ord = o;
         take_snapshot(lr, lh, lrest);
+        if (e.prune) incumbent_offer(e.inc + f, t);
       }
     } else if (t <= st.budget) {
       const double s = layout_sse(lr, lh, lrest);
@@ -217,9 +294,11 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   //      cannot complete and are skipped.
   const int rmax_c = imin(e.n - c + 1, rows);
   int WL[SC_MAX_COLS + 1], WH[SC_MAX_COLS + 1];
+  uint64_t PW[SC_MAX_COLS + 1];  // pruned mode: max of the columns' lower bounds
   X0[0] = 0;
   WL[0] = 1;
   WH[0] = e.max_area;
+  PW[0] = 0;
   bool ok = (e.n >= c) && (e.n <= c * rows);
   for (int i = 0; i < d && ok; ++i) {
     W[i] = wi.w[i];
@@ -227,6 +306,10 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     WL[i + 1] = imax(WL[i], e.ilo[W[i] * e.rstride + rmax_c]);
     WH[i + 1] = imin(WH[i], W[i] * rows);
     ok = WL[i + 1] <= WH[i + 1];
+    if (e.prune) {
+      PW[i + 1] = umax64(PW[i], lb_m(X0[i], W[i], rmax_c));
+      ok = ok && viable(PW[i + 1]);
+    }
   }
   int pos = d;
   const bool fixed_widths = d == c;
@@ -248,6 +331,10 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         const int nL = imax(WL[pos], e.ilo[wv * e.rstride + rmax_c]);
         const int nH = imin(WH[pos], wv * rows);
         if (nL > nH) continue;
+        if (e.prune) {
+          PW[pos + 1] = umax64(PW[pos], lb_m(X0[pos], wv, rmax_c));
+          if (!viable(PW[pos + 1])) continue;
+        }
         X0[pos + 1] = X0[pos] + wv;
         WL[pos + 1] = nL;
         WH[pos + 1] = nH;
@@ -261,12 +348,15 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       if (!got) break;
     }
     SCB_STAT(widths);
+    if (STEP == 1 && e.prune) st.inc = incumbent_load(e.inc + f);
     // ---- runs DFS (lex, search.cpp:145-161).  The skeleton (widths, runs)
     //      has an admissible completion iff the column windows
     //      I(w, r) = [aneed[w*ceil(rows/r)], w*floor(rows/r)] intersect; I
     //      slides down as r grows, so the feasible r of a position form one
     //      contiguous range.
     int RL[SC_MAX_COLS], RH[SC_MAX_COLS], SL[SC_MAX_COLS];
+    uint64_t PR[SC_MAX_COLS + 1];  // pruned mode: widths bound, tightened per exact r
+    PR[0] = e.prune ? PW[c] : 0;
     int rp = 0;
     RL[0] = 1;
     RH[0] = e.max_area;
@@ -296,6 +386,10 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       R[rp] = r;
       const int nL = imax(RL[rp], lo), nH = imin(RH[rp], hi);
       if (nL > nH) continue;
+      if (e.prune) {
+        PR[rp + 1] = umax64(PR[rp], lb_r(X0[rp], W[rp], r));
+        if (!viable(PR[rp + 1])) continue;
+      }
       if (rp < c - 1) {
         SL[rp + 1] = SL[rp] - r;
         RL[rp + 1] = nL;
@@ -308,6 +402,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       //      [win_lo, bmax[nH]] for a window a in [nL, nH]
       const int win_lo = nL, win_hi = e.bmax[nH];
       SCB_STAT(skeletons);
+      if (STEP == 1 && e.prune) st.inc = incumbent_load(e.inc + f);
       int amin = kBigArea, amax = 0;
       int run = 0, nl = 0;
       for (int i = 0; i < c; ++i) {
@@ -331,10 +426,11 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       for (int i = 0; i < c; ++i)
         if (R[i] == 1) P = umax64(P, rt_at(X0[i], W[i], 0, rows));
       if (nl == 0) {  // the skeleton is a single candidate
-        if (slot == 0) score(P, ord, -1, 0, 0);
+        if (slot == 0 && viable(P)) score(P, ord, -1, 0, 0);
         ord += 1;
         continue;
       }
+      if (!viable(P)) continue;
       // ---- heights DFS over the multi-run columns (search.cpp:163-190)
       int l = 0;
       const bool leaf_now = (nl == 1);
@@ -392,6 +488,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             curH[ridx + 1] = (uint8_t)(rows_left - h);
             Pn = umax64(Pn, rt[(size_t)(lb + e.sfx[y0 + h]) * FPW + f]);
           }
+          if (!viable(Pn)) continue;
           const int nxt = l + 1;
           const bool new_col = Lrun[nxt] == 0;
           const int y0n = new_col ? 0 : y0 + h;
@@ -431,7 +528,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
 #if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
           ++g_stats.leafr[R[i]];
 #endif
-          if (lo + slot <= hi) {
+          if (lo + slot <= hi && viable(Pl)) {
             // rect 1 = (y0l, h) advances by +1 per h; rect 2 = (y0l+h,
             // rows_left-h) by rows_left-h-1 (yh numbering); lanes step h by J.
             int h = lo + slot;

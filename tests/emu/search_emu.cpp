@@ -16,7 +16,7 @@
 using namespace scb;
 
 extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols, int coverage,
-                          int step, int frames, const double* rect_time /*[F][NR]*/,
+                          int step, int prune, int frames, const double* rect_time /*[F][NR]*/,
                           const double* rect_sse /*[F][NR] or NULL*/, const double* budget,
                           int warps, size_t item_target, int item_offset, int item_stride,
                           double* out_t, double* out_sse, uint64_t* out_count,
@@ -55,6 +55,17 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       rt[r * fpw + f] = (t > 0.0) ? bits : 0;
       if (rect_sse) rs[r * fpw + f] = rect_sse[(size_t)f * nr + r];
     }
+  // pruned mode: per-frame column lower bounds, shared incumbents
+  const int nxw = cols * (cols + 1) / 2;
+  std::vector<uint64_t> lbr((size_t)nxw * rstride * fpw, 0), lbm((size_t)nxw * rstride * fpw, 0);
+  std::vector<uint64_t> inc(fpw, ~0ull);
+  if (prune)
+    for (int xw = 0; xw < nxw; ++xw)
+      for (int f = 0; f < frames; ++f) {
+        const size_t off = (size_t)xw * rstride * fpw + f;
+        column_bounds(rt.data(), fpw, f, rows, xw * nyh, rstride - 1, lbr.data() + off,
+                      lbm.data() + off, (size_t)fpw);
+      }
   WalkEnv e;
   e.cols = cols;
   e.rows = rows;
@@ -63,6 +74,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.max_area = cols * rows;
   e.coverage = coverage;
   e.patho = patho ? 1 : 0;
+  e.prune = prune;
   e.rstride = rstride;
   e.bmax = tab.data();
   e.aneed = tab.data() + A;
@@ -73,6 +85,17 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.sfx = sfx.data();
   e.rt = rt.data();
   e.rs = rs.data();
+  e.lbr = lbr.data();
+  e.lbm = lbm.data();
+  e.inc = inc.data();
+  e.seed_inc = nullptr;
+  std::vector<uint64_t> frozen(fpw, ~0ull);
+  // seeded pruned step 1 like api.cu: phase A = the first seed_items items
+  size_t seed_items = 0;
+  for (const WorkItem& wi : items) {
+    if (wi.c > 1) break;
+    ++seed_items;
+  }
 
   std::vector<LaneState> st((size_t)warps * 32);
   std::vector<uint8_t> snaps((size_t)warps * 32 * kSnap, 0);
@@ -84,6 +107,8 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       s.best_ord = ~0ull;
       s.best_sse = INFINITY;
       s.count = 0;
+      s.scored = 0;
+      s.inc = ~0ull;
       s.snap = &snaps[((size_t)wp * 32 + l) * kSnap];
       s.budget = 0;
       if (step == 2 && (l % fpw) < frames) {
@@ -94,7 +119,15 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       }
     }
   size_t kk = 0;
+  const size_t mine = items.size() > (size_t)item_offset
+                          ? (items.size() - item_offset + item_stride - 1) / item_stride
+                          : 0;
+  const size_t seed_local = (prune && step == 1) ? std::min(mine, seed_items) : 0;
   for (size_t it = (size_t)item_offset; it < items.size(); it += (size_t)item_stride, ++kk) {
+    if (prune && step == 1 && kk == seed_local && seed_local > 0) {  // phase B begins
+      frozen = inc;
+      e.seed_inc = frozen.data();
+    }
     const int wp = (int)(kk % (size_t)warps);
     for (int l = 0; l < 32; ++l) {
       LaneState& s = st[(size_t)wp * 32 + l];
@@ -120,12 +153,22 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       if (step == 2 && s.best_sse != b.best_sse) less = s.best_sse < b.best_sse;
       else if (s.best_t != b.best_t) less = s.best_t < b.best_t;
       else if (s.best_item != b.best_item) less = s.best_item < b.best_item;
-      else less = s.best_ord < b.best_ord;
+      else {  // position inside the item: the layout, lexicographically (k_finalize)
+        less = false;
+        for (int j = 0; j < 2 * 16 + n; ++j)
+          if (s.snap[j] != b.snap[j]) {
+            less = s.snap[j] < b.snap[j];
+            break;
+          }
+      }
       if (less) win = i;
     }
     out_found[f] = win >= 0;
     uint64_t cnt = 0;
     for (int wp = 0; wp < warps; ++wp) cnt += st[(size_t)wp * 32].count;
+    if (prune) {  // pruned walks: the exact DP count (api.cu does the same)
+      cnt = (uint64_t)count_candidates_dp(cols, rows, n, maxc, coverage == 1, tab, 1);
+    }
     out_count[f] = cnt;
     if (win >= 0) {
       std::memcpy(&out_t[f], &st[win].best_t, 8);

@@ -154,7 +154,8 @@ def test_synthetic_generator_is_deterministic():
 
 
 def test_shard_merge_picks_first_in_order():
-    """sc_shard_merge: per frame, min (key, item, ordinal); counts summed."""
+    """sc_shard_merge: per frame, min (key, item, position in the item = the
+    layout's lex order); counts summed."""
     from paper_2012_14792_b200._abi import SearchResult, ShardBest, check, lib
     world, F = 3, 2
     recs = (ShardBest * (world * F))()
@@ -171,5 +172,5 @@ def test_shard_merge_picks_first_in_order():
         res[f].argmin.n_slices = 1
     check(lib().sc_shard_merge(1, world, F, C.cast(recs, C.c_void_p), C.cast(res, C.c_void_p)))
     assert res[0].argmin.col_widths[0] == 2  # rank 1: t=5, item 4 < 10
-    assert res[1].argmin.col_widths[0] == 3  # rank 2: t=8, item 30, ord 0 < 1
+    assert res[1].argmin.col_widths[0] == 2  # t=8, item 30 tie: layout [2] < [3]
     assert res[0].candidates_step1 == 303

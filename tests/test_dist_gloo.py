@@ -38,7 +38,7 @@ def _problem(step):
     return cols, rows, n, mc, k, lam, F, est, luma
 
 
-def _worker(rank, world, port, step, out_dir):
+def _worker(rank, world, port, step, prune, out_dir):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -60,7 +60,7 @@ def _worker(rank, world, port, step, out_dir):
                            (1.0 + lam) for f in range(F)])
     t, sse, cnt, snap, found, item, ordn = e.search(cols, rows, n, k, mc, 0, step, rt, rs, budget,
                                                     item_target=64, offset=rank, stride=world,
-                                                    full=True)
+                                                    full=True, prune=prune)
     mine = (ShardBest * F)()
     for f in range(F):
         s = mine[f]
@@ -68,7 +68,8 @@ def _worker(rank, world, port, step, out_dir):
         s.key_sse = float(sse[f])
         s.item = int(item[f]) if found[f] else (1 << 64) - 1
         s.ord = int(ordn[f])
-        s.count = int(cnt[f])
+        # pruned walks report the global DP count from rank 0 only (sc_shard_export)
+        s.count = int(cnt[f]) if (not prune or rank == 0) else 0
         s.layout.n_cols = int(np.count_nonzero(snap[f][:16]))
         for i in range(16):
             s.layout.col_widths[i] = int(snap[f][i])
@@ -108,16 +109,17 @@ def _worker(rank, world, port, step, out_dir):
                 ok = (res[f].t_best_us == r.t_best_us and res[f].sse_best == r.sse_best and
                       got == exp and res[f].candidates_step2 == r.candidates_step2)
             lines.append(f"{f} {int(ok)}")
-        open(os.path.join(out_dir, f"step{step}.txt"), "w").write("\n".join(lines))
+        open(os.path.join(out_dir, f"step{step}_{prune}.txt"), "w").write("\n".join(lines))
     dist.barrier()
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("prune", [0, 1])
 @pytest.mark.parametrize("step", [1, 2])
-def test_candidate_space_sharding_gloo(tmp_path, emu, step):
+def test_candidate_space_sharding_gloo(tmp_path, emu, step, prune):
     port = _free_port()
-    mp.spawn(_worker, args=(2, port, step, str(tmp_path)), nprocs=2, join=True)
-    res = open(tmp_path / f"step{step}.txt").read().split("\n")
+    mp.spawn(_worker, args=(2, port, step, prune, str(tmp_path)), nprocs=2, join=True)
+    res = open(tmp_path / f"step{step}_{prune}.txt").read().split("\n")
     assert len(res) == 4 and all(line.endswith(" 1") for line in res), res
 
 

@@ -14,8 +14,9 @@ def _case(rng, max_cells=9):
     return cols, rows, n
 
 
+@pytest.mark.parametrize("prune", [0, 1])
 @pytest.mark.parametrize("seed", range(4))
-def test_step1_vs_oracle(emu, oracle, seed):
+def test_step1_vs_oracle(emu, oracle, seed, prune):
     from emu.emu import Emu
     rng = np.random.default_rng(seed)
     for trial in range(60):
@@ -30,7 +31,7 @@ def test_step1_vs_oracle(emu, oracle, seed):
         rt = np.stack([oracle.rect_times(est[f], cols, rows) for f in range(F)])
         tgt = int(rng.choice([1, 16, 100000]))
         t, _, cnt, snap, found = emu.search(cols, rows, n, k, mc, cov, 1, rt, item_target=tgt,
-                                            warps=int(rng.integers(1, 5)))
+                                            warps=int(rng.integers(1, 5)), prune=prune)
         for f in range(F):
             st, r = oracle.search(cols * 64, rows * 64, 64, est[f], None, n, 0.0, k, mc, cov, 1)
             if st:
@@ -42,8 +43,9 @@ def test_step1_vs_oracle(emu, oracle, seed):
             assert Emu.slices(snap[f], n, rows) == r.argmin1.slices(rows), ctx
 
 
+@pytest.mark.parametrize("prune", [0, 1])
 @pytest.mark.parametrize("seed", range(3))
-def test_step2_vs_oracle(emu, oracle, seed):
+def test_step2_vs_oracle(emu, oracle, seed, prune):
     from emu.emu import Emu
     rng = np.random.default_rng(100 + seed)
     for trial in range(40):
@@ -67,13 +69,29 @@ def test_step2_vs_oracle(emu, oracle, seed):
         if any(st != 0 for st, _ in res):
             continue
         budget = np.array([r.t_min_us * (1.0 + lam) for _, r in res])
-        t, sse, cnt, snap, found = emu.search(cols, rows, n, k, mc, cov, 2, rt, rs, budget)
+        t, sse, cnt, snap, found = emu.search(cols, rows, n, k, mc, cov, 2, rt, rs, budget,
+                                              prune=prune)
         for f in range(F):
             r = res[f][1]
             ctx = (seed, trial, f, cols, rows, n, mc, k, cov, lam, F)
             assert t[f] == r.t_best_us and sse[f] == r.sse_best, ctx
             assert cnt[f] == r.candidates_step2, ctx
             assert Emu.slices(snap[f], n, rows) == r.best.slices(rows), ctx
+
+
+def test_dp_counts_match_enumeration(emu, oracle):
+    """The exact counting DP (pruned mode's counters) == enumerated counts,
+    and the survey's reference-enumerated ladder values."""
+    rng = np.random.default_rng(9)
+    for _ in range(40):
+        cols, rows = int(rng.integers(1, 8)), int(rng.integers(1, 8))
+        n = int(rng.integers(1, min(9, cols * rows) + 1))
+        mc = int(rng.integers(0, 5))
+        k = float(rng.choice([3.0, 2.5, 2.0, 1.5]))
+        cov = int(rng.integers(0, 2))
+        rt = np.ones((1, cols * (cols + 1) // 2 * (rows * (rows + 1) // 2)))
+        _, _, cnt, _, _ = emu.search(cols, rows, n, k, mc, cov, 1, rt, prune=1)
+        assert cnt[0] == oracle.count(cols, rows, n, k, mc, cov)
 
 
 def test_baseline_grid_counts(emu, oracle):

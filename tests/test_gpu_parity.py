@@ -78,14 +78,16 @@ def _rec3(rec):
     return np.stack([rec["count"], rec["sum"], rec["sumsq"]], axis=1)
 
 
-def test_search_small_golden(part):
-    """200 reference-generated instances: step 1 and step 2, bit-exact."""
+@pytest.mark.parametrize("mode", [0, 1])
+def test_search_small_golden(part, mode):
+    """200 reference-generated instances: step 1 and step 2, bit-exact, in the
+    exhaustive and the exact pruned mode."""
     from paper_2012_14792_b200 import RECORD_DTYPE, CtuGrid, SearchConfig, SlicecraftError
     cases = json.load(open(os.path.join(GOLDEN, "search_small.json")))
     for i, c in enumerate(cases):
         g = CtuGrid.make(c["w"], c["h"], c["ctu"])
         cfg = SearchConfig(n_slices=c["n"], lambda_=c["lambda"], k_area=c["k"],
-                           max_tile_cols=c["max_tile_cols"])
+                           max_tile_cols=c["max_tile_cols"], mode=mode)
         rec = np.zeros(g.cell_count(), RECORD_DTYPE)
         r3 = np.array(c["records"], dtype=np.uint64)
         rec["count"], rec["sum"], rec["sumsq"] = r3[:, 0], r3[:, 1], r3[:, 2]
@@ -105,9 +107,10 @@ def test_search_small_golden(part):
         assert o.candidates_step2 == c["candidates_step2"], i
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("coverage", [0, 1])
 @pytest.mark.parametrize("seed", range(6))
-def test_search_random_vs_oracle(part, oracle, coverage, seed):
+def test_search_random_vs_oracle(part, oracle, coverage, seed, mode):
     from paper_2012_14792_b200 import CtuGrid, SearchConfig, SlicecraftError
     rng = np.random.default_rng(seed + 100 * coverage)
     for trial in range(12):
@@ -123,7 +126,8 @@ def test_search_random_vs_oracle(part, oracle, coverage, seed):
             est = np.round(est)
         luma = rng.integers(0, 1024, size=(F, g.frame_height, g.frame_width)).astype(np.uint16)
         rec = part.ctu_stats_batch(luma, 64)
-        cfg = SearchConfig(n_slices=n, lambda_=lam, k_area=k, max_tile_cols=mc, coverage=coverage)
+        cfg = SearchConfig(n_slices=n, lambda_=lam, k_area=k, max_tile_cols=mc, coverage=coverage,
+                           mode=mode)
         exp = [oracle.search(g.frame_width, g.frame_height, 64, est[f], _rec3(rec[f]), n, lam, k,
                              mc, coverage, 3) for f in range(F)]
         if any(st != 0 for st, _ in exp):
@@ -175,11 +179,13 @@ def test_min_time_search_api(part, oracle):
 def _config_inputs(ci, frames):
     from paper_2012_14792_b200 import workloads as wl
     w = wl.WORKLOADS[ci]
+    frames = w.frames if frames is None else frames
     return w, wl.cost_trace(w, frames=frames), wl.synth_luma(w, frames=frames)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("ci", [1, 2, 3])
-def test_baseline_configs_vs_reference_golden(part, ci):
+def test_baseline_configs_vs_reference_golden(part, ci, mode):
     """cfg1 (all), cfg2 (POC 1..4), cfg3 (POC 1) against the reference itself."""
     import hashlib
     from paper_2012_14792_b200 import workloads as wl
@@ -189,7 +195,7 @@ def test_baseline_configs_vs_reference_golden(part, ci):
     g = w.grid()
     rec = np.zeros((F, g.cell_count()), dtype=__import__(
         "paper_2012_14792_b200").RECORD_DTYPE)
-    res = part.partition_frames(g, luma, tr.est, w.cfg(), records_out=rec)
+    res = part.partition_frames(g, luma, tr.est, w.cfg(mode=mode), records_out=rec)
     for fr in gold["frames"]:
         p = fr["poc"]
         r3 = np.ascontiguousarray(_rec3(rec[p - 1]), dtype=np.uint64)
@@ -235,6 +241,55 @@ def test_cfg3_counts_all_frames(part):
         assert r.candidates_step1 == r.candidates_step2 == 66007331
         assert r.t_best_us <= r.t_min_us * (1.0 + 0.0)  # lambda = 0: t_best == t_min
         assert r.t_best_us == r.t_min_us
+
+
+# ---- configs 4 and 5 (exact pruned mode) ---------------------------------------------
+# Survey-verified exact candidate counts (reference enumeration ladder + the
+# counting DP): the reference's own counters.
+CFG_COUNTS = {4: 5362975262506, 5: 610308283606383278175018310268}
+
+
+def _check_result_properties(oracle, w, g, est, rec, r, lam=0.0):
+    """Size-independent checks of one frame's result: the returned layouts are
+    admissible, their times / SSE recomputed by the CPU oracle from its own
+    rectangle tables equal t_min / t_best / sse_best, t_best is within budget."""
+    from paper_2012_14792_b200.partitioner import Partition
+    nyh = g.rows * (g.rows + 1) // 2
+    rt = oracle.rect_times(est, g.cols, g.rows)
+    rs = oracle.rect_sse(w.width, w.height, w.ctu, _rec3(rec))
+
+    def rid(s):
+        return (s[0] * g.cols - s[0] * (s[0] - 1) // 2 + s[2] - 1) * nyh + \
+            (s[1] * g.rows - s[1] * (s[1] - 1) // 2 + s[3] - 1)
+    for L, tref in ((r.argmin, r.t_min_us), (r.best, r.t_best_us)):
+        rects = Partition.from_layout(g, L).rects()
+        assert len(rects) == w.n_slices
+        areas = [s[2] * s[3] for s in rects]
+        assert 3.0 * min(areas) > max(areas)
+        t = 0.0
+        for s in rects:
+            t = max(t, rt[rid(s)])
+        assert t == tref
+    sse = 0.0
+    for s in Partition.from_layout(g, r.best).rects():
+        sse += rs[rid(s)]
+    assert sse == r.sse_best
+    assert r.t_best_us <= r.t_min_us * (1.0 + lam)
+
+
+@pytest.mark.parametrize("ci", [4, 5])
+def test_cfg4_cfg5_pruned(part, oracle, ci):
+    from paper_2012_14792_b200 import RECORD_DTYPE
+    w, tr, luma = _config_inputs(ci, None)
+    g = w.grid()
+    F = w.frames
+    rec = np.zeros((F, g.cell_count()), dtype=RECORD_DTYPE)
+    res = part.partition_frames(g, luma, tr.est, w.cfg(mode=1), records_out=rec)
+    for f in range(F):
+        r = res[f]
+        cnt = r.candidates_step1 | (r.candidates_step1_hi << 64)
+        assert cnt == CFG_COUNTS[ci] == (r.candidates_step2 | (r.candidates_step2_hi << 64))
+        _check_result_properties(oracle, w, g, tr.est[f], rec[f], r)
 
 
 # ---- error behaviour -----------------------------------------------------------------
