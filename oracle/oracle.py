@@ -97,6 +97,19 @@ class Oracle:
                                t_min, C.byref(r))
         return st, r
 
+    def search_pruned(self, fw, fh, ctu, est, records, n, lam=0.0, k=3.0, max_cols=0,
+                      coverage=0, step=3, t_min=0.0):
+        """Independent branch-and-bound restatement (counts not enumerated)."""
+        r = OrcResult()
+        e = np.ascontiguousarray(est, dtype=np.float64)
+        rec = None if records is None else np.ascontiguousarray(records, dtype=np.uint64).reshape(-1)
+        self.L.orc_search_pruned.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                             C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                             C.c_int, C.c_double, C.c_void_p]
+        st = self.L.orc_search_pruned(fw, fh, ctu, _p(e), _p(rec), n, lam, k, max_cols, coverage,
+                                      step, t_min, C.byref(r))
+        return st, r
+
     def count(self, cols, rows, n, k=3.0, max_cols=0, coverage=0) -> int:
         out = C.c_uint64()
         self.L.orc_count.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,

@@ -437,3 +437,202 @@ int orc_count(int cols, int rows, int n, double k, int max_tile_cols, int covera
   free(d);
   return ORC_OK;
 }
+
+/* ---- exact branch-and-bound restatement (configs 4/5) ---------------------
+ * The reference DFS (rec_widths / rec_runs / rec_heights, search.cpp:133-190)
+ * in the reference's order, scoring like run_step1 / the step-2 reduction
+ * (search.cpp:283-289, 386-394), but skipping a subtree when no candidate in
+ * it can win under the reference's strict comparisons:
+ *   step 1: a lower bound LB >= best_t (ties later in order never replace),
+ *   step 2: LB > budget (infeasible).
+ * LB is the running max of the slices already fixed, tightened at the widths
+ * and runs levels by colLB(x0, w, r): the minimum over all compositions of the
+ * column into r runs of its slowest run (area constraint relaxed), from a DP
+ * over rows.  Written independently of the GPU walk; counts are not
+ * enumerated (the caller takes them from the exact DP). */
+typedef struct {
+  dfs_t d;
+  double* lb;   /* lb[(xw * (rmax+1) + r)] exact r */
+  double* lbm;  /* prefix min over r' <= r */
+  int rmax;
+} bb_t;
+
+static double rt_clamped(const dfs_t* d, int x0, int y0, int w, int h) {
+  double v = rect_sum(d->sat, d->cols, x0, y0, w, h);
+  return v > 0.0 ? v : 0.0; /* layout_time's max from 0.0 (search.cpp:78-81) */
+}
+
+static void bb_bounds(bb_t* b) {
+  dfs_t* d = &b->d;
+  int cols = d->cols, rows = d->rows, R = b->rmax;
+  int nxw = cols * (cols + 1) / 2;
+  b->lb = malloc(sizeof(double) * nxw * (R + 1));
+  b->lbm = malloc(sizeof(double) * nxw * (R + 1));
+  double* prev = malloc(sizeof(double) * (rows + 1));
+  double* cur = malloc(sizeof(double) * (rows + 1));
+  for (int x0 = 0; x0 < cols; ++x0)
+    for (int w = 1; w <= cols - x0; ++w) {
+      long xw = xw_index(cols, x0, w);
+      for (int y = 0; y <= rows; ++y) prev[y] = y == 0 ? 0.0 : INFINITY;
+      double runmin = INFINITY;
+      b->lb[xw * (R + 1)] = INFINITY;
+      b->lbm[xw * (R + 1)] = INFINITY;
+      for (int r = 1; r <= R; ++r) {
+        for (int y = 0; y <= rows; ++y) {
+          double best = INFINITY;
+          for (int y0 = 0; y0 < y; ++y0) {
+            if (prev[y0] == INFINITY) continue;
+            double v = rt_clamped(d, x0, y0, w, y - y0);
+            double m = prev[y0] > v ? prev[y0] : v;
+            if (m < best) best = m;
+          }
+          cur[y] = best;
+        }
+        b->lb[xw * (R + 1) + r] = cur[rows];
+        if (cur[rows] < runmin) runmin = cur[rows];
+        b->lbm[xw * (R + 1) + r] = runmin;
+        memcpy(prev, cur, sizeof(double) * (rows + 1));
+      }
+    }
+  free(prev);
+  free(cur);
+}
+
+static int bb_dead(const bb_t* b, double lbv) {
+  const dfs_t* d = &b->d;
+  return d->step == 1 ? !(lbv < d->best_t) : (lbv > d->budget);
+}
+
+static void bb_heights(bb_t* b, int col, int run, int rows_left, int64_t amin, int64_t amax,
+                       int x, double P) {
+  dfs_t* d = &b->d;
+  if (col == d->c) {
+    leaf(d);
+    return;
+  }
+  int runs = d->r[col];
+  if (run == runs) {
+    bb_heights(b, col + 1, 0, d->rows, amin, amax, x + d->w[col], P);
+    return;
+  }
+  int w = d->w[col], runs_left = runs - run;
+  int lo = runs_left == 1 ? rows_left : 1, hi = rows_left - (runs_left - 1);
+  int y0 = d->rows - rows_left;
+  for (int h = lo; h <= hi; ++h) {
+    int64_t area = (int64_t)w * h;
+    int64_t na = amin < area ? amin : area, nx = amax > area ? amax : area;
+    if (!(d->k * (double)na > (double)nx)) continue;
+    double v = rt_clamped(d, x, y0, w, h);
+    double Pn = P > v ? P : v;
+    if (bb_dead(b, Pn)) continue;
+    d->h[d->nh++] = h;
+    bb_heights(b, col, run + 1, rows_left - h, na, nx, x, Pn);
+    d->nh--;
+  }
+}
+
+static void bb_runs(bb_t* b, int col, int slices_left, int x, double PR) {
+  dfs_t* d = &b->d;
+  if (col == d->c) {
+    if (slices_left == 0) {
+      d->nh = 0;
+      bb_heights(b, 0, 0, d->rows, INT64_MAX, 0, 0, 0.0);
+    }
+    return;
+  }
+  int after = d->c - col - 1;
+  int lo = slices_left - after * d->rows; if (lo < 1) lo = 1;
+  int hi = slices_left - after; if (hi > d->rows) hi = d->rows;
+  long xw = xw_index(d->cols, x, d->w[col]);
+  for (int r = lo; r <= hi; ++r) {
+    double v = r <= b->rmax ? b->lb[xw * (b->rmax + 1) + r] : 0.0;
+    double P = PR > v ? PR : v;
+    if (bb_dead(b, P)) continue;
+    d->r[col] = r;
+    bb_runs(b, col + 1, slices_left - r, x + d->w[col], P);
+  }
+}
+
+static void bb_widths(bb_t* b, int col, int cols_left, double PW, int rmax_c) {
+  dfs_t* d = &b->d;
+  if (col == d->c) {
+    if (d->coverage && cols_left != 0) return;
+    bb_runs(b, 0, d->n, 0, PW);
+    return;
+  }
+  int max_w = cols_left - (d->c - col - 1);
+  int x = d->cols - cols_left;
+  for (int w = 1; w <= max_w; ++w) {
+    double v = b->lbm[xw_index(d->cols, x, w) * (b->rmax + 1) + rmax_c];
+    double P = PW > v ? PW : v;
+    if (bb_dead(b, P)) continue;
+    d->w[col] = w;
+    bb_widths(b, col + 1, cols_left - w, P, rmax_c);
+  }
+}
+
+static void bb_generator(bb_t* b) {
+  dfs_t* d = &b->d;
+  int maxc = d->n;
+  if (d->ncols_max < maxc) maxc = d->ncols_max;
+  if (d->cols < maxc) maxc = d->cols;
+  for (int c = 1; c <= maxc; ++c) {
+    d->c = c;
+    int rmax_c = d->n - c + 1;
+    if (rmax_c > d->rows) rmax_c = d->rows;
+    if (rmax_c > b->rmax) rmax_c = b->rmax;
+    bb_widths(b, 0, d->cols, 0.0, rmax_c);
+  }
+}
+
+/* Same contract as orc_search (steps, outputs), counts left at 0. */
+int orc_search_pruned(int fw, int fh, int ctu, const double* est, const uint64_t* rec, int n,
+                      double lambda, double k, int max_tile_cols, int coverage, int step,
+                      double t_min_in, orc_result* out) {
+  int cols, rows;
+  int st = grid_make(fw, fh, ctu, &cols, &rows);
+  if (st) return st;
+  st = check_cfg(n, lambda, k, max_tile_cols);
+  if (st) return st;
+  if (n > cols * rows) return ORC_ERR_GEOMETRY;
+  if (n > ORC_MAX_SLICES) return ORC_ERR_SIZE;
+  memset(out, 0, sizeof(*out));
+  bb_t* b = calloc(1, sizeof(bb_t));
+  dfs_t* d = &b->d;
+  double* sat = malloc(sizeof(double) * (cols + 1) * (rows + 1));
+  sat_f64(est, cols, rows, sat);
+  uint64_t* usat = NULL;
+  d->cols = cols; d->rows = rows; d->n = n; d->k = k; d->coverage = coverage;
+  d->ncols_max = max_tile_cols > 0 ? max_tile_cols : n;
+  d->sat = sat;
+  b->rmax = n < rows ? n : rows;
+  bb_bounds(b);
+  double t_min = t_min_in;
+  if (step & 1) {
+    d->step = 1; d->found = 0; d->best_t = INFINITY;
+    bb_generator(b);
+    if (!d->found) { st = ORC_ERR_NO_CANDIDATE; goto done; }
+    out->t_min_us = d->best_t;
+    out->argmin1 = d->best;
+    t_min = d->best_t;
+  }
+  if (step & 2) {
+    st = orc_texture_validate(fw, fh, ctu, rec);
+    if (st) goto done;
+    usat = malloc(sizeof(uint64_t) * 3 * (cols + 1) * (rows + 1));
+    sat_u64(rec, cols, rows, usat);
+    d->usat = usat;
+    d->step = 2; d->found = 0;
+    d->best_t = INFINITY; d->best_sse = INFINITY;
+    d->budget = t_min * (1.0 + lambda);
+    bb_generator(b);
+    if (!d->found) { st = ORC_ERR_NO_CANDIDATE; goto done; }
+    if (!(step & 1)) out->t_min_us = t_min;
+    out->t_best_us = d->best_t;
+    out->sse_best = d->best_sse;
+    out->best = d->best;
+  }
+done:
+  free(sat); free(usat); free(b->lb); free(b->lbm); free(b);
+  return st;
+}

@@ -279,7 +279,11 @@ def _check_result_properties(oracle, w, g, est, rec, r, lam=0.0):
 
 @pytest.mark.parametrize("ci", [4, 5])
 def test_cfg4_cfg5_pruned(part, oracle, ci):
+    """Every frame of configs 4 and 5: the GPU's exact pruned search against the
+    oracle's independent branch-and-bound restatement (bit-exact), the exact
+    counts, and size-independent properties of the returned partitions."""
     from paper_2012_14792_b200 import RECORD_DTYPE
+    from paper_2012_14792_b200.partitioner import Partition
     w, tr, luma = _config_inputs(ci, None)
     g = w.grid()
     F = w.frames
@@ -290,6 +294,28 @@ def test_cfg4_cfg5_pruned(part, oracle, ci):
         cnt = r.candidates_step1 | (r.candidates_step1_hi << 64)
         assert cnt == CFG_COUNTS[ci] == (r.candidates_step2 | (r.candidates_step2_hi << 64))
         _check_result_properties(oracle, w, g, tr.est[f], rec[f], r)
+        st, e = oracle.search_pruned(w.width, w.height, w.ctu, tr.est[f], _rec3(rec[f]),
+                                     w.n_slices, 0.0, 3.0, w.max_tile_cols, 0, 3)
+        assert st == 0
+        assert r.t_min_us == e.t_min_us and r.t_best_us == e.t_best_us
+        assert r.sse_best == e.sse_best
+        assert Partition.from_layout(g, r.argmin).rects() == e.argmin1.slices(g.rows)
+        assert Partition.from_layout(g, r.best).rects() == e.best.slices(g.rows)
+
+
+@pytest.mark.parametrize("ci", [2, 3])
+def test_exhaustive_and_pruned_agree_all_frames(part, ci):
+    """Both search modes give identical results on every frame of cfg2/cfg3."""
+    w, tr, luma = _config_inputs(ci, None)
+    g = w.grid()
+    a = part.partition_frames(g, luma, tr.est, w.cfg(mode=0))
+    b = part.partition_frames(g, luma, tr.est, w.cfg(mode=1))
+    from paper_2012_14792_b200.partitioner import Partition
+    for x, y in zip(a, b):
+        assert x.t_min_us == y.t_min_us and x.t_best_us == y.t_best_us and x.sse_best == y.sse_best
+        assert x.candidates_step1 == y.candidates_step1 and x.candidates_step2 == y.candidates_step2
+        assert Partition.from_layout(g, x.argmin).rects() == Partition.from_layout(g, y.argmin).rects()
+        assert Partition.from_layout(g, x.best).rects() == Partition.from_layout(g, y.best).rects()
 
 
 # ---- error behaviour -----------------------------------------------------------------
