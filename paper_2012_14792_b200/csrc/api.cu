@@ -18,6 +18,8 @@ namespace scb {
 void texture_moments_device(const void* d_luma, int bps, int W, int H, size_t pitch,
                             size_t fstride, int ctu, int frames, int cols, int rows,
                             sc_ctu_record* d_out, cudaStream_t st);
+void split_table_device(const uint64_t* d_rt, int cols, int rows, int groups, int fpw,
+                        uint64_t* d_rts, int sm_count, cudaStream_t st);
 void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, int rows,
                      int frames, double* d_sat, uint64_t* d_usat, cudaStream_t st);
 void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16_t* d_dec,
@@ -248,6 +250,9 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   rect_tables_device(ctx->sat.as<double>(), nullptr, dec, g.cols, g.rows, L.frames, L.fpw,
                      raw ? ctx->rect_t.as<double>() : nullptr, nullptr,
                      ctx->rt_search.as<uint64_t>(), nullptr, ctx->sm_count, st);
+  ctx->rt_split.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint64_t));
+  split_table_device(ctx->rt_search.as<uint64_t>(), g.cols, g.rows, L.groups, L.fpw,
+                     ctx->rt_split.as<uint64_t>(), ctx->sm_count, st);
 }
 
 // K2 (u64 SATs) + K3 (SSE tables) from ctx->records.
@@ -330,6 +335,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     a.bmax = plan->d_bmax.as<int32_t>();
     a.pathological = plan->pathological ? 1 : 0;
     a.rt = ctx->rt_search.as<uint64_t>() + (size_t)gi * L.nr * L.fpw;
+    a.rts = ctx->rt_split.as<uint64_t>() + (size_t)gi * L.nr * L.fpw;
     a.rs = step == 2 ? ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw : nullptr;
     a.budget = ctx->budget.as<uint64_t>() + (size_t)gi * L.fpw;
     a.lanes = reinterpret_cast<LaneBest*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
@@ -530,7 +536,7 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
 }  // namespace
 
 sc_ctx::~sc_ctx() {
-  for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rs_search, &usat,
+  for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rt_split, &rs_search, &usat,
                   &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc})
     b->release();
   h_stage.release();

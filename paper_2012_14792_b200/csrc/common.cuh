@@ -134,6 +134,7 @@ struct SearchArgs {
   uint32_t* counter;
   const int32_t* bmax;    // bmax[A] | aneed[A] | mstar[(cols+1)*(rows+1)], A = max_area+1
   const uint64_t* rt;     // [NR][FPW] clamped time bits, this frame group
+  const uint64_t* rts;    // [NR][FPW] split table (run + forced rest of its column)
   const double* rs;       // [NR][FPW] SSE (step 2)
   const uint64_t* budget; // [FPW] budget bits (step 2)
   LaneBest* lanes;        // [warps * 32]
@@ -172,7 +173,7 @@ struct sc_ctx {
   double timings[5] = {0, 0, 0, 0, 0};
   int shard_rank = 0, shard_world = 1;
   // staging / tables
-  scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rs_search, usat;
+  scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rt_split, rs_search, usat;
   scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec, lbr, lbm, inc, seed_inc;
   int dec_cols = -1, dec_rows = -1;
   scb::HostBuf h_stage, h_records, h_frame_best, h_budget;

@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
   e.ybase = s_ybase;
   e.sfx = s_sfx;
   e.rt = a.rt;
+  e.rts = a.rts;
   e.rs = a.rs;
   e.lbr = a.lbr;
   e.lbm = a.lbm;

@@ -72,6 +72,9 @@ struct WalkEnv {
   const int32_t* ybase;   // [rows+1]: yh(y, 1), the first rectangle starting at row y
   const int32_t* sfx;     // [rows+1]: yh(y, rows - y), the rectangle from row y to the bottom
   const uint64_t* rt;     // [NR][FPW] clamped f64 time bits of every rectangle
+  const uint64_t* rts;    // [NR][FPW] split table: at rect(x0,w,y0,h) with y0+h < rows,
+                          // max(time(y0,h), time(y0+h, rows-y0-h)) -- a run plus the
+                          // forced rest of its column in one load
   const double* rs;       // [NR][FPW] SSE of every rectangle (step 2)
   // pruned mode only: per-frame lower bounds on a column's slowest slice,
   // lbr[(xw*rstride + r)*FPW + f] for exactly r runs and lbm[...] for any
@@ -480,13 +483,16 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           const int ridx = RS0[i] + j;
           curH[ridx] = (uint8_t)h;
           const int lb = Lbase[l];
-          uint64_t Pn = umax64(Pin[l], rt[(size_t)(lb + e.ybase[y0] + h - 1) * FPW + f]);
+          const size_t ri = (size_t)(lb + e.ybase[y0] + h - 1) * FPW + f;
+          uint64_t Pn;
           if (forced) {
             const int a2 = w * (rows_left - h);
             na = imin(na, a2);
             nx = imax(nx, a2);
             curH[ridx + 1] = (uint8_t)(rows_left - h);
-            Pn = umax64(Pn, rt[(size_t)(lb + e.sfx[y0 + h]) * FPW + f]);
+            Pn = umax64(Pin[l], e.rts[ri]);
+          } else {
+            Pn = umax64(Pin[l], rt[ri]);
           }
           if (!viable(Pn)) continue;
           const int nxt = l + 1;
@@ -529,29 +535,20 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           ++g_stats.leafr[R[i]];
 #endif
           if (lo + slot <= hi && viable(Pl)) {
-            // rect 1 = (y0l, h) advances by +1 per h; rect 2 = (y0l+h,
-            // rows_left-h) by rows_left-h-1 (yh numbering); lanes step h by J.
+            // the split table holds max(run h, forced rest) at the run's own
+            // rectangle index, which advances by +1 per h; lanes step h by J.
             int h = lo + slot;
-            const uint64_t* p1 = rt + (size_t)(xwb + e.ybase[y0l] + h - 1) * FPW + f;
-            int i2 = xwb + e.sfx[y0l + h];
-            uint64_t v1 = *p1, v2 = rt[(size_t)i2 * FPW + f];
+            const uint64_t* p = e.rts + (size_t)(xwb + e.ybase[y0l] + h - 1) * FPW + f;
+            uint64_t v = *p;
             while (true) {
               const int hn = h + J;
               const bool more = hn <= hi;
-              const uint64_t* p1n = p1 + J * FPW;
-              const int i2n = i2 + J * (rows_left - h - 1) - (J * (J - 1)) / 2;
-              uint64_t v1n = 0, v2n = 0;
-              if (more) {  // prefetch the next height before scoring this one
-                v1n = *p1n;
-                v2n = rt[(size_t)i2n * FPW + f];
-              }
-              score(umax64(Pl, umax64(v1, v2)), ord + (uint64_t)(h - lo), lr, h, rows_left - h);
+              const uint64_t vn = more ? p[J * FPW] : 0;  // prefetch the next height
+              score(umax64(Pl, v), ord + (uint64_t)(h - lo), lr, h, rows_left - h);
               if (!more) break;
               h = hn;
-              p1 = p1n;
-              i2 = i2n;
-              v1 = v1n;
-              v2 = v2n;
+              p += J * FPW;
+              v = vn;
             }
           }
           if (hi >= lo) ord += (uint64_t)(hi - lo + 1);

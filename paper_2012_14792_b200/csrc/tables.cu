@@ -141,6 +141,51 @@ __global__ void k_rect_tables(const double* __restrict__ sat, const uint64_t* __
   }
 }
 
+// Split table (search_walk.cuh WalkEnv::rts): for every rectangle (x0,w,y0,h)
+// with y0+h < rows, max(time(y0,h), time(y0+h, rows-y0-h)), i.e. a run and
+// the forced remainder of its column, so the search scores a two-run split
+// with one load.  Same [group][rect][FPW] layout as the time table.
+__global__ void k_split_table(const uint64_t* __restrict__ rt, int cols, int rows,
+                              size_t slots /* groups * fpw */, int fpw,
+                              uint64_t* __restrict__ rts) {
+  const int nyh = rows * (rows + 1) / 2;
+  const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
+  const size_t total = nr * slots;
+  for (size_t id = blockIdx.x * (size_t)blockDim.x + threadIdx.x; id < total;
+       id += (size_t)gridDim.x * blockDim.x) {
+    const size_t g = id / (nr * fpw);
+    const size_t rem = id % (nr * fpw);
+    const int rr = (int)(rem / fpw), slot = (int)(rem % fpw);
+    const int xw = rr / nyh, yh = rr % nyh;
+    // decode (y0, h) from yh: y0 is the largest y with yh(y, 1) <= yh
+    int y0 = 0;
+    while (y0 + 1 < rows && (y0 + 1) * rows - ((y0 + 1) * y0) / 2 <= yh) ++y0;
+    const int h = yh - (y0 * rows - (y0 * (y0 - 1)) / 2) + 1;
+    const size_t base = g * nr * fpw;
+    uint64_t v = 0;
+    if (y0 + h < rows) {
+      const uint64_t a = rt[base + (size_t)rr * fpw + slot];
+      const int y1 = y0 + h, h1 = rows - y1;
+      const int rr2 = xw * nyh + (y1 * rows - (y1 * (y1 - 1)) / 2 + h1 - 1);
+      const uint64_t b = rt[base + (size_t)rr2 * fpw + slot];
+      v = a > b ? a : b;
+    }
+    rts[base + (size_t)rr * fpw + slot] = v;
+  }
+}
+
+void split_table_device(const uint64_t* d_rt, int cols, int rows, int groups, int fpw,
+                        uint64_t* d_rts, int sm_count, cudaStream_t st) {
+  const size_t total = (size_t)cols * (cols + 1) / 2 * (rows * (rows + 1) / 2) * groups * fpw;
+  size_t blocks = (total + 255) / 256;
+  const size_t cap = (size_t)sm_count * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_split_table<<<(unsigned)blocks, 256, 0, st>>>(d_rt, cols, rows, (size_t)groups * fpw, fpw,
+                                                  d_rts);
+  SCB_CUDA(cudaGetLastError());
+}
+
 void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, int rows,
                      int frames, double* d_sat, uint64_t* d_usat, cudaStream_t st) {
   const int nsat = (cols + 1) * (rows + 1);

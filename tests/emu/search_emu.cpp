@@ -66,6 +66,16 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
         column_bounds(rt.data(), fpw, f, rows, xw * nyh, rstride - 1, lbr.data() + off,
                       lbm.data() + off, (size_t)fpw);
       }
+  // split table (tables.cu k_split_table): max(run, forced rest of the column)
+  std::vector<uint64_t> rts(nr * fpw, 0);
+  for (int xw = 0; xw < cols * (cols + 1) / 2; ++xw)
+    for (int y0 = 0; y0 < rows; ++y0)
+      for (int h = 1; y0 + h < rows; ++h)
+        for (int f = 0; f < fpw; ++f) {
+          const size_t r1 = (size_t)xw * nyh + yh_of(rows, y0, h);
+          const size_t r2 = (size_t)xw * nyh + yh_of(rows, y0 + h, rows - y0 - h);
+          rts[r1 * fpw + f] = std::max(rt[r1 * fpw + f], rt[r2 * fpw + f]);
+        }
   WalkEnv e;
   e.cols = cols;
   e.rows = rows;
@@ -84,6 +94,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.ybase = ybase.data();
   e.sfx = sfx.data();
   e.rt = rt.data();
+  e.rts = rts.data();
   e.rs = rs.data();
   e.lbr = lbr.data();
   e.lbm = lbm.data();
