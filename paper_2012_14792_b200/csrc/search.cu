@@ -35,7 +35,7 @@ namespace scb {
 #define SCB_SEARCH_MINB 2
 #endif
 
-template <int FPW, int STEP>
+template <int FPW, int STEP, bool PRUNE>
 __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
   // area tables + column windows + division magics in shared memory
   extern __shared__ int32_t s_tab[];
@@ -68,15 +68,18 @@ __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
     s_magic[w] = w >= 1 ? div_magic(w) : 0ull;
   int32_t* s_ybase = reinterpret_cast<int32_t*>(s_magic + a.cols + 1);
   int32_t* s_sfx = s_ybase + a.rows + 1;
+  int32_t* s_rq = s_sfx + a.rows + 1;
   for (int y = threadIdx.x; y <= a.rows; y += blockDim.x) {
     s_ybase[y] = yh_of(a.rows, y, 1);
     s_sfx[y] = y < a.rows ? yh_of(a.rows, y, a.rows - y) : 0;
+    s_rq[y] = y >= 1 ? a.rows / y : 0;
   }
   __syncthreads();
   e.ilo = s_ilo;
   e.magic = s_magic;
   e.ybase = s_ybase;
   e.sfx = s_sfx;
+  e.rq = s_rq;
   e.rt = a.rt;
   e.rts = a.rts;
   e.rs = a.rs;
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
     if (k >= a.n_items) break;
     const uint64_t item = (uint64_t)a.item_offset + (uint64_t)k * a.item_stride;
     const WorkItem wi = a.items[item];
-    walk_item<FPW, STEP>(e, item, wi, f, slot, st);
+    walk_item<FPW, STEP, PRUNE>(e, item, wi, f, slot, st);
     __syncwarp();
   }
   LaneBest lb;
@@ -236,11 +239,14 @@ template <int FPW, int STEP>
 static void launch_fpw(const SearchArgs& a, int blocks, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    SCB_CUDA(cudaFuncSetAttribute(k_search<FPW, STEP>,
+    SCB_CUDA(cudaFuncSetAttribute(k_search<FPW, STEP, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SCB_CUDA(cudaFuncSetAttribute(k_search<FPW, STEP, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr = true;
   }
-  k_search<FPW, STEP><<<blocks, 256, smem, st>>>(a);
+  if (a.prune) k_search<FPW, STEP, true><<<blocks, 256, smem, st>>>(a);
+  else k_search<FPW, STEP, false><<<blocks, 256, smem, st>>>(a);
 }
 
 int search_blocks_per_sm(int fpw, int step) {
@@ -249,9 +255,9 @@ int search_blocks_per_sm(int fpw, int step) {
 #define OCC(F)                                                                               \
   if (fpw == F) {                                                                            \
     if (step == 1)                                                                           \
-      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 1>, 256, smem)); \
+      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 1, false>, 256, smem)); \
     else                                                                                     \
-      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 2>, 256, smem)); \
+      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 2, false>, 256, smem)); \
   }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
 #undef OCC
@@ -261,7 +267,7 @@ int search_blocks_per_sm(int fpw, int step) {
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st) {
   const size_t smem = ((size_t)2 * (a.max_area + 1) + (size_t)(a.cols + 1) * (a.rows + 1) +
                        (size_t)(a.cols + 1) * (std::min(a.n, a.rows) + 1) + 2 +
-                       (size_t)(a.cols + 1) * 2 + (size_t)(a.rows + 1) * 2) *
+                       (size_t)(a.cols + 1) * 2 + (size_t)(a.rows + 1) * 3) *
                       sizeof(int32_t);
   if (smem > 64 * 1024) fail(SC_ERR_SIZE, "CTU grid too large for the area tables");
   switch (fpw * 10 + step) {

@@ -70,6 +70,7 @@ struct WalkEnv {
   const int32_t* ilo;     // [(cols+1) * rstride]: lower end of window I(w, r)
   const uint64_t* magic;  // [cols+1]: division by w (div_magic)
   const int32_t* ybase;   // [rows+1]: yh(y, 1), the first rectangle starting at row y
+  const int32_t* rq;      // [rows+1]: rows / r (no integer division in the runs DFS)
   const int32_t* sfx;     // [rows+1]: yh(y, rows - y), the rectangle from row y to the bottom
   const uint64_t* rt;     // [NR][FPW] clamped f64 time bits of every rectangle
   const uint64_t* rts;    // [NR][FPW] split table: at rect(x0,w,y0,h) with y0+h < rows,
@@ -182,7 +183,7 @@ SCB_HD void height_interval(const WalkEnv& e, Thr t, int w, int rl, int runs_lef
 
 // Walk work item `item` (prefix wi) for frame slot f and leaf slot `slot`
 // (J = 32 / FPW lanes share a frame and split the innermost height loop).
-template <int FPW, int STEP>
+template <int FPW, int STEP, bool PRUNE>
 SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f, int slot,
                       LaneState& st) {
   constexpr int J = 32 / FPW;
@@ -255,12 +256,12 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     return tot;
   };
   // can a subtree whose fixed slices already reach time P still win?
-  const uint64_t seed_inc = (STEP == 1 && e.prune && e.seed_inc) ? e.seed_inc[f] : ~0ull;
+  const uint64_t seed_inc = (STEP == 1 && PRUNE && e.seed_inc) ? e.seed_inc[f] : ~0ull;
   auto viable = [&](uint64_t P) -> bool {
-    return !e.prune ||
+    return !PRUNE ||
            (STEP == 1 ? (P < st.best_t && P <= st.inc && P < seed_inc) : (P <= st.budget));
   };
-  if (STEP == 1 && e.prune) st.inc = incumbent_load(e.inc + f);
+  if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
   // lower bound of column (x0, w) with r runs (exact r) / any r' <= r
   auto lb_r = [&](int x0, int w, int r) -> uint64_t {
     return e.lbr[((size_t)xw_of(cols, x0, w) * e.rstride + r) * FPW + f];
@@ -270,14 +271,14 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   };
   // score one candidate (strict comparisons keep the first in order)
   auto score = [&](uint64_t t, uint64_t o, int lr, int lh, int lrest) {
-    ++st.scored;
+    if (PRUNE) ++st.scored;
     if (STEP == 1) {
       if (t < st.best_t) {
         st.best_t = t;
         st.best_item = item;
         st.best_ord = o;
         take_snapshot(lr, lh, lrest);
-        if (e.prune) incumbent_offer(e.inc + f, t);
+        if (PRUNE) incumbent_offer(e.inc + f, t);
       }
     } else if (t <= st.budget) {
       const double s = layout_sse(lr, lh, lrest);
@@ -309,7 +310,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     WL[i + 1] = imax(WL[i], e.ilo[W[i] * e.rstride + rmax_c]);
     WH[i + 1] = imin(WH[i], W[i] * rows);
     ok = WL[i + 1] <= WH[i + 1];
-    if (e.prune) {
+    if (PRUNE) {
       PW[i + 1] = umax64(PW[i], lb_m(X0[i], W[i], rmax_c));
       ok = ok && viable(PW[i + 1]);
     }
@@ -334,7 +335,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         const int nL = imax(WL[pos], e.ilo[wv * e.rstride + rmax_c]);
         const int nH = imin(WH[pos], wv * rows);
         if (nL > nH) continue;
-        if (e.prune) {
+        if (PRUNE) {
           PW[pos + 1] = umax64(PW[pos], lb_m(X0[pos], wv, rmax_c));
           if (!viable(PW[pos + 1])) continue;
         }
@@ -351,7 +352,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       if (!got) break;
     }
     SCB_STAT(widths);
-    if (STEP == 1 && e.prune) st.inc = incumbent_load(e.inc + f);
+    if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
     // ---- runs DFS (lex, search.cpp:145-161).  The skeleton (widths, runs)
     //      has an admissible completion iff the column windows
     //      I(w, r) = [aneed[w*ceil(rows/r)], w*floor(rows/r)] intersect; I
@@ -359,7 +360,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     //      contiguous range.
     int RL[SC_MAX_COLS], RH[SC_MAX_COLS], SL[SC_MAX_COLS];
     uint64_t PR[SC_MAX_COLS + 1];  // pruned mode: widths bound, tightened per exact r
-    PR[0] = e.prune ? PW[c] : 0;
+    PR[0] = PRUNE ? PW[c] : 0;
     int rp = 0;
     RL[0] = 1;
     RH[0] = e.max_area;
@@ -374,7 +375,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       bool found = false;
       for (; r <= rhi; ++r) {
         lo = e.ilo[w * e.rstride + r];
-        hi = w * (rows / r);
+        hi = w * e.rq[r];
         if (hi < RL[rp]) break;  // every larger r is lower still
         if (lo <= RH[rp]) {
           found = true;
@@ -389,7 +390,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       R[rp] = r;
       const int nL = imax(RL[rp], lo), nH = imin(RH[rp], hi);
       if (nL > nH) continue;
-      if (e.prune) {
+      if (PRUNE) {
         PR[rp + 1] = umax64(PR[rp], lb_r(X0[rp], W[rp], r));
         if (!viable(PR[rp + 1])) continue;
       }
@@ -405,7 +406,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       //      [win_lo, bmax[nH]] for a window a in [nL, nH]
       const int win_lo = nL, win_hi = e.bmax[nH];
       SCB_STAT(skeletons);
-      if (STEP == 1 && e.prune) st.inc = incumbent_load(e.inc + f);
+      if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
       int amin = kBigArea, amax = 0;
       int run = 0, nl = 0;
       for (int i = 0; i < c; ++i) {

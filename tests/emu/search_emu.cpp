@@ -39,7 +39,8 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
     magic[w] = div_magic(w);
   }
   const int nyh = rows * (rows + 1) / 2;
-  std::vector<int32_t> ybase(rows + 1), sfx(rows + 1);
+  std::vector<int32_t> ybase(rows + 1), sfx(rows + 1), rq(rows + 1, 0);
+  for (int r = 1; r <= rows; ++r) rq[r] = rows / r;
   for (int y = 0; y <= rows; ++y) {
     ybase[y] = yh_of(rows, y, 1);
     sfx[y] = y < rows ? yh_of(rows, y, rows - y) : 0;
@@ -92,6 +93,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.ilo = ilo.data();
   e.magic = magic.data();
   e.ybase = ybase.data();
+  e.rq = rq.data();
   e.sfx = sfx.data();
   e.rt = rt.data();
   e.rts = rts.data();
@@ -144,8 +146,14 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       LaneState& s = st[(size_t)wp * 32 + l];
       switch (fpw * 10 + step) {
 #define CASE(F)                                                                   \
-  case F * 10 + 1: walk_item<F, 1>(e, it, items[it], l % F, l / F, s); break;    \
-  case F * 10 + 2: walk_item<F, 2>(e, it, items[it], l % F, l / F, s); break;
+  case F * 10 + 1:                                                                \
+    if (prune) walk_item<F, 1, true>(e, it, items[it], l % F, l / F, s);          \
+    else walk_item<F, 1, false>(e, it, items[it], l % F, l / F, s);               \
+    break;                                                                        \
+  case F * 10 + 2:                                                                \
+    if (prune) walk_item<F, 2, true>(e, it, items[it], l % F, l / F, s);          \
+    else walk_item<F, 2, false>(e, it, items[it], l % F, l / F, s);               \
+    break;
         CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
 #undef CASE
         default: return 2;
