@@ -15,8 +15,17 @@ $(PKG)/libslicecraft_b200.so: $(SRCS) $(HDRS)
 oracle:
 	$(MAKE) -C oracle
 
+# Drop-in check binary (needs the reference headers; built where they exist,
+# runs on the GPU box): the reference library and the B200 binding side by side.
+REF_INC ?= /root/reference/proj/include
+dropin: dropin/dropin_test
+dropin/dropin_test: dropin/dropin_test.cpp dropin/slicecraft_b200.hpp $(PKG)/libslicecraft_b200.so oracle
+	g++ -std=c++20 -O2 -I$(REF_INC) -Iinclude -Idropin $< \
+	    -Loracle/_ref -lslicecraft_ref -L$(PKG) -lslicecraft_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
+
 clean:
 	rm -f $(PKG)/libslicecraft_b200.so build_ptxas.log
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean dropin

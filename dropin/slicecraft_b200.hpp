@@ -1,0 +1,183 @@
+// Drop-in binding of the B200 partitioner core for code written against the
+// reference `slicecraft` API (proj/include/slicecraft/*.hpp).
+//
+// Header-only; compile it together with the reference headers and link
+// libslicecraft_b200.so.  Every function takes and returns the reference's own
+// types and throws the reference's own exception classes (errors.hpp:10-85);
+// the compute runs in the sm_100a kernels behind include/slicecraft_b200.h.
+//
+//   slicecraft::ctu_stats(luma, grid, poc)              -> b200::ctu_stats(ctx, ...)
+//   slicecraft::min_time_search(est, cfg)               -> b200::min_time_search(ctx, ...)
+//   slicecraft::constrained_clustering_search(...)      -> b200::constrained_clustering_search(ctx, ...)
+//   slicecraft::two_step_partition(history, stats, ...) -> b200::two_step_partition(ctx, ...)
+#pragma once
+
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "slicecraft/cost.hpp"
+#include "slicecraft/errors.hpp"
+#include "slicecraft/grid.hpp"
+#include "slicecraft/search.hpp"
+#include "slicecraft/texture.hpp"
+#include "slicecraft_b200.h"
+
+namespace slicecraft {
+namespace b200 {
+
+// sc_status -> the reference exception class (errors.hpp:10-85).
+[[noreturn]] inline void rethrow(sc_status s) {
+  const std::string m = sc_last_error();
+  switch (s) {
+    case SC_ERR_GEOMETRY: throw GeometryError(m);
+    case SC_ERR_OVERLAP: throw OverlapError(m);
+    case SC_ERR_COVERAGE: throw CoverageError(m);
+    case SC_ERR_STRUCTURE: throw StructureError(m);
+    case SC_ERR_IO: throw IoError(m);
+    case SC_ERR_RANGE: throw RangeError(m);
+    case SC_ERR_FORMAT: throw FormatError(m);
+    case SC_ERR_CONFIG: throw ConfigError(m);
+    case SC_ERR_TRACE: throw TraceError(m);
+    case SC_ERR_NO_CANDIDATE: throw NoCandidateError(m);
+    case SC_ERR_SIZE: throw SizeError(m);
+    case SC_ERR_USAGE: throw UsageError(m);
+    default: throw Error(m);
+  }
+}
+inline void check(sc_status s) {
+  if (s != SC_OK) rethrow(s);
+}
+
+// One device context (streams, device tables, cached search plans).
+class Context {
+ public:
+  explicit Context(int device = 0) { check(sc_ctx_create(device, &ctx_)); }
+  ~Context() { sc_ctx_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  sc_ctx* get() const { return ctx_; }
+
+ private:
+  sc_ctx* ctx_ = nullptr;
+};
+
+inline sc_grid to_c(const CtuGrid& g) {
+  return sc_grid{g.frame_width, g.frame_height, g.ctu_size, g.cols, g.rows};
+}
+
+// SearchConfig (search.hpp:22-34); the B200 fields default to the reference
+// family (widths summing to <= cols) and the exhaustive walk.
+inline sc_search_cfg to_c(const SearchConfig& c, int mode = SC_MODE_EXHAUSTIVE) {
+  sc_search_cfg r;
+  r.n_slices = c.n_slices;
+  r.lambda = c.lambda;
+  r.k_area = c.k_area;
+  r.family = c.family == CandidateFamily::UniformOnly ? SC_FAMILY_UNIFORM_ONLY
+                                                      : SC_FAMILY_COLUMN_SPLIT;
+  r.max_tile_cols = c.max_tile_cols;
+  r.workers = c.workers;
+  r.coverage = SC_COVERAGE_REFERENCE;
+  r.mode = mode;
+  return r;
+}
+
+// layout_to_partition (search.cpp:63-75).
+inline Partition to_partition(const CtuGrid& g, const sc_layout& L) {
+  Partition p;
+  p.grid = g;
+  p.origin = PartitionOrigin::Proposed;
+  p.tiles.col_widths.assign(L.col_widths, L.col_widths + L.n_cols);
+  p.tiles.row_heights = {g.rows};
+  int x = 0, run = 0, id = 0;
+  for (int c = 0; c < L.n_cols; ++c) {
+    int y = 0;
+    for (int j = 0; j < L.runs_per_col[c]; ++j, ++run) {
+      p.slices.push_back(RectSlice{x, y, L.col_widths[c], L.run_heights[run], id++});
+      y += L.run_heights[run];
+    }
+    x += L.col_widths[c];
+  }
+  return p;
+}
+
+static_assert(sizeof(CtuRecord) == sizeof(sc_ctu_record), "CtuRecord layout");
+
+// ctu_stats (texture.hpp:83): K1 on the plane's uint16 samples.
+inline TextureStats ctu_stats(Context& ctx, const LumaPlane& luma, const CtuGrid& grid,
+                              int poc = 0) {
+  if (luma.width != grid.frame_width || luma.height != grid.frame_height)
+    throw GeometryError("plane dimensions do not match the grid");
+  std::vector<CtuRecord> rec(static_cast<size_t>(grid.cell_count()));
+  check(sc_texture_moments(ctx.get(), luma.samples.data(), 2, luma.width, luma.height,
+                           static_cast<size_t>(luma.width) * 2,
+                           static_cast<size_t>(luma.width) * luma.height * 2, grid.ctu_size, 1,
+                           reinterpret_cast<sc_ctu_record*>(rec.data())));
+  return TextureStats(grid, std::move(rec), poc);
+}
+
+// min_time_search (search.hpp:66-67).
+inline std::pair<double, Partition> min_time_search(Context& ctx, const CostMap& est,
+                                                    const SearchConfig& cfg,
+                                                    int mode = SC_MODE_EXHAUSTIVE) {
+  const sc_grid g = to_c(est.grid);
+  const sc_search_cfg c = to_c(cfg, mode);
+  sc_search_result r;
+  check(sc_min_time_search(ctx.get(), &g, &c, est.times_us.data(), 1, &r));
+  return {r.t_min_us, to_partition(est.grid, r.argmin)};
+}
+
+inline SearchOutcome to_outcome(const CtuGrid& g, const sc_search_result& r) {
+  SearchOutcome o;
+  o.best = to_partition(g, r.best);
+  o.t_min_us = r.t_min_us;
+  o.t_best_us = r.t_best_us;
+  o.sse_best = r.sse_best;
+  o.candidates_evaluated = r.candidates_evaluated;
+  o.candidates_step1 = r.candidates_step1;
+  o.candidates_step2 = r.candidates_step2;
+  o.search_time_us = r.search_time_us;
+  o.time_min_step_us = r.time_min_step_us;
+  o.clustering_step_us = r.clustering_step_us;
+  return o;
+}
+
+// constrained_clustering_search (search.hpp:72-75).
+inline SearchOutcome constrained_clustering_search(Context& ctx, const CostMap& est,
+                                                   const TextureStats& stats, double t_min_us,
+                                                   const SearchConfig& cfg,
+                                                   int mode = SC_MODE_EXHAUSTIVE) {
+  if (stats.grid() != est.grid)
+    throw GeometryError("texture stats grid does not match the cost map grid");
+  const sc_grid g = to_c(est.grid);
+  const sc_search_cfg c = to_c(cfg, mode);
+  sc_search_result r;
+  check(sc_constrained_clustering(ctx.get(), &g, &c, est.times_us.data(),
+                                  reinterpret_cast<const sc_ctu_record*>(stats.records().data()),
+                                  &t_min_us, 1, &r));
+  return to_outcome(est.grid, r);
+}
+
+// two_step_partition (search.hpp:80-82): host estimate (cost.cpp:66-95), then
+// both steps on the device.
+inline SearchOutcome two_step_partition(Context& ctx, const CostHistory& history,
+                                        const TextureStats& stats, int poc,
+                                        const SearchConfig& cfg, int mode = SC_MODE_EXHAUSTIVE) {
+  if (stats.grid() != history.grid())
+    throw GeometryError("texture stats grid does not match the history grid");
+  const CostMap est = estimate_ctu_times(history, poc);
+  const sc_grid g = to_c(history.grid());
+  const sc_search_cfg c = to_c(cfg, mode);
+  sc_search_result r;
+  check(sc_two_step(ctx.get(), &g, &c, est.times_us.data(),
+                    reinterpret_cast<const sc_ctu_record*>(stats.records().data()), 1, &r));
+  SearchOutcome o = to_outcome(history.grid(), r);
+  o.candidates_step1 = r.candidates_step1;
+  o.est_source = est.source;
+  o.est_source_poc = est.source_poc;
+  return o;
+}
+
+}  // namespace b200
+}  // namespace slicecraft

@@ -28,6 +28,7 @@ void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16
                         cudaStream_t st);
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st);
 int search_blocks_per_sm(int fpw, int step);
+int search_block_threads();
 void column_bounds_launch(const uint64_t* rt, int fpw, int frames_in_group, int cols, int rows,
                           int rmax, int rstride, uint64_t* lbr, uint64_t* lbm, cudaStream_t st);
 void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
@@ -275,7 +276,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
                   const Layouts& L, int step, bool compute_bounds, cudaStream_t st) {
   const int bps = search_blocks_per_sm(L.fpw, step);
   const int blocks = ctx->sm_count * bps;
-  const uint32_t warps = (uint32_t)blocks * 8;
+  const uint32_t warps = (uint32_t)blocks * (search_block_threads() / 32);
   const size_t lane_bytes = (size_t)warps * 32 * sizeof(LaneBest);
   const size_t snap_bytes = (size_t)warps * 32 * kSnapBytes;
   ctx->lanes.ensure(lane_bytes * L.groups);

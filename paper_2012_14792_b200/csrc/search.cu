@@ -34,9 +34,13 @@ namespace scb {
 #ifndef SCB_SEARCH_MINB
 #define SCB_SEARCH_MINB 2
 #endif
+#ifndef SCB_SEARCH_BLOCK
+#define SCB_SEARCH_BLOCK 256
+#endif
+int search_block_threads() { return SCB_SEARCH_BLOCK; }
 
 template <int FPW, int STEP, bool PRUNE>
-__global__ void __launch_bounds__(256, SCB_SEARCH_MINB) k_search(SearchArgs a) {
+__global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(SearchArgs a) {
   // area tables + column windows + division magics in shared memory
   extern __shared__ int32_t s_tab[];
   const int A = a.max_area + 1;
@@ -245,8 +249,8 @@ static void launch_fpw(const SearchArgs& a, int blocks, size_t smem, cudaStream_
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr = true;
   }
-  if (a.prune) k_search<FPW, STEP, true><<<blocks, 256, smem, st>>>(a);
-  else k_search<FPW, STEP, false><<<blocks, 256, smem, st>>>(a);
+  if (a.prune) k_search<FPW, STEP, true><<<blocks, SCB_SEARCH_BLOCK, smem, st>>>(a);
+  else k_search<FPW, STEP, false><<<blocks, SCB_SEARCH_BLOCK, smem, st>>>(a);
 }
 
 int search_blocks_per_sm(int fpw, int step) {
@@ -255,9 +259,9 @@ int search_blocks_per_sm(int fpw, int step) {
 #define OCC(F)                                                                               \
   if (fpw == F) {                                                                            \
     if (step == 1)                                                                           \
-      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 1, false>, 256, smem)); \
+      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 1, false>, SCB_SEARCH_BLOCK, smem)); \
     else                                                                                     \
-      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 2, false>, 256, smem)); \
+      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 2, false>, SCB_SEARCH_BLOCK, smem)); \
   }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
 #undef OCC
