@@ -18,8 +18,12 @@ namespace scb {
 void texture_moments_device(const void* d_luma, int bps, int W, int H, size_t pitch,
                             size_t fstride, int ctu, int frames, int cols, int rows,
                             sc_ctu_record* d_out, cudaStream_t st);
-void split_table_device(const uint64_t* d_rt, int cols, int rows, int groups, int fpw,
-                        uint64_t* d_rts, int sm_count, cudaStream_t st);
+void split_table_device(const uint32_t* d_rt, int cols, int rows, int groups, int fpw,
+                        uint32_t* d_rts, int sm_count, cudaStream_t st);
+void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
+                       uint32_t* keys, uint64_t* vals, uint32_t* nvals, cudaStream_t st);
+void budget_keys_device(const double* d_budgets, const uint64_t* vals, const uint32_t* nvals,
+                        size_t nr, int frames, int64_t* out, cudaStream_t st);
 void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, int rows,
                      int frames, double* d_sat, uint64_t* d_usat, cudaStream_t st);
 void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16_t* d_dec,
@@ -29,12 +33,13 @@ void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st);
 int search_blocks_per_sm(int fpw, int step);
 int search_block_threads();
-void column_bounds_launch(const uint64_t* rt, int fpw, int frames_in_group, int cols, int rows,
-                          int rmax, int rstride, uint64_t* lbr, uint64_t* lbm, cudaStream_t st);
+void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int cols, int rows,
+                          int rmax, int rstride, uint32_t* lbr, uint32_t* lbm, cudaStream_t st);
 void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
                      const LaneBest* lanes, const uint8_t* snaps,
                      const unsigned long long* count, const unsigned long long* scored,
-                     double lambda, FrameBest* out, uint64_t* budget_out, cudaStream_t st);
+                     double lambda, const uint64_t* vals, const uint32_t* nvals, size_t nr,
+                     FrameBest* out, int64_t* budget_out, cudaStream_t st);
 }  // namespace scb
 
 using namespace scb;
@@ -244,16 +249,23 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
                          cudaStream_t st) {
   const int16_t* dec = decode_table(ctx, g);
   ctx->sat.ensure((size_t)L.frames * L.nsat * sizeof(double));
-  ctx->rt_search.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint64_t));
+  ctx->rt_bits.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
+  ctx->rt_search.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint32_t));
+  ctx->vals.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
+  ctx->nvals.ensure((size_t)L.frames * sizeof(uint32_t));
   if (raw) ctx->rect_t.ensure((size_t)L.frames * L.nr * sizeof(double));
   grid_sat_device(ctx->est.as<double>(), nullptr, g.cols, g.rows, L.frames, ctx->sat.as<double>(),
                   nullptr, st);
   rect_tables_device(ctx->sat.as<double>(), nullptr, dec, g.cols, g.rows, L.frames, L.fpw,
                      raw ? ctx->rect_t.as<double>() : nullptr, nullptr,
-                     ctx->rt_search.as<uint64_t>(), nullptr, ctx->sm_count, st);
-  ctx->rt_split.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint64_t));
-  split_table_device(ctx->rt_search.as<uint64_t>(), g.cols, g.rows, L.groups, L.fpw,
-                     ctx->rt_split.as<uint64_t>(), ctx->sm_count, st);
+                     ctx->rt_bits.as<uint64_t>(), nullptr, ctx->sm_count, st);
+  // exact per-frame ranks of the times (rank.cu) -> 32-bit search keys
+  rank_times_device(ctx, ctx->rt_bits.as<uint64_t>(), L.nr, L.frames, L.fpw,
+                    ctx->rt_search.as<uint32_t>(), ctx->vals.as<uint64_t>(),
+                    ctx->nvals.as<uint32_t>(), st);
+  ctx->rt_split.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint32_t));
+  split_table_device(ctx->rt_search.as<uint32_t>(), g.cols, g.rows, L.groups, L.fpw,
+                     ctx->rt_split.as<uint32_t>(), ctx->sm_count, st);
 }
 
 // K2 (u64 SATs) + K3 (SSE tables) from ctx->records.
@@ -283,7 +295,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
   ctx->snaps.ensure(snap_bytes * L.groups);
   ctx->counter.ensure((size_t)L.groups * 8 * sizeof(uint64_t));
   ctx->frame_best.ensure((size_t)2 * L.groups * L.fpw * sizeof(FrameBest));
-  ctx->budget.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+  ctx->budget.ensure((size_t)L.groups * L.fpw * sizeof(int64_t));
   // per group: 4 u64 per step = {item counter, candidates, scored, pad}
   uint64_t* ctr_base = ctx->counter.as<uint64_t>() + (step - 1) * 4;
   SCB_CUDA(cudaMemsetAsync(ctr_base, 0, sizeof(uint64_t) * 4, st));
@@ -297,19 +309,19 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
   const int rstride = std::min(cfg.n_slices, g.rows) + 1;
   const size_t lb_per_group = (size_t)n_xw(g.cols) * rstride * L.fpw;
   if (prune) {
-    ctx->inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
-    ctx->seed_inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+    ctx->inc.ensure((size_t)L.groups * L.fpw * sizeof(uint32_t));
+    ctx->seed_inc.ensure((size_t)L.groups * L.fpw * sizeof(uint32_t));
     if (compute_bounds) {
       // column lower bounds from the time tables; shared incumbents to +inf
-      ctx->lbr.ensure(lb_per_group * L.groups * sizeof(uint64_t));
-      ctx->lbm.ensure(lb_per_group * L.groups * sizeof(uint64_t));
+      ctx->lbr.ensure(lb_per_group * L.groups * sizeof(uint32_t));
+      ctx->lbm.ensure(lb_per_group * L.groups * sizeof(uint32_t));
       for (int gi = 0; gi < L.groups; ++gi)
-        column_bounds_launch(ctx->rt_search.as<uint64_t>() + (size_t)gi * L.nr * L.fpw, L.fpw,
+        column_bounds_launch(ctx->rt_search.as<uint32_t>() + (size_t)gi * L.nr * L.fpw, L.fpw,
                              std::min(L.fpw, L.frames - gi * L.fpw), g.cols, g.rows,
-                             rstride - 1, rstride, ctx->lbr.as<uint64_t>() + gi * lb_per_group,
-                             ctx->lbm.as<uint64_t>() + gi * lb_per_group, st);
+                             rstride - 1, rstride, ctx->lbr.as<uint32_t>() + gi * lb_per_group,
+                             ctx->lbm.as<uint32_t>() + gi * lb_per_group, st);
     }
-    SCB_CUDA(cudaMemsetAsync(ctx->inc.p, 0xff, (size_t)L.groups * L.fpw * sizeof(uint64_t), st));
+    SCB_CUDA(cudaMemsetAsync(ctx->inc.p, 0xff, (size_t)L.groups * L.fpw * sizeof(uint32_t), st));
   }
   for (int gi = 0; gi < L.groups; ++gi) {
     SearchArgs a{};
@@ -329,16 +341,16 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     a.scored_out = reinterpret_cast<unsigned long long*>(ctr + 2);
     a.prune = prune ? 1 : 0;
     if (prune) {
-      a.lbr = ctx->lbr.as<uint64_t>() + gi * lb_per_group;
-      a.lbm = ctx->lbm.as<uint64_t>() + gi * lb_per_group;
-      a.inc = ctx->inc.as<uint64_t>() + (size_t)gi * L.fpw;
+      a.lbr = ctx->lbr.as<uint32_t>() + gi * lb_per_group;
+      a.lbm = ctx->lbm.as<uint32_t>() + gi * lb_per_group;
+      a.inc = ctx->inc.as<uint32_t>() + (size_t)gi * L.fpw;
     }
     a.bmax = plan->d_bmax.as<int32_t>();
     a.pathological = plan->pathological ? 1 : 0;
-    a.rt = ctx->rt_search.as<uint64_t>() + (size_t)gi * L.nr * L.fpw;
-    a.rts = ctx->rt_split.as<uint64_t>() + (size_t)gi * L.nr * L.fpw;
+    a.rt = ctx->rt_search.as<uint32_t>() + (size_t)gi * L.nr * L.fpw;
+    a.rts = ctx->rt_split.as<uint32_t>() + (size_t)gi * L.nr * L.fpw;
     a.rs = step == 2 ? ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw : nullptr;
-    a.budget = ctx->budget.as<uint64_t>() + (size_t)gi * L.fpw;
+    a.budget = ctx->budget.as<int64_t>() + (size_t)gi * L.fpw;
     a.lanes = reinterpret_cast<LaneBest*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
     a.snaps = ctx->snaps.as<uint8_t>() + snap_bytes * gi;
     if (prune && step == 1 && mine > 1) {
@@ -350,8 +362,8 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
       a.k_begin = 0;
       a.n_items = seed_items;
       search_launch(L.fpw, step, a, blocks, st);
-      uint64_t* frozen = ctx->seed_inc.as<uint64_t>() + (size_t)gi * L.fpw;
-      SCB_CUDA(cudaMemcpyAsync(frozen, a.inc, L.fpw * sizeof(uint64_t),
+      uint32_t* frozen = ctx->seed_inc.as<uint32_t>() + (size_t)gi * L.fpw;
+      SCB_CUDA(cudaMemcpyAsync(frozen, a.inc, L.fpw * sizeof(uint32_t),
                                cudaMemcpyDeviceToDevice, st));
       a.seed_inc = frozen;
       a.k_begin = seed_items;
@@ -365,27 +377,28 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     const int fig = std::min(L.fpw, L.frames - gi * L.fpw);
     finalize_launch(step, cfg.n_slices, L.fpw, fig, warps, a.lanes, a.snaps, a.count_out,
                     a.scored_out, cfg.lambda,
+                    ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr,
+                    ctx->nvals.as<uint32_t>() + (size_t)gi * L.fpw, L.nr,
                     fb + (size_t)gi * L.fpw,
-                    step == 1 ? ctx->budget.as<uint64_t>() + (size_t)gi * L.fpw : nullptr, st);
+                    step == 1 ? ctx->budget.as<int64_t>() + (size_t)gi * L.fpw : nullptr, st);
   }
 }
 
-// Device budgets from host t_min values (constrained_clustering with a
-// caller-supplied t_min; budget = t_min * (1.0 + lambda), search.cpp:344).
+// Device budget keys from caller t_min values (constrained_clustering with a
+// caller-supplied t_min; budget = t_min * (1.0 + lambda), search.cpp:344):
+// the doubles are computed here, then mapped to time keys on the device.
 void upload_budgets(sc_ctx* ctx, const Layouts& L, const double* t_min, double lambda,
                     cudaStream_t st) {
-  ctx->h_budget.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
-  uint64_t* b = ctx->h_budget.as<uint64_t>();
-  std::memset(b, 0, (size_t)L.groups * L.fpw * sizeof(uint64_t));
-  for (int f = 0; f < L.frames; ++f) {
-    const double v = t_min[f] * (1.0 + lambda);
-    uint64_t bits;
-    std::memcpy(&bits, &v, 8);
-    b[f] = (v > 0.0) ? bits : 0;
-  }
-  ctx->budget.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
-  SCB_CUDA(cudaMemcpyAsync(ctx->budget.p, b, (size_t)L.groups * L.fpw * sizeof(uint64_t),
+  ctx->h_budget.ensure((size_t)L.frames * sizeof(double));
+  double* b = ctx->h_budget.as<double>();
+  SCB_CUDA(cudaMemcpy(b, t_min, (size_t)L.frames * sizeof(double), cudaMemcpyDefault));
+  for (int f = 0; f < L.frames; ++f) b[f] = b[f] * (1.0 + lambda);
+  ctx->budget_f64.ensure((size_t)L.frames * sizeof(double));
+  SCB_CUDA(cudaMemcpyAsync(ctx->budget_f64.p, b, (size_t)L.frames * sizeof(double),
                            cudaMemcpyHostToDevice, st));
+  ctx->budget.ensure((size_t)L.groups * L.fpw * sizeof(int64_t));
+  budget_keys_device(ctx->budget_f64.as<double>(), ctx->vals.as<uint64_t>(),
+                     ctx->nvals.as<uint32_t>(), L.nr, L.frames, ctx->budget.as<int64_t>(), st);
 }
 
 double bits_to_double(uint64_t b) {
@@ -538,7 +551,8 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
 
 sc_ctx::~sc_ctx() {
   for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rt_split, &rs_search, &usat,
-                  &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc})
+                  &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc, &rt_bits, &vals, &nvals, &budget_f64, &rk_idx, &rk_sorted,
+                  &rk_flags, &rk_offsets, &rk_temp})
     b->release();
   h_stage.release();
   h_records.release();

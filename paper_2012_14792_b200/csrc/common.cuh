@@ -133,18 +133,18 @@ struct SearchArgs {
   uint32_t item_stride;
   uint32_t* counter;
   const int32_t* bmax;    // bmax[A] | aneed[A] | mstar[(cols+1)*(rows+1)], A = max_area+1
-  const uint64_t* rt;     // [NR][FPW] clamped time bits, this frame group
-  const uint64_t* rts;    // [NR][FPW] split table (run + forced rest of its column)
+  const uint32_t* rt;     // [NR][FPW] time keys (rank.cu), this frame group
+  const uint32_t* rts;    // [NR][FPW] split table (run + forced rest of its column)
   const double* rs;       // [NR][FPW] SSE (step 2)
-  const uint64_t* budget; // [FPW] budget bits (step 2)
+  const int64_t* budget;  // [FPW] step-2 budget keys (-1: nothing feasible)
   LaneBest* lanes;        // [warps * 32]
   uint8_t* snaps;         // [warps * 32][kSnapBytes]
   unsigned long long* count_out;
   unsigned long long* scored_out;  // candidate-frame scores actually evaluated
-  const uint64_t* lbr;             // pruned mode: column lower bounds (search_walk.cuh)
-  const uint64_t* lbm;
-  uint64_t* inc;                   // pruned mode: shared step-1 incumbent [FPW]
-  const uint64_t* seed_inc;        // pruned mode, phase B: incumbent frozen after phase A
+  const uint32_t* lbr;             // pruned mode: column lower bounds (search_walk.cuh)
+  const uint32_t* lbm;
+  uint32_t* inc;                   // pruned mode: shared step-1 incumbent [FPW]
+  const uint32_t* seed_inc;        // pruned mode, phase B: incumbent frozen after phase A
 };
 
 // Device-side per-frame result written by finalize.
@@ -175,6 +175,8 @@ struct sc_ctx {
   // staging / tables
   scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rt_split, rs_search, usat;
   scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec, lbr, lbm, inc, seed_inc;
+  scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
+  scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp;       // rank.cu scratch
   int dec_cols = -1, dec_rows = -1;
   scb::HostBuf h_stage, h_records, h_frame_best, h_budget;
   std::vector<scb::Plan*> plans;

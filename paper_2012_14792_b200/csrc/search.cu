@@ -97,21 +97,21 @@ __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(Se
   const int slot = lane / FPW;
   const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   LaneState st;
-  st.best_t = ~0ull;
+  st.best_t = kKeyInf;
   st.best_item = ~0ull;
   st.best_ord = ~0ull;
   st.best_sse = __longlong_as_double(0x7ff0000000000000ll);
   if (a.resume) {  // second phase of a seeded launch: keep this lane's best
     const LaneBest prev = a.lanes[(size_t)gwarp * 32 + lane];
-    st.best_t = prev.t;
+    st.best_t = (tkey)prev.t;
     st.best_item = prev.item;
     st.best_ord = prev.ord;
     st.best_sse = prev.sse;
   }
-  st.budget = STEP == 2 ? a.budget[f] : 0;
+  st.budget = STEP == 2 ? a.budget[f] : -1;
   st.count = 0;
   st.scored = 0;
-  st.inc = ~0ull;
+  st.inc = kKeyInf;
   st.snap = a.snaps + ((size_t)gwarp * 32 + lane) * kSnapBytes;
   for (;;) {
     uint32_t k = 0;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(Se
     __syncwarp();
   }
   LaneBest lb;
-  lb.t = st.best_t;
+  lb.t = st.best_t == kKeyInf ? ~0ull : (uint64_t)st.best_t;
   lb.sse = st.best_sse;
   lb.item = st.best_item;
   lb.ord = st.best_ord;
@@ -136,9 +136,9 @@ __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(Se
 }
 
 // ---- pruned mode: per-frame column lower bounds (search_walk.cuh) -------------
-__global__ void k_column_bounds(const uint64_t* __restrict__ rt, int fpw, int frames_in_group,
-                                int cols, int rows, int rmax, int rstride, uint64_t* lbr,
-                                uint64_t* lbm) {
+__global__ void k_column_bounds(const uint32_t* __restrict__ rt, int fpw, int frames_in_group,
+                                int cols, int rows, int rmax, int rstride, uint32_t* lbr,
+                                uint32_t* lbm) {
   const int nxw = cols * (cols + 1) / 2;
   const int nyh = rows * (rows + 1) / 2;
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
@@ -149,8 +149,8 @@ __global__ void k_column_bounds(const uint64_t* __restrict__ rt, int fpw, int fr
   column_bounds(rt, fpw, f, rows, xw * nyh, rmax, lbr + off, lbm + off, (size_t)fpw);
 }
 
-void column_bounds_launch(const uint64_t* rt, int fpw, int frames_in_group, int cols, int rows,
-                          int rmax, int rstride, uint64_t* lbr, uint64_t* lbm, cudaStream_t st) {
+void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int cols, int rows,
+                          int rmax, int rstride, uint32_t* lbr, uint32_t* lbm, cudaStream_t st) {
   const int nxw = cols * (cols + 1) / 2;
   const int threads = 128, total = nxw * fpw;
   k_column_bounds<<<(total + threads - 1) / threads, threads, 0, st>>>(
@@ -180,11 +180,24 @@ __device__ __forceinline__ bool lane_less(int step, int n, const LaneBest& x, ui
   return xi < yi;
 }
 
+__device__ __forceinline__ int64_t budget_key_f(const uint64_t* vals, uint32_t n, double b) {
+  if (!(b >= 0.0)) return -1;
+  const uint64_t bits = (uint64_t)__double_as_longlong(b);
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (vals[mid] <= bits) lo = mid + 1;
+    else hi = mid;
+  }
+  return (int64_t)lo - 1;
+}
+
 __global__ void k_finalize(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
                            const LaneBest* __restrict__ lanes, const uint8_t* __restrict__ snaps,
                            const unsigned long long* count, const unsigned long long* scored,
-                           double lambda, FrameBest* __restrict__ out,
-                           uint64_t* __restrict__ budget_out) {
+                           double lambda, const uint64_t* __restrict__ vals,
+                           const uint32_t* __restrict__ nvals, size_t nr,
+                           FrameBest* __restrict__ out, int64_t* __restrict__ budget_out) {
   const int f = blockIdx.x;
   if (f >= frames_in_group) return;
   __shared__ LaneBest sb[256];
@@ -218,19 +231,20 @@ __global__ void k_finalize(int step, int n, int fpw, int frames_in_group, uint32
   if (threadIdx.x == 0) win = si[0];
   __syncthreads();
   FrameBest* o = out + f;
+  const uint64_t* fv = vals + (size_t)f * nr;  // this frame's key -> time bits
   if (threadIdx.x == 0) {
-    o->t = sb[0].t;
+    o->t = win == 0xffffffffu ? ~0ull : fv[sb[0].t];
     o->sse = sb[0].sse;
     o->item = sb[0].item;
     o->ord = sb[0].ord;
     o->count = *count;
     o->scored = *scored;
     o->found = (win == 0xffffffffu) ? 0 : 1;
-    if (budget_out && step == 1) {
-      // budget = t_min * (1.0 + lambda)   (search.cpp:344)
-      const double tmin = __longlong_as_double((long long)sb[0].t);
+    if (budget_out && step == 1 && win != 0xffffffffu) {
+      // budget = t_min * (1.0 + lambda)   (search.cpp:344), as a time key
+      const double tmin = __longlong_as_double((long long)fv[sb[0].t]);
       const double b = __dmul_rn(tmin, __dadd_rn(1.0, lambda));
-      budget_out[f] = (b > 0.0) ? (uint64_t)__double_as_longlong(b) : 0ull;
+      budget_out[f] = budget_key_f(fv, nvals[f], b);
     }
   }
   if (win != 0xffffffffu)
@@ -295,9 +309,11 @@ void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStrea
 void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
                      const LaneBest* lanes, const uint8_t* snaps,
                      const unsigned long long* count, const unsigned long long* scored,
-                     double lambda, FrameBest* out, uint64_t* budget_out, cudaStream_t st) {
+                     double lambda, const uint64_t* vals, const uint32_t* nvals, size_t nr,
+                     FrameBest* out, int64_t* budget_out, cudaStream_t st) {
   k_finalize<<<frames_in_group, 256, 0, st>>>(step, n, fpw, frames_in_group, n_warps, lanes, snaps,
-                                              count, scored, lambda, out, budget_out);
+                                              count, scored, lambda, vals, nvals, nr, out,
+                                              budget_out);
   SCB_CUDA(cudaGetLastError());
 }
 

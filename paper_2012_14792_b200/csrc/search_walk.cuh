@@ -51,6 +51,14 @@ SCB_HD int imin(int a, int b) { return a < b ? a : b; }
 SCB_HD int imax(int a, int b) { return a > b ? a : b; }
 SCB_HD uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 
+// Time key: the exact per-frame RANK of a (clamped) time among all rectangle
+// times of that frame.  Ranks are an injective, order-preserving image of the
+// doubles, so max / < / <= on keys equal max / < / <= on the times
+// (DESIGN.md §Search); 32 bits instead of 64 halve the table traffic.
+typedef uint32_t tkey;
+constexpr tkey kKeyInf = 0xffffffffu;
+SCB_HD tkey kmax(tkey a, tkey b) { return a > b ? a : b; }
+
 SCB_HD int xw_of(int cols, int x0, int w) { return x0 * cols - (x0 * (x0 - 1)) / 2 + (w - 1); }
 SCB_HD int yh_of(int rows, int y0, int h) { return y0 * rows - (y0 * (y0 - 1)) / 2 + (h - 1); }
 
@@ -72,45 +80,46 @@ struct WalkEnv {
   const int32_t* ybase;   // [rows+1]: yh(y, 1), the first rectangle starting at row y
   const int32_t* rq;      // [rows+1]: rows / r (no integer division in the runs DFS)
   const int32_t* sfx;     // [rows+1]: yh(y, rows - y), the rectangle from row y to the bottom
-  const uint64_t* rt;     // [NR][FPW] clamped f64 time bits of every rectangle
-  const uint64_t* rts;    // [NR][FPW] split table: at rect(x0,w,y0,h) with y0+h < rows,
+  const tkey* rt;         // [NR][FPW] time key of every rectangle
+  const tkey* rts;        // [NR][FPW] split table: at rect(x0,w,y0,h) with y0+h < rows,
                           // max(time(y0,h), time(y0+h, rows-y0-h)) -- a run plus the
                           // forced rest of its column in one load
   const double* rs;       // [NR][FPW] SSE of every rectangle (step 2)
   // pruned mode only: per-frame lower bounds on a column's slowest slice,
   // lbr[(xw*rstride + r)*FPW + f] for exactly r runs and lbm[...] for any
   // r' <= r (prefix minimum); inc[f] is the shared step-1 incumbent.
-  const uint64_t* lbr;
-  const uint64_t* lbm;
-  uint64_t* inc;
+  const tkey* lbr;
+  const tkey* lbm;
+  tkey* inc;
   // incumbent frozen after the seed phase (or nullptr): its candidate precedes
   // every item still to walk, so a tie with it can never win -> prune P >= it
-  const uint64_t* seed_inc;
+  const tkey* seed_inc;
 };
 
 // One lane's running first-in-order best and its candidate snapshot.
 struct LaneState {
-  uint64_t best_t, best_item, best_ord;
+  tkey best_t;
+  uint64_t best_item, best_ord;
   double best_sse;
-  uint64_t budget;  // step 2: t_min * (1 + lambda) as f64 bits
+  int64_t budget;   // step 2: largest key whose time is <= t_min * (1 + lambda), -1: none
   uint64_t count;   // candidates enumerated (uniform over the warp)
   uint64_t scored;  // candidates this lane actually scored
-  uint64_t inc;     // last seen shared incumbent (pruned step 1)
+  tkey inc;         // last seen shared incumbent (pruned step 1)
   uint8_t* snap;
 };
 
 // Shared incumbent: a candidate with time t exists for this frame, so no
 // candidate slower than t can win (equal ones still can: first in order).
-SCB_HD uint64_t incumbent_load(uint64_t* p) {
+SCB_HD tkey incumbent_load(tkey* p) {
 #ifdef __CUDA_ARCH__
-  return *(volatile uint64_t*)p;
+  return *(volatile tkey*)p;
 #else
   return *p;
 #endif
 }
-SCB_HD void incumbent_offer(uint64_t* p, uint64_t t) {
+SCB_HD void incumbent_offer(tkey* p, tkey t) {
 #ifdef __CUDA_ARCH__
-  atomicMin((unsigned long long*)p, (unsigned long long)t);
+  atomicMin((unsigned int*)p, (unsigned int)t);
 #else
   if (t < *p) *p = t;
 #endif
@@ -120,21 +129,21 @@ SCB_HD void incumbent_offer(uint64_t* p, uint64_t t) {
 // runs, for every r <= rmax: min over all compositions (area constraint
 // relaxed) of the max run time, by a DP over rows.  lbr/lbm are written at
 // [r * stride] (lbm: prefix minimum over r).  Times are clamped f64 bits.
-SCB_HD void column_bounds(const uint64_t* rt, int fpw, int f, int rows, int base, int rmax,
-                          uint64_t* lbr, uint64_t* lbm, size_t stride) {
-  uint64_t prev[256], cur[256];
-  const uint64_t INF = ~0ull;
+SCB_HD void column_bounds(const tkey* rt, int fpw, int f, int rows, int base, int rmax,
+                          tkey* lbr, tkey* lbm, size_t stride) {
+  tkey prev[256], cur[256];
+  const tkey INF = kKeyInf;
   for (int y = 0; y <= rows; ++y) prev[y] = y == 0 ? 0 : INF;
-  uint64_t run_min = INF;
+  tkey run_min = INF;
   lbr[0] = INF;
   lbm[0] = INF;
   for (int r = 1; r <= rmax; ++r) {
     for (int y = 0; y <= rows; ++y) {
-      uint64_t best = INF;
+      tkey best = INF;
       for (int y0 = r - 1; y0 < y; ++y0) {
         if (prev[y0] == INF) continue;
-        const uint64_t v = rt[(size_t)(base + yh_of(rows, y0, y - y0)) * fpw + f];
-        const uint64_t m = prev[y0] > v ? prev[y0] : v;
+        const tkey v = rt[(size_t)(base + yh_of(rows, y0, y - y0)) * fpw + f];
+        const tkey m = prev[y0] > v ? prev[y0] : v;
         if (m < best) best = m;
       }
       cur[y] = best;
@@ -188,7 +197,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
                       LaneState& st) {
   constexpr int J = 32 / FPW;
   const int rows = e.rows, cols = e.cols, nyh = e.nyh;
-  const uint64_t* rt = e.rt;
+  const tkey* rt = e.rt;
   const double* rs = e.rs;
   const int c = wi.c, d = wi.d;
   uint64_t ord = 0;  // ordinal of the next candidate inside this item
@@ -198,7 +207,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   uint8_t curH[SC_MAX_SLICES];
   uint8_t Lcol[kMaxLevels], Lrun[kMaxLevels], Ly0[kMaxLevels], Lh[kMaxLevels], Lhi[kMaxLevels];
   int32_t Amin[kMaxLevels], Amax[kMaxLevels], Lbase[kMaxLevels];
-  uint64_t Pin[kMaxLevels];
+  tkey Pin[kMaxLevels];
 
   auto thresholds = [&](int amin, int amax, int win_lo, int win_hi) -> Thr {
     Thr t;
@@ -208,7 +217,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     t.t1 = imin(t.t1, win_hi);
     return t;
   };
-  auto rt_at = [&](int x0, int w, int y0, int h) -> uint64_t {
+  auto rt_at = [&](int x0, int w, int y0, int h) -> tkey {
     return rt[(size_t)(xw_of(cols, x0, w) * nyh + yh_of(rows, y0, h)) * FPW + f];
   };
   // Every multi-run column from `from` on can still be filled with runs of
@@ -256,21 +265,22 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     return tot;
   };
   // can a subtree whose fixed slices already reach time P still win?
-  const uint64_t seed_inc = (STEP == 1 && PRUNE && e.seed_inc) ? e.seed_inc[f] : ~0ull;
-  auto viable = [&](uint64_t P) -> bool {
+  const tkey seed_inc = (STEP == 1 && PRUNE && e.seed_inc) ? e.seed_inc[f] : kKeyInf;
+  auto viable = [&](tkey P) -> bool {
     return !PRUNE ||
-           (STEP == 1 ? (P < st.best_t && P <= st.inc && P < seed_inc) : (P <= st.budget));
+           (STEP == 1 ? (P < st.best_t && P <= st.inc && P < seed_inc)
+                      : ((int64_t)P <= st.budget));
   };
   if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
   // lower bound of column (x0, w) with r runs (exact r) / any r' <= r
-  auto lb_r = [&](int x0, int w, int r) -> uint64_t {
+  auto lb_r = [&](int x0, int w, int r) -> tkey {
     return e.lbr[((size_t)xw_of(cols, x0, w) * e.rstride + r) * FPW + f];
   };
-  auto lb_m = [&](int x0, int w, int r) -> uint64_t {
+  auto lb_m = [&](int x0, int w, int r) -> tkey {
     return e.lbm[((size_t)xw_of(cols, x0, w) * e.rstride + r) * FPW + f];
   };
   // score one candidate (strict comparisons keep the first in order)
-  auto score = [&](uint64_t t, uint64_t o, int lr, int lh, int lrest) {
+  auto score = [&](tkey t, uint64_t o, int lr, int lh, int lrest) {
     if (PRUNE) ++st.scored;
     if (STEP == 1) {
       if (t < st.best_t) {
@@ -280,7 +290,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         take_snapshot(lr, lh, lrest);
         if (PRUNE) incumbent_offer(e.inc + f, t);
       }
-    } else if (t <= st.budget) {
+    } else if ((int64_t)t <= st.budget) {
       const double s = layout_sse(lr, lh, lrest);
       if (s < st.best_sse || (s == st.best_sse && t < st.best_t)) {
         st.best_sse = s;
@@ -298,7 +308,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   //      cannot complete and are skipped.
   const int rmax_c = imin(e.n - c + 1, rows);
   int WL[SC_MAX_COLS + 1], WH[SC_MAX_COLS + 1];
-  uint64_t PW[SC_MAX_COLS + 1];  // pruned mode: max of the columns' lower bounds
+  tkey PW[SC_MAX_COLS + 1];  // pruned mode: max of the columns' lower bounds
   X0[0] = 0;
   WL[0] = 1;
   WH[0] = e.max_area;
@@ -311,7 +321,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     WH[i + 1] = imin(WH[i], W[i] * rows);
     ok = WL[i + 1] <= WH[i + 1];
     if (PRUNE) {
-      PW[i + 1] = umax64(PW[i], lb_m(X0[i], W[i], rmax_c));
+      PW[i + 1] = kmax(PW[i], lb_m(X0[i], W[i], rmax_c));
       ok = ok && viable(PW[i + 1]);
     }
   }
@@ -336,7 +346,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         const int nH = imin(WH[pos], wv * rows);
         if (nL > nH) continue;
         if (PRUNE) {
-          PW[pos + 1] = umax64(PW[pos], lb_m(X0[pos], wv, rmax_c));
+          PW[pos + 1] = kmax(PW[pos], lb_m(X0[pos], wv, rmax_c));
           if (!viable(PW[pos + 1])) continue;
         }
         X0[pos + 1] = X0[pos] + wv;
@@ -359,7 +369,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     //      slides down as r grows, so the feasible r of a position form one
     //      contiguous range.
     int RL[SC_MAX_COLS], RH[SC_MAX_COLS], SL[SC_MAX_COLS];
-    uint64_t PR[SC_MAX_COLS + 1];  // pruned mode: widths bound, tightened per exact r
+    tkey PR[SC_MAX_COLS + 1];  // pruned mode: widths bound, tightened per exact r
     PR[0] = PRUNE ? PW[c] : 0;
     int rp = 0;
     RL[0] = 1;
@@ -391,7 +401,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       const int nL = imax(RL[rp], lo), nH = imin(RH[rp], hi);
       if (nL > nH) continue;
       if (PRUNE) {
-        PR[rp + 1] = umax64(PR[rp], lb_r(X0[rp], W[rp], r));
+        PR[rp + 1] = kmax(PR[rp], lb_r(X0[rp], W[rp], r));
         if (!viable(PR[rp + 1])) continue;
       }
       if (rp < c - 1) {
@@ -426,9 +436,9 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         }
         run += R[i];
       }
-      uint64_t P = 0;
+      tkey P = 0;
       for (int i = 0; i < c; ++i)
-        if (R[i] == 1) P = umax64(P, rt_at(X0[i], W[i], 0, rows));
+        if (R[i] == 1) P = kmax(P, rt_at(X0[i], W[i], 0, rows));
       if (nl == 0) {  // the skeleton is a single candidate
         if (slot == 0 && viable(P)) score(P, ord, -1, 0, 0);
         ord += 1;
@@ -451,7 +461,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       }
       while (true) {
         int lv;  // level whose state feeds the leaf loop
-        uint64_t Pl;
+        tkey Pl;
         int amin_l, amax_l, y0l;
         if (leaf_now) {
           lv = 0;
@@ -485,15 +495,15 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           curH[ridx] = (uint8_t)h;
           const int lb = Lbase[l];
           const size_t ri = (size_t)(lb + e.ybase[y0] + h - 1) * FPW + f;
-          uint64_t Pn;
+          tkey Pn;
           if (forced) {
             const int a2 = w * (rows_left - h);
             na = imin(na, a2);
             nx = imax(nx, a2);
             curH[ridx + 1] = (uint8_t)(rows_left - h);
-            Pn = umax64(Pin[l], e.rts[ri]);
+            Pn = kmax(Pin[l], e.rts[ri]);
           } else {
-            Pn = umax64(Pin[l], rt[ri]);
+            Pn = kmax(Pin[l], rt[ri]);
           }
           if (!viable(Pn)) continue;
           const int nxt = l + 1;
@@ -539,13 +549,13 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             // the split table holds max(run h, forced rest) at the run's own
             // rectangle index, which advances by +1 per h; lanes step h by J.
             int h = lo + slot;
-            const uint64_t* p = e.rts + (size_t)(xwb + e.ybase[y0l] + h - 1) * FPW + f;
-            uint64_t v = *p;
+            const tkey* p = e.rts + (size_t)(xwb + e.ybase[y0l] + h - 1) * FPW + f;
+            tkey v = *p;
             while (true) {
               const int hn = h + J;
               const bool more = hn <= hi;
-              const uint64_t vn = more ? p[J * FPW] : 0;  // prefetch the next height
-              score(umax64(Pl, v), ord + (uint64_t)(h - lo), lr, h, rows_left - h);
+              const tkey vn = more ? p[J * FPW] : 0;  // prefetch the next height
+              score(kmax(Pl, v), ord + (uint64_t)(h - lo), lr, h, rows_left - h);
               if (!more) break;
               h = hn;
               p += J * FPW;

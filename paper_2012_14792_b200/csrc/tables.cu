@@ -127,7 +127,9 @@ __global__ void k_rect_tables(const double* __restrict__ sat, const uint64_t* __
       if (rect_t) rect_t[(size_t)f * nr + rr] = t;
       // layout_time's running max starts at 0.0 and keeps it on ties/NaN
       // (search.cpp:77-83): clamp to +0.0 so u64 bit order == double order.
-      if (rt_search) rt_search[so] = (t > 0.0) ? (uint64_t)__double_as_longlong(t) : 0ull;
+      // Frame-major bits, ranked into time keys by rank.cu.
+      if (rt_search) rt_search[(size_t)f * nr + rr] =
+          (t > 0.0) ? (uint64_t)__double_as_longlong(t) : 0ull;
     }
     if (usat) {
       const uint64_t* U = usat + (size_t)f * 3 * nsat;
@@ -145,9 +147,9 @@ __global__ void k_rect_tables(const double* __restrict__ sat, const uint64_t* __
 // with y0+h < rows, max(time(y0,h), time(y0+h, rows-y0-h)), i.e. a run and
 // the forced remainder of its column, so the search scores a two-run split
 // with one load.  Same [group][rect][FPW] layout as the time table.
-__global__ void k_split_table(const uint64_t* __restrict__ rt, int cols, int rows,
+__global__ void k_split_table(const uint32_t* __restrict__ rt, int cols, int rows,
                               size_t slots /* groups * fpw */, int fpw,
-                              uint64_t* __restrict__ rts) {
+                              uint32_t* __restrict__ rts) {
   const int nyh = rows * (rows + 1) / 2;
   const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
   const size_t total = nr * slots;
@@ -162,20 +164,20 @@ __global__ void k_split_table(const uint64_t* __restrict__ rt, int cols, int row
     while (y0 + 1 < rows && (y0 + 1) * rows - ((y0 + 1) * y0) / 2 <= yh) ++y0;
     const int h = yh - (y0 * rows - (y0 * (y0 - 1)) / 2) + 1;
     const size_t base = g * nr * fpw;
-    uint64_t v = 0;
+    uint32_t v = 0;
     if (y0 + h < rows) {
-      const uint64_t a = rt[base + (size_t)rr * fpw + slot];
+      const uint32_t a = rt[base + (size_t)rr * fpw + slot];
       const int y1 = y0 + h, h1 = rows - y1;
       const int rr2 = xw * nyh + (y1 * rows - (y1 * (y1 - 1)) / 2 + h1 - 1);
-      const uint64_t b = rt[base + (size_t)rr2 * fpw + slot];
+      const uint32_t b = rt[base + (size_t)rr2 * fpw + slot];
       v = a > b ? a : b;
     }
     rts[base + (size_t)rr * fpw + slot] = v;
   }
 }
 
-void split_table_device(const uint64_t* d_rt, int cols, int rows, int groups, int fpw,
-                        uint64_t* d_rts, int sm_count, cudaStream_t st) {
+void split_table_device(const uint32_t* d_rt, int cols, int rows, int groups, int fpw,
+                        uint32_t* d_rts, int sm_count, cudaStream_t st) {
   const size_t total = (size_t)cols * (cols + 1) / 2 * (rows * (rows + 1) / 2) * groups * fpw;
   size_t blocks = (total + 255) / 256;
   const size_t cap = (size_t)sm_count * 16;

@@ -46,20 +46,31 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
     sfx[y] = y < rows ? yh_of(rows, y, rows - y) : 0;
   }
   const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
-  std::vector<uint64_t> rt(nr * fpw, 0);
+  // time keys: per-frame exact ranks of the clamped rectangle times (api.cu
+  // ranks on the device); vals[f] maps a rank back to its time bits
+  std::vector<tkey> rt(nr * fpw, 0);
   std::vector<double> rs(nr * fpw, 0.0);
-  for (int f = 0; f < frames; ++f)
+  std::vector<std::vector<uint64_t>> vals(fpw);
+  for (int f = 0; f < frames; ++f) {
+    std::vector<uint64_t> bits(nr);
     for (size_t r = 0; r < nr; ++r) {
       const double t = rect_time[(size_t)f * nr + r];
-      uint64_t bits;
-      std::memcpy(&bits, &t, 8);
-      rt[r * fpw + f] = (t > 0.0) ? bits : 0;
+      uint64_t b;
+      std::memcpy(&b, &t, 8);
+      bits[r] = (t > 0.0) ? b : 0;
       if (rect_sse) rs[r * fpw + f] = rect_sse[(size_t)f * nr + r];
     }
+    vals[f] = bits;
+    std::sort(vals[f].begin(), vals[f].end());
+    vals[f].erase(std::unique(vals[f].begin(), vals[f].end()), vals[f].end());
+    for (size_t r = 0; r < nr; ++r)
+      rt[r * fpw + f] =
+          (tkey)(std::lower_bound(vals[f].begin(), vals[f].end(), bits[r]) - vals[f].begin());
+  }
   // pruned mode: per-frame column lower bounds, shared incumbents
   const int nxw = cols * (cols + 1) / 2;
-  std::vector<uint64_t> lbr((size_t)nxw * rstride * fpw, 0), lbm((size_t)nxw * rstride * fpw, 0);
-  std::vector<uint64_t> inc(fpw, ~0ull);
+  std::vector<tkey> lbr((size_t)nxw * rstride * fpw, 0), lbm((size_t)nxw * rstride * fpw, 0);
+  std::vector<tkey> inc(fpw, kKeyInf);
   if (prune)
     for (int xw = 0; xw < nxw; ++xw)
       for (int f = 0; f < frames; ++f) {
@@ -68,7 +79,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
                       lbm.data() + off, (size_t)fpw);
       }
   // split table (tables.cu k_split_table): max(run, forced rest of the column)
-  std::vector<uint64_t> rts(nr * fpw, 0);
+  std::vector<tkey> rts(nr * fpw, 0);
   for (int xw = 0; xw < cols * (cols + 1) / 2; ++xw)
     for (int y0 = 0; y0 < rows; ++y0)
       for (int h = 1; y0 + h < rows; ++h)
@@ -102,7 +113,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.lbm = lbm.data();
   e.inc = inc.data();
   e.seed_inc = nullptr;
-  std::vector<uint64_t> frozen(fpw, ~0ull);
+  std::vector<tkey> frozen(fpw, kKeyInf);
   // seeded pruned step 1 like api.cu: phase A = the first seed_items items
   size_t seed_items = 0;
   for (const WorkItem& wi : items) {
@@ -115,20 +126,24 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   for (int wp = 0; wp < warps; ++wp)
     for (int l = 0; l < 32; ++l) {
       LaneState& s = st[(size_t)wp * 32 + l];
-      s.best_t = ~0ull;
+      s.best_t = kKeyInf;
       s.best_item = ~0ull;
       s.best_ord = ~0ull;
       s.best_sse = INFINITY;
       s.count = 0;
       s.scored = 0;
-      s.inc = ~0ull;
+      s.inc = kKeyInf;
       s.snap = &snaps[((size_t)wp * 32 + l) * kSnap];
-      s.budget = 0;
-      if (step == 2 && (l % fpw) < frames) {
+      s.budget = -1;
+      if (step == 2 && (l % fpw) < frames) {  // largest key whose time is <= budget
         const double b = budget[l % fpw];
-        uint64_t bits;
-        std::memcpy(&bits, &b, 8);
-        s.budget = (b > 0.0) ? bits : 0;
+        s.budget = -1;  // nothing feasible (negative or NaN budget)
+        if (b >= 0.0) {
+          uint64_t bits;
+          std::memcpy(&bits, &b, 8);
+          const auto& v = vals[l % fpw];
+          s.budget = (int64_t)(std::upper_bound(v.begin(), v.end(), bits) - v.begin()) - 1;
+        }
       }
     }
   size_t kk = 0;
@@ -190,7 +205,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
     }
     out_count[f] = cnt;
     if (win >= 0) {
-      std::memcpy(&out_t[f], &st[win].best_t, 8);
+      std::memcpy(&out_t[f], &vals[f][st[win].best_t], 8);
       out_sse[f] = st[win].best_sse;
       std::memcpy(out_snap + (size_t)f * kSnap, st[win].snap, kSnap);
       out_item[f] = st[win].best_item;
