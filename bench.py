@@ -122,6 +122,15 @@ def make_inputs(w, rank, frames, pinned=True):
     return luma_t, est_t
 
 
+def kernel_src_sha():
+    """Hash of the search-kernel sources an ncu instruction count belongs to."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("search_walk.cuh", "search.cu", "rank.cu", "plan.h"):
+        h.update(open(os.path.join(ROOT, "paper_2012_14792_b200", "csrc", f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 # ---- our arm -------------------------------------------------------------------------
 def run_ours(args):
     import ctypes as C
@@ -175,6 +184,8 @@ def run_ours(args):
     # ---- warm-up (device-resident) ----
     for _ in range(max(args.warmup, 0)):
         call(luma_d.data_ptr(), est_d.data_ptr())
+    if args.warmup <= 0:
+        call(luma_d.data_ptr(), est_d.data_ptr())  # counts for the metric
     cands = sum(r.candidates_step1 + r.candidates_step2 for r in res)
     counts = sorted({(r.candidates_step1, r.candidates_step2) for r in res})
 
@@ -230,7 +241,11 @@ def run_ours(args):
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "search_issue.json")))
         key = f"cfg{args.config}_mode{args.mode}"
-        if key in prof:
+        if key in prof and prof[key].get("kernel_src_sha") != kernel_src_sha():
+            issue = {"bound": "alu", "achieved": None, "peak": None, "unit": "Gwarp-inst/s",
+                     "frac": None, "traffic": None,
+                     "note": "committed ncu instruction count is for an older kernel source"}
+        elif key in prof:
             p = prof[key]
             clk = ck.get("sm_mhz") or p.get("sm_mhz_ncu") or 1965.0
             sms = torch.cuda.get_device_properties(local).multi_processor_count

@@ -282,6 +282,16 @@ void enqueue_moment_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool
                      ctx->rs_search.as<double>(), ctx->sm_count, st);
 }
 
+// Exhaustive mode, step 2: walk only the subtrees whose partial time can still
+// meet the budget.  Exact: a subtree whose fixed slices already exceed the
+// budget holds no feasible candidate, and step 1 evaluated the time of every
+// candidate of the family.  SLICECRAFT_B200_STEP2_BOUND=0 walks them all.
+bool step2_bounded(const sc_search_cfg& cfg) {
+  if (cfg.mode != SC_MODE_EXHAUSTIVE) return false;
+  const char* v = getenv("SLICECRAFT_B200_STEP2_BOUND");
+  return !(v && v[0] == '0');
+}
+
 // One search step over all frame groups; finalize writes FrameBest[step] and,
 // after step 1, the device budgets of step 2.  No host synchronisation.
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
@@ -305,7 +315,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
   const uint32_t rank = (uint32_t)ctx->shard_rank, world = (uint32_t)ctx->shard_world;
   const uint32_t mine = total > rank ? (total - rank + world - 1) / world : 0;
   FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)(step - 1) * L.groups * L.fpw;
-  const bool prune = cfg.mode == SC_MODE_PRUNED;
+  const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
   const int rstride = std::min(cfg.n_slices, g.rows) + 1;
   const size_t lb_per_group = (size_t)n_xw(g.cols) * rstride * L.fpw;
   if (prune) {
@@ -440,43 +450,58 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   // fork the side stream from the caller's stream
   SCB_CUDA(cudaEventRecord(ev[7], s));
   SCB_CUDA(cudaStreamWaitEvent(s2, ev[7], 0));
+  // With a host luma batch, the main stream goes first: its small est upload
+  // must not queue behind the luma copy on the copy engine, and step 1 then
+  // overlaps that copy.  Otherwise K1 goes first (it needs the SMs that the
+  // persistent step-1 walk would hold).
   const bool need_moments = do2;
-  SCB_CUDA(cudaEventRecord(ev[4], s2));
-  if (need_moments) {
-    ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
-    if (luma) {
-      const int W = g.frame_width, H = g.frame_height;
-      const size_t span = (size_t)(frames - 1) * fstride + pitch * (H - 1) + (size_t)W * bps;
-      const void* d_luma = luma;
-      if (!is_device_ptr(luma)) {
-        ctx->luma.ensure(span);
-        SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyDefault, s2));
-        d_luma = ctx->luma.p;
+  const bool main_first = need_moments && luma && !is_device_ptr(luma);
+  auto enqueue_main = [&] {
+    ctx->est.ensure((size_t)frames * cells * sizeof(double));
+    SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
+                             cudaMemcpyDefault, s));
+    enqueue_time_tables(ctx, g, L, false, s);
+    SCB_CUDA(cudaEventRecord(ev[1], s));
+    if (do1) enqueue_step(ctx, g, cfg, plan, L, 1, true, s);
+    else upload_budgets(ctx, L, t_min_in, cfg.lambda, s);
+    SCB_CUDA(cudaEventRecord(ev[2], s));
+  };
+  auto enqueue_side = [&] {
+    SCB_CUDA(cudaEventRecord(ev[4], s2));
+    if (need_moments) {
+      ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
+      if (luma) {
+        const int W = g.frame_width, H = g.frame_height;
+        const size_t span = (size_t)(frames - 1) * fstride + pitch * (H - 1) + (size_t)W * bps;
+        const void* d_luma = luma;
+        if (!is_device_ptr(luma)) {
+          ctx->luma.ensure(span);
+          SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyDefault, s2));
+          d_luma = ctx->luma.p;
+        }
+        SCB_CUDA(cudaEventRecord(ev[4], s2));
+        texture_moments_device(d_luma, bps, W, H, pitch, fstride, g.ctu_size, frames, g.cols, g.rows,
+                               ctx->records.as<sc_ctu_record>(), s2);
+      } else {
+        SCB_CUDA(cudaMemcpyAsync(ctx->records.p, records, cells * frames * sizeof(sc_ctu_record),
+                                 cudaMemcpyDefault, s2));
+        SCB_CUDA(cudaEventRecord(ev[4], s2));
       }
-      SCB_CUDA(cudaEventRecord(ev[4], s2));
-      texture_moments_device(d_luma, bps, W, H, pitch, fstride, g.ctu_size, frames, g.cols, g.rows,
-                             ctx->records.as<sc_ctu_record>(), s2);
-    } else {
-      SCB_CUDA(cudaMemcpyAsync(ctx->records.p, records, cells * frames * sizeof(sc_ctu_record),
-                               cudaMemcpyDefault, s2));
-      SCB_CUDA(cudaEventRecord(ev[4], s2));
     }
+    SCB_CUDA(cudaEventRecord(ev[5], s2));
+    if (need_moments) enqueue_moment_tables(ctx, g, L, false, s2);
+    SCB_CUDA(cudaEventRecord(ev[6], s2));
+  };
+  if (main_first) {
+    enqueue_main();
+    enqueue_side();
+  } else {
+    enqueue_side();
+    enqueue_main();
   }
-  SCB_CUDA(cudaEventRecord(ev[5], s2));
-  if (need_moments) enqueue_moment_tables(ctx, g, L, false, s2);
-  SCB_CUDA(cudaEventRecord(ev[6], s2));
-  // main stream
-  ctx->est.ensure((size_t)frames * cells * sizeof(double));
-  SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
-                           cudaMemcpyDefault, s));
-  enqueue_time_tables(ctx, g, L, false, s);
-  SCB_CUDA(cudaEventRecord(ev[1], s));
-  if (do1) enqueue_step(ctx, g, cfg, plan, L, 1, true, s);
-  else upload_budgets(ctx, L, t_min_in, cfg.lambda, s);
-  SCB_CUDA(cudaEventRecord(ev[2], s));
   SCB_CUDA(cudaStreamWaitEvent(s, ev[6], 0));  // join
   SCB_CUDA(cudaEventRecord(ev[8], s));
-  if (do2) enqueue_step(ctx, g, cfg, plan, L, 2, !do1, s);
+  if (do2) enqueue_step(ctx, g, cfg, plan, L, 2, !do1 || step2_bounded(cfg), s);
   SCB_CUDA(cudaEventRecord(ev[3], s));
   const size_t nfb = (size_t)2 * L.groups * L.fpw;
   ctx->h_frame_best.ensure(nfb * sizeof(FrameBest));
@@ -500,16 +525,24 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   ctx->last_best[0].assign(b1, b1 + frames);
   ctx->last_best[1].assign(b2, b2 + frames);
   ctx->last_pruned = cfg.mode == SC_MODE_PRUNED;
-  if (ctx->last_pruned) {  // shards export the global DP count from rank 0 only
+  // walks that skip subtrees report the family's exact DP count (plan.h);
+  // shards export it from rank 0 only
+  const bool dp1 = cfg.mode == SC_MODE_PRUNED;
+  const bool dp2 = dp1 || (do2 && step2_bounded(cfg));
+  if (dp1 || dp2) {
     const unsigned __int128 cnt = plan_count(plan, g, cfg);
     for (int s2 = 0; s2 < 2; ++s2)
-      for (auto& fbv : ctx->last_best[s2]) fbv.count = ctx->shard_rank == 0 ? (uint64_t)cnt : 0;
+      if (s2 == 0 ? dp1 : dp2)
+        for (auto& fbv : ctx->last_best[s2]) fbv.count = ctx->shard_rank == 0 ? (uint64_t)cnt : 0;
   }
+  const bool whole = ctx->shard_world == 1;  // false: per-shard results, merged later
   for (int f = 0; f < frames; ++f) {
     sc_search_result& r = out[f];
     std::memset(&r, 0, sizeof(r));
     if (do1) {
-      if (!b1[f].found) fail(SC_ERR_NO_CANDIDATE, "area constraint admits no candidate partition");
+      // a shard may hold no candidate of a frame: sc_shard_merge decides
+      if (!b1[f].found && whole)
+        fail(SC_ERR_NO_CANDIDATE, "area constraint admits no candidate partition");
       r.t_min_us = bits_to_double(b1[f].t);
       r.candidates_step1 = b1[f].count;
       r.leaves_scored_step1 = b1[f].scored / (uint64_t)L.fpw;
@@ -520,22 +553,23 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
       r.t_min_us = tm;
     }
     if (do2) {
-      if (!b2[f].found) fail(SC_ERR_NO_CANDIDATE, "no candidate within the time budget");
+      if (!b2[f].found && whole) fail(SC_ERR_NO_CANDIDATE, "no candidate within the time budget");
       r.t_best_us = bits_to_double(b2[f].t);
       r.sse_best = b2[f].sse;
       r.candidates_step2 = b2[f].count;
       r.leaves_scored_step2 = b2[f].scored / (uint64_t)L.fpw;
       layout_from_snap(b2[f], cfg.n_slices, &r.best);
     }
-    if (cfg.mode == SC_MODE_PRUNED) {
-      // pruned walks do not enumerate every candidate: the counters come from
-      // the exact DP (plan.h count_candidates_dp) -- the reference's values
+    if (dp1 || dp2) {
+      // walks that skip subtrees do not enumerate every candidate: the
+      // counters come from the exact DP (plan.h count_candidates_dp) -- the
+      // reference's values
       const unsigned __int128 cnt = plan_count(plan, g, cfg);
-      if (do1) {
+      if (do1 && dp1) {
         r.candidates_step1 = (uint64_t)cnt;
         r.candidates_step1_hi = (uint64_t)(cnt >> 64);
       }
-      if (do2) {
+      if (do2 && dp2) {
         r.candidates_step2 = (uint64_t)cnt;
         r.candidates_step2_hi = (uint64_t)(cnt >> 64);
       }

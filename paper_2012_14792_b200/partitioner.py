@@ -238,6 +238,12 @@ class Partitioner:
         check(lib().sc_ctx_set_shard(self._h, rank, world))
 
     # ---- texture map --------------------------------------------------------
+    def timings(self) -> dict:
+        """Device time (us, CUDA events) of the phases of the last search call."""
+        t = (C.c_double * 5)()
+        check(lib().sc_ctx_timings(self._h, t))
+        return dict(zip(("texture", "tables", "step1", "step2", "total"), list(t)))
+
     def ctu_stats_batch(self, frames: np.ndarray, ctu_size: int = 128) -> np.ndarray:
         """K1 over a [F, H, W] uint8/uint16 array (host numpy or any array
         exposing ``data_ptr``/``ctypes``); returns [F, rows*cols] records."""

@@ -96,7 +96,10 @@ def main():
         key = os.environ.get("KEY", "cfg3_mode0")
         if "issue_active_pct_step1" in issue:
             issue["issue_active_pct"] = issue["issue_active_pct_step1"]
-        d[key] = {**d.get(key, {}), **issue, "source": os.path.basename(rep)}
+        sys.path.insert(0, os.path.dirname(HERE))
+        from bench import kernel_src_sha
+        d[key] = {**d.get(key, {}), **issue, "source": os.path.basename(rep),
+                  "kernel_src_sha": kernel_src_sha()}
         json.dump(d, open(sj, "w"), indent=1)
     print("\n".join(lines))
 

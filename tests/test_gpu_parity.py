@@ -74,15 +74,27 @@ def test_rect_tables_bit_exact(part, oracle, grid):
 
 
 # ---- K4/K5 search -----------------------------------------------------------------
+# search modes under test: exhaustive (step 2 bounded by its budget), the
+# same with an unbounded step-2 walk, and the exact pruned mode
+MODES = ["exhaustive", "exhaustive-full", "pruned"]
+
+
+def _mode(monkeypatch, m):
+    if m == "exhaustive-full":
+        monkeypatch.setenv("SLICECRAFT_B200_STEP2_BOUND", "0")
+    return 1 if m == "pruned" else 0
+
+
 def _rec3(rec):
     return np.stack([rec["count"], rec["sum"], rec["sumsq"]], axis=1)
 
 
-@pytest.mark.parametrize("mode", [0, 1])
-def test_search_small_golden(part, mode):
+@pytest.mark.parametrize("m", MODES)
+def test_search_small_golden(part, monkeypatch, m):
     """200 reference-generated instances: step 1 and step 2, bit-exact, in the
     exhaustive and the exact pruned mode."""
     from paper_2012_14792_b200 import RECORD_DTYPE, CtuGrid, SearchConfig, SlicecraftError
+    mode = _mode(monkeypatch, m)
     cases = json.load(open(os.path.join(GOLDEN, "search_small.json")))
     for i, c in enumerate(cases):
         g = CtuGrid.make(c["w"], c["h"], c["ctu"])
@@ -107,11 +119,12 @@ def test_search_small_golden(part, mode):
         assert o.candidates_step2 == c["candidates_step2"], i
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("m", MODES)
 @pytest.mark.parametrize("coverage", [0, 1])
 @pytest.mark.parametrize("seed", range(6))
-def test_search_random_vs_oracle(part, oracle, coverage, seed, mode):
+def test_search_random_vs_oracle(part, oracle, monkeypatch, coverage, seed, m):
     from paper_2012_14792_b200 import CtuGrid, SearchConfig, SlicecraftError
+    mode = _mode(monkeypatch, m)
     rng = np.random.default_rng(seed + 100 * coverage)
     for trial in range(12):
         cols, rows = int(rng.integers(1, 9)), int(rng.integers(1, 9))
@@ -183,11 +196,12 @@ def _config_inputs(ci, frames):
     return w, wl.cost_trace(w, frames=frames), wl.synth_luma(w, frames=frames)
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("m", MODES)
 @pytest.mark.parametrize("ci", [1, 2, 3])
-def test_baseline_configs_vs_reference_golden(part, ci, mode):
+def test_baseline_configs_vs_reference_golden(part, monkeypatch, ci, m):
     """cfg1 (all), cfg2 (POC 1..4), cfg3 (POC 1) against the reference itself."""
     import hashlib
+    mode = _mode(monkeypatch, m)
     from paper_2012_14792_b200 import workloads as wl
     gold = json.load(open(os.path.join(GOLDEN, "configs.json")))[str(ci)]
     F = max(fr["poc"] for fr in gold["frames"])
@@ -230,6 +244,57 @@ def test_cfg2_all_frames_vs_oracle(part, oracle):
         assert r.t_min_us == e.t_min_us and r.t_best_us == e.t_best_us and r.sse_best == e.sse_best
         assert Partition.from_layout(g, r.best).rects() == e.best.slices(g.rows)
         assert r.candidates_step1 == e.candidates_step1 == 171788
+
+
+@pytest.mark.parametrize("m", MODES)
+@pytest.mark.parametrize("world", [2, 3])
+def test_candidate_space_shards(part, oracle, monkeypatch, m, world):
+    """Candidate-space sharding through the product library: shard r walks
+    work items r, r+world, ... (sc_ctx_set_shard), exports its per-frame best
+    (sc_shard_export), and sc_shard_merge combines the rank-major records --
+    step 1, then step 2 under the merged t_min.  The shards run one after the
+    other on this GPU (no rank waits on another); the merge equals the oracle."""
+    from paper_2012_14792_b200 import CtuGrid, SearchConfig
+    from paper_2012_14792_b200._abi import SearchResult
+    from paper_2012_14792_b200.partitioner import Partition, shard_merge
+    mode = _mode(monkeypatch, m)
+    rng = np.random.default_rng(11 + world)
+    g = CtuGrid.make(7 * 64, 6 * 64, 64)
+    F, n, lam = 3, 6, 0.25
+    est = rng.lognormal(0, 0.5, size=(F, g.cell_count()))
+    luma = rng.integers(0, 1024, size=(F, g.frame_height, g.frame_width)).astype(np.uint16)
+    rec = part.ctu_stats_batch(luma, 64)
+    cfg = SearchConfig(n_slices=n, lambda_=lam, k_area=3.0, max_tile_cols=4, mode=mode)
+    merged = {}
+    try:
+        for step in (1, 2):
+            blobs = b""
+            for r in range(world):
+                part.set_shard(r, world)
+                if step == 1:
+                    part.min_time_search_batch(g, est, cfg)
+                else:
+                    tmin = np.array([merged[1][f].t_min_us for f in range(F)])
+                    part.constrained_clustering_batch(g, est, rec, tmin, cfg)
+                blobs += bytes(part.shard_export(step, F))
+            res = (SearchResult * F)()
+            for f in range(F):
+                res[f].argmin.n_slices = n
+                res[f].best.n_slices = n
+            shard_merge(step, world, F, blobs, res)
+            merged[step] = res
+    finally:
+        part.set_shard(0, 1)
+    for f in range(F):
+        st, e = oracle.search(g.frame_width, g.frame_height, 64, est[f], _rec3(rec[f]), n, lam, 3.0,
+                              4, 0, 3)
+        assert st == 0
+        r1, r2 = merged[1][f], merged[2][f]
+        assert r1.t_min_us == e.t_min_us and r1.candidates_step1 == e.candidates_step1, (m, f)
+        assert Partition.from_layout(g, r1.argmin).rects() == e.argmin1.slices(g.rows), (m, f)
+        assert r2.t_best_us == e.t_best_us and r2.sse_best == e.sse_best, (m, f)
+        assert r2.candidates_step2 == e.candidates_step2, (m, f)
+        assert Partition.from_layout(g, r2.best).rects() == e.best.slices(g.rows), (m, f)
 
 
 def test_cfg3_counts_all_frames(part):
