@@ -250,9 +250,11 @@ def run_ours(args):
             clk = ck.get("sm_mhz") or p.get("sm_mhz_ncu") or 1965.0
             sms = torch.cuda.get_device_properties(local).multi_processor_count
             peak = sms * 4 * clk * 1e6 / 1e9  # G warp-instr / s at the measured clock
-            ach = (p["warp_inst_step1"] / (s1_us * 1e-6) + p["warp_inst_step2"] / (s2_us * 1e-6)) \
-                / 2 / 1e9
-            issue = {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 2),
+            # dominant kernel: the step-1 walk (every candidate's time); the
+            # step-1 phase is that launch plus its few-us finalize
+            ach = p["warp_inst_step1"] / (s1_us * 1e-6) / 1e9
+            issue = {"bound": "alu", "kernel": "k_search<FPW,1> (step-1 walk)",
+                     "achieved": round(ach, 2), "peak": round(peak, 2),
                      "unit": "Gwarp-inst/s", "frac": round(ach / peak, 4),
                      "traffic": p.get("dram_bytes_per_launch"),
                      "ncu_issue_active_pct": p.get("issue_active_pct"),
@@ -297,7 +299,11 @@ def run_ours(args):
         "roofline_texture": tex_roof,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": luma_bytes + F * g.cell_count() * 8,
                 "d2h_bytes_per_step": 2 * 32 * ((F + 31) // 32) * 168, "ms_per_step": ms_e2e},
-        "gpu_launches": args.steps * (5 + 4 * ((F + 31) // 32)),
+        # per call (profiles/r01_cfg3_launches.md): K1, 2x(K2 + K3), the rank
+        # pipeline (6 own + 14 CUB launches), split table; per frame group:
+        # column bounds, step-1 walk + finalize, step-2 walk + finalize (+1
+        # seed-phase launch in pruned mode)
+        "gpu_launches": args.steps * (25 + (5 + args.mode) * ((F + 31) // 32)),
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_extra and args.mode == 0:

@@ -11,6 +11,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -66,7 +67,8 @@ def main():
                 lines.append(f"- {k}: {v} {u}")
         lines.append("")
         if "k_search" in kname:
-            step = "1" if ", 1>" in kname or ",(int)1>" in kname.replace(" ", "") else "2"
+            mt = re.search(r"k_search<[^,]*,\s*(?:\(int\))?(\d)", kname)
+            step = mt.group(1) if mt else "1"
             try:
                 issue[f"warp_inst_step{step}"] = float(m["Executed Instructions"][0].replace(",", ""))
                 issue[f"issue_active_pct_step{step}"] = float(m["Issue Slots Busy"][0])
