@@ -112,6 +112,7 @@ int check_cfg(const sc_grid& g, const sc_search_cfg* c) {
     fail(SC_ERR_SIZE, "n_slices exceeds the compiled limit SC_MAX_SLICES");
   if (maxc > SC_MAX_COLS) fail(SC_ERR_SIZE, "tile-column count exceeds SC_MAX_COLS");
   if (g.rows > 255) fail(SC_ERR_SIZE, "more than 255 CTU rows");
+  if (g.cols > 255) fail(SC_ERR_SIZE, "more than 255 CTU columns");
   return maxc;
 }
 

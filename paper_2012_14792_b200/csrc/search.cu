@@ -41,11 +41,29 @@ int search_block_threads() { return SCB_SEARCH_BLOCK; }
 
 template <int FPW, int STEP, bool PRUNE>
 __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(SearchArgs a) {
-  // area tables + column windows + division magics in shared memory
-  extern __shared__ int32_t s_tab[];
+  // shared-memory tables (search_walk.cuh): g_dyn = bmax|aneed interleaved
+  // [2A], mstar [(cols+1)(rows+1)], ilo [(cols+1) * rstride]; static magic,
+  // ybase, rq
   const int A = a.max_area + 1;
-  const int ntab = 2 * A + (a.cols + 1) * (a.rows + 1);
-  for (int i = threadIdx.x; i < ntab; i += blockDim.x) s_tab[i] = a.bmax[i];
+  const int nms = (a.cols + 1) * (a.rows + 1);
+  const int rstride = min(a.n, a.rows) + 1;
+  for (int i = threadIdx.x; i < A; i += blockDim.x) {
+    g_dyn[2 * i] = a.bmax[i];
+    g_dyn[2 * i + 1] = a.bmax[A + i];
+  }
+  for (int i = threadIdx.x; i < nms; i += blockDim.x) g_dyn[2 * A + i] = a.bmax[2 * A + i];
+  __syncthreads();
+  const int ilo_off = 2 * A + nms;
+  for (int i = threadIdx.x; i < (a.cols + 1) * rstride; i += blockDim.x) {
+    const int w = i / rstride, r = i % rstride;
+    g_dyn[ilo_off + i] = (w >= 1 && r >= 1) ? g_dyn[2 * (w * ((a.rows + r - 1) / r)) + 1] : 0;
+  }
+  for (int w = threadIdx.x; w < kTabDim; w += blockDim.x)
+    g_magic[w] = (w >= 1 && w <= a.cols) ? div_magic(w) : 0ull;
+  for (int y = threadIdx.x; y < kTabDim; y += blockDim.x) {
+    g_ybase[y] = y <= a.rows ? yh_of(a.rows, y, 1) : 0;
+    g_rq[y] = (y >= 1 && y <= a.rows) ? a.rows / y : 0;
+  }
   __syncthreads();
   WalkEnv e;
   e.cols = a.cols;
@@ -56,34 +74,9 @@ __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(Se
   e.coverage = a.coverage;
   e.patho = a.pathological;
   e.prune = a.prune;
-  e.rstride = min(a.n, a.rows) + 1;
-  e.bmax = s_tab;
-  e.aneed = s_tab + A;
-  e.mstar = s_tab + 2 * A;
-  int32_t* s_ilo = s_tab + ntab;
-  // 8-byte aligned slot after the windows table
-  uint64_t* s_magic =
-      reinterpret_cast<uint64_t*>(s_tab + ((ntab + (a.cols + 1) * e.rstride + 1) & ~1));
-  for (int i = threadIdx.x; i < (a.cols + 1) * e.rstride; i += blockDim.x) {
-    const int w = i / e.rstride, r = i % e.rstride;
-    s_ilo[i] = (w >= 1 && r >= 1) ? e.aneed[w * ((a.rows + r - 1) / r)] : 0;
-  }
-  for (int w = threadIdx.x; w <= a.cols; w += blockDim.x)
-    s_magic[w] = w >= 1 ? div_magic(w) : 0ull;
-  int32_t* s_ybase = reinterpret_cast<int32_t*>(s_magic + a.cols + 1);
-  int32_t* s_sfx = s_ybase + a.rows + 1;
-  int32_t* s_rq = s_sfx + a.rows + 1;
-  for (int y = threadIdx.x; y <= a.rows; y += blockDim.x) {
-    s_ybase[y] = yh_of(a.rows, y, 1);
-    s_sfx[y] = y < a.rows ? yh_of(a.rows, y, a.rows - y) : 0;
-    s_rq[y] = y >= 1 ? a.rows / y : 0;
-  }
-  __syncthreads();
-  e.ilo = s_ilo;
-  e.magic = s_magic;
-  e.ybase = s_ybase;
-  e.sfx = s_sfx;
-  e.rq = s_rq;
+  e.rstride = rstride;
+  e.mstar_off = 2 * A;
+  e.ilo_off = ilo_off;
   e.rt = a.rt;
   e.rts = a.rts;
   e.rs = a.rs;
@@ -284,8 +277,7 @@ int search_blocks_per_sm(int fpw, int step) {
 
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st) {
   const size_t smem = ((size_t)2 * (a.max_area + 1) + (size_t)(a.cols + 1) * (a.rows + 1) +
-                       (size_t)(a.cols + 1) * (std::min(a.n, a.rows) + 1) + 2 +
-                       (size_t)(a.cols + 1) * 2 + (size_t)(a.rows + 1) * 3) *
+                       (size_t)(a.cols + 1) * (std::min(a.n, a.rows) + 1)) *
                       sizeof(int32_t);
   if (smem > 64 * 1024) fail(SC_ERR_SIZE, "CTU grid too large for the area tables");
   switch (fpw * 10 + step) {

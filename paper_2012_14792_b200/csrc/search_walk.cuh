@@ -66,6 +66,35 @@ constexpr int kMaxLevels = SC_MAX_SLICES;
 constexpr int kBigArea = 1 << 20;  // "no slice yet" sentinel for amin
 constexpr int kSnap = 96;          // snapshot bytes: W[16] R[16] H[64]
 
+// Table access.  On the GPU the small tables are static shared arrays and the
+// area tables sit at the start of dynamic shared memory, bmax/aneed
+// interleaved, so every table address is a compile-time constant plus the
+// index (no base pointers to keep live or rematerialise in the register-bound
+// walk).  The host build (tests/emu) reads the same tables through WalkEnv.
+constexpr int kTabDim = 256;  // grid cols and rows are <= 255 (api.cu check_cfg)
+#ifdef __CUDACC__
+__shared__ uint64_t g_magic[kTabDim];
+__shared__ int32_t g_ybase[kTabDim], g_rq[kTabDim];
+extern __shared__ int32_t g_dyn[];  // [2A] bmax|aneed interleaved, mstar, ilo
+#endif
+#ifdef __CUDA_ARCH__
+#define SCB_BMAX(a) (g_dyn[2 * (a)])
+#define SCB_ANEED(a) (g_dyn[2 * (a) + 1])
+#define SCB_MSTAR(i) (g_dyn[e.mstar_off + (i)])
+#define SCB_ILO(i) (g_dyn[e.ilo_off + (i)])
+#define SCB_MAGIC(w) (g_magic[w])
+#define SCB_YBASE(y) (g_ybase[y])
+#define SCB_RQ(r) (g_rq[r])
+#else
+#define SCB_BMAX(a) (e.bmax[a])
+#define SCB_ANEED(a) (e.aneed[a])
+#define SCB_MSTAR(i) (e.mstar[i])
+#define SCB_ILO(i) (e.ilo[i])
+#define SCB_MAGIC(w) (e.magic[w])
+#define SCB_YBASE(y) (e.ybase[y])
+#define SCB_RQ(r) (e.rq[r])
+#endif
+
 // Read-only walk environment (tables live in shared memory on the GPU).
 struct WalkEnv {
   int cols, rows, n, nyh, max_area, coverage, patho, rstride;
@@ -79,7 +108,7 @@ struct WalkEnv {
   const uint64_t* magic;  // [cols+1]: division by w (div_magic)
   const int32_t* ybase;   // [rows+1]: yh(y, 1), the first rectangle starting at row y
   const int32_t* rq;      // [rows+1]: rows / r (no integer division in the runs DFS)
-  const int32_t* sfx;     // [rows+1]: yh(y, rows - y), the rectangle from row y to the bottom
+  int mstar_off, ilo_off;  // GPU: offsets of mstar / ilo in dynamic shared memory
   const tkey* rt;         // [NR][FPW] time key of every rectangle
   const tkey* rts;        // [NR][FPW] split table: at rect(x0,w,y0,h) with y0+h < rows,
                           // max(time(y0,h), time(y0+h, rows-y0-h)) -- a run plus the
@@ -175,12 +204,12 @@ SCB_HD uint64_t div_magic(int w) { return 0x100000000ull / (uint64_t)w + 1ull; }
 // runs_left - 1 runs of admissible height (thresholds only tighten).
 SCB_HD void height_interval(const WalkEnv& e, Thr t, int w, int rl, int runs_left, int& lo,
                             int& hi) {
-  const uint64_t mg = e.magic[w];
+  const uint64_t mg = SCB_MAGIC(w);
   const int hmin_a = imax(1, div_w(t.t2 + w - 1, mg));
   const int hmax_a = t.t1 < 0 ? 0 : div_w(t.t1, mg);
   if (runs_left == 2) {
     int m = imax(hmin_a, rl - hmax_a);
-    m = imax(m, e.mstar[w * (e.rows + 1) + rl]);
+    m = imax(m, SCB_MSTAR(w * (e.rows + 1) + rl));
     lo = m;
     hi = rl - m;
     return;
@@ -211,8 +240,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
 
   auto thresholds = [&](int amin, int amax, int win_lo, int win_hi) -> Thr {
     Thr t;
-    t.t1 = amin >= kBigArea ? kBigArea : e.bmax[amin];
-    t.t2 = e.aneed[amax];
+    t.t1 = amin >= kBigArea ? kBigArea : SCB_BMAX(amin);
+    t.t2 = SCB_ANEED(amax);
     t.t2 = imax(t.t2, win_lo);
     t.t1 = imin(t.t1, win_hi);
     return t;
@@ -226,7 +255,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     for (int i = from; i < c; ++i) {
       if (R[i] < 2) continue;
       const int w = W[i];
-      const uint64_t mg = e.magic[w];
+      const uint64_t mg = SCB_MAGIC(w);
       const int hmin_a = imax(1, div_w(t.t2 + w - 1, mg));
       const int hmax_a = t.t1 < 0 ? 0 : div_w(t.t1, mg);
       if (R[i] * hmin_a > rows || R[i] * hmax_a < rows) return false;
@@ -317,7 +346,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   for (int i = 0; i < d && ok; ++i) {
     W[i] = wi.w[i];
     X0[i + 1] = X0[i] + W[i];
-    WL[i + 1] = imax(WL[i], e.ilo[W[i] * e.rstride + rmax_c]);
+    WL[i + 1] = imax(WL[i], SCB_ILO(W[i] * e.rstride + rmax_c));
     WH[i + 1] = imin(WH[i], W[i] * rows);
     ok = WL[i + 1] <= WH[i + 1];
     if (PRUNE) {
@@ -342,7 +371,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           continue;
         }
         W[pos] = wv;
-        const int nL = imax(WL[pos], e.ilo[wv * e.rstride + rmax_c]);
+        const int nL = imax(WL[pos], SCB_ILO(wv * e.rstride + rmax_c));
         const int nH = imin(WH[pos], wv * rows);
         if (nL > nH) continue;
         if (PRUNE) {
@@ -384,8 +413,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       int r = R[rp] + 1, lo = 0, hi = 0;
       bool found = false;
       for (; r <= rhi; ++r) {
-        lo = e.ilo[w * e.rstride + r];
-        hi = w * e.rq[r];
+        lo = SCB_ILO(w * e.rstride + r);
+        hi = w * SCB_RQ(r);
         if (hi < RL[rp]) break;  // every larger r is lower still
         if (lo <= RH[rp]) {
           found = true;
@@ -414,7 +443,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       }
       // ---- one live skeleton (c, widths, runs); every area lies in
       //      [win_lo, bmax[nH]] for a window a in [nL, nH]
-      const int win_lo = nL, win_hi = e.bmax[nH];
+      const int win_lo = nL, win_hi = SCB_BMAX(nH);
       SCB_STAT(skeletons);
       if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
       int amin = kBigArea, amax = 0;
@@ -482,7 +511,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           int h = Lh[l] + 1;
           const int hhi = Lhi[l];
           if (e.patho && !forced)
-            while (h <= hhi && !(w * h <= e.bmax[w * h])) ++h;
+            while (h <= hhi && !(w * h <= SCB_BMAX(w * h))) ++h;
           if (h > hhi) {
             if (l == 0) break;
             --l;
@@ -494,7 +523,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           const int ridx = RS0[i] + j;
           curH[ridx] = (uint8_t)h;
           const int lb = Lbase[l];
-          const size_t ri = (size_t)(lb + e.ybase[y0] + h - 1) * FPW + f;
+          const size_t ri = (size_t)(lb + SCB_YBASE(y0) + h - 1) * FPW + f;
           tkey Pn;
           if (forced) {
             const int a2 = w * (rows_left - h);
@@ -549,7 +578,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             // the split table holds max(run h, forced rest) at the run's own
             // rectangle index, which advances by +1 per h; lanes step h by J.
             int h = lo + slot;
-            const tkey* p = e.rts + (size_t)(xwb + e.ybase[y0l] + h - 1) * FPW + f;
+            const tkey* p = e.rts + (size_t)(xwb + SCB_YBASE(y0l) + h - 1) * FPW + f;
             tkey v = *p;
             while (true) {
               const int hn = h + J;
