@@ -87,6 +87,42 @@ int main() {
     std::printf("case %dx%d n=%d: t_min=%.17g sse=%.17g candidates=%llu\n", cs.w, cs.h, cs.n,
                 ref.t_min_us, ref.sse_best, (unsigned long long)ref.candidates_evaluated);
   }
+  // UniformOnly family, uniform_partition, partition_time / partition_sse
+  for (int n : {1, 4, 6, 7, 13}) {
+    const CtuGrid g = CtuGrid::make(1920, 1080, 128);
+    const LumaPlane luma = make_plane(1920, 1080, 10, (unsigned)(40 + n));
+    const TextureStats stats = ctu_stats(luma, g, 3);
+    CostHistory hist(g, 16);
+    hist.append(make_map(g, 0, 0, 9 + n));
+    SearchConfig cfg;
+    cfg.n_slices = n;
+    cfg.family = CandidateFamily::UniformOnly;
+    cfg.lambda = 0.1;
+    const Partition up = uniform_partition(g, n);
+    EXPECT(b200::uniform_partition(g, n) == up, "uniform_partition");
+    const CostMap est = estimate_ctu_times(hist, 3);
+    const SliceTimeTable rt = partition_time(est, up);
+    const SliceTimeTable gt = b200::partition_time(ctx, est, up);
+    EXPECT(rt.slice_times_us == gt.slice_times_us && rt.max_us == gt.max_us &&
+               rt.total_us == gt.total_us && rt.argmax == gt.argmax,
+           "partition_time");
+    EXPECT(partition_sse(stats, up) == b200::partition_sse(ctx, stats, up), "partition_sse");
+    bool ref_threw = false, gpu_threw = false;
+    SearchOutcome ro, go;
+    try { ro = two_step_partition(hist, stats, 3, cfg); } catch (const NoCandidateError&) { ref_threw = true; }
+    try { go = b200::two_step_partition(ctx, hist, stats, 3, cfg); } catch (const NoCandidateError&) { gpu_threw = true; }
+    EXPECT(ref_threw == gpu_threw, "UniformOnly NoCandidateError");
+    if (!ref_threw) {
+      EXPECT(go.best == ro.best, "UniformOnly best partition");
+      EXPECT(go.t_min_us == ro.t_min_us && go.t_best_us == ro.t_best_us &&
+                 go.sse_best == ro.sse_best,
+             "UniformOnly values");
+      EXPECT(go.candidates_step1 == ro.candidates_step1 &&
+                 go.candidates_step2 == ro.candidates_step2 &&
+                 go.candidates_evaluated == ro.candidates_evaluated,
+             "UniformOnly counts");
+    }
+  }
   // exception classes cross the boundary unchanged
   {
     const CtuGrid g = CtuGrid::make(256, 128, 128);

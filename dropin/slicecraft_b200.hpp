@@ -10,6 +10,9 @@
 //   slicecraft::min_time_search(est, cfg)               -> b200::min_time_search(ctx, ...)
 //   slicecraft::constrained_clustering_search(...)      -> b200::constrained_clustering_search(ctx, ...)
 //   slicecraft::two_step_partition(history, stats, ...) -> b200::two_step_partition(ctx, ...)
+//   slicecraft::uniform_partition(grid, n)              -> b200::uniform_partition(grid, n)
+//   slicecraft::partition_time(costs, p)                -> b200::partition_time(ctx, costs, p)
+//   slicecraft::partition_sse(stats, p)                 -> b200::partition_sse(ctx, stats, p)
 #pragma once
 
 #include <memory>
@@ -102,7 +105,67 @@ inline Partition to_partition(const CtuGrid& g, const sc_layout& L) {
   return p;
 }
 
+// uniform_partition (grid.cpp:186-262) through sc_uniform_partition.
+inline Partition uniform_partition(const CtuGrid& g, int n_slices) {
+  const sc_grid cg = to_c(g);
+  sc_partition u;
+  check(sc_uniform_partition(&cg, n_slices, &u));
+  Partition p;
+  p.grid = g;
+  p.origin = PartitionOrigin::Uniform;
+  p.tiles.col_widths.assign(u.tile_col_widths, u.tile_col_widths + u.n_tile_cols);
+  p.tiles.row_heights.assign(u.tile_row_heights, u.tile_row_heights + u.n_tile_rows);
+  for (int i = 0; i < u.n_slices; ++i)
+    p.slices.push_back(RectSlice{u.slices[i].x0, u.slices[i].y0, u.slices[i].w, u.slices[i].h,
+                                 u.slices[i].id});
+  return p;
+}
+
+// A search result's partition: the ColumnSplit layout, or the uniform one.
+inline Partition result_partition(const CtuGrid& g, const sc_search_result& r,
+                                  const sc_layout& L) {
+  if (r.origin == SC_ORIGIN_UNIFORM) return b200::uniform_partition(g, L.n_slices);
+  return to_partition(g, L);
+}
+
 static_assert(sizeof(CtuRecord) == sizeof(sc_ctu_record), "CtuRecord layout");
+
+inline std::vector<sc_rect> to_rects(const Partition& p) {
+  std::vector<sc_rect> r;
+  for (const RectSlice& s : p.slices) r.push_back(sc_rect{s.x0, s.y0, s.w, s.h, s.id});
+  return r;
+}
+
+// partition_time (cost.hpp:102-105) on the device: SliceTimeTable of one
+// partition (slice times by id, first-strict-> argmax, total in id order).
+inline SliceTimeTable partition_time(Context& ctx, const CostMap& costs, const Partition& p) {
+  if (costs.grid != p.grid) throw GeometryError("cost map grid does not match the partition grid");
+  const sc_grid g = to_c(p.grid);
+  const std::vector<sc_rect> r = to_rects(p);
+  sc_partition_stats st;
+  SliceTimeTable out;
+  out.slice_times_us.resize(r.size());
+  check(sc_partition_eval(ctx.get(), &g, r.data(), static_cast<int32_t>(r.size()),
+                          costs.times_us.data(), nullptr, 1, &st, out.slice_times_us.data(),
+                          nullptr));
+  out.max_us = st.max_us;
+  out.total_us = st.total_us;
+  out.argmax = static_cast<std::size_t>(st.argmax);
+  return out;
+}
+
+// partition_sse (texture.hpp:92) on the device.
+inline double partition_sse(Context& ctx, const TextureStats& stats, const Partition& p) {
+  if (stats.grid() != p.grid)
+    throw GeometryError("texture stats grid does not match the partition grid");
+  const sc_grid g = to_c(p.grid);
+  const std::vector<sc_rect> r = to_rects(p);
+  sc_partition_stats st;
+  check(sc_partition_eval(ctx.get(), &g, r.data(), static_cast<int32_t>(r.size()), nullptr,
+                          reinterpret_cast<const sc_ctu_record*>(stats.records().data()), 1, &st,
+                          nullptr, nullptr));
+  return st.sse;
+}
 
 // ctu_stats (texture.hpp:83): K1 on the plane's uint16 samples.
 inline TextureStats ctu_stats(Context& ctx, const LumaPlane& luma, const CtuGrid& grid,
@@ -125,12 +188,12 @@ inline std::pair<double, Partition> min_time_search(Context& ctx, const CostMap&
   const sc_search_cfg c = to_c(cfg, mode);
   sc_search_result r;
   check(sc_min_time_search(ctx.get(), &g, &c, est.times_us.data(), 1, &r));
-  return {r.t_min_us, to_partition(est.grid, r.argmin)};
+  return {r.t_min_us, result_partition(est.grid, r, r.argmin)};
 }
 
 inline SearchOutcome to_outcome(const CtuGrid& g, const sc_search_result& r) {
   SearchOutcome o;
-  o.best = to_partition(g, r.best);
+  o.best = result_partition(g, r, r.best);
   o.t_min_us = r.t_min_us;
   o.t_best_us = r.t_best_us;
   o.sse_best = r.sse_best;

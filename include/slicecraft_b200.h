@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define SC_ABI_VERSION 1
+#define SC_ABI_VERSION 2
 
 /* Compile-time limits of the search kernels.  Larger requests fail with
  * SC_ERR_SIZE (the reference has no such limits). */
@@ -97,6 +97,35 @@ typedef struct sc_layout {
   int32_t run_heights[SC_MAX_SLICES];
 } sc_layout;
 
+/* RectSlice (grid.hpp:47-58): a slice in CTU units with its id. */
+typedef struct sc_rect {
+  int32_t x0, y0, w, h, id;
+} sc_rect;
+
+/* PartitionOrigin (grid.hpp:70): Proposed = a ColumnSplit layout (sc_layout),
+ * Uniform = uniform_partition(grid, n) (sc_uniform_partition). */
+enum { SC_ORIGIN_PROPOSED = 0, SC_ORIGIN_UNIFORM = 1 };
+
+/* A general Partition (grid.hpp:60-77): tile grid + slices in id order. */
+typedef struct sc_partition {
+  int32_t n_tile_cols;
+  int32_t n_tile_rows;
+  int32_t tile_col_widths[SC_MAX_SLICES];
+  int32_t tile_row_heights[SC_MAX_SLICES];
+  int32_t n_slices;
+  int32_t origin; /* SC_ORIGIN_* */
+  sc_rect slices[SC_MAX_SLICES];
+} sc_partition;
+
+/* SliceTimeTable (cost.hpp:93-98) summary + partition_sse (texture.hpp:92),
+ * per frame (sc_partition_eval). */
+typedef struct sc_partition_stats {
+  double max_us;    /* first-strict-> maximum of the slice times (cost.cpp:133-143) */
+  double total_us;  /* slice times summed in id order */
+  int64_t argmax;
+  double sse;       /* slice SSEs summed in id order (texture.cpp:183-189) */
+} sc_partition_stats;
+
 /* SearchOutcome (search.hpp:36-49) + the step-1 argmin of min_time_search. */
 typedef struct sc_search_result {
   double t_min_us;
@@ -117,6 +146,11 @@ typedef struct sc_search_result {
    * for spaces beyond 2^64 such as config 5 (~6.1e29). */
   uint64_t candidates_step1_hi;
   uint64_t candidates_step2_hi;
+  /* SC_ORIGIN_UNIFORM for the UniformOnly family: argmin / best are then the
+   * partition sc_uniform_partition(grid, n) returns (their sc_layout fields
+   * are left empty: the uniform grid is not a ColumnSplit layout). */
+  int32_t origin;
+  int32_t pad;
 } sc_search_result;
 
 typedef struct sc_ctx sc_ctx;
@@ -169,6 +203,22 @@ sc_status sc_texture_validate(const sc_grid* grid, const sc_ctu_record* records)
 sc_status sc_grid_tables(sc_ctx* ctx, const sc_grid* grid, const double* est_times,
                          const sc_ctu_record* records, int32_t n_frames,
                          double* rect_time, double* rect_sse, double* sat);
+
+/* ---- partitions (grid.cpp:186-262, cost.cpp:117-145, texture.cpp:171-189) */
+/* uniform_partition (grid.cpp:186-262).  GeometryError if n_slices is not in
+ * [1, cells]. */
+sc_status sc_uniform_partition(const sc_grid* grid, int32_t n_slices, sc_partition* out);
+/* partition_time + partition_sse (+ slice_moments) of one partition on
+ * n_frames frames, on the device.  slices: n_slices rects whose ids are a
+ * permutation of 0..n_slices-1 (host pointer).  est_times / records: host or
+ * device, either may be NULL (its outputs are then left untouched).  out:
+ * n_frames summaries; slice_times (n_frames * n_slices doubles, by id) and
+ * slice_moments (n_frames * n_slices records, by id) may be NULL. */
+sc_status sc_partition_eval(sc_ctx* ctx, const sc_grid* grid, const sc_rect* slices,
+                            int32_t n_slices, const double* est_times,
+                            const sc_ctu_record* records, int32_t n_frames,
+                            sc_partition_stats* out, double* slice_times,
+                            sc_ctu_record* slice_moments);
 
 /* ---- partition search (search.cpp:257-434) ------------------------------ */
 /* min_time_search (search.cpp:328-332) for n_frames est maps. */

@@ -232,6 +232,12 @@ class Ref:
                                  _p(est), C.byref(src), C.byref(srcp))
         return st, est, src.value, srcp.value
 
+    def uniform_partition(self, fw, fh, ctu, n):
+        """uniform_partition (grid.cpp:186-262) -> (status, RefLayout)."""
+        lay = RefLayout()
+        st = self.L.ref_uniform_partition(fw, fh, ctu, n, C.byref(lay))
+        return st, lay
+
     def partition_eval(self, fw, fh, ctu, col_widths, row_heights, slices, times=None,
                        records=None, validate=False):
         cw = np.ascontiguousarray(col_widths, dtype=np.int32)

@@ -54,7 +54,29 @@ class SearchResult(C.Structure):
                 ("time_min_step_us", C.c_double), ("clustering_step_us", C.c_double),
                 ("leaves_scored_step1", C.c_uint64), ("leaves_scored_step2", C.c_uint64),
                 ("argmin", Layout), ("best", Layout),
-                ("candidates_step1_hi", C.c_uint64), ("candidates_step2_hi", C.c_uint64)]
+                ("candidates_step1_hi", C.c_uint64), ("candidates_step2_hi", C.c_uint64),
+                ("origin", C.c_int32), ("pad", C.c_int32)]
+
+
+SC_ORIGIN_PROPOSED, SC_ORIGIN_UNIFORM = 0, 1
+
+
+class Rect(C.Structure):
+    _fields_ = [("x0", C.c_int32), ("y0", C.c_int32), ("w", C.c_int32), ("h", C.c_int32),
+                ("id", C.c_int32)]
+
+
+class PartitionC(C.Structure):
+    _fields_ = [("n_tile_cols", C.c_int32), ("n_tile_rows", C.c_int32),
+                ("tile_col_widths", C.c_int32 * SC_MAX_SLICES),
+                ("tile_row_heights", C.c_int32 * SC_MAX_SLICES),
+                ("n_slices", C.c_int32), ("origin", C.c_int32),
+                ("slices", Rect * SC_MAX_SLICES)]
+
+
+class PartitionStats(C.Structure):
+    _fields_ = [("max_us", C.c_double), ("total_us", C.c_double), ("argmax", C.c_int64),
+                ("sse", C.c_double)]
 
 
 class ShardBest(C.Structure):
@@ -75,6 +97,9 @@ SIGNATURES = [
     ("sc_ctx_set_shard", C.c_int, [_P, C.c_int32, C.c_int32]),
     ("sc_ctx_set_stream", C.c_int, [_P, _P]),
     ("sc_ctx_timings", C.c_int, [_P, _P]),
+    ("sc_uniform_partition", C.c_int, [C.POINTER(Grid), C.c_int32, C.POINTER(PartitionC)]),
+    ("sc_partition_eval", C.c_int, [_P, C.POINTER(Grid), _P, C.c_int32, _P, _P, C.c_int32, _P,
+                                    _P, _P]),
     ("sc_texture_moments", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_size_t,
                                      C.c_size_t, C.c_int32, C.c_int32, _P]),
     ("sc_texture_validate", C.c_int, [C.POINTER(Grid), _P]),

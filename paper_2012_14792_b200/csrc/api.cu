@@ -35,6 +35,9 @@ int search_blocks_per_sm(int fpw, int step);
 int search_block_threads();
 void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int cols, int rows,
                           int rmax, int rstride, uint32_t* lbr, uint32_t* lbm, cudaStream_t st);
+void partition_eval_device(const double* d_sat, const uint64_t* d_usat, const int* d_rects, int n,
+                           int cols, int rows, int frames, sc_partition_stats* d_out,
+                           double* d_slice_times, sc_ctu_record* d_slice_mom, cudaStream_t st);
 void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
                      const LaneBest* lanes, const uint8_t* snaps,
                      const unsigned long long* count, const unsigned long long* scored,
@@ -110,7 +113,8 @@ int check_cfg(const sc_grid& g, const sc_search_cfg* c) {
   const int maxc = std::min({c->n_slices, eff, g.cols});
   if (c->n_slices > SC_MAX_SLICES)
     fail(SC_ERR_SIZE, "n_slices exceeds the compiled limit SC_MAX_SLICES");
-  if (maxc > SC_MAX_COLS) fail(SC_ERR_SIZE, "tile-column count exceeds SC_MAX_COLS");
+  if (c->family == SC_FAMILY_COLUMN_SPLIT && maxc > SC_MAX_COLS)
+    fail(SC_ERR_SIZE, "tile-column count exceeds SC_MAX_COLS");
   if (g.rows > 255) fail(SC_ERR_SIZE, "more than 255 CTU rows");
   if (g.cols > 255) fail(SC_ERR_SIZE, "more than 255 CTU columns");
   return maxc;
@@ -427,20 +431,167 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-void require_column_split(const sc_search_cfg* cfg) {
-  if (cfg->family == SC_FAMILY_UNIFORM_ONLY)
-    fail(SC_ERR_USAGE, "UniformOnly family is not implemented on the device path yet");
-}
 
 // The per-batch hot path.  luma (host or device) may be NULL when records
 // are given; est / records / t_min_in are host or device pointers.
 //   main stream : est -> K2/K3 time tables -> step 1 -> [join] -> step 2
 //   side stream : luma H2D -> K1 -> K2/K3 moment tables          (overlaps step 1)
+// Host uniform_partition (plan.h) with the reference's errors.
+UniformPartition uniform_or_fail(const sc_grid& g, int n) {
+  UniformPartition u;
+  if (n < 1) fail(SC_ERR_GEOMETRY, "slice count must be >= 1");
+  if (!uniform_partition(g.cols, g.rows, n, u))
+    fail(SC_ERR_GEOMETRY, "slice count exceeds CTU cell count");
+  return u;
+}
+
+// area_constraint_ok (search.cpp:93-108): k * min area > max area.
+bool uniform_area_ok(const UniformPartition& u, double k) {
+  int64_t amin = INT64_MAX, amax = 0;
+  for (size_t i = 0; i < u.rects.size(); i += 4) {
+    const int64_t a = (int64_t)u.rects[i + 2] * u.rects[i + 3];
+    amin = std::min(amin, a);
+    amax = std::max(amax, a);
+  }
+  return k * (double)amin > (double)amax;
+}
+
+// partition_time / partition_sse of `rects` (id order) on the device, from
+// est (host/device, may be NULL) and records already in ctx->records (or
+// `records`, host/device, may be NULL).  Results in ctx->h_stage.
+const sc_partition_stats* eval_partition(sc_ctx* ctx, const sc_grid& g, const std::vector<int>& rects,
+                                        const double* est, const sc_ctu_record* records,
+                                        bool records_resident, int frames, cudaStream_t s,
+                                        double* slice_times, sc_ctu_record* slice_mom) {
+  const int n = (int)rects.size() / 4;
+  const size_t cells = (size_t)g.cols * g.rows;
+  const int nsat = (g.cols + 1) * (g.rows + 1);
+  ctx->scratch.ensure(rects.size() * sizeof(int) + (size_t)frames * sizeof(sc_partition_stats) +
+                      (size_t)frames * n * (sizeof(double) + sizeof(sc_ctu_record)) + 64);
+  int* d_rects = ctx->scratch.as<int>();
+  sc_partition_stats* d_out = reinterpret_cast<sc_partition_stats*>(
+      ctx->scratch.as<uint8_t>() + ((rects.size() * sizeof(int) + 15) & ~size_t(15)));
+  double* d_times = reinterpret_cast<double*>(d_out + frames);
+  sc_ctu_record* d_mom = reinterpret_cast<sc_ctu_record*>(d_times + (size_t)frames * n);
+  SCB_CUDA(cudaMemcpyAsync(d_rects, rects.data(), rects.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, s));
+  if (est) {
+    ctx->est.ensure((size_t)frames * cells * sizeof(double));
+    ctx->sat.ensure((size_t)frames * nsat * sizeof(double));
+    SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
+                             cudaMemcpyDefault, s));
+    grid_sat_device(ctx->est.as<double>(), nullptr, g.cols, g.rows, frames, ctx->sat.as<double>(),
+                    nullptr, s);
+  }
+  const bool have_rec = records || records_resident;
+  if (have_rec) {
+    if (!records_resident) {
+      ctx->records.ensure((size_t)frames * cells * sizeof(sc_ctu_record));
+      SCB_CUDA(cudaMemcpyAsync(ctx->records.p, records, (size_t)frames * cells * sizeof(sc_ctu_record),
+                               cudaMemcpyDefault, s));
+    }
+    ctx->usat.ensure((size_t)frames * 3 * nsat * sizeof(uint64_t));
+    grid_sat_device(nullptr, ctx->records.as<sc_ctu_record>(), g.cols, g.rows, frames, nullptr,
+                    ctx->usat.as<uint64_t>(), s);
+  }
+  partition_eval_device(est ? ctx->sat.as<double>() : nullptr,
+                        have_rec ? ctx->usat.as<uint64_t>() : nullptr, d_rects, n, g.cols, g.rows,
+                        frames, d_out, d_times, d_mom, s);
+  ctx->h_stage.ensure((size_t)frames * sizeof(sc_partition_stats));
+  sc_partition_stats* h = ctx->h_stage.as<sc_partition_stats>();
+  std::memset(h, 0, (size_t)frames * sizeof(sc_partition_stats));
+  SCB_CUDA(cudaMemcpyAsync(h, d_out, (size_t)frames * sizeof(sc_partition_stats),
+                           cudaMemcpyDeviceToHost, s));
+  if (slice_times && est)
+    SCB_CUDA(cudaMemcpyAsync(slice_times, d_times, (size_t)frames * n * sizeof(double),
+                             cudaMemcpyDefault, s));
+  if (slice_mom && have_rec)
+    SCB_CUDA(cudaMemcpyAsync(slice_mom, d_mom, (size_t)frames * n * sizeof(sc_ctu_record),
+                             cudaMemcpyDefault, s));
+  SCB_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+// The UniformOnly family (search.cpp:265-275 step 1, 349-364 step 2): the one
+// uniform candidate, evaluated on the device for every frame.
+void run_uniform(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int frames,
+                 const void* luma, int bps, size_t pitch, size_t fstride, const double* est,
+                 const sc_ctu_record* records, const double* t_min_in, bool do1, bool do2,
+                 sc_search_result* out, sc_ctu_record* records_out) {
+  const UniformPartition u = uniform_or_fail(g, cfg.n_slices);
+  if (!uniform_area_ok(u, cfg.k_area))
+    fail(SC_ERR_NO_CANDIDATE, "uniform partition violates the area constraint");
+  cudaStream_t s = main_stream(ctx);
+  cudaEvent_t* ev = ctx->ev;
+  SCB_CUDA(cudaEventRecord(ev[0], s));
+  const size_t cells = (size_t)g.cols * g.rows;
+  bool resident = false;
+  if (do2 && luma) {  // K1 on the batch
+    const int W = g.frame_width, H = g.frame_height;
+    const size_t span = (size_t)(frames - 1) * fstride + pitch * (H - 1) + (size_t)W * bps;
+    const void* d_luma = luma;
+    if (!is_device_ptr(luma)) {
+      ctx->luma.ensure(span);
+      SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyDefault, s));
+      d_luma = ctx->luma.p;
+    }
+    ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
+    texture_moments_device(d_luma, bps, W, H, pitch, fstride, g.ctu_size, frames, g.cols, g.rows,
+                           ctx->records.as<sc_ctu_record>(), s);
+    resident = true;
+  }
+  const sc_partition_stats* h =
+      eval_partition(ctx, g, u.rects, est, do2 ? records : nullptr, resident, frames, s, nullptr,
+                     nullptr);
+  if (records_out && resident)
+    SCB_CUDA(cudaMemcpy(records_out, ctx->records.p, cells * frames * sizeof(sc_ctu_record),
+                        cudaMemcpyDefault));
+  SCB_CUDA(cudaEventRecord(ev[9], s));
+  SCB_CUDA(cudaEventSynchronize(ev[9]));
+  const double us = 1000.0 * ev_ms(ev[0], ev[9]);
+  for (int i = 0; i < 5; ++i) ctx->timings[i] = 0.0;
+  ctx->timings[do1 ? 2 : 3] = us;
+  ctx->timings[4] = us;
+  ctx->last_best[0].clear();
+  ctx->last_best[1].clear();
+  for (int f = 0; f < frames; ++f) {
+    sc_search_result& r = out[f];
+    std::memset(&r, 0, sizeof(r));
+    r.origin = SC_ORIGIN_UNIFORM;
+    r.argmin.n_slices = r.best.n_slices = cfg.n_slices;
+    double t_min = 0.0;
+    if (do1) {
+      t_min = h[f].max_us;
+      r.candidates_step1 = 1;
+    } else {
+      SCB_CUDA(cudaMemcpy(&t_min, t_min_in + f, sizeof(double), cudaMemcpyDefault));
+    }
+    r.t_min_us = t_min;
+    if (do2) {
+      const double budget = t_min * (1.0 + cfg.lambda);
+      if (h[f].max_us > budget)
+        fail(SC_ERR_NO_CANDIDATE, "uniform partition exceeds the time budget");
+      r.t_best_us = h[f].max_us;
+      r.sse_best = h[f].sse;
+      r.candidates_step2 = 1;
+    }
+    r.candidates_evaluated = r.candidates_step1 + r.candidates_step2;
+    r.time_min_step_us = ctx->timings[2] / frames;
+    r.clustering_step_us = ctx->timings[3] / frames;
+    r.search_time_us = us / frames;
+  }
+}
+
 void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc, int frames,
                   const void* luma, int bps, size_t pitch, size_t fstride, const double* est,
                   const sc_ctu_record* records, const double* t_min_in, bool do1, bool do2,
                   sc_search_result* out, sc_ctu_record* records_out) {
   if (frames < 1) fail(SC_ERR_USAGE, "n_frames must be >= 1");
+  if (cfg.family == SC_FAMILY_UNIFORM_ONLY) {
+    run_uniform(ctx, g, cfg, frames, luma, bps, pitch, fstride, est, records, t_min_in, do1, do2,
+                out, records_out);
+    return;
+  }
   Plan* plan = get_plan(ctx, g, cfg, maxc);
   upload_plan(ctx, plan);
   const Layouts L = layouts_for(g, frames);
@@ -784,7 +935,6 @@ sc_status sc_min_time_search(sc_ctx* ctx, const sc_grid* grid, const sc_search_c
     if (!ctx || !est || !out) fail(SC_ERR_USAGE, "NULL argument");
     check_grid(grid);
     const int maxc = check_cfg(*grid, cfg);
-    require_column_split(cfg);
     SCB_CUDA(cudaSetDevice(ctx->device));
     run_pipeline(ctx, *grid, *cfg, maxc, frames, nullptr, 0, 0, 0, est, nullptr, nullptr, true,
                  false, out, nullptr);
@@ -798,7 +948,6 @@ sc_status sc_constrained_clustering(sc_ctx* ctx, const sc_grid* grid, const sc_s
     if (!ctx || !est || !records || !t_min || !out) fail(SC_ERR_USAGE, "NULL argument");
     check_grid(grid);
     const int maxc = check_cfg(*grid, cfg);
-    require_column_split(cfg);
     SCB_CUDA(cudaSetDevice(ctx->device));
     const size_t cells = (size_t)grid->cols * grid->rows;
     if (!is_device_ptr(records))
@@ -815,7 +964,6 @@ sc_status sc_two_step(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg
     if (!ctx || !est || !records || !out) fail(SC_ERR_USAGE, "NULL argument");
     check_grid(grid);
     const int maxc = check_cfg(*grid, cfg);
-    require_column_split(cfg);
     SCB_CUDA(cudaSetDevice(ctx->device));
     const size_t cells = (size_t)grid->cols * grid->rows;
     if (!is_device_ptr(records))
@@ -833,7 +981,6 @@ sc_status sc_partition_frames(sc_ctx* ctx, const sc_grid* grid, const sc_search_
     if (!ctx || !luma || !est || !out) fail(SC_ERR_USAGE, "NULL argument");
     check_grid(grid);
     const int maxc = check_cfg(*grid, cfg);
-    require_column_split(cfg);
     SCB_CUDA(cudaSetDevice(ctx->device));
     if (bps != 1 && bps != 2) fail(SC_ERR_FORMAT, "bytes_per_sample must be 1 or 2");
     if (pitch < (size_t)grid->frame_width * bps) fail(SC_ERR_GEOMETRY, "pitch smaller than a row");
@@ -850,14 +997,72 @@ sc_status sc_count_candidates(sc_ctx* ctx, const sc_grid* grid, const sc_search_
     if (!ctx || !count) fail(SC_ERR_USAGE, "NULL argument");
     check_grid(grid);
     const int maxc = check_cfg(*grid, cfg);
-    require_column_split(cfg);
     SCB_CUDA(cudaSetDevice(ctx->device));
     const size_t cells = (size_t)grid->cols * grid->rows;
     std::vector<double> ones(cells, 1.0);
     sc_search_result r;
+    if (cfg->family == SC_FAMILY_UNIFORM_ONLY) {  // for_each_candidate (search.cpp:308-312)
+      *count = uniform_area_ok(uniform_or_fail(*grid, cfg->n_slices), cfg->k_area) ? 1 : 0;
+      return;
+    }
     run_pipeline(ctx, *grid, *cfg, maxc, 1, nullptr, 0, 0, 0, ones.data(), nullptr, nullptr, true,
                  false, &r, nullptr);
     *count = r.candidates_step1;
+  });
+}
+
+sc_status sc_uniform_partition(const sc_grid* grid, int32_t n_slices, sc_partition* out) {
+  return guarded([&] {
+    if (!out) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const UniformPartition u = uniform_or_fail(*grid, n_slices);
+    std::memset(out, 0, sizeof(*out));
+    if (n_slices > SC_MAX_SLICES) fail(SC_ERR_SIZE, "n_slices exceeds SC_MAX_SLICES");
+    out->n_tile_cols = (int32_t)u.tile_cols.size();
+    out->n_tile_rows = (int32_t)u.tile_rows.size();
+    for (size_t i = 0; i < u.tile_cols.size(); ++i) out->tile_col_widths[i] = u.tile_cols[i];
+    for (size_t i = 0; i < u.tile_rows.size(); ++i) out->tile_row_heights[i] = u.tile_rows[i];
+    out->n_slices = n_slices;
+    out->origin = SC_ORIGIN_UNIFORM;
+    for (int i = 0; i < n_slices; ++i)
+      out->slices[i] = sc_rect{u.rects[4 * i], u.rects[4 * i + 1], u.rects[4 * i + 2],
+                               u.rects[4 * i + 3], i};
+  });
+}
+
+sc_status sc_partition_eval(sc_ctx* ctx, const sc_grid* grid, const sc_rect* slices,
+                            int32_t n_slices, const double* est, const sc_ctu_record* records,
+                            int32_t frames, sc_partition_stats* out, double* slice_times,
+                            sc_ctu_record* slice_moments) {
+  return guarded([&] {
+    if (!ctx || !slices || !out) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    if (frames < 1) fail(SC_ERR_USAGE, "n_frames must be >= 1");
+    if (n_slices < 1 || n_slices > SC_MAX_SLICES)
+      fail(SC_ERR_SIZE, "slice count must be in [1, SC_MAX_SLICES]");
+    std::vector<int> rects((size_t)n_slices * 4, 0);
+    std::vector<char> seen((size_t)n_slices, 0);
+    for (int i = 0; i < n_slices; ++i) {
+      const sc_rect& r = slices[i];
+      if (r.id < 0 || r.id >= n_slices || seen[(size_t)r.id])
+        fail(SC_ERR_USAGE, "slice ids must be a permutation of 0..n_slices-1");
+      if (r.w < 1 || r.h < 1 || r.x0 < 0 || r.y0 < 0 || r.x0 + r.w > grid->cols ||
+          r.y0 + r.h > grid->rows)
+        fail(SC_ERR_GEOMETRY, "slice outside the CTU grid");
+      seen[(size_t)r.id] = 1;
+      int* d = &rects[(size_t)r.id * 4];
+      d[0] = r.x0, d[1] = r.y0, d[2] = r.w, d[3] = r.h;
+    }
+    if (records && !is_device_ptr(records))
+      for (int f = 0; f < frames; ++f)
+        validate_records(*grid, records + (size_t)f * grid->cols * grid->rows);
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    const sc_partition_stats* h = eval_partition(ctx, *grid, rects, est, records, false, frames,
+                                                main_stream(ctx), slice_times, slice_moments);
+    for (int f = 0; f < frames; ++f) {
+      out[f] = h[f];
+      if (!est) out[f].max_us = out[f].total_us = 0.0, out[f].argmax = -1;
+    }
   });
 }
 

@@ -103,6 +103,59 @@ inline bool make_area_tables(int cols, int rows, double k, std::vector<int32_t>&
   return pathological;
 }
 
+// uniform_partition (grid.cpp:186-262): the best r x c factorization of n by
+// its largest slice area (ties toward more columns), tiles from split_even
+// (grid.cpp:53-61), slices row-major; when no factorization fits, c =
+// min(n, cols) columns each cut into near-equal runs.  Returns false if n is
+// outside [1, cols * rows] (the reference's GeometryError).  Slices as
+// {x0, y0, w, h} in id order.
+struct UniformPartition {
+  std::vector<int> tile_cols, tile_rows;
+  std::vector<int> rects;  // 4 ints per slice
+};
+inline std::vector<int> split_even(int total, int parts) {
+  std::vector<int> out((size_t)parts);
+  for (int i = 0; i < parts; ++i) out[(size_t)i] = total / parts + (i < total % parts ? 1 : 0);
+  return out;
+}
+inline bool uniform_partition(int cols, int rows, int n, UniformPartition& p) {
+  if (n < 1 || (int64_t)n > (int64_t)cols * rows) return false;
+  int best_c = -1, best_r = -1;
+  int64_t best_area = -1;
+  for (int c = 1; c <= std::min(n, cols); ++c) {
+    if (n % c != 0) continue;
+    const int r = n / c;
+    if (r > rows) continue;
+    const int64_t a = (int64_t)((cols + c - 1) / c) * ((rows + r - 1) / r);
+    if (best_area < 0 || a < best_area || (a == best_area && c > best_c)) {
+      best_area = a;
+      best_c = c;
+      best_r = r;
+    }
+  }
+  p.rects.clear();
+  if (best_c > 0) {
+    p.tile_cols = split_even(cols, best_c);
+    p.tile_rows = split_even(rows, best_r);
+    for (int r = 0, y = 0; r < best_r; y += p.tile_rows[(size_t)r], ++r)
+      for (int c = 0, x = 0; c < best_c; x += p.tile_cols[(size_t)c], ++c)
+        p.rects.insert(p.rects.end(), {x, y, p.tile_cols[(size_t)c], p.tile_rows[(size_t)r]});
+    return true;
+  }
+  const int c = std::min(n, cols);
+  p.tile_cols = split_even(cols, c);
+  p.tile_rows = {rows};
+  const std::vector<int> counts = split_even(n, c);
+  for (int col = 0, x = 0; col < c; x += p.tile_cols[(size_t)col], ++col) {
+    int y = 0;
+    for (int h : split_even(rows, counts[(size_t)col])) {
+      p.rects.insert(p.rects.end(), {x, y, p.tile_cols[(size_t)col], h});
+      y += h;
+    }
+  }
+  return true;
+}
+
 }  // namespace scb
 
 #include <thread>

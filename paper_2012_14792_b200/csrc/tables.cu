@@ -188,6 +188,69 @@ void split_table_device(const uint32_t* d_rt, int cols, int rows, int groups, in
   SCB_CUDA(cudaGetLastError());
 }
 
+// partition_time (cost.cpp:117-145) + slice_moments / partition_sse
+// (texture.cpp:171-189) of one partition on every frame: one CTA per frame,
+// one thread per slice for the rectangle sums, then thread 0 folds in id
+// order exactly like the reference (max from slice 0 with strict >, totals
+// summed in id order).  rects: {x0, y0, w, h} indexed by slice id.
+__global__ void k_partition_eval(const double* __restrict__ sat, const uint64_t* __restrict__ usat,
+                                 const int4* __restrict__ rects, int n, int cols, int rows,
+                                 sc_partition_stats* __restrict__ out,
+                                 double* __restrict__ slice_times,
+                                 sc_ctu_record* __restrict__ slice_mom) {
+  __shared__ double st[SC_MAX_SLICES], ss[SC_MAX_SLICES];
+  const int f = blockIdx.x;
+  const int stride = cols + 1;
+  const int nsat = stride * (rows + 1);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int4 r = rects[j];
+    const int ia = r.y * stride + r.x, ib = r.y * stride + r.x + r.z;
+    const int ic = (r.y + r.w) * stride + r.x, idd = (r.y + r.w) * stride + r.x + r.z;
+    if (sat) {
+      const double* T = sat + (size_t)f * nsat;
+      st[j] = __dadd_rn(__dsub_rn(__dsub_rn(T[idd], T[ib]), T[ic]), T[ia]);
+      if (slice_times) slice_times[(size_t)f * n + j] = st[j];
+    }
+    if (usat) {
+      const uint64_t* U = usat + (size_t)f * 3 * nsat;
+      const uint64_t c = U[idd] - U[ib] - U[ic] + U[ia];
+      const uint64_t sm = U[nsat + idd] - U[nsat + ib] - U[nsat + ic] + U[nsat + ia];
+      const uint64_t q = U[2 * nsat + idd] - U[2 * nsat + ib] - U[2 * nsat + ic] + U[2 * nsat + ia];
+      ss[j] = moments_sse(c, sm, q);
+      if (slice_mom) slice_mom[(size_t)f * n + j] = sc_ctu_record{c, sm, q};
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sc_partition_stats& o = out[f];
+    if (sat) {
+      o.max_us = st[0];
+      o.argmax = 0;
+      o.total_us = 0.0;
+      for (int j = 0; j < n; ++j) {
+        o.total_us = __dadd_rn(o.total_us, st[j]);
+        if (st[j] > o.max_us) {
+          o.max_us = st[j];
+          o.argmax = j;
+        }
+      }
+    }
+    if (usat) {
+      double tot = 0.0;
+      for (int j = 0; j < n; ++j) tot = __dadd_rn(tot, ss[j]);
+      o.sse = tot;
+    }
+  }
+}
+
+void partition_eval_device(const double* d_sat, const uint64_t* d_usat, const int* d_rects, int n,
+                           int cols, int rows, int frames, sc_partition_stats* d_out,
+                           double* d_slice_times, sc_ctu_record* d_slice_mom, cudaStream_t st) {
+  k_partition_eval<<<frames, 64, 0, st>>>(d_sat, d_usat, reinterpret_cast<const int4*>(d_rects),
+                                          n, cols, rows, d_out, d_slice_times, d_slice_mom);
+  SCB_CUDA(cudaGetLastError());
+}
+
 void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, int rows,
                      int frames, double* d_sat, uint64_t* d_usat, cudaStream_t st) {
   const int nsat = (cols + 1) * (rows + 1);

@@ -25,8 +25,8 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from ._abi import (CtuRecord, Grid, Layout, SearchCfg, SearchResult, ShardBest,
-                   SlicecraftError, check, lib)
+from ._abi import (SC_ORIGIN_UNIFORM, CtuRecord, Grid, Layout, PartitionC, PartitionStats, Rect,
+                   SearchCfg, SearchResult, ShardBest, SlicecraftError, check, lib)
 
 COLUMN_SPLIT, UNIFORM_ONLY = 0, 1
 COVERAGE_REFERENCE, COVERAGE_COVERING = 0, 1
@@ -164,6 +164,7 @@ class Partition:
     col_widths: List[int]
     row_heights: List[int]
     slices: List[Slice] = field(default_factory=list)
+    origin: str = "proposed"  # PartitionOrigin (grid.hpp:70)
 
     @staticmethod
     def from_layout(grid: CtuGrid, L: Layout) -> "Partition":
@@ -180,6 +181,23 @@ class Partition:
                 y += h
             x += w
         return p
+
+    @staticmethod
+    def uniform(grid: CtuGrid, n_slices: int) -> "Partition":
+        """uniform_partition (grid.cpp:186-262) via sc_uniform_partition."""
+        out = PartitionC()
+        check(lib().sc_uniform_partition(C.byref(grid.c()), n_slices, C.byref(out)))
+        p = Partition(grid, [out.tile_col_widths[i] for i in range(out.n_tile_cols)],
+                      [out.tile_row_heights[i] for i in range(out.n_tile_rows)])
+        p.slices = [Slice(r.x0, r.y0, r.w, r.h, r.id) for r in out.slices[:out.n_slices]]
+        p.origin = "uniform"
+        return p
+
+    @staticmethod
+    def from_result(grid: CtuGrid, r: SearchResult, L: Layout) -> "Partition":
+        if r.origin == SC_ORIGIN_UNIFORM:
+            return Partition.uniform(grid, L.n_slices)
+        return Partition.from_layout(grid, L)
 
     def rects(self):
         return [(s.x0, s.y0, s.w, s.h, s.id) for s in self.slices]
@@ -207,8 +225,8 @@ class SearchOutcome:
 
 def _outcome(grid: CtuGrid, r: SearchResult, step1: bool, step2: bool) -> SearchOutcome:
     return SearchOutcome(
-        best=Partition.from_layout(grid, r.best) if step2 else None,
-        argmin=Partition.from_layout(grid, r.argmin) if step1 else None,
+        best=Partition.from_result(grid, r, r.best) if step2 else None,
+        argmin=Partition.from_result(grid, r, r.argmin) if step1 else None,
         t_min_us=r.t_min_us, t_best_us=r.t_best_us, sse_best=r.sse_best,
         candidates_evaluated=r.candidates_evaluated, candidates_step1=r.candidates_step1,
         candidates_step2=r.candidates_step2, search_time_us=r.search_time_us,
@@ -346,6 +364,29 @@ class Partitioner:
                                         _ptr(luma), bps, W * bps, W * H * bps, _ptr(est), F,
                                         _ptr(records_out), C.cast(res, C.c_void_p)))
         return res
+
+    def partition_eval(self, p: "Partition", est: Optional[np.ndarray] = None,
+                       records: Optional[np.ndarray] = None, slice_values: bool = False):
+        """partition_time (cost.cpp:117-145) and partition_sse / slice_moments
+        (texture.cpp:171-189) of one partition on a batch of frames, on the
+        device.  Returns a list of dicts (max_us, total_us, argmax, sse) and,
+        with slice_values, the per-slice times [F][n] and moments [F][n]."""
+        g = p.grid
+        n = len(p.slices)
+        rects = (Rect * n)(*[Rect(s.x0, s.y0, s.w, s.h, s.id) for s in p.slices])
+        e = None if est is None else np.ascontiguousarray(est, dtype=np.float64).reshape(
+            -1, g.cell_count())
+        r = None if records is None else np.ascontiguousarray(records).reshape(-1, g.cell_count())
+        F = (e if e is not None else r).shape[0]
+        out = (PartitionStats * F)()
+        st = np.zeros((F, n)) if slice_values and e is not None else None
+        sm = np.zeros((F, n), RECORD_DTYPE) if slice_values and r is not None else None
+        check(lib().sc_partition_eval(self._h, C.byref(g.c()), C.cast(rects, C.c_void_p), n,
+                                      _ptr(e), _ptr(r), F, C.cast(out, C.c_void_p), _ptr(st),
+                                      _ptr(sm)))
+        res = [dict(max_us=o.max_us, total_us=o.total_us, argmax=o.argmax, sse=o.sse)
+               for o in out]
+        return (res, st, sm) if slice_values else res
 
     def count_candidates(self, grid: CtuGrid, cfg: SearchConfig) -> int:
         n = C.c_uint64()

@@ -11,6 +11,10 @@ Contents
   search_small.json  200 seeded random small instances (grids <= 6x6, n <= 6,
                    lambda in {0, .1, .3, 1}, k in {3, 2.5, 1.5}): the reference's
                    min_time_search + constrained_clustering_search outputs.
+  uniform.json     UniformOnly family: uniform_partition
+                   shapes, min_time_search / constrained_clustering_search
+                   outputs, and partition_time / partition_sse of random
+                   column partitions (ids permuted, some negative times).
   configs.json     BASELINE configs on their real synthetic inputs: cfg1 (all),
                    cfg2 (POC 1..4), cfg3 (POC 1): two_step_partition outputs,
                    with a hash of the estimate maps / records that were used.
@@ -151,13 +155,86 @@ def configs(r: Ref) -> dict:
     return out
 
 
+def uniform(r: Ref) -> dict:
+    """UniformOnly family: uniform_partition shapes, the family's search
+    outputs, and partition_time / partition_sse of arbitrary partitions."""
+    rng = np.random.default_rng(1479)
+    parts = []
+    for cols, rows in [(15, 9), (30, 17), (60, 34), (7, 5), (1, 1), (3, 11), (13, 2)]:
+        for n in [1, 2, 3, 4, 5, 6, 7, 8, 12, 13, 16, 17, 31, 32, 37, 64, 65]:
+            st, lay = r.uniform_partition(cols * 32, rows * 32, 32, n)
+            parts.append({"cols": cols, "rows": rows, "n": n, "status": st,
+                          "tile_cols": lay.widths() if st == 0 else [],
+                          "tile_rows": [lay.row_heights[i] for i in range(lay.n_tile_rows)]
+                          if st == 0 else [],
+                          "slices": lay.rects() if st == 0 else []})
+    searches = []
+    while len(searches) < 60:
+        ctu = 32
+        cols, rows = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        W, H = cols * ctu - int(rng.integers(0, ctu)), rows * ctu - int(rng.integers(0, ctu))
+        n = int(rng.integers(1, min(12, cols * rows) + 1))
+        lam = float(rng.choice([0.0, 0.1, 1.0]))
+        k = float(rng.choice([3.0, 2.0, 1.2]))
+        est = rng.lognormal(0, 0.7, cols * rows)
+        plane = rng.integers(0, 1024, size=(H, W)).astype(np.uint16)
+        _, rec = r.ctu_stats(plane, 10, ctu)
+        st1, t1, lay1 = r.min_time_search(W, H, ctu, est, n, lam, k, 1, 0)
+        case = {"w": W, "h": H, "ctu": ctu, "n": n, "lambda": lam, "k": k, "est": est.tolist(),
+                "records": rec.tolist(), "status1": st1}
+        if st1 == 0:
+            case.update({"t_min": t1, "argmin": lay1.rects()})
+            # the reference's step 2 with its own t_min, and with a t_min that
+            # puts the uniform candidate over budget
+            st2, o = r.constrained(W, H, ctu, est, rec, t1, n, lam, k, 1, 0)
+            st3, _ = r.constrained(W, H, ctu, est, rec, t1 * 0.5, n, 0.0, k, 1, 0)
+            case.update({"status2": st2, "t_best": o.t_best_us, "sse_best": o.sse_best,
+                         "best": o.best.rects(), "candidates_step2": o.candidates_step2,
+                         "candidates_evaluated": o.candidates_evaluated, "status_over": st3})
+        searches.append(case)
+    evals = []
+    for i in range(40):
+        cols, rows = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        ctu = 32
+        W, H = cols * ctu, rows * ctu
+        # a random column layout: widths, then each column cut into runs
+        widths, x = [], 0
+        while x < cols:
+            w = int(rng.integers(1, cols - x + 1))
+            widths.append(w)
+            x += w
+        slices, x = [], 0
+        for w in widths:
+            y = 0
+            while y < rows:
+                h = int(rng.integers(1, rows - y + 1))
+                slices.append([x, y, w, h])
+                y += h
+            x += w
+        perm = rng.permutation(len(slices))
+        slices = [s + [int(perm[j])] for j, s in enumerate(slices)]
+        est = rng.lognormal(0, 0.7, cols * rows) * (1 if i % 4 else -1)  # negative times too
+        plane = rng.integers(0, 1024, size=(H, W)).astype(np.uint16)
+        _, rec = r.ctu_stats(plane, 10, ctu)
+        res = r.partition_eval(W, H, ctu, widths, [rows], slices, times=est, records=rec)
+        evals.append({"w": W, "h": H, "ctu": ctu, "slices": slices, "est": est.tolist(),
+                      "records": rec.tolist(), "status": res[0], "max_us": res[1],
+                      "total_us": res[2], "argmax": res[3], "sse": res[4]})
+    return {"partitions": parts, "searches": searches, "evals": evals}
+
+
 def main():
     r = Ref()
-    with open(os.path.join(OUT, "spec_kats.json"), "w") as f:
-        json.dump(spec_kats(r), f, indent=1)
-    with open(os.path.join(OUT, "search_small.json"), "w") as f:
-        json.dump(search_small(r), f)
-    which = sys.argv[1:] or ["configs"]
+    which = sys.argv[1:] or ["kats", "small", "uniform", "configs"]
+    if "kats" in which:
+        with open(os.path.join(OUT, "spec_kats.json"), "w") as f:
+            json.dump(spec_kats(r), f, indent=1)
+    if "small" in which:
+        with open(os.path.join(OUT, "search_small.json"), "w") as f:
+            json.dump(search_small(r), f)
+    if "uniform" in which:
+        with open(os.path.join(OUT, "uniform.json"), "w") as f:
+            json.dump(uniform(r), f)
     if "configs" in which:
         with open(os.path.join(OUT, "configs.json"), "w") as f:
             json.dump(configs(r), f, indent=1)

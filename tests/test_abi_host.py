@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert sorted(n for n, _, _ in SIGNATURES) == syms  # the ctypes mirror is complete
-    assert L.sc_abi_version() == 1
+    assert L.sc_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
@@ -40,9 +40,10 @@ def test_struct_layouts_match_header():
     from paper_2012_14792_b200 import _abi
     src = """#include <stdio.h>
 #include "slicecraft_b200.h"
-int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(sc_grid), sizeof(sc_ctu_record),
- sizeof(sc_search_cfg), sizeof(sc_layout), sizeof(sc_search_result), sizeof(sc_shard_best),
- sizeof(sc_status));return 0;}"""
+int main(void){printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(sc_grid),
+ sizeof(sc_ctu_record), sizeof(sc_search_cfg), sizeof(sc_layout), sizeof(sc_search_result),
+ sizeof(sc_shard_best), sizeof(sc_status), sizeof(sc_rect), sizeof(sc_partition),
+ sizeof(sc_partition_stats));return 0;}"""
     with tempfile.TemporaryDirectory() as d:
         c = os.path.join(d, "t.c")
         open(c, "w").write(src)
@@ -51,8 +52,32 @@ int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(sc_grid), sizeof(
         sizes = list(map(int, subprocess.run([exe], capture_output=True, text=True,
                                              check=True).stdout.split()))
     mine = [C.sizeof(_abi.Grid), C.sizeof(_abi.CtuRecord), C.sizeof(_abi.SearchCfg),
-            C.sizeof(_abi.Layout), C.sizeof(_abi.SearchResult), C.sizeof(_abi.ShardBest), 4]
+            C.sizeof(_abi.Layout), C.sizeof(_abi.SearchResult), C.sizeof(_abi.ShardBest), 4,
+            C.sizeof(_abi.Rect), C.sizeof(_abi.PartitionC), C.sizeof(_abi.PartitionStats)]
     assert sizes == mine
+
+
+def test_uniform_partition_matches_reference_golden():
+    """sc_uniform_partition (host code) == the reference's uniform_partition
+    (grid.cpp:186-262) on factorizable, prime-fallback and too-many-slice
+    cases (tests/golden/uniform.json)."""
+    import json
+    from paper_2012_14792_b200 import CtuGrid, SlicecraftError
+    from paper_2012_14792_b200.partitioner import Partition
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "uniform.json")))["partitions"]
+    for c in gold:
+        g = CtuGrid.make(c["cols"] * 32, c["rows"] * 32, 32)
+        if c["status"] != 0:
+            with pytest.raises(SlicecraftError) as e:
+                Partition.uniform(g, c["n"])
+            assert e.value.status == c["status"], c
+            continue
+        if c["n"] > 64:
+            continue  # beyond SC_MAX_SLICES
+        p = Partition.uniform(g, c["n"])
+        assert p.col_widths == c["tile_cols"], c
+        assert p.row_heights == c["tile_rows"], c
+        assert p.rects() == [tuple(x) for x in c["slices"]], c
 
 
 def test_grid_make_matches_reference_rules():

@@ -408,3 +408,80 @@ def test_errors(part):
     with pytest.raises(SlicecraftError) as e:
         part.two_step_batch(g, est, bad, SearchConfig(n_slices=1))
     assert e.value.kind == "FormatError"
+
+
+# ---- UniformOnly family and partition evaluation -----------
+def _uniform_gold():
+    return json.load(open(os.path.join(GOLDEN, "uniform.json")))
+
+
+def test_uniform_only_family_vs_reference_golden(part):
+    """min_time_search / constrained_clustering_search / two_step with the
+    UniformOnly family (search.cpp:265-275, 349-364) against the reference:
+    values, counts, the uniform Partition, and the NoCandidateError cases
+    (area constraint; time budget)."""
+    from paper_2012_14792_b200 import RECORD_DTYPE, CtuGrid, SearchConfig, SlicecraftError
+    for i, c in enumerate(_uniform_gold()["searches"]):
+        g = CtuGrid.make(c["w"], c["h"], c["ctu"])
+        cfg = SearchConfig(n_slices=c["n"], lambda_=c["lambda"], k_area=c["k"], family=1)
+        est = np.array(c["est"])[None]
+        rec = np.zeros((1, g.cell_count()), RECORD_DTYPE)
+        r3 = np.array(c["records"], dtype=np.uint64)
+        rec["count"], rec["sum"], rec["sumsq"] = r3[:, 0], r3[:, 1], r3[:, 2]
+        if c["status1"] != 0:
+            with pytest.raises(SlicecraftError) as e:
+                part.min_time_search_batch(g, est, cfg)
+            assert e.value.status == c["status1"], i
+            assert part.count_candidates(g, cfg) == 0
+            continue
+        assert part.count_candidates(g, cfg) == 1
+        o1 = part.min_time_search_batch(g, est, cfg)[0]
+        assert o1.t_min_us == c["t_min"], i
+        assert o1.argmin.rects() == [tuple(x) for x in c["argmin"]], i
+        assert o1.argmin.origin == "uniform"
+        o2 = part.constrained_clustering_batch(g, est, rec, [c["t_min"]], cfg)[0]
+        assert c["status2"] == 0
+        assert o2.t_best_us == c["t_best"] and o2.sse_best == c["sse_best"], i
+        assert o2.best.rects() == [tuple(x) for x in c["best"]], i
+        assert o2.candidates_step2 == c["candidates_step2"] == 1
+        assert o2.candidates_evaluated == c["candidates_evaluated"]
+        o3 = part.two_step_batch(g, est, rec, cfg)[0]
+        assert (o3.t_min_us, o3.t_best_us, o3.sse_best) == (c["t_min"], c["t_best"], c["sse_best"])
+        assert (o3.candidates_step1, o3.candidates_step2, o3.candidates_evaluated) == (1, 1, 2)
+        over = SearchConfig(n_slices=c["n"], lambda_=0.0, k_area=c["k"], family=1)
+        with pytest.raises(SlicecraftError) as e:
+            part.constrained_clustering_batch(g, est, rec, [c["t_min"] * 0.5], over)
+        assert e.value.status == c["status_over"] == 10
+
+
+def test_partition_eval_vs_reference_golden(part):
+    """sc_partition_eval == partition_time (cost.cpp:117-145: max from slice 0
+    with strict >, total in id order, raw sums incl. negative times) and
+    partition_sse (texture.cpp:183-189) of the reference, bit for bit; the
+    per-slice values equal the oracle's rectangle tables."""
+    from paper_2012_14792_b200 import RECORD_DTYPE, CtuGrid
+    from paper_2012_14792_b200.partitioner import Partition, Slice
+    for i, c in enumerate(_uniform_gold()["evals"]):
+        g = CtuGrid.make(c["w"], c["h"], c["ctu"])
+        p = Partition(g, [], [g.rows], [Slice(*s) for s in c["slices"]])
+        rec = np.zeros((1, g.cell_count()), RECORD_DTYPE)
+        r3 = np.array(c["records"], dtype=np.uint64)
+        rec["count"], rec["sum"], rec["sumsq"] = r3[:, 0], r3[:, 1], r3[:, 2]
+        est = np.array(c["est"])[None]
+        res, st, sm = part.partition_eval(p, est, rec, slice_values=True)
+        assert c["status"] == 0
+        r = res[0]
+        assert (r["max_us"], r["total_us"], r["argmax"], r["sse"]) == \
+            (c["max_us"], c["total_us"], c["argmax"], c["sse"]), i
+        for s in c["slices"]:  # slice moments by id
+            x0, y0, w, h, sid = s
+            cells = [(y, x) for y in range(y0, y0 + h) for x in range(x0, x0 + w)]
+            tot = r3[[y * g.cols + x for y, x in cells]].sum(axis=0)
+            assert tuple(int(v) for v in sm[0][sid]) == tuple(int(v) for v in tot), (i, sid)
+    # batch of frames, est only / records only
+    g = CtuGrid.make(8 * 32, 5 * 32, 32)
+    p = Partition.uniform(g, 6)
+    rng = np.random.default_rng(5)
+    est = rng.lognormal(0, 0.5, size=(7, g.cell_count()))
+    res = part.partition_eval(p, est=est)
+    assert len(res) == 7 and all(r["argmax"] >= 0 for r in res)
