@@ -192,6 +192,34 @@ sc_status sc_texture_moments(sc_ctx* ctx, const void* luma, int32_t bytes_per_sa
                              int32_t width, int32_t height, size_t pitch_bytes,
                              size_t frame_stride_bytes, int32_t ctu_size,
                              int32_t n_frames, sc_ctu_record* out);
+/* ---- raw YUV ingest (texture.cpp:9-81) ----------------------------------- */
+/* yuv_frame_count: whole planar 4:2:0 frames in the file (bit_depth 8 or 10).
+ * IoError (stat), FormatError (dimensions, bit depth, size not a multiple). */
+sc_status sc_yuv_frame_count(const char* path, int32_t width, int32_t height,
+                             int32_t bit_depth, int32_t* out);
+/* load_yuv_frame: the luma plane of frame `poc`, widened to uint16 (out:
+ * width * height).  RangeError for a poc outside the file. */
+sc_status sc_yuv_load_luma(const char* path, int32_t width, int32_t height, int32_t poc,
+                           int32_t bit_depth, uint16_t* out);
+/* Raw luma planes of frames [first_poc, first_poc + n_frames), in the file's
+ * own sample format (uint8, or uint16 LE for 10-bit), packed: n_frames *
+ * width * height * bytes_per_sample bytes into a host buffer.  Chroma is
+ * never read. */
+sc_status sc_yuv_read_luma(const char* path, int32_t width, int32_t height, int32_t bit_depth,
+                           int32_t first_poc, int32_t n_frames, void* out);
+/* K1 straight from a YUV file: sc_yuv_read_luma into pinned staging, then
+ * sc_texture_moments on the device (out: n_frames * cells records, host or
+ * device). */
+sc_status sc_yuv_texture_moments(sc_ctx* ctx, const char* path, int32_t width, int32_t height,
+                                 int32_t bit_depth, int32_t ctu_size, int32_t first_poc,
+                                 int32_t n_frames, sc_ctu_record* out);
+/* sc_partition_frames on frames [first_poc, first_poc + n_frames) of a YUV
+ * file (est: n_frames maps). */
+sc_status sc_partition_yuv(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                           const char* path, int32_t bit_depth, int32_t first_poc,
+                           int32_t n_frames, const double* est, sc_ctu_record* records_out,
+                           sc_search_result* out);
+
 /* TextureStats ctor validation (texture.cpp:90-111) of caller records. */
 sc_status sc_texture_validate(const sc_grid* grid, const sc_ctu_record* records);
 

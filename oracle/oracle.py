@@ -232,6 +232,16 @@ class Ref:
                                  _p(est), C.byref(src), C.byref(srcp))
         return st, est, src.value, srcp.value
 
+    def yuv_frame_count(self, path, w, h, bit_depth):
+        n = C.c_int()
+        st = self.L.ref_yuv_frame_count(path.encode(), w, h, bit_depth, C.byref(n))
+        return st, n.value
+
+    def load_yuv_frame(self, path, w, h, poc, bit_depth):
+        out = np.zeros((h, w), np.uint16)
+        st = self.L.ref_load_yuv_frame(path.encode(), w, h, poc, bit_depth, _p(out))
+        return st, out
+
     def uniform_partition(self, fw, fh, ctu, n):
         """uniform_partition (grid.cpp:186-262) -> (status, RefLayout)."""
         lay = RefLayout()

@@ -359,4 +359,20 @@ int ref_partition_eval(int fw, int fh, int ctu, int n_cols, const int* col_width
   } catch (...) { return map_exception(); }
 }
 
+// yuv_frame_count (texture.cpp:25-40) and load_yuv_frame (texture.cpp:42-81)
+int ref_yuv_frame_count(const char* path, int w, int h, int bit_depth, int* out) {
+  try {
+    *out = yuv_frame_count(path, w, h, bit_depth);
+    return 0;
+  } catch (...) { return map_exception(); }
+}
+
+int ref_load_yuv_frame(const char* path, int w, int h, int poc, int bit_depth, uint16_t* out) {
+  try {
+    const LumaPlane p = load_yuv_frame(path, w, h, poc, bit_depth);
+    std::memcpy(out, p.samples.data(), p.samples.size() * sizeof(uint16_t));
+    return 0;
+  } catch (...) { return map_exception(); }
+}
+
 }  // extern "C"

@@ -98,6 +98,15 @@ SIGNATURES = [
     ("sc_ctx_set_stream", C.c_int, [_P, _P]),
     ("sc_ctx_timings", C.c_int, [_P, _P]),
     ("sc_uniform_partition", C.c_int, [C.POINTER(Grid), C.c_int32, C.POINTER(PartitionC)]),
+    ("sc_yuv_frame_count", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(C.c_int32)]),
+    ("sc_yuv_load_luma", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
+    ("sc_yuv_read_luma", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                   C.c_int32, _P]),
+    ("sc_yuv_texture_moments", C.c_int, [_P, C.c_char_p, C.c_int32, C.c_int32, C.c_int32,
+                                         C.c_int32, C.c_int32, C.c_int32, _P]),
+    ("sc_partition_yuv", C.c_int, [_P, C.POINTER(Grid), C.POINTER(SearchCfg), C.c_char_p,
+                                   C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
     ("sc_partition_eval", C.c_int, [_P, C.POINTER(Grid), _P, C.c_int32, _P, _P, C.c_int32, _P,
                                     _P, _P]),
     ("sc_texture_moments", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_size_t,

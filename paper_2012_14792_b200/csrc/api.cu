@@ -38,6 +38,9 @@ void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int 
 void partition_eval_device(const double* d_sat, const uint64_t* d_usat, const int* d_rects, int n,
                            int cols, int rows, int frames, sc_partition_stats* d_out,
                            double* d_slice_times, sc_ctu_record* d_slice_mom, cudaStream_t st);
+int yuv_bytes_per_sample(int bit_depth);
+int yuv_frame_count(const char* path, int w, int h, int bit_depth);
+void yuv_read_luma(const char* path, int w, int h, int bit_depth, int first, int n, void* dst);
 void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
                      const LaneBest* lanes, const uint8_t* snaps,
                      const unsigned long long* count, const unsigned long long* scored,
@@ -436,6 +439,29 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // are given; est / records / t_min_in are host or device pointers.
 //   main stream : est -> K2/K3 time tables -> step 1 -> [join] -> step 2
 //   side stream : luma H2D -> K1 -> K2/K3 moment tables          (overlaps step 1)
+// The luma batch on the device: device pointers are used in place; host
+// batches are copied on `s`, luma planes only (a frame stride wider than the
+// plane, e.g. planar 4:2:0 frames, is skipped by a 2D copy).  Returns the
+// device pointer and its frame stride.
+const void* stage_luma(sc_ctx* ctx, const void* luma, int bps, int W, int H, size_t pitch,
+                       size_t fstride, int frames, cudaStream_t s, size_t* d_fstride) {
+  *d_fstride = fstride;
+  if (is_device_ptr(luma)) return luma;
+  const size_t plane = pitch * (H - 1) + (size_t)W * bps;
+  if (frames > 1 && fstride > pitch * H) {
+    const size_t dense = pitch * H;
+    ctx->luma.ensure(dense * frames);
+    SCB_CUDA(cudaMemcpy2DAsync(ctx->luma.p, dense, luma, fstride, plane, frames,
+                               cudaMemcpyHostToDevice, s));
+    *d_fstride = dense;
+    return ctx->luma.p;
+  }
+  const size_t span = (size_t)(frames - 1) * fstride + plane;
+  ctx->luma.ensure(span);
+  SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyHostToDevice, s));
+  return ctx->luma.p;
+}
+
 // Host uniform_partition (plan.h) with the reference's errors.
 UniformPartition uniform_or_fail(const sc_grid& g, int n) {
   UniformPartition u;
@@ -528,15 +554,10 @@ void run_uniform(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int fr
   bool resident = false;
   if (do2 && luma) {  // K1 on the batch
     const int W = g.frame_width, H = g.frame_height;
-    const size_t span = (size_t)(frames - 1) * fstride + pitch * (H - 1) + (size_t)W * bps;
-    const void* d_luma = luma;
-    if (!is_device_ptr(luma)) {
-      ctx->luma.ensure(span);
-      SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyDefault, s));
-      d_luma = ctx->luma.p;
-    }
+    size_t dfs = fstride;
+    const void* d_luma = stage_luma(ctx, luma, bps, W, H, pitch, fstride, frames, s, &dfs);
     ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
-    texture_moments_device(d_luma, bps, W, H, pitch, fstride, g.ctu_size, frames, g.cols, g.rows,
+    texture_moments_device(d_luma, bps, W, H, pitch, dfs, g.ctu_size, frames, g.cols, g.rows,
                            ctx->records.as<sc_ctu_record>(), s);
     resident = true;
   }
@@ -624,15 +645,10 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
       ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
       if (luma) {
         const int W = g.frame_width, H = g.frame_height;
-        const size_t span = (size_t)(frames - 1) * fstride + pitch * (H - 1) + (size_t)W * bps;
-        const void* d_luma = luma;
-        if (!is_device_ptr(luma)) {
-          ctx->luma.ensure(span);
-          SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyDefault, s2));
-          d_luma = ctx->luma.p;
-        }
+        size_t dfs = fstride;
+        const void* d_luma = stage_luma(ctx, luma, bps, W, H, pitch, fstride, frames, s2, &dfs);
         SCB_CUDA(cudaEventRecord(ev[4], s2));
-        texture_moments_device(d_luma, bps, W, H, pitch, fstride, g.ctu_size, frames, g.cols, g.rows,
+        texture_moments_device(d_luma, bps, W, H, pitch, dfs, g.ctu_size, frames, g.cols, g.rows,
                                ctx->records.as<sc_ctu_record>(), s2);
       } else {
         SCB_CUDA(cudaMemcpyAsync(ctx->records.p, records, cells * frames * sizeof(sc_ctu_record),
@@ -741,6 +757,7 @@ sc_ctx::~sc_ctx() {
                   &rk_flags, &rk_offsets, &rk_temp})
     b->release();
   h_stage.release();
+  h_luma.release();
   h_records.release();
   h_frame_best.release();
   h_budget.release();
@@ -866,13 +883,8 @@ sc_status sc_texture_moments(sc_ctx* ctx, const void* luma, int32_t bps, int32_t
     if (pitch < (size_t)width * bps) fail(SC_ERR_GEOMETRY, "pitch smaller than a row");
     if (frames > 1 && fstride < pitch * height) fail(SC_ERR_GEOMETRY, "frame stride too small");
     cudaStream_t s = main_stream(ctx);
-    const size_t span = (size_t)(frames - 1) * fstride + pitch * (height - 1) + (size_t)width * bps;
-    const void* d_luma = luma;
-    if (!is_device_ptr(luma)) {
-      ctx->luma.ensure(span);
-      SCB_CUDA(cudaMemcpyAsync(ctx->luma.p, luma, span, cudaMemcpyDefault, s));
-      d_luma = ctx->luma.p;
-    }
+    size_t dfs = fstride;
+    const void* d_luma = stage_luma(ctx, luma, bps, width, height, pitch, fstride, frames, s, &dfs);
     const size_t cells = (size_t)g.cols * g.rows;
     sc_ctu_record* d_out = out;
     const bool out_dev = is_device_ptr(out);
@@ -881,7 +893,7 @@ sc_status sc_texture_moments(sc_ctx* ctx, const void* luma, int32_t bps, int32_t
       d_out = ctx->records.as<sc_ctu_record>();
     }
     SCB_CUDA(cudaEventRecord(ctx->ev[4], s));
-    texture_moments_device(d_luma, bps, width, height, pitch, fstride, ctu, frames, g.cols, g.rows,
+    texture_moments_device(d_luma, bps, width, height, pitch, dfs, ctu, frames, g.cols, g.rows,
                            d_out, s);
     SCB_CUDA(cudaEventRecord(ctx->ev[5], s));
     if (!out_dev)
@@ -1009,6 +1021,76 @@ sc_status sc_count_candidates(sc_ctx* ctx, const sc_grid* grid, const sc_search_
                  false, &r, nullptr);
     *count = r.candidates_step1;
   });
+}
+
+sc_status sc_yuv_frame_count(const char* path, int32_t w, int32_t h, int32_t bit_depth,
+                             int32_t* out) {
+  return guarded([&] {
+    if (!path || !out) fail(SC_ERR_USAGE, "NULL argument");
+    *out = yuv_frame_count(path, w, h, bit_depth);
+  });
+}
+
+sc_status sc_yuv_load_luma(const char* path, int32_t w, int32_t h, int32_t poc,
+                           int32_t bit_depth, uint16_t* out) {
+  return guarded([&] {
+    if (!path || !out) fail(SC_ERR_USAGE, "NULL argument");
+    const int bps = yuv_bytes_per_sample(bit_depth);
+    const size_t n = (size_t)w * h;
+    if (bps == 2) {  // little-endian 16-bit containers (texture.cpp:64-72)
+      std::vector<uint8_t> raw(n * 2);
+      yuv_read_luma(path, w, h, bit_depth, poc, 1, raw.data());
+      for (size_t i = 0; i < n; ++i) out[i] = (uint16_t)(raw[2 * i] | (raw[2 * i + 1] << 8));
+    } else {
+      std::vector<uint8_t> raw(n);
+      yuv_read_luma(path, w, h, bit_depth, poc, 1, raw.data());
+      for (size_t i = 0; i < n; ++i) out[i] = raw[i];
+    }
+  });
+}
+
+sc_status sc_yuv_read_luma(const char* path, int32_t w, int32_t h, int32_t bit_depth,
+                           int32_t first, int32_t n, void* out) {
+  return guarded([&] {
+    if (!path || !out) fail(SC_ERR_USAGE, "NULL argument");
+    yuv_read_luma(path, w, h, bit_depth, first, n, out);
+  });
+}
+
+// Luma planes of a YUV file in the context's pinned staging buffer.
+const void* yuv_stage(sc_ctx* ctx, const char* path, int w, int h, int bit_depth, int first,
+                      int n) {
+  const size_t plane = (size_t)w * h * yuv_bytes_per_sample(bit_depth);
+  ctx->h_luma.ensure(plane * (size_t)std::max(n, 1));
+  yuv_read_luma(path, w, h, bit_depth, first, n, ctx->h_luma.p);
+  return ctx->h_luma.p;
+}
+
+sc_status sc_yuv_texture_moments(sc_ctx* ctx, const char* path, int32_t w, int32_t h,
+                                 int32_t bit_depth, int32_t ctu, int32_t first, int32_t n,
+                                 sc_ctu_record* out) {
+  if (!ctx || !path || !out) return set_error(SC_ERR_USAGE, "NULL argument");
+  const void* luma = nullptr;
+  const sc_status st = guarded([&] { luma = yuv_stage(ctx, path, w, h, bit_depth, first, n); });
+  if (st != SC_OK) return st;
+  const int bps = bit_depth == 8 ? 1 : 2;
+  return sc_texture_moments(ctx, luma, bps, w, h, (size_t)w * bps, (size_t)w * h * bps, ctu, n,
+                            out);
+}
+
+sc_status sc_partition_yuv(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                           const char* path, int32_t bit_depth, int32_t first, int32_t n,
+                           const double* est, sc_ctu_record* records_out, sc_search_result* out) {
+  if (!ctx || !grid || !path) return set_error(SC_ERR_USAGE, "NULL argument");
+  const void* luma = nullptr;
+  const sc_status st = guarded([&] {
+    luma = yuv_stage(ctx, path, grid->frame_width, grid->frame_height, bit_depth, first, n);
+  });
+  if (st != SC_OK) return st;
+  const int bps = bit_depth == 8 ? 1 : 2;
+  const int W = grid->frame_width, H = grid->frame_height;
+  return sc_partition_frames(ctx, grid, cfg, luma, bps, (size_t)W * bps, (size_t)W * H * bps, est,
+                             n, records_out, out);
 }
 
 sc_status sc_uniform_partition(const sc_grid* grid, int32_t n_slices, sc_partition* out) {

@@ -178,7 +178,7 @@ struct sc_ctx {
   scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
   scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp;       // rank.cu scratch
   int dec_cols = -1, dec_rows = -1;
-  scb::HostBuf h_stage, h_records, h_frame_best, h_budget;
+  scb::HostBuf h_stage, h_records, h_frame_best, h_budget, h_luma;  // h_luma: YUV reads
   std::vector<scb::Plan*> plans;
   // last step results (for shard export)
   std::vector<scb::FrameBest> last_best[2];

@@ -388,6 +388,26 @@ class Partitioner:
                for o in out]
         return (res, st, sm) if slice_values else res
 
+    def ctu_stats_yuv(self, path: str, grid: CtuGrid, bit_depth: int, first_poc: int = 0,
+                      n_frames: int = 1) -> np.ndarray:
+        """K1 straight from a planar 4:2:0 file: luma planes only, no widening."""
+        out = np.zeros((n_frames, grid.cell_count()), RECORD_DTYPE)
+        check(lib().sc_yuv_texture_moments(self._h, path.encode(), grid.frame_width,
+                                           grid.frame_height, bit_depth, grid.ctu_size, first_poc,
+                                           n_frames, _ptr(out)))
+        return out
+
+    def partition_yuv(self, grid: CtuGrid, path: str, bit_depth: int, first_poc: int,
+                      est: np.ndarray, cfg: SearchConfig, records_out: Optional[np.ndarray] = None):
+        """partition_frames over frames [first_poc, first_poc + len(est)) of a YUV file."""
+        est = np.ascontiguousarray(est, dtype=np.float64).reshape(-1, grid.cell_count())
+        F = est.shape[0]
+        res = (SearchResult * F)()
+        check(lib().sc_partition_yuv(self._h, C.byref(grid.c()), C.byref(cfg.c()), path.encode(),
+                                     bit_depth, first_poc, F, _ptr(est), _ptr(records_out),
+                                     C.cast(res, C.c_void_p)))
+        return res
+
     def count_candidates(self, grid: CtuGrid, cfg: SearchConfig) -> int:
         n = C.c_uint64()
         check(lib().sc_count_candidates(self._h, C.byref(grid.c()), C.byref(cfg.c()), C.byref(n)))
@@ -404,6 +424,29 @@ def shard_merge(step: int, world: int, frames: int, gathered: bytes, results) ->
     buf = (ShardBest * (world * frames)).from_buffer_copy(gathered)
     check(lib().sc_shard_merge(step, world, frames, C.cast(buf, C.c_void_p),
                                C.cast(results, C.c_void_p)))
+
+
+def yuv_frame_count(path: str, width: int, height: int, bit_depth: int) -> int:
+    """yuv_frame_count (texture.cpp:25-40)."""
+    n = C.c_int32()
+    check(lib().sc_yuv_frame_count(path.encode(), width, height, bit_depth, C.byref(n)))
+    return n.value
+
+
+def load_yuv_frame(path: str, width: int, height: int, poc: int, bit_depth: int) -> np.ndarray:
+    """load_yuv_frame (texture.cpp:42-81): the luma plane widened to uint16."""
+    out = np.empty((height, width), np.uint16)
+    check(lib().sc_yuv_load_luma(path.encode(), width, height, poc, bit_depth, _ptr(out)))
+    return out
+
+
+def read_yuv_luma(path: str, width: int, height: int, bit_depth: int, first_poc: int,
+                  n_frames: int) -> np.ndarray:
+    """Raw luma planes (uint8, or uint16 for 10-bit) of consecutive frames."""
+    out = np.empty((n_frames, height, width), np.uint8 if bit_depth == 8 else np.uint16)
+    check(lib().sc_yuv_read_luma(path.encode(), width, height, bit_depth, first_poc, n_frames,
+                                 _ptr(out)))
+    return out
 
 
 def texture_validate(grid: CtuGrid, records: np.ndarray) -> None:
