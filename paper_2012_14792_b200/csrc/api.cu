@@ -300,6 +300,28 @@ bool step2_bounded(const sc_search_cfg& cfg) {
   return !(v && v[0] == '0');
 }
 
+// Cost-ordered schedule of the exhaustive step-1 walk (Plan::order_state);
+// SLICECRAFT_B200_SCHEDULE=0 keeps the enumeration order.
+bool schedule_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_SCHEDULE");
+  return !(v && v[0] == '0');
+}
+
+// After a measuring call: items by decreasing measured walk cost (ties by
+// index), uploaded for the next calls.
+void finish_schedule(Plan* p) {
+  if (p->order_state != 1) return;
+  const size_t n = p->items.size();
+  std::vector<uint32_t> cost(n), order(n);
+  SCB_CUDA(cudaMemcpy(cost.data(), p->d_cost.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n; ++i) order[i] = (uint32_t)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+  p->d_order.ensure(n * sizeof(uint32_t));
+  SCB_CUDA(cudaMemcpy(p->d_order.p, order.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  p->order_state = 2;
+}
+
 // One search step over all frame groups; finalize writes FrameBest[step] and,
 // after step 1, the device budgets of step 2.  No host synchronisation.
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
@@ -324,6 +346,11 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
   const uint32_t mine = total > rank ? (total - rank + world - 1) / world : 0;
   FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)(step - 1) * L.groups * L.fpw;
   const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
+  const bool sched = step == 1 && !prune && world == 1 && schedule_enabled();
+  if (sched && plan->order_state != 2) {
+    plan->d_cost.ensure(plan->items.size() * sizeof(uint32_t));
+    plan->order_state = 1;
+  }
   const int rstride = std::min(cfg.n_slices, g.rows) + 1;
   const size_t lb_per_group = (size_t)n_xw(g.cols) * rstride * L.fpw;
   if (prune) {
@@ -369,6 +396,10 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     a.rts = ctx->rt_split.as<uint32_t>() + (size_t)gi * L.nr * L.fpw;
     a.rs = step == 2 ? ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw : nullptr;
     a.budget = ctx->budget.as<int64_t>() + (size_t)gi * L.fpw;
+    if (sched) {
+      if (plan->order_state == 2) a.order = plan->d_order.as<uint32_t>();
+      else a.cost = plan->d_cost.as<uint32_t>();
+    }
     a.lanes = reinterpret_cast<LaneBest*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
     a.snaps = ctx->snaps.as<uint8_t>() + snap_bytes * gi;
     if (prune && step == 1 && mine > 1) {
@@ -680,6 +711,7 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
                              cudaMemcpyDefault, s));
   SCB_CUDA(cudaEventRecord(ev[9], s));
   SCB_CUDA(cudaStreamSynchronize(s));
+  finish_schedule(plan);
   // timings
   ctx->timings[0] = need_moments && luma ? 1000.0 * ev_ms(ev[4], ev[5]) : 0.0;
   ctx->timings[1] = 1000.0 * (ev_ms(ev[0], ev[1]) + (need_moments ? ev_ms(ev[5], ev[6]) : 0.f));
@@ -764,6 +796,8 @@ sc_ctx::~sc_ctx() {
   for (Plan* p : plans) {
     p->d_items.release();
     p->d_bmax.release();
+    p->d_order.release();
+    p->d_cost.release();
     delete p;
   }
   for (auto& e : ev)

@@ -107,6 +107,10 @@ struct Plan {
   bool pathological = false;  // some single area fails the test (k ~ 1)
   uint32_t seed_items = 0;    // pruned mode: items of the seeding phase
   bool have_count = false;    // exact DP count computed (pruned mode)
+  // exhaustive step 1 schedule: the first call measures each item's walk
+  // cost, later calls take the items in decreasing cost (shorter tail)
+  int order_state = 0;        // 0: measure, 1: measured (copy pending), 2: ordered
+  DevBuf d_order, d_cost;
   unsigned __int128 count = 0;
   DevBuf d_items, d_bmax;
   bool uploaded = false;
@@ -145,6 +149,8 @@ struct SearchArgs {
   const uint32_t* lbm;
   uint32_t* inc;                   // pruned mode: shared step-1 incumbent [FPW]
   const uint32_t* seed_inc;        // pruned mode, phase B: incumbent frozen after phase A
+  const uint32_t* order;           // exhaustive step 1: item k -> work item (or nullptr)
+  uint32_t* cost;                  // per work item: walk cycles / 64 (or nullptr)
 };
 
 // Device-side per-frame result written by finalize.

@@ -111,10 +111,13 @@ __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(Se
     if (lane == 0) k = a.k_begin + atomicAdd(a.counter, 1u);
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= a.n_items) break;
-    const uint64_t item = (uint64_t)a.item_offset + (uint64_t)k * a.item_stride;
+    const uint64_t item =
+        a.order ? (uint64_t)a.order[k] : (uint64_t)a.item_offset + (uint64_t)k * a.item_stride;
     const WorkItem wi = a.items[item];
+    const long long c0 = a.cost ? clock64() : 0;
     walk_item<FPW, STEP, PRUNE>(e, item, wi, f, slot, st);
     __syncwarp();
+    if (a.cost && lane == 0) a.cost[item] = (uint32_t)min((clock64() - c0) >> 6, 0xffffffffll);
   }
   LaneBest lb;
   lb.t = st.best_t == kKeyInf ? ~0ull : (uint64_t)st.best_t;

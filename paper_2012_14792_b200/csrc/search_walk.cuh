@@ -134,6 +134,7 @@ struct LaneState {
   uint64_t count;   // candidates enumerated (uniform over the warp)
   uint64_t scored;  // candidates this lane actually scored
   tkey inc;         // last seen shared incumbent (pruned step 1)
+  tkey bcmp;        // exhaustive step 1: a candidate wins iff t < bcmp (see walk_item)
   uint8_t* snap;
 };
 
@@ -230,6 +231,12 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   const double* rs = e.rs;
   const int c = wi.c, d = wi.d;
   uint64_t ord = 0;  // ordinal of the next candidate inside this item
+  // Exhaustive step 1 may take items in any order (api.cu schedules them by
+  // measured cost): a candidate beats the lane's best iff its time is lower,
+  // or equal with an earlier item; inside an item candidates come in order,
+  // so after the first update the comparison is strict again.
+  if (STEP == 1 && !PRUNE)
+    st.bcmp = (st.best_t != kKeyInf && item < st.best_item) ? st.best_t + 1 : st.best_t;
 
   // warp-uniform DFS state (identical in every lane of the warp)
   int W[SC_MAX_COLS], R[SC_MAX_COLS], X0[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
@@ -264,11 +271,19 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   };
   // snapshot of the current candidate; run `lr` takes height lh and the
   // forced run lr+1 the rest of its column (lr < 0: no leaf loop).
+  // (rolled loops: constant indices would pull W and R into 32 registers)
   auto take_snapshot = [&](int lr, int lh, int lrest) {
-    for (int i = 0; i < SC_MAX_COLS; ++i) {
-      st.snap[i] = (uint8_t)(i < c ? W[i] : 0);
-      st.snap[SC_MAX_COLS + i] = (uint8_t)(i < c ? R[i] : 0);
+#pragma unroll 1
+    for (int i = 0; i < c; ++i) {
+      st.snap[i] = (uint8_t)W[i];
+      st.snap[SC_MAX_COLS + i] = (uint8_t)R[i];
     }
+#pragma unroll 1
+    for (int i = c; i < SC_MAX_COLS; ++i) {
+      st.snap[i] = 0;
+      st.snap[SC_MAX_COLS + i] = 0;
+    }
+#pragma unroll 1
     for (int i = 0; i < e.n; ++i) {
       uint8_t v = curH[i];
       if (i == lr) v = (uint8_t)lh;
@@ -312,8 +327,9 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   auto score = [&](tkey t, uint64_t o, int lr, int lh, int lrest) {
     if (PRUNE) ++st.scored;
     if (STEP == 1) {
-      if (t < st.best_t) {
+      if (t < (PRUNE ? st.best_t : st.bcmp)) {
         st.best_t = t;
+        st.bcmp = t;
         st.best_item = item;
         st.best_ord = o;
         take_snapshot(lr, lh, lrest);

@@ -21,7 +21,9 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
                           int warps, size_t item_target, int item_offset, int item_stride,
                           double* out_t, double* out_sse, uint64_t* out_count,
                           uint8_t* out_snap /*[F][96]*/, int* out_found, uint64_t* out_item,
-                          uint64_t* out_ord) {
+                          uint64_t* out_ord, int order_mode) {
+  // order_mode (exhaustive step 1 only, like api.cu's cost schedule): 0 the
+  // enumeration order, 1 reversed, 2 a fixed pseudo-random permutation
   if (frames < 1 || frames > 32) return 1;
   int fpw = 1;
   while (fpw < frames) fpw <<= 1;
@@ -150,7 +152,18 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
                           ? (items.size() - item_offset + item_stride - 1) / item_stride
                           : 0;
   const size_t seed_local = (prune && step == 1) ? std::min(mine, seed_items) : 0;
-  for (size_t it = (size_t)item_offset; it < items.size(); it += (size_t)item_stride, ++kk) {
+  std::vector<size_t> seq;
+  for (size_t it = (size_t)item_offset; it < items.size(); it += (size_t)item_stride) seq.push_back(it);
+  if (step == 1 && !prune && order_mode == 1) std::reverse(seq.begin(), seq.end());
+  if (step == 1 && !prune && order_mode == 2) {
+    uint64_t z = 0x9e3779b97f4a7c15ull;
+    for (size_t i = seq.size(); i > 1; --i) {
+      z = z * 6364136223846793005ull + 1442695040888963407ull;
+      std::swap(seq[i - 1], seq[(size_t)((z >> 33) % i)]);
+    }
+  }
+  for (size_t si = 0; si < seq.size(); ++si, ++kk) {
+    const size_t it = seq[si];
     if (prune && step == 1 && kk == seed_local && seed_local > 0) {  // phase B begins
       frozen = inc;
       e.seed_inc = frozen.data();

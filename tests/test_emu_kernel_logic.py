@@ -43,6 +43,34 @@ def test_step1_vs_oracle(emu, oracle, seed, prune):
             assert Emu.slices(snap[f], n, rows) == r.argmin1.slices(rows), ctx
 
 
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("seed", range(3))
+def test_step1_any_item_order(emu, oracle, seed, order):
+    """Exhaustive step 1 with the work items taken out of enumeration order
+    (reversed / permuted, as the cost-ordered schedule does): the lanes' tie
+    rule still returns the reference's first-in-order argmin.  Times are
+    rounded hard so that many candidates tie."""
+    from emu.emu import Emu
+    rng = np.random.default_rng(500 + seed)
+    for trial in range(40):
+        cols, rows, n = _case(rng, 9)
+        mc = int(rng.integers(0, 5))
+        cov = int(rng.integers(0, 2))
+        F = int(rng.choice([1, 2, 4, 8, 32]))
+        est = np.round(rng.lognormal(0, 0.4, size=(F, cols * rows)) * 2) / 2
+        rt = np.stack([oracle.rect_times(est[f], cols, rows) for f in range(F)])
+        t, _, cnt, snap, found = emu.search(cols, rows, n, 3.0, mc, cov, 1, rt,
+                                            item_target=int(rng.choice([1, 16, 64])),
+                                            warps=int(rng.integers(1, 5)), order=order)
+        for f in range(F):
+            st, r = oracle.search(cols * 64, rows * 64, 64, est[f], None, n, 0.0, 3.0, mc, cov, 1)
+            if st:
+                continue
+            ctx = (seed, trial, f, cols, rows, n, mc, cov, F)
+            assert t[f] == r.t_min_us and cnt[f] == r.candidates_step1, ctx
+            assert Emu.slices(snap[f], n, rows) == r.argmin1.slices(rows), ctx
+
+
 @pytest.mark.parametrize("prune", [0, 1])
 @pytest.mark.parametrize("seed", range(3))
 def test_step2_vs_oracle(emu, oracle, seed, prune):

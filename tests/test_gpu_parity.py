@@ -297,6 +297,29 @@ def test_candidate_space_shards(part, oracle, monkeypatch, m, world):
         assert Partition.from_layout(g, r2.best).rects() == e.best.slices(g.rows), (m, f)
 
 
+def test_cost_ordered_schedule_keeps_first_in_order(part, oracle):
+    """The first exhaustive call measures each work item's walk cost, later
+    calls take the items by decreasing cost; with heavily tied times the
+    argmin is still the reference's first-in-order one on every call."""
+    from paper_2012_14792_b200 import CtuGrid, SearchConfig
+    from paper_2012_14792_b200.partitioner import Partition
+    rng = np.random.default_rng(99)
+    g = CtuGrid.make(9 * 64, 7 * 64, 64)
+    F = 6
+    est = np.round(rng.lognormal(0, 0.3, size=(F, g.cell_count())) * 2) / 2
+    cfg = SearchConfig(n_slices=6, lambda_=0.0, k_area=3.0, max_tile_cols=4)
+    exp = [oracle.search(g.frame_width, g.frame_height, 64, est[f], None, 6, 0.0, 3.0, 4, 0, 1)
+           for f in range(F)]
+    for call in range(3):
+        out = part.min_time_search_batch(g, est, cfg)
+        for f in range(F):
+            st, e = exp[f]
+            assert st == 0
+            assert out[f].t_min_us == e.t_min_us, (call, f)
+            assert out[f].argmin.rects() == e.argmin1.slices(g.rows), (call, f)
+            assert out[f].candidates_step1 == e.candidates_step1
+
+
 def test_cfg3_counts_all_frames(part):
     """Size-independent checks on the full cfg3 batch: counts, budget, feasibility."""
     w, tr, luma = _config_inputs(3, 32)
