@@ -186,8 +186,11 @@ def run_ours(args):
         call(luma_d.data_ptr(), est_d.data_ptr())
     if args.warmup <= 0:
         call(luma_d.data_ptr(), est_d.data_ptr())  # counts for the metric
-    cands = sum(r.candidates_step1 + r.candidates_step2 for r in res)
-    counts = sorted({(r.candidates_step1, r.candidates_step2) for r in res})
+    # exact counts: the low 64 bits plus candidates_step*_hi (cfg5 is ~6.1e29)
+    c1 = [r.candidates_step1 | (r.candidates_step1_hi << 64) for r in res]
+    c2 = [r.candidates_step2 | (r.candidates_step2_hi << 64) for r in res]
+    cands = sum(c1) + sum(c2)
+    counts = sorted(set(zip(c1, c2)))
 
     # ---- timed: device-resident inputs ----
     clocks = Clocks(local)

@@ -24,9 +24,12 @@ namespace scb {
 #if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
 struct WalkStats {
   uint64_t widths, runs_steps, skeletons, levels, leaf_calls, leaves, levels_leafcol, leafr[65];
+  uint64_t width_steps, items;
 };
 inline WalkStats g_stats;
 #define SCB_STAT(x) (++g_stats.x)
+#elif defined(SCB_COUNT_STEPS) && defined(__CUDA_ARCH__)
+#define SCB_STAT(x) (++st.scored)  // diagnostics build: DFS steps in `scored`
 #else
 #define SCB_STAT(x) ((void)0)
 #endif
@@ -387,6 +390,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           continue;
         }
         W[pos] = wv;
+        SCB_STAT(width_steps);
         const int nL = imax(WL[pos], SCB_ILO(wv * e.rstride + rmax_c));
         const int nH = imin(WH[pos], wv * rows);
         if (nL > nH) continue;
