@@ -302,6 +302,20 @@ bool step2_bounded(const sc_search_cfg& cfg) {
 
 // Cost-ordered schedule of the exhaustive step-1 walk (Plan::order_state);
 // SLICECRAFT_B200_SCHEDULE=0 keeps the enumeration order.
+// Pruned mode: warps sharing one work item (SLICECRAFT_B200_SPLIT, default
+// 8) and the heights level whose subtrees they deal out
+// (SLICECRAFT_B200_SPLIT_DEPTH, default 1).
+int split_ways() {
+  const char* v = getenv("SLICECRAFT_B200_SPLIT");
+  const int g = v ? atoi(v) : 8;
+  return g < 1 ? 1 : (g > 64 ? 64 : g);
+}
+int split_depth() {
+  const char* v = getenv("SLICECRAFT_B200_SPLIT_DEPTH");
+  const int d = v ? atoi(v) : 1;
+  return d < 0 ? 0 : (d > 8 ? 8 : d);
+}
+
 bool schedule_enabled() {
   const char* v = getenv("SLICECRAFT_B200_SCHEDULE");
   return !(v && v[0] == '0');
@@ -354,8 +368,8 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
   const int rstride = std::min(cfg.n_slices, g.rows) + 1;
   const size_t lb_per_group = (size_t)n_xw(g.cols) * rstride * L.fpw;
   if (prune) {
-    ctx->inc.ensure((size_t)L.groups * L.fpw * sizeof(uint32_t));
-    ctx->seed_inc.ensure((size_t)L.groups * L.fpw * sizeof(uint32_t));
+    ctx->inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+    ctx->seed_inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
     if (compute_bounds) {
       // column lower bounds from the time tables; shared incumbents to +inf
       ctx->lbr.ensure(lb_per_group * L.groups * sizeof(uint32_t));
@@ -366,7 +380,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
                              rstride - 1, rstride, ctx->lbr.as<uint32_t>() + gi * lb_per_group,
                              ctx->lbm.as<uint32_t>() + gi * lb_per_group, st);
     }
-    SCB_CUDA(cudaMemsetAsync(ctx->inc.p, 0xff, (size_t)L.groups * L.fpw * sizeof(uint32_t), st));
+    SCB_CUDA(cudaMemsetAsync(ctx->inc.p, 0xff, (size_t)L.groups * L.fpw * sizeof(uint64_t), st));
   }
   for (int gi = 0; gi < L.groups; ++gi) {
     SearchArgs a{};
@@ -377,7 +391,10 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     a.max_area = g.cols * g.rows;
     a.coverage = cfg.coverage;
     a.items = plan->d_items.as<WorkItem>();
-    a.n_items = mine;
+    const uint32_t G = prune ? (uint32_t)split_ways() : 1u;
+    a.split_g = (int)G;
+    a.split_depth = split_depth();
+    a.n_items = mine * G;
     a.item_offset = rank;
     a.item_stride = world;
     uint64_t* ctr = ctr_base + 8 * gi;
@@ -388,7 +405,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     if (prune) {
       a.lbr = ctx->lbr.as<uint32_t>() + gi * lb_per_group;
       a.lbm = ctx->lbm.as<uint32_t>() + gi * lb_per_group;
-      a.inc = ctx->inc.as<uint32_t>() + (size_t)gi * L.fpw;
+      a.inc = ctx->inc.as<uint64_t>() + (size_t)gi * L.fpw;
     }
     a.bmax = plan->d_bmax.as<int32_t>();
     a.pathological = plan->pathological ? 1 : 0;
@@ -400,6 +417,11 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
       if (plan->order_state == 2) a.order = plan->d_order.as<uint32_t>();
       else a.cost = plan->d_cost.as<uint32_t>();
     }
+#ifdef SCB_DIAG_COSTS  // diagnostics build: per-item walk cycles of every launch
+    plan->d_cost.ensure(plan->items.size() * sizeof(uint32_t));
+    a.cost = plan->d_cost.as<uint32_t>();
+    ctx->diag_step = step;
+#endif
     a.lanes = reinterpret_cast<LaneBest*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
     a.snaps = ctx->snaps.as<uint8_t>() + snap_bytes * gi;
     if (prune && step == 1 && mine > 1) {
@@ -409,14 +431,14 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
       // space over all warps.  Both phases keep each lane's items increasing.
       const uint32_t seed_items = std::min<uint32_t>(mine, plan->seed_items);
       a.k_begin = 0;
-      a.n_items = seed_items;
+      a.n_items = seed_items * G;
       search_launch(L.fpw, step, a, blocks, st);
-      uint32_t* frozen = ctx->seed_inc.as<uint32_t>() + (size_t)gi * L.fpw;
-      SCB_CUDA(cudaMemcpyAsync(frozen, a.inc, L.fpw * sizeof(uint32_t),
+      uint64_t* frozen = ctx->seed_inc.as<uint64_t>() + (size_t)gi * L.fpw;
+      SCB_CUDA(cudaMemcpyAsync(frozen, a.inc, L.fpw * sizeof(uint64_t),
                                cudaMemcpyDeviceToDevice, st));
       a.seed_inc = frozen;
-      a.k_begin = seed_items;
-      a.n_items = mine;
+      a.k_begin = seed_items * G;
+      a.n_items = mine * G;
       a.resume = 1;
       a.counter = reinterpret_cast<uint32_t*>(ctr + 3);
       search_launch(L.fpw, step, a, blocks, st);
@@ -712,6 +734,16 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   SCB_CUDA(cudaEventRecord(ev[9], s));
   SCB_CUDA(cudaStreamSynchronize(s));
   finish_schedule(plan);
+#ifdef SCB_DIAG_COSTS
+  if (const char* path = getenv("SCB_DIAG_COSTS_OUT")) {
+    std::vector<uint32_t> cost(plan->items.size());
+    SCB_CUDA(cudaMemcpy(cost.data(), plan->d_cost.p, cost.size() * 4, cudaMemcpyDeviceToHost));
+    if (FILE* fp = fopen(path, "wb")) {
+      fwrite(cost.data(), 4, cost.size(), fp);
+      fclose(fp);
+    }
+  }
+#endif
   // timings
   ctx->timings[0] = need_moments && luma ? 1000.0 * ev_ms(ev[4], ev[5]) : 0.0;
   ctx->timings[1] = 1000.0 * (ev_ms(ev[0], ev[1]) + (need_moments ? ev_ms(ev[5], ev[6]) : 0.f));

@@ -147,9 +147,10 @@ struct SearchArgs {
   unsigned long long* scored_out;  // candidate-frame scores actually evaluated
   const uint32_t* lbr;             // pruned mode: column lower bounds (search_walk.cuh)
   const uint32_t* lbm;
-  uint32_t* inc;                   // pruned mode: shared step-1 incumbent [FPW]
-  const uint32_t* seed_inc;        // pruned mode, phase B: incumbent frozen after phase A
+  uint64_t* inc;                   // pruned mode: shared step-1 incumbent [FPW] (t << 32 | item)
+  const uint64_t* seed_inc;        // pruned mode, phase B: incumbent frozen after phase A
   const uint32_t* order;           // exhaustive step 1: item k -> work item (or nullptr)
+  int split_g, split_depth;        // pruned mode: warps per work item (WalkEnv)
   uint32_t* cost;                  // per work item: walk cycles / 64 (or nullptr)
 };
 
@@ -190,5 +191,6 @@ struct sc_ctx {
   std::vector<scb::FrameBest> last_best[2];
   uint64_t last_leaves[2] = {0, 0};
   bool last_pruned = false;  // last search ran in SC_MODE_PRUNED (DP counts)
+  int diag_step = 0;         // diagnostics builds only
   ~sc_ctx();
 };

@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(Se
   e.patho = a.pathological;
   e.prune = a.prune;
   e.rstride = rstride;
+  e.split_g = (PRUNE && a.split_g > 1) ? a.split_g : 1;
+  e.split_depth = a.split_depth;
   e.mstar_off = 2 * A;
   e.ilo_off = ilo_off;
   e.rt = a.rt;
@@ -104,18 +106,20 @@ __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(Se
   st.budget = STEP == 2 ? a.budget[f] : -1;
   st.count = 0;
   st.scored = 0;
-  st.inc = kKeyInf;
+  st.inc = ~0ull;
   st.snap = a.snaps + ((size_t)gwarp * 32 + lane) * kSnapBytes;
   for (;;) {
     uint32_t k = 0;
     if (lane == 0) k = a.k_begin + atomicAdd(a.counter, 1u);
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= a.n_items) break;
+    // pruned mode: split_g consecutive counter values share one work item
+    const uint32_t kk = k / (uint32_t)e.split_g, part = k % (uint32_t)e.split_g;
     const uint64_t item =
-        a.order ? (uint64_t)a.order[k] : (uint64_t)a.item_offset + (uint64_t)k * a.item_stride;
+        a.order ? (uint64_t)a.order[kk] : (uint64_t)a.item_offset + (uint64_t)kk * a.item_stride;
     const WorkItem wi = a.items[item];
     const long long c0 = a.cost ? clock64() : 0;
-    walk_item<FPW, STEP, PRUNE>(e, item, wi, f, slot, st);
+    walk_item<FPW, STEP, PRUNE>(e, item, wi, f, slot, st, (int)part);
     __syncwarp();
     if (a.cost && lane == 0) a.cost[item] = (uint32_t)min((clock64() - c0) >> 6, 0xffffffffll);
   }

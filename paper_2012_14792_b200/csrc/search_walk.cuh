@@ -112,6 +112,10 @@ struct WalkEnv {
   const int32_t* ybase;   // [rows+1]: yh(y, 1), the first rectangle starting at row y
   const int32_t* rq;      // [rows+1]: rows / r (no integer division in the runs DFS)
   int mstar_off, ilo_off;  // GPU: offsets of mstar / ilo in dynamic shared memory
+  // pruned mode: split_g warps share each work item; the subtrees below
+  // level split_depth of the heights DFS (or a whole skeleton, if it has
+  // fewer levels) are dealt to them by a hash of their identity
+  int split_g, split_depth;
   const tkey* rt;         // [NR][FPW] time key of every rectangle
   const tkey* rts;        // [NR][FPW] split table: at rect(x0,w,y0,h) with y0+h < rows,
                           // max(time(y0,h), time(y0+h, rows-y0-h)) -- a run plus the
@@ -119,13 +123,14 @@ struct WalkEnv {
   const double* rs;       // [NR][FPW] SSE of every rectangle (step 2)
   // pruned mode only: per-frame lower bounds on a column's slowest slice,
   // lbr[(xw*rstride + r)*FPW + f] for exactly r runs and lbm[...] for any
-  // r' <= r (prefix minimum); inc[f] is the shared step-1 incumbent.
+  // r' <= r (prefix minimum); inc[f] is the shared step-1 incumbent, packed
+  // (time key << 32 | work item) so that ties are ordered by item.
   const tkey* lbr;
   const tkey* lbm;
-  tkey* inc;
+  uint64_t* inc;
   // incumbent frozen after the seed phase (or nullptr): its candidate precedes
-  // every item still to walk, so a tie with it can never win -> prune P >= it
-  const tkey* seed_inc;
+  // every item still to walk, so a tie with it can never win
+  const uint64_t* seed_inc;
 };
 
 // One lane's running first-in-order best and its candidate snapshot.
@@ -136,32 +141,37 @@ struct LaneState {
   int64_t budget;   // step 2: largest key whose time is <= t_min * (1 + lambda), -1: none
   uint64_t count;   // candidates enumerated (uniform over the warp)
   uint64_t scored;  // candidates this lane actually scored
-  tkey inc;         // last seen shared incumbent (pruned step 1)
+  uint64_t inc;     // last seen shared incumbent (pruned step 1), packed as EnvWalk::inc
   tkey bcmp;        // exhaustive step 1: a candidate wins iff t < bcmp (see walk_item)
+  bool tie;         // pruned, shared items: this item part may precede the best's layout
   uint8_t* snap;
 };
 
-// Shared incumbent: a candidate with time t exists for this frame, so no
-// candidate slower than t can win (equal ones still can: first in order).
-SCB_HD tkey incumbent_load(tkey* p) {
+// Shared incumbent (t << 32 | item): a candidate with time t exists in work
+// item `item` of this frame, so no slower candidate can win, and an equal one
+// only from an item not after it (positions inside one item are unknown).
+// A subtree of item X with lower bound P can still win iff (P << 32 | X) <= inc.
+SCB_HD uint64_t inc_pack(tkey t, uint64_t item) { return ((uint64_t)t << 32) | (uint32_t)item; }
+SCB_HD uint64_t incumbent_load(uint64_t* p) {
 #ifdef __CUDA_ARCH__
-  return *(volatile tkey*)p;
+  return *(volatile uint64_t*)p;
 #else
   return *p;
 #endif
 }
-SCB_HD void incumbent_offer(tkey* p, tkey t) {
+SCB_HD void incumbent_offer(uint64_t* p, uint64_t v) {
 #ifdef __CUDA_ARCH__
-  atomicMin((unsigned int*)p, (unsigned int)t);
+  atomicMin((unsigned long long*)p, (unsigned long long)v);
 #else
-  if (t < *p) *p = t;
+  if (v < *p) *p = v;
 #endif
 }
 
 // Lower bound on the slowest slice of a column (x0, w) cut into exactly r
 // runs, for every r <= rmax: min over all compositions (area constraint
 // relaxed) of the max run time, by a DP over rows.  lbr/lbm are written at
-// [r * stride] (lbm: prefix minimum over r).  Times are clamped f64 bits.
+// [r * stride] (lbm: prefix minimum over r).  Keys are ranks, so max / min
+// are exact.
 SCB_HD void column_bounds(const tkey* rt, int fpw, int f, int rows, int base, int rmax,
                           tkey* lbr, tkey* lbm, size_t stride) {
   tkey prev[256], cur[256];
@@ -225,9 +235,20 @@ SCB_HD void height_interval(const WalkEnv& e, Thr t, int w, int rl, int runs_lef
 
 // Walk work item `item` (prefix wi) for frame slot f and leaf slot `slot`
 // (J = 32 / FPW lanes share a frame and split the innermost height loop).
+// Owner (0..g-1) of a subtree of the pruned walk: a hash of the skeleton and
+// of the heights fixed above the split level.  It depends only on the
+// subtree's identity, never on what a warp pruned before reaching it, so every
+// subtree has exactly one owner among the warps sharing its work item.
+SCB_HD uint32_t split_owner(uint64_t key, int g) {
+  key ^= key >> 31;
+  key *= 0x9e3779b97f4a7c15ull;
+  key ^= key >> 29;
+  return (uint32_t)((key >> 32) % (uint64_t)g);
+}
+
 template <int FPW, int STEP, bool PRUNE>
 SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f, int slot,
-                      LaneState& st) {
+                      LaneState& st, int split_r = 0) {
   constexpr int J = 32 / FPW;
   const int rows = e.rows, cols = e.cols, nyh = e.nyh;
   const tkey* rt = e.rt;
@@ -240,6 +261,10 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   // so after the first update the comparison is strict again.
   if (STEP == 1 && !PRUNE)
     st.bcmp = (st.best_t != kKeyInf && item < st.best_item) ? st.best_t + 1 : st.best_t;
+  // Pruned mode with shared items: another part of this same item may have
+  // produced the lane's best, and this part's subtrees can precede it, so ties
+  // with the best are decided by the layouts (enumeration order).
+  if (PRUNE) st.tie = e.split_g > 1 && item == st.best_item;
 
   // warp-uniform DFS state (identical in every lane of the warp)
   int W[SC_MAX_COLS], R[SC_MAX_COLS], X0[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
@@ -312,11 +337,33 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     return tot;
   };
   // can a subtree whose fixed slices already reach time P still win?
-  const tkey seed_inc = (STEP == 1 && PRUNE && e.seed_inc) ? e.seed_inc[f] : kKeyInf;
+  const uint64_t seed_inc = (STEP == 1 && PRUNE && e.seed_inc) ? e.seed_inc[f] : ~0ull;
+  const uint64_t item32 = (uint32_t)item;
   auto viable = [&](tkey P) -> bool {
     return !PRUNE ||
-           (STEP == 1 ? (P < st.best_t && P <= st.inc && P < seed_inc)
+           (STEP == 1 ? ((P < st.best_t || (st.tie && P == st.best_t)) &&
+                         (((uint64_t)P << 32) | item32) <= st.inc &&
+                         (((uint64_t)P << 32) | item32) < seed_inc)
                       : ((int64_t)P <= st.budget));
+  };
+  // does the current candidate precede the lane's best in enumeration order?
+  // (same item: compare the layouts lexicographically, as k_finalize does)
+  auto precedes_best = [&](int lr, int lh, int lrest) -> bool {
+    for (int i = 0; i < SC_MAX_COLS; ++i) {
+      const int v = i < c ? W[i] : 0;
+      if (v != st.snap[i]) return v < st.snap[i];
+    }
+    for (int i = 0; i < SC_MAX_COLS; ++i) {
+      const int v = i < c ? R[i] : 0;
+      if (v != st.snap[SC_MAX_COLS + i]) return v < st.snap[SC_MAX_COLS + i];
+    }
+    for (int i = 0; i < e.n; ++i) {
+      int v = curH[i];
+      if (i == lr) v = lh;
+      if (i == lr + 1 && lr >= 0) v = lrest;
+      if (v != st.snap[2 * SC_MAX_COLS + i]) return v < st.snap[2 * SC_MAX_COLS + i];
+    }
+    return false;
   };
   if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
   // lower bound of column (x0, w) with r runs (exact r) / any r' <= r
@@ -330,22 +377,29 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   auto score = [&](tkey t, uint64_t o, int lr, int lh, int lrest) {
     if (PRUNE) ++st.scored;
     if (STEP == 1) {
-      if (t < (PRUNE ? st.best_t : st.bcmp)) {
+      if (t < (PRUNE ? st.best_t : st.bcmp) ||
+          (PRUNE && st.tie && t == st.best_t && precedes_best(lr, lh, lrest))) {
         st.best_t = t;
         st.bcmp = t;
         st.best_item = item;
         st.best_ord = o;
         take_snapshot(lr, lh, lrest);
-        if (PRUNE) incumbent_offer(e.inc + f, t);
+        if (PRUNE) {
+          st.tie = false;  // the rest of this part comes after it
+          incumbent_offer(e.inc + f, inc_pack(t, item));
+        }
       }
     } else if ((int64_t)t <= st.budget) {
       const double s = layout_sse(lr, lh, lrest);
-      if (s < st.best_sse || (s == st.best_sse && t < st.best_t)) {
+      if (s < st.best_sse ||
+          (s == st.best_sse && (t < st.best_t || (PRUNE && st.tie && t == st.best_t &&
+                                                  precedes_best(lr, lh, lrest))))) {
         st.best_sse = s;
         st.best_t = t;
         st.best_item = item;
         st.best_ord = o;
         take_snapshot(lr, lh, lrest);
+        if (PRUNE) st.tie = false;
       }
     }
   };
@@ -488,12 +542,27 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
       tkey P = 0;
       for (int i = 0; i < c; ++i)
         if (R[i] == 1) P = kmax(P, rt_at(X0[i], W[i], 0, rows));
+      // pruned mode, shared items: identity of this skeleton
+      const bool split = PRUNE && e.split_g > 1;
+      uint64_t skey = 0;
+      int lsplit = -1;  // heights level whose values are dealt to the warps
+      if (split) {
+        skey = (uint64_t)c;
+        for (int i = 0; i < c; ++i) skey = skey * 0x100000001b3ull ^ (uint64_t)(W[i] | (R[i] << 8));
+        if (nl >= 2) lsplit = imin(e.split_depth, nl - 2);
+        else if (split_owner(skey, e.split_g) != (uint32_t)split_r) {
+          ord += 1;
+          continue;
+        }
+      }
       if (nl == 0) {  // the skeleton is a single candidate
         if (slot == 0 && viable(P)) score(P, ord, -1, 0, 0);
         ord += 1;
         continue;
       }
-      if (!viable(P)) continue;
+      // pruned mode: every column's bound (PR) floors the whole subtree
+      const tkey colfloor = PRUNE ? kmax(P, PR[c]) : P;
+      if (!viable(colfloor)) continue;
       // ---- heights DFS over the multi-run columns (search.cpp:163-190)
       int l = 0;
       const bool leaf_now = (nl == 1);
@@ -538,6 +607,11 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             continue;
           }
           Lh[l] = (uint8_t)h;
+          if (split && l == lsplit) {  // deal this subtree to one warp of the item
+            uint64_t k = skey;
+            for (int q = 0; q <= l; ++q) k = k * 0x100000001b3ull ^ (uint64_t)(Lh[q] + 1);
+            if (split_owner(k, e.split_g) != (uint32_t)split_r) continue;
+          }
           const int a1 = w * h;
           int na = imin(Amin[l], a1), nx = imax(Amax[l], a1);
           const int ridx = RS0[i] + j;
@@ -554,7 +628,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           } else {
             Pn = kmax(Pin[l], rt[ri]);
           }
-          if (!viable(Pn)) continue;
+          if (!viable(PRUNE ? kmax(Pn, colfloor) : Pn)) continue;
           const int nxt = l + 1;
           const bool new_col = Lrun[nxt] == 0;
           const int y0n = new_col ? 0 : y0 + h;
@@ -594,7 +668,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
 #if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
           ++g_stats.leafr[R[i]];
 #endif
-          if (lo + slot <= hi && viable(Pl)) {
+          if (lo + slot <= hi && viable(PRUNE ? kmax(Pl, colfloor) : Pl)) {
             // the split table holds max(run h, forced rest) at the run's own
             // rectangle index, which advances by +1 per h; lanes step h by J.
             int h = lo + slot;

@@ -19,11 +19,11 @@ class Emu:
         self.L = C.CDLL(SO)
         I, D, P = C.c_int, C.c_double, C.c_void_p
         self.L.emu_search.argtypes = [I, I, I, D, I, I, I, I, I, P, P, P, I, C.c_size_t, I, I, P, P, P, P,
-                                      P, P, P, I]
+                                      P, P, P, I, I, I]
 
     def search(self, cols, rows, n, k, max_cols, coverage, step, rect_time, rect_sse=None,
                budget=None, warps=3, item_target=16, offset=0, stride=1, full=False, prune=0,
-               order=0):
+               order=0, split=1, split_depth=1):
         rt = np.ascontiguousarray(rect_time, dtype=np.float64)
         F = rt.shape[0]
         rs = None if rect_sse is None else np.ascontiguousarray(rect_sse, dtype=np.float64)
@@ -38,7 +38,8 @@ class Emu:
         st = self.L.emu_search(cols, rows, n, k, max_cols, coverage, step, prune, F, _p(rt), _p(rs),
                                _p(b),
                                warps, item_target, offset, stride, _p(t), _p(sse), _p(cnt),
-                               _p(snap), _p(found), _p(item), _p(ordn), order)
+                               _p(snap), _p(found), _p(item), _p(ordn), order, split,
+                               split_depth)
         assert st == 0
         if full:
             return t, sse, cnt, snap, found, item, ordn

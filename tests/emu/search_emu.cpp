@@ -21,7 +21,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
                           int warps, size_t item_target, int item_offset, int item_stride,
                           double* out_t, double* out_sse, uint64_t* out_count,
                           uint8_t* out_snap /*[F][96]*/, int* out_found, uint64_t* out_item,
-                          uint64_t* out_ord, int order_mode) {
+                          uint64_t* out_ord, int order_mode, int split_g, int split_depth) {
   // order_mode (exhaustive step 1 only, like api.cu's cost schedule): 0 the
   // enumeration order, 1 reversed, 2 a fixed pseudo-random permutation
   if (frames < 1 || frames > 32) return 1;
@@ -72,7 +72,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   // pruned mode: per-frame column lower bounds, shared incumbents
   const int nxw = cols * (cols + 1) / 2;
   std::vector<tkey> lbr((size_t)nxw * rstride * fpw, 0), lbm((size_t)nxw * rstride * fpw, 0);
-  std::vector<tkey> inc(fpw, kKeyInf);
+  std::vector<uint64_t> inc(fpw, ~0ull);
   if (prune)
     for (int xw = 0; xw < nxw; ++xw)
       for (int f = 0; f < frames; ++f) {
@@ -114,7 +114,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.lbm = lbm.data();
   e.inc = inc.data();
   e.seed_inc = nullptr;
-  std::vector<tkey> frozen(fpw, kKeyInf);
+  std::vector<uint64_t> frozen(fpw, ~0ull);
   // seeded pruned step 1 like api.cu: phase A = the first seed_items items
   size_t seed_items = 0;
   for (const WorkItem& wi : items) {
@@ -133,7 +133,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       s.best_sse = INFINITY;
       s.count = 0;
       s.scored = 0;
-      s.inc = kKeyInf;
+      s.inc = ~0ull;
       s.snap = &snaps[((size_t)wp * 32 + l) * kSnap];
       s.budget = -1;
       if (step == 2 && (l % fpw) < frames) {  // largest key whose time is <= budget
@@ -162,9 +162,14 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       std::swap(seq[i - 1], seq[(size_t)((z >> 33) % i)]);
     }
   }
-  for (size_t si = 0; si < seq.size(); ++si, ++kk) {
-    const size_t it = seq[si];
-    if (prune && step == 1 && kk == seed_local && seed_local > 0) {  // phase B begins
+  // pruned mode: split_g units per item (api.cu / k_search), dealt round-robin
+  const int G = prune ? (split_g > 1 ? split_g : 1) : 1;
+  e.split_g = G;
+  e.split_depth = split_depth;
+  for (size_t su = 0; su < seq.size() * (size_t)G; ++su, ++kk) {
+    const size_t it = seq[su / (size_t)G];
+    const int part = (int)(su % (size_t)G);
+    if (prune && step == 1 && kk == seed_local * (size_t)G && seed_local > 0) {  // phase B
       frozen = inc;
       e.seed_inc = frozen.data();
     }
@@ -174,11 +179,11 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       switch (fpw * 10 + step) {
 #define CASE(F)                                                                   \
   case F * 10 + 1:                                                                \
-    if (prune) walk_item<F, 1, true>(e, it, items[it], l % F, l / F, s);          \
+    if (prune) walk_item<F, 1, true>(e, it, items[it], l % F, l / F, s, part);    \
     else walk_item<F, 1, false>(e, it, items[it], l % F, l / F, s);               \
     break;                                                                        \
   case F * 10 + 2:                                                                \
-    if (prune) walk_item<F, 2, true>(e, it, items[it], l % F, l / F, s);          \
+    if (prune) walk_item<F, 2, true>(e, it, items[it], l % F, l / F, s, part);    \
     else walk_item<F, 2, false>(e, it, items[it], l % F, l / F, s);               \
     break;
         CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)

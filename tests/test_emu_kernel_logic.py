@@ -71,6 +71,50 @@ def test_step1_any_item_order(emu, oracle, seed, order):
             assert Emu.slices(snap[f], n, rows) == r.argmin1.slices(rows), ctx
 
 
+@pytest.mark.parametrize("split,depth", [(3, 0), (8, 1), (5, 2)])
+def test_pruned_split_items_vs_oracle(emu, oracle, split, depth):
+    """Pruned mode with `split` warps per work item: the heights subtrees below
+    level `depth` (or whole small skeletons) are dealt out by a hash of their
+    identity; both steps still equal the oracle."""
+    from emu.emu import Emu
+    rng = np.random.default_rng(700 + split)
+    for trial in range(40):
+        cols, rows, n = _case(rng, 10)
+        mc = int(rng.integers(0, 5))
+        cov = int(rng.integers(0, 2))
+        lam = float(rng.choice([0.0, 0.2]))
+        F = int(rng.choice([1, 2, 4, 8]))
+        W, H = cols * 64, rows * 64
+        est = rng.lognormal(0, 0.6, size=(F, cols * rows))
+        if trial % 3 == 0:
+            est = np.round(est)
+        luma = rng.integers(0, 1024, size=(F, H, W)).astype(np.uint16)
+        recs = [oracle.ctu_stats(luma[f], 64) for f in range(F)]
+        rt = np.stack([oracle.rect_times(est[f], cols, rows) for f in range(F)])
+        rs = np.stack([oracle.rect_sse(W, H, 64, recs[f]) for f in range(F)])
+        res = [oracle.search(W, H, 64, est[f], recs[f], n, lam, 3.0, mc, cov, 3) for f in range(F)]
+        kw = dict(item_target=int(rng.choice([1, 16])), warps=int(rng.integers(1, 5)), prune=1,
+                  split=split, split_depth=depth)
+        t, _, _, snap, found = emu.search(cols, rows, n, 3.0, mc, cov, 1, rt, **kw)
+        for f in range(F):
+            st, r = res[f]
+            ctx = (split, depth, trial, f, cols, rows, n, mc, cov, F)
+            if st:
+                assert not found[f], ctx
+                continue
+            assert t[f] == r.t_min_us, ctx
+            assert Emu.slices(snap[f], n, rows) == r.argmin1.slices(rows), ctx
+        if any(st for st, _ in res):
+            continue
+        budget = np.array([r.t_min_us * (1.0 + lam) for _, r in res])
+        t2, sse, _, snap2, _ = emu.search(cols, rows, n, 3.0, mc, cov, 2, rt, rs, budget, **kw)
+        for f in range(F):
+            r = res[f][1]
+            ctx = (split, depth, trial, f, cols, rows, n, mc, cov, lam, F)
+            assert t2[f] == r.t_best_us and sse[f] == r.sse_best, ctx
+            assert Emu.slices(snap2[f], n, rows) == r.best.slices(rows), ctx
+
+
 @pytest.mark.parametrize("prune", [0, 1])
 @pytest.mark.parametrize("seed", range(3))
 def test_step2_vs_oracle(emu, oracle, seed, prune):
