@@ -302,12 +302,19 @@ bool step2_bounded(const sc_search_cfg& cfg) {
 
 // Cost-ordered schedule of the exhaustive step-1 walk (Plan::order_state);
 // SLICECRAFT_B200_SCHEDULE=0 keeps the enumeration order.
-// Pruned mode: warps sharing one work item (SLICECRAFT_B200_SPLIT, default
-// 8) and the heights level whose subtrees they deal out
-// (SLICECRAFT_B200_SPLIT_DEPTH, default 1).
-int split_ways() {
-  const char* v = getenv("SLICECRAFT_B200_SPLIT");
-  const int g = v ? atoi(v) : 8;
+// Pruned mode: warps sharing one work item and the heights level whose
+// subtrees they deal out.  Sharing costs every warp of an item the walk down
+// to the split level, so it only pays where a few pruned items dominate the
+// launch: measured on B200 (profiles/r01_split_sweep.md) 1 way is best for
+// n <= 8 and for the bounded step 2 of the exhaustive mode, 2 for n = 16,
+// 16 for n = 32.  SLICECRAFT_B200_SPLIT / SLICECRAFT_B200_SPLIT2 (step 2)
+// override; SLICECRAFT_B200_SPLIT_DEPTH sets the level (default 1).
+int split_ways(int step, int n, bool pruned_mode) {
+  const char* v = getenv(step == 1 ? "SLICECRAFT_B200_SPLIT" : "SLICECRAFT_B200_SPLIT2");
+  int g;
+  if (v) g = atoi(v);
+  else if (!pruned_mode) g = 1;  // exhaustive mode's budget-bounded step 2
+  else g = n <= 8 ? 1 : (n <= 16 ? 2 : 16);
   return g < 1 ? 1 : (g > 64 ? 64 : g);
 }
 int split_depth() {
@@ -391,7 +398,8 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     a.max_area = g.cols * g.rows;
     a.coverage = cfg.coverage;
     a.items = plan->d_items.as<WorkItem>();
-    const uint32_t G = prune ? (uint32_t)split_ways() : 1u;
+    const uint32_t G =
+        prune ? (uint32_t)split_ways(step, cfg.n_slices, cfg.mode == SC_MODE_PRUNED) : 1u;
     a.split_g = (int)G;
     a.split_depth = split_depth();
     a.n_items = mine * G;

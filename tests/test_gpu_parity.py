@@ -75,14 +75,19 @@ def test_rect_tables_bit_exact(part, oracle, grid):
 
 # ---- K4/K5 search -----------------------------------------------------------------
 # search modes under test: exhaustive (step 2 bounded by its budget), the
-# same with an unbounded step-2 walk, and the exact pruned mode
-MODES = ["exhaustive", "exhaustive-full", "pruned"]
+# same with an unbounded step-2 walk, the exact pruned mode, and the pruned
+# mode with every work item shared by several warps (forced on small grids,
+# where the default keeps one warp per item)
+MODES = ["exhaustive", "exhaustive-full", "pruned", "pruned-split"]
 
 
 def _mode(monkeypatch, m):
     if m == "exhaustive-full":
         monkeypatch.setenv("SLICECRAFT_B200_STEP2_BOUND", "0")
-    return 1 if m == "pruned" else 0
+    if m == "pruned-split":
+        monkeypatch.setenv("SLICECRAFT_B200_SPLIT", "5")
+        monkeypatch.setenv("SLICECRAFT_B200_SPLIT2", "3")
+    return 1 if m.startswith("pruned") else 0
 
 
 def _rec3(rec):
