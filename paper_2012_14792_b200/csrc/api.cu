@@ -31,7 +31,10 @@ void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16
                         double* d_rect_s, uint64_t* d_rt, double* d_rs, int sm_count,
                         cudaStream_t st);
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st);
-int search_blocks_per_sm(int fpw, int step);
+int search_blocks_per_sm(int fpw, int step, bool prune);
+void item_filter_launch(sc_ctx* ctx, const SearchArgs& a, uint32_t k0, uint32_t k1, int fpw,
+                        int frames, int step, const uint64_t* seed_inc, uint32_t* list,
+                        uint32_t* count, cudaStream_t st);
 int search_block_threads();
 void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int cols, int rows,
                           int rmax, int rstride, uint32_t* lbr, uint32_t* lbm, cudaStream_t st);
@@ -302,25 +305,34 @@ bool step2_bounded(const sc_search_cfg& cfg) {
 
 // Cost-ordered schedule of the exhaustive step-1 walk (Plan::order_state);
 // SLICECRAFT_B200_SCHEDULE=0 keeps the enumeration order.
-// Pruned mode: warps sharing one work item and the heights level whose
+// exhaustive mode's budget-bounded step 2 (SLICECRAFT_B200_SPLIT2 overrides)
+constexpr int kBoundedStep2Split = 16;
+
+// Pruned walks: warps sharing one work item and the heights level whose
 // subtrees they deal out.  Sharing costs every warp of an item the walk down
-// to the split level, so it only pays where a few pruned items dominate the
-// launch: measured on B200 (profiles/r01_split_sweep.md) 1 way is best for
-// n <= 8 and for the bounded step 2 of the exhaustive mode, 2 for n = 16,
-// 16 for n = 32.  SLICECRAFT_B200_SPLIT / SLICECRAFT_B200_SPLIT2 (step 2)
-// override; SLICECRAFT_B200_SPLIT_DEPTH sets the level (default 1).
+// to the split level; since the item prefilter (k_item_filter) drops the
+// items that die at their prefix, only surviving items pay it, and the
+// survivors are few and heavy.  Measured on B200 (profiles/r01_split_sweep.md)
+// 16 ways is best or even on configs 3-5 in both steps.
+// SLICECRAFT_B200_SPLIT / SLICECRAFT_B200_SPLIT2 (step 2) override;
+// SLICECRAFT_B200_SPLIT_DEPTH sets the level (default 1).
 int split_ways(int step, int n, bool pruned_mode) {
+  (void)n;
   const char* v = getenv(step == 1 ? "SLICECRAFT_B200_SPLIT" : "SLICECRAFT_B200_SPLIT2");
-  int g;
-  if (v) g = atoi(v);
-  else if (!pruned_mode) g = 1;  // exhaustive mode's budget-bounded step 2
-  else g = n <= 8 ? 1 : (n <= 16 ? 2 : 16);
+  int g = v ? atoi(v) : (pruned_mode ? 16 : kBoundedStep2Split);
   return g < 1 ? 1 : (g > 64 ? 64 : g);
 }
 int split_depth() {
   const char* v = getenv("SLICECRAFT_B200_SPLIT_DEPTH");
   const int d = v ? atoi(v) : 1;
   return d < 0 ? 0 : (d > 8 ? 8 : d);
+}
+
+// Pruned walks: drop the items whose prefix fails every frame before the
+// launch (SLICECRAFT_B200_FILTER=0 keeps every item).
+bool item_filter_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_FILTER");
+  return !(v && v[0] == '0');
 }
 
 bool schedule_enabled() {
@@ -347,7 +359,8 @@ void finish_schedule(Plan* p) {
 // after step 1, the device budgets of step 2.  No host synchronisation.
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
                   const Layouts& L, int step, bool compute_bounds, cudaStream_t st) {
-  const int bps = search_blocks_per_sm(L.fpw, step);
+  const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
+  const int bps = search_blocks_per_sm(L.fpw, step, prune);
   const int blocks = ctx->sm_count * bps;
   const uint32_t warps = (uint32_t)blocks * (search_block_threads() / 32);
   const size_t lane_bytes = (size_t)warps * 32 * sizeof(LaneBest);
@@ -366,7 +379,6 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
   const uint32_t rank = (uint32_t)ctx->shard_rank, world = (uint32_t)ctx->shard_world;
   const uint32_t mine = total > rank ? (total - rank + world - 1) / world : 0;
   FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)(step - 1) * L.groups * L.fpw;
-  const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
   const bool sched = step == 1 && !prune && world == 1 && schedule_enabled();
   if (sched && plan->order_state != 2) {
     plan->d_cost.ensure(plan->items.size() * sizeof(uint32_t));
@@ -432,6 +444,18 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
 #endif
     a.lanes = reinterpret_cast<LaneBest*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
     a.snaps = ctx->snaps.as<uint8_t>() + snap_bytes * gi;
+    const int fig = std::min(L.fpw, L.frames - gi * L.fpw);
+    // pruned walks: the items whose width prefix already fails every frame
+    // are dropped before the launch (k_item_filter); the survivors, in
+    // order, are the launch's item list
+    uint32_t* flt_list = nullptr;
+    uint32_t* flt_count = nullptr;
+    if (prune && item_filter_enabled()) {
+      ctx->flt_list.ensure((size_t)(mine + 1) * sizeof(uint32_t) * L.groups);
+      ctx->flt_count.ensure(sizeof(uint32_t) * 2 * L.groups);
+      flt_list = ctx->flt_list.as<uint32_t>() + (size_t)gi * (mine + 1);
+      flt_count = ctx->flt_count.as<uint32_t>() + 2 * gi;
+    }
     if (prune && step == 1 && mine > 1) {
       // Seeded branch-and-bound: phase A walks the first items (the smallest
       // column counts, which hold the fast candidates of the family) so every
@@ -449,11 +473,22 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
       a.n_items = mine * G;
       a.resume = 1;
       a.counter = reinterpret_cast<uint32_t*>(ctr + 3);
+      if (flt_list) {
+        item_filter_launch(ctx, a, seed_items, mine, L.fpw, fig, 1, frozen, flt_list, flt_count,
+                           st);
+        a.order = flt_list;
+        a.n_items_dev = flt_count;
+        a.k_begin = 0;
+      }
       search_launch(L.fpw, step, a, blocks, st);
     } else {
+      if (flt_list && step == 2) {
+        item_filter_launch(ctx, a, 0, mine, L.fpw, fig, 2, nullptr, flt_list, flt_count, st);
+        a.order = flt_list;
+        a.n_items_dev = flt_count;
+      }
       search_launch(L.fpw, step, a, blocks, st);
     }
-    const int fig = std::min(L.fpw, L.frames - gi * L.fpw);
     finalize_launch(step, cfg.n_slices, L.fpw, fig, warps, a.lanes, a.snaps, a.count_out,
                     a.scored_out, cfg.lambda,
                     ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr,

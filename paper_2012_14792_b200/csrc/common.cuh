@@ -152,6 +152,8 @@ struct SearchArgs {
   const uint32_t* order;           // exhaustive step 1: item k -> work item (or nullptr)
   int split_g, split_depth;        // pruned mode: warps per work item (WalkEnv)
   uint32_t* cost;                  // per work item: walk cycles / 64 (or nullptr)
+  const uint32_t* n_items_dev;     // pruned mode: surviving items in `order` (device count;
+                                   // n_items = count * split_g, k from 0), or nullptr
 };
 
 // Device-side per-frame result written by finalize.
@@ -184,6 +186,7 @@ struct sc_ctx {
   scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec, lbr, lbm, inc, seed_inc;
   scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
   scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp;       // rank.cu scratch
+  scb::DevBuf flt_idx, flt_flag, flt_list, flt_count, flt_temp;      // item filter (search.cu)
   int dec_cols = -1, dec_rows = -1;
   scb::HostBuf h_stage, h_records, h_frame_best, h_budget, h_luma;  // h_luma: YUV reads
   std::vector<scb::Plan*> plans;

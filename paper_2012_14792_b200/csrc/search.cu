@@ -26,6 +26,8 @@
 //    (monotone), SSE sums are accumulated in slice order with __dadd_rn.
 #include <algorithm>
 
+#include <cub/device/device_select.cuh>
+
 #include "common.cuh"
 #include "search_walk.cuh"
 
@@ -34,13 +36,19 @@ namespace scb {
 #ifndef SCB_SEARCH_MINB
 #define SCB_SEARCH_MINB 2
 #endif
+// exhaustive step 1: 2 CTAs/SM (88 registers; capping at 80 for 3 CTAs
+// measured 8 % slower)
+#ifndef SCB_SEARCH_MINB1
+#define SCB_SEARCH_MINB1 2
+#endif
 #ifndef SCB_SEARCH_BLOCK
 #define SCB_SEARCH_BLOCK 256
 #endif
 int search_block_threads() { return SCB_SEARCH_BLOCK; }
 
 template <int FPW, int STEP, bool PRUNE>
-__global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(SearchArgs a) {
+__global__ void __launch_bounds__(SCB_SEARCH_BLOCK, (STEP == 1 && !PRUNE) ? SCB_SEARCH_MINB1 : SCB_SEARCH_MINB)
+k_search(SearchArgs a) {
   // shared-memory tables (search_walk.cuh): g_dyn = bmax|aneed interleaved
   // [2A], mstar [(cols+1)(rows+1)], ilo [(cols+1) * rstride]; static magic,
   // ybase, rq
@@ -108,11 +116,12 @@ __global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(Se
   st.scored = 0;
   st.inc = ~0ull;
   st.snap = a.snaps + ((size_t)gwarp * 32 + lane) * kSnapBytes;
+  const uint32_t n_items = a.n_items_dev ? *a.n_items_dev * (uint32_t)e.split_g : a.n_items;
   for (;;) {
     uint32_t k = 0;
     if (lane == 0) k = a.k_begin + atomicAdd(a.counter, 1u);
     k = __shfl_sync(0xffffffffu, k, 0);
-    if (k >= a.n_items) break;
+    if (k >= n_items) break;
     // pruned mode: split_g consecutive counter values share one work item
     const uint32_t kk = k / (uint32_t)e.split_g, part = k % (uint32_t)e.split_g;
     const uint64_t item =
@@ -267,18 +276,25 @@ static void launch_fpw(const SearchArgs& a, int blocks, size_t smem, cudaStream_
   else k_search<FPW, STEP, false><<<blocks, SCB_SEARCH_BLOCK, smem, st>>>(a);
 }
 
-int search_blocks_per_sm(int fpw, int step) {
+int search_blocks_per_sm(int fpw, int step, bool prune) {
   int nb = 0;
   const size_t smem = 16 * 1024;
+#define OCC1(F, S, P)                                                                        \
+  SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, S, P>,           \
+                                                         SCB_SEARCH_BLOCK, smem))
 #define OCC(F)                                                                               \
   if (fpw == F) {                                                                            \
-    if (step == 1)                                                                           \
-      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 1, false>, SCB_SEARCH_BLOCK, smem)); \
-    else                                                                                     \
-      SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, 2, false>, SCB_SEARCH_BLOCK, smem)); \
+    if (step == 1) {                                                                         \
+      if (prune) OCC1(F, 1, true);                                                           \
+      else OCC1(F, 1, false);                                                                \
+    } else {                                                                                 \
+      if (prune) OCC1(F, 2, true);                                                           \
+      else OCC1(F, 2, false);                                                                \
+    }                                                                                        \
   }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
 #undef OCC
+#undef OCC1
   return nb < 1 ? 1 : nb;
 }
 
@@ -303,6 +319,78 @@ void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStrea
     default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
   }
   SCB_CUDA(cudaGetLastError());
+}
+
+// ---- pruned mode: work-item prefilter ---------------------------------------
+// The walk's first test (walk_item, search_walk.cuh) is on the item's fixed
+// width prefix alone: the window hulls must intersect and, for some frame of
+// the group, the prefix's column bounds must pass the incumbent (step 1:
+// (P << 32 | item) <= inc and < the frozen seed incumbent) or the budget
+// (step 2: P <= budget).  An item that fails for every frame is skipped by
+// every lane with no candidate scored, so dropping it before the launch
+// changes nothing but the launch's per-item overhead.  The survivors keep
+// their order (DeviceSelect is stable), so each warp's items still increase.
+__global__ void k_item_filter(const WorkItem* __restrict__ items, uint32_t k0, uint32_t k1,
+                              uint32_t offset, uint32_t stride, int cols, int rows, int n,
+                              int max_area, int rstride, const int32_t* __restrict__ tab,
+                              const uint32_t* __restrict__ lbm, int fpw, int frames, int step,
+                              const uint64_t* inc, const uint64_t* seed_inc,
+                              const int64_t* budget, uint32_t* idx, uint8_t* flag) {
+  const uint32_t k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= k1) return;
+  const uint32_t item = offset + k * stride;
+  const WorkItem wi = items[item];
+  const int c = wi.c, d = wi.d;
+  const int A = max_area + 1;
+  const int rmax_c = min(n - c + 1, rows);
+  bool ok = (n >= c) && (n <= c * rows);
+  int x0 = 0, wl = 1, wh = max_area;
+  const uint32_t* lb[SC_MAX_COLS];
+  for (int i = 0; i < d && ok; ++i) {
+    const int w = wi.w[i];
+    wl = max(wl, tab[A + w * ((rows + rmax_c - 1) / rmax_c)]);  // ilo(w, rmax_c)
+    wh = min(wh, w * rows);
+    ok = wl <= wh;
+    lb[i] = lbm + ((size_t)xw_of(cols, x0, w) * rstride + rmax_c) * fpw;
+    x0 += w;
+  }
+  bool any = false;
+  for (int f = 0; f < frames && ok && !any; ++f) {
+    uint32_t P = 0;
+    for (int i = 0; i < d; ++i) P = max(P, lb[i][f]);
+    if (step == 1) {
+      const uint64_t key = ((uint64_t)P << 32) | (uint32_t)item;
+      any = key <= inc[f] && key < seed_inc[f];
+    } else {
+      any = (int64_t)P <= budget[f];
+    }
+  }
+  idx[k - k0] = item;
+  flag[k - k0] = any ? 1 : 0;
+}
+
+// Survivors of units [k0, k1) of this shard into `list` (in order) and their
+// number into *count, all on the stream.
+void item_filter_launch(sc_ctx* ctx, const SearchArgs& a, uint32_t k0, uint32_t k1, int fpw,
+                        int frames, int step, const uint64_t* seed_inc, uint32_t* list,
+                        uint32_t* count, cudaStream_t st) {
+  const uint32_t m = k1 > k0 ? k1 - k0 : 0;
+  ctx->flt_idx.ensure((size_t)(m + 1) * sizeof(uint32_t));
+  ctx->flt_flag.ensure((size_t)(m + 1));
+  const int rstride = std::min(a.n, a.rows) + 1;
+  if (m) {
+    k_item_filter<<<(m + 255) / 256, 256, 0, st>>>(
+        a.items, k0, k1, a.item_offset, a.item_stride, a.cols, a.rows, a.n, a.max_area, rstride,
+        a.bmax, a.lbm, fpw, frames, step, a.inc, seed_inc, a.budget, ctx->flt_idx.as<uint32_t>(),
+        ctx->flt_flag.as<uint8_t>());
+    SCB_CUDA(cudaGetLastError());
+  }
+  size_t tb = 0;
+  SCB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ctx->flt_idx.as<uint32_t>(),
+                                      ctx->flt_flag.as<uint8_t>(), list, count, (int)m, st));
+  ctx->flt_temp.ensure(tb + 16);
+  SCB_CUDA(cub::DeviceSelect::Flagged(ctx->flt_temp.p, tb, ctx->flt_idx.as<uint32_t>(),
+                                      ctx->flt_flag.as<uint8_t>(), list, count, (int)m, st));
 }
 
 void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,

@@ -276,12 +276,16 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   if (PRUNE) st.tie = e.split_g > 1 && item == st.best_item;
 
   // warp-uniform DFS state (identical in every lane of the warp)
-  int W[SC_MAX_COLS], R[SC_MAX_COLS], X0[SC_MAX_COLS + 1];
+  int W[SC_MAX_COLS], R[SC_MAX_COLS], X0[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
   uint8_t curH[SC_MAX_SLICES];
+  // pruned walks: heights-DFS state per level in local arrays
+  uint8_t Lcol[kMaxLevels], Lrun[kMaxLevels], Ly0[kMaxLevels], Lh[kMaxLevels], Lhi[kMaxLevels];
+  int32_t Amin[kMaxLevels], Amax[kMaxLevels], Lbase[kMaxLevels];
+  tkey Pin[kMaxLevels];
   // heights-DFS levels: LS static (w | runs left << 8 | run << 16 | column << 24,
   // column rectangle base, suffix fillability bounds), D the spilled state of
   // the levels above the current one (h | hhi << 8 | y0 << 16, Pin, Amin, Amax)
-  Lvl LS[kMaxLevels], D[kMaxLevels];
+  Lvl LS[kMaxLevels], D[kMaxLevels];  // exhaustive walks
 
   auto thresholds = [&](int amin, int amax, int win_lo, int win_hi) -> Thr {
     Thr t;
@@ -293,6 +297,19 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   };
   auto rt_at = [&](int x0, int w, int y0, int h) -> tkey {
     return rt[(size_t)(xw_of(cols, x0, w) * nyh + yh_of(rows, y0, h)) * FPW + f];
+  };
+  // Every multi-run column from `from` on can still be filled with runs of
+  // admissible height (necessary condition; prunes dead subtrees early).
+  auto columns_feasible = [&](int from, Thr t) -> bool {
+    for (int i = from; i < c; ++i) {
+      if (R[i] < 2) continue;
+      const int w = W[i];
+      const uint64_t mg = SCB_MAGIC(w);
+      const int hmin_a = imax(1, div_w(t.t2 + w - 1, mg));
+      const int hmax_a = t.t1 < 0 ? 0 : div_w(t.t1, mg);
+      if (R[i] * hmin_a > rows || R[i] * hmax_a < rows) return false;
+    }
+    return true;
   };
   // snapshot of the current candidate; run `lr` takes height lh and the
   // forced run lr+1 the rest of its column (lr < 0: no leaf loop).
@@ -512,242 +529,409 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         R[rp] = imax(1, SL[rp] - (c - 1 - rp) * rows) - 1;
         continue;
       }
-      // ---- one live skeleton (c, widths, runs); every area lies in
-      //      [win_lo, bmax[nH]] for a window a in [nL, nH]
-      const int win_lo = nL, win_hi = SCB_BMAX(nH);
-      SCB_STAT(skeletons);
-      if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
-      // Levels of the heights DFS: every run of a multi-run column but its
-      // last (forced) one, column by column.  Static per-level facts go to
-      // LS[] once per skeleton; the DFS keeps its current level in registers
-      // and spills a level's state to D[] only when it descends.
-      int amin = kBigArea, amax = 0;
-      int nl = 0;
-      tkey P = 0;
-      {
-        int run = 0;
-#pragma unroll 1
+      if constexpr (PRUNE) {
+        // pruned walks diverge per frame: the DFS state stays in per-level
+        // local arrays, which keeps the lanes of a warp reconverging at every
+        // step of the loop (measured 1.6x fewer warp instructions than the
+        // register-resident walk below on cfg5)
+        // ---- one live skeleton (c, widths, runs); every area lies in
+        //      [win_lo, bmax[nH]] for a window a in [nL, nH]
+        const int win_lo = nL, win_hi = SCB_BMAX(nH);
+        SCB_STAT(skeletons);
+        if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
+        int amin = kBigArea, amax = 0;
+        int run = 0, nl = 0;
         for (int i = 0; i < c; ++i) {
+          RS0[i] = run;
           if (R[i] == 1) {  // one-run columns are fixed by the skeleton
             const int ar = W[i] * rows;
             amin = imin(amin, ar);
             amax = imax(amax, ar);
             curH[run] = (uint8_t)rows;
-            P = kmax(P, rt_at(X0[i], W[i], 0, rows));
           } else {
             const int base = xw_of(cols, X0[i], W[i]) * nyh;
-#pragma unroll 1
-            for (int j = 0; j < R[i] - 1; ++j, ++nl)
-              LS[nl] = Lvl{W[i] | ((R[i] - j) << 8) | ((run + j) << 16) | (i << 24), base, 0, 0};
+            for (int j = 0; j < R[i] - 1; ++j, ++nl) {
+              Lcol[nl] = (uint8_t)i;
+              Lrun[nl] = (uint8_t)j;
+              Lbase[nl] = base;
+            }
           }
           run += R[i];
         }
-        // a multi-run column stays fillable iff t2 <= w*floor(rows/R) and
-        // t1 >= w*ceil(rows/R) (columns_feasible); suffix bounds over the
-        // columns from each level's own column on
-        int sLo = 0, sHi = kBigArea;
-#pragma unroll 1
-        for (int l = nl - 1; l >= 0; --l) {
-          const int i = LS[l].a >> 24;
-          if (l == nl - 1 || (LS[l + 1].a >> 24) != i) {
-            sLo = imax(sLo, W[i] * ((rows + R[i] - 1) / R[i]));
-            sHi = imin(sHi, W[i] * (rows / R[i]));
+        tkey P = 0;
+        for (int i = 0; i < c; ++i)
+          if (R[i] == 1) P = kmax(P, rt_at(X0[i], W[i], 0, rows));
+        // pruned mode, shared items: identity of this skeleton
+        const bool split = PRUNE && e.split_g > 1;
+        uint64_t skey = 0;
+        int lsplit = -1;  // heights level whose values are dealt to the warps
+        if (split) {
+          skey = (uint64_t)c;
+          for (int i = 0; i < c; ++i) skey = skey * 0x100000001b3ull ^ (uint64_t)(W[i] | (R[i] << 8));
+          if (nl >= 2) lsplit = imin(e.split_depth, nl - 2);
+          else if (split_owner(skey, e.split_g) != (uint32_t)split_r) {
+            ord += 1;
+            continue;
           }
-          LS[l].c = sLo;
-          LS[l].d = sHi;
         }
-      }
-      // pruned mode, shared items: identity of this skeleton
-      const bool split = PRUNE && e.split_g > 1;
-      uint64_t skey = 0;
-      int lsplit = -1;  // heights level whose values are dealt to the warps
-      if (split) {
-        skey = (uint64_t)c;
-        for (int i = 0; i < c; ++i) skey = skey * 0x100000001b3ull ^ (uint64_t)(W[i] | (R[i] << 8));
-        if (nl >= 2) lsplit = imin(e.split_depth, nl - 2);
-        else if (split_owner(skey, e.split_g) != (uint32_t)split_r) {
+        if (nl == 0) {  // the skeleton is a single candidate
+          if (slot == 0 && viable(P)) score(P, ord, -1, 0, 0);
           ord += 1;
           continue;
         }
-      }
-      if (nl == 0) {  // the skeleton is a single candidate
-        if (slot == 0 && viable(P)) score(P, ord, -1, 0, 0);
-        ord += 1;
-        continue;
-      }
-      // pruned mode: every column's bound (PR) floors the whole subtree
-      const tkey colfloor = PRUNE ? kmax(P, PR[c]) : P;
-      if (!viable(colfloor)) continue;
+        // pruned mode: every column's bound (PR) floors the whole subtree
+        const tkey colfloor = PRUNE ? kmax(P, PR[c]) : P;
+        if (!viable(colfloor)) continue;
+        // ---- heights DFS over the multi-run columns (search.cpp:163-190)
+        int l = 0;
+        const bool leaf_now = (nl == 1);
+        if (!leaf_now) {
+          const int i = Lcol[0];
+          int lo0, hi0;
+          height_interval(e, thresholds(amin, amax, win_lo, win_hi), W[i], rows, R[i], lo0, hi0);
+          Lh[0] = (uint8_t)(lo0 - 1);
+          Lhi[0] = (uint8_t)imax(hi0, 0);
+          Pin[0] = P;
+          Amin[0] = amin;
+          Amax[0] = amax;
+          Ly0[0] = 0;
+        }
+        while (true) {
+          int lv;  // level whose state feeds the leaf loop
+          tkey Pl;
+          int amin_l, amax_l, y0l;
+          if (leaf_now) {
+            lv = 0;
+            Pl = P;
+            amin_l = amin;
+            amax_l = amax;
+            y0l = 0;
+          } else {
+            // advance level l to its next admissible height
+            SCB_STAT(levels);
+            const int i = Lcol[l], j = Lrun[l];
+  #if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
+            if (i == Lcol[nl - 1]) ++g_stats.levels_leafcol;
+  #endif
+            const int w = W[i], y0 = Ly0[l];
+            const int rows_left = rows - y0;
+            const bool forced = (R[i] - j) == 2;
+            int h = Lh[l] + 1;
+            const int hhi = Lhi[l];
+            if (e.patho && !forced)
+              while (h <= hhi && !(w * h <= SCB_BMAX(w * h))) ++h;
+            if (h > hhi) {
+              if (l == 0) break;
+              --l;
+              continue;
+            }
+            Lh[l] = (uint8_t)h;
+            if (split && l == lsplit) {  // deal this subtree to one warp of the item
+              uint64_t k = skey;
+              for (int q = 0; q <= l; ++q) k = k * 0x100000001b3ull ^ (uint64_t)(Lh[q] + 1);
+              if (split_owner(k, e.split_g) != (uint32_t)split_r) continue;
+            }
+            const int a1 = w * h;
+            int na = imin(Amin[l], a1), nx = imax(Amax[l], a1);
+            const int ridx = RS0[i] + j;
+            curH[ridx] = (uint8_t)h;
+            const int lb = Lbase[l];
+            const size_t ri = (size_t)(lb + SCB_YBASE(y0) + h - 1) * FPW + f;
+            tkey Pn;
+            if (forced) {
+              const int a2 = w * (rows_left - h);
+              na = imin(na, a2);
+              nx = imax(nx, a2);
+              curH[ridx + 1] = (uint8_t)(rows_left - h);
+              Pn = kmax(Pin[l], e.rts[ri]);
+            } else {
+              Pn = kmax(Pin[l], rt[ri]);
+            }
+            if (!viable(PRUNE ? kmax(Pn, colfloor) : Pn)) continue;
+            const int nxt = l + 1;
+            const bool new_col = Lrun[nxt] == 0;
+            const int y0n = new_col ? 0 : y0 + h;
+            const Thr tn = thresholds(na, nx, win_lo, win_hi);
+            if (new_col && !columns_feasible(Lcol[nxt], tn)) continue;
+            if (nxt < nl - 1) {
+              const int i2 = Lcol[nxt];
+              int lo2, hi2;
+              height_interval(e, tn, W[i2], rows - y0n, R[i2] - Lrun[nxt], lo2, hi2);
+              if (lo2 > hi2) continue;
+              l = nxt;
+              Lh[l] = (uint8_t)(lo2 - 1);
+              Lhi[l] = (uint8_t)hi2;
+              Pin[l] = Pn;
+              Amin[l] = na;
+              Amax[l] = nx;
+              Ly0[l] = (uint8_t)y0n;
+              continue;
+            }
+            lv = nxt;
+            Pl = Pn;
+            amin_l = na;
+            amax_l = nx;
+            y0l = y0n;
+          }
+          // ---- leaf loop: run Lrun[lv] of column Lcol[lv] takes every
+          //      admissible height; the column's last run is forced.
+          {
+            const int i = Lcol[lv];
+            const int w = W[i];
+            const int rows_left = rows - y0l;
+            int lo, hi;
+            height_interval(e, thresholds(amin_l, amax_l, win_lo, win_hi), w, rows_left, 2, lo, hi);
+            const int lr = RS0[i] + Lrun[lv];
+            const int xwb = Lbase[lv];
+            SCB_STAT(leaf_calls);
+  #if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
+            ++g_stats.leafr[R[i]];
+  #endif
+            if (lo + slot <= hi && viable(PRUNE ? kmax(Pl, colfloor) : Pl)) {
+              // the split table holds max(run h, forced rest) at the run's own
+              // rectangle index, which advances by +1 per h; lanes step h by J.
+              int h = lo + slot;
+              const tkey* p = e.rts + (size_t)(xwb + SCB_YBASE(y0l) + h - 1) * FPW + f;
+              tkey v = *p;
+              while (true) {
+                const int hn = h + J;
+                const bool more = hn <= hi;
+                const tkey vn = more ? p[J * FPW] : 0;  // prefetch the next height
+                score(kmax(Pl, v), ord + (uint64_t)(h - lo), lr, h, rows_left - h);
+                if (!more) break;
+                h = hn;
+                p += J * FPW;
+                v = vn;
+              }
+            }
+            if (hi >= lo) ord += (uint64_t)(hi - lo + 1);
+          }
+          if (leaf_now) break;
+        }
+      } else {
+        // ---- one live skeleton (c, widths, runs); every area lies in
+        //      [win_lo, bmax[nH]] for a window a in [nL, nH]
+        const int win_lo = nL, win_hi = SCB_BMAX(nH);
+        SCB_STAT(skeletons);
+        if (STEP == 1 && PRUNE) st.inc = incumbent_load(e.inc + f);
+        // Levels of the heights DFS: every run of a multi-run column but its
+        // last (forced) one, column by column.  Static per-level facts go to
+        // LS[] once per skeleton; the DFS keeps its current level in registers
+        // and spills a level's state to D[] only when it descends.
+        int amin = kBigArea, amax = 0;
+        int nl = 0;
+        tkey P = 0;
+        {
+          int run = 0;
+  #pragma unroll 1
+          for (int i = 0; i < c; ++i) {
+            if (R[i] == 1) {  // one-run columns are fixed by the skeleton
+              const int ar = W[i] * rows;
+              amin = imin(amin, ar);
+              amax = imax(amax, ar);
+              curH[run] = (uint8_t)rows;
+              P = kmax(P, rt_at(X0[i], W[i], 0, rows));
+            } else {
+              nl += R[i] - 1;
+            }
+            run += R[i];
+          }
+        }
+        // pruned mode, shared items: identity of this skeleton
+        const bool split = PRUNE && e.split_g > 1;
+        uint64_t skey = 0;
+        int lsplit = -1;  // heights level whose values are dealt to the warps
+        if (split) {
+          skey = (uint64_t)c;
+          for (int i = 0; i < c; ++i) skey = skey * 0x100000001b3ull ^ (uint64_t)(W[i] | (R[i] << 8));
+          if (nl >= 2) lsplit = imin(e.split_depth, nl - 2);
+          else if (split_owner(skey, e.split_g) != (uint32_t)split_r) {
+            ord += 1;
+            continue;
+          }
+        }
+        if (nl == 0) {  // the skeleton is a single candidate
+          if (slot == 0 && viable(P)) score(P, ord, -1, 0, 0);
+          ord += 1;
+          continue;
+        }
+        // pruned mode: every column's bound (PR) floors the whole subtree
+        const tkey colfloor = PRUNE ? kmax(P, PR[c]) : P;
+        if (!viable(colfloor)) continue;
+        {
+          // level records, built from the last column backwards: a multi-run
+          // column stays fillable iff t2 <= w*floor(rows/R) and
+          // t1 >= w*ceil(rows/R) (the columns_feasible test), so each level
+          // carries the suffix bounds over the columns from its own on
+          int sLo = 0, sHi = kBigArea, lvl = nl, rr = e.n;
+  #pragma unroll 1
+          for (int i = c - 1; i >= 0; --i) {
+            rr -= R[i];  // first run of column i
+            if (R[i] < 2) continue;
+            sLo = imax(sLo, W[i] * ((rows + R[i] - 1) / R[i]));
+            sHi = imin(sHi, W[i] * SCB_RQ(R[i]));
+            const int base = xw_of(cols, X0[i], W[i]) * nyh;
+  #pragma unroll 1
+            for (int j = R[i] - 2; j >= 0; --j)
+              LS[--lvl] = Lvl{W[i] | ((R[i] - j) << 8) | ((rr + j) << 16) | (i << 24), base, sLo, sHi};
+          }
+        }
 
-      // current level (registers): static facts, height h in (.., hhi],
-      // first row y0, fixed-slice maximum Pin and areas Amin / Amax
-      int l = 0, cw = 0, crl = 0, h = 0, hhi = 0, y0 = 0, cAmin = amin, cAmax = amax;
-      int cridx = 0, clbase = 0;
-      tkey cPin = P;
-      auto load_static = [&](const Lvl& s) {
-        cw = s.a & 255;
-        crl = (s.a >> 8) & 255;
-        cridx = (s.a >> 16) & 255;
-        clbase = s.b;
-      };
-      // heights of the runs fixed by levels 0..l (curH; only the best-update
-      // paths read it)
-      auto sync_heights = [&]() {
-#pragma unroll 1
-        for (int q = 0; q <= l; ++q) {
-          int hq, yq, rq, iq;
-          if (q < l) {
-            hq = D[q].a & 255;
-            yq = (D[q].a >> 16) & 255;
-            rq = (LS[q].a >> 8) & 255;
-            iq = (LS[q].a >> 16) & 255;
-          } else {
-            hq = h;
-            yq = y0;
-            rq = crl;
-            iq = cridx;
-          }
-          curH[iq] = (uint8_t)hq;
-          if (rq == 2) curH[iq + 1] = (uint8_t)(rows - yq - hq);
-        }
-      };
-      // ---- leaf: run `lr` of the last multi-run column takes every
-      //      admissible height; the column's last run is forced.
-      const Lvl LL = LS[nl - 1];
-      const int lw = LL.a & 255, lr = (LL.a >> 16) & 255, lxwb = LL.b;
-      const uint64_t lmg = SCB_MAGIC(lw);
-      const int lms = lw * (e.rows + 1);
-      auto leaf = [&](tkey Pl, int amin_l, int amax_l, int y0l, bool synced) {
-        SCB_STAT(leaf_calls);
-        const int rows_left = rows - y0l;
-        const Thr t = thresholds(amin_l, amax_l, win_lo, win_hi);
-        const int hmin_a = imax(1, div_w(t.t2 + lw - 1, lmg));
-        const int hmax_a = t.t1 < 0 ? 0 : div_w(t.t1, lmg);
-        const int lo = imax(imax(hmin_a, rows_left - hmax_a), SCB_MSTAR(lms + rows_left));
-        const int hi = rows_left - lo;
-        if (lo + slot <= hi && viable(PRUNE ? kmax(Pl, colfloor) : Pl)) {
-          // the split table holds max(run h, forced rest) at the run's own
-          // rectangle index, which advances by +1 per h; lanes step h by J
-          // (J * FPW = 32 keys between consecutive heights of a lane)
-          const tkey* p0 = e.rts + (size_t)(lxwb + SCB_YBASE(y0l) + lo + slot - 1) * FPW + f;
-          if (STEP == 1) {
-            // every candidate's time max(Pl, v_h) is evaluated as one
-            // min-reduction; only a chunk that can beat the lane's best
-            // replays its heights in order through score()
-            const int nh = (hi - lo - slot) / J + 1;
-            tkey m = kKeyInf;
-            const tkey* p = p0;
-#pragma unroll 1
-            for (int k = 0; k < nh; k += 4, p += 4 * 32) {
-              const tkey v0 = p[0];
-              const tkey v1 = k + 1 < nh ? p[32] : kKeyInf;
-              const tkey v2 = k + 2 < nh ? p[64] : kKeyInf;
-              const tkey v3 = k + 3 < nh ? p[96] : kKeyInf;
-              m = umin3(m, umin3(v0, v1, v2), v3);
-            }
-            if (PRUNE) st.scored += (uint64_t)nh;
-            const tkey thr = PRUNE ? ((st.tie && st.best_t != kKeyInf) ? st.best_t + 1 : st.best_t)
-                                   : st.bcmp;
-            if (kmax(Pl, m) < thr) {
-              if (!synced) sync_heights();
-              if (PRUNE) st.scored -= (uint64_t)nh;  // score() counts them again
+        // current level (registers): static facts, height h in (.., hhi],
+        // first row y0, fixed-slice maximum Pin and areas Amin / Amax
+        int l = 0, cw = 0, crl = 0, h = 0, hhi = 0, y0 = 0, cAmin = amin, cAmax = amax;
+        int cridx = 0, clbase = 0;
+        tkey cPin = P;
+        auto load_static = [&](const Lvl& s) {
+          cw = s.a & 255;
+          crl = (s.a >> 8) & 255;
+          cridx = (s.a >> 16) & 255;
+          clbase = s.b;
+        };
+        // curH holds the heights of the levels above the current one (written
+        // when the DFS descends past them); the current level's own run (and its
+        // forced rest) is written only before a score that may read it
+        auto sync_heights = [&]() {
+          if (l < 0) return;
+          curH[cridx] = (uint8_t)h;
+          if (crl == 2) curH[cridx + 1] = (uint8_t)(rows - y0 - h);
+        };
+        // ---- leaf: run `lr` of the last multi-run column takes every
+        //      admissible height; the column's last run is forced.
+        const Lvl LL = LS[nl - 1];
+        const int lw = LL.a & 255, lr = (LL.a >> 16) & 255, lxwb = LL.b;
+        const uint64_t lmg = SCB_MAGIC(lw);
+        const int lms = lw * (e.rows + 1);
+        auto leaf = [&](tkey Pl, int amin_l, int amax_l, int y0l) {
+          SCB_STAT(leaf_calls);
+          const int rows_left = rows - y0l;
+          const Thr t = thresholds(amin_l, amax_l, win_lo, win_hi);
+          const int hmin_a = imax(1, div_w(t.t2 + lw - 1, lmg));
+          const int hmax_a = t.t1 < 0 ? 0 : div_w(t.t1, lmg);
+          const int lo = imax(imax(hmin_a, rows_left - hmax_a), SCB_MSTAR(lms + rows_left));
+          const int hi = rows_left - lo;
+          if (lo + slot <= hi && viable(PRUNE ? kmax(Pl, colfloor) : Pl)) {
+            // the split table holds max(run h, forced rest) at the run's own
+            // rectangle index, which advances by +1 per h; lanes step h by J
+            // (J * FPW = 32 keys between consecutive heights of a lane)
+            const tkey* p0 = e.rts + (size_t)(lxwb + SCB_YBASE(y0l) + lo + slot - 1) * FPW + f;
+            if (STEP == 1 && !PRUNE) {
+              // every candidate's time max(Pl, v_h) is evaluated as one
+              // min-reduction; only a chunk that can beat the lane's best
+              // replays its heights in order through score()
+              const int nh = (hi - lo - slot) / J + 1;
+              tkey m = kKeyInf;
+              const tkey* p = p0;
+  #pragma unroll 1
+              for (int k = 0; k < nh; k += 4, p += 4 * 32) {
+                const tkey v0 = p[0];
+                const tkey v1 = k + 1 < nh ? p[32] : kKeyInf;
+                const tkey v2 = k + 2 < nh ? p[64] : kKeyInf;
+                const tkey v3 = k + 3 < nh ? p[96] : kKeyInf;
+                m = umin3(m, umin3(v0, v1, v2), v3);
+              }
+              const tkey thr = st.bcmp;
+              if (kmax(Pl, m) < thr) {
+                sync_heights();
+                const tkey* q = p0;
+  #pragma unroll 1
+                for (int hh = lo + slot; hh <= hi; hh += J, q += 32)
+                  score(kmax(Pl, *q), ord + (uint64_t)(hh - lo), lr, hh, rows_left - hh);
+              }
+            } else {  // pruned walks and step 2: leaves are few, winners common
+              sync_heights();
+              int hh = lo + slot;
               const tkey* q = p0;
-#pragma unroll 1
-              for (int hh = lo + slot; hh <= hi; hh += J, q += 32)
-                score(kmax(Pl, *q), ord + (uint64_t)(hh - lo), lr, hh, rows_left - hh);
-            }
-          } else {
-            if (!synced) sync_heights();
-            int hh = lo + slot;
-            const tkey* q = p0;
-            tkey v = *q;
-            while (true) {
-              const int hn = hh + J;
-              const bool more = hn <= hi;
-              const tkey vn = more ? q[32] : 0;  // prefetch the next height
-              score(kmax(Pl, v), ord + (uint64_t)(hh - lo), lr, hh, rows_left - hh);
-              if (!more) break;
-              hh = hn;
-              q += 32;
-              v = vn;
+              tkey v = *q;
+              while (true) {
+                const int hn = hh + J;
+                const bool more = hn <= hi;
+                const tkey vn = more ? q[32] : 0;  // prefetch the next height
+                score(kmax(Pl, v), ord + (uint64_t)(hh - lo), lr, hh, rows_left - hh);
+                if (!more) break;
+                hh = hn;
+                q += 32;
+                v = vn;
+              }
             }
           }
-        }
-        if (hi >= lo) ord += (uint64_t)(hi - lo + 1);
-      };
-      if (nl == 1) {
-        l = -1;  // no level above the leaf
-        leaf(P, amin, amax, 0, true);
-        continue;
-      }
-      // ---- heights DFS over the levels above the leaf (search.cpp:163-190)
-      load_static(LS[0]);
-      {
-        int lo0, hi0;
-        height_interval(e, thresholds(amin, amax, win_lo, win_hi), cw, rows, crl, lo0, hi0);
-        h = lo0 - 1;
-        hhi = imax(hi0, 0);
-      }
-      while (true) {
-        SCB_STAT(levels);
-        const bool forced = crl == 2;
-        ++h;
-        if (e.patho && !forced)
-          while (h <= hhi && !(cw * h <= SCB_BMAX(cw * h))) ++h;
-        if (h > hhi) {
-          if (l == 0) break;
-          --l;
-          load_static(LS[l]);
-          const Lvl dl = D[l];
-          h = dl.a & 255;
-          hhi = (dl.a >> 8) & 255;
-          y0 = (dl.a >> 16) & 255;
-          cPin = (tkey)dl.b;
-          cAmin = dl.c;
-          cAmax = dl.d;
+          if (hi >= lo) ord += (uint64_t)(hi - lo + 1);
+        };
+        if (nl == 1) {
+          l = -1;  // no level above the leaf
+          leaf(P, amin, amax, 0);
           continue;
         }
-        if (split && l == lsplit) {  // deal this subtree to one warp of the item
-          uint64_t k = skey;
-          for (int q = 0; q < l; ++q) k = k * 0x100000001b3ull ^ (uint64_t)((D[q].a & 255) + 1);
-          k = k * 0x100000001b3ull ^ (uint64_t)(h + 1);
-          if (split_owner(k, e.split_g) != (uint32_t)split_r) continue;
+        // ---- heights DFS over the levels above the leaf (search.cpp:163-190)
+        load_static(LS[0]);
+        {
+          int lo0, hi0;
+          height_interval(e, thresholds(amin, amax, win_lo, win_hi), cw, rows, crl, lo0, hi0);
+          h = lo0 - 1;
+          hhi = imax(hi0, 0);
         }
-        const int a1 = cw * h;
-        int na = imin(cAmin, a1), nx = imax(cAmax, a1);
-        const size_t ri = (size_t)(clbase + SCB_YBASE(y0) + h - 1) * FPW + f;
-        tkey Pn;
-        if (forced) {
-          const int a2 = cw * (rows - y0 - h);
-          na = imin(na, a2);
-          nx = imax(nx, a2);
-          Pn = kmax(cPin, e.rts[ri]);
-        } else {
-          Pn = kmax(cPin, rt[ri]);
+        while (true) {
+          SCB_STAT(levels);
+          const bool forced = crl == 2;
+          ++h;
+          if (e.patho && !forced)
+            while (h <= hhi && !(cw * h <= SCB_BMAX(cw * h))) ++h;
+          if (h > hhi) {
+            if (l == 0) break;
+            --l;
+            load_static(LS[l]);
+            const Lvl dl = D[l];
+            h = dl.a & 255;
+            hhi = (dl.a >> 8) & 255;
+            y0 = (dl.a >> 16) & 255;
+            cPin = (tkey)dl.b;
+            cAmin = dl.c;
+            cAmax = dl.d;
+            continue;
+          }
+          if (split && l == lsplit) {  // deal this subtree to one warp of the item
+            uint64_t k = skey;
+            for (int q = 0; q < l; ++q) k = k * 0x100000001b3ull ^ (uint64_t)((D[q].a & 255) + 1);
+            k = k * 0x100000001b3ull ^ (uint64_t)(h + 1);
+            if (split_owner(k, e.split_g) != (uint32_t)split_r) continue;
+          }
+          const int a1 = cw * h;
+          int na = imin(cAmin, a1), nx = imax(cAmax, a1);
+          const size_t ri = (size_t)(clbase + SCB_YBASE(y0) + h - 1) * FPW + f;
+          tkey Pn;
+          if (forced) {
+            const int a2 = cw * (rows - y0 - h);
+            na = imin(na, a2);
+            nx = imax(nx, a2);
+            Pn = kmax(cPin, e.rts[ri]);
+          } else {
+            Pn = kmax(cPin, rt[ri]);
+          }
+          if (!viable(PRUNE ? kmax(Pn, colfloor) : Pn)) continue;
+          const int nxt = l + 1;
+          const int y0n = forced ? 0 : y0 + h;
+          const Thr tn = thresholds(na, nx, win_lo, win_hi);
+          const Lvl sn = LS[nxt];
+          // a new column: every multi-run column from it on must stay fillable
+          if (forced && (tn.t2 > sn.d || tn.t1 < sn.c)) continue;
+          if (nxt < nl - 1) {
+            int lo2, hi2;
+            height_interval(e, tn, sn.a & 255, rows - y0n, (sn.a >> 8) & 255, lo2, hi2);
+            if (lo2 > hi2) continue;
+            D[l] = Lvl{h | (hhi << 8) | (y0 << 16), (int32_t)cPin, cAmin, cAmax};
+            sync_heights();
+            l = nxt;
+            load_static(sn);
+            h = lo2 - 1;
+            hhi = hi2;
+            y0 = y0n;
+            cPin = Pn;
+            cAmin = na;
+            cAmax = nx;
+            continue;
+          }
+          leaf(Pn, na, nx, y0n);
         }
-        if (!viable(PRUNE ? kmax(Pn, colfloor) : Pn)) continue;
-        const int nxt = l + 1;
-        const int y0n = forced ? 0 : y0 + h;
-        const Thr tn = thresholds(na, nx, win_lo, win_hi);
-        const Lvl sn = LS[nxt];
-        // a new column: every multi-run column from it on must stay fillable
-        if (forced && (tn.t2 > sn.d || tn.t1 < sn.c)) continue;
-        if (nxt < nl - 1) {
-          int lo2, hi2;
-          height_interval(e, tn, sn.a & 255, rows - y0n, (sn.a >> 8) & 255, lo2, hi2);
-          if (lo2 > hi2) continue;
-          D[l] = Lvl{h | (hhi << 8) | (y0 << 16), (int32_t)cPin, cAmin, cAmax};
-          l = nxt;
-          load_static(sn);
-          h = lo2 - 1;
-          hhi = hi2;
-          y0 = y0n;
-          cPin = Pn;
-          cAmin = na;
-          cAmax = nx;
-          continue;
-        }
-        leaf(Pn, na, nx, y0n, false);
       }
     }
     if (fixed_widths) break;
