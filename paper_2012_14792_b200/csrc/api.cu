@@ -31,11 +31,12 @@ void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16
                         double* d_rect_s, uint64_t* d_rt, double* d_rs, int sm_count,
                         cudaStream_t st);
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st);
-int search_blocks_per_sm(int fpw, int step, bool prune);
+int search_blocks_per_sm(int fpw, int step, bool prune, size_t smem);
+size_t search_smem_bytes(int cols, int rows, int n, int step, bool prune);
 void item_filter_launch(sc_ctx* ctx, const SearchArgs& a, uint32_t k0, uint32_t k1, int fpw,
                         int frames, int step, const uint64_t* seed_inc, uint32_t* list,
                         uint32_t* count, cudaStream_t st);
-int search_block_threads();
+int search_block_threads(int step, bool prune);
 void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int cols, int rows,
                           int rmax, int rstride, uint32_t* lbr, uint32_t* lbm, cudaStream_t st);
 void partition_eval_device(const double* d_sat, const uint64_t* d_usat, const int* d_rects, int n,
@@ -360,9 +361,11 @@ void finish_schedule(Plan* p) {
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
                   const Layouts& L, int step, bool compute_bounds, cudaStream_t st) {
   const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
-  const int bps = search_blocks_per_sm(L.fpw, step, prune);
+  const int bps =
+      search_blocks_per_sm(L.fpw, step, prune,
+                           search_smem_bytes(g.cols, g.rows, cfg.n_slices, step, prune));
   const int blocks = ctx->sm_count * bps;
-  const uint32_t warps = (uint32_t)blocks * (search_block_threads() / 32);
+  const uint32_t warps = (uint32_t)blocks * (search_block_threads(step, prune) / 32);
   const size_t lane_bytes = (size_t)warps * 32 * sizeof(LaneBest);
   const size_t snap_bytes = (size_t)warps * 32 * kSnapBytes;
   ctx->lanes.ensure(lane_bytes * L.groups);

@@ -36,18 +36,47 @@ namespace scb {
 #ifndef SCB_SEARCH_MINB
 #define SCB_SEARCH_MINB 2
 #endif
-// exhaustive step 1: 2 CTAs/SM (88 registers; capping at 80 for 3 CTAs
-// measured 8 % slower)
-#ifndef SCB_SEARCH_MINB1
-#define SCB_SEARCH_MINB1 2
-#endif
 #ifndef SCB_SEARCH_BLOCK
 #define SCB_SEARCH_BLOCK 256
 #endif
-int search_block_threads() { return SCB_SEARCH_BLOCK; }
+// Exhaustive step 1 (the headline walk, warp-uniform, ~88 registers): 64-thread
+// blocks so the register file, not the block granularity, sets the warps per
+// SM (11 blocks = 22 warps vs 16 with 256-thread blocks).
+#ifndef SCB_SEARCH_BLOCK1
+#define SCB_SEARCH_BLOCK1 256
+#endif
+#ifndef SCB_SEARCH_MINB1
+#define SCB_SEARCH_MINB1 2
+#endif
+template <int STEP, bool PRUNE>
+struct SearchShape {
+  static constexpr bool kHead = STEP == 1 && !PRUNE;
+  static constexpr int kBlock = kHead ? SCB_SEARCH_BLOCK1 : SCB_SEARCH_BLOCK;
+  static constexpr int kMinBlocks = kHead ? SCB_SEARCH_MINB1 : SCB_SEARCH_MINB;
+};
+int search_block_threads(int step, bool prune) {
+  return (step == 1 && !prune) ? SCB_SEARCH_BLOCK1 : SCB_SEARCH_BLOCK;
+}
+// dynamic shared memory of the search kernels: bmax|aneed [2A], mstar, ilo
+// (int32), then, for the warp-uniform exhaustive walks, 2 * n level records
+// (16 B) per warp (search_walk.cuh WalkEnv::lvl)
+size_t search_tables_bytes(int cols, int rows, int n) {
+  return ((size_t)2 * (cols * rows + 1) + (size_t)(cols + 1) * (rows + 1) +
+          (size_t)(cols + 1) * (std::min(n, rows) + 1)) *
+         sizeof(int32_t);
+}
+size_t search_smem_bytes(int cols, int rows, int n, int step, bool prune) {
+  size_t b = search_tables_bytes(cols, rows, n);
+  // per warp: 2 * n level records + 32 lanes x n Pin keys
+  if (!prune)
+    b = (b + 15) / 16 * 16 + (size_t)(search_block_threads(step, prune) / 32) * std::max(n, 1) *
+                                 (2 * sizeof(Lvl) + 32 * sizeof(uint32_t));
+  return b;
+}
 
 template <int FPW, int STEP, bool PRUNE>
-__global__ void __launch_bounds__(SCB_SEARCH_BLOCK, (STEP == 1 && !PRUNE) ? SCB_SEARCH_MINB1 : SCB_SEARCH_MINB)
+__global__ void __launch_bounds__(SearchShape<STEP, PRUNE>::kBlock,
+                                  SearchShape<STEP, PRUNE>::kMinBlocks)
 k_search(SearchArgs a) {
   // shared-memory tables (search_walk.cuh): g_dyn = bmax|aneed interleaved
   // [2A], mstar [(cols+1)(rows+1)], ilo [(cols+1) * rstride]; static magic,
@@ -87,6 +116,20 @@ k_search(SearchArgs a) {
   e.split_depth = a.split_depth;
   e.mstar_off = 2 * A;
   e.ilo_off = ilo_off;
+  if (!PRUNE) {
+    const int tab_words = ilo_off + (a.cols + 1) * rstride;
+    const int lvl_cap = max(a.n, 1);
+    Lvl* const lvl0 = reinterpret_cast<Lvl*>(g_dyn + (tab_words + 3) / 4 * 4);
+    const int nwarps = blockDim.x >> 5, wib = threadIdx.x >> 5;
+    e.lvl = lvl0 + (size_t)wib * 2 * lvl_cap;
+    e.pin = reinterpret_cast<tkey*>(lvl0 + (size_t)nwarps * 2 * lvl_cap) +
+            (size_t)wib * 32 * lvl_cap + (threadIdx.x & 31);
+    e.lvl_cap = lvl_cap;
+  } else {
+    e.lvl = nullptr;
+    e.pin = nullptr;
+    e.lvl_cap = 0;
+  }
   e.rt = a.rt;
   e.rts = a.rts;
   e.rs = a.rs;
@@ -267,21 +310,22 @@ static void launch_fpw(const SearchArgs& a, int blocks, size_t smem, cudaStream_
   static bool attr = false;
   if (!attr) {
     SCB_CUDA(cudaFuncSetAttribute(k_search<FPW, STEP, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     SCB_CUDA(cudaFuncSetAttribute(k_search<FPW, STEP, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     attr = true;
   }
-  if (a.prune) k_search<FPW, STEP, true><<<blocks, SCB_SEARCH_BLOCK, smem, st>>>(a);
-  else k_search<FPW, STEP, false><<<blocks, SCB_SEARCH_BLOCK, smem, st>>>(a);
+  if (a.prune)
+    k_search<FPW, STEP, true><<<blocks, SearchShape<STEP, true>::kBlock, smem, st>>>(a);
+  else
+    k_search<FPW, STEP, false><<<blocks, SearchShape<STEP, false>::kBlock, smem, st>>>(a);
 }
 
-int search_blocks_per_sm(int fpw, int step, bool prune) {
+int search_blocks_per_sm(int fpw, int step, bool prune, size_t smem) {
   int nb = 0;
-  const size_t smem = 16 * 1024;
 #define OCC1(F, S, P)                                                                        \
   SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, S, P>,           \
-                                                         SCB_SEARCH_BLOCK, smem))
+                                                         SearchShape<S, P>::kBlock, smem))
 #define OCC(F)                                                                               \
   if (fpw == F) {                                                                            \
     if (step == 1) {                                                                         \
@@ -299,10 +343,9 @@ int search_blocks_per_sm(int fpw, int step, bool prune) {
 }
 
 void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStream_t st) {
-  const size_t smem = ((size_t)2 * (a.max_area + 1) + (size_t)(a.cols + 1) * (a.rows + 1) +
-                       (size_t)(a.cols + 1) * (std::min(a.n, a.rows) + 1)) *
-                      sizeof(int32_t);
-  if (smem > 64 * 1024) fail(SC_ERR_SIZE, "CTU grid too large for the area tables");
+  const size_t smem = search_smem_bytes(a.cols, a.rows, a.n, step, a.prune != 0);
+  if (search_tables_bytes(a.cols, a.rows, a.n) > 64 * 1024)
+    fail(SC_ERR_SIZE, "CTU grid too large for the area tables");
   switch (fpw * 10 + step) {
     case 11: launch_fpw<1, 1>(a, blocks, smem, st); break;
     case 12: launch_fpw<1, 2>(a, blocks, smem, st); break;

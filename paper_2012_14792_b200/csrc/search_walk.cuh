@@ -35,6 +35,11 @@ inline WalkStats g_stats;
 #endif
 
 // ---- portable intrinsics -------------------------------------------------------
+#ifdef __CUDA_ARCH__
+#define SCB_SYNCWARP() __syncwarp()
+#else
+#define SCB_SYNCWARP() ((void)0)
+#endif
 SCB_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
 #ifdef __CUDA_ARCH__
   return __umulhi(a, b);
@@ -121,6 +126,13 @@ struct WalkEnv {
   const int32_t* ybase;   // [rows+1]: yh(y, 1), the first rectangle starting at row y
   const int32_t* rq;      // [rows+1]: rows / r (no integer division in the runs DFS)
   int mstar_off, ilo_off;  // GPU: offsets of mstar / ilo in dynamic shared memory
+  // GPU, exhaustive walks: this warp's heights-DFS level records in shared
+  // memory (LS = lvl[0, lvl_cap), D = lvl[lvl_cap, 2 lvl_cap)).  The walk is
+  // warp-uniform, so one copy per warp replaces 32 per-thread copies in local
+  // memory (which crowded L1); only the per-frame Pin stays per lane.
+  Lvl* lvl;
+  tkey* pin;  // this lane's Pin slots: pin[l * 32]
+  int lvl_cap;
   // pruned mode: split_g warps share each work item; the subtrees below
   // level split_depth of the heights DFS (or a whole skeleton, if it has
   // fewer levels) are dealt to them by a hash of their identity
@@ -284,8 +296,24 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   tkey Pin[kMaxLevels];
   // heights-DFS levels: LS static (w | runs left << 8 | run << 16 | column << 24,
   // column rectangle base, suffix fillability bounds), D the spilled state of
-  // the levels above the current one (h | hhi << 8 | y0 << 16, Pin, Amin, Amax)
-  Lvl LS[kMaxLevels], D[kMaxLevels];  // exhaustive walks
+  // the levels above the current one (h | hhi << 8 | y0 << 16, -, Amin, Amax; Pin
+  // per lane in PIN)
+#ifdef __CUDA_ARCH__
+  // exhaustive walks: the level records are warp-uniform, one copy per warp
+  // in shared memory; the fixed-slice maximum Pin of a level depends on the
+  // lane's frame, so it has its own lane-interleaved array (PIN[l * 32])
+  Lvl* const LS = e.lvl;
+  Lvl* const D = e.lvl + e.lvl_cap;
+  tkey* const PIN = e.pin;
+  constexpr int PS = 32;
+#else
+  Lvl LSa[kMaxLevels], Da[kMaxLevels];
+  tkey PINa[kMaxLevels];
+  Lvl* const LS = LSa;
+  Lvl* const D = Da;
+  tkey* const PIN = PINa;
+  constexpr int PS = 1;
+#endif
 
   auto thresholds = [&](int amin, int amax, int win_lo, int win_hi) -> Thr {
     Thr t;
@@ -758,6 +786,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         // pruned mode: every column's bound (PR) floors the whole subtree
         const tkey colfloor = PRUNE ? kmax(P, PR[c]) : P;
         if (!viable(colfloor)) continue;
+        SCB_SYNCWARP();  // every lane is done with the previous skeleton's records
         {
           // level records, built from the last column backwards: a multi-run
           // column stays fillable iff t2 <= w*floor(rows/R) and
@@ -872,6 +901,9 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         }
         while (true) {
           SCB_STAT(levels);
+          // the level records are written by every lane with the same value;
+          // a lane may only overwrite one after all lanes finished reading it
+          SCB_SYNCWARP();
           const bool forced = crl == 2;
           ++h;
           if (e.patho && !forced)
@@ -884,7 +916,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             h = dl.a & 255;
             hhi = (dl.a >> 8) & 255;
             y0 = (dl.a >> 16) & 255;
-            cPin = (tkey)dl.b;
+            cPin = PIN[l * PS];
             cAmin = dl.c;
             cAmax = dl.d;
             continue;
@@ -918,7 +950,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             int lo2, hi2;
             height_interval(e, tn, sn.a & 255, rows - y0n, (sn.a >> 8) & 255, lo2, hi2);
             if (lo2 > hi2) continue;
-            D[l] = Lvl{h | (hhi << 8) | (y0 << 16), (int32_t)cPin, cAmin, cAmax};
+            D[l] = Lvl{h | (hhi << 8) | (y0 << 16), 0, cAmin, cAmax};
+          PIN[l * PS] = cPin;
             sync_heights();
             l = nxt;
             load_static(sn);
