@@ -308,6 +308,7 @@ bool step2_bounded(const sc_search_cfg& cfg) {
 // SLICECRAFT_B200_SCHEDULE=0 keeps the enumeration order.
 // exhaustive mode's budget-bounded step 2 (SLICECRAFT_B200_SPLIT2 overrides)
 constexpr int kBoundedStep2Split = 16;
+constexpr int kSplitDepth1 = 8;
 
 // Pruned walks: warps sharing one work item and the heights level whose
 // subtrees they deal out.  Sharing costs every warp of an item the walk down
@@ -323,10 +324,18 @@ int split_ways(int step, int n, bool pruned_mode) {
   int g = v ? atoi(v) : (pruned_mode ? 16 : kBoundedStep2Split);
   return g < 1 ? 1 : (g > 64 ? 64 : g);
 }
-int split_depth() {
-  const char* v = getenv("SLICECRAFT_B200_SPLIT_DEPTH");
-  const int d = v ? atoi(v) : 1;
-  return d < 0 ? 0 : (d > 8 ? 8 : d);
+// Heights level whose subtrees the warps of a shared item deal out.  Step 1
+// (SLICECRAFT_B200_SPLIT_DEPTH): deep, so the seed phase's few long
+// single-column walks spread over all the item's warps; step 2
+// (SLICECRAFT_B200_SPLIT_DEPTH2): shallow, its leaves are expensive and a
+// deep split repeats the walk above it in every warp
+// (profiles/r01_split_sweep.md).
+int split_depth(int step, int n) {
+  const char* v = getenv(step == 1 ? "SLICECRAFT_B200_SPLIT_DEPTH" : "SLICECRAFT_B200_SPLIT_DEPTH2");
+  // measured: depth 8 takes cfg5 (n = 32) step 1 from 4.8 to 3.6 ms, but
+  // costs cfg3 (n = 8) 13 %; cfg4 (n = 16) is even
+  const int d = v ? atoi(v) : ((step == 1 && n >= 24) ? kSplitDepth1 : 1);
+  return d < 0 ? 0 : (d > 62 ? 62 : d);
 }
 
 // Pruned walks: drop the items whose prefix fails every frame before the
@@ -416,7 +425,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     const uint32_t G =
         prune ? (uint32_t)split_ways(step, cfg.n_slices, cfg.mode == SC_MODE_PRUNED) : 1u;
     a.split_g = (int)G;
-    a.split_depth = split_depth();
+    a.split_depth = split_depth(step, cfg.n_slices);
     a.n_items = mine * G;
     a.item_offset = rank;
     a.item_stride = world;

@@ -87,6 +87,7 @@ def _mode(monkeypatch, m):
     if m == "pruned-split":
         monkeypatch.setenv("SLICECRAFT_B200_SPLIT", "5")
         monkeypatch.setenv("SLICECRAFT_B200_SPLIT2", "3")
+        monkeypatch.setenv("SLICECRAFT_B200_SPLIT_DEPTH", "3")
     return 1 if m.startswith("pruned") else 0
 
 
