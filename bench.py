@@ -302,11 +302,12 @@ def run_ours(args):
         "roofline_texture": tex_roof,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": luma_bytes + F * g.cell_count() * 8,
                 "d2h_bytes_per_step": 2 * 32 * ((F + 31) // 32) * 168, "ms_per_step": ms_e2e},
-        # per call (profiles/r01_cfg3_launches.md): K1, 2x(K2 + K3), the rank
-        # pipeline (6 own + 14 CUB launches), split table; per frame group:
-        # column bounds, step-1 walk + finalize, step-2 walk + finalize (+1
-        # seed-phase launch in pruned mode)
-        "gpu_launches": args.steps * (25 + (5 + args.mode) * ((F + 31) // 32)),
+        # per call (profiles/r01f_cfg3_launches.md, 33 launches): K1, 2x(K2 +
+        # K3), the rank pipeline (6 own + 13 CUB launches), split table; per
+        # frame group: column bounds, step-1 walk + finalize, item filter (own
+        # + 2 CUB select launches), step-2 walk + finalize; pruned mode adds the
+        # seed-phase walk and the phase-B item filter (+4)
+        "gpu_launches": args.steps * (25 + (8 + 4 * args.mode) * ((F + 31) // 32)),
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_extra and args.mode == 0:
