@@ -142,9 +142,19 @@ def run_ours(args):
     from paper_2012_14792_b200 import workloads as wl
 
     rank, world, local = dist_env()
+    # SLICECRAFT_BENCH_BACKEND=gloo (test only): exercise the multi-rank path
+    # with more ranks than GPUs -- ranks share devices round-robin, their
+    # kernels never wait on one another (frame sharding has no data-path
+    # collective), and only the timing max crosses ranks, on the host
+    backend = os.environ.get("SLICECRAFT_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     w = wl.WORKLOADS[args.config]
     F = w.frames
     g = w.grid()
@@ -177,7 +187,7 @@ def run_ours(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
