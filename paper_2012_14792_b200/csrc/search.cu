@@ -201,12 +201,79 @@ __global__ void k_column_bounds(const uint32_t* __restrict__ rt, int fpw, int fr
   column_bounds(rt, fpw, f, rows, xw * nyh, rmax, lbr + off, lbm + off, (size_t)fpw);
 }
 
+// One block per column (x0, w): the column's rectangle keys of every frame of
+// the group are staged in shared memory ([yh][fpw], coalesced) and the DP over
+// rows runs with one thread per (row end y, frame), a barrier per run count r
+// -- the same recurrence as column_bounds() (search_walk.cuh), parallel over y.
+__global__ void k_column_bounds_blk(const uint32_t* __restrict__ rt, int fpw, int frames_in_group,
+                                   int rows, int rmax, int rstride, uint32_t* lbr,
+                                   uint32_t* lbm) {
+  extern __shared__ uint32_t cb_sm[];
+  const int xw = blockIdx.x;
+  const int nyh = rows * (rows + 1) / 2;
+  const int ny = (rows + 1) * fpw;
+  uint32_t* tab = cb_sm;          // [nyh][fpw]
+  uint32_t* prev = tab + (size_t)nyh * fpw;  // [rows + 1][fpw]
+  uint32_t* cur = prev + ny;
+  uint32_t* rmin = cur + ny;      // [fpw] running minimum over r
+  const uint32_t INF = kKeyInf;
+  const uint32_t* src = rt + (size_t)xw * nyh * fpw;
+  for (int i = threadIdx.x; i < nyh * fpw; i += blockDim.x) tab[i] = src[i];
+  for (int i = threadIdx.x; i < ny; i += blockDim.x) prev[i] = i < fpw ? 0u : INF;
+  for (int i = threadIdx.x; i < fpw; i += blockDim.x) rmin[i] = INF;
+  __syncthreads();
+  const size_t out0 = (size_t)xw * rstride * fpw;
+  for (int i = threadIdx.x; i < frames_in_group; i += blockDim.x) {
+    lbr[out0 + i] = INF;
+    lbm[out0 + i] = INF;
+  }
+  for (int r = 1; r <= rmax; ++r) {
+    for (int i = threadIdx.x; i < ny; i += blockDim.x) {
+      const int y = i / fpw, f = i - y * fpw;
+      uint32_t best = INF;
+      for (int y0 = r - 1; y0 < y; ++y0) {
+        const uint32_t p = prev[y0 * fpw + f];
+        if (p == INF) continue;
+        const uint32_t v = tab[yh_of(rows, y0, y - y0) * fpw + f];
+        const uint32_t m = p > v ? p : v;
+        best = m < best ? m : best;
+      }
+      cur[i] = best;
+    }
+    __syncthreads();
+    for (int f = threadIdx.x; f < frames_in_group; f += blockDim.x) {
+      const uint32_t c = cur[rows * fpw + f];
+      const uint32_t m = c < rmin[f] ? c : rmin[f];
+      rmin[f] = m;
+      lbr[out0 + (size_t)r * fpw + f] = c;
+      lbm[out0 + (size_t)r * fpw + f] = m;
+    }
+    uint32_t* t = prev;
+    prev = cur;
+    cur = t;
+    __syncthreads();
+  }
+}
+
 void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int cols, int rows,
                           int rmax, int rstride, uint32_t* lbr, uint32_t* lbm, cudaStream_t st) {
   const int nxw = cols * (cols + 1) / 2;
-  const int threads = 128, total = nxw * fpw;
-  k_column_bounds<<<(total + threads - 1) / threads, threads, 0, st>>>(
-      rt, fpw, frames_in_group, cols, rows, rmax, rstride, lbr, lbm);
+  const size_t nyh = (size_t)rows * (rows + 1) / 2;
+  const size_t smem = (nyh * fpw + 2 * (size_t)(rows + 1) * fpw + fpw) * sizeof(uint32_t);
+  if (smem <= 96 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      SCB_CUDA(cudaFuncSetAttribute(k_column_bounds_blk,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+      attr = true;
+    }
+    k_column_bounds_blk<<<nxw, 256, smem, st>>>(rt, fpw, frames_in_group, rows, rmax, rstride,
+                                                lbr, lbm);
+  } else {  // tall grids: one thread per (column, frame)
+    const int threads = 128, total = nxw * fpw;
+    k_column_bounds<<<(total + threads - 1) / threads, threads, 0, st>>>(
+        rt, fpw, frames_in_group, cols, rows, rmax, rstride, lbr, lbm);
+  }
   SCB_CUDA(cudaGetLastError());
 }
 
