@@ -18,6 +18,8 @@ Contents
   configs.json     BASELINE configs on their real synthetic inputs: cfg1 (all),
                    cfg2 (POC 1..4), cfg3 (POC 1): two_step_partition outputs,
                    with a hash of the estimate maps / records that were used.
+  configs_lambda.json  the same inputs with lambda in {0.1, 0.3} (SURVEY.md
+                   §8d): cfg1 (POC 1), cfg2 (POC 1..2), cfg3 (POC 1).
 """
 from __future__ import annotations
 
@@ -123,9 +125,9 @@ def search_small(r: Ref, n_cases: int = 200) -> list:
     return cases
 
 
-def configs(r: Ref) -> dict:
+def configs(r: Ref, lambdas=(0.0,), plan=None) -> dict:
     out = {}
-    plan = {1: [1], 2: [1, 2, 3, 4], 3: [1]}
+    plan = plan or {1: [1], 2: [1, 2, 3, 4], 3: [1]}
     for ci, pocs in plan.items():
         w = wl.WORKLOADS[ci]
         F = max(pocs)
@@ -136,21 +138,25 @@ def configs(r: Ref) -> dict:
         htls = [m.temporal_layer for m in tr.history_maps]
         res = []
         for p in pocs:
-            t0 = time.time()
             st, rec = r.ctu_stats(luma[p - 1].astype(np.uint16), w.bit_depth, w.ctu)
-            # history visible to frame p: POCs 0..p-1
-            st, o = r.two_step(w.width, w.height, w.ctu, 16, maps[:p], hpocs[:p], htls[:p], rec, p,
-                               w.n_slices, 0.0, 3.0, 0, w.max_tile_cols)
-            assert st == 0, r.err()
-            res.append({"poc": p, "records_hash": h(rec), "est_hash": h(tr.est[p - 1]),
-                        "records": rec.tolist() if ci == 1 else None,
-                        "t_min": o.t_min_us, "t_best": o.t_best_us, "sse_best": o.sse_best,
-                        "best": o.best.rects(), "best_widths": o.best.widths(),
-                        "candidates_step1": o.candidates_step1,
-                        "candidates_step2": o.candidates_step2,
-                        "est_source": o.est_source, "est_source_poc": o.est_source_poc,
-                        "ref_seconds": time.time() - t0})
-            print(f"cfg{ci} poc {p}: {time.time() - t0:.1f}s", flush=True)
+            for lam in lambdas:
+                t0 = time.time()
+                # history visible to frame p: POCs 0..p-1
+                st, o = r.two_step(w.width, w.height, w.ctu, 16, maps[:p], hpocs[:p], htls[:p],
+                                   rec, p, w.n_slices, lam, 3.0, 0, w.max_tile_cols)
+                assert st == 0, r.err()
+                fr = {"poc": p, "records_hash": h(rec), "est_hash": h(tr.est[p - 1]),
+                      "records": rec.tolist() if ci == 1 else None,
+                      "t_min": o.t_min_us, "t_best": o.t_best_us, "sse_best": o.sse_best,
+                      "best": o.best.rects(), "best_widths": o.best.widths(),
+                      "candidates_step1": o.candidates_step1,
+                      "candidates_step2": o.candidates_step2,
+                      "est_source": o.est_source, "est_source_poc": o.est_source_poc,
+                      "ref_seconds": time.time() - t0}
+                if lam != 0.0 or len(lambdas) > 1:
+                    fr["lambda"] = lam
+                res.append(fr)
+                print(f"cfg{ci} poc {p} lambda {lam}: {time.time() - t0:.1f}s", flush=True)
         out[str(ci)] = {"name": w.name, "frames": res}
     return out
 
@@ -238,6 +244,10 @@ def main():
     if "configs" in which:
         with open(os.path.join(OUT, "configs.json"), "w") as f:
             json.dump(configs(r), f, indent=1)
+    if "lambda" in which:
+        with open(os.path.join(OUT, "configs_lambda.json"), "w") as f:
+            json.dump(configs(r, lambdas=(0.1, 0.3), plan={1: [1], 2: [1, 2], 3: [1]}), f,
+                      indent=1)
 
 
 if __name__ == "__main__":

@@ -235,6 +235,68 @@ def test_baseline_configs_vs_reference_golden(part, monkeypatch, ci, m):
     assert wl  # noqa
 
 
+@pytest.mark.parametrize("m", ["exhaustive", "pruned"])
+@pytest.mark.parametrize("ci", [1, 2, 3])
+def test_baseline_configs_lambda_vs_reference_golden(part, monkeypatch, ci, m):
+    """lambda in {0.1, 0.3} on cfg1 (POC 1), cfg2 (POC 1..2) and
+    cfg3 (POC 1) against the reference's own two_step_partition outputs."""
+    import hashlib
+    mode = _mode(monkeypatch, m)
+    from paper_2012_14792_b200 import RECORD_DTYPE
+    from paper_2012_14792_b200.partitioner import Partition
+    gold = json.load(open(os.path.join(GOLDEN, "configs_lambda.json")))[str(ci)]
+    F = max(fr["poc"] for fr in gold["frames"])
+    w, tr, luma = _config_inputs(ci, F)
+    g = w.grid()
+    for lam in sorted({fr["lambda"] for fr in gold["frames"]}):
+        rec = np.zeros((F, g.cell_count()), dtype=RECORD_DTYPE)
+        res = part.partition_frames(g, luma, tr.est, w.cfg(mode=mode, lambda_=lam),
+                                    records_out=rec)
+        for fr in gold["frames"]:
+            if fr["lambda"] != lam:
+                continue
+            p = fr["poc"]
+            r3 = np.ascontiguousarray(_rec3(rec[p - 1]), dtype=np.uint64)
+            assert hashlib.sha256(r3.tobytes()).hexdigest()[:16] == fr["records_hash"]
+            r = res[p - 1]
+            ctx = (ci, p, lam, m)
+            assert r.t_min_us == fr["t_min"], ctx
+            assert r.t_best_us == fr["t_best"], ctx
+            assert r.sse_best == fr["sse_best"], ctx
+            assert Partition.from_layout(g, r.best).rects() == [tuple(x) for x in fr["best"]], ctx
+            assert r.candidates_step1 == fr["candidates_step1"], ctx
+            assert r.candidates_step2 == fr["candidates_step2"], ctx
+
+
+@pytest.mark.parametrize("m", ["exhaustive", "pruned"])
+@pytest.mark.parametrize("ci,frames", [(1, 1), (2, 2), (3, 1)])
+def test_baseline_configs_covering_vs_oracle(part, oracle, monkeypatch, ci, frames, m):
+    """The covering family (sum of widths = cols) on the
+    cfg1-3 inputs, lambda 0 and 0.3, against the C oracle (pinned to the
+    reference's primitives in test_oracle_pin)."""
+    mode = _mode(monkeypatch, m)
+    from paper_2012_14792_b200 import RECORD_DTYPE
+    from paper_2012_14792_b200.partitioner import Partition
+    w, tr, luma = _config_inputs(ci, frames)
+    g = w.grid()
+    for lam in (0.0, 0.3):
+        rec = np.zeros((frames, g.cell_count()), dtype=RECORD_DTYPE)
+        res = part.partition_frames(g, luma, tr.est, w.cfg(mode=mode, lambda_=lam, coverage=1),
+                                    records_out=rec)
+        for f in range(frames):
+            st, e = oracle.search(w.width, w.height, w.ctu, tr.est[f], _rec3(rec[f]), w.n_slices,
+                                  lam, 3.0, w.max_tile_cols, 1, 3)
+            assert st == 0
+            r = res[f]
+            ctx = (ci, f, lam, m)
+            assert r.t_min_us == e.t_min_us, ctx
+            assert r.t_best_us == e.t_best_us and r.sse_best == e.sse_best, ctx
+            assert Partition.from_layout(g, r.best).rects() == e.best.slices(g.rows), ctx
+            assert r.candidates_step1 == e.candidates_step1, ctx
+            assert r.candidates_step2 == e.candidates_step2, ctx
+            assert sum(Partition.from_layout(g, r.best).col_widths) == g.cols, ctx
+
+
 def test_cfg2_all_frames_vs_oracle(part, oracle):
     """All 64 frames of config 2 (two GPU frame groups) against the C oracle."""
     w, tr, luma = _config_inputs(2, 64)
