@@ -39,14 +39,16 @@ namespace scb {
 #ifndef SCB_SEARCH_BLOCK
 #define SCB_SEARCH_BLOCK 256
 #endif
-// Exhaustive step 1 (the headline walk, warp-uniform, ~88 registers): 64-thread
-// blocks so the register file, not the block granularity, sets the warps per
-// SM (11 blocks = 22 warps vs 16 with 256-thread blocks).
+// Exhaustive step 1 (the headline walk, warp-uniform): 64-thread blocks, at
+// most 8 per SM by launch bound, so ptxas keeps 96 registers and the register
+// file sets the residency at 10 blocks = 20 warps/SM.  Measured on cfg3
+// (DESIGN.md §3.5): 5.37 ms vs 5.72 (256 x 2, 16 warps), 5.64 (128 x 4),
+// 5.81 (64 x 10 -> 86 registers), 6.22 (64 x 12 -> 77), 6.45 (32 x 21 -> 70).
 #ifndef SCB_SEARCH_BLOCK1
-#define SCB_SEARCH_BLOCK1 256
+#define SCB_SEARCH_BLOCK1 64
 #endif
 #ifndef SCB_SEARCH_MINB1
-#define SCB_SEARCH_MINB1 2
+#define SCB_SEARCH_MINB1 8
 #endif
 template <int STEP, bool PRUNE>
 struct SearchShape {
@@ -67,10 +69,12 @@ size_t search_tables_bytes(int cols, int rows, int n) {
 }
 size_t search_smem_bytes(int cols, int rows, int n, int step, bool prune) {
   size_t b = search_tables_bytes(cols, rows, n);
-  // per warp: 2 * n level records + 32 lanes x n Pin keys
+  // per warp: 2 * n level records, 32 lanes x n Pin keys, the uniform arrays
   if (!prune)
-    b = (b + 15) / 16 * 16 + (size_t)(search_block_threads(step, prune) / 32) * std::max(n, 1) *
-                                 (2 * sizeof(Lvl) + 32 * sizeof(uint32_t));
+    b = (b + 15) / 16 * 16 +
+        (size_t)(search_block_threads(step, prune) / 32) *
+            ((size_t)std::max(n, 1) * (2 * sizeof(Lvl) + 32 * sizeof(uint32_t)) +
+             kUniInts * sizeof(int));
   return b;
 }
 
@@ -122,12 +126,14 @@ k_search(SearchArgs a) {
     Lvl* const lvl0 = reinterpret_cast<Lvl*>(g_dyn + (tab_words + 3) / 4 * 4);
     const int nwarps = blockDim.x >> 5, wib = threadIdx.x >> 5;
     e.lvl = lvl0 + (size_t)wib * 2 * lvl_cap;
-    e.pin = reinterpret_cast<tkey*>(lvl0 + (size_t)nwarps * 2 * lvl_cap) +
-            (size_t)wib * 32 * lvl_cap + (threadIdx.x & 31);
+    tkey* const pin0 = reinterpret_cast<tkey*>(lvl0 + (size_t)nwarps * 2 * lvl_cap);
+    e.pin = pin0 + (size_t)wib * 32 * lvl_cap + (threadIdx.x & 31);
+    e.uni = reinterpret_cast<int*>(pin0 + (size_t)nwarps * 32 * lvl_cap) + (size_t)wib * kUniInts;
     e.lvl_cap = lvl_cap;
   } else {
     e.lvl = nullptr;
     e.pin = nullptr;
+    e.uni = nullptr;
     e.lvl_cap = 0;
   }
   e.rt = a.rt;

@@ -71,6 +71,11 @@ SCB_HD tkey umin3(tkey a, tkey b, tkey c) {
   return m < c ? m : c;
 }
 
+// Warp-uniform DFS arrays of the exhaustive walk, one copy per warp in shared
+// memory on the GPU (int offsets; curH bytes at kUniH).
+constexpr int kUniW = 0, kUniR = 16, kUniX0 = 32, kUniWL = 49, kUniWH = 66, kUniRL = 83,
+              kUniRH = 99, kUniSL = 115, kUniH = 131, kUniInts = 148;  // 592 B
+
 // one 16-byte record of the heights DFS (a single 128-bit local access)
 struct alignas(16) Lvl {
   int32_t a, b, c, d;
@@ -132,6 +137,7 @@ struct WalkEnv {
   // memory (which crowded L1); only the per-frame Pin stays per lane.
   Lvl* lvl;
   tkey* pin;  // this lane's Pin slots: pin[l * 32]
+  int* uni;   // this warp's uniform DFS arrays (kUni* offsets)
   int lvl_cap;
   // pruned mode: split_g warps share each work item; the subtrees below
   // level split_depth of the heights DFS (or a whole skeleton, if it has
@@ -288,8 +294,27 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   if (PRUNE) st.tie = e.split_g > 1 && item == st.best_item;
 
   // warp-uniform DFS state (identical in every lane of the warp)
-  int W[SC_MAX_COLS], R[SC_MAX_COLS], X0[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
-  uint8_t curH[SC_MAX_SLICES];
+  int W_[SC_MAX_COLS], R_[SC_MAX_COLS], X0_[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
+  int WL_[SC_MAX_COLS + 1], WH_[SC_MAX_COLS + 1], RL_[SC_MAX_COLS], RH_[SC_MAX_COLS],
+      SL_[SC_MAX_COLS];
+  uint8_t curH_[SC_MAX_SLICES];
+  // exhaustive walks on the GPU: these warp-uniform DFS arrays live once per
+  // warp in shared memory (WalkEnv::uni, layout kUni*); pruned walks and the
+  // host emulator keep them per lane
+#ifdef __CUDA_ARCH__
+  constexpr bool kUniform = !PRUNE;
+#else
+  constexpr bool kUniform = false;
+#endif
+  int* const W = kUniform ? e.uni + kUniW : W_;
+  int* const R = kUniform ? e.uni + kUniR : R_;
+  int* const X0 = kUniform ? e.uni + kUniX0 : X0_;
+  int* const WL = kUniform ? e.uni + kUniWL : WL_;
+  int* const WH = kUniform ? e.uni + kUniWH : WH_;
+  int* const RL = kUniform ? e.uni + kUniRL : RL_;
+  int* const RH = kUniform ? e.uni + kUniRH : RH_;
+  int* const SL = kUniform ? e.uni + kUniSL : SL_;
+  uint8_t* const curH = kUniform ? reinterpret_cast<uint8_t*>(e.uni + kUniH) : curH_;
   // pruned walks: heights-DFS state per level in local arrays
   uint8_t Lcol[kMaxLevels], Lrun[kMaxLevels], Ly0[kMaxLevels], Lh[kMaxLevels], Lhi[kMaxLevels];
   int32_t Amin[kMaxLevels], Amax[kMaxLevels], Lbase[kMaxLevels];
@@ -451,7 +476,6 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   //      column windows (r <= n-c+1): prefixes whose hulls do not intersect
   //      cannot complete and are skipped.
   const int rmax_c = imin(e.n - c + 1, rows);
-  int WL[SC_MAX_COLS + 1], WH[SC_MAX_COLS + 1];
   tkey PW[SC_MAX_COLS + 1];  // pruned mode: max of the columns' lower bounds
   X0[0] = 0;
   WL[0] = 1;
@@ -476,6 +500,9 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     if (!fixed_widths) {
       bool got = false;
       while (true) {
+        // uniform arrays: no lane may still read the previous skeleton's
+        // state (a best update's snapshot) when they change
+        if (kUniform) SCB_SYNCWARP();
         const int maxw = cols - X0[pos] - (c - pos - 1);
         int wv;
         if (e.coverage && pos == c - 1) wv = (W[pos] == 0) ? maxw : maxw + 1;
@@ -513,7 +540,6 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     //      I(w, r) = [aneed[w*ceil(rows/r)], w*floor(rows/r)] intersect; I
     //      slides down as r grows, so the feasible r of a position form one
     //      contiguous range.
-    int RL[SC_MAX_COLS], RH[SC_MAX_COLS], SL[SC_MAX_COLS];
     tkey PR[SC_MAX_COLS + 1];  // pruned mode: widths bound, tightened per exact r
     PR[0] = PRUNE ? PW[c] : 0;
     int rp = 0;
@@ -522,6 +548,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     SL[0] = e.n;
     R[0] = imax(1, e.n - (c - 1) * rows) - 1;
     while (true) {
+      if (kUniform) SCB_SYNCWARP();
       SCB_STAT(runs_steps);
       const int after = c - 1 - rp;
       const int rhi = imin(rows, SL[rp] - after);
