@@ -39,22 +39,22 @@ namespace scb {
 #ifndef SCB_SEARCH_BLOCK
 #define SCB_SEARCH_BLOCK 256
 #endif
-// Exhaustive step 1 (the headline walk, warp-uniform): 64-thread blocks, at
-// most 8 per SM by launch bound, so ptxas keeps 96 registers and the register
-// file sets the residency at 10 blocks = 20 warps/SM.  Measured on cfg3
-// (DESIGN.md §3.5): 5.37 ms vs 5.72 (256 x 2, 16 warps), 5.64 (128 x 4),
-// 5.81 (64 x 10 -> 86 registers), 6.22 (64 x 12 -> 77), 6.45 (32 x 21 -> 70).
+// Exhaustive step 1 (the headline walk, warp-uniform): 64-thread blocks under
+// a register cap (__maxnreg__) instead of a blocks-per-SM launch bound, with
+// which ptxas settles at 96 registers, so the register file holds 10 blocks =
+// 20 warps/SM.  Measured on cfg3, step-1 ms by cap ->
+// registers: 96 -> 86: 5.12, 100 -> 88: 5.06, 104 -> 92: 4.98, 112 -> 96:
+// 5.00, 128 -> 96: 4.96 (256-thread blocks, 16 warps/SM: +7 %).
 #ifndef SCB_SEARCH_BLOCK1
 #define SCB_SEARCH_BLOCK1 64
 #endif
-#ifndef SCB_SEARCH_MINB1
-#define SCB_SEARCH_MINB1 8
+#ifndef SCB_SEARCH_REGS1
+#define SCB_SEARCH_REGS1 128
 #endif
 template <int STEP, bool PRUNE>
 struct SearchShape {
   static constexpr bool kHead = STEP == 1 && !PRUNE;
   static constexpr int kBlock = kHead ? SCB_SEARCH_BLOCK1 : SCB_SEARCH_BLOCK;
-  static constexpr int kMinBlocks = kHead ? SCB_SEARCH_MINB1 : SCB_SEARCH_MINB;
 };
 int search_block_threads(int step, bool prune) {
   return (step == 1 && !prune) ? SCB_SEARCH_BLOCK1 : SCB_SEARCH_BLOCK;
@@ -79,9 +79,7 @@ size_t search_smem_bytes(int cols, int rows, int n, int step, bool prune) {
 }
 
 template <int FPW, int STEP, bool PRUNE>
-__global__ void __launch_bounds__(SearchShape<STEP, PRUNE>::kBlock,
-                                  SearchShape<STEP, PRUNE>::kMinBlocks)
-k_search(SearchArgs a) {
+__device__ __forceinline__ void search_body(const SearchArgs& a) {
   // shared-memory tables (search_walk.cuh): g_dyn = bmax|aneed interleaved
   // [2A], mstar [(cols+1)(rows+1)], ilo [(cols+1) * rstride]; static magic,
   // ybase, rq
@@ -191,6 +189,23 @@ k_search(SearchArgs a) {
   unsigned long long sc = st.scored;
   for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
   if (lane == 0 && sc) atomicAdd(a.scored_out, sc);
+}
+
+// The headline walk (exhaustive step 1) under a register cap that keeps 10
+// blocks of 2 warps resident; the other walks under a plain launch bound.
+template <int FPW>
+__global__ void __maxnreg__(SCB_SEARCH_REGS1)
+    k_search_head(SearchArgs a) {
+  search_body<FPW, 1, false>(a);
+}
+template <int FPW, int STEP, bool PRUNE>
+__global__ void __launch_bounds__(SCB_SEARCH_BLOCK, SCB_SEARCH_MINB) k_search(SearchArgs a) {
+  search_body<FPW, STEP, PRUNE>(a);
+}
+template <int FPW, int STEP, bool PRUNE>
+constexpr void (*search_kernel())(SearchArgs) {
+  if constexpr (STEP == 1 && !PRUNE) return k_search_head<FPW>;
+  else return k_search<FPW, STEP, PRUNE>;
 }
 
 // ---- pruned mode: per-frame column lower bounds (search_walk.cuh) -------------
@@ -382,22 +397,22 @@ template <int FPW, int STEP>
 static void launch_fpw(const SearchArgs& a, int blocks, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    SCB_CUDA(cudaFuncSetAttribute(k_search<FPW, STEP, false>,
+    SCB_CUDA(cudaFuncSetAttribute(search_kernel<FPW, STEP, false>(),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    SCB_CUDA(cudaFuncSetAttribute(k_search<FPW, STEP, true>,
+    SCB_CUDA(cudaFuncSetAttribute(search_kernel<FPW, STEP, true>(),
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     attr = true;
   }
   if (a.prune)
-    k_search<FPW, STEP, true><<<blocks, SearchShape<STEP, true>::kBlock, smem, st>>>(a);
+    search_kernel<FPW, STEP, true>()<<<blocks, SearchShape<STEP, true>::kBlock, smem, st>>>(a);
   else
-    k_search<FPW, STEP, false><<<blocks, SearchShape<STEP, false>::kBlock, smem, st>>>(a);
+    search_kernel<FPW, STEP, false>()<<<blocks, SearchShape<STEP, false>::kBlock, smem, st>>>(a);
 }
 
 int search_blocks_per_sm(int fpw, int step, bool prune, size_t smem) {
   int nb = 0;
 #define OCC1(F, S, P)                                                                        \
-  SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_search<F, S, P>,           \
+  SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, search_kernel<F, S, P>(),           \
                                                          SearchShape<S, P>::kBlock, smem))
 #define OCC(F)                                                                               \
   if (fpw == F) {                                                                            \

@@ -74,7 +74,8 @@ SCB_HD tkey umin3(tkey a, tkey b, tkey c) {
 // Warp-uniform DFS arrays of the exhaustive walk, one copy per warp in shared
 // memory on the GPU (int offsets; curH bytes at kUniH).
 constexpr int kUniW = 0, kUniR = 16, kUniX0 = 32, kUniWL = 49, kUniWH = 66, kUniRL = 83,
-              kUniRH = 99, kUniSL = 115, kUniH = 131, kUniInts = 148;  // 592 B
+              kUniRH = 99, kUniSL = 115, kUniH = 131, kUniSMN = 147, kUniSMX = 164,
+              kUniInts = 184;  // 736 B
 
 // one 16-byte record of the heights DFS (a single 128-bit local access)
 struct alignas(16) Lvl {
@@ -296,7 +297,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   // warp-uniform DFS state (identical in every lane of the warp)
   int W_[SC_MAX_COLS], R_[SC_MAX_COLS], X0_[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
   int WL_[SC_MAX_COLS + 1], WH_[SC_MAX_COLS + 1], RL_[SC_MAX_COLS], RH_[SC_MAX_COLS],
-      SL_[SC_MAX_COLS];
+      SL_[SC_MAX_COLS], SMN_[SC_MAX_COLS + 1], SMX_[SC_MAX_COLS + 1];
   uint8_t curH_[SC_MAX_SLICES];
   // exhaustive walks on the GPU: these warp-uniform DFS arrays live once per
   // warp in shared memory (WalkEnv::uni, layout kUni*); pruned walks and the
@@ -315,6 +316,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   int* const RH = kUniform ? e.uni + kUniRH : RH_;
   int* const SL = kUniform ? e.uni + kUniSL : SL_;
   uint8_t* const curH = kUniform ? reinterpret_cast<uint8_t*>(e.uni + kUniH) : curH_;
+  int* const SMN = kUniform ? e.uni + kUniSMN : SMN_;
+  int* const SMX = kUniform ? e.uni + kUniSMX : SMX_;
   // pruned walks: heights-DFS state per level in local arrays
   uint8_t Lcol[kMaxLevels], Lrun[kMaxLevels], Ly0[kMaxLevels], Lh[kMaxLevels], Lhi[kMaxLevels];
   int32_t Amin[kMaxLevels], Amax[kMaxLevels], Lbase[kMaxLevels];
@@ -540,20 +543,45 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     //      I(w, r) = [aneed[w*ceil(rows/r)], w*floor(rows/r)] intersect; I
     //      slides down as r grows, so the feasible r of a position form one
     //      contiguous range.
+    //      Suffix run-count bounds: column j can only take r runs whose
+    //      window meets the widths hull [WL[c], WH[c]] (r in [r1_j, r2_j],
+    //      the window only shrinks from there), so position rp only tries r
+    //      with SL - r in [SMN[rp+1], SMX[rp+1]] (sums of r1 / r2 over the
+    //      columns after it); a width vector whose sums miss n has no
+    //      skeleton.  Skipped r lead to no skeleton: the walk is unchanged.
+    bool dead = false;
+    SMN[c] = 0;
+    SMX[c] = 0;
+#pragma unroll 1
+    for (int j = c - 1; j >= 0 && !dead; --j) {
+      const int w = W[j];
+      int r1 = 0, r2 = 0;
+#pragma unroll 1
+      for (int r = 1; r <= rmax_c; ++r) {
+        if (w * SCB_RQ(r) < WL[c]) break;  // every larger r is lower still
+        if (SCB_ILO(w * e.rstride + r) <= WH[c]) {
+          if (!r1) r1 = r;
+          r2 = r;
+        }
+      }
+      dead = r1 == 0;
+      SMN[j] = SMN[j + 1] + r1;
+      SMX[j] = SMX[j + 1] + r2;
+    }
+    dead = dead || SMN[0] > e.n || SMX[0] < e.n;
     tkey PR[SC_MAX_COLS + 1];  // pruned mode: widths bound, tightened per exact r
     PR[0] = PRUNE ? PW[c] : 0;
     int rp = 0;
     RL[0] = 1;
     RH[0] = e.max_area;
     SL[0] = e.n;
-    R[0] = imax(1, e.n - (c - 1) * rows) - 1;
+    R[0] = dead ? rows : imax(1, e.n - (c - 1) * rows) - 1;  // dead: the loop ends at once
     while (true) {
       if (kUniform) SCB_SYNCWARP();
       SCB_STAT(runs_steps);
-      const int after = c - 1 - rp;
-      const int rhi = imin(rows, SL[rp] - after);
+      const int rhi = imin(rows, SL[rp] - SMN[rp + 1]);
       const int w = W[rp];
-      int r = R[rp] + 1, lo = 0, hi = 0;
+      int r = imax(R[rp] + 1, SL[rp] - SMX[rp + 1]), lo = 0, hi = 0;
       bool found = false;
       for (; r <= rhi; ++r) {
         lo = SCB_ILO(w * e.rstride + r);
