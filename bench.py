@@ -266,7 +266,7 @@ def run_ours(args):
             # dominant kernel: the step-1 walk (every candidate's time); the
             # step-1 phase is that launch plus its few-us finalize
             ach = p["warp_inst_step1"] / (s1_us * 1e-6) / 1e9
-            issue = {"bound": "alu", "kernel": "k_search<FPW,1> (step-1 walk)",
+            issue = {"bound": "alu", "kernel": "k_search_head<FPW> (exhaustive step-1 walk)",
                      "achieved": round(ach, 2), "peak": round(peak, 2),
                      "unit": "Gwarp-inst/s", "frac": round(ach / peak, 4),
                      "traffic": p.get("dram_bytes_per_launch"),

@@ -66,6 +66,7 @@ SCB_HD uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
 typedef uint32_t tkey;
 constexpr tkey kKeyInf = 0xffffffffu;
 SCB_HD tkey kmax(tkey a, tkey b) { return a > b ? a : b; }
+SCB_HD tkey kmin(tkey a, tkey b) { return a < b ? a : b; }
 SCB_HD tkey umin3(tkey a, tkey b, tkey c) {
   const tkey m = a < b ? a : b;
   return m < c ? m : c;
@@ -904,10 +905,12 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
               // min-reduction; only a chunk that can beat the lane's best
               // replays its heights in order through score()
               const int nh = (hi - lo - slot) / J + 1;
-              tkey m = kKeyInf;
-              const tkey* p = p0;
+              // first four heights outside the loop (most leaves have <= 4)
+              tkey m = umin3(p0[0], nh > 1 ? p0[32] : kKeyInf, nh > 2 ? p0[64] : kKeyInf);
+              m = nh > 3 ? kmin(m, p0[96]) : m;
+              const tkey* p = p0 + 4 * 32;
   #pragma unroll 1
-              for (int k = 0; k < nh; k += 4, p += 4 * 32) {
+              for (int k = 4; k < nh; k += 4, p += 4 * 32) {
                 const tkey v0 = p[0];
                 const tkey v1 = k + 1 < nh ? p[32] : kKeyInf;
                 const tkey v2 = k + 2 < nh ? p[64] : kKeyInf;
