@@ -176,7 +176,11 @@ Plan* get_plan(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int maxc
   Plan* p = new Plan();
   p->key = key;
   const bool covering = cfg.coverage == SC_COVERAGE_COVERING;
-  p->items = make_items(g.cols, maxc, covering, (size_t)ctx->sm_count * 16 * 32);
+  // work-item granularity: at least SLICECRAFT_B200_ITEMS_PER_SM (512) width
+  // prefixes per SM (make_items deepens the prefixes until there are)
+  const char* ips = getenv("SLICECRAFT_B200_ITEMS_PER_SM");
+  const size_t per_sm = ips ? (size_t)std::max(1, atoi(ips)) : 512;
+  p->items = make_items(g.cols, maxc, covering, (size_t)ctx->sm_count * per_sm);
   // seed phase of the pruned mode: the items of the smallest column count(s)
   p->seed_items = 0;
   for (const WorkItem& it : p->items) {
