@@ -501,6 +501,51 @@ def test_errors(part):
     assert e.value.kind == "FormatError"
 
 
+@pytest.mark.parametrize("m", MODES)
+def test_edge_shapes_vs_oracle(part, oracle, monkeypatch, m):
+    """Edge shapes: one cell; one column of 64 rows cut into the maximum 64
+    slices (63-level heights DFS); a single-row grid; partial border CTUs; a
+    ragged frame batch (35 frames = one full 32-frame group + 3 in the next)."""
+    from paper_2012_14792_b200 import CtuGrid, SearchConfig
+    from paper_2012_14792_b200.partitioner import Partition
+    mode = _mode(monkeypatch, m)
+    rng = np.random.default_rng(77)
+    cases = [((64, 64, 64), 1, 0, 1), ((64, 64 * 64, 64), 64, 0, 1),
+             ((64, 18 * 64, 64), 12, 1, 2), ((12 * 64, 64, 64), 5, 0, 3),
+             ((5 * 64 - 17, 4 * 64 - 33, 64), 6, 0, 2), ((6 * 64, 5 * 64, 64), 5, 4, 35)]
+    for (W, H, ctu), n, mc, F in cases:
+        g = CtuGrid.make(W, H, ctu)
+        est = rng.lognormal(0, 0.5, size=(F, g.cell_count()))
+        luma = rng.integers(0, 1024, size=(F, H, W)).astype(np.uint16)
+        rec = part.ctu_stats_batch(luma, ctu)
+        cfg = SearchConfig(n_slices=n, lambda_=0.2, k_area=3.0, max_tile_cols=mc, mode=mode)
+        got = part.two_step_batch(g, est, rec, cfg)
+        for f in range(F):
+            st, e = oracle.search(W, H, ctu, est[f], _rec3(rec[f]), n, 0.2, 3.0, mc, 0, 3)
+            ctx = (W, H, n, mc, F, f, m)
+            assert st == 0, ctx
+            o = got[f]
+            assert o.t_min_us == e.t_min_us and o.candidates_step1 == e.candidates_step1, ctx
+            assert o.argmin.rects() == e.argmin1.slices(g.rows), ctx
+            assert o.t_best_us == e.t_best_us and o.sse_best == e.sse_best, ctx
+            assert o.best.rects() == e.best.slices(g.rows), ctx
+            assert o.candidates_step2 == e.candidates_step2, ctx
+
+
+def test_size_limits(part):
+    """Requests beyond the compiled limits fail with SizeError,
+    the reference's own checks keep their classes."""
+    from paper_2012_14792_b200 import CtuGrid, SearchConfig, SlicecraftError
+    g = CtuGrid.make(64, 65 * 64, 64)  # 1 x 65 cells
+    with pytest.raises(SlicecraftError) as e:
+        part.min_time_search_batch(g, np.ones((1, 65)), SearchConfig(n_slices=65))
+    assert e.value.kind == "SizeError"
+    g = CtuGrid.make(256 * 64, 64, 64)  # 256 columns
+    with pytest.raises(SlicecraftError) as e:
+        part.min_time_search_batch(g, np.ones((1, 256)), SearchConfig(n_slices=2))
+    assert e.value.kind == "SizeError"
+
+
 # ---- UniformOnly family and partition evaluation (SURVEY.md §8a a9, a18) -----------
 def _uniform_gold():
     return json.load(open(os.path.join(GOLDEN, "uniform.json")))
