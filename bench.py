@@ -19,7 +19,9 @@ e2e    = the same metric through the public C-ABI call with HOST (pinned)
 Multi-GPU (torchrun): frames are independent once estimated,
 so every rank partitions its own batch (POCs offset by rank) -- weak scaling,
 no data-path collective; the timed region is barrier-bracketed and the max
-over ranks is reported.
+over ranks is reported.  --shard candidates instead splits each frame's
+candidate space over the ranks (strong scaling, cfg4/cfg5 style): one
+sc_shard_best record per frame is all-gathered after each step.
 
 --impl reference runs the UNMODIFIED reference CPU path (oracle/_ref, built
 from /root/reference; the C oracle port when that is absent) on the host
@@ -331,6 +333,132 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_candidates(args):
+    """--shard candidates: every rank holds the SAME frames and walks the work
+    items rank, rank + N, ... of each frame's candidate space
+    (sc_ctx_set_shard); after each step the ranks exchange one sc_shard_best
+    record per frame (all-gather, NCCL over NVLink) and sc_shard_merge picks
+    the first-in-order winner, so step 2 runs under the global t_min.  Total
+    work is fixed as N grows: strong scaling.  One step = K1 over the batch +
+    step 1 + exchange + step 2 + exchange, timed with CUDA events between
+    barriers, max over ranks."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+    from paper_2012_14792_b200 import Partitioner, lib
+    from paper_2012_14792_b200._abi import SearchResult, check
+    from paper_2012_14792_b200 import workloads as wl
+    from paper_2012_14792_b200.partitioner import shard_merge
+
+    rank, world, local = dist_env()
+    backend = os.environ.get("SLICECRAFT_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    w = wl.WORKLOADS[args.config]
+    F, g, bps = w.frames, w.grid(), w.bps
+    cfg = w.cfg(mode=args.mode)
+    luma_h, est_h = make_inputs(w, 0, F)  # the same frames on every rank
+    luma_d, est_d = luma_h.cuda(), est_h.cuda()
+    rec_d = torch.empty(F * g.cell_count() * 24, dtype=torch.uint8, device="cuda")
+    part = Partitioner(local)
+    stream = torch.cuda.current_stream()
+    check(lib().sc_ctx_set_stream(part._h, C.c_void_p(stream.cuda_stream)))
+    part.set_shard(rank, world)
+    gc, cc = g.c(), cfg.c()
+    pitch, fstride = w.width * bps, w.width * w.height * bps
+
+    def gather(blob: bytes) -> bytes:
+        if world == 1:
+            return blob
+        t = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+        if backend == "nccl":
+            t = t.cuda()
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return b"".join(x.cpu().numpy().tobytes() for x in out)
+
+    def fresh():
+        r = (SearchResult * F)()
+        for f in range(F):
+            r[f].argmin.n_slices = w.n_slices
+            r[f].best.n_slices = w.n_slices
+        return r
+
+    def step():
+        check(lib().sc_texture_moments(part._h, C.c_void_p(luma_d.data_ptr()), bps, w.width,
+                                       w.height, pitch, fstride, w.ctu, F,
+                                       C.c_void_p(rec_d.data_ptr())))
+        r1 = fresh()
+        check(lib().sc_min_time_search(part._h, C.byref(gc), C.byref(cc),
+                                       C.c_void_p(est_d.data_ptr()), F, C.cast(r1, C.c_void_p)))
+        m1 = fresh()
+        shard_merge(1, world, F, gather(bytes(part.shard_export(1, F))), m1)
+        tmin = np.array([m1[f].t_min_us for f in range(F)], dtype=np.float64)
+        r2 = fresh()
+        check(lib().sc_constrained_clustering(part._h, C.byref(gc), C.byref(cc),
+                                              C.c_void_p(est_d.data_ptr()),
+                                              C.c_void_p(rec_d.data_ptr()),
+                                              C.c_void_p(tmin.ctypes.data), F,
+                                              C.cast(r2, C.c_void_p)))
+        m2 = fresh()
+        shard_merge(2, world, F, gather(bytes(part.shard_export(2, F))), m2)
+        return m1, m2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 1)):
+        m1, m2 = step()
+    cands = sum((m1[f].candidates_step1 | (m1[f].candidates_step1_hi << 64)) +
+                (m2[f].candidates_step2 | (m2[f].candidates_step2_hi << 64)) for f in range(F))
+    digest = hash(tuple((m2[f].t_best_us, m2[f].sse_best) for f in range(F)))
+    clocks = Clocks(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    out = {
+        "metric": METRIC, "value": cands / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64/f64", "data": "synthetic (seeded; SURVEY.md \u00a78d generator)",
+        "config": {"workload": w.name, "frames": F, "frame": f"{w.width}x{w.height}",
+                   "grid": f"{g.cols}x{g.rows}", "n_slices": w.n_slices,
+                   "max_tile_cols": w.max_tile_cols,
+                   "mode": "pruned" if args.mode else "exhaustive",
+                   "parallelism": f"candidate space sharded over {world} rank(s), "
+                                  "per-frame argmin all-gathered after each step"},
+        "frames_per_s": F / (ms / 1e3),
+        "result_digest": digest,
+        "clocks": ck,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    part.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def pruned_extras(part, stream, args, w3, luma3_d, est3_d):
     """The exact pruned mode (identical results and counters)
     on the headline workload and on configs 4 and 5, whose candidate spaces
@@ -479,9 +607,14 @@ def main():
                     help="0 exhaustive (every candidate scored), 1 exact branch-and-bound")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the pruned-mode extras")
+    ap.add_argument("--shard", default="frames", choices=["frames", "candidates"],
+                    help="frames: each rank its own batch (weak scaling); candidates: the "
+                         "ranks split each frame's candidate space (strong scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.shard == "candidates":
+        run_candidates(args)
     else:
         run_ours(args)
 

@@ -281,8 +281,9 @@ typedef struct sc_shard_best {
   uint64_t key_t;     /* f64 bits of t (non-negative => monotone) */
   uint64_t item;      /* global work-item index (lex order) */
   uint64_t ord;       /* candidate ordinal inside the item */
-  uint64_t count;     /* this shard's candidate count */
+  uint64_t count;     /* this shard's candidate count (low 64 bits) */
   uint64_t leaves;    /* this shard's scored leaves */
+  uint64_t count_hi;  /* high 64 bits of the count (pruned DP counts reach ~6e29) */
   sc_layout layout;
 } sc_shard_best;
 /* Export this context's last step-1 (step=1) or step-2 (step=2) shard bests. */

@@ -82,7 +82,7 @@ class PartitionStats(C.Structure):
 class ShardBest(C.Structure):
     _fields_ = [("key_sse", C.c_double), ("key_t", C.c_uint64), ("item", C.c_uint64),
                 ("ord", C.c_uint64), ("count", C.c_uint64), ("leaves", C.c_uint64),
-                ("layout", Layout)]
+                ("count_hi", C.c_uint64), ("layout", Layout)]
 
 
 # (name, restype, argtypes) for every symbol declared in the header.

@@ -820,11 +820,15 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   // shards export it from rank 0 only
   const bool dp1 = cfg.mode == SC_MODE_PRUNED;
   const bool dp2 = dp1 || (do2 && step2_bounded(cfg));
+  ctx->last_count_hi[0] = ctx->last_count_hi[1] = 0;
   if (dp1 || dp2) {
     const unsigned __int128 cnt = plan_count(plan, g, cfg);
     for (int s2 = 0; s2 < 2; ++s2)
       if (s2 == 0 ? dp1 : dp2)
         for (auto& fbv : ctx->last_best[s2]) fbv.count = ctx->shard_rank == 0 ? (uint64_t)cnt : 0;
+    for (int s2 = 0; s2 < 2; ++s2)
+      ctx->last_count_hi[s2] =
+          ((s2 == 0 ? dp1 : dp2) && ctx->shard_rank == 0) ? (uint64_t)(cnt >> 64) : 0;
   }
   const bool whole = ctx->shard_world == 1;  // false: per-shard results, merged later
   for (int f = 0; f < frames; ++f) {
@@ -1288,6 +1292,7 @@ sc_status sc_shard_export(sc_ctx* ctx, int32_t step, int32_t frames, sc_shard_be
       s.item = b.found ? b.item : ~0ull;
       s.ord = b.found ? b.ord : ~0ull;
       s.count = b.count;
+      s.count_hi = ctx->last_count_hi[step - 1];
       s.leaves = b.count;
       layout_from_snap(b, SC_MAX_SLICES, &s.layout);
     }
@@ -1300,10 +1305,10 @@ sc_status sc_shard_merge(int32_t step, int32_t world, int32_t frames,
     if (!gathered || !inout) fail(SC_ERR_USAGE, "NULL argument");
     for (int f = 0; f < frames; ++f) {
       int win = -1;
-      uint64_t total = 0;
+      unsigned __int128 total = 0;
       for (int r = 0; r < world; ++r) {
         const sc_shard_best& s = gathered[(size_t)r * frames + f];
-        total += s.count;
+        total += ((unsigned __int128)s.count_hi << 64) | s.count;
         if (s.item == ~0ull) continue;
         if (win < 0) { win = r; continue; }
         const sc_shard_best& b = gathered[(size_t)win * frames + f];
@@ -1323,14 +1328,16 @@ sc_status sc_shard_merge(int32_t step, int32_t world, int32_t frames,
       if (step == 1) {
         r.t_min_us = bits_to_double(b.key_t);
         r.argmin = L;
-        r.candidates_step1 = total;
-        r.leaves_scored_step1 = total;
+        r.candidates_step1 = (uint64_t)total;
+        r.candidates_step1_hi = (uint64_t)(total >> 64);
+        r.leaves_scored_step1 = (uint64_t)total;
       } else {
         r.t_best_us = bits_to_double(b.key_t);
         r.sse_best = b.key_sse;
         r.best = L;
-        r.candidates_step2 = total;
-        r.leaves_scored_step2 = total;
+        r.candidates_step2 = (uint64_t)total;
+        r.candidates_step2_hi = (uint64_t)(total >> 64);
+        r.leaves_scored_step2 = (uint64_t)total;
       }
       r.candidates_evaluated = r.candidates_step1 + r.candidates_step2;
     }

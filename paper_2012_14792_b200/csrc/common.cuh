@@ -194,6 +194,7 @@ struct sc_ctx {
   std::vector<scb::FrameBest> last_best[2];
   uint64_t last_leaves[2] = {0, 0};
   bool last_pruned = false;  // last search ran in SC_MODE_PRUNED (DP counts)
+  uint64_t last_count_hi[2] = {0, 0};  // high bits of this shard's DP count per step
   int diag_step = 0;         // diagnostics builds only
   ~sc_ctx();
 };

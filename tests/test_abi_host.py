@@ -199,3 +199,22 @@ def test_shard_merge_picks_first_in_order():
     assert res[0].argmin.col_widths[0] == 2  # rank 1: t=5, item 4 < 10
     assert res[1].argmin.col_widths[0] == 2  # t=8, item 30 tie: layout [2] < [3]
     assert res[0].candidates_step1 == 303
+
+
+def test_shard_merge_wide_counts():
+    """Pruned-mode DP counts exceed 64 bits (cfg5: ~6.1e29 per frame and step):
+    sc_shard_best carries count_hi and the merge sums 128-bit counts."""
+    from paper_2012_14792_b200._abi import SearchResult, ShardBest, check, lib
+    world, F = 2, 1
+    recs = (ShardBest * (world * F))()
+    total = 610308283606383278175018310268  # cfg5's count (SURVEY.md §8d)
+    for r in range(world):
+        s = recs[r]
+        s.key_t, s.item, s.ord, s.key_sse = 5 + r, 1, 0, 0.0
+        s.layout.n_cols = 1
+        s.layout.col_widths[0] = 1
+    recs[0].count, recs[0].count_hi = total & ((1 << 64) - 1), total >> 64  # rank 0 carries it
+    res = (SearchResult * F)()
+    res[0].argmin.n_slices = 1
+    check(lib().sc_shard_merge(1, world, F, C.cast(recs, C.c_void_p), C.cast(res, C.c_void_p)))
+    assert res[0].candidates_step1 | (res[0].candidates_step1_hi << 64) == total
