@@ -319,13 +319,14 @@ constexpr int kSplitDepth1 = 8;
 // to the split level; since the item prefilter (k_item_filter) drops the
 // items that die at their prefix, only surviving items pay it, and the
 // survivors are few and heavy.  Measured on B200 (profiles/r01_split_sweep.md)
-// 16 ways is best or even on configs 3-5 in both steps.
-// SLICECRAFT_B200_SPLIT / SLICECRAFT_B200_SPLIT2 (step 2) override;
-// SLICECRAFT_B200_SPLIT_DEPTH sets the level (default 1).
+// 16 ways is best or even on configs 3-5 in both steps, 64 for cfg5's step 2.
+// SLICECRAFT_B200_SPLIT / SLICECRAFT_B200_SPLIT2 (step 2) override.
 int split_ways(int step, int n, bool pruned_mode) {
-  (void)n;
   const char* v = getenv(step == 1 ? "SLICECRAFT_B200_SPLIT" : "SLICECRAFT_B200_SPLIT2");
-  int g = v ? atoi(v) : (pruned_mode ? 16 : kBoundedStep2Split);
+  // n >= 24 (cfg5): step 2 spreads its few deep items over 64 warps (4.7 ->
+  // 4.2 ms on cfg5, with depth 2 below); 16 elsewhere
+  int g = v ? atoi(v)
+            : (!pruned_mode ? kBoundedStep2Split : (step == 2 && n >= 24 ? 64 : 16));
   return g < 1 ? 1 : (g > 64 ? 64 : g);
 }
 // Heights level whose subtrees the warps of a shared item deal out.  Step 1
@@ -337,8 +338,8 @@ int split_ways(int step, int n, bool pruned_mode) {
 int split_depth(int step, int n) {
   const char* v = getenv(step == 1 ? "SLICECRAFT_B200_SPLIT_DEPTH" : "SLICECRAFT_B200_SPLIT_DEPTH2");
   // measured: depth 8 takes cfg5 (n = 32) step 1 from 4.8 to 3.6 ms, but
-  // costs cfg3 (n = 8) 13 %; cfg4 (n = 16) is even
-  const int d = v ? atoi(v) : ((step == 1 && n >= 24) ? kSplitDepth1 : 1);
+  // costs cfg3 (n = 8) 13 %; cfg4 (n = 16) is even.  Step 2: depth 2 for n >= 24
+  const int d = v ? atoi(v) : (n >= 24 ? (step == 1 ? kSplitDepth1 : 2) : 1);
   return d < 0 ? 0 : (d > 62 ? 62 : d);
 }
 
