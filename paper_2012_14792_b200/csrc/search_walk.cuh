@@ -323,6 +323,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   uint8_t Lcol[kMaxLevels], Lrun[kMaxLevels], Ly0[kMaxLevels], Lh[kMaxLevels], Lhi[kMaxLevels];
   int32_t Amin[kMaxLevels], Amax[kMaxLevels], Lbase[kMaxLevels];
   tkey Pin[kMaxLevels];
+  double Sp[STEP == 2 && PRUNE ? kMaxLevels : 1];  // pruned step 2: SSE prefix per level
   // heights-DFS levels: LS static (w | runs left << 8 | run << 16 | column << 24,
   // column rectangle base, suffix fillability bounds), D the spilled state of
   // the levels above the current one (h | hhi << 8 | y0 << 16, -, Amin, Amax; Pin
@@ -445,7 +446,9 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     return e.lbm[((size_t)xw_of(cols, x0, w) * e.rstride + r) * FPW + f];
   };
   // score one candidate (strict comparisons keep the first in order)
-  auto score = [&](tkey t, uint64_t o, int lr, int lh, int lrest) {
+  // sse_pre >= 0: the candidate's SSE, already folded in slice order by the
+  // caller (pruned step 2); otherwise layout_sse computes it
+  auto score = [&](tkey t, uint64_t o, int lr, int lh, int lrest, double sse_pre = -1.0) {
     if (PRUNE) ++st.scored;
     if (STEP == 1) {
       if (t < (PRUNE ? st.best_t : st.bcmp) ||
@@ -461,7 +464,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         }
       }
     } else if ((int64_t)t <= st.budget) {
-      const double s = layout_sse(lr, lh, lrest);
+      const double s = sse_pre >= 0.0 ? sse_pre : layout_sse(lr, lh, lrest);
       if (s < st.best_sse ||
           (s == st.best_sse && (t < st.best_t || (PRUNE && st.tie && t == st.best_t &&
                                                   precedes_best(lr, lh, lrest))))) {
@@ -666,6 +669,25 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         // pruned mode: every column's bound (PR) floors the whole subtree
         const tkey colfloor = PRUNE ? kmax(P, PR[c]) : P;
         if (!viable(colfloor)) continue;
+        // step 2: SSE prefix in slice order (the left fold of layout_sse,
+        // search.cpp:85-91).  Slice SSEs are >= 0, so a prefix above the
+        // lane's best SSE already loses (strictly): the subtree is skipped.
+        // Sp[l] = the fold of every slice before level l's run; one-run
+        // columns enter at their positions.
+        auto sse_at = [&](int lb, int y0, int h) -> double {
+          return rs[(size_t)(lb + SCB_YBASE(y0) + h - 1) * FPW + f];
+        };
+        auto fold_one_run = [&](double acc, int from, int to) -> double {
+          for (int i = from; i < to; ++i)
+            if (R[i] == 1)
+              acc = dadd_rn(acc, rs[(size_t)(xw_of(cols, X0[i], W[i]) * nyh +
+                                             yh_of(rows, 0, rows)) * FPW + f]);
+          return acc;
+        };
+        if (STEP == 2) {
+          Sp[0] = fold_one_run(0.0, 0, Lcol[0]);
+          if (Sp[0] > st.best_sse) continue;
+        }
         // ---- heights DFS over the multi-run columns (search.cpp:163-190)
         int l = 0;
         const bool leaf_now = (nl == 1);
@@ -684,12 +706,14 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           int lv;  // level whose state feeds the leaf loop
           tkey Pl;
           int amin_l, amax_l, y0l;
+          double Sl = 0.0;  // step 2: SSE fold before the leaf run
           if (leaf_now) {
             lv = 0;
             Pl = P;
             amin_l = amin;
             amax_l = amax;
             y0l = 0;
+            if (STEP == 2) Sl = Sp[0];
           } else {
             // advance level l to its next admissible height
             SCB_STAT(levels);
@@ -735,6 +759,15 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             const int nxt = l + 1;
             const bool new_col = Lrun[nxt] == 0;
             const int y0n = new_col ? 0 : y0 + h;
+            double Sn = 0.0;
+            if (STEP == 2) {
+              Sn = dadd_rn(Sp[l], sse_at(lb, y0, h));
+              if (forced) {
+                Sn = dadd_rn(Sn, sse_at(lb, y0 + h, rows_left - h));
+                Sn = fold_one_run(Sn, i + 1, Lcol[nxt]);
+              }
+              if (Sn > st.best_sse) continue;
+            }
             const Thr tn = thresholds(na, nx, win_lo, win_hi);
             if (new_col && !columns_feasible(Lcol[nxt], tn)) continue;
             if (nxt < nl - 1) {
@@ -746,6 +779,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
               Lh[l] = (uint8_t)(lo2 - 1);
               Lhi[l] = (uint8_t)hi2;
               Pin[l] = Pn;
+              if (STEP == 2) Sp[l] = Sn;
               Amin[l] = na;
               Amax[l] = nx;
               Ly0[l] = (uint8_t)y0n;
@@ -756,6 +790,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             amin_l = na;
             amax_l = nx;
             y0l = y0n;
+            Sl = Sn;
           }
           // ---- leaf loop: run Lrun[lv] of column Lcol[lv] takes every
           //      admissible height; the column's last run is forced.
@@ -771,7 +806,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   #if defined(SCB_STATS) && !defined(__CUDA_ARCH__)
             ++g_stats.leafr[R[i]];
   #endif
-            if (lo + slot <= hi && viable(PRUNE ? kmax(Pl, colfloor) : Pl)) {
+            if (lo + slot <= hi && viable(PRUNE ? kmax(Pl, colfloor) : Pl) &&
+                !(STEP == 2 && Sl > st.best_sse)) {
               // the split table holds max(run h, forced rest) at the run's own
               // rectangle index, which advances by +1 per h; lanes step h by J.
               int h = lo + slot;
@@ -781,7 +817,14 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
                 const int hn = h + J;
                 const bool more = hn <= hi;
                 const tkey vn = more ? p[J * FPW] : 0;  // prefetch the next height
-                score(kmax(Pl, v), ord + (uint64_t)(h - lo), lr, h, rows_left - h);
+                double sc = -1.0;
+                if (STEP == 2 && (int64_t)kmax(Pl, v) <= st.budget) {
+                  // the candidate's SSE: the prefix, the leaf run, its forced
+                  // rest, then the one-run columns after the leaf column
+                  sc = dadd_rn(dadd_rn(Sl, sse_at(xwb, y0l, h)), sse_at(xwb, y0l + h, rows_left - h));
+                  sc = fold_one_run(sc, i + 1, c);
+                }
+                score(kmax(Pl, v), ord + (uint64_t)(h - lo), lr, h, rows_left - h, sc);
                 if (!more) break;
                 h = hn;
                 p += J * FPW;
