@@ -417,6 +417,11 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
                              ctx->lbm.as<uint32_t>() + gi * lb_per_group, st);
     }
     SCB_CUDA(cudaMemsetAsync(ctx->inc.p, 0xff, (size_t)L.groups * L.fpw * sizeof(uint64_t), st));
+    if (step == 2) {  // shared SSE incumbents start at "none" (all-ones bits)
+      ctx->sse_inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
+      SCB_CUDA(cudaMemsetAsync(ctx->sse_inc.p, 0xff,
+                               (size_t)L.groups * L.fpw * sizeof(uint64_t), st));
+    }
   }
   for (int gi = 0; gi < L.groups; ++gi) {
     SearchArgs a{};
@@ -443,6 +448,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
       a.lbr = ctx->lbr.as<uint32_t>() + gi * lb_per_group;
       a.lbm = ctx->lbm.as<uint32_t>() + gi * lb_per_group;
       a.inc = ctx->inc.as<uint64_t>() + (size_t)gi * L.fpw;
+      if (step == 2) a.sse_inc = ctx->sse_inc.as<uint64_t>() + (size_t)gi * L.fpw;
     }
     a.bmax = plan->d_bmax.as<int32_t>();
     a.pathological = plan->pathological ? 1 : 0;

@@ -149,6 +149,7 @@ struct SearchArgs {
   const uint32_t* lbm;
   uint64_t* inc;                   // pruned mode: shared step-1 incumbent [FPW] (t << 32 | item)
   const uint64_t* seed_inc;        // pruned mode, phase B: incumbent frozen after phase A
+  uint64_t* sse_inc;               // pruned step 2: shared SSE incumbent [FPW] (f64 bits)
   const uint32_t* order;           // exhaustive step 1: item k -> work item (or nullptr)
   int split_g, split_depth;        // pruned mode: warps per work item (WalkEnv)
   uint32_t* cost;                  // per work item: walk cycles / 64 (or nullptr)
@@ -184,6 +185,7 @@ struct sc_ctx {
   // staging / tables
   scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rt_split, rs_search, usat;
   scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec, lbr, lbm, inc, seed_inc;
+  scb::DevBuf sse_inc;
   scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
   scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp;       // rank.cu scratch
   scb::DevBuf flt_idx, flt_flag, flt_list, flt_count, flt_temp;      // item filter (search.cu)

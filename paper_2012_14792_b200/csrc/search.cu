@@ -141,6 +141,7 @@ __device__ __forceinline__ void search_body(const SearchArgs& a) {
   e.lbm = a.lbm;
   e.inc = a.inc;
   e.seed_inc = a.seed_inc;
+  e.sse_inc = (PRUNE && STEP == 2) ? a.sse_inc : nullptr;
 
   const int lane = threadIdx.x & 31;
   const int f = lane % FPW;
@@ -162,6 +163,7 @@ __device__ __forceinline__ void search_body(const SearchArgs& a) {
   st.count = 0;
   st.scored = 0;
   st.inc = ~0ull;
+  st.sbound = __longlong_as_double(0x7ff0000000000000ll);
   st.snap = a.snaps + ((size_t)gwarp * 32 + lane) * kSnapBytes;
   const uint32_t n_items = a.n_items_dev ? *a.n_items_dev * (uint32_t)e.split_g : a.n_items;
   for (;;) {

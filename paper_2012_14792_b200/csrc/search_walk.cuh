@@ -9,6 +9,7 @@
 
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "plan.h"
 #include "slicecraft_b200.h"
@@ -160,6 +161,9 @@ struct WalkEnv {
   // incumbent frozen after the seed phase (or nullptr): its candidate precedes
   // every item still to walk, so a tie with it can never win
   const uint64_t* seed_inc;
+  // pruned step 2: shared per-frame SSE incumbent (f64 bits; SSEs are >= 0,
+  // so the bit patterns order like the values), or nullptr
+  uint64_t* sse_inc;
 };
 
 // One lane's running first-in-order best and its candidate snapshot.
@@ -171,6 +175,7 @@ struct LaneState {
   uint64_t count;   // candidates enumerated (uniform over the warp)
   uint64_t scored;  // candidates this lane actually scored
   uint64_t inc;     // last seen shared incumbent (pruned step 1), packed as EnvWalk::inc
+  double sbound;    // pruned step 2: min(own best SSE, last seen shared SSE incumbent)
   tkey bcmp;        // exhaustive step 1: a candidate wins iff t < bcmp (see walk_item)
   bool tie;         // pruned, shared items: this item part may precede the best's layout
   uint8_t* snap;
@@ -187,6 +192,12 @@ SCB_HD uint64_t incumbent_load(uint64_t* p) {
 #else
   return *p;
 #endif
+}
+SCB_HD double sse_incumbent(const uint64_t* p) {
+  uint64_t b = incumbent_load(const_cast<uint64_t*>(p));
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
 }
 SCB_HD void incumbent_offer(uint64_t* p, uint64_t v) {
 #ifdef __CUDA_ARCH__
@@ -473,7 +484,15 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         st.best_item = item;
         st.best_ord = o;
         take_snapshot(lr, lh, lrest);
-        if (PRUNE) st.tie = false;
+        if (PRUNE) {
+          st.tie = false;
+          st.sbound = s < st.sbound ? s : st.sbound;
+          if (e.sse_inc) {
+            uint64_t b;
+            memcpy(&b, &s, 8);
+            incumbent_offer(e.sse_inc + f, b);
+          }
+        }
       }
     }
   };
@@ -685,8 +704,15 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           return acc;
         };
         if (STEP == 2) {
+          // bound: the lane's own best, or a better one another warp found
+          if (e.sse_inc) {
+            const double sh = sse_incumbent(e.sse_inc + f);
+            st.sbound = sh < st.best_sse ? sh : st.best_sse;
+          } else {
+            st.sbound = st.best_sse;
+          }
           Sp[0] = fold_one_run(0.0, 0, Lcol[0]);
-          if (Sp[0] > st.best_sse) continue;
+          if (Sp[0] > st.sbound) continue;
         }
         // ---- heights DFS over the multi-run columns (search.cpp:163-190)
         int l = 0;
@@ -766,7 +792,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
                 Sn = dadd_rn(Sn, sse_at(lb, y0 + h, rows_left - h));
                 Sn = fold_one_run(Sn, i + 1, Lcol[nxt]);
               }
-              if (Sn > st.best_sse) continue;
+              if (Sn > st.sbound) continue;
             }
             const Thr tn = thresholds(na, nx, win_lo, win_hi);
             if (new_col && !columns_feasible(Lcol[nxt], tn)) continue;
@@ -807,7 +833,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             ++g_stats.leafr[R[i]];
   #endif
             if (lo + slot <= hi && viable(PRUNE ? kmax(Pl, colfloor) : Pl) &&
-                !(STEP == 2 && Sl > st.best_sse)) {
+                !(STEP == 2 && Sl > st.sbound)) {
               // the split table holds max(run h, forced rest) at the run's own
               // rectangle index, which advances by +1 per h; lanes step h by J.
               int h = lo + slot;

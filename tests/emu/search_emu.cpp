@@ -114,6 +114,8 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.lbm = lbm.data();
   e.inc = inc.data();
   e.seed_inc = nullptr;
+  std::vector<uint64_t> sse_inc(fpw, ~0ull);  // pruned step 2: shared SSE incumbent
+  e.sse_inc = (prune && step == 2) ? sse_inc.data() : nullptr;
   std::vector<uint64_t> frozen(fpw, ~0ull);
   // seeded pruned step 1 like api.cu: phase A = the first seed_items items
   size_t seed_items = 0;
@@ -134,6 +136,7 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
       s.count = 0;
       s.scored = 0;
       s.inc = ~0ull;
+      s.sbound = INFINITY;
       s.snap = &snaps[((size_t)wp * 32 + l) * kSnap];
       s.budget = -1;
       if (step == 2 && (l % fpw) < frames) {  // largest key whose time is <= budget
