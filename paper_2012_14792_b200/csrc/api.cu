@@ -260,7 +260,19 @@ const int16_t* decode_table(sc_ctx* ctx, const sc_grid& g) {
   return ctx->dec.as<int16_t>();
 }
 
-// K2 (f64 SAT) + K3 (time tables) from ctx->est.
+// CUDA graphs for the time-table phase (SLICECRAFT_B200_GRAPHS=0: plain launches).
+bool graphs_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_GRAPHS");
+  return !(v && v[0] == '0');
+}
+
+void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
+                              const int16_t* dec, cudaStream_t st);
+
+// K2 (f64 SAT) + K3 (time tables) from ctx->est.  The ~20 short launches of
+// this phase leave the device waiting on the host's launch rate, so when a
+// call repeats the previous call's shape and buffers (the steady state of a
+// frame pipeline) the phase is captured once into a CUDA graph and replayed.
 void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
                          cudaStream_t st) {
   const int16_t* dec = decode_table(ctx, g);
@@ -270,6 +282,47 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   ctx->vals.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
   ctx->nvals.ensure((size_t)L.frames * sizeof(uint32_t));
   if (raw) ctx->rect_t.ensure((size_t)L.frames * L.nr * sizeof(double));
+  ctx->rt_split.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint32_t));
+  if (!graphs_enabled()) {
+    enqueue_time_tables_body(ctx, g, L, raw, dec, st);
+    return;
+  }
+  // everything a replay depends on: shape and every buffer address
+  std::vector<uintptr_t> key = {
+      (uintptr_t)g.cols, (uintptr_t)g.rows, (uintptr_t)L.frames, (uintptr_t)L.fpw,
+      (uintptr_t)L.groups, (uintptr_t)L.nr, (uintptr_t)raw, (uintptr_t)st, (uintptr_t)dec,
+      (uintptr_t)ctx->est.p, (uintptr_t)ctx->sat.p, (uintptr_t)ctx->rt_bits.p,
+      (uintptr_t)ctx->rt_search.p, (uintptr_t)ctx->vals.p, (uintptr_t)ctx->nvals.p,
+      (uintptr_t)ctx->rect_t.p, (uintptr_t)ctx->rt_split.p, (uintptr_t)ctx->rk_idx.p,
+      (uintptr_t)ctx->rk_sorted.p, (uintptr_t)ctx->rk_flags.p, (uintptr_t)ctx->rk_temp.p,
+      (uintptr_t)ctx->rk_temp.bytes};
+  if (ctx->tt_exec && key == ctx->tt_key) {
+    SCB_CUDA(cudaGraphLaunch(ctx->tt_exec, st));
+    return;
+  }
+  if (ctx->tt_exec) {
+    cudaGraphExecDestroy(ctx->tt_exec);
+    ctx->tt_exec = nullptr;
+  }
+  if (key != ctx->tt_prev_key) {
+    // first call of this shape: plain launches (they size the scratch buffers)
+    enqueue_time_tables_body(ctx, g, L, raw, dec, st);
+    ctx->tt_prev_key = key;
+    return;
+  }
+  // second call of the same shape: capture, instantiate, launch
+  cudaGraph_t graph = nullptr;
+  SCB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  enqueue_time_tables_body(ctx, g, L, raw, dec, st);
+  SCB_CUDA(cudaStreamEndCapture(st, &graph));
+  SCB_CUDA(cudaGraphInstantiate(&ctx->tt_exec, graph, 0));
+  cudaGraphDestroy(graph);
+  ctx->tt_key = key;
+  SCB_CUDA(cudaGraphLaunch(ctx->tt_exec, st));
+}
+
+void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
+                              const int16_t* dec, cudaStream_t st) {
   grid_sat_device(ctx->est.as<double>(), nullptr, g.cols, g.rows, L.frames, ctx->sat.as<double>(),
                   nullptr, st);
   rect_tables_device(ctx->sat.as<double>(), nullptr, dec, g.cols, g.rows, L.frames, L.fpw,
@@ -279,7 +332,6 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   rank_times_device(ctx, ctx->rt_bits.as<uint64_t>(), L.nr, L.frames, L.fpw,
                     ctx->rt_search.as<uint32_t>(), ctx->vals.as<uint64_t>(),
                     ctx->nvals.as<uint32_t>(), st);
-  ctx->rt_split.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint32_t));
   split_table_device(ctx->rt_search.as<uint32_t>(), g.cols, g.rows, L.groups, L.fpw,
                      ctx->rt_split.as<uint32_t>(), ctx->sm_count, st);
 }
@@ -886,9 +938,11 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
 }  // namespace
 
 sc_ctx::~sc_ctx() {
+  if (tt_exec) cudaGraphExecDestroy(tt_exec);
   for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rt_split, &rs_search, &usat,
                   &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc, &rt_bits, &vals, &nvals, &budget_f64, &rk_idx, &rk_sorted,
-                  &rk_flags, &rk_offsets, &rk_temp})
+                  &rk_flags, &rk_offsets, &rk_temp, &sse_inc, &flt_idx, &flt_flag, &flt_list,
+                  &flt_count, &flt_temp})
     b->release();
   h_stage.release();
   h_luma.release();

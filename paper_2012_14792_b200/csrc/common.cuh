@@ -186,6 +186,10 @@ struct sc_ctx {
   scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rt_split, rs_search, usat;
   scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec, lbr, lbm, inc, seed_inc;
   scb::DevBuf sse_inc;
+  // the time-table phase (K2 + K3 + ranks + split table, ~20 launches) as a
+  // CUDA graph, replayed while the call shape and buffers repeat (api.cu)
+  std::vector<uintptr_t> tt_key, tt_prev_key;
+  cudaGraphExec_t tt_exec = nullptr;
   scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
   scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp;       // rank.cu scratch
   scb::DevBuf flt_idx, flt_flag, flt_list, flt_count, flt_temp;      // item filter (search.cu)
