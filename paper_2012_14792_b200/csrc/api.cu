@@ -313,7 +313,14 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   // second call of the same shape: capture, instantiate, launch
   cudaGraph_t graph = nullptr;
   SCB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  enqueue_time_tables_body(ctx, g, L, raw, dec, st);
+  try {
+    enqueue_time_tables_body(ctx, g, L, raw, dec, st);
+  } catch (...) {  // leave the stream out of capture mode before reporting
+    cudaStreamEndCapture(st, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    ctx->tt_prev_key.clear();
+    throw;
+  }
   SCB_CUDA(cudaStreamEndCapture(st, &graph));
   SCB_CUDA(cudaGraphInstantiate(&ctx->tt_exec, graph, 0));
   cudaGraphDestroy(graph);
