@@ -532,6 +532,27 @@ def test_edge_shapes_vs_oracle(part, oracle, monkeypatch, m):
             assert o.candidates_step2 == e.candidates_step2, ctx
 
 
+def test_graph_replay_sees_new_inputs(part, oracle):
+    """The time-table phase is captured into a CUDA graph on the second call of
+    a shape and replayed afterwards: every call must still read its own
+    estimate maps (new data in the same buffers) and match the oracle."""
+    from paper_2012_14792_b200 import CtuGrid, SearchConfig
+    g = CtuGrid.make(9 * 64, 7 * 64, 64)
+    rng = np.random.default_rng(5)
+    cfg = SearchConfig(n_slices=6, lambda_=0.1, max_tile_cols=3)
+    luma = rng.integers(0, 1024, size=(3, g.frame_height, g.frame_width)).astype(np.uint16)
+    rec = part.ctu_stats_batch(luma, 64)
+    for call in range(4):
+        est = rng.lognormal(0, 0.6, size=(3, g.cell_count()))
+        got = part.two_step_batch(g, est, rec, cfg)
+        for f in range(3):
+            st, e = oracle.search(g.frame_width, g.frame_height, 64, est[f], _rec3(rec[f]), 6,
+                                  0.1, 3.0, 3, 0, 3)
+            assert st == 0
+            assert got[f].t_min_us == e.t_min_us and got[f].sse_best == e.sse_best, (call, f)
+            assert got[f].best.rects() == e.best.slices(g.rows), (call, f)
+
+
 def test_size_limits(part):
     """Requests beyond the compiled limits fail with SizeError,
     the reference's own checks keep their classes."""
