@@ -935,6 +935,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         // first row y0, fixed-slice maximum Pin and areas Amin / Amax
         int l = 0, cw = 0, crl = 0, h = 0, hhi = 0, y0 = 0, cAmin = amin, cAmax = amax;
         int cridx = 0, clbase = 0;
+        int crow = 0;  // rectangle index of the current level's run at h = 0
         tkey cPin = P;
         auto load_static = [&](const Lvl& s) {
           cw = s.a & 255;
@@ -1025,6 +1026,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           height_interval(e, thresholds(amin, amax, win_lo, win_hi), cw, rows, crl, lo0, hi0);
           h = lo0 - 1;
           hhi = imax(hi0, 0);
+          crow = clbase - 1;  // y0 = 0: ybase(0) = 0
         }
         while (true) {
           SCB_STAT(levels);
@@ -1046,6 +1048,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             cPin = PIN[l * PS];
             cAmin = dl.c;
             cAmax = dl.d;
+            crow = clbase + SCB_YBASE(y0) - 1;
             continue;
           }
           if (split && l == lsplit) {  // deal this subtree to one warp of the item
@@ -1056,7 +1059,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           }
           const int a1 = cw * h;
           int na = imin(cAmin, a1), nx = imax(cAmax, a1);
-          const size_t ri = (size_t)(clbase + SCB_YBASE(y0) + h - 1) * FPW + f;
+          const size_t ri = (size_t)(crow + h) * FPW + f;
           tkey Pn;
           if (forced) {
             const int a2 = cw * (rows - y0 - h);
@@ -1088,6 +1091,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             cPin = Pn;
             cAmin = na;
             cAmax = nx;
+            crow = clbase + SCB_YBASE(y0) - 1;
             continue;
           }
           leaf(Pn, na, nx, y0n);
