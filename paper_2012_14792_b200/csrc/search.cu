@@ -82,7 +82,7 @@ template <int FPW, int STEP, bool PRUNE>
 __device__ __forceinline__ void search_body(const SearchArgs& a) {
   // shared-memory tables (search_walk.cuh): g_dyn = bmax|aneed interleaved
   // [2A], mstar [(cols+1)(rows+1)], ilo [(cols+1) * rstride]; static magic,
-  // ybase, rq
+  // rq
   const int A = a.max_area + 1;
   const int nms = (a.cols + 1) * (a.rows + 1);
   const int rstride = min(a.n, a.rows) + 1;
@@ -100,7 +100,6 @@ __device__ __forceinline__ void search_body(const SearchArgs& a) {
   for (int w = threadIdx.x; w < kTabDim; w += blockDim.x)
     g_magic[w] = (w >= 1 && w <= a.cols) ? div_magic(w) : 0ull;
   for (int y = threadIdx.x; y < kTabDim; y += blockDim.x) {
-    g_ybase[y] = y <= a.rows ? yh_of(a.rows, y, 1) : 0;
     g_rq[y] = (y >= 1 && y <= a.rows) ? a.rows / y : 0;
   }
   __syncthreads();

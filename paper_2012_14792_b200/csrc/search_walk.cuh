@@ -99,7 +99,7 @@ constexpr int kSnap = 96;          // snapshot bytes: W[16] R[16] H[64]
 constexpr int kTabDim = 256;  // grid cols and rows are <= 255 (api.cu check_cfg)
 #ifdef __CUDACC__
 __shared__ uint64_t g_magic[kTabDim];
-__shared__ int32_t g_ybase[kTabDim], g_rq[kTabDim];
+__shared__ int32_t g_rq[kTabDim];
 extern __shared__ int32_t g_dyn[];  // [2A] bmax|aneed interleaved, mstar, ilo
 #endif
 #ifdef __CUDA_ARCH__
@@ -108,7 +108,6 @@ extern __shared__ int32_t g_dyn[];  // [2A] bmax|aneed interleaved, mstar, ilo
 #define SCB_MSTAR(i) (g_dyn[e.mstar_off + (i)])
 #define SCB_ILO(i) (g_dyn[e.ilo_off + (i)])
 #define SCB_MAGIC(w) (g_magic[w])
-#define SCB_YBASE(y) (g_ybase[y])
 #define SCB_RQ(r) (g_rq[r])
 #else
 #define SCB_BMAX(a) (e.bmax[a])
@@ -116,9 +115,13 @@ extern __shared__ int32_t g_dyn[];  // [2A] bmax|aneed interleaved, mstar, ilo
 #define SCB_MSTAR(i) (e.mstar[i])
 #define SCB_ILO(i) (e.ilo[i])
 #define SCB_MAGIC(w) (e.magic[w])
-#define SCB_YBASE(y) (e.ybase[y])
 #define SCB_RQ(r) (e.rq[r])
 #endif
+
+// yh(y, 1) = y*rows - y*(y-1)/2, the first rectangle starting at row y:
+// computed (4 ALU operations) rather than loaded, off the shared-memory
+// latency chain of the walk's address computations
+#define SCB_YBASE(y) ((y) * e.rows - (((y) * ((y) - 1)) >> 1))
 
 // Read-only walk environment (tables live in shared memory on the GPU).
 struct WalkEnv {
@@ -131,7 +134,6 @@ struct WalkEnv {
   const int32_t* mstar;   // [(cols+1) * (rows+1)]
   const int32_t* ilo;     // [(cols+1) * rstride]: lower end of window I(w, r)
   const uint64_t* magic;  // [cols+1]: division by w (div_magic)
-  const int32_t* ybase;   // [rows+1]: yh(y, 1), the first rectangle starting at row y
   const int32_t* rq;      // [rows+1]: rows / r (no integer division in the runs DFS)
   int mstar_off, ilo_off;  // GPU: offsets of mstar / ilo in dynamic shared memory
   // GPU, exhaustive walks: this warp's heights-DFS level records in shared

@@ -105,7 +105,6 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   e.mstar = tab.data() + 2 * A;
   e.ilo = ilo.data();
   e.magic = magic.data();
-  e.ybase = ybase.data();
   e.rq = rq.data();
   e.rt = rt.data();
   e.rts = rts.data();
