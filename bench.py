@@ -53,18 +53,56 @@ def dist_env():
     return rank, world, local
 
 
-# ---- clocks sampler (nvidia-smi during the timed region) ------------------------
+# ---- clocks sampler (during the timed region) -----------------------------------
 class Clocks:
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML polled every 2 ms from a background thread (a step is a few
+    ms, so nvidia-smi's 100 ms loop would often see none); nvidia-smi -lms
+    as the fallback where NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
         self.lines = []
+        self.nvml = None
+        self.samples = []  # (sm_mhz, reason bitmask)
+        self.reason_bits = {}
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.nvml = N
+            self.h = N.nvmlDeviceGetHandleByIndex(gpu)
+            self.smax = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self.reason_bits = {
+                "hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        except Exception:
+            self.nvml = None
 
     def start(self):
+        if self.nvml is not None:
+            self._stop = threading.Event()
+            self.samples = []
+
+            def poll():
+                N = self.nvml
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(
+                            (float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)),
+                             int(N.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+                    except Exception:
+                        pass
+                    self._stop.wait(0.002)
+            self._t = threading.Thread(target=poll, daemon=True)
+            self._t.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -84,6 +122,17 @@ class Clocks:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+            sm = [c for c, _ in self.samples]
+            reasons = set()
+            for _, m in self.samples:
+                for nm, bit in self.reason_bits.items():
+                    if m & bit:
+                        reasons.add(nm)
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.smax,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -92,7 +141,6 @@ class Clocks:
         except Exception:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 9:
@@ -102,14 +150,13 @@ class Clocks:
                 smax = float(p[2])
             except ValueError:
                 continue
-            for nm, v in zip(names, p[5:9]):
+            for nm, v in zip(self.NAMES, p[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
-# ---- inputs ------------------------------------------------------------------------
 def make_inputs(w, rank, frames, pinned=True):
     import torch
     from paper_2012_14792_b200 import workloads as wl
