@@ -250,6 +250,12 @@ def run_ours(args):
     c2 = [r.candidates_step2 | (r.candidates_step2_hi << 64) for r in res]
     cands = sum(c1) + sum(c2)
     counts = sorted(set(zip(c1, c2)))
+    # what the walks actually scored (transparency beside the reference-counted
+    # value): step-2 leaves under the budget-bounded / pruned walks
+    # (the exhaustive step 1 scores every candidate; the pruned and budget-
+    # bounded walks count what they score)
+    walked = sum((c1[i] if args.mode == 0 else r.leaves_scored_step1) + r.leaves_scored_step2
+                 for i, r in enumerate(res))
 
     # ---- timed: device-resident inputs ----
     clocks = Clocks(local)
@@ -352,6 +358,7 @@ def run_ours(args):
                    "parallelism": f"frames sharded, {world} rank(s)",
                    "l2": "inputs larger than L2 (luma batch %.0f MB/step)" % (luma_bytes / 1e6)},
         "frames_per_s": frames_total / (ms / 1e3),
+        "candidates_scored_by_the_walks_per_s": walked * world / (ms / 1e3),
         "frames_per_s_e2e": frames_total / (ms_e2e / 1e3),
         "texture_gbs": tex_gbs,
         "phase_us": {"texture_k1": round(tex_us, 2), "tables_k2k3": round(tab_us, 2),
