@@ -1030,15 +1030,32 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
           hhi = imax(hi0, 0);
           crow = clbase - 1;  // y0 = 0: ybase(0) = 0
         }
+        // the leaf's parent level runs in the leaf's own column (the column has
+        // three or more runs): its heights go straight into the leaf from a
+        // tight loop -- never forced, no column change, nothing to push
+        const bool tail_fused = nl >= 2 && (LS[nl - 2].a >> 24) == (LS[nl - 1].a >> 24);
         while (true) {
           SCB_STAT(levels);
           // the level records are written by every lane with the same value;
           // a lane may only overwrite one after all lanes finished reading it
           SCB_SYNCWARP();
           const bool forced = crl == 2;
-          ++h;
-          if (e.patho && !forced)
-            while (h <= hhi && !(cw * h <= SCB_BMAX(cw * h))) ++h;
+          if (tail_fused && l == nl - 2) {
+            while (true) {
+              ++h;
+              if (e.patho)
+                while (h <= hhi && !(cw * h <= SCB_BMAX(cw * h))) ++h;
+              if (h > hhi) break;
+              const int a1 = cw * h;
+              const tkey Pn = kmax(cPin, rt[(size_t)(crow + h) * FPW + f]);
+              leaf(Pn, imin(cAmin, a1), imax(cAmax, a1), y0 + h);
+              SCB_SYNCWARP();
+            }
+          } else {
+            ++h;
+            if (e.patho && !forced)
+              while (h <= hhi && !(cw * h <= SCB_BMAX(cw * h))) ++h;
+          }
           if (h > hhi) {
             if (l == 0) break;
             --l;
