@@ -40,16 +40,16 @@ namespace scb {
 #define SCB_SEARCH_BLOCK 256
 #endif
 // Exhaustive step 1 (the headline walk, warp-uniform): 64-thread blocks under
-// a register cap (__maxnreg__) instead of a blocks-per-SM launch bound, with
-// which ptxas settles at 96 registers, so the register file holds 10 blocks =
+// a register cap (__maxnreg__) instead of a blocks-per-SM launch bound; the
+// cap keeps ptxas at <= 96 registers, so the register file holds 10 blocks =
 // 20 warps/SM.  Measured on cfg3, step-1 ms by cap ->
-// registers: 96 -> 86: 5.12, 100 -> 88: 5.06, 104 -> 92: 4.98, 112 -> 96:
-// 5.00, 128 -> 96: 4.96 (256-thread blocks, 16 warps/SM: +7 %).
+// registers chosen: 96 -> 89: 4.47, 100 -> 92: 4.49, uncapped (128) -> 102
+// (9 blocks): 4.79; 256-thread blocks at 16 warps/SM were 7 % slower.
 #ifndef SCB_SEARCH_BLOCK1
 #define SCB_SEARCH_BLOCK1 64
 #endif
 #ifndef SCB_SEARCH_REGS1
-#define SCB_SEARCH_REGS1 128
+#define SCB_SEARCH_REGS1 96
 #endif
 template <int STEP, bool PRUNE>
 struct SearchShape {

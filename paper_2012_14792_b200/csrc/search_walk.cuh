@@ -1051,6 +1051,22 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
               leaf(Pn, imin(cAmin, a1), imax(cAmax, a1), y0 + h);
               SCB_SYNCWARP();
             }
+          } else if (forced && l == nl - 2) {
+            // the leaf's parent closes its column (forced rest): the leaf
+            // starts the next column at row 0, whose fillability bounds are
+            // fixed for the loop
+            const Lvl sn = LS[nl - 1];
+            while (true) {
+              ++h;
+              if (h > hhi) break;
+              const int a1 = cw * h, a2 = cw * (rows - y0 - h);
+              const int na = imin(imin(cAmin, a1), a2), nx = imax(imax(cAmax, a1), a2);
+              const tkey Pn = kmax(cPin, e.rts[(size_t)(crow + h) * FPW + f]);
+              const Thr tn = thresholds(na, nx, win_lo, win_hi);
+              if (tn.t2 > sn.d || tn.t1 < sn.c) continue;
+              leaf(Pn, na, nx, 0);
+              SCB_SYNCWARP();
+            }
           } else {
             ++h;
             if (e.patho && !forced)
