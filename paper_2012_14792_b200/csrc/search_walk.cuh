@@ -959,10 +959,10 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         const int lw = LL.a & 255, lr = (LL.a >> 16) & 255, lxwb = LL.b;
         const uint64_t lmg = SCB_MAGIC(lw);
         const int lms = lw * (e.rows + 1);
-        auto leaf = [&](tkey Pl, int amin_l, int amax_l, int y0l) {
+        // t: the area thresholds after every slice fixed above the leaf
+        auto leaf = [&](tkey Pl, Thr t, int y0l) {
           SCB_STAT(leaf_calls);
           const int rows_left = rows - y0l;
-          const Thr t = thresholds(amin_l, amax_l, win_lo, win_hi);
           const int hmin_a = imax(1, div_w(t.t2 + lw - 1, lmg));
           const int hmax_a = t.t1 < 0 ? 0 : div_w(t.t1, lmg);
           const int lo = imax(imax(hmin_a, rows_left - hmax_a), SCB_MSTAR(lms + rows_left));
@@ -1018,7 +1018,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         };
         if (nl == 1) {
           l = -1;  // no level above the leaf
-          leaf(P, amin, amax, 0);
+          leaf(P, thresholds(amin, amax, win_lo, win_hi), 0);
           continue;
         }
         // ---- heights DFS over the levels above the leaf (search.cpp:163-190)
@@ -1048,7 +1048,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
               if (h > hhi) break;
               const int a1 = cw * h;
               const tkey Pn = kmax(cPin, rt[(size_t)(crow + h) * FPW + f]);
-              leaf(Pn, imin(cAmin, a1), imax(cAmax, a1), y0 + h);
+              leaf(Pn, thresholds(imin(cAmin, a1), imax(cAmax, a1), win_lo, win_hi), y0 + h);
               SCB_SYNCWARP();
             }
           } else if (forced && l == nl - 2) {
@@ -1064,7 +1064,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
               const tkey Pn = kmax(cPin, e.rts[(size_t)(crow + h) * FPW + f]);
               const Thr tn = thresholds(na, nx, win_lo, win_hi);
               if (tn.t2 > sn.d || tn.t1 < sn.c) continue;
-              leaf(Pn, na, nx, 0);
+              leaf(Pn, tn, 0);
               SCB_SYNCWARP();
             }
           } else {
@@ -1129,7 +1129,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             crow = clbase + SCB_YBASE(y0) - 1;
             continue;
           }
-          leaf(Pn, na, nx, y0n);
+          leaf(Pn, tn, y0n);
         }
       }
     }
