@@ -77,7 +77,7 @@ SCB_HD tkey umin3(tkey a, tkey b, tkey c) {
 // memory on the GPU (int offsets; curH bytes at kUniH).
 constexpr int kUniW = 0, kUniR = 16, kUniX0 = 32, kUniWL = 49, kUniWH = 66, kUniRL = 83,
               kUniRH = 99, kUniSL = 115, kUniH = 131, kUniSMN = 147, kUniSMX = 164,
-              kUniInts = 184;  // 736 B
+              kUniCR1 = 184, kUniCR2 = 200, kUniInts = 216;  // 864 B
 
 // one 16-byte record of the heights DFS (a single 128-bit local access)
 struct alignas(16) Lvl {
@@ -311,7 +311,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   // warp-uniform DFS state (identical in every lane of the warp)
   int W_[SC_MAX_COLS], R_[SC_MAX_COLS], X0_[SC_MAX_COLS + 1], RS0[SC_MAX_COLS];
   int WL_[SC_MAX_COLS + 1], WH_[SC_MAX_COLS + 1], RL_[SC_MAX_COLS], RH_[SC_MAX_COLS],
-      SL_[SC_MAX_COLS], SMN_[SC_MAX_COLS + 1], SMX_[SC_MAX_COLS + 1];
+      SL_[SC_MAX_COLS], SMN_[SC_MAX_COLS + 1], SMX_[SC_MAX_COLS + 1], CR1_[SC_MAX_COLS],
+      CR2_[SC_MAX_COLS];
   uint8_t curH_[SC_MAX_SLICES];
   // exhaustive walks on the GPU: these warp-uniform DFS arrays live once per
   // warp in shared memory (WalkEnv::uni, layout kUni*); pruned walks and the
@@ -332,6 +333,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
   uint8_t* const curH = kUniform ? reinterpret_cast<uint8_t*>(e.uni + kUniH) : curH_;
   int* const SMN = kUniform ? e.uni + kUniSMN : SMN_;
   int* const SMX = kUniform ? e.uni + kUniSMX : SMX_;
+  int* const CR1 = kUniform ? e.uni + kUniCR1 : CR1_;  // per column: run counts whose
+  int* const CR2 = kUniform ? e.uni + kUniCR2 : CR2_;  // window meets the widths hull
   // pruned walks: heights-DFS state per level in local arrays
   uint8_t Lcol[kMaxLevels], Lrun[kMaxLevels], Ly0[kMaxLevels], Lh[kMaxLevels], Lhi[kMaxLevels];
   int32_t Amin[kMaxLevels], Amax[kMaxLevels], Lbase[kMaxLevels];
@@ -590,6 +593,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         }
       }
       dead = r1 == 0;
+      CR1[j] = r1;
+      CR2[j] = r2;
       SMN[j] = SMN[j + 1] + r1;
       SMX[j] = SMX[j + 1] + r2;
     }
@@ -604,9 +609,9 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
     while (true) {
       if (kUniform) SCB_SYNCWARP();
       SCB_STAT(runs_steps);
-      const int rhi = imin(rows, SL[rp] - SMN[rp + 1]);
+      const int rhi = imin(CR2[rp], SL[rp] - SMN[rp + 1]);
       const int w = W[rp];
-      int r = imax(R[rp] + 1, SL[rp] - SMX[rp + 1]), lo = 0, hi = 0;
+      int r = imax(imax(R[rp] + 1, CR1[rp]), SL[rp] - SMX[rp + 1]), lo = 0, hi = 0;
       bool found = false;
       for (; r <= rhi; ++r) {
         lo = SCB_ILO(w * e.rstride + r);
