@@ -965,6 +965,10 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
         const uint64_t lmg = SCB_MAGIC(lw);
         const int lms = lw * (e.rows + 1);
         // t: the area thresholds after every slice fixed above the leaf
+        // candidates counted by the leaves since the last flush into `ord`: a
+        // 32-bit add per leaf (a level has at most 255 heights of at most 255
+        // candidates each between flushes)
+        uint32_t ordl = 0;
         auto leaf = [&](tkey Pl, Thr t, int y0l) {
           SCB_STAT(leaf_calls);
           const int rows_left = rows - y0l;
@@ -1000,7 +1004,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
                 const tkey* q = p0;
   #pragma unroll 1
                 for (int hh = lo + slot; hh <= hi; hh += J, q += 32)
-                  score(kmax(Pl, *q), ord + (uint64_t)(hh - lo), lr, hh, rows_left - hh);
+                  score(kmax(Pl, *q), ord + (uint64_t)(ordl + (uint32_t)(hh - lo)), lr, hh, rows_left - hh);
               }
             } else {  // pruned walks and step 2: leaves are few, winners common
               sync_heights();
@@ -1011,7 +1015,7 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
                 const int hn = hh + J;
                 const bool more = hn <= hi;
                 const tkey vn = more ? q[32] : 0;  // prefetch the next height
-                score(kmax(Pl, v), ord + (uint64_t)(hh - lo), lr, hh, rows_left - hh);
+                score(kmax(Pl, v), ord + (uint64_t)(ordl + (uint32_t)(hh - lo)), lr, hh, rows_left - hh);
                 if (!more) break;
                 hh = hn;
                 q += 32;
@@ -1019,11 +1023,12 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
               }
             }
           }
-          if (hi >= lo) ord += (uint64_t)(hi - lo + 1);
+          if (hi >= lo) ordl += (uint32_t)(hi - lo + 1);
         };
         if (nl == 1) {
           l = -1;  // no level above the leaf
           leaf(P, thresholds(amin, amax, win_lo, win_hi), 0);
+          ord += ordl;
           continue;
         }
         // ---- heights DFS over the levels above the leaf (search.cpp:163-190)
@@ -1056,6 +1061,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
               leaf(Pn, thresholds(imin(cAmin, a1), imax(cAmax, a1), win_lo, win_hi), y0 + h);
               SCB_SYNCWARP();
             }
+            ord += ordl;
+            ordl = 0;
           } else if (forced && l == nl - 2) {
             // the leaf's parent closes its column (forced rest): the leaf
             // starts the next column at row 0, whose fillability bounds are
@@ -1072,6 +1079,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
               leaf(Pn, tn, 0);
               SCB_SYNCWARP();
             }
+            ord += ordl;
+            ordl = 0;
           } else {
             ++h;
             if (e.patho && !forced)
@@ -1135,6 +1144,8 @@ SCB_HD void walk_item(const WalkEnv& e, uint64_t item, const WorkItem& wi, int f
             continue;
           }
           leaf(Pn, tn, y0n);
+          ord += ordl;
+          ordl = 0;
         }
       }
     }
