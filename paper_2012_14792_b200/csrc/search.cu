@@ -39,14 +39,16 @@ namespace scb {
 #ifndef SCB_SEARCH_BLOCK
 #define SCB_SEARCH_BLOCK 256
 #endif
-// Exhaustive step 1 (the headline walk, warp-uniform): 64-thread blocks under
+// Exhaustive step 1 (the headline walk, warp-uniform): 128-thread blocks under
 // a register cap (__maxnreg__) instead of a blocks-per-SM launch bound; the
-// cap keeps ptxas at <= 96 registers, so the register file holds 10 blocks =
-// 20 warps/SM.  Measured on cfg3, step-1 ms by cap ->
-// registers chosen: 96 -> 89: 4.47, 100 -> 92: 4.49, uncapped (128) -> 102
-// (9 blocks): 4.79; 256-thread blocks at 16 warps/SM were 7 % slower.
+// cap keeps ptxas at <= 96 registers (86 used), so the register file holds 20
+// warps/SM.  Measured on cfg3, step-1 ms: block 128 / 160 /
+// 320 (5 / 4 / 2 blocks): 4.31; 64 (10 blocks, twice the per-block table
+// copies in shared memory, less L1): 4.39; 192 (3 blocks, 18 warps): 4.56.
+// Cap -> registers (64-thread blocks): 96 -> 89: 4.47, 100 -> 92: 4.49,
+// uncapped -> 102 (fewer warps): 4.79.
 #ifndef SCB_SEARCH_BLOCK1
-#define SCB_SEARCH_BLOCK1 64
+#define SCB_SEARCH_BLOCK1 128
 #endif
 #ifndef SCB_SEARCH_REGS1
 #define SCB_SEARCH_REGS1 96
