@@ -1,10 +1,15 @@
 // Drop-in binding of the B200 partitioner core for code written against the
 // reference `slicecraft` API (proj/include/slicecraft/*.hpp).
 //
-// Header-only; compile it together with the reference headers and link
-// libslicecraft_b200.so.  Every function takes and returns the reference's own
-// types and throws the reference's own exception classes (errors.hpp:10-85);
-// the compute runs in the sm_100a kernels behind include/slicecraft_b200.h.
+// Compile it together with the reference headers (the API contract) and link
+// libslicecraft_dropin.so (dropin/slicecraft_api.cpp: every out-of-line
+// function those headers declare, on the C-ABI) + libslicecraft_b200.so; no
+// reference library is needed.  Every function takes and returns the
+// reference's own types and throws the reference's own exception classes
+// (errors.hpp:10-85); the compute runs in the sm_100a kernels behind
+// include/slicecraft_b200.h.  The functions below take an explicit Context
+// and search mode; the unqualified slicecraft:: functions use the implicit
+// per-thread context.
 //
 //   slicecraft::ctu_stats(luma, grid, poc)              -> b200::ctu_stats(ctx, ...)
 //   slicecraft::min_time_search(est, cfg)               -> b200::min_time_search(ctx, ...)
@@ -52,6 +57,16 @@ namespace b200 {
 inline void check(sc_status s) {
   if (s != SC_OK) rethrow(s);
 }
+
+class Context;
+// The implicit context behind the reference-API functions of the link-level
+// drop-in (dropin/slicecraft_api.cpp, libslicecraft_dropin.so): one per host
+// thread on device SLICECRAFT_B200_DEVICE (default 0), searching in
+// SLICECRAFT_B200_MODE (exhaustive, or pruned) unless set here.
+void set_default_device(int device);
+void set_default_mode(int mode);  // SC_MODE_EXHAUSTIVE / SC_MODE_PRUNED
+int default_mode();
+Context& default_context();
 
 // One device context (streams, device tables, cached search plans).
 class Context {
@@ -105,19 +120,21 @@ inline Partition to_partition(const CtuGrid& g, const sc_layout& L) {
   return p;
 }
 
-// uniform_partition (grid.cpp:186-262) through sc_uniform_partition.
+// uniform_partition (grid.cpp:186-262) through sc_uniform_partition_n.
 inline Partition uniform_partition(const CtuGrid& g, int n_slices) {
   const sc_grid cg = to_c(g);
-  sc_partition u;
-  check(sc_uniform_partition(&cg, n_slices, &u));
+  const std::size_t n = static_cast<std::size_t>(n_slices > 0 ? n_slices : 1);
+  std::vector<int32_t> cw(n), rh(n);
+  std::vector<sc_rect> s(n);
+  int32_t nc = 0, nr = 0;
+  check(sc_uniform_partition_n(&cg, n_slices, cw.data(), &nc, rh.data(), &nr, s.data()));
   Partition p;
   p.grid = g;
   p.origin = PartitionOrigin::Uniform;
-  p.tiles.col_widths.assign(u.tile_col_widths, u.tile_col_widths + u.n_tile_cols);
-  p.tiles.row_heights.assign(u.tile_row_heights, u.tile_row_heights + u.n_tile_rows);
-  for (int i = 0; i < u.n_slices; ++i)
-    p.slices.push_back(RectSlice{u.slices[i].x0, u.slices[i].y0, u.slices[i].w, u.slices[i].h,
-                                 u.slices[i].id});
+  p.tiles.col_widths.assign(cw.begin(), cw.begin() + nc);
+  p.tiles.row_heights.assign(rh.begin(), rh.begin() + nr);
+  for (int i = 0; i < n_slices; ++i)
+    p.slices.push_back(RectSlice{s[i].x0, s[i].y0, s[i].w, s[i].h, s[i].id});
   return p;
 }
 

@@ -165,6 +165,10 @@ sc_status sc_grid_make(int32_t frame_width, int32_t frame_height, int32_t ctu_si
 /* temporal_layer_of_poc (cost.cpp:28-38, cost.hpp:39) */
 sc_status sc_temporal_layer(int32_t poc, int32_t gop_size, int32_t* out);
 
+/* SearchConfig::check (search.cpp:28-36): ConfigError for n_slices < 1,
+ * k_area <= 1, lambda < 0 or not finite, workers < 1, max_tile_cols < 0. */
+sc_status sc_search_cfg_check(const sc_search_cfg* cfg);
+
 /* ---- context ------------------------------------------------------------ */
 sc_status sc_ctx_create(int32_t device, sc_ctx** out);
 sc_status sc_ctx_destroy(sc_ctx* ctx);
@@ -236,6 +240,11 @@ sc_status sc_grid_tables(sc_ctx* ctx, const sc_grid* grid, const double* est_tim
 /* uniform_partition (grid.cpp:186-262).  GeometryError if n_slices is not in
  * [1, cells]. */
 sc_status sc_uniform_partition(const sc_grid* grid, int32_t n_slices, sc_partition* out);
+/* uniform_partition for any n in [1, cells] into caller arrays of n_slices
+ * entries each (tile widths, tile heights, slices in id order). */
+sc_status sc_uniform_partition_n(const sc_grid* grid, int32_t n_slices, int32_t* tile_col_widths,
+                                 int32_t* n_tile_cols, int32_t* tile_row_heights,
+                                 int32_t* n_tile_rows, sc_rect* slices);
 /* partition_time + partition_sse (+ slice_moments) of one partition on
  * n_frames frames, on the device.  slices: n_slices rects whose ids are a
  * permutation of 0..n_slices-1 (host pointer).  est_times / records: host or
@@ -273,6 +282,75 @@ sc_status sc_partition_frames(sc_ctx* ctx, const sc_grid* grid, const sc_search_
 /* for_each_candidate / enumerate_candidates count (search.cpp:302-326). */
 sc_status sc_count_candidates(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
                               uint64_t* count);
+
+/* ---- device post-check and candidate stream ---------------------------- */
+/* validate_partition (grid.cpp:86-184): the tile and per-slice bound / id
+ * checks on the host, then the exact-disjoint-cover and structure checks in
+ * one device block, with the reference's error classes and first-failure
+ * order (GeometryError, CoverageError, OverlapError, StructureError).
+ * slice_map (cols*rows, host or device, may be NULL): the slice id of every
+ * CTU (-1 where none) -- written on success and on Overlap/Coverage/Structure
+ * failures. */
+sc_status sc_validate_partition(sc_ctx* ctx, const sc_grid* grid, int32_t n_tile_cols,
+                                const int32_t* tile_col_widths, int32_t n_tile_rows,
+                                const int32_t* tile_row_heights, const sc_rect* slices,
+                                int32_t n_slices, int32_t* slice_map);
+/* The CTU -> slice-id maps (n_frames * cols * rows, -1 for cells outside the
+ * layout's tile columns, as render_ascii's '?', grid.cpp:279-287) of the
+ * step-1 argmin (step=1) or step-2 best (step=2) partitions the last search
+ * call on this context returned.  Every returned partition passes the device
+ * post-check (validate_partition over the columns its widths span) before
+ * the call returns; SLICECRAFT_B200_POSTCHECK=0 skips it (no maps then). */
+sc_status sc_result_slice_maps(sc_ctx* ctx, int32_t step, int32_t n_frames, int32_t* out);
+/* for_each_candidate / enumerate_candidates (search.cpp:302-326) as a
+ * device-materialised stream: the candidates with ordinals [first, first +
+ * max_out) of the family's enumeration order, as layouts (out, host).
+ * *n_out = candidates written, *total = family size.  The first call per
+ * (grid, config) counts the family on the device (families above 2^36
+ * candidates: SizeError).  UniformOnly: total is 0 or 1 and its candidate is
+ * sc_uniform_partition(grid, n) (out[0].n_cols == 0). */
+sc_status sc_enumerate_candidates(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                                  uint64_t first, uint64_t max_out, sc_layout* out,
+                                  uint64_t* n_out, uint64_t* total);
+
+/* ---- host-side model pieces (no device needed) -------------------------- */
+/* CostSource (cost.hpp:11-16). */
+enum {
+  SC_SOURCE_MEASURED = 0,
+  SC_SOURCE_CO_TEMPORAL_LAYER = 1,
+  SC_SOURCE_MOST_RECENT_ANY = 2,
+  SC_SOURCE_UNIFORM = 3
+};
+/* CostHistory::append validation (cost.cpp:45-64) of a map about to join a
+ * history whose maps carry history_pocs: GeometryError (grid, entry count),
+ * FormatError (a time not finite or < 0), TraceError (duplicate poc). */
+sc_status sc_cost_map_check(const sc_grid* history_grid, const sc_grid* map_grid,
+                            const double* times, int64_t n_times, int32_t poc,
+                            const int32_t* history_pocs, int32_t n_history);
+/* estimate_ctu_times (cost.cpp:66-95) over a history of n_maps maps (encode
+ * order; maps[i] points at cols*rows times, pocs / temporal_layers per map):
+ * the most recent map of poc's temporal layer (gop_size, ConfigError), else
+ * the most recent map, else all-ones.  out: cols*rows times; source
+ * (SC_SOURCE_*), source_poc (-1 for Uniform) and the temporal layer of poc
+ * (may be NULL). */
+sc_status sc_estimate_ctu_times(const sc_grid* grid, int32_t gop_size, int32_t n_maps,
+                                const double* const* maps, const int32_t* pocs,
+                                const int32_t* temporal_layers, int32_t poc, double* out,
+                                int32_t* source, int32_t* source_poc, int32_t* temporal_layer);
+/* TextureStats ctor (texture.cpp:90-130): validates n_records records
+ * (GeometryError on the count, FormatError on pixel counts / moments) and
+ * builds the (cols+1)*(rows+1) u64 inclusion-exclusion tables (any output may
+ * be NULL). */
+sc_status sc_texture_tables(const sc_grid* grid, const sc_ctu_record* records, int64_t n_records,
+                            uint64_t* pre_count, uint64_t* pre_sum, uint64_t* pre_sumsq);
+/* SliceMoments::sse (texture.cpp:83-88). */
+sc_status sc_moments_sse(const sc_ctu_record* moments, double* out);
+/* PrefixSumTable (cost.cpp:97-112): the f64 summed-area table,
+ * (cols+1)*(rows+1) doubles in the reference's operation order. */
+sc_status sc_prefix_sum_table(const double* values, int64_t n_values, int32_t cols, int32_t rows,
+                              double* table);
+/* split_even (grid.cpp:52-60). */
+sc_status sc_split_even(int32_t total, int32_t parts, int32_t* out);
 
 /* ---- multi-GPU shard merge --------------------------------------------- */
 /* Opaque per-frame shard best, exchanged by an all-gather (NCCL or gloo). */

@@ -92,12 +92,15 @@ SIGNATURES = [
     ("sc_abi_version", C.c_int, []),
     ("sc_grid_make", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(Grid)]),
     ("sc_temporal_layer", C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32)]),
+    ("sc_search_cfg_check", C.c_int, [C.POINTER(SearchCfg)]),
     ("sc_ctx_create", C.c_int, [C.c_int32, C.POINTER(_P)]),
     ("sc_ctx_destroy", C.c_int, [_P]),
     ("sc_ctx_set_shard", C.c_int, [_P, C.c_int32, C.c_int32]),
     ("sc_ctx_set_stream", C.c_int, [_P, _P]),
     ("sc_ctx_timings", C.c_int, [_P, _P]),
     ("sc_uniform_partition", C.c_int, [C.POINTER(Grid), C.c_int32, C.POINTER(PartitionC)]),
+    ("sc_uniform_partition_n", C.c_int, [C.POINTER(Grid), C.c_int32, _P, C.POINTER(C.c_int32),
+                                         _P, C.POINTER(C.c_int32), _P]),
     ("sc_yuv_frame_count", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32,
                                      C.POINTER(C.c_int32)]),
     ("sc_yuv_load_luma", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
@@ -124,6 +127,21 @@ SIGNATURES = [
                                       _P]),
     ("sc_count_candidates", C.c_int, [_P, C.POINTER(Grid), C.POINTER(SearchCfg),
                                       C.POINTER(C.c_uint64)]),
+    ("sc_validate_partition", C.c_int, [_P, C.POINTER(Grid), C.c_int32, _P, C.c_int32, _P, _P,
+                                        C.c_int32, _P]),
+    ("sc_result_slice_maps", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
+    ("sc_enumerate_candidates", C.c_int, [_P, C.POINTER(Grid), C.POINTER(SearchCfg), C.c_uint64,
+                                          C.c_uint64, _P, C.POINTER(C.c_uint64),
+                                          C.POINTER(C.c_uint64)]),
+    ("sc_cost_map_check", C.c_int, [C.POINTER(Grid), C.POINTER(Grid), _P, C.c_int64, C.c_int32,
+                                    _P, C.c_int32]),
+    ("sc_estimate_ctu_times", C.c_int, [C.POINTER(Grid), C.c_int32, C.c_int32, _P, _P, _P,
+                                        C.c_int32, _P, C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    ("sc_texture_tables", C.c_int, [C.POINTER(Grid), _P, C.c_int64, _P, _P, _P]),
+    ("sc_moments_sse", C.c_int, [C.POINTER(CtuRecord), C.POINTER(C.c_double)]),
+    ("sc_prefix_sum_table", C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P]),
+    ("sc_split_even", C.c_int, [C.c_int32, C.c_int32, _P]),
     ("sc_shard_export", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
     ("sc_shard_merge", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     ("sc_synth_luma", C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

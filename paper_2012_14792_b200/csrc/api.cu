@@ -50,13 +50,33 @@ void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_w
                      const unsigned long long* count, const unsigned long long* scored,
                      double lambda, const uint64_t* vals, const uint32_t* nvals, size_t nr,
                      FrameBest* out, int64_t* budget_out, cudaStream_t st);
+// device post-check and candidate stream (validate.cu, enumerate.cu)
+void validate_device(int n, const int* d_rects, int nbx, const int* d_bx, int nby, const int* d_by,
+                     int cols, int rows, int* d_owner, int32_t* d_map, VCheck* d_out,
+                     cudaStream_t st);
+void result_maps_device(const FrameBest* d_fb, int frames, int n, int cols, int rows, int* d_owner,
+                        int32_t* d_maps, VCheck* d_out, cudaStream_t st);
+void enumerate_count_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
+                            double k, int covering, uint64_t* d_counts, uint64_t* d_offsets,
+                            DevBuf& temp, cudaStream_t st);
+void enumerate_emit_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
+                           double k, int covering, const uint64_t* d_counts,
+                           const uint64_t* d_offsets, uint64_t first, uint64_t limit,
+                           uint8_t* d_out, cudaStream_t st);
+}  // namespace scb
+
+namespace scb {
+thread_local std::string g_last_error;
+// shared with host.cpp: the thread's sc_last_error() message
+sc_status set_last_error(sc_status s, const char* msg) {
+  g_last_error = msg;
+  return s;
+}
 }  // namespace scb
 
 using namespace scb;
 
 namespace {
-
-thread_local std::string g_last_error;
 
 sc_status set_error(sc_status s, const std::string& m) {
   g_last_error = m;
@@ -99,8 +119,8 @@ void check_grid(const sc_grid* g) {
     fail(SC_ERR_GEOMETRY, "grid cols/rows inconsistent with frame and CTU size");
 }
 
-// SearchConfig::check (search.cpp:28-36) + the kernels' compiled limits.
-int check_cfg(const sc_grid& g, const sc_search_cfg* c) {
+// SearchConfig::check (search.cpp:28-36), same order and messages.
+void check_cfg_fields(const sc_search_cfg* c) {
   if (!c) fail(SC_ERR_USAGE, "cfg is NULL");
   if (c->n_slices < 1) fail(SC_ERR_CONFIG, "n_slices must be >= 1");
   if (!(c->k_area > 1.0)) fail(SC_ERR_CONFIG, "k_area must be > 1");
@@ -108,6 +128,11 @@ int check_cfg(const sc_grid& g, const sc_search_cfg* c) {
     fail(SC_ERR_CONFIG, "lambda must be finite and >= 0");
   if (c->workers < 1) fail(SC_ERR_CONFIG, "workers must be >= 1");
   if (c->max_tile_cols < 0) fail(SC_ERR_CONFIG, "max_tile_cols must be >= 0");
+}
+
+// SearchConfig::check + the B200 fields and the kernels' compiled limits.
+int check_cfg(const sc_grid& g, const sc_search_cfg* c) {
+  check_cfg_fields(c);
   if (c->family != SC_FAMILY_COLUMN_SPLIT && c->family != SC_FAMILY_UNIFORM_ONLY)
     fail(SC_ERR_CONFIG, "unknown candidate family");
   if (c->coverage != SC_COVERAGE_REFERENCE && c->coverage != SC_COVERAGE_COVERING)
@@ -409,6 +434,12 @@ bool item_filter_enabled() {
   return !(v && v[0] == '0');
 }
 
+// Device post-check of returned partitions (SLICECRAFT_B200_POSTCHECK=0: off).
+bool postcheck_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_POSTCHECK");
+  return !(v && v[0] == '0');
+}
+
 bool schedule_enabled() {
   const char* v = getenv("SLICECRAFT_B200_SCHEDULE");
   return !(v && v[0] == '0');
@@ -645,7 +676,8 @@ UniformPartition uniform_or_fail(const sc_grid& g, int n) {
   UniformPartition u;
   if (n < 1) fail(SC_ERR_GEOMETRY, "slice count must be >= 1");
   if (!uniform_partition(g.cols, g.rows, n, u))
-    fail(SC_ERR_GEOMETRY, "slice count exceeds CTU cell count");
+    fail(SC_ERR_GEOMETRY, "slice count " + std::to_string(n) + " exceeds CTU cell count " +
+                              std::to_string(g.cols * g.rows));
   return u;
 }
 
@@ -725,6 +757,7 @@ void run_uniform(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int fr
   const UniformPartition u = uniform_or_fail(g, cfg.n_slices);
   if (!uniform_area_ok(u, cfg.k_area))
     fail(SC_ERR_NO_CANDIDATE, "uniform partition violates the area constraint");
+  ctx->maps_frames[0] = ctx->maps_frames[1] = 0;  // no ColumnSplit layouts returned
   cudaStream_t s = main_stream(ctx);
   cudaEvent_t* ev = ctx->ev;
   SCB_CUDA(cudaEventRecord(ev[0], s));
@@ -849,6 +882,28 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   SCB_CUDA(cudaEventRecord(ev[8], s));
   if (do2) enqueue_step(ctx, g, cfg, plan, L, 2, !do1 || step2_bounded(cfg), s);
   SCB_CUDA(cudaEventRecord(ev[3], s));
+  // device post-check of the partitions this call returns (validate_partition,
+  // grid.cpp:86-184, over the columns the layout spans) and their CTU ->
+  // slice-id maps (sc_result_slice_maps)
+  const bool post = postcheck_enabled();
+  const size_t vb = (size_t)frames * sizeof(VCheck);
+  if (post) {
+    ctx->slice_maps.ensure((size_t)2 * frames * cells * sizeof(int32_t));
+    ctx->owner.ensure((size_t)frames * cells * sizeof(int));
+    ctx->vcheck.ensure(2 * vb);
+    ctx->h_vcheck.ensure(2 * vb);
+    for (int st = 1; st <= 2; ++st) {
+      if (st == 1 ? !do1 : !do2) continue;
+      result_maps_device(ctx->frame_best.as<FrameBest>() + (size_t)(st - 1) * L.groups * L.fpw,
+                         frames, cfg.n_slices, g.cols, g.rows, ctx->owner.as<int>(),
+                         ctx->slice_maps.as<int32_t>() + (size_t)(st - 1) * frames * cells,
+                         ctx->vcheck.as<VCheck>() + (size_t)(st - 1) * frames, s);
+    }
+    SCB_CUDA(cudaMemcpyAsync(ctx->h_vcheck.p, ctx->vcheck.p, 2 * vb, cudaMemcpyDeviceToHost, s));
+  }
+  ctx->maps_cells = cells;
+  ctx->maps_frames[0] = post && do1 ? frames : 0;
+  ctx->maps_frames[1] = post && do2 ? frames : 0;
   const size_t nfb = (size_t)2 * L.groups * L.fpw;
   ctx->h_frame_best.ensure(nfb * sizeof(FrameBest));
   SCB_CUDA(cudaMemcpyAsync(ctx->h_frame_best.p, ctx->frame_best.p, nfb * sizeof(FrameBest),
@@ -859,6 +914,18 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   SCB_CUDA(cudaEventRecord(ev[9], s));
   SCB_CUDA(cudaStreamSynchronize(s));
   finish_schedule(plan);
+  if (post) {
+    const VCheck* vc = ctx->h_vcheck.as<VCheck>();
+    for (int st = 1; st <= 2; ++st)
+      for (int f = 0; f < frames && ctx->maps_frames[st - 1]; ++f) {
+        const VCheck& v = vc[(size_t)(st - 1) * frames + f];
+        if (v.status != SC_OK)
+          fail(SC_ERR_INTERNAL, "device post-check: the step-" + std::to_string(st) +
+                                    " partition of frame " + std::to_string(f) +
+                                    " failed validate_partition (status " +
+                                    std::to_string(v.status) + ")");
+      }
+  }
 #ifdef SCB_DIAG_COSTS
   if (const char* path = getenv("SCB_DIAG_COSTS_OUT")) {
     std::vector<uint32_t> cost(plan->items.size());
@@ -882,6 +949,7 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   ctx->last_best[0].assign(b1, b1 + frames);
   ctx->last_best[1].assign(b2, b2 + frames);
   ctx->last_pruned = cfg.mode == SC_MODE_PRUNED;
+  ctx->last_fpw = L.fpw;
   // walks that skip subtrees report the family's exact DP count (plan.h);
   // shards export it from rank 0 only
   const bool dp1 = cfg.mode == SC_MODE_PRUNED;
@@ -949,8 +1017,10 @@ sc_ctx::~sc_ctx() {
   for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rt_split, &rs_search, &usat,
                   &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc, &rt_bits, &vals, &nvals, &budget_f64, &rk_idx, &rk_sorted,
                   &rk_flags, &rk_offsets, &rk_temp, &sse_inc, &flt_idx, &flt_flag, &flt_list,
-                  &flt_count, &flt_temp})
+                  &flt_count, &flt_temp, &slice_maps, &owner, &vcheck, &val_in, &enum_out,
+                  &enum_temp})
     b->release();
+  h_vcheck.release();
   h_stage.release();
   h_luma.release();
   h_records.release();
@@ -961,6 +1031,8 @@ sc_ctx::~sc_ctx() {
     p->d_bmax.release();
     p->d_order.release();
     p->d_cost.release();
+    p->d_enum_counts.release();
+    p->d_enum_offsets.release();
     delete p;
   }
   for (auto& e : ev)
@@ -1002,6 +1074,10 @@ sc_status sc_temporal_layer(int32_t poc, int32_t gop, int32_t* out) {
     const unsigned rem = (unsigned)poc % (unsigned)gop;
     *out = rem == 0 ? 0 : (__builtin_ctz((unsigned)gop) - __builtin_ctz(rem));
   });
+}
+
+sc_status sc_search_cfg_check(const sc_search_cfg* cfg) {
+  return guarded([&] { check_cfg_fields(cfg); });
 }
 
 sc_status sc_ctx_create(int32_t device, sc_ctx** out) {
@@ -1309,6 +1385,24 @@ sc_status sc_uniform_partition(const sc_grid* grid, int32_t n_slices, sc_partiti
   });
 }
 
+sc_status sc_uniform_partition_n(const sc_grid* grid, int32_t n_slices, int32_t* tile_col_widths,
+                                 int32_t* n_tile_cols, int32_t* tile_row_heights,
+                                 int32_t* n_tile_rows, sc_rect* slices) {
+  return guarded([&] {
+    if (!tile_col_widths || !n_tile_cols || !tile_row_heights || !n_tile_rows || !slices)
+      fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const UniformPartition u = uniform_or_fail(*grid, n_slices);
+    *n_tile_cols = (int32_t)u.tile_cols.size();
+    *n_tile_rows = (int32_t)u.tile_rows.size();
+    for (size_t i = 0; i < u.tile_cols.size(); ++i) tile_col_widths[i] = u.tile_cols[i];
+    for (size_t i = 0; i < u.tile_rows.size(); ++i) tile_row_heights[i] = u.tile_rows[i];
+    for (int i = 0; i < n_slices; ++i)
+      slices[i] = sc_rect{u.rects[4 * i], u.rects[4 * i + 1], u.rects[4 * i + 2],
+                          u.rects[4 * i + 3], i};
+  });
+}
+
 sc_status sc_partition_eval(sc_ctx* ctx, const sc_grid* grid, const sc_rect* slices,
                             int32_t n_slices, const double* est, const sc_ctu_record* records,
                             int32_t frames, sc_partition_stats* out, double* slice_times,
@@ -1361,7 +1455,9 @@ sc_status sc_shard_export(sc_ctx* ctx, int32_t step, int32_t frames, sc_shard_be
       s.ord = b.found ? b.ord : ~0ull;
       s.count = b.count;
       s.count_hi = ctx->last_count_hi[step - 1];
-      s.leaves = b.count;
+      // leaves this shard actually scored (per frame; the walks count
+      // candidate-frame scores for the whole warp)
+      s.leaves = b.scored / (uint64_t)ctx->last_fpw;
       layout_from_snap(b, SC_MAX_SLICES, &s.layout);
     }
   });
@@ -1374,9 +1470,11 @@ sc_status sc_shard_merge(int32_t step, int32_t world, int32_t frames,
     for (int f = 0; f < frames; ++f) {
       int win = -1;
       unsigned __int128 total = 0;
+      uint64_t leaves = 0;
       for (int r = 0; r < world; ++r) {
         const sc_shard_best& s = gathered[(size_t)r * frames + f];
         total += ((unsigned __int128)s.count_hi << 64) | s.count;
+        leaves += s.leaves;
         if (s.item == ~0ull) continue;
         if (win < 0) { win = r; continue; }
         const sc_shard_best& b = gathered[(size_t)win * frames + f];
@@ -1398,17 +1496,179 @@ sc_status sc_shard_merge(int32_t step, int32_t world, int32_t frames,
         r.argmin = L;
         r.candidates_step1 = (uint64_t)total;
         r.candidates_step1_hi = (uint64_t)(total >> 64);
-        r.leaves_scored_step1 = (uint64_t)total;
+        r.leaves_scored_step1 = leaves;
       } else {
         r.t_best_us = bits_to_double(b.key_t);
         r.sse_best = b.key_sse;
         r.best = L;
         r.candidates_step2 = (uint64_t)total;
         r.candidates_step2_hi = (uint64_t)(total >> 64);
-        r.leaves_scored_step2 = (uint64_t)total;
+        r.leaves_scored_step2 = leaves;
       }
       r.candidates_evaluated = r.candidates_step1 + r.candidates_step2;
     }
+  });
+}
+
+sc_status sc_validate_partition(sc_ctx* ctx, const sc_grid* grid, int32_t n_tile_cols,
+                                const int32_t* tile_col_widths, int32_t n_tile_rows,
+                                const int32_t* tile_row_heights, const sc_rect* slices,
+                                int32_t n_slices, int32_t* slice_map) {
+  return guarded([&] {
+    if (!ctx || (n_tile_cols > 0 && !tile_col_widths) || (n_tile_rows > 0 && !tile_row_heights) ||
+        (n_slices > 0 && !slices))
+      fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const sc_grid& g = *grid;
+    // host part of validate_partition (grid.cpp:86-124): tiles, then each
+    // slice's bounds and id, in list order
+    if (n_tile_cols < 1 || n_tile_rows < 1)
+      fail(SC_ERR_GEOMETRY, "tile grid must have at least one column and row");
+    for (int i = 0; i < n_tile_cols; ++i)
+      if (tile_col_widths[i] < 1) fail(SC_ERR_GEOMETRY, "tile column width must be >= 1");
+    for (int i = 0; i < n_tile_rows; ++i)
+      if (tile_row_heights[i] < 1) fail(SC_ERR_GEOMETRY, "tile row height must be >= 1");
+    std::vector<int> bx(1, 0), by(1, 0);
+    for (int i = 0; i < n_tile_cols; ++i) bx.push_back(bx.back() + tile_col_widths[i]);
+    for (int i = 0; i < n_tile_rows; ++i) by.push_back(by.back() + tile_row_heights[i]);
+    if (bx.back() != g.cols || by.back() != g.rows)
+      fail(SC_ERR_GEOMETRY, "tile sums (" + std::to_string(bx.back()) + "x" +
+                                std::to_string(by.back()) + ") do not match grid (" +
+                                std::to_string(g.cols) + "x" + std::to_string(g.rows) + ")");
+    if (n_slices < 1) fail(SC_ERR_COVERAGE, "partition has no slices");
+    std::vector<char> seen((size_t)n_slices, 0);
+    std::vector<int> rects((size_t)n_slices * 5);
+    for (int i = 0; i < n_slices; ++i) {
+      const sc_rect& r = slices[i];
+      if (r.w < 1 || r.h < 1 || r.x0 < 0 || r.y0 < 0 || r.x0 + r.w > g.cols ||
+          r.y0 + r.h > g.rows)
+        fail(SC_ERR_GEOMETRY, "slice " + std::to_string(r.id) + " (" + std::to_string(r.x0) +
+                                  "," + std::to_string(r.y0) + " " + std::to_string(r.w) + "x" +
+                                  std::to_string(r.h) + ") outside the " + std::to_string(g.cols) +
+                                  "x" + std::to_string(g.rows) + " grid");
+      if (r.id < 0 || r.id >= n_slices || seen[(size_t)r.id])
+        fail(SC_ERR_GEOMETRY, "slice ids must be a permutation of 0..n-1");
+      seen[(size_t)r.id] = 1;
+      int* d = &rects[(size_t)i * 5];
+      d[0] = r.x0, d[1] = r.y0, d[2] = r.w, d[3] = r.h, d[4] = r.id;
+    }
+    // device part: exact disjoint cover, then structure (validate.cu)
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s = main_stream(ctx);
+    const size_t cells = (size_t)g.cols * g.rows;
+    const size_t nin = rects.size() + bx.size() + by.size();
+    ctx->val_in.ensure(nin * sizeof(int) + cells * sizeof(int32_t) + sizeof(VCheck));
+    int* d_rects = ctx->val_in.as<int>();
+    int* d_bx = d_rects + rects.size();
+    int* d_by = d_bx + bx.size();
+    int32_t* d_map = d_by + by.size();
+    VCheck* d_out = reinterpret_cast<VCheck*>(d_map + cells);
+    ctx->owner.ensure(cells * sizeof(int));
+    std::vector<int> in(rects);
+    in.insert(in.end(), bx.begin(), bx.end());
+    in.insert(in.end(), by.begin(), by.end());
+    SCB_CUDA(cudaMemcpyAsync(d_rects, in.data(), nin * sizeof(int), cudaMemcpyHostToDevice, s));
+    validate_device(n_slices, d_rects, (int)bx.size(), d_bx, (int)by.size(), d_by, g.cols, g.rows,
+                    ctx->owner.as<int>(), d_map, d_out, s);
+    VCheck v;
+    SCB_CUDA(cudaMemcpyAsync(&v, d_out, sizeof(VCheck), cudaMemcpyDeviceToHost, s));
+    if (slice_map)
+      SCB_CUDA(cudaMemcpyAsync(slice_map, d_map, cells * sizeof(int32_t), cudaMemcpyDefault, s));
+    SCB_CUDA(cudaStreamSynchronize(s));
+    const std::string cell = "(" + std::to_string(v.x) + "," + std::to_string(v.y) + ")";
+    if (v.status == SC_ERR_OVERLAP)
+      fail(SC_ERR_OVERLAP, "slices " + std::to_string(v.a) + " and " + std::to_string(v.b) +
+                               " both cover cell " + cell);
+    if (v.status == SC_ERR_COVERAGE)
+      fail(SC_ERR_COVERAGE, "cell " + cell + " is not covered by any slice");
+    if (v.status == SC_ERR_STRUCTURE)
+      fail(SC_ERR_STRUCTURE, "slice " + std::to_string(v.a) +
+                                 " is neither a rectangle of complete tiles nor a CTU-row run "
+                                 "inside a single tile");
+  });
+}
+
+sc_status sc_result_slice_maps(sc_ctx* ctx, int32_t step, int32_t n_frames, int32_t* out) {
+  return guarded([&] {
+    if (!ctx || !out) fail(SC_ERR_USAGE, "NULL argument");
+    if (step != 1 && step != 2) fail(SC_ERR_USAGE, "step must be 1 or 2");
+    const int have = ctx->maps_frames[step - 1];
+    if (n_frames < 1 || n_frames > have)
+      fail(SC_ERR_USAGE, "the last search returned no step-" + std::to_string(step) +
+                             " partitions for that many frames");
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    SCB_CUDA(cudaMemcpy(out, ctx->slice_maps.as<int32_t>() + (size_t)(step - 1) * have * ctx->maps_cells,
+                        (size_t)n_frames * ctx->maps_cells * sizeof(int32_t), cudaMemcpyDefault));
+  });
+}
+
+sc_status sc_enumerate_candidates(sc_ctx* ctx, const sc_grid* grid, const sc_search_cfg* cfg,
+                                  uint64_t first, uint64_t max_out, sc_layout* out,
+                                  uint64_t* n_out, uint64_t* total) {
+  return guarded([&] {
+    if (!ctx || (max_out > 0 && !out)) fail(SC_ERR_USAGE, "NULL argument");
+    check_grid(grid);
+    const int maxc = check_cfg(*grid, cfg);
+    const sc_grid& g = *grid;
+    uint64_t n = 0, tot = 0;
+    if (cfg->family == SC_FAMILY_UNIFORM_ONLY) {
+      // for_each_candidate (search.cpp:308-312): the uniform partition if it
+      // passes the area test; out[0].n_cols = 0 marks it (sc_uniform_partition)
+      tot = uniform_area_ok(uniform_or_fail(g, cfg->n_slices), cfg->k_area) ? 1 : 0;
+      if (tot && first == 0 && max_out > 0) {
+        std::memset(out, 0, sizeof(sc_layout));
+        out[0].n_slices = cfg->n_slices;
+        n = 1;
+      }
+    } else {
+      SCB_CUDA(cudaSetDevice(ctx->device));
+      Plan* plan = get_plan(ctx, g, *cfg, maxc);
+      upload_plan(ctx, plan);
+      cudaStream_t s = main_stream(ctx);
+      const uint32_t ni = (uint32_t)plan->items.size();
+      if (!plan->have_enum) {
+        const unsigned __int128 dp = plan_count(plan, g, *cfg);
+        if (dp > ((unsigned __int128)1 << 36))
+          fail(SC_ERR_SIZE, "candidate stream limited to 2^36 candidates (the family has more)");
+        plan->d_enum_counts.ensure((size_t)ni * sizeof(uint64_t) + 8);
+        plan->d_enum_offsets.ensure((size_t)ni * sizeof(uint64_t) + 8);
+        enumerate_count_device(plan->d_items.as<WorkItem>(), ni, g.cols, g.rows, cfg->n_slices,
+                               cfg->k_area, cfg->coverage, plan->d_enum_counts.as<uint64_t>(),
+                               plan->d_enum_offsets.as<uint64_t>(), ctx->enum_temp, s);
+        uint64_t last[2] = {0, 0};
+        if (ni) {
+          SCB_CUDA(cudaMemcpyAsync(&last[0], plan->d_enum_offsets.as<uint64_t>() + ni - 1, 8,
+                                   cudaMemcpyDeviceToHost, s));
+          SCB_CUDA(cudaMemcpyAsync(&last[1], plan->d_enum_counts.as<uint64_t>() + ni - 1, 8,
+                                   cudaMemcpyDeviceToHost, s));
+        }
+        SCB_CUDA(cudaStreamSynchronize(s));
+        plan->enum_total = last[0] + last[1];
+        plan->have_enum = true;
+        if ((unsigned __int128)plan->enum_total != dp)
+          fail(SC_ERR_INTERNAL, "candidate stream count differs from the counting DP");
+      }
+      tot = plan->enum_total;
+      n = first < tot ? std::min<uint64_t>(max_out, tot - first) : 0;
+      if (n) {
+        ctx->enum_out.ensure((size_t)n * kSnapBytes);
+        enumerate_emit_device(plan->d_items.as<WorkItem>(), ni, g.cols, g.rows, cfg->n_slices,
+                              cfg->k_area, cfg->coverage, plan->d_enum_counts.as<uint64_t>(),
+                              plan->d_enum_offsets.as<uint64_t>(), first, n,
+                              ctx->enum_out.as<uint8_t>(), s);
+        std::vector<uint8_t> snaps((size_t)n * kSnapBytes);
+        SCB_CUDA(cudaMemcpyAsync(snaps.data(), ctx->enum_out.p, snaps.size(),
+                                 cudaMemcpyDeviceToHost, s));
+        SCB_CUDA(cudaStreamSynchronize(s));
+        FrameBest fb;
+        for (uint64_t i = 0; i < n; ++i) {
+          std::memcpy(fb.snap, snaps.data() + i * kSnapBytes, kSnapBytes);
+          layout_from_snap(fb, cfg->n_slices, &out[i]);
+        }
+      }
+    }
+    if (n_out) *n_out = n;
+    if (total) *total = tot;
   });
 }
 

@@ -5,7 +5,10 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "plan.h"
@@ -28,6 +31,29 @@ struct Fail {
     if (e_ != cudaSuccess)                                                          \
       ::scb::fail(SC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
+
+// ---- per-device kernel attributes ---------------------------------------------
+// cudaFuncSetAttribute acts on the current device only, so an opt-in (e.g. the
+// dynamic shared-memory limit) is applied once per (device, kernel), under a
+// lock: a process may drive several GPUs from several host threads.
+template <typename F>
+void once_per_device(const void* kernel, F&& set) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  SCB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, kernel})) return;
+  set();
+  done.insert({dev, kernel});
+}
+// The device's opt-in shared-memory limit per block (227 KB on B200).
+inline int smem_optin_bytes() {
+  int dev = 0, v = 0;
+  SCB_CUDA(cudaGetDevice(&dev));
+  SCB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  return v;
+}
 
 // ---- geometry --------------------------------------------------------------
 inline int cell_w(const sc_grid& g, int x) {
@@ -114,6 +140,10 @@ struct Plan {
   unsigned __int128 count = 0;
   DevBuf d_items, d_bmax;
   bool uploaded = false;
+  // candidate stream (enumerate.cu): per-item counts, their offsets, total
+  DevBuf d_enum_counts, d_enum_offsets;
+  bool have_enum = false;
+  uint64_t enum_total = 0;
 };
 
 // Per-lane best record written by the search kernels (one per lane of every
@@ -170,6 +200,14 @@ struct FrameBest {
   int32_t pad;
 };
 
+// Verdict of the device post-check of one partition (validate.cu).
+struct VCheck {
+  int32_t status;  // SC_OK, SC_ERR_OVERLAP, SC_ERR_COVERAGE, SC_ERR_STRUCTURE
+                   // (SC_ERR_GEOMETRY: a result snapshot that does not decode)
+  int32_t a, b;    // overlap: owner id, claiming id; structure: slice id
+  int32_t x, y;    // overlap / coverage: the cell
+};
+
 }  // namespace scb
 
 // The opaque context behind sc_ctx*.
@@ -193,6 +231,12 @@ struct sc_ctx {
   scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
   scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp;       // rank.cu scratch
   scb::DevBuf flt_idx, flt_flag, flt_list, flt_count, flt_temp;      // item filter (search.cu)
+  // device post-check of the returned partitions (validate.cu): CTU -> slice
+  // id maps [2][frames][cells] of the last search, owner scratch, verdicts
+  scb::DevBuf slice_maps, owner, vcheck, val_in, enum_out, enum_temp;
+  scb::HostBuf h_vcheck;
+  int maps_frames[2] = {0, 0};
+  size_t maps_cells = 0;
   int dec_cols = -1, dec_rows = -1;
   scb::HostBuf h_stage, h_records, h_frame_best, h_budget, h_luma;  // h_luma: YUV reads
   std::vector<scb::Plan*> plans;
@@ -200,6 +244,7 @@ struct sc_ctx {
   std::vector<scb::FrameBest> last_best[2];
   uint64_t last_leaves[2] = {0, 0};
   bool last_pruned = false;  // last search ran in SC_MODE_PRUNED (DP counts)
+  int last_fpw = 1;          // frames per warp of the last search (leaf counters)
   uint64_t last_count_hi[2] = {0, 0};  // high bits of this shard's DP count per step
   int diag_step = 0;         // diagnostics builds only
   ~sc_ctx();

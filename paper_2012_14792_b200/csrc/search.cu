@@ -194,8 +194,8 @@ __device__ __forceinline__ void search_body(const SearchArgs& a) {
   if (lane == 0 && sc) atomicAdd(a.scored_out, sc);
 }
 
-// The headline walk (exhaustive step 1) under a register cap that keeps 10
-// blocks of 2 warps resident; the other walks under a plain launch bound.
+// The headline walk (exhaustive step 1) under a register cap (5 blocks of 4
+// warps resident per SM); the other walks under a plain launch bound.
 template <int FPW>
 __global__ void __maxnreg__(SCB_SEARCH_REGS1)
     k_search_head(SearchArgs a) {
@@ -285,12 +285,10 @@ void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int 
   const size_t nyh = (size_t)rows * (rows + 1) / 2;
   const size_t smem = (nyh * fpw + 2 * (size_t)(rows + 1) * fpw + fpw) * sizeof(uint32_t);
   if (smem <= 96 * 1024) {
-    static bool attr = false;
-    if (!attr) {
+    once_per_device((const void*)k_column_bounds_blk, [] {
       SCB_CUDA(cudaFuncSetAttribute(k_column_bounds_blk,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-      attr = true;
-    }
+    });
     k_column_bounds_blk<<<nxw, 256, smem, st>>>(rt, fpw, frames_in_group, rows, rmax, rstride,
                                                 lbr, lbm);
   } else {  // tall grids: one thread per (column, frame)
@@ -371,10 +369,16 @@ __global__ void k_finalize(int step, int n, int fpw, int frames_in_group, uint32
     __syncthreads();
   }
   __shared__ uint32_t win;
-  if (threadIdx.x == 0) win = si[0];
+  const uint64_t* fv = vals + (size_t)f * nr;  // this frame's key -> time bits
+  if (threadIdx.x == 0) {
+    win = si[0];
+    // step 1 keeps `t < best_t` from best_t = +inf (search.cpp:277-285): a
+    // family whose every time is +inf has no argmin (NoCandidateError)
+    if (step == 1 && win != 0xffffffffu && fv[sb[0].t] == 0x7ff0000000000000ull)
+      win = 0xffffffffu;
+  }
   __syncthreads();
   FrameBest* o = out + f;
-  const uint64_t* fv = vals + (size_t)f * nr;  // this frame's key -> time bits
   if (threadIdx.x == 0) {
     o->t = win == 0xffffffffu ? ~0ull : fv[sb[0].t];
     o->sse = sb[0].sse;
@@ -396,16 +400,21 @@ __global__ void k_finalize(int step, int n, int fpw, int frames_in_group, uint32
 }
 
 // ---- host launchers ------------------------------------------------------------
+// The walks may use the device's whole opt-in shared memory (per device).
+template <int FPW, int STEP>
+static void set_search_attrs() {
+  once_per_device((const void*)search_kernel<FPW, STEP, false>(), [] {
+    const int lim = smem_optin_bytes();
+    SCB_CUDA(cudaFuncSetAttribute(search_kernel<FPW, STEP, false>(),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+    SCB_CUDA(cudaFuncSetAttribute(search_kernel<FPW, STEP, true>(),
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  });
+}
+
 template <int FPW, int STEP>
 static void launch_fpw(const SearchArgs& a, int blocks, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    SCB_CUDA(cudaFuncSetAttribute(search_kernel<FPW, STEP, false>(),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    SCB_CUDA(cudaFuncSetAttribute(search_kernel<FPW, STEP, true>(),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr = true;
-  }
+  set_search_attrs<FPW, STEP>();
   if (a.prune)
     search_kernel<FPW, STEP, true>()<<<blocks, SearchShape<STEP, true>::kBlock, smem, st>>>(a);
   else
@@ -415,16 +424,17 @@ static void launch_fpw(const SearchArgs& a, int blocks, size_t smem, cudaStream_
 int search_blocks_per_sm(int fpw, int step, bool prune, size_t smem) {
   int nb = 0;
 #define OCC1(F, S, P)                                                                        \
+  set_search_attrs<F, S>();                                                                  \
   SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, search_kernel<F, S, P>(),           \
                                                          SearchShape<S, P>::kBlock, smem))
 #define OCC(F)                                                                               \
   if (fpw == F) {                                                                            \
     if (step == 1) {                                                                         \
-      if (prune) OCC1(F, 1, true);                                                           \
-      else OCC1(F, 1, false);                                                                \
+      if (prune) { OCC1(F, 1, true); }                                                       \
+      else { OCC1(F, 1, false); }                                                            \
     } else {                                                                                 \
-      if (prune) OCC1(F, 2, true);                                                           \
-      else OCC1(F, 2, false);                                                                \
+      if (prune) { OCC1(F, 2, true); }                                                       \
+      else { OCC1(F, 2, false); }                                                            \
     }                                                                                        \
   }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
@@ -437,6 +447,9 @@ void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStrea
   const size_t smem = search_smem_bytes(a.cols, a.rows, a.n, step, a.prune != 0);
   if (search_tables_bytes(a.cols, a.rows, a.n) > 64 * 1024)
     fail(SC_ERR_SIZE, "CTU grid too large for the area tables");
+  if (smem > (size_t)smem_optin_bytes())
+    fail(SC_ERR_SIZE, "search walk state (" + std::to_string(smem) +
+                          " B of shared memory per block) exceeds the device limit");
   switch (fpw * 10 + step) {
     case 11: launch_fpw<1, 1>(a, blocks, smem, st); break;
     case 12: launch_fpw<1, 2>(a, blocks, smem, st); break;

@@ -256,12 +256,10 @@ void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, 
   const int nsat = (cols + 1) * (rows + 1);
   const size_t smem = (size_t)nsat * (8 + 24);
   if (smem > 227 * 1024) fail(SC_ERR_SIZE, "CTU grid too large for the shared-memory SAT");
-  static bool attr_set = false;
-  if (!attr_set) {
+  once_per_device((const void*)k_grid_sat, [] {
     SCB_CUDA(cudaFuncSetAttribute(k_grid_sat, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   227 * 1024));
-    attr_set = true;
-  }
+  });
   int threads = rows < 32 ? 32 : (rows > 1024 ? 1024 : ((rows + 31) / 32) * 32);
   k_grid_sat<<<frames, threads, smem, st>>>(d_est, d_rec, cols, rows, d_sat, d_usat);
   SCB_CUDA(cudaGetLastError());

@@ -114,30 +114,69 @@ class CostHistory:
         self.maps: List[CostMap] = []
 
     def append(self, m: CostMap) -> None:
-        if m.grid != self.grid:
-            raise SlicecraftError(1, "cost map grid does not match the history grid")
-        t = np.asarray(m.times_us, dtype=np.float64)
-        if t.size != self.grid.cell_count():
-            raise SlicecraftError(1, "cost map has wrong number of entries")
-        if not np.all(np.isfinite(t)) or np.any(t < 0.0):
-            raise SlicecraftError(7, "CTU times must be finite and >= 0")
-        if any(x.poc == m.poc for x in self.maps):
-            raise SlicecraftError(9, f"duplicate poc {m.poc} in cost history")
+        """CostHistory::append: validated by sc_cost_map_check (cost.cpp:45-64)."""
+        t = np.ascontiguousarray(m.times_us, dtype=np.float64).reshape(-1)
+        pocs = np.array([x.poc for x in self.maps], dtype=np.int32)
+        check(lib().sc_cost_map_check(C.byref(self.grid.c()), C.byref(m.grid.c()), _ptr(t),
+                                      t.size, m.poc, _ptr(pocs), len(pocs)))
+        m.times_us = t
         self.maps.append(m)
 
 
 def estimate_ctu_times(history: CostHistory, poc: int) -> CostMap:
-    """estimate_ctu_times (cost.cpp:66-95): co-TL, else most recent, else ones."""
-    tl = temporal_layer_of_poc(poc, history.gop_size)
-    for m in reversed(history.maps):
-        if m.temporal_layer == tl:
-            return CostMap(history.grid, np.array(m.times_us, dtype=np.float64), poc, tl, m.qp,
-                           CO_TEMPORAL_LAYER, m.poc)
-    if history.maps:
-        m = history.maps[-1]
-        return CostMap(history.grid, np.array(m.times_us, dtype=np.float64), poc, tl, m.qp,
-                       MOST_RECENT_ANY, m.poc)
-    return CostMap(history.grid, np.ones(history.grid.cell_count()), poc, tl, 0, UNIFORM, -1)
+    """estimate_ctu_times (cost.cpp:66-95) via sc_estimate_ctu_times: co-TL,
+    else most recent, else ones."""
+    n = len(history.maps)
+    arrs = [np.ascontiguousarray(m.times_us, dtype=np.float64) for m in history.maps]
+    ptrs = (C.c_void_p * max(n, 1))(*[a.ctypes.data for a in arrs])
+    pocs = np.array([m.poc for m in history.maps], dtype=np.int32)
+    tls = np.array([m.temporal_layer for m in history.maps], dtype=np.int32)
+    out = np.empty(history.grid.cell_count())
+    src, src_poc, tl = C.c_int32(), C.c_int32(), C.c_int32()
+    check(lib().sc_estimate_ctu_times(C.byref(history.grid.c()), history.gop_size, n,
+                                      C.cast(ptrs, C.c_void_p), _ptr(pocs), _ptr(tls), poc,
+                                      _ptr(out), C.byref(src), C.byref(src_poc), C.byref(tl)))
+    qp = next((m.qp for m in history.maps if m.poc == src_poc.value), 0) if n else 0
+    return CostMap(history.grid, out, poc, tl.value, qp, src.value, src_poc.value)
+
+
+class PrefixSumTable:
+    """PrefixSumTable (cost.hpp:67-89) built by sc_prefix_sum_table."""
+
+    def __init__(self, values, cols: int, rows: int):
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        self.cols, self.rows = cols, rows
+        self.table = np.empty((rows + 1) * (cols + 1))
+        check(lib().sc_prefix_sum_table(_ptr(v), v.size, cols, rows, _ptr(self.table)))
+
+    def rect_sum(self, x0: int, y0: int, w: int, h: int) -> float:
+        s, t = self.cols + 1, self.table
+        return ((t[(y0 + h) * s + x0 + w] - t[y0 * s + x0 + w]) - t[(y0 + h) * s + x0]) + \
+            t[y0 * s + x0]
+
+
+def split_even(total: int, parts: int) -> List[int]:
+    """split_even (grid.cpp:52-60)."""
+    out = (C.c_int32 * max(parts, 1))()
+    check(lib().sc_split_even(total, parts, out))
+    return list(out[:parts])
+
+
+def moments_sse(count: int, sum_: int, sumsq: int) -> float:
+    """SliceMoments::sse (texture.cpp:83-88)."""
+    out = C.c_double()
+    check(lib().sc_moments_sse(C.byref(CtuRecord(count, sum_, sumsq)), C.byref(out)))
+    return out.value
+
+
+def texture_tables(grid: CtuGrid, records: np.ndarray):
+    """TextureStats ctor (texture.cpp:90-130): validation + the three u64 SATs."""
+    rec = np.ascontiguousarray(records)
+    n = (grid.cols + 1) * (grid.rows + 1)
+    tabs = [np.empty(n, np.uint64) for _ in range(3)]
+    check(lib().sc_texture_tables(C.byref(grid.c()), _ptr(rec), rec.shape[0] if rec.ndim else 0,
+                                  *[_ptr(t) for t in tabs]))
+    return tabs
 
 
 @dataclass
@@ -407,6 +446,56 @@ class Partitioner:
                                      bit_depth, first_poc, F, _ptr(est), _ptr(records_out),
                                      C.cast(res, C.c_void_p)))
         return res
+
+    def validate_partition(self, grid: CtuGrid, col_widths: Sequence[int],
+                           row_heights: Sequence[int], slices: Sequence[Slice]) -> np.ndarray:
+        """validate_partition (grid.cpp:86-184) on the device; returns the
+        CTU -> slice-id map (rows x cols)."""
+        cw = np.ascontiguousarray(col_widths, dtype=np.int32)
+        rh = np.ascontiguousarray(row_heights, dtype=np.int32)
+        n = len(slices)
+        rects = (Rect * max(n, 1))(*[Rect(q.x0, q.y0, q.w, q.h, q.id) for q in slices])
+        out = np.empty((grid.rows, grid.cols), np.int32)
+        check(lib().sc_validate_partition(self._h, C.byref(grid.c()), len(cw), _ptr(cw), len(rh),
+                                          _ptr(rh), C.cast(rects, C.c_void_p), n, _ptr(out)))
+        return out
+
+    def result_slice_maps(self, grid: CtuGrid, step: int, frames: int) -> np.ndarray:
+        """CTU -> slice-id maps [F, rows, cols] of the last search's argmin
+        (step 1) / best (step 2) partitions (-1 outside the layout's columns)."""
+        out = np.empty((frames, grid.rows, grid.cols), np.int32)
+        check(lib().sc_result_slice_maps(self._h, step, frames, _ptr(out)))
+        return out
+
+    def enumerate_layouts(self, grid: CtuGrid, cfg: SearchConfig, first: int = 0,
+                          max_out: int = 1 << 16):
+        """A window of the family's candidate stream (search.cpp:302-326) as
+        layouts: (layouts, total)."""
+        buf = (Layout * max(max_out, 1))()
+        n, tot = C.c_uint64(), C.c_uint64()
+        check(lib().sc_enumerate_candidates(self._h, C.byref(grid.c()), C.byref(cfg.c()), first,
+                                            max_out, C.cast(buf, C.c_void_p), C.byref(n),
+                                            C.byref(tot)))
+        return list(buf[:n.value]), tot.value
+
+    def for_each_candidate(self, grid: CtuGrid, cfg: SearchConfig, sink, page: int = 1 << 16):
+        """for_each_candidate (search.cpp:302-320): every admissible candidate
+        in enumeration order, as a Partition, through `sink`."""
+        first = 0
+        while True:
+            lays, tot = self.enumerate_layouts(grid, cfg, first, page)
+            for L in lays:
+                sink(Partition.uniform(grid, cfg.n_slices) if L.n_cols == 0
+                     else Partition.from_layout(grid, L))
+            first += len(lays)
+            if first >= tot or not lays:
+                return
+
+    def enumerate_candidates(self, grid: CtuGrid, cfg: SearchConfig) -> List["Partition"]:
+        """enumerate_candidates (search.cpp:322-326)."""
+        out: List[Partition] = []
+        self.for_each_candidate(grid, cfg, out.append)
+        return out
 
     def count_candidates(self, grid: CtuGrid, cfg: SearchConfig) -> int:
         n = C.c_uint64()

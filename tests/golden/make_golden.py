@@ -20,6 +20,17 @@ Contents
                    with a hash of the estimate maps / records that were used.
   configs_lambda.json  the same inputs with lambda in {0.1, 0.3} (SURVEY.md
                    §8d): cfg1 (POC 1), cfg2 (POC 1..2), cfg3 (POC 1).
+  validate.json    validate_partition (grid.cpp:86-184) on valid partitions and
+                   on mutations hitting every error class: status + message.
+  enumerate.json   for_each_candidate (search.cpp:302-320): the ordered candidate
+                   lists of small spaces (full lists, or count + sha256 of the
+                   list + its first / last 40 for larger ones).
+  ladder.json      the reference-checkable ladder on the REAL cfg4 / cfg5 grids
+                   (SURVEY.md §8c): cfg4's POC-1 inputs (30x17) at n=16 cap 1/2
+                   and n=8 cap 4; cfg5's POC-1 inputs (60x34) at n=4, n=6,
+                   n=8 cap 2 and n=32 cap 1 (several lambdas): the reference's
+                   two_step_partition outputs (search.cpp:407-434) with the
+                   estimate maps and records that were used.
 """
 from __future__ import annotations
 
@@ -161,6 +172,168 @@ def configs(r: Ref, lambdas=(0.0,), plan=None) -> dict:
     return out
 
 
+LADDER = [  # (cfg, n, max_tile_cols, lambda); candidate counts from SURVEY.md §8c
+    (4, 16, 1, 0.0), (4, 16, 2, 0.0), (4, 8, 4, 0.0), (4, 8, 4, 0.3),
+    (4, 16, 2, 1.0), (5, 32, 1, 0.0), (5, 32, 1, 0.3), (5, 4, 0, 0.0), (5, 4, 0, 0.1),
+    (5, 4, 0, 2.0), (5, 6, 0, 0.0), (5, 6, 0, 0.3), (5, 8, 2, 0.0), (5, 8, 2, 0.5),
+]
+
+
+def ladder(r: Ref) -> dict:
+    """two_step_partition of the unmodified reference on the cfg4 / cfg5 grids
+    (30x17, 60x34) at the candidate spaces it can enumerate (<= 3.2e8)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    inputs = {}
+    for ci in (4, 5):
+        w = wl.WORKLOADS[ci]
+        tr = wl.cost_trace(w, frames=1)
+        luma = wl.synth_luma(w, frames=1)
+        st, rec = r.ctu_stats(luma[0].astype(np.uint16), w.bit_depth, w.ctu)
+        assert st == 0
+        maps = np.stack([m.times_us for m in tr.history_maps[:1]])
+        inputs[ci] = {"w": w, "rec": rec, "maps": maps, "est": tr.est[0],
+                      "hpocs": [tr.history_maps[0].poc], "htls": [tr.history_maps[0].temporal_layer]}
+
+    def run(case):
+        ci, n, mc, lam = case
+        I = inputs[ci]
+        w = I["w"]
+        t0 = time.time()
+        st, o = r.two_step(w.width, w.height, w.ctu, 16, I["maps"], I["hpocs"], I["htls"], I["rec"],
+                           1, n, lam, 3.0, 0, mc)
+        assert st == 0, r.err()
+        dt = time.time() - t0
+        print(f"ladder cfg{ci} n={n} cap={mc} lambda={lam}: {o.candidates_step1} cand, {dt:.1f}s",
+              flush=True)
+        return {"cfg": ci, "n": n, "max_tile_cols": mc, "lambda": lam, "k": 3.0,
+                "t_min": o.t_min_us, "t_best": o.t_best_us, "sse_best": o.sse_best,
+                "best": o.best.rects(), "best_widths": o.best.widths(),
+                "candidates_step1": o.candidates_step1, "candidates_step2": o.candidates_step2,
+                "est_source": o.est_source, "est_source_poc": o.est_source_poc,
+                "ref_seconds": dt}
+
+    with ThreadPoolExecutor(max_workers=min(len(LADDER), os.cpu_count() or 1)) as ex:
+        cases = list(ex.map(run, LADDER))
+    grids = {}
+    for ci, I in inputs.items():
+        w = I["w"]
+        grids[str(ci)] = {"name": w.name, "width": w.width, "height": w.height, "ctu": w.ctu,
+                          "poc": 1, "est": I["est"].tolist(), "records": I["rec"].tolist(),
+                          "est_hash": h(I["est"]), "records_hash": h(I["rec"])}
+    return {"grids": grids, "cases": cases}
+
+
+def validate(r: Ref) -> list:
+    """validate_partition on valid partitions and on mutations of them."""
+    rng = np.random.default_rng(86184)
+    cases = []
+
+    def rec(cols, rows, cw, rh, sl, kind):
+        st, *_ = r.partition_eval(cols * 32, rows * 32, 32, cw, rh, sl, validate=True)
+        cases.append({"cols": cols, "rows": rows, "tile_cols": list(map(int, cw)),
+                      "tile_rows": list(map(int, rh)),
+                      "slices": [list(map(int, q)) for q in sl], "kind": kind, "status": st,
+                      "message": r.err() if st else ""})
+
+    while len(cases) < 400:
+        cols, rows = int(rng.integers(1, 10)), int(rng.integers(1, 10))
+        # random tile grid, then slices: some tiles whole, some cut into row runs
+        def comp(total):
+            out, left = [], total
+            while left:
+                v = int(rng.integers(1, left + 1))
+                out.append(v)
+                left -= v
+            return out
+        cw, rh = comp(cols), comp(rows)
+        sl, x = [], 0
+        for w in cw:
+            y = 0
+            for h in rh:
+                if rng.random() < 0.5:
+                    sl.append([x, y, w, h])
+                else:
+                    yy = y
+                    for hh in comp(h):
+                        sl.append([x, yy, w, hh])
+                        yy += hh
+                y += h
+            x += w
+        perm = rng.permutation(len(sl))
+        sl = [q + [int(perm[i])] for i, q in enumerate(sl)]
+        order = rng.permutation(len(sl))
+        sl = [sl[i] for i in order]
+        rec(cols, rows, cw, rh, sl, "valid")
+        m = int(rng.integers(0, 9))
+        sl2 = [list(q) for q in sl]
+        if m == 0 and len(sl2) > 1:  # drop a slice -> coverage (ids break too)
+            del sl2[int(rng.integers(0, len(sl2)))]
+            for i, q in enumerate(sorted(sl2, key=lambda q: q[4])):
+                q[4] = i
+            rec(cols, rows, cw, rh, sl2, "drop")
+        elif m == 1:  # grow a slice -> overlap / bounds
+            q = sl2[int(rng.integers(0, len(sl2)))]
+            q[2 + int(rng.integers(0, 2))] += 1
+            rec(cols, rows, cw, rh, sl2, "grow")
+        elif m == 2:  # duplicate id
+            if len(sl2) > 1:
+                sl2[0][4] = sl2[1][4]
+            rec(cols, rows, cw, rh, sl2, "dup_id")
+        elif m == 3:  # tile grid that cuts slices -> structure
+            if cols > 1:
+                cw2 = [1] * cols
+                rec(cols, rows, cw2, rh, sl2, "fine_tiles")
+        elif m == 4:  # bad tiles
+            rec(cols, rows, cw + [1], rh, sl2, "tile_sum")
+            rec(cols, rows, [0] + cw, rh, sl2, "tile_zero")
+            rec(cols, rows, [], rh, sl2, "tile_empty")
+        elif m == 5:  # overlapping duplicate appended with a fresh id
+            q = list(sl2[int(rng.integers(0, len(sl2)))])
+            q[4] = len(sl2)
+            sl2.insert(int(rng.integers(0, len(sl2) + 1)), q)
+            rec(cols, rows, cw, rh, sl2, "overlap")
+        elif m == 6:  # shift a slice by one cell
+            q = sl2[int(rng.integers(0, len(sl2)))]
+            q[int(rng.integers(0, 2))] += 1 if rng.random() < 0.7 else -1
+            rec(cols, rows, cw, rh, sl2, "shift")
+        elif m == 7:
+            rec(cols, rows, cw, rh, [], "empty")
+        else:  # merge two vertically adjacent runs across a tile row -> structure or ok
+            rec(cols, rows, [cols], [rows], sl2, "one_tile")
+    return cases
+
+
+def enumerate_lists(r: Ref) -> list:
+    """Ordered candidate streams of the reference's for_each_candidate."""
+    rng = np.random.default_rng(302326)
+    out = []
+    inst = [(64, 64, 32, 2, 3.0, 0, 0), (128, 32, 32, 2, 3.0, 0, 0), (192, 192, 32, 4, 3.0, 0, 0),
+            (1920, 1080, 128, 4, 3.0, 0, 2), (1920, 1080, 128, 1, 3.0, 0, 0),
+            (1920, 1080, 128, 2, 3.0, 0, 0), (1920, 1080, 128, 4, 3.0, 0, 0),
+            (1920, 1080, 128, 8, 3.0, 0, 4), (256, 256, 32, 5, 1.2, 0, 0),
+            (256, 160, 32, 6, 2.0, 0, 3), (1920, 1080, 128, 6, 3.0, 1, 0)]
+    while len(inst) < 40:
+        cols, rows = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        n = int(rng.integers(1, min(7, cols * rows) + 1))
+        inst.append((cols * 32 - int(rng.integers(0, 32)), rows * 32 - int(rng.integers(0, 32)),
+                     32, n, float(rng.choice([3.0, 2.0, 1.5, 1.1])), 0, int(rng.integers(0, 4))))
+    for fw, fh, ctu, n, k, fam, mc in inst:
+        st, cnt, _ = r.enumerate(fw, fh, ctu, n, k, fam, mc)
+        case = {"w": fw, "h": fh, "ctu": ctu, "n": n, "k": k, "family": fam,
+                "max_tile_cols": mc, "status": st, "count": cnt}
+        if st == 0 and cnt:
+            _, _, lays = r.enumerate(fw, fh, ctu, n, k, fam, mc, max_out=cnt)
+            rects = [[list(q) for q in L.rects()] for L in lays]
+            case["sha256"] = hashlib.sha256(json.dumps(rects).encode()).hexdigest()
+            if cnt <= 3000:
+                case["list"] = rects
+            else:
+                case["head"], case["tail"] = rects[:40], rects[-40:]
+        out.append(case)
+    return out
+
+
 def uniform(r: Ref) -> dict:
     """UniformOnly family: uniform_partition shapes, the family's search
     outputs, and partition_time / partition_sse of arbitrary partitions."""
@@ -244,6 +417,15 @@ def main():
     if "configs" in which:
         with open(os.path.join(OUT, "configs.json"), "w") as f:
             json.dump(configs(r), f, indent=1)
+    if "validate" in which:
+        with open(os.path.join(OUT, "validate.json"), "w") as f:
+            json.dump(validate(r), f)
+    if "enumerate" in which:
+        with open(os.path.join(OUT, "enumerate.json"), "w") as f:
+            json.dump(enumerate_lists(r), f)
+    if "ladder" in which:
+        with open(os.path.join(OUT, "ladder.json"), "w") as f:
+            json.dump(ladder(r), f)
     if "lambda" in which:
         with open(os.path.join(OUT, "configs_lambda.json"), "w") as f:
             json.dump(configs(r, lambdas=(0.1, 0.3), plan={1: [1], 2: [1, 2], 3: [1]}), f,
