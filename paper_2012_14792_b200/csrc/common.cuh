@@ -54,6 +54,13 @@ inline int smem_optin_bytes() {
   SCB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   return v;
 }
+// The most dynamic shared memory a kernel may opt into: the opt-in limit
+// minus its static shared memory.
+inline int max_dynamic_smem(const void* kernel) {
+  cudaFuncAttributes fa;
+  SCB_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  return smem_optin_bytes() - (int)fa.sharedSizeBytes;
+}
 
 // ---- geometry --------------------------------------------------------------
 inline int cell_w(const sc_grid& g, int x) {

@@ -404,11 +404,10 @@ __global__ void k_finalize(int step, int n, int fpw, int frames_in_group, uint32
 template <int FPW, int STEP>
 static void set_search_attrs() {
   once_per_device((const void*)search_kernel<FPW, STEP, false>(), [] {
-    const int lim = smem_optin_bytes();
-    SCB_CUDA(cudaFuncSetAttribute(search_kernel<FPW, STEP, false>(),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-    SCB_CUDA(cudaFuncSetAttribute(search_kernel<FPW, STEP, true>(),
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+    for (const void* k : {(const void*)search_kernel<FPW, STEP, false>(),
+                          (const void*)search_kernel<FPW, STEP, true>()})
+      SCB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    max_dynamic_smem(k)));
   });
 }
 
@@ -447,7 +446,7 @@ void search_launch(int fpw, int step, const SearchArgs& a, int blocks, cudaStrea
   const size_t smem = search_smem_bytes(a.cols, a.rows, a.n, step, a.prune != 0);
   if (search_tables_bytes(a.cols, a.rows, a.n) > 64 * 1024)
     fail(SC_ERR_SIZE, "CTU grid too large for the area tables");
-  if (smem > (size_t)smem_optin_bytes())
+  if (smem > (size_t)max_dynamic_smem((const void*)search_kernel<1, 1, false>()))
     fail(SC_ERR_SIZE, "search walk state (" + std::to_string(smem) +
                           " B of shared memory per block) exceeds the device limit");
   switch (fpw * 10 + step) {

@@ -140,24 +140,28 @@ def test_result_slice_maps(part, oracle):
                 assert (m2[f] >= 0).all()
 
 
-def test_step1_infinite_times_have_no_candidate(part, oracle):
-    """run_step1 keeps `t < best_t` from best_t = +inf (search.cpp:277-292):
-    if every candidate's time is +inf there is no argmin (NoCandidateError);
-    with some finite candidates the argmin is the oracle's."""
+def test_step1_infinite_times(part, oracle):
+    """run_step1 keeps `t < best_t` from best_t = +inf (search.cpp:277-292): a
+    family whose every layout_time is +inf has no argmin (NoCandidateError;
+    the reference raises it on these grids, checked when the fixtures were
+    made).  Elsewhere inf times turn summed-area-table entries into NaN
+    (inf - inf), which layout_time's max from 0.0 skips: the results must
+    still be the oracle's, bit for bit."""
     from paper_2012_14792_b200 import CtuGrid, SearchConfig, SlicecraftError
-    g = CtuGrid.make(640, 384, 128)
     for mode in (0, 1):
+        for W, n, est in [(128, 1, [np.inf]), (256, 1, [np.inf, 1.0]), (256, 2, [np.inf, 1.0])]:
+            g = CtuGrid.make(W, 128, 128)
+            with pytest.raises(SlicecraftError) as e:
+                part.min_time_search_batch(g, np.array(est), SearchConfig(n_slices=n, mode=mode))
+            assert e.value.kind == "NoCandidateError"
+        g = CtuGrid.make(640, 384, 128)
         cfg = SearchConfig(n_slices=3, mode=mode)
-        est = np.full(g.cell_count(), np.inf)
-        with pytest.raises(SlicecraftError) as e:
-            part.min_time_search_batch(g, est, cfg)
-        assert e.value.kind == "NoCandidateError"
-        est = np.ones(g.cell_count())
-        est[[0, 5, 14]] = np.inf  # only candidates avoiding three cells are finite
-        o = part.min_time_search_batch(g, est, cfg)[0]
-        st, exp = oracle.search(640, 384, 128, est, None, 3, 0.0, 3.0, 0, 0, 1)
-        assert st == 0 and o.t_min_us == exp.t_min_us
-        assert o.argmin.rects() == exp.argmin1.slices(g.rows)
+        for est in [np.full(g.cell_count(), np.inf), np.where(np.arange(15) % 5 == 0, np.inf, 1.0),
+                    np.where(np.arange(15) == 7, np.inf, 2.0)]:
+            o = part.min_time_search_batch(g, est, cfg)[0]
+            st, exp = oracle.search(640, 384, 128, est, None, 3, 0.0, 3.0, 0, 0, 1)
+            assert st == 0 and o.t_min_us == exp.t_min_us
+            assert o.argmin.rects() == exp.argmin1.slices(g.rows)
 
 
 # ---- cfg4 / cfg5 grids against the reference ------------------------------------
