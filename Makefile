@@ -9,7 +9,13 @@ HDRS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/slicec
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Iinclude --expt-relaxed-constexpr -Xptxas -v
 
-all: $(PKG)/libslicecraft_b200.so oracle
+all: $(PKG)/libslicecraft_b200.so synth oracle
+
+# synthetic-input generator shared by the bench arms and the tests (not the
+# product, not the oracle)
+synth: synth/libscsynth.so
+synth/libscsynth.so: synth/sc_synth.c
+	gcc -std=gnu11 -O2 -fPIC -shared -pthread $< -o $@ -lm
 
 $(PKG)/libslicecraft_b200.so: $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared $(SRCS) -o $@ -lpthread 2> build_ptxas.log || (cat build_ptxas.log; false)
@@ -35,7 +41,7 @@ dropin/cases_ref: dropin/dropin_cases.cpp oracle
 	$(CXX) $(DROPIN_FLAGS) $< -Loracle/_ref -lslicecraft_ref -Wl,-rpath,'$$ORIGIN/../oracle/_ref' -o $@
 
 clean:
-	rm -f $(PKG)/libslicecraft_b200.so build_ptxas.log dropin/*.so dropin/cases_b200 dropin/cases_ref
+	rm -f $(PKG)/libslicecraft_b200.so build_ptxas.log dropin/*.so dropin/cases_b200 dropin/cases_ref synth/*.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean dropin
+.PHONY: all oracle clean dropin synth

@@ -9,10 +9,12 @@ n=8 slices, exhaustive tile columns) -- the "at 4K" configuration the metric
 is quoted on that fits one GPU.  Config 1 is the reference's CPU-runnable
 case; configs 2/4/5 are parity cases (tests/).
 
-value  = TRS candidates scored per second over the whole job, inputs resident
-         in HBM (device pointers into sc_partition_frames).  A candidate is
-         one (frame, candidate) pair counted by the reference's own counters
-         (candidates_step1 + candidates_step2, search.hpp:41-43).
+value  = TRS candidates resolved per second over the whole job, inputs
+         resident in HBM (device pointers into sc_partition_frames).  A
+         candidate is one (frame, candidate) pair counted by the reference's
+         own counters (candidates_step1 + candidates_step2, search.hpp:41-43);
+         candidates_scored_by_the_walks_per_s beside it counts only what the
+         walks evaluated (step 2 skips subtrees over its budget).
 e2e    = the same metric through the public C-ABI call with HOST (pinned)
          buffers: the H2D copy of that step's luma + estimate maps and the D2H
          of the per-frame results happen inside the timed region.
@@ -25,7 +27,8 @@ sc_shard_best record per frame is all-gathered after each step.
 
 --impl reference runs the UNMODIFIED reference CPU path (oracle/_ref, built
 from /root/reference; the C oracle port when that is absent) on the host
-cores, one frame per thread, on a bounded prefix sample of the same workload.
+cores: whole frames of the same workload (full enumeration), one frame per
+host thread, a step being one frame (bounded sample: --steps frames).
 """
 from __future__ import annotations
 
@@ -44,6 +47,25 @@ sys.path.insert(0, ROOT)
 
 METRIC = "TRS candidates scored/sec & frames partitioned/sec at 4K; texture pass GB/s"
 UNIT = "candidates/s"
+DATA = "synthetic (seeded; SURVEY.md \u00a78d generator, synth/libscsynth.so; no public dataset)"
+VALUE_DEF = ("candidates resolved per second: the reference's own per-frame counters "
+             "candidates_step1 + candidates_step2 (search.hpp:41-43) summed over the frames of "
+             "a step, per second of step time.  Step 1 scores every candidate; step 2 resolves "
+             "the family under the t_min*(1+lambda) budget (the B200 walk skips subtrees whose "
+             "fixed slices already exceed it: candidates_scored_by_the_walks_per_s counts what "
+             "it actually scored)")
+
+
+def workload_config(w, counts):
+    """The workload-defining config, identical in both arms."""
+    cols, rows = -(-w.width // w.ctu), -(-w.height // w.ctu)
+    return {"workload": w.name, "frames_per_rank": w.frames, "frame": f"{w.width}x{w.height}",
+            "bit_depth": w.bit_depth, "ctu": w.ctu, "grid": f"{cols}x{rows}",
+            "n_slices": w.n_slices, "max_tile_cols": w.max_tile_cols, "lambda": 0.0,
+            "k_area": 3.0, "coverage": "reference",
+            "candidates_per_frame_step": [list(c) for c in counts],
+            "l2": "inputs larger than L2 (luma batch %.0f MB per %d frames)"
+                  % (w.frames * w.width * w.height * w.bps / 1e6, w.frames)}
 
 
 def dist_env():
@@ -348,15 +370,10 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
-        "data": "synthetic (seeded; SURVEY.md §8d generator, no public dataset)",
-        "config": {"workload": w.name, "frames_per_rank": F, "frame": f"{w.width}x{w.height}",
-                   "bit_depth": w.bit_depth, "ctu": w.ctu, "grid": f"{g.cols}x{g.rows}",
-                   "n_slices": w.n_slices, "max_tile_cols": w.max_tile_cols,
-                   "lambda": cfg.lambda_, "k_area": cfg.k_area,
-                   "coverage": "reference", "mode": "exhaustive" if args.mode == 0 else "pruned",
-                   "candidates_per_frame_step": [list(c) for c in counts],
-                   "parallelism": f"frames sharded, {world} rank(s)",
-                   "l2": "inputs larger than L2 (luma batch %.0f MB/step)" % (luma_bytes / 1e6)},
+        "data": DATA, "config": workload_config(w, counts),
+        "parallelism": f"frames sharded, {world} rank(s)",
+        "search_mode": "exhaustive" if args.mode == 0 else "pruned",
+        "value_definition": VALUE_DEF,
         "frames_per_s": frames_total / (ms / 1e3),
         "candidates_scored_by_the_walks_per_s": walked * world / (ms / 1e3),
         "frames_per_s_e2e": frames_total / (ms_e2e / 1e3),
@@ -372,14 +389,15 @@ def run_ours(args):
         # K3), the rank pipeline (6 own + 13 CUB launches), split table; per
         # frame group: column bounds, step-1 walk + finalize, item filter (own
         # + 2 CUB select launches), step-2 walk + finalize; pruned mode adds the
-        # seed-phase walk and the phase-B item filter (+4)
-        "gpu_launches": args.steps * (25 + (8 + 4 * args.mode) * ((F + 31) // 32)),
+        # seed-phase walk and the phase-B item filter (+4); the device
+        # post-check of the returned partitions adds one launch per step
+        "gpu_launches": args.steps * (27 + (8 + 4 * args.mode) * ((F + 31) // 32)),
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_extra and args.mode == 0:
         out["pruned"] = pruned_extras(part, stream, args, w, luma_d, est_d)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline_sample(w, threads=1, steps=1)["cpu_baseline"]
+        out["cpu_baseline"] = cpu_baseline_sample(w, threads=os.cpu_count() or 1)
     if rank == 0:
         print(json.dumps(out), flush=True)
     part.close()
@@ -567,14 +585,27 @@ def pruned_extras(part, stream, args, w3, luma3_d, est3_d):
 
 
 # ---- reference (CPU) arm ------------------------------------------------------------
-def _sample_cap(total_steps):
-    # enumeration prefix c <= cap (c ascending is the outermost loop of the
-    # reference's order, search.cpp:120-128): 12.4M candidates/step/frame at
-    # cap 3, 1.27M at cap 2 (30x17 grid, n = 8)
-    return 3 if total_steps * 12 <= 200 else 2
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
-def cpu_baseline_sample(w, threads, steps, warmup=0):
+def reference_frames(w, threads, steps, warmup):
+    """The unmodified reference CPU path (oracle/_ref: ctu_stats +
+    two_step_partition, search.cpp:407-434, the FULL enumeration of the
+    workload's family -- nothing capped) on whole frames of the workload, one
+    frame per task on a pool of `threads` host threads (the reference's own
+    `workers` threads are slower than one frame per thread).
+    `warmup` frames run first, untimed; then `steps` frames are timed
+    together (wall clock): a step is one frame.  Falls back to the C oracle
+    port where oracle/_ref was not built."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle.oracle import Oracle, Ref
     from paper_2012_14792_b200 import workloads as wl
     kind = "reference"
@@ -583,52 +614,72 @@ def cpu_baseline_sample(w, threads, steps, warmup=0):
     except Exception:
         R, kind = None, "port"
     O = Oracle()
-    cap = _sample_cap(steps + warmup) if w.index == 3 else w.max_tile_cols
-    nfr = threads
-    tr = wl.cost_trace(w, frames=nfr)
-    luma = wl.synth_luma(w, frames=nfr)
-    maps = np.stack([m.times_us for m in tr.history_maps])
-    hp = [m.poc for m in tr.history_maps]
-    ht = [m.temporal_layer for m in tr.history_maps]
-    counts = [0] * nfr
+    n_pocs = min(w.frames, max(steps + warmup, 1))
+    # inputs from the shared generator only: this arm never loads the product
+    # library (the reference estimates from the raw history itself)
+    maps, hp, ht = wl.history_maps(w, frames=n_pocs)
+    luma = wl.synth_luma(w, frames=n_pocs)
+    frame_bytes = w.width * w.height * w.bps
 
-    def one(i):
-        p = i + 1
-        plane = luma[i].astype(np.uint16)
+    def est_port(p):  # estimate_ctu_times for the port fallback (cost.cpp:66-95)
+        same = [i for i in range(p) if ht[i] == ht[p]]
+        return maps[same[-1] if same else p - 1]
+
+    def one(k):
+        i = k % n_pocs
+        p = i + 1  # POC p, estimated from POCs 0..p-1 (workloads.cost_trace)
+        t0 = time.perf_counter()
         if R is not None:
-            _, rec = R.ctu_stats(plane, w.bit_depth, w.ctu)
+            _, rec = R.ctu_stats(luma[i].astype(np.uint16), w.bit_depth, w.ctu)
+            t1 = time.perf_counter()
             st, o = R.two_step(w.width, w.height, w.ctu, 16, maps[:p], hp[:p], ht[:p], rec, p,
-                               w.n_slices, 0.0, 3.0, 0, cap)
-            counts[i] = o.candidates_step1 + o.candidates_step2
+                               w.n_slices, 0.0, 3.0, 0, w.max_tile_cols)
         else:
             rec = O.ctu_stats(luma[i], w.ctu)
-            st, o = O.search(w.width, w.height, w.ctu, tr.est[i], rec, w.n_slices, 0.0, 3.0, cap,
-                             0, 3)
-            counts[i] = o.candidates_step1 + o.candidates_step2
+            t1 = time.perf_counter()
+            st, o = O.search(w.width, w.height, w.ctu, est_port(p), rec, w.n_slices, 0.0, 3.0,
+                             w.max_tile_cols, 0, 3)
+        assert st == 0
+        return o.candidates_step1, o.candidates_step2, t1 - t0, time.perf_counter() - t1
 
-    def step():
-        th = [threading.Thread(target=one, args=(i,)) for i in range(nfr)]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, range(warmup)))
         t0 = time.perf_counter()
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-        return time.perf_counter() - t0, sum(counts)
+        res = list(ex.map(one, range(warmup, warmup + steps)))
+        wall = time.perf_counter() - t0
+        # ctu_stats alone, one frame per thread, all threads at once
+        # (texture.cpp:145-169 is single-threaded by design)
+        def tex(k):
+            a = time.perf_counter()
+            if R is not None:
+                R.ctu_stats(luma[k % n_pocs].astype(np.uint16), w.bit_depth, w.ctu)
+            else:
+                O.ctu_stats(luma[k % n_pocs], w.ctu)
+            return time.perf_counter() - a
+        t1 = time.perf_counter()
+        tex_t = list(ex.map(tex, range(threads)))
+        tex_wall = time.perf_counter() - t1
+    cands = sum(a + b for a, b, _, _ in res)
+    counts = sorted({(a, b) for a, b, _, _ in res})
+    per_thread_tex = frame_bytes / float(np.mean([r[2] for r in res]))
+    return {"kind": kind, "cands": cands, "wall": wall, "counts": counts,
+            "ctu_stats": {"gbs_per_thread": per_thread_tex / 1e9,
+                          "gbs_all_threads": threads * frame_bytes / tex_wall / 1e9,
+                          "threads": threads, "frame_bytes": frame_bytes,
+                          "per_thread_spread_s": [round(min(tex_t), 4), round(max(tex_t), 4)]},
+            "frames": steps}
 
-    for _ in range(warmup):
-        step()
-    tot_t, tot_c = 0.0, 0
-    for _ in range(steps):
-        dt, c = step()
-        tot_t += dt
-        tot_c += c
-    v = tot_c / tot_t
-    sample = (f"{w.name}: ctu_stats + two_step_partition on {nfr} frame(s) (POC 1..{nfr}), one "
-              f"frame per thread, over the enumeration prefix c <= {cap} "
-              f"({tot_c // max(steps, 1) // nfr:,} candidates per frame, both steps)")
-    return {"value": v, "seconds": tot_t,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nfr, "kind": kind,
-                             "sample": sample}}
+
+def cpu_baseline_sample(w, threads):
+    """cpu_baseline of the GPU line: one wave of whole frames of the workload
+    (one per host thread) through the unmodified reference."""
+    r = reference_frames(w, threads, steps=threads, warmup=0)
+    v = r["cands"] / r["wall"]
+    return {"value": v, "unit": UNIT, "cores": threads, "kind": r["kind"],
+            "sample": f"{w.name}: ctu_stats + two_step_partition (full enumeration, "
+                      f"{r['counts'][0][0]:,} + {r['counts'][0][1]:,} candidates per frame) on "
+                      f"{threads} whole frame(s), one per host thread, {r['wall']:.1f} s wall",
+            "cpu_model": cpu_model(), "ctu_stats": r["ctu_stats"]}
 
 
 def run_reference(args):
@@ -637,15 +688,22 @@ def run_reference(args):
         return
     from paper_2012_14792_b200 import workloads as wl
     w = wl.WORKLOADS[args.config]
-    threads = min(os.cpu_count() or 1, w.frames) if w.frames > 1 else 1
-    r = cpu_baseline_sample(w, threads=threads, steps=args.steps, warmup=args.warmup)
-    v = r["value"]
+    threads = os.cpu_count() or 1
+    r = reference_frames(w, threads, steps=args.steps, warmup=args.warmup)
+    v = r["cands"] / r["wall"]
     out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / max(args.steps, 1),
+           "warmup": args.warmup, "ms_per_step": 1e3 * r["wall"] / max(args.steps, 1),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
-           "data": "synthetic (seeded; SURVEY.md §8d generator)",
-           "config": {"workload": w.name, "host_threads": threads},
-           "impl": "reference", "cpu_baseline": r["cpu_baseline"],
+           "data": DATA, "config": workload_config(w, r["counts"]),
+           "parallelism": f"{threads} host threads, one whole frame per thread",
+           "value_definition": VALUE_DEF,
+           "impl": "reference",
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": r["kind"],
+                            "sample": f"{args.steps} whole frames of {w.name} (a step is one "
+                                      f"frame: ctu_stats + two_step_partition, full "
+                                      f"enumeration), {args.warmup} warm-up frames first, "
+                                      f"{threads} frames in flight",
+                            "cpu_model": cpu_model(), "ctu_stats": r["ctu_stats"]},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

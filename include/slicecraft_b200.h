@@ -370,18 +370,6 @@ sc_status sc_shard_export(sc_ctx* ctx, int32_t step, int32_t n_frames, sc_shard_
 sc_status sc_shard_merge(int32_t step, int32_t world, int32_t n_frames,
                          const sc_shard_best* gathered, sc_search_result* inout);
 
-/* ---- synthetic inputs (bench/test utility; BASELINE.json configs) ------- */
-/* Seeded luma frames: bytes_per_sample 1 or 2, max value
- * (1<<bit_depth)-1, `textured_pct` percent of 128x128 blocks noise, mode 1 =
- * the three-class (flat/gradient/noise) mix of config 2.  Frame f drifts the
- * block lattice by 4*f px.  Host buffer, frame stride width*height*bps. */
-sc_status sc_synth_luma(uint64_t seed, int32_t width, int32_t height, int32_t bit_depth,
-                        int32_t n_frames, int32_t first_frame, int32_t textured_pct,
-                        int32_t mode, void* out);
-/* Seeded lognormal(0, sigma) per-CTU times, (float) rounded then widened. */
-sc_status sc_synth_times(uint64_t seed, int32_t tag, int32_t cells, double sigma,
-                         double* out);
-
 #ifdef __cplusplus
 }
 #endif

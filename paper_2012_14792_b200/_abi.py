@@ -144,9 +144,6 @@ SIGNATURES = [
     ("sc_split_even", C.c_int, [C.c_int32, C.c_int32, _P]),
     ("sc_shard_export", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
     ("sc_shard_merge", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P]),
-    ("sc_synth_luma", C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                C.c_int32, C.c_int32, C.c_int32, _P]),
-    ("sc_synth_times", C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_double, _P]),
 ]
 
 _lib = None

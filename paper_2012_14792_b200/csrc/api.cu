@@ -1672,76 +1672,4 @@ sc_status sc_enumerate_candidates(sc_ctx* ctx, const sc_grid* grid, const sc_sea
   });
 }
 
-// ---- synthetic inputs ----------------------------------------
-static inline uint64_t mix64(uint64_t z) {
-  z += 0x9e3779b97f4a7c15ull;
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  return z ^ (z >> 31);
-}
-static inline uint64_t H4(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
-  return mix64(mix64(mix64(seed ^ mix64(a)) ^ b) ^ (c * 0x2545f4914f6cdd1dull));
-}
-
-sc_status sc_synth_luma(uint64_t seed, int32_t W, int32_t H, int32_t bit_depth, int32_t frames,
-                        int32_t first_frame, int32_t pct, int32_t mode, void* out) {
-  return guarded([&] {
-    if (!out || W < 1 || H < 1 || frames < 1) fail(SC_ERR_USAGE, "bad synth arguments");
-    if (bit_depth < 1 || bit_depth > 16) fail(SC_ERR_FORMAT, "bit depth must be 1..16");
-    const int bps = bit_depth <= 8 ? 1 : 2;
-    const uint32_t M = (1u << bit_depth) - 1u;
-    const size_t fbytes = (size_t)W * H * bps;
-    auto work = [&](int f0, int f1) {
-      for (int fi = f0; fi < f1; ++fi) {
-        const int f = first_frame + fi;
-        unsigned char* base = static_cast<unsigned char*>(out) + (size_t)fi * fbytes;
-        for (int y = 0; y < H; ++y) {
-          const int by = y / 128;
-          for (int x = 0; x < W; ++x) {
-            const int bx = (x + 4 * f) / 128;
-            const uint32_t g = (uint32_t)(((uint64_t)x * M / (uint64_t)(W > 1 ? W - 1 : 1) +
-                                           (uint64_t)y * M / (uint64_t)(H > 1 ? H - 1 : 1)) / 2);
-            uint32_t v;
-            const uint64_t hb = H4(seed, (uint64_t)bx, (uint64_t)by, 0);
-            if (mode == 1) {
-              const uint32_t cls = (uint32_t)(H4(seed, (uint64_t)bx, (uint64_t)by, 1) % 3);
-              if (cls == 0) v = (uint32_t)(H4(seed, (uint64_t)bx, (uint64_t)by, 2) % (M + 1));
-              else if (cls == 1) v = g;
-              else v = (uint32_t)(H4(seed, (uint64_t)f, (uint64_t)x, (uint64_t)y) % (M + 1));
-            } else if ((int)(hb % 100) < pct) {
-              v = (uint32_t)(H4(seed, (uint64_t)f, (uint64_t)x, (uint64_t)y) % (M + 1));
-            } else {
-              v = g;
-            }
-            if (bps == 1) base[(size_t)y * W + x] = (unsigned char)v;
-            else reinterpret_cast<uint16_t*>(base)[(size_t)y * W + x] = (uint16_t)v;
-          }
-        }
-      }
-    };
-    int nt = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
-    nt = std::min(nt, frames);
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t) {
-      const int f0 = (int)((int64_t)frames * t / nt), f1 = (int)((int64_t)frames * (t + 1) / nt);
-      th.emplace_back(work, f0, f1);
-    }
-    for (auto& t : th) t.join();
-  });
-}
-
-sc_status sc_synth_times(uint64_t seed, int32_t tag, int32_t cells, double sigma, double* out) {
-  return guarded([&] {
-    if (!out || cells < 1) fail(SC_ERR_USAGE, "bad synth arguments");
-    for (int i = 0; i < cells; ++i) {
-      const double u1 = ((H4(seed, 0x71e5ull + (uint64_t)tag, (uint64_t)i, 1) >> 11) + 1) *
-                        (1.0 / 9007199254740992.0);
-      const double u2 = (H4(seed, 0x71e5ull + (uint64_t)tag, (uint64_t)i, 2) >> 11) *
-                        (1.0 / 9007199254740992.0);
-      const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
-      out[i] = (double)(float)std::exp(sigma * z);
-    }
-  });
-}
-
 }  // extern "C"

@@ -218,3 +218,21 @@ def test_shard_merge_wide_counts():
     res[0].argmin.n_slices = 1
     check(lib().sc_shard_merge(1, world, F, C.cast(recs, C.c_void_p), C.cast(res, C.c_void_p)))
     assert res[0].candidates_step1 | (res[0].candidates_step1_hi << 64) == total
+
+
+def test_synthetic_inputs_reproduce_the_golden_hashes():
+    """synth/libscsynth.so regenerates the very estimate maps the reference
+    fixtures were made from (configs.json cfg1-3, ladder.json cfg4 / cfg5)."""
+    from paper_2012_14792_b200 import workloads as wl
+
+    def h(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+    cfgs = json.load(open(os.path.join(GOLDEN, "configs.json")))
+    for ci in ("1", "2", "3"):
+        fr = cfgs[ci]["frames"][0]
+        tr = wl.cost_trace(wl.WORKLOADS[int(ci)], frames=fr["poc"])
+        assert h(tr.est[fr["poc"] - 1]) == fr["est_hash"], ci
+    lad = json.load(open(os.path.join(GOLDEN, "ladder.json")))["grids"]
+    for ci in ("4", "5"):
+        tr = wl.cost_trace(wl.WORKLOADS[int(ci)], frames=1)
+        assert h(tr.est[0]) == lad[ci]["est_hash"], ci
