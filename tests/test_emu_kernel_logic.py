@@ -152,8 +152,8 @@ def test_step2_vs_oracle(emu, oracle, seed, prune):
 
 
 def test_dp_counts_match_enumeration(emu, oracle):
-    """The exact counting DP (pruned mode's counters) == enumerated counts,
-    and the survey's reference-enumerated ladder values."""
+    """The exact counting DP (pruned mode's counters) == the oracle's
+    enumerated counts on 40 random grids up to 7x7."""
     rng = np.random.default_rng(9)
     for _ in range(40):
         cols, rows = int(rng.integers(1, 8)), int(rng.integers(1, 8))
@@ -174,3 +174,29 @@ def test_baseline_grid_counts(emu, oracle):
         for cov in (0, 1):
             _, _, cnt, _, _ = emu.search(cols, rows, n, 3.0, mc, cov, 1, rt, item_target=512)
             assert cnt[0] == oracle.count(cols, rows, n, 3.0, mc, cov)
+
+
+def test_dp_counts_match_reference_ladder(emu):
+    """The counting DP == the counts the UNMODIFIED reference enumerated on the
+    real cfg4 (30x17) and cfg5 (60x34) grids (tests/golden/ladder.json,
+    SURVEY.md §8c: 480 ... 314,959,056 candidates) and on the SPEC / survey
+    instances of spec_kats.json."""
+    import json
+    import os
+    from conftest import GOLDEN
+    lad = json.load(open(os.path.join(GOLDEN, "ladder.json")))
+    for c in lad["cases"]:
+        cols, rows = (30, 17) if c["cfg"] == 4 else (60, 34)
+        rt = np.ones((1, cols * (cols + 1) // 2 * (rows * (rows + 1) // 2)))
+        _, _, cnt, _, _ = emu.search(cols, rows, c["n"], c["k"], c["max_tile_cols"], 0, 1, rt,
+                                     prune=1)
+        assert cnt[0] == c["candidates_step1"] == c["candidates_step2"], c
+    kats = json.load(open(os.path.join(GOLDEN, "spec_kats.json")))["enumeration_counts"]
+    for key, want in kats.items():
+        dims, ctu, n, mc = key.split("/")
+        fw, fh = map(int, dims.split("x"))
+        ctu, n, mc = int(ctu), int(n[1:]), int(mc[1:])
+        cols, rows = -(-fw // ctu), -(-fh // ctu)
+        rt = np.ones((1, cols * (cols + 1) // 2 * (rows * (rows + 1) // 2)))
+        _, _, cnt, _, _ = emu.search(cols, rows, n, 3.0, mc, 0, 1, rt, prune=1)
+        assert cnt[0] == want, key
