@@ -63,6 +63,24 @@ void enumerate_emit_device(const WorkItem* d_items, uint32_t n_items, int cols, 
                            double k, int covering, const uint64_t* d_counts,
                            const uint64_t* d_offsets, uint64_t first, uint64_t limit,
                            uint8_t* d_out, cudaStream_t st);
+// exhaustive step 1 as a trace interpreter (trace.cu)
+bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
+                        double k, int covering, uint64_t max_ops, DevBuf& ops, DevBuf& skel_pos,
+                        DevBuf& skel_ord, DevBuf& chunk_skel, DevBuf& scratch, DevBuf& temp,
+                        int sm_count, TraceHost* out, cudaStream_t st);
+size_t trace_smem_bytes(int depth_cap);
+int trace_blocks_per_sm(int fpw, int depth_cap);
+void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skel_pos,
+                       const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
+                       uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* rt,
+                       const uint32_t* rts, int depth_cap, uint64_t* lanes,
+                       unsigned long long* count_out, cudaStream_t st);
+void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
+                           const uint32_t* ops, const uint32_t* skel_pos, const uint64_t* skel_ord,
+                           uint32_t nskel, int cols, int rows, int n,
+                           const unsigned long long* count, double lambda, const uint64_t* vals,
+                           const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
+                           cudaStream_t st);
 }  // namespace scb
 
 namespace scb {
@@ -460,11 +478,85 @@ void finish_schedule(Plan* p) {
   p->order_state = 2;
 }
 
+// Exhaustive step 1 through the candidate trace (trace.cuh): on by default
+// for families up to kTraceMaxCands candidates (the build runs the
+// enumeration once per plan); SLICECRAFT_B200_TRACE=0 keeps the DFS walk.
+constexpr double kTraceMaxCands = 2e9;
+constexpr uint64_t kTraceMaxOps = 1ull << 28;  // 1 GiB of ops
+bool trace_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_TRACE");
+  return !(v && v[0] == '0');
+}
+
+// Builds the plan's trace on first use; false when the plan does not use one.
+bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& cfg,
+                  cudaStream_t st) {
+  if (p->trace_state != 0) return p->trace_state == 1;
+  p->trace_state = -1;
+  if ((double)plan_count(p, g, cfg) > kTraceMaxCands) return false;
+  if ((size_t)n_xw(g.cols) * n_yh(g.rows) > ((size_t)1 << 22)) return false;
+  TraceHost th;
+  DevBuf scratch, temp;
+  const bool ok = trace_build_device(p->d_items.as<WorkItem>(), (uint32_t)p->items.size(), g.cols,
+                                     g.rows, cfg.n_slices, cfg.k_area, cfg.coverage, kTraceMaxOps,
+                                     p->tr_ops, p->tr_skel_pos, p->tr_skel_ord, p->tr_chunk_skel,
+                                     scratch, temp, ctx->sm_count, &th, st);
+  scratch.release();
+  temp.release();
+  if (!ok) {
+    p->tr_ops.release();
+    p->tr_skel_pos.release();
+    p->tr_skel_ord.release();
+    p->tr_chunk_skel.release();
+    return false;
+  }
+  if ((unsigned __int128)th.cands != plan_count(p, g, cfg))
+    fail(SC_ERR_INTERNAL, "candidate trace count differs from the counting DP");
+  p->trace_ops = th.ops;
+  p->trace_cands = th.cands;
+  p->trace_nskel = th.nskel;
+  p->trace_chunks = th.n_chunks;
+  p->trace_state = 1;
+  return true;
+}
+
 // One search step over all frame groups; finalize writes FrameBest[step] and,
 // after step 1, the device budgets of step 2.  No host synchronisation.
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
                   const Layouts& L, int step, bool compute_bounds, cudaStream_t st) {
   const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
+  if (step == 1 && !prune && trace_enabled() && ensure_trace(ctx, plan, g, cfg, st)) {
+    const int depth_cap = std::max(cfg.n_slices, 2);
+    const int blocks = ctx->sm_count * trace_blocks_per_sm(L.fpw, depth_cap);
+    const uint32_t n_lanes = (uint32_t)blocks * 256;
+    const size_t lane_bytes = (size_t)n_lanes * 2 * sizeof(uint64_t);
+    ctx->lanes.ensure(lane_bytes * L.groups);
+    ctx->counter.ensure((size_t)L.groups * 8 * sizeof(uint64_t));
+    ctx->frame_best.ensure((size_t)2 * L.groups * L.fpw * sizeof(FrameBest));
+    ctx->budget.ensure((size_t)L.groups * L.fpw * sizeof(int64_t));
+    for (int gi = 0; gi < L.groups; ++gi) {
+      uint64_t* ctr = ctx->counter.as<uint64_t>() + 8 * gi;
+      SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));
+      uint64_t* lanes = reinterpret_cast<uint64_t*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
+      trace_walk_launch(L.fpw, blocks, plan->tr_ops.as<uint32_t>(),
+                        plan->tr_skel_pos.as<uint32_t>(), plan->tr_skel_ord.as<uint64_t>(),
+                        plan->tr_chunk_skel.as<uint32_t>(), plan->trace_chunks,
+                        (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,
+                        reinterpret_cast<uint32_t*>(ctr),
+                        ctx->rt_search.as<uint32_t>() + (size_t)gi * L.nr * L.fpw,
+                        ctx->rt_split.as<uint32_t>() + (size_t)gi * L.nr * L.fpw, depth_cap, lanes,
+                        reinterpret_cast<unsigned long long*>(ctr + 1), st);
+      trace_finalize_launch(L.fpw, std::min(L.fpw, L.frames - gi * L.fpw), n_lanes, lanes,
+                            plan->tr_ops.as<uint32_t>(), plan->tr_skel_pos.as<uint32_t>(),
+                            plan->tr_skel_ord.as<uint64_t>(), plan->trace_nskel, g.cols, g.rows,
+                            cfg.n_slices, reinterpret_cast<unsigned long long*>(ctr + 1),
+                            cfg.lambda, ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr,
+                            ctx->nvals.as<uint32_t>() + (size_t)gi * L.fpw, L.nr,
+                            ctx->frame_best.as<FrameBest>() + (size_t)gi * L.fpw,
+                            ctx->budget.as<int64_t>() + (size_t)gi * L.fpw, st);
+    }
+    return;
+  }
   const int bps =
       search_blocks_per_sm(L.fpw, step, prune,
                            search_smem_bytes(g.cols, g.rows, cfg.n_slices, step, prune));
@@ -1033,6 +1125,7 @@ sc_ctx::~sc_ctx() {
     p->d_cost.release();
     p->d_enum_counts.release();
     p->d_enum_offsets.release();
+    for (auto* b : {&p->tr_ops, &p->tr_skel_pos, &p->tr_skel_ord, &p->tr_chunk_skel}) b->release();
     delete p;
   }
   for (auto& e : ev)

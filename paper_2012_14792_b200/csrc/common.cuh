@@ -147,6 +147,12 @@ struct Plan {
   unsigned __int128 count = 0;
   DevBuf d_items, d_bmax;
   bool uploaded = false;
+  // exhaustive step 1 as a trace interpreter (trace.cu): the family's
+  // candidate trace, its skeleton starts (op index, first ordinal) and chunks
+  int trace_state = 0;  // 0: not built, 1: built, -1: not used for this plan
+  uint64_t trace_ops = 0, trace_cands = 0;
+  uint32_t trace_nskel = 0, trace_chunks = 0;
+  DevBuf tr_ops, tr_skel_pos, tr_skel_ord, tr_chunk_skel;
   // candidate stream (enumerate.cu): per-item counts, their offsets, total
   DevBuf d_enum_counts, d_enum_offsets;
   bool have_enum = false;
@@ -205,6 +211,12 @@ struct FrameBest {
   uint8_t snap[kSnapBytes];
   int32_t found;
   int32_t pad;
+};
+
+// Size of a plan's candidate trace (trace.cu).
+struct TraceHost {
+  uint64_t ops = 0, cands = 0;
+  uint32_t nskel = 0, n_chunks = 0;
 };
 
 // Verdict of the device post-check of one partition (validate.cu).

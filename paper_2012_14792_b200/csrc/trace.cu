@@ -1,0 +1,374 @@
+// K4 (exhaustive step 1) as an interpreter of the plan's candidate trace
+// (trace.cuh): build the trace once per plan, then every call streams it.
+//
+// Build (first call of a plan): one thread per work item runs the reference
+// enumeration below its width prefix twice -- counting ops, candidates and
+// skeletons, then writing them at scanned offsets -- and the trace is cut into
+// chunks of ~kChunkOps ops at skeleton starts (the interpreter's state resets
+// there), each with the global ordinal of its first candidate.
+//
+// Walk (every call): persistent warps take chunks from an atomic counter; the
+// 32 lanes of a warp are frames (lanes = FPW frames x J slots), so every op is
+// warp-uniform: a warp fetches 32 ops with one coalesced load and broadcasts
+// them with shuffles.  Per lane: the running maxima P[depth] (shared memory,
+// [depth][lane]), the best (time key, ordinal) and the tie threshold.  A LEAF
+// evaluates its candidates' times as one min-reduction over consecutive split-
+// table keys; only a leaf that beats the lane's best is replayed in order.
+// Every candidate's time key is loaded; the candidate set, order, ordinals and
+// first-in-order tie rule are the reference's (search.cpp:257-298).
+//
+// Finalize: per frame, the lexicographic minimum of (time key, ordinal) over
+// the lanes; the winner's layout is rebuilt from its skeleton's ops
+// (trace_layout) into the same FrameBest record the walk kernels produce.
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+#include "search_walk.cuh"
+#include "trace.cuh"
+
+namespace scb {
+
+// ---- build -----------------------------------------------------------------------
+__global__ void k_trace_count(const WorkItem* __restrict__ items, uint32_t n_items, int cols,
+                              int rows, int n, double k, int covering, uint64_t* ops,
+                              uint64_t* cands, uint64_t* skels) {
+  const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  TraceCount c;
+  trace_item(items[it], cols, rows, n, k, covering, c);
+  ops[it] = c.ops;
+  cands[it] = c.cands;
+  skels[it] = c.skels;
+}
+
+__global__ void k_trace_emit(const WorkItem* __restrict__ items, uint32_t n_items, int cols,
+                             int rows, int n, double k, int covering,
+                             const uint64_t* __restrict__ op_off, const uint64_t* __restrict__ cand_off,
+                             const uint64_t* __restrict__ skel_off, uint32_t* ops,
+                             uint32_t* skel_pos, uint64_t* skel_ord) {
+  const uint32_t it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  TraceWrite w;
+  w.ops = ops + op_off[it];
+  w.op_base = op_off[it];
+  w.cand = cand_off[it];
+  w.skel_pos = skel_pos + skel_off[it];
+  w.skel_ord = skel_ord + skel_off[it];
+  trace_item(items[it], cols, rows, n, k, covering, w);
+}
+
+// chunk c starts at the first skeleton whose first op is at or after c * size
+__global__ void k_trace_chunks(const uint32_t* __restrict__ skel_pos, uint32_t nskel,
+                               uint32_t n_chunks, uint32_t size, uint32_t* chunk_skel) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > n_chunks) return;
+  if (c == n_chunks) {
+    chunk_skel[c] = nskel;
+    return;
+  }
+  const uint64_t target = (uint64_t)c * size;
+  uint32_t lo = 0, hi = nskel;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (skel_pos[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  chunk_skel[c] = lo;
+}
+
+// ---- walk ------------------------------------------------------------------------
+struct TraceArgs {
+  const uint32_t* ops;
+  const uint32_t* skel_pos;   // [nskel + 1] (last = total ops)
+  const uint64_t* skel_ord;   // [nskel + 1] (last = total candidates)
+  const uint32_t* chunk_skel; // [n_chunks + 1]
+  uint32_t n_chunks;
+  uint32_t chunk_offset, chunk_stride;  // shard: chunks offset, offset + stride, ...
+  uint32_t n_mine;            // chunks of this shard
+  uint32_t* counter;
+  const uint32_t* rt;         // [NR][FPW] time keys of this frame group
+  const uint32_t* rts;        // [NR][FPW] split table
+  int depth_cap;              // P stack entries per lane
+  uint64_t* lanes;            // [warps * 32] x {time key (u64), ordinal}
+  unsigned long long* count_out;
+};
+
+template <int FPW>
+__global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
+  constexpr int J = 32 / FPW;
+  extern __shared__ uint32_t tr_sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int f = lane % FPW, slot = lane / FPW;
+  uint32_t* P = tr_sm + (size_t)wib * a.depth_cap * 32 + lane;  // P[d] at P[d * 32]
+  const uint32_t* __restrict__ rt = a.rt + f;
+  const uint32_t* __restrict__ rts = a.rts + f;
+  tkey best = kKeyInf;
+  uint64_t best_ord = ~0ull;
+  uint64_t count = 0;
+  while (true) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(a.counter, 1u);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= a.n_mine) break;
+    const uint32_t chunk = a.chunk_offset + k * a.chunk_stride;
+    const uint32_t s0 = a.chunk_skel[chunk], s1 = a.chunk_skel[chunk + 1];
+    if (s0 >= s1) continue;
+    const uint32_t b = a.skel_pos[s0], e = a.skel_pos[s1];
+    uint64_t ord = a.skel_ord[s0];
+    // ties: a candidate of this chunk precedes the lane's best iff the best
+    // comes from a later ordinal; inside the chunk ordinals only grow
+    tkey bcmp = (best != kKeyInf && best_ord > ord) ? best + 1 : best;
+    int ld = 0;
+    for (uint32_t p0 = b; p0 < e; p0 += 32) {
+      const uint32_t mine = p0 + lane < e ? __ldg(a.ops + p0 + lane) : 0u;
+      const int nb = (int)min(32u, e - p0);
+#pragma unroll 1
+      for (int q = 0; q < nb; ++q) {
+        const uint32_t op = __shfl_sync(0xffffffffu, mine, q);
+        const uint32_t code = op >> 30;
+        const uint32_t idx = op & kTrIdxMask;
+        if (code == kOpPush) {
+          const int d = (int)((op >> 23) & 63u);
+          const uint32_t v = ((op >> 29) & 1u) ? __ldg(rts + (size_t)idx * FPW)
+                                               : __ldg(rt + (size_t)idx * FPW);
+          P[(d + 1) * 32] = kmax(P[d * 32], v);
+        } else if (code == kOpLeaf) {
+          const int cnt = (int)((op >> 22) & 255u);
+          const tkey Pl = P[ld * 32];
+          if (cnt == 0) {  // the skeleton's single candidate
+            if (slot == 0 && Pl < bcmp) {
+              best = Pl;
+              bcmp = Pl;
+              best_ord = ord;
+            }
+            ord += 1;
+            count += 1;
+            continue;
+          }
+          const uint32_t* pv = rts + (size_t)idx * FPW;
+          tkey m = kKeyInf;
+#pragma unroll 4
+          for (int h = slot; h < cnt; h += J) m = kmin(m, __ldg(pv + (size_t)h * FPW));
+          if (kmax(Pl, m) < bcmp) {  // replay in order: the first minimum wins
+            const tkey t = kmax(Pl, m);
+            int hit = slot;
+            for (int h = slot; h < cnt; h += J)
+              if (kmax(Pl, __ldg(pv + (size_t)h * FPW)) == t) {
+                hit = h;
+                break;
+              }
+            best = t;
+            bcmp = t;
+            best_ord = ord + (uint64_t)hit;
+          }
+          ord += (uint64_t)cnt;
+          count += (uint64_t)cnt;
+        } else if ((op >> 29) & 1u) {  // FIX
+          P[0] = kmax(P[0], __ldg(rt + (size_t)idx * FPW));
+        } else {  // SKEL
+          ld = (int)((op >> 23) & 63u);
+          P[0] = 0;
+        }
+      }
+    }
+  }
+  const size_t gl = (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * 32 + lane;
+  a.lanes[2 * gl] = best == kKeyInf ? ~0ull : (uint64_t)best;
+  a.lanes[2 * gl + 1] = best_ord;
+  if (lane == 0 && count) atomicAdd(a.count_out, (unsigned long long)count);
+}
+
+__device__ __forceinline__ int64_t budget_key_t(const uint64_t* vals, uint32_t n, double b) {
+  if (!(b >= 0.0)) return -1;
+  const uint64_t bits = (uint64_t)__double_as_longlong(b);
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (vals[mid] <= bits) lo = mid + 1;
+    else hi = mid;
+  }
+  return (int64_t)lo - 1;
+}
+
+// Per frame: min (key, ordinal) over the lanes of frame f, then the winner's
+// layout from its skeleton's ops; the step-2 budget as in k_finalize.
+__global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
+                                 const uint64_t* __restrict__ lanes, const uint32_t* ops,
+                                 const uint32_t* __restrict__ skel_pos,
+                                 const uint64_t* __restrict__ skel_ord, uint32_t nskel, int cols,
+                                 int rows, int n, const unsigned long long* count, double lambda,
+                                 const uint64_t* __restrict__ vals, const uint32_t* __restrict__ nvals,
+                                 size_t nr, FrameBest* __restrict__ out,
+                                 int64_t* __restrict__ budget_out) {
+  const int f = blockIdx.x;
+  if (f >= frames_in_group) return;
+  __shared__ uint64_t skey[256], sord[256];
+  uint64_t bk = ~0ull, bo = ~0ull;
+  for (uint32_t li = threadIdx.x * fpw + f; li < n_lanes; li += blockDim.x * fpw) {
+    const uint64_t k = lanes[2 * li], o = lanes[2 * li + 1];
+    if (k < bk || (k == bk && o < bo)) bk = k, bo = o;
+  }
+  skey[threadIdx.x] = bk;
+  sord[threadIdx.x] = bo;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const uint64_t k = skey[threadIdx.x + s], o = sord[threadIdx.x + s];
+      if (k < skey[threadIdx.x] || (k == skey[threadIdx.x] && o < sord[threadIdx.x]))
+        skey[threadIdx.x] = k, sord[threadIdx.x] = o;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  FrameBest* o = out + f;
+  const uint64_t* fv = vals + (size_t)f * nr;
+  bk = skey[0];
+  bo = sord[0];
+  // step 1 keeps `t < best_t` from best_t = +inf (search.cpp:277-285)
+  const bool found = bk != ~0ull && fv[bk] != 0x7ff0000000000000ull;
+  o->t = found ? fv[bk] : ~0ull;
+  o->sse = __longlong_as_double(0x7ff0000000000000ll);
+  o->item = found ? bo : ~0ull;  // the global ordinal (shard merge orders by it)
+  o->ord = 0;
+  o->count = *count;
+  o->scored = *count * (uint64_t)fpw;
+  o->found = found ? 1 : 0;
+  if (!found) return;
+  uint32_t lo = 0, hi = nskel;  // last skeleton whose first ordinal <= bo
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (skel_ord[mid] <= bo) lo = mid;
+    else hi = mid;
+  }
+  if (!trace_layout(ops + skel_pos[lo], skel_pos[lo + 1] - skel_pos[lo], bo - skel_ord[lo], cols,
+                    rows, n, o->snap))
+    o->found = 0;
+  if (budget_out) {
+    const double tmin = __longlong_as_double((long long)o->t);
+    budget_out[f] = budget_key_t(fv, nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, lambda)));
+  }
+}
+
+// ---- host side -------------------------------------------------------------------
+
+// Builds the trace into the plan's buffers.  Returns false (and builds
+// nothing) when it would exceed `max_ops`.
+bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
+                        double k, int covering, uint64_t max_ops, DevBuf& ops, DevBuf& skel_pos,
+                        DevBuf& skel_ord, DevBuf& chunk_skel, DevBuf& scratch, DevBuf& temp,
+                        int sm_count, TraceHost* out, cudaStream_t st) {
+  scratch.ensure((size_t)n_items * 6 * sizeof(uint64_t) + 64);
+  uint64_t* c_ops = scratch.as<uint64_t>();
+  uint64_t* c_cand = c_ops + n_items;
+  uint64_t* c_skel = c_cand + n_items;
+  uint64_t* o_ops = c_skel + n_items;
+  uint64_t* o_cand = o_ops + n_items;
+  uint64_t* o_skel = o_cand + n_items;
+  const unsigned blocks = (n_items + 127) / 128;
+  k_trace_count<<<blocks, 128, 0, st>>>(d_items, n_items, cols, rows, n, k, covering, c_ops, c_cand,
+                                        c_skel);
+  SCB_CUDA(cudaGetLastError());
+  size_t tb = 0;
+  SCB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c_ops, o_ops, (int)n_items, st));
+  temp.ensure(tb + 16);
+  for (int i = 0; i < 3; ++i)
+    SCB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, c_ops + (size_t)i * n_items,
+                                           o_ops + (size_t)i * n_items, (int)n_items, st));
+  uint64_t last[6];
+  for (int i = 0; i < 3; ++i) {
+    SCB_CUDA(cudaMemcpyAsync(&last[i], c_ops + (size_t)i * n_items + n_items - 1, 8,
+                             cudaMemcpyDeviceToHost, st));
+    SCB_CUDA(cudaMemcpyAsync(&last[3 + i], o_ops + (size_t)i * n_items + n_items - 1, 8,
+                             cudaMemcpyDeviceToHost, st));
+  }
+  SCB_CUDA(cudaStreamSynchronize(st));
+  const uint64_t tot_ops = last[0] + last[3], tot_cand = last[1] + last[4],
+                 tot_skel = last[2] + last[5];
+  if (tot_ops > max_ops || tot_ops >= (1ull << 32) || tot_skel >= (1ull << 32)) return false;
+  ops.ensure(tot_ops * sizeof(uint32_t) + 128);
+  skel_pos.ensure((tot_skel + 1) * sizeof(uint32_t));
+  skel_ord.ensure((tot_skel + 1) * sizeof(uint64_t));
+  k_trace_emit<<<blocks, 128, 0, st>>>(d_items, n_items, cols, rows, n, k, covering, o_ops,
+                                       o_cand, o_skel, ops.as<uint32_t>(), skel_pos.as<uint32_t>(),
+                                       skel_ord.as<uint64_t>());
+  SCB_CUDA(cudaGetLastError());
+  const uint32_t tail_pos = (uint32_t)tot_ops;
+  SCB_CUDA(cudaMemcpyAsync(skel_pos.as<uint32_t>() + tot_skel, &tail_pos, 4, cudaMemcpyHostToDevice,
+                           st));
+  SCB_CUDA(cudaMemcpyAsync(skel_ord.as<uint64_t>() + tot_skel, &tot_cand, 8, cudaMemcpyHostToDevice,
+                           st));
+  // ~128 chunks per SM (persistent warps take them dynamically), 256..8192 ops
+  const uint64_t chunk_ops = std::min<uint64_t>(
+      8192, std::max<uint64_t>(256, (tot_ops + (uint64_t)sm_count * 128 - 1) /
+                                        ((uint64_t)sm_count * 128)));
+  const uint32_t n_chunks = (uint32_t)std::max<uint64_t>(1, (tot_ops + chunk_ops - 1) / chunk_ops);
+  chunk_skel.ensure(((size_t)n_chunks + 1) * sizeof(uint32_t));
+  k_trace_chunks<<<(n_chunks + 1 + 255) / 256, 256, 0, st>>>(skel_pos.as<uint32_t>(),
+                                                             (uint32_t)tot_skel, n_chunks,
+                                                             (uint32_t)chunk_ops,
+                                                             chunk_skel.as<uint32_t>());
+  SCB_CUDA(cudaGetLastError());
+  SCB_CUDA(cudaStreamSynchronize(st));  // tail_pos / tot_cand live on this stack frame
+  out->ops = tot_ops;
+  out->cands = tot_cand;
+  out->nskel = (uint32_t)tot_skel;
+  out->n_chunks = n_chunks;
+  return true;
+}
+
+size_t trace_smem_bytes(int depth_cap) { return (size_t)8 * depth_cap * 32 * sizeof(uint32_t); }
+
+int trace_blocks_per_sm(int fpw, int depth_cap) {
+  int nb = 0;
+  const size_t smem = trace_smem_bytes(depth_cap);
+#define OCC(F) \
+  if (fpw == F) SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk<F>, 256, smem));
+  OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
+#undef OCC
+  return nb < 1 ? 1 : nb;
+}
+
+void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skel_pos,
+                       const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
+                       uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* rt,
+                       const uint32_t* rts, int depth_cap, uint64_t* lanes,
+                       unsigned long long* count_out, cudaStream_t st) {
+  TraceArgs a;
+  a.ops = ops;
+  a.skel_pos = skel_pos;
+  a.skel_ord = skel_ord;
+  a.chunk_skel = chunk_skel;
+  a.n_chunks = n_chunks;
+  a.chunk_offset = rank;
+  a.chunk_stride = world;
+  a.n_mine = n_chunks > rank ? (n_chunks - rank + world - 1) / world : 0;
+  a.counter = counter;
+  a.rt = rt;
+  a.rts = rts;
+  a.depth_cap = depth_cap;
+  a.lanes = lanes;
+  a.count_out = count_out;
+  const size_t smem = trace_smem_bytes(depth_cap);
+  switch (fpw) {
+#define L(F) \
+  case F: k_trace_walk<F><<<blocks, 256, smem, st>>>(a); break;
+    L(1) L(2) L(4) L(8) L(16) L(32)
+#undef L
+    default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
+  }
+  SCB_CUDA(cudaGetLastError());
+}
+
+void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
+                           const uint32_t* ops, const uint32_t* skel_pos, const uint64_t* skel_ord,
+                           uint32_t nskel, int cols, int rows, int n,
+                           const unsigned long long* count, double lambda, const uint64_t* vals,
+                           const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
+                           cudaStream_t st) {
+  k_trace_finalize<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
+                                                    skel_pos, skel_ord, nskel, cols, rows, n, count,
+                                                    lambda, vals, nvals, nr, out, budget_out);
+  SCB_CUDA(cudaGetLastError());
+}
+
+}  // namespace scb

@@ -1,0 +1,352 @@
+// The candidate family compiled into a time-evaluation program ("trace").
+//
+// The ColumnSplit enumeration (search.cpp:110-196) does not depend on the
+// frame: for a given grid and configuration it always yields the same
+// candidates in the same order.  Step 1 of the exhaustive search only needs,
+// per candidate, the maximum of its slices' time keys.  So instead of
+// re-running the DFS (widths, runs, heights, area windows) for every call --
+// which is what the warp-uniform walk in search_walk.cuh does, and where most
+// of its instructions go -- the DFS runs ONCE per plan and writes its
+// pre-order as a stream of 32-bit ops; the per-call kernel (trace.cu) is an
+// interpreter that keeps one running maximum per DFS depth:
+//
+//   SKEL  ld        new skeleton (widths + runs): P[0] = 0, its leaf depth ld
+//   FIX   idx       P[0] = max(P[0], rt[idx])          a one-run column
+//   PUSH  d, T, idx P[d+1] = max(P[d], T[idx])          a run of a multi-run
+//                   column; T = the split table (run + forced rest of its
+//                   column) for the column's second-to-last run, else rt
+//   LEAF  idx, cnt  candidates time max(P[ld], rts[idx + i]), i < cnt (<= 255): the
+//                   last decision run takes cnt consecutive heights (its
+//                   forced rest and any later one-run columns are in the key)
+//   LEAF  -, 0      the skeleton's single candidate (no decision run): P[ld]
+//
+// Only ops that lead to a candidate are emitted (a PUSH is written lazily,
+// right before the first LEAF below it), so the trace holds every candidate
+// exactly once, in the reference's enumeration order: candidate ordinals are
+// the running sum of the LEAF counts.  The trace is independent of k, of the
+// coverage flag and of the frame: those only decide which ops exist.
+//
+// Written as __host__ __device__ code: the generator runs on the device (two
+// passes over the plan's work items, trace.cu) and, for the CPU test suite,
+// on the host (tests/emu), together with a scalar reference interpreter.
+#pragma once
+
+#include <stdint.h>
+
+#include "plan.h"
+#include "slicecraft_b200.h"
+
+#ifdef __CUDACC__
+#define SCB_TR_HD __host__ __device__ __forceinline__
+#else
+#define SCB_TR_HD inline
+#endif
+
+namespace scb {
+
+constexpr uint32_t kOpPush = 0u, kOpLeaf = 2u, kOpSkel = 3u;  // bits 31..30
+constexpr int kTrIdxBits = 22;                                 // rectangle index
+constexpr uint32_t kTrIdxMask = (1u << kTrIdxBits) - 1u;
+
+SCB_TR_HD uint32_t op_push(int d, bool split, uint32_t idx) {
+  return (kOpPush << 30) | ((split ? 1u : 0u) << 29) | ((uint32_t)d << 23) | idx;
+}
+SCB_TR_HD uint32_t op_leaf(uint32_t idx, int cnt) {
+  return (kOpLeaf << 30) | ((uint32_t)cnt << 22) | idx;
+}
+SCB_TR_HD uint32_t op_skel(int ld) { return (kOpSkel << 30) | ((uint32_t)ld << 23); }
+SCB_TR_HD uint32_t op_fix(uint32_t idx) { return (kOpSkel << 30) | (1u << 29) | idx; }
+
+SCB_TR_HD int tr_xw(int cols, int x0, int w) { return x0 * cols - (x0 * (x0 - 1)) / 2 + (w - 1); }
+SCB_TR_HD int tr_yh(int rows, int y0, int h) { return y0 * rows - (y0 * (y0 - 1)) / 2 + (h - 1); }
+
+// Counting sink (pass 1) and writing sink (pass 2) of the generator.
+struct TraceCount {
+  uint64_t ops = 0, cands = 0, skels = 0;
+  SCB_TR_HD void skel(int) { ++ops; ++skels; }
+  SCB_TR_HD void fix(uint32_t) { ++ops; }
+  SCB_TR_HD void push(int, bool, uint32_t) { ++ops; }
+  SCB_TR_HD void leaf(uint32_t, int cnt) { ++ops; cands += cnt ? (uint64_t)cnt : 1u; }
+};
+struct TraceWrite {
+  uint32_t* ops;          // this item's ops
+  uint64_t pos = 0;       // ops written
+  uint64_t cand;          // global ordinal of the next candidate
+  uint32_t* skel_pos;     // this item's skeleton starts: global op index
+  uint64_t* skel_ord;     // and the ordinal of their first candidate
+  uint64_t op_base;       // global index of ops[0]
+  uint64_t nsk = 0;
+  SCB_TR_HD void skel(int ld) {
+    skel_pos[nsk] = (uint32_t)(op_base + pos);
+    skel_ord[nsk] = cand;
+    ++nsk;
+    ops[pos++] = op_skel(ld);
+  }
+  SCB_TR_HD void fix(uint32_t idx) { ops[pos++] = op_fix(idx); }
+  SCB_TR_HD void push(int d, bool s, uint32_t idx) { ops[pos++] = op_push(d, s, idx); }
+  SCB_TR_HD void leaf(uint32_t idx, int cnt) {
+    ops[pos++] = op_leaf(idx, cnt);
+    cand += cnt ? (uint64_t)cnt : 1u;
+  }
+};
+
+// The enumeration below the width prefix of one work item (plan.h), in the
+// reference's order: remaining widths (search.cpp:133-143; covering: the last
+// width closes the grid), runs per column (145-161), run heights with the
+// area test k * (double)amin > (double)amax (163-190).  The area test prunes
+// partial candidates exactly as the reference does (adding areas only
+// tightens it), so the emitted candidates are the reference's.
+template <class Sink>
+SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double k, int covering,
+                          Sink& out) {
+  const int c = wi.c, d = wi.d;
+  const int nyh = rows * (rows + 1) / 2;
+  int W[SC_MAX_COLS], R[SC_MAX_COLS], CL[SC_MAX_COLS + 1], SL[SC_MAX_COLS + 1];
+  // decision runs (every run of a multi-run column but its last), in order
+  int Dx0[SC_MAX_SLICES], Dw[SC_MAX_SLICES], Dleft[SC_MAX_SLICES];  // runs left incl. this
+  int H[SC_MAX_SLICES], Y0[SC_MAX_SLICES], AMIN[SC_MAX_SLICES + 1], AMAX[SC_MAX_SLICES + 1];
+  uint32_t FIXI[SC_MAX_COLS];
+  CL[0] = cols;
+  for (int i = 0; i < d; ++i) {
+    W[i] = wi.w[i];
+    CL[i + 1] = CL[i] - W[i];
+  }
+  int pos = d;
+  const bool fixed = d == c;
+  if (!fixed) W[pos] = 0;
+  while (true) {
+    if (!fixed) {
+      bool got = false;
+      while (true) {
+        const int maxw = CL[pos] - (c - pos - 1);
+        const int wv = (covering && pos == c - 1) ? (W[pos] == 0 ? maxw : maxw + 1) : W[pos] + 1;
+        if (wv > maxw) {
+          if (pos == d) break;
+          --pos;
+          continue;
+        }
+        W[pos] = wv;
+        CL[pos + 1] = CL[pos] - wv;
+        if (pos == c - 1) {
+          got = true;
+          break;
+        }
+        W[++pos] = 0;
+      }
+      if (!got) break;
+    }
+    // ---- runs per column (rec_runs)
+    int rp = 0;
+    SL[0] = n;
+    R[0] = (n - (c - 1) * rows > 1 ? n - (c - 1) * rows : 1) - 1;
+    while (rp >= 0) {
+      const int hi_r = rows < SL[rp] - (c - rp - 1) ? rows : SL[rp] - (c - rp - 1);
+      if (++R[rp] > hi_r) {
+        --rp;
+        continue;
+      }
+      SL[rp + 1] = SL[rp] - R[rp];
+      if (rp < c - 1) {
+        ++rp;
+        const int lo_r = SL[rp] - (c - rp - 1) * rows;
+        R[rp] = (lo_r > 1 ? lo_r : 1) - 1;
+        continue;
+      }
+      if (SL[c] != 0) continue;
+      // ---- one skeleton: fixed one-run columns, then the decision runs
+      int amin = 0x7fffffff, amax = 0, nl = 0, nfix = 0, x0 = 0;
+      bool ok = true;
+      for (int i = 0; i < c; ++i) {
+        if (R[i] == 1) {
+          const int a = W[i] * rows;
+          amin = a < amin ? a : amin;
+          amax = a > amax ? a : amax;
+          ok = ok && (k * (double)amin > (double)amax);
+          FIXI[nfix++] = (uint32_t)(tr_xw(cols, x0, W[i]) * nyh + tr_yh(rows, 0, rows));
+        } else {
+          for (int j = 0; j < R[i] - 1; ++j, ++nl) {
+            Dx0[nl] = x0;
+            Dw[nl] = W[i];
+            Dleft[nl] = R[i] - j;
+          }
+        }
+        x0 += W[i];
+      }
+      if (!ok) continue;
+      bool skel_out = false;
+      int emitted = 0;  // PUSH depths already written for the current path
+      if (nl == 0) {    // the skeleton is one candidate
+        out.skel(0);
+        for (int i = 0; i < nfix; ++i) out.fix(FIXI[i]);
+        out.leaf(0, 0);
+        continue;
+      }
+      // heights DFS over the decision runs; depth nl-1 is the leaf
+      int t = 0;
+      AMIN[0] = amin;
+      AMAX[0] = amax;
+      Y0[0] = 0;
+      H[0] = 0;
+      while (t >= 0) {
+        const int w = Dw[t], left = Dleft[t], y0 = Y0[t];
+        const int rl = rows - y0;
+        const int hmax = rl - (left - 1);  // leave one row per later run of the column
+        if (t < nl - 1) {
+          int h = ++H[t];
+          if (h > hmax) {
+            --t;
+            if (t >= 0 && emitted > t) emitted = t;
+            continue;
+          }
+          int na = AMIN[t] < w * h ? AMIN[t] : w * h, nx = AMAX[t] > w * h ? AMAX[t] : w * h;
+          if (left == 2) {  // the forced rest of the column
+            const int a2 = w * (rl - h);
+            na = a2 < na ? a2 : na;
+            nx = a2 > nx ? a2 : nx;
+          }
+          if (emitted > t) emitted = t;
+          if (!(k * (double)na > (double)nx)) continue;
+          AMIN[t + 1] = na;
+          AMAX[t + 1] = nx;
+          Y0[t + 1] = left == 2 ? 0 : y0 + h;
+          H[t + 1] = 0;
+          ++t;
+          continue;
+        }
+        // leaf: the column's second-to-last run takes every admissible height;
+        // maximal runs of consecutive heights become one LEAF op each
+        const uint32_t base = (uint32_t)(tr_xw(cols, Dx0[t], w) * nyh + tr_yh(rows, y0, 1));
+        int h = 1;
+        while (h <= rl - 1) {
+          int h0 = -1;
+          for (; h <= rl - 1; ++h) {
+            const int a1 = w * h, a2 = w * (rl - h);
+            const int na = AMIN[t] < (a1 < a2 ? a1 : a2) ? AMIN[t] : (a1 < a2 ? a1 : a2);
+            const int nx = AMAX[t] > (a1 > a2 ? a1 : a2) ? AMAX[t] : (a1 > a2 ? a1 : a2);
+            const bool adm = k * (double)na > (double)nx;
+            if (adm && h0 < 0) h0 = h;
+            if (!adm && h0 >= 0) break;
+          }
+          if (h0 < 0) break;
+          if (!skel_out) {
+            out.skel(nl - 1);
+            for (int i = 0; i < nfix; ++i) out.fix(FIXI[i]);
+            skel_out = true;
+            emitted = 0;
+          }
+          for (int dd = emitted; dd < nl - 1; ++dd)
+            out.push(dd, Dleft[dd] == 2,
+                     (uint32_t)(tr_xw(cols, Dx0[dd], Dw[dd]) * nyh + tr_yh(rows, Y0[dd], H[dd])));
+          emitted = nl - 1;
+          out.leaf(base + (uint32_t)(h0 - 1), h - h0);  // h - h0 <= rows - 2 <= 253
+        }
+        --t;
+      }
+    }
+    if (fixed) break;
+  }
+}
+
+// The layout of a skeleton's candidate from its ops (replay of one skeleton):
+// FIX ops give the one-run columns, the PUSH path and the LEAF the runs of
+// the multi-run columns; `which` is the candidate's position inside the
+// skeleton.  Writes the 96-byte snapshot W[16] R[16] H[64] (search.cu).
+// dec: rectangle index -> (x0, w, y0, h) decoders.
+SCB_TR_HD bool trace_layout(const uint32_t* ops, uint64_t nops, uint64_t which, int cols, int rows,
+                            int n, uint8_t* snap) {
+  const int nyh = rows * (rows + 1) / 2;
+  uint32_t path[SC_MAX_SLICES];
+  uint32_t fixes[SC_MAX_COLS];
+  int nfix = 0, ld = 0;
+  uint64_t seen = 0;
+  auto decode = [&](uint32_t idx, int& x0, int& w, int& y0, int& h) {
+    const int xw = (int)(idx / (uint32_t)nyh), yh = (int)(idx % (uint32_t)nyh);
+    x0 = 0;
+    while (tr_xw(cols, x0 + 1, 1) <= xw && x0 + 1 < cols) ++x0;
+    w = xw - tr_xw(cols, x0, 1) + 1;
+    y0 = 0;
+    while (tr_yh(rows, y0 + 1, 1) <= yh && y0 + 1 < rows) ++y0;
+    h = yh - tr_yh(rows, y0, 1) + 1;
+  };
+  for (uint64_t p = 0; p < nops; ++p) {
+    const uint32_t op = ops[p];
+    const uint32_t code = op >> 30;
+    if (code == kOpSkel) {
+      if ((op >> 29) & 1u) fixes[nfix++] = op & kTrIdxMask;
+      else if (p == 0) ld = (int)((op >> 23) & 63u);
+      else return false;  // next skeleton: `which` was not in this one
+      continue;
+    }
+    if (code == kOpPush) {
+      path[(op >> 23) & 63u] = op & kTrIdxMask;
+      continue;
+    }
+    const int cnt = (int)((op >> 22) & 255u);
+    const uint64_t m = cnt ? (uint64_t)cnt : 1u;
+    if (which >= seen + m) {
+      seen += m;
+      continue;
+    }
+    // the candidate: columns from the one-run FIXes and the decision runs
+    int cx0[SC_MAX_COLS], cw[SC_MAX_COLS], cr[SC_MAX_COLS], nc = 0;
+    uint8_t ch[SC_MAX_COLS][SC_MAX_SLICES];
+    for (int i = 0; i < nfix; ++i) {
+      int x0, w, y0, h;
+      decode(fixes[i], x0, w, y0, h);
+      cx0[nc] = x0, cw[nc] = w, cr[nc] = 1, ch[nc][0] = (uint8_t)rows;
+      ++nc;
+    }
+    if (cnt) {
+      path[ld] = (op & kTrIdxMask) + (uint32_t)(which - seen);
+      for (int dd = 0; dd <= ld; ++dd) {
+        int x0, w, y0, h;
+        decode(path[dd], x0, w, y0, h);
+        int col = -1;
+        for (int i = 0; i < nc; ++i)
+          if (cx0[i] == x0) col = i;
+        if (col < 0) {
+          col = nc++;
+          cx0[col] = x0, cw[col] = w, cr[col] = 0;
+        }
+        ch[col][cr[col]++] = (uint8_t)h;
+        // the column's second-to-last run: the forced rest follows (the leaf
+        // always is one; a PUSH is one iff its next decision run starts a new
+        // column or it is the deepest PUSH before a leaf of another column)
+        bool closes = dd == ld;
+        if (!closes) {
+          int nx0, nw, ny0, nh;
+          decode(path[dd + 1], nx0, nw, ny0, nh);
+          closes = nx0 != x0;
+        }
+        if (closes) ch[col][cr[col]++] = (uint8_t)(rows - y0 - h);
+      }
+    }
+    // columns in x order
+    for (int i = 0; i < nc; ++i)
+      for (int j = i + 1; j < nc; ++j)
+        if (cx0[j] < cx0[i]) {
+          int t;
+          t = cx0[i], cx0[i] = cx0[j], cx0[j] = t;
+          t = cw[i], cw[i] = cw[j], cw[j] = t;
+          t = cr[i], cr[i] = cr[j], cr[j] = t;
+          for (int q = 0; q < SC_MAX_SLICES; ++q) {
+            const uint8_t u = ch[i][q];
+            ch[i][q] = ch[j][q];
+            ch[j][q] = u;
+          }
+        }
+    for (int i = 0; i < SC_MAX_COLS; ++i) {
+      snap[i] = (uint8_t)(i < nc ? cw[i] : 0);
+      snap[SC_MAX_COLS + i] = (uint8_t)(i < nc ? cr[i] : 0);
+    }
+    int run = 0;
+    for (int i = 0; i < nc; ++i)
+      for (int j = 0; j < cr[i]; ++j) snap[2 * SC_MAX_COLS + run++] = ch[i][j];
+    for (; run < SC_MAX_SLICES; ++run) snap[2 * SC_MAX_COLS + run] = 0;
+    (void)n;
+    return true;
+  }
+  return false;
+}
+
+}  // namespace scb

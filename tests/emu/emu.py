@@ -21,6 +21,25 @@ class Emu:
         self.L.emu_search.argtypes = [I, I, I, D, I, I, I, I, I, P, P, P, I, C.c_size_t, I, I, P, P, P, P,
                                       P, P, P, I, I, I]
 
+    def trace_search(self, cols, rows, n, k, max_cols, coverage, rect_time, item_target=16):
+        """Exhaustive step 1 through the host build of the candidate trace
+        (csrc/trace.cuh): (t_min, count, ordinal, snapshot, found, n_ops)."""
+        rt = np.ascontiguousarray(rect_time, dtype=np.float64)
+        F = rt.shape[0]
+        t = np.zeros(F)
+        cnt = np.zeros(F, dtype=np.uint64)
+        ordn = np.zeros(F, dtype=np.uint64)
+        snap = np.zeros((F, 96), dtype=np.uint8)
+        found = np.zeros(F, dtype=np.int32)
+        nops = C.c_uint64()
+        I, D, P = C.c_int, C.c_double, C.c_void_p
+        self.L.emu_trace_search.argtypes = [I, I, I, D, I, I, I, P, C.c_size_t, P, P, P, P, P, P]
+        st = self.L.emu_trace_search(cols, rows, n, k, max_cols, coverage, F, _p(rt), item_target,
+                                     _p(t), _p(cnt), _p(ordn), _p(snap), _p(found),
+                                     C.byref(nops))
+        assert st == 0, st
+        return t, cnt, ordn, snap, found, nops.value
+
     def search(self, cols, rows, n, k, max_cols, coverage, step, rect_time, rect_sse=None,
                budget=None, warps=3, item_target=16, offset=0, stride=1, full=False, prune=0,
                order=0, split=1, split_depth=1):

@@ -233,3 +233,102 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
   }
   return 0;
 }
+
+// The exhaustive step 1 through the candidate trace (csrc/trace.cuh): the host
+// build of the same generator and a scalar interpreter (one frame at a time,
+// exact doubles instead of rank keys; max / < on doubles equal max / < on
+// the keys), plus the layout rebuilt from the winning ordinal.  Work items
+// are split in `item_target`-sized prefixes like api.cu's plan, processed in
+// order, so any item-boundary mistake shows up as a different candidate set.
+#include "trace.cuh"
+extern "C" int emu_trace_search(int cols, int rows, int n, double k, int max_tile_cols,
+                                int coverage, int frames, const double* rect_time /*[F][NR]*/,
+                                size_t item_target, double* out_t, uint64_t* out_count,
+                                uint64_t* out_ord, uint8_t* out_snap /*[F][96]*/, int* out_found,
+                                uint64_t* out_ops) {
+  const int eff = max_tile_cols > 0 ? max_tile_cols : n;
+  const int maxc = std::min(std::min(n, eff), cols);
+  const std::vector<WorkItem> items = make_items(cols, maxc, coverage == 1, item_target);
+  std::vector<uint32_t> ops;
+  std::vector<uint32_t> skel_pos;
+  std::vector<uint64_t> skel_ord;
+  uint64_t cand = 0;
+  for (const WorkItem& wi : items) {
+    TraceCount c;
+    trace_item(wi, cols, rows, n, k, coverage, c);
+    const size_t o0 = ops.size(), s0 = skel_pos.size();
+    ops.resize(o0 + c.ops);
+    skel_pos.resize(s0 + c.skels);
+    skel_ord.resize(s0 + c.skels);
+    TraceWrite w;
+    w.ops = ops.data() + o0;
+    w.op_base = o0;
+    w.cand = cand;
+    w.skel_pos = skel_pos.data() + s0;
+    w.skel_ord = skel_ord.data() + s0;
+    trace_item(wi, cols, rows, n, k, coverage, w);
+    if (w.pos != c.ops || w.cand - cand != c.cands || w.nsk != c.skels) return 3;
+    cand = w.cand;
+  }
+  skel_pos.push_back((uint32_t)ops.size());
+  skel_ord.push_back(cand);
+  *out_ops = ops.size();
+  const int nyh = rows * (rows + 1) / 2;
+  const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
+  for (int f = 0; f < frames; ++f) {
+    const double* T = rect_time + (size_t)f * nr;
+    auto clamp = [](double t) { return t > 0.0 ? t : 0.0; };  // layout_time's max from 0.0
+    auto tsplit = [&](uint32_t idx) {  // run + forced rest of its column
+      const int xw = (int)(idx / (uint32_t)nyh), yh = (int)(idx % (uint32_t)nyh);
+      int y0 = 0;
+      while (tr_yh(rows, y0 + 1, 1) <= yh && y0 + 1 < rows) ++y0;
+      const int h = yh - tr_yh(rows, y0, 1) + 1;
+      const double a = clamp(T[idx]);
+      if (y0 + h >= rows) return a;
+      const double b = clamp(T[(size_t)xw * nyh + tr_yh(rows, y0 + h, rows - y0 - h)]);
+      return a > b ? a : b;
+    };
+    std::vector<double> P(n + 2, 0.0);
+    double best = INFINITY;
+    uint64_t best_ord = ~0ull, ord = 0;
+    int ld = 0;
+    for (size_t p = 0; p < ops.size(); ++p) {
+      const uint32_t op = ops[p], code = op >> 30, idx = op & kTrIdxMask;
+      if (code == kOpPush) {
+        const int d = (int)((op >> 23) & 63u);
+        const double v = ((op >> 29) & 1u) ? tsplit(idx) : clamp(T[idx]);
+        P[d + 1] = P[d] > v ? P[d] : v;
+      } else if (code == kOpLeaf) {
+        const int cnt = (int)((op >> 22) & 255u);
+        if (cnt == 0) {
+          if (P[ld] < best) best = P[ld], best_ord = ord;
+          ord += 1;
+          continue;
+        }
+        for (int h = 0; h < cnt; ++h) {
+          const double v = tsplit(idx + (uint32_t)h);
+          const double t = P[ld] > v ? P[ld] : v;
+          if (t < best) best = t, best_ord = ord + (uint64_t)h;
+        }
+        ord += (uint64_t)cnt;
+      } else if ((op >> 29) & 1u) {
+        const double v = clamp(T[idx]);
+        P[0] = P[0] > v ? P[0] : v;
+      } else {
+        ld = (int)((op >> 23) & 63u);
+        P[0] = 0.0;
+      }
+    }
+    out_count[f] = ord;
+    out_found[f] = best_ord != ~0ull;
+    out_t[f] = best;
+    out_ord[f] = best_ord;
+    if (best_ord != ~0ull) {
+      size_t s = std::upper_bound(skel_ord.begin(), skel_ord.end(), best_ord) - skel_ord.begin() - 1;
+      if (!trace_layout(ops.data() + skel_pos[s], skel_pos[s + 1] - skel_pos[s],
+                        best_ord - skel_ord[s], cols, rows, n, out_snap + (size_t)f * kSnap))
+        return 4;
+    }
+  }
+  return 0;
+}

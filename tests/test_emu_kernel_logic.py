@@ -200,3 +200,48 @@ def test_dp_counts_match_reference_ladder(emu):
         rt = np.ones((1, cols * (cols + 1) // 2 * (rows * (rows + 1) // 2)))
         _, _, cnt, _, _ = emu.search(cols, rows, n, 3.0, mc, 0, 1, rt, prune=1)
         assert cnt[0] == want, key
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_trace_step1_matches_oracle(emu, oracle, seed):
+    """The candidate trace (csrc/trace.cuh, the exhaustive step-1 program):
+    host build of the generator + a scalar interpreter == the oracle's
+    exhaustive step 1 (t_min bit-exact, first-in-order argmin, count), on
+    random grids, both families, k down to the pathological 1.05, with items
+    split at several prefix depths."""
+    rng = np.random.default_rng(700 + seed)
+    for case in range(30):
+        cols, rows = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        n = int(rng.integers(1, min(9, cols * rows) + 1))
+        mc = int(rng.integers(0, 5))
+        k = float(rng.choice([3.0, 2.5, 1.5, 1.05]))
+        cov = int(rng.integers(0, 2))
+        F = 3
+        est = rng.lognormal(0, 0.7, (F, cols * rows))
+        est[1] = np.round(est[1])      # ties
+        est[2, :cols * rows // 3] *= -1  # non-positive slices (clamped by the max from 0.0)
+        rt = np.stack([oracle.rect_times(est[f], cols, rows) for f in range(F)])
+        t, cnt, ordn, snap, found, nops = emu.trace_search(cols, rows, n, k, mc, cov, rt,
+                                                           item_target=int(rng.integers(1, 64)))
+        for f in range(F):
+            st, e = oracle.search(cols * 32, rows * 32, 32, est[f], None, n, 0.0, k, mc, cov, 1)
+            ctx = (cols, rows, n, mc, k, cov, f)
+            if st != 0:
+                assert not found[f] and cnt[f] == 0, ctx
+                continue
+            assert found[f] and cnt[f] == e.candidates_step1, ctx
+            assert t[f] == e.t_min_us, ctx
+            assert emu.slices(snap[f], n, rows) == e.argmin1.slices(rows), ctx
+
+
+def test_trace_cfg_grids_counts_and_size(emu, oracle):
+    """cfg1 / cfg2 / cfg3 grids: trace candidate counts (= the reference's);
+    the trace stays within two ops per candidate."""
+    for cols, rows, n, mc, want in [(15, 9, 4, 2, 1232), (15, 9, 8, 4, 171788),
+                                    (30, 17, 8, 0, 66007331)]:
+        est = np.ones((1, cols * rows))
+        rt = np.stack([oracle.rect_times(est[0], cols, rows)])
+        _, cnt, _, _, found, nops = emu.trace_search(cols, rows, n, 3.0, mc, 0, rt,
+                                                     item_target=4096)
+        assert cnt[0] == want
+        assert nops < 2 * want

@@ -78,12 +78,16 @@ def test_rect_tables_bit_exact(part, oracle, grid):
 # same with an unbounded step-2 walk, the exact pruned mode, and the pruned
 # mode with every work item shared by several warps (forced on small grids,
 # where the default keeps one warp per item)
-MODES = ["exhaustive", "exhaustive-full", "pruned", "pruned-split"]
+# exhaustive step 1 runs the candidate-trace interpreter (trace.cu) by
+# default; "exhaustive-dfs" forces the warp-uniform DFS walk instead
+MODES = ["exhaustive", "exhaustive-full", "exhaustive-dfs", "pruned", "pruned-split"]
 
 
 def _mode(monkeypatch, m):
     if m == "exhaustive-full":
         monkeypatch.setenv("SLICECRAFT_B200_STEP2_BOUND", "0")
+    if m == "exhaustive-dfs":
+        monkeypatch.setenv("SLICECRAFT_B200_TRACE", "0")
     if m == "pruned-split":
         monkeypatch.setenv("SLICECRAFT_B200_SPLIT", "5")
         monkeypatch.setenv("SLICECRAFT_B200_SPLIT2", "3")
