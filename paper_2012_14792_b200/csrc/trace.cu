@@ -318,11 +318,23 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
 
 size_t trace_smem_bytes(int depth_cap) { return (size_t)8 * depth_cap * 32 * sizeof(uint32_t); }
 
+// deep skeletons (n up to 64) need more than the 48 KB default per block
+template <int F>
+static void trace_attrs() {
+  once_per_device((const void*)k_trace_walk<F>, [] {
+    SCB_CUDA(cudaFuncSetAttribute(k_trace_walk<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_dynamic_smem((const void*)k_trace_walk<F>)));
+  });
+}
+
 int trace_blocks_per_sm(int fpw, int depth_cap) {
   int nb = 0;
   const size_t smem = trace_smem_bytes(depth_cap);
-#define OCC(F) \
-  if (fpw == F) SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk<F>, 256, smem));
+#define OCC(F)                                                                                  \
+  if (fpw == F) {                                                                               \
+    trace_attrs<F>();                                                                           \
+    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk<F>, 256, smem));   \
+  }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
 #undef OCC
   return nb < 1 ? 1 : nb;
