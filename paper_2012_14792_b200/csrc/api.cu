@@ -18,8 +18,8 @@ namespace scb {
 void texture_moments_device(const void* d_luma, int bps, int W, int H, size_t pitch,
                             size_t fstride, int ctu, int frames, int cols, int rows,
                             sc_ctu_record* d_out, cudaStream_t st);
-void split_table_device(const uint32_t* d_rt, int cols, int rows, int groups, int fpw,
-                        uint32_t* d_rts, int sm_count, cudaStream_t st);
+void split_table_device(uint32_t* d_keys, int cols, int rows, int groups, int fpw, int sm_count,
+                        cudaStream_t st);
 void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
                        uint32_t* keys, uint64_t* vals, uint32_t* nvals, cudaStream_t st);
 void budget_keys_device(const double* d_budgets, const uint64_t* vals, const uint32_t* nvals,
@@ -72,13 +72,12 @@ size_t trace_smem_bytes(int depth_cap);
 int trace_blocks_per_sm(int fpw, int depth_cap);
 void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skel_pos,
                        const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
-                       uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* rt,
-                       const uint32_t* rts, int depth_cap, uint64_t* lanes,
-                       unsigned long long* count_out, cudaStream_t st);
+                       uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
+                       uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st);
 void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
                            const uint32_t* ops, const uint32_t* skel_pos, const uint64_t* skel_ord,
-                           uint32_t nskel, int cols, int rows, int n,
-                           const unsigned long long* count, double lambda, const uint64_t* vals,
+                           uint32_t nskel, int cols, int rows, int n, uint64_t count,
+                           double lambda, const uint64_t* vals,
                            const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
                            cudaStream_t st);
 }  // namespace scb
@@ -279,6 +278,13 @@ Layouts layouts_for(const sc_grid& g, int frames) {
   return L;
 }
 
+// Time keys of frame group gi: [groups][rt | rts][rect][fpw] in ctx->rt_search
+// (rank.cu writes rt, the split table rts).
+uint32_t* rt_of(sc_ctx* ctx, const Layouts& L, int gi) {
+  return ctx->rt_search.as<uint32_t>() + (size_t)gi * 2 * L.nr * L.fpw;
+}
+uint32_t* rts_of(sc_ctx* ctx, const Layouts& L, int gi) { return rt_of(ctx, L, gi) + L.nr * L.fpw; }
+
 // Rectangle decode table (xw -> x0,w ; yh -> y0,h), cached per grid.
 const int16_t* decode_table(sc_ctx* ctx, const sc_grid& g) {
   if (ctx->dec_cols == g.cols && ctx->dec_rows == g.rows) return ctx->dec.as<int16_t>();
@@ -321,11 +327,10 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   const int16_t* dec = decode_table(ctx, g);
   ctx->sat.ensure((size_t)L.frames * L.nsat * sizeof(double));
   ctx->rt_bits.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
-  ctx->rt_search.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint32_t));
+  ctx->rt_search.ensure((size_t)L.groups * 2 * L.fpw * L.nr * sizeof(uint32_t));
   ctx->vals.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
   ctx->nvals.ensure((size_t)L.frames * sizeof(uint32_t));
   if (raw) ctx->rect_t.ensure((size_t)L.frames * L.nr * sizeof(double));
-  ctx->rt_split.ensure((size_t)L.groups * L.fpw * L.nr * sizeof(uint32_t));
   if (!graphs_enabled()) {
     enqueue_time_tables_body(ctx, g, L, raw, dec, st);
     return;
@@ -336,7 +341,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
       (uintptr_t)L.groups, (uintptr_t)L.nr, (uintptr_t)raw, (uintptr_t)st, (uintptr_t)dec,
       (uintptr_t)ctx->est.p, (uintptr_t)ctx->sat.p, (uintptr_t)ctx->rt_bits.p,
       (uintptr_t)ctx->rt_search.p, (uintptr_t)ctx->vals.p, (uintptr_t)ctx->nvals.p,
-      (uintptr_t)ctx->rect_t.p, (uintptr_t)ctx->rt_split.p, (uintptr_t)ctx->rk_idx.p,
+      (uintptr_t)ctx->rect_t.p, (uintptr_t)ctx->rk_idx.p,
       (uintptr_t)ctx->rk_sorted.p, (uintptr_t)ctx->rk_flags.p, (uintptr_t)ctx->rk_temp.p,
       (uintptr_t)ctx->rk_temp.bytes};
   if (ctx->tt_exec && key == ctx->tt_key) {
@@ -382,8 +387,8 @@ void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, b
   rank_times_device(ctx, ctx->rt_bits.as<uint64_t>(), L.nr, L.frames, L.fpw,
                     ctx->rt_search.as<uint32_t>(), ctx->vals.as<uint64_t>(),
                     ctx->nvals.as<uint32_t>(), st);
-  split_table_device(ctx->rt_search.as<uint32_t>(), g.cols, g.rows, L.groups, L.fpw,
-                     ctx->rt_split.as<uint32_t>(), ctx->sm_count, st);
+  split_table_device(ctx->rt_search.as<uint32_t>(), g.cols, g.rows, L.groups, L.fpw, ctx->sm_count,
+                     st);
 }
 
 // K2 (u64 SATs) + K3 (SSE tables) from ctx->records.
@@ -520,6 +525,23 @@ bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& c
   return true;
 }
 
+// Candidates in the trace chunks of shard `rank` of `world` (all of them for
+// world 1), from the chunk and skeleton tables (once per shard layout).
+uint64_t trace_shard_count(Plan* p, int rank, int world) {
+  if (world == 1) return p->trace_cands;
+  if (p->trace_shard_key == (uint64_t)rank << 32 | (uint32_t)world) return p->trace_shard_cands;
+  std::vector<uint32_t> cs(p->trace_chunks + 1);
+  SCB_CUDA(cudaMemcpy(cs.data(), p->tr_chunk_skel.p, cs.size() * 4, cudaMemcpyDeviceToHost));
+  std::vector<uint64_t> so(p->trace_nskel + 1);
+  SCB_CUDA(cudaMemcpy(so.data(), p->tr_skel_ord.p, so.size() * 8, cudaMemcpyDeviceToHost));
+  uint64_t tot = 0;
+  for (uint32_t c = (uint32_t)rank; c < p->trace_chunks; c += (uint32_t)world)
+    tot += so[cs[c + 1]] - so[cs[c]];
+  p->trace_shard_key = (uint64_t)rank << 32 | (uint32_t)world;
+  p->trace_shard_cands = tot;
+  return tot;
+}
+
 // One search step over all frame groups; finalize writes FrameBest[step] and,
 // after step 1, the device budgets of step 2.  No host synchronisation.
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
@@ -543,13 +565,12 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
                         plan->tr_chunk_skel.as<uint32_t>(), plan->trace_chunks,
                         (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,
                         reinterpret_cast<uint32_t*>(ctr),
-                        ctx->rt_search.as<uint32_t>() + (size_t)gi * L.nr * L.fpw,
-                        ctx->rt_split.as<uint32_t>() + (size_t)gi * L.nr * L.fpw, depth_cap, lanes,
-                        reinterpret_cast<unsigned long long*>(ctr + 1), st);
+                        rt_of(ctx, L, gi), (uint32_t)L.nr, depth_cap, lanes, st);
       trace_finalize_launch(L.fpw, std::min(L.fpw, L.frames - gi * L.fpw), n_lanes, lanes,
                             plan->tr_ops.as<uint32_t>(), plan->tr_skel_pos.as<uint32_t>(),
                             plan->tr_skel_ord.as<uint64_t>(), plan->trace_nskel, g.cols, g.rows,
-                            cfg.n_slices, reinterpret_cast<unsigned long long*>(ctr + 1),
+                            cfg.n_slices, trace_shard_count(plan, ctx->shard_rank,
+                                                            ctx->shard_world),
                             cfg.lambda, ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr,
                             ctx->nvals.as<uint32_t>() + (size_t)gi * L.fpw, L.nr,
                             ctx->frame_best.as<FrameBest>() + (size_t)gi * L.fpw,
@@ -593,7 +614,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
       ctx->lbr.ensure(lb_per_group * L.groups * sizeof(uint32_t));
       ctx->lbm.ensure(lb_per_group * L.groups * sizeof(uint32_t));
       for (int gi = 0; gi < L.groups; ++gi)
-        column_bounds_launch(ctx->rt_search.as<uint32_t>() + (size_t)gi * L.nr * L.fpw, L.fpw,
+        column_bounds_launch(rt_of(ctx, L, gi), L.fpw,
                              std::min(L.fpw, L.frames - gi * L.fpw), g.cols, g.rows,
                              rstride - 1, rstride, ctx->lbr.as<uint32_t>() + gi * lb_per_group,
                              ctx->lbm.as<uint32_t>() + gi * lb_per_group, st);
@@ -634,8 +655,8 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
     }
     a.bmax = plan->d_bmax.as<int32_t>();
     a.pathological = plan->pathological ? 1 : 0;
-    a.rt = ctx->rt_search.as<uint32_t>() + (size_t)gi * L.nr * L.fpw;
-    a.rts = ctx->rt_split.as<uint32_t>() + (size_t)gi * L.nr * L.fpw;
+    a.rt = rt_of(ctx, L, gi);
+    a.rts = rts_of(ctx, L, gi);
     a.rs = step == 2 ? ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw : nullptr;
     a.budget = ctx->budget.as<int64_t>() + (size_t)gi * L.fpw;
     if (sched) {
@@ -1106,7 +1127,7 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
 
 sc_ctx::~sc_ctx() {
   if (tt_exec) cudaGraphExecDestroy(tt_exec);
-  for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rt_split, &rs_search, &usat,
+  for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rs_search, &usat,
                   &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc, &rt_bits, &vals, &nvals, &budget_f64, &rk_idx, &rk_sorted,
                   &rk_flags, &rk_offsets, &rk_temp, &sse_inc, &flt_idx, &flt_flag, &flt_list,
                   &flt_count, &flt_temp, &slice_maps, &owner, &vcheck, &val_in, &enum_out,

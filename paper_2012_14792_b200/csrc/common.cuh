@@ -152,6 +152,7 @@ struct Plan {
   int trace_state = 0;  // 0: not built, 1: built, -1: not used for this plan
   uint64_t trace_ops = 0, trace_cands = 0;
   uint32_t trace_nskel = 0, trace_chunks = 0;
+  uint64_t trace_shard_key = ~0ull, trace_shard_cands = 0;  // candidates of one shard
   DevBuf tr_ops, tr_skel_pos, tr_skel_ord, tr_chunk_skel;
   // candidate stream (enumerate.cu): per-item counts, their offsets, total
   DevBuf d_enum_counts, d_enum_offsets;
@@ -240,7 +241,8 @@ struct sc_ctx {
   double timings[5] = {0, 0, 0, 0, 0};
   int shard_rank = 0, shard_world = 1;
   // staging / tables
-  scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rt_split, rs_search, usat;
+  scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rs_search, usat;
+  // rt_search: the time keys [groups][rt | rts][rect][fpw] (rank.cu, split table)
   scb::DevBuf lanes, snaps, frame_best, counter, budget, scratch, dec, lbr, lbm, inc, seed_inc;
   scb::DevBuf sse_inc;
   // the time-table phase (K2 + K3 + ranks + split table, ~20 launches) as a

@@ -72,14 +72,15 @@ __global__ void k_rank_scatter(const uint64_t* __restrict__ sorted_bits,
     const uint32_t p = pos[i];
     const uint32_t rect = packed[p] & ((1u << kRectBits) - 1u);
     const size_t g = f / fpw, slot = f % fpw;
-    keys[(g * nr + rect) * fpw + slot] = key;
+    keys[(g * 2 * nr + rect) * fpw + slot] = key;  // [group][rt | rts][rect][fpw]
     if (flags[i]) vals[start + key] = sorted_bits[p];
     if (i == start + nr - 1) nvals[f] = key + 1;
   }
 }
 
-// bits_fm: [frames][nr] clamped time bits.  Outputs keys [groups][nr][fpw]
-// (slots of frames >= `frames` are left untouched), vals [frames][nr], nvals.
+// bits_fm: [frames][nr] clamped time bits.  Outputs keys into the rt half of
+// [groups][2][nr][fpw] (the rts half is the split table; slots of frames >=
+// `frames` are left untouched), vals [frames][nr], nvals.
 void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
                        uint32_t* keys, uint64_t* vals, uint32_t* nvals, cudaStream_t st) {
   const size_t total = nr * (size_t)frames;

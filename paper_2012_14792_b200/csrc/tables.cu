@@ -147,9 +147,9 @@ __global__ void k_rect_tables(const double* __restrict__ sat, const uint64_t* __
 // with y0+h < rows, max(time(y0,h), time(y0+h, rows-y0-h)), i.e. a run and
 // the forced remainder of its column, so the search scores a two-run split
 // with one load.  Same [group][rect][FPW] layout as the time table.
-__global__ void k_split_table(const uint32_t* __restrict__ rt, int cols, int rows,
-                              size_t slots /* groups * fpw */, int fpw,
-                              uint32_t* __restrict__ rts) {
+// keys: [groups][2][nr][fpw] -- reads the rt half, writes the rts half
+__global__ void k_split_table(uint32_t* __restrict__ keys, int cols, int rows,
+                              size_t slots /* groups * fpw */, int fpw) {
   const int nyh = rows * (rows + 1) / 2;
   const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
   const size_t total = nr * slots;
@@ -163,28 +163,27 @@ __global__ void k_split_table(const uint32_t* __restrict__ rt, int cols, int row
     int y0 = 0;
     while (y0 + 1 < rows && (y0 + 1) * rows - ((y0 + 1) * y0) / 2 <= yh) ++y0;
     const int h = yh - (y0 * rows - (y0 * (y0 - 1)) / 2) + 1;
-    const size_t base = g * nr * fpw;
+    const uint32_t* rt = keys + g * 2 * nr * fpw;
     uint32_t v = 0;
     if (y0 + h < rows) {
-      const uint32_t a = rt[base + (size_t)rr * fpw + slot];
+      const uint32_t a = rt[(size_t)rr * fpw + slot];
       const int y1 = y0 + h, h1 = rows - y1;
       const int rr2 = xw * nyh + (y1 * rows - (y1 * (y1 - 1)) / 2 + h1 - 1);
-      const uint32_t b = rt[base + (size_t)rr2 * fpw + slot];
+      const uint32_t b = rt[(size_t)rr2 * fpw + slot];
       v = a > b ? a : b;
     }
-    rts[base + (size_t)rr * fpw + slot] = v;
+    keys[g * 2 * nr * fpw + nr * fpw + (size_t)rr * fpw + slot] = v;
   }
 }
 
-void split_table_device(const uint32_t* d_rt, int cols, int rows, int groups, int fpw,
-                        uint32_t* d_rts, int sm_count, cudaStream_t st) {
+void split_table_device(uint32_t* d_keys, int cols, int rows, int groups, int fpw, int sm_count,
+                        cudaStream_t st) {
   const size_t total = (size_t)cols * (cols + 1) / 2 * (rows * (rows + 1) / 2) * groups * fpw;
   size_t blocks = (total + 255) / 256;
   const size_t cap = (size_t)sm_count * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_split_table<<<(unsigned)blocks, 256, 0, st>>>(d_rt, cols, rows, (size_t)groups * fpw, fpw,
-                                                  d_rts);
+  k_split_table<<<(unsigned)blocks, 256, 0, st>>>(d_keys, cols, rows, (size_t)groups * fpw, fpw);
   SCB_CUDA(cudaGetLastError());
 }
 

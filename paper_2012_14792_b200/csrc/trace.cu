@@ -86,11 +86,10 @@ struct TraceArgs {
   uint32_t chunk_offset, chunk_stride;  // shard: chunks offset, offset + stride, ...
   uint32_t n_mine;            // chunks of this shard
   uint32_t* counter;
-  const uint32_t* rt;         // [NR][FPW] time keys of this frame group
-  const uint32_t* rts;        // [NR][FPW] split table
+  const uint32_t* keys;       // [2][NR][FPW] time keys | split table of this frame group
+  uint32_t nr;
   int depth_cap;              // P stack entries per lane
   uint64_t* lanes;            // [warps * 32] x {time key (u64), ordinal}
-  unsigned long long* count_out;
 };
 
 template <int FPW>
@@ -100,11 +99,10 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int f = lane % FPW, slot = lane / FPW;
   uint32_t* P = tr_sm + (size_t)wib * a.depth_cap * 32 + lane;  // P[d] at P[d * 32]
-  const uint32_t* __restrict__ rt = a.rt + f;
-  const uint32_t* __restrict__ rts = a.rts + f;
+  const uint32_t* __restrict__ keys = a.keys + f;
+  const uint32_t* __restrict__ rts = a.keys + (size_t)a.nr * FPW + f;
   tkey best = kKeyInf;
   uint64_t best_ord = ~0ull;
-  uint64_t count = 0;
   while (true) {
     uint32_t k = 0;
     if (lane == 0) k = atomicAdd(a.counter, 1u);
@@ -114,10 +112,11 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
     const uint32_t s0 = a.chunk_skel[chunk], s1 = a.chunk_skel[chunk + 1];
     if (s0 >= s1) continue;
     const uint32_t b = a.skel_pos[s0], e = a.skel_pos[s1];
-    uint64_t ord = a.skel_ord[s0];
+    const uint64_t ord0 = a.skel_ord[s0];
+    uint32_t ord = 0;  // ordinal inside the chunk (< 2^21: <= 8192 ops x 255)
     // ties: a candidate of this chunk precedes the lane's best iff the best
     // comes from a later ordinal; inside the chunk ordinals only grow
-    tkey bcmp = (best != kKeyInf && best_ord > ord) ? best + 1 : best;
+    tkey bcmp = (best != kKeyInf && best_ord > ord0) ? best + 1 : best;
     int ld = 0;
     for (uint32_t p0 = b; p0 < e; p0 += 32) {
       const uint32_t mine = p0 + lane < e ? __ldg(a.ops + p0 + lane) : 0u;
@@ -126,11 +125,9 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
       for (int q = 0; q < nb; ++q) {
         const uint32_t op = __shfl_sync(0xffffffffu, mine, q);
         const uint32_t code = op >> 30;
-        const uint32_t idx = op & kTrIdxMask;
         if (code == kOpPush) {
-          const int d = (int)((op >> 23) & 63u);
-          const uint32_t v = ((op >> 29) & 1u) ? __ldg(rts + (size_t)idx * FPW)
-                                               : __ldg(rt + (size_t)idx * FPW);
+          const uint32_t d = (op >> 24) & 63u;
+          const uint32_t v = __ldg(keys + (op & kTrKeyMask) * FPW);
           P[(d + 1) * 32] = kmax(P[d * 32], v);
         } else if (code == kOpLeaf) {
           const int cnt = (int)((op >> 22) & 255u);
@@ -139,32 +136,40 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
             if (slot == 0 && Pl < bcmp) {
               best = Pl;
               bcmp = Pl;
-              best_ord = ord;
+              best_ord = ord0 + ord;
             }
             ord += 1;
-            count += 1;
             continue;
           }
-          const uint32_t* pv = rts + (size_t)idx * FPW;
-          tkey m = kKeyInf;
-#pragma unroll 4
-          for (int h = slot; h < cnt; h += J) m = kmin(m, __ldg(pv + (size_t)h * FPW));
+          const uint32_t* pv = rts + (op & kTrIdxMask) * FPW;
+          tkey m;
+          if (J == 1) {
+            // most leaves hold <= 4 heights: predicated loads, then a loop
+            m = umin3(__ldg(pv), cnt > 1 ? __ldg(pv + FPW) : kKeyInf,
+                      cnt > 2 ? __ldg(pv + 2 * FPW) : kKeyInf);
+            m = cnt > 3 ? kmin(m, __ldg(pv + 3 * FPW)) : m;
+#pragma unroll 1
+            for (int h = 4; h < cnt; h += 2)
+              m = umin3(m, __ldg(pv + h * FPW), h + 1 < cnt ? __ldg(pv + (h + 1) * FPW) : kKeyInf);
+          } else {
+            m = kKeyInf;
+            for (int h = slot; h < cnt; h += J) m = kmin(m, __ldg(pv + h * FPW));
+          }
           if (kmax(Pl, m) < bcmp) {  // replay in order: the first minimum wins
             const tkey t = kmax(Pl, m);
             int hit = slot;
             for (int h = slot; h < cnt; h += J)
-              if (kmax(Pl, __ldg(pv + (size_t)h * FPW)) == t) {
+              if (kmax(Pl, __ldg(pv + h * FPW)) == t) {
                 hit = h;
                 break;
               }
             best = t;
             bcmp = t;
-            best_ord = ord + (uint64_t)hit;
+            best_ord = ord0 + ord + (uint32_t)hit;
           }
-          ord += (uint64_t)cnt;
-          count += (uint64_t)cnt;
+          ord += (uint32_t)cnt;
         } else if ((op >> 29) & 1u) {  // FIX
-          P[0] = kmax(P[0], __ldg(rt + (size_t)idx * FPW));
+          P[0] = kmax(P[0], __ldg(keys + (op & kTrIdxMask) * FPW));
         } else {  // SKEL
           ld = (int)((op >> 23) & 63u);
           P[0] = 0;
@@ -175,7 +180,6 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
   const size_t gl = (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * 32 + lane;
   a.lanes[2 * gl] = best == kKeyInf ? ~0ull : (uint64_t)best;
   a.lanes[2 * gl + 1] = best_ord;
-  if (lane == 0 && count) atomicAdd(a.count_out, (unsigned long long)count);
 }
 
 __device__ __forceinline__ int64_t budget_key_t(const uint64_t* vals, uint32_t n, double b) {
@@ -196,7 +200,7 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
                                  const uint64_t* __restrict__ lanes, const uint32_t* ops,
                                  const uint32_t* __restrict__ skel_pos,
                                  const uint64_t* __restrict__ skel_ord, uint32_t nskel, int cols,
-                                 int rows, int n, const unsigned long long* count, double lambda,
+                                 int rows, int n, uint64_t count, double lambda,
                                  const uint64_t* __restrict__ vals, const uint32_t* __restrict__ nvals,
                                  size_t nr, FrameBest* __restrict__ out,
                                  int64_t* __restrict__ budget_out) {
@@ -230,8 +234,8 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
   o->sse = __longlong_as_double(0x7ff0000000000000ll);
   o->item = found ? bo : ~0ull;  // the global ordinal (shard merge orders by it)
   o->ord = 0;
-  o->count = *count;
-  o->scored = *count * (uint64_t)fpw;
+  o->count = count;
+  o->scored = count * (uint64_t)fpw;
   o->found = found ? 1 : 0;
   if (!found) return;
   uint32_t lo = 0, hi = nskel;  // last skeleton whose first ordinal <= bo
@@ -342,9 +346,8 @@ int trace_blocks_per_sm(int fpw, int depth_cap) {
 
 void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skel_pos,
                        const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
-                       uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* rt,
-                       const uint32_t* rts, int depth_cap, uint64_t* lanes,
-                       unsigned long long* count_out, cudaStream_t st) {
+                       uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
+                       uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st) {
   TraceArgs a;
   a.ops = ops;
   a.skel_pos = skel_pos;
@@ -355,11 +358,10 @@ void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t*
   a.chunk_stride = world;
   a.n_mine = n_chunks > rank ? (n_chunks - rank + world - 1) / world : 0;
   a.counter = counter;
-  a.rt = rt;
-  a.rts = rts;
+  a.keys = keys;
+  a.nr = nr;
   a.depth_cap = depth_cap;
   a.lanes = lanes;
-  a.count_out = count_out;
   const size_t smem = trace_smem_bytes(depth_cap);
   switch (fpw) {
 #define L(F) \
@@ -373,8 +375,8 @@ void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t*
 
 void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
                            const uint32_t* ops, const uint32_t* skel_pos, const uint64_t* skel_ord,
-                           uint32_t nskel, int cols, int rows, int n,
-                           const unsigned long long* count, double lambda, const uint64_t* vals,
+                           uint32_t nskel, int cols, int rows, int n, uint64_t count,
+                           double lambda, const uint64_t* vals,
                            const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
                            cudaStream_t st) {
   k_trace_finalize<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,

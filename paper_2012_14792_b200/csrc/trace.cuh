@@ -12,9 +12,10 @@
 //
 //   SKEL  ld        new skeleton (widths + runs): P[0] = 0, its leaf depth ld
 //   FIX   idx       P[0] = max(P[0], rt[idx])          a one-run column
-//   PUSH  d, T, idx P[d+1] = max(P[d], T[idx])          a run of a multi-run
-//                   column; T = the split table (run + forced rest of its
-//                   column) for the column's second-to-last run, else rt
+//   PUSH  d, kidx   P[d+1] = max(P[d], keys[kidx])     a run of a multi-run
+//                   column; keys = rt | rts (the time keys, then the split
+//                   table: run + forced rest of its column), kidx = idx for
+//                   rt and NR + idx for the column's second-to-last run
 //   LEAF  idx, cnt  candidates time max(P[ld], rts[idx + i]), i < cnt (<= 255): the
 //                   last decision run takes cnt consecutive heights (its
 //                   forced rest and any later one-run columns are in the key)
@@ -47,9 +48,11 @@ namespace scb {
 constexpr uint32_t kOpPush = 0u, kOpLeaf = 2u, kOpSkel = 3u;  // bits 31..30
 constexpr int kTrIdxBits = 22;                                 // rectangle index
 constexpr uint32_t kTrIdxMask = (1u << kTrIdxBits) - 1u;
+constexpr uint32_t kTrKeyMask = (1u << (kTrIdxBits + 1)) - 1u;  // rt | rts key index
 
-SCB_TR_HD uint32_t op_push(int d, bool split, uint32_t idx) {
-  return (kOpPush << 30) | ((split ? 1u : 0u) << 29) | ((uint32_t)d << 23) | idx;
+// PUSH: depth in bits 29..24, key index (rt | rts) in 22..0
+SCB_TR_HD uint32_t op_push(int d, uint32_t kidx) {
+  return (kOpPush << 30) | ((uint32_t)d << 24) | kidx;
 }
 SCB_TR_HD uint32_t op_leaf(uint32_t idx, int cnt) {
   return (kOpLeaf << 30) | ((uint32_t)cnt << 22) | idx;
@@ -65,7 +68,7 @@ struct TraceCount {
   uint64_t ops = 0, cands = 0, skels = 0;
   SCB_TR_HD void skel(int) { ++ops; ++skels; }
   SCB_TR_HD void fix(uint32_t) { ++ops; }
-  SCB_TR_HD void push(int, bool, uint32_t) { ++ops; }
+  SCB_TR_HD void push(int, uint32_t) { ++ops; }
   SCB_TR_HD void leaf(uint32_t, int cnt) { ++ops; cands += cnt ? (uint64_t)cnt : 1u; }
 };
 struct TraceWrite {
@@ -83,7 +86,7 @@ struct TraceWrite {
     ops[pos++] = op_skel(ld);
   }
   SCB_TR_HD void fix(uint32_t idx) { ops[pos++] = op_fix(idx); }
-  SCB_TR_HD void push(int d, bool s, uint32_t idx) { ops[pos++] = op_push(d, s, idx); }
+  SCB_TR_HD void push(int d, uint32_t kidx) { ops[pos++] = op_push(d, kidx); }
   SCB_TR_HD void leaf(uint32_t idx, int cnt) {
     ops[pos++] = op_leaf(idx, cnt);
     cand += cnt ? (uint64_t)cnt : 1u;
@@ -101,6 +104,7 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
                           Sink& out) {
   const int c = wi.c, d = wi.d;
   const int nyh = rows * (rows + 1) / 2;
+  const uint32_t nr = (uint32_t)(cols * (cols + 1) / 2 * nyh);
   int W[SC_MAX_COLS], R[SC_MAX_COLS], CL[SC_MAX_COLS + 1], SL[SC_MAX_COLS + 1];
   // decision runs (every run of a multi-run column but its last), in order
   int Dx0[SC_MAX_SLICES], Dw[SC_MAX_SLICES], Dleft[SC_MAX_SLICES];  // runs left incl. this
@@ -235,8 +239,9 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
             emitted = 0;
           }
           for (int dd = emitted; dd < nl - 1; ++dd)
-            out.push(dd, Dleft[dd] == 2,
-                     (uint32_t)(tr_xw(cols, Dx0[dd], Dw[dd]) * nyh + tr_yh(rows, Y0[dd], H[dd])));
+            out.push(dd, (Dleft[dd] == 2 ? nr : 0u) +
+                             (uint32_t)(tr_xw(cols, Dx0[dd], Dw[dd]) * nyh +
+                                        tr_yh(rows, Y0[dd], H[dd])));
           emitted = nl - 1;
           out.leaf(base + (uint32_t)(h0 - 1), h - h0);  // h - h0 <= rows - 2 <= 253
         }
@@ -255,6 +260,7 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
 SCB_TR_HD bool trace_layout(const uint32_t* ops, uint64_t nops, uint64_t which, int cols, int rows,
                             int n, uint8_t* snap) {
   const int nyh = rows * (rows + 1) / 2;
+  const uint32_t nr = (uint32_t)(cols * (cols + 1) / 2 * nyh);
   uint32_t path[SC_MAX_SLICES];
   uint32_t fixes[SC_MAX_COLS];
   int nfix = 0, ld = 0;
@@ -278,7 +284,8 @@ SCB_TR_HD bool trace_layout(const uint32_t* ops, uint64_t nops, uint64_t which, 
       continue;
     }
     if (code == kOpPush) {
-      path[(op >> 23) & 63u] = op & kTrIdxMask;
+      const uint32_t kidx = op & kTrKeyMask;
+      path[(op >> 24) & 63u] = kidx >= nr ? kidx - nr : kidx;
       continue;
     }
     const int cnt = (int)((op >> 22) & 255u);

@@ -295,8 +295,9 @@ extern "C" int emu_trace_search(int cols, int rows, int n, double k, int max_til
     for (size_t p = 0; p < ops.size(); ++p) {
       const uint32_t op = ops[p], code = op >> 30, idx = op & kTrIdxMask;
       if (code == kOpPush) {
-        const int d = (int)((op >> 23) & 63u);
-        const double v = ((op >> 29) & 1u) ? tsplit(idx) : clamp(T[idx]);
+        const int d = (int)((op >> 24) & 63u);
+        const uint32_t kidx = op & kTrKeyMask;
+        const double v = kidx >= nr ? tsplit(kidx - (uint32_t)nr) : clamp(T[kidx]);
         P[d + 1] = P[d] > v ? P[d] : v;
       } else if (code == kOpLeaf) {
         const int cnt = (int)((op >> 22) & 255u);
