@@ -529,7 +529,8 @@ bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& c
 // world 1), from the chunk and skeleton tables (once per shard layout).
 uint64_t trace_shard_count(Plan* p, int rank, int world) {
   if (world == 1) return p->trace_cands;
-  if (p->trace_shard_key == (uint64_t)rank << 32 | (uint32_t)world) return p->trace_shard_cands;
+  const uint64_t key = ((uint64_t)rank << 32) | (uint32_t)world;
+  if (p->trace_shard_key == key) return p->trace_shard_cands;
   std::vector<uint32_t> cs(p->trace_chunks + 1);
   SCB_CUDA(cudaMemcpy(cs.data(), p->tr_chunk_skel.p, cs.size() * 4, cudaMemcpyDeviceToHost));
   std::vector<uint64_t> so(p->trace_nskel + 1);
@@ -537,7 +538,7 @@ uint64_t trace_shard_count(Plan* p, int rank, int world) {
   uint64_t tot = 0;
   for (uint32_t c = (uint32_t)rank; c < p->trace_chunks; c += (uint32_t)world)
     tot += so[cs[c + 1]] - so[cs[c]];
-  p->trace_shard_key = (uint64_t)rank << 32 | (uint32_t)world;
+  p->trace_shard_key = key;
   p->trace_shard_cands = tot;
   return tot;
 }
