@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
   const uint32_t* __restrict__ rts = a.keys + (size_t)a.nr * FPW + f;
   tkey best = kKeyInf;
   uint64_t best_ord = ~0ull;
+  uint32_t best_skel = 0;
   while (true) {
     uint32_t k = 0;
     if (lane == 0) k = atomicAdd(a.counter, 1u);
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
     const uint32_t b = a.skel_pos[s0], e = a.skel_pos[s1];
     const uint64_t ord0 = a.skel_ord[s0];
     uint32_t ord = 0;  // ordinal inside the chunk (< 2^21: <= 8192 ops x 255)
+    uint32_t skel = s0 - 1;  // current skeleton (the chunk starts with a SKEL op)
     // ties: a candidate of this chunk precedes the lane's best iff the best
     // comes from a later ordinal; inside the chunk ordinals only grow
     tkey bcmp = (best != kKeyInf && best_ord > ord0) ? best + 1 : best;
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
               best = Pl;
               bcmp = Pl;
               best_ord = ord0 + ord;
+              best_skel = skel;
             }
             ord += 1;
             continue;
@@ -166,6 +169,7 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
             best = t;
             bcmp = t;
             best_ord = ord0 + ord + (uint32_t)hit;
+            best_skel = skel;
           }
           ord += (uint32_t)cnt;
         } else if ((op >> 29) & 1u) {  // FIX
@@ -173,12 +177,14 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
         } else {  // SKEL
           ld = (int)((op >> 23) & 63u);
           P[0] = 0;
+          ++skel;
         }
       }
     }
   }
   const size_t gl = (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * 32 + lane;
-  a.lanes[2 * gl] = best == kKeyInf ? ~0ull : (uint64_t)best;
+  // {time key << 32 | skeleton, ordinal}; all ones: no candidate
+  a.lanes[2 * gl] = best == kKeyInf ? ~0ull : ((uint64_t)best << 32) | best_skel;
   a.lanes[2 * gl + 1] = best_ord;
 }
 
@@ -194,23 +200,28 @@ __device__ __forceinline__ int64_t budget_key_t(const uint64_t* vals, uint32_t n
   return (int64_t)lo - 1;
 }
 
-// Per frame: min (key, ordinal) over the lanes of frame f, then the winner's
-// layout from its skeleton's ops; the step-2 budget as in k_finalize.
+// Per frame: min (key, ordinal) over the lanes of frame f; then warp 0
+// rebuilds the winner's layout from its skeleton's ops (the walk recorded the
+// skeleton): the LEAF holding the winning ordinal (warp scan of the leaf
+// counts), the last PUSH of every depth before it (lane d owns depths d and
+// d + 32) and the one-run columns (the FIX ops after the SKEL).  The step-2
+// budget as in k_finalize.
 __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
-                                 const uint64_t* __restrict__ lanes, const uint32_t* ops,
+                                 const uint64_t* __restrict__ lanes, const uint32_t* __restrict__ ops,
                                  const uint32_t* __restrict__ skel_pos,
-                                 const uint64_t* __restrict__ skel_ord, uint32_t nskel, int cols,
-                                 int rows, int n, uint64_t count, double lambda,
+                                 const uint64_t* __restrict__ skel_ord, uint32_t nr, int cols,
+                                 int rows, uint64_t count, double lambda,
                                  const uint64_t* __restrict__ vals, const uint32_t* __restrict__ nvals,
-                                 size_t nr, FrameBest* __restrict__ out,
+                                 size_t nr_vals, FrameBest* __restrict__ out,
                                  int64_t* __restrict__ budget_out) {
   const int f = blockIdx.x;
   if (f >= frames_in_group) return;
   __shared__ uint64_t skey[256], sord[256];
+  __shared__ uint32_t path[64], fixes[SC_MAX_COLS];
   uint64_t bk = ~0ull, bo = ~0ull;
   for (uint32_t li = threadIdx.x * fpw + f; li < n_lanes; li += blockDim.x * fpw) {
     const uint64_t k = lanes[2 * li], o = lanes[2 * li + 1];
-    if (k < bk || (k == bk && o < bo)) bk = k, bo = o;
+    if ((k >> 32) < (bk >> 32) || ((k >> 32) == (bk >> 32) && o < bo)) bk = k, bo = o;
   }
   skey[threadIdx.x] = bk;
   sord[threadIdx.x] = bo;
@@ -218,38 +229,92 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
       const uint64_t k = skey[threadIdx.x + s], o = sord[threadIdx.x + s];
-      if (k < skey[threadIdx.x] || (k == skey[threadIdx.x] && o < sord[threadIdx.x]))
+      if ((k >> 32) < (skey[threadIdx.x] >> 32) ||
+          ((k >> 32) == (skey[threadIdx.x] >> 32) && o < sord[threadIdx.x]))
         skey[threadIdx.x] = k, sord[threadIdx.x] = o;
     }
     __syncthreads();
   }
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   FrameBest* o = out + f;
-  const uint64_t* fv = vals + (size_t)f * nr;
+  const uint64_t* fv = vals + (size_t)f * nr_vals;
   bk = skey[0];
   bo = sord[0];
   // step 1 keeps `t < best_t` from best_t = +inf (search.cpp:277-285)
-  const bool found = bk != ~0ull && fv[bk] != 0x7ff0000000000000ull;
-  o->t = found ? fv[bk] : ~0ull;
-  o->sse = __longlong_as_double(0x7ff0000000000000ll);
-  o->item = found ? bo : ~0ull;  // the global ordinal (shard merge orders by it)
-  o->ord = 0;
-  o->count = count;
-  o->scored = count * (uint64_t)fpw;
-  o->found = found ? 1 : 0;
-  if (!found) return;
-  uint32_t lo = 0, hi = nskel;  // last skeleton whose first ordinal <= bo
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (skel_ord[mid] <= bo) lo = mid;
-    else hi = mid;
+  const bool found = bk != ~0ull && fv[bk >> 32] != 0x7ff0000000000000ull;
+  if (lane == 0) {
+    o->t = found ? fv[bk >> 32] : ~0ull;
+    o->sse = __longlong_as_double(0x7ff0000000000000ll);
+    o->item = found ? bo : ~0ull;  // the global ordinal (shard merge orders by it)
+    o->ord = 0;
+    o->count = count;
+    o->scored = count * (uint64_t)fpw;
+    o->found = found ? 1 : 0;
   }
-  if (!trace_layout(ops + skel_pos[lo], skel_pos[lo + 1] - skel_pos[lo], bo - skel_ord[lo], cols,
-                    rows, n, o->snap))
-    o->found = 0;
-  if (budget_out) {
-    const double tmin = __longlong_as_double((long long)o->t);
-    budget_out[f] = budget_key_t(fv, nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, lambda)));
+  if (!found) return;
+  const uint32_t sk = (uint32_t)bk;
+  const uint32_t b = skel_pos[sk], e = skel_pos[sk + 1];
+  const uint64_t which = bo - skel_ord[sk];
+  const int ld = (int)((ops[b] >> 23) & 63u);
+  // the LEAF holding candidate `which` of the skeleton
+  uint64_t seen = 0;
+  uint32_t leafpos = e, leafoff = 0;
+  for (uint32_t p0 = b; p0 < e; p0 += 32) {
+    const uint32_t p = p0 + lane;
+    const uint32_t op = p < e ? ops[p] : ~0u;
+    const bool isleaf = p < e && (op >> 30) == kOpLeaf;
+    const uint32_t c = isleaf ? (((op >> 22) & 255u) ? ((op >> 22) & 255u) : 1u) : 0u;
+    uint32_t incl = c;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const uint32_t excl = incl - c;
+    const bool hit = isleaf && which >= seen + excl && which < seen + incl;
+    const uint32_t m = __ballot_sync(0xffffffffu, hit);
+    if (m) {
+      const int L = __ffs(m) - 1;
+      leafpos = p0 + L;
+      leafoff = (uint32_t)(which - seen - __shfl_sync(0xffffffffu, excl, L));
+      break;
+    }
+    seen += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  // the decision path: the last PUSH of each depth before the leaf
+  uint32_t my0 = ~0u, my1 = ~0u;
+  for (uint32_t p0 = b; p0 < leafpos; p0 += 32) {
+    const uint32_t mine = p0 + lane < leafpos ? ops[p0 + lane] : ~0u;
+    const int nb = (int)min(32u, leafpos - p0);
+    for (int q = 0; q < nb; ++q) {
+      const uint32_t op = __shfl_sync(0xffffffffu, mine, q);
+      if ((op >> 30) == kOpPush) {
+        const int d = (int)((op >> 24) & 63u);
+        const uint32_t kidx = op & kTrKeyMask;
+        const uint32_t idx = kidx >= nr ? kidx - nr : kidx;
+        if (d == lane) my0 = idx;
+        if (d == lane + 32) my1 = idx;
+      }
+    }
+  }
+  path[lane] = my0;
+  path[lane + 32] = my1;
+  // one-run columns: the FIX ops right after the SKEL
+  const uint32_t fop = b + 1 + lane < e && lane < SC_MAX_COLS ? ops[b + 1 + lane] : 0u;
+  const bool isfix = (fop >> 29) == 7u;  // code 3 with the FIX bit
+  const uint32_t fm = __ballot_sync(0xffffffffu, isfix);
+  const int nfix = __ffs(~fm) - 1;       // consecutive FIXes from the start
+  if (lane < nfix) fixes[lane] = fop & kTrIdxMask;
+  __syncwarp();
+  if (lane == 0) {
+    const uint32_t lop = ops[leafpos];
+    const uint32_t cnt = (lop >> 22) & 255u;
+    trace_snapshot(fixes, nfix, path, ld, cnt ? (lop & kTrIdxMask) + leafoff : ~0u, cols, rows,
+                   o->snap);
+    if (budget_out) {
+      const double tmin = __longlong_as_double((long long)o->t);
+      budget_out[f] = budget_key_t(fv, nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, lambda)));
+    }
   }
 }
 
@@ -379,9 +444,12 @@ void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const
                            double lambda, const uint64_t* vals,
                            const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
                            cudaStream_t st) {
+  (void)nskel;
+  (void)n;
   k_trace_finalize<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
-                                                    skel_pos, skel_ord, nskel, cols, rows, n, count,
-                                                    lambda, vals, nvals, nr, out, budget_out);
+                                                    skel_pos, skel_ord, (uint32_t)nr, cols, rows,
+                                                    count, lambda, vals, nvals, nr, out,
+                                                    budget_out);
   SCB_CUDA(cudaGetLastError());
 }
 

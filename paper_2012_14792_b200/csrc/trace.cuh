@@ -252,11 +252,82 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
   }
 }
 
-// The layout of a skeleton's candidate from its ops (replay of one skeleton):
-// FIX ops give the one-run columns, the PUSH path and the LEAF the runs of
-// the multi-run columns; `which` is the candidate's position inside the
-// skeleton.  Writes the 96-byte snapshot W[16] R[16] H[64] (search.cu).
-// dec: rectangle index -> (x0, w, y0, h) decoders.
+// The layout of one candidate from its skeleton's one-run columns (fixes,
+// rectangle indices), its decision path (path[0..ld-1]: the rectangle index
+// of each PUSH) and its leaf run (leaf: rectangle index, or ~0u for a
+// skeleton without decision runs).  Writes the 96-byte snapshot W[16] R[16]
+// H[64] of search.cu (columns by x, runs column-major).
+SCB_TR_HD void trace_snapshot(const uint32_t* fixes, int nfix, const uint32_t* path, int ld,
+                              uint32_t leaf, int cols, int rows, uint8_t* snap) {
+  const int nyh = rows * (rows + 1) / 2;
+  auto decode = [&](uint32_t idx, int& x0, int& w, int& y0, int& h) {
+    const int xw = (int)(idx / (uint32_t)nyh), yh = (int)(idx % (uint32_t)nyh);
+    x0 = 0;
+    while (x0 + 1 < cols && tr_xw(cols, x0 + 1, 1) <= xw) ++x0;
+    w = xw - tr_xw(cols, x0, 1) + 1;
+    y0 = 0;
+    while (y0 + 1 < rows && tr_yh(rows, y0 + 1, 1) <= yh) ++y0;
+    h = yh - tr_yh(rows, y0, 1) + 1;
+  };
+  int cx0[SC_MAX_COLS], cw[SC_MAX_COLS], cr[SC_MAX_COLS], cs[SC_MAX_COLS], nc = 0;
+  uint8_t hh[SC_MAX_SLICES];  // heights in path order, then re-ordered by column
+  int hcol[SC_MAX_SLICES], nh = 0;
+  for (int i = 0; i < nfix; ++i) {
+    int x0, w, y0, h;
+    decode(fixes[i], x0, w, y0, h);
+    cx0[nc] = x0, cw[nc] = w, cr[nc] = 1;
+    hcol[nh] = nc, hh[nh++] = (uint8_t)rows;
+    ++nc;
+  }
+  if (leaf != ~0u) {
+    for (int dd = 0; dd <= ld; ++dd) {
+      int x0, w, y0, h;
+      decode(dd == ld ? leaf : path[dd], x0, w, y0, h);
+      int col = -1;
+      for (int i = 0; i < nc; ++i)
+        if (cx0[i] == x0) col = i;
+      if (col < 0) {
+        col = nc++;
+        cx0[col] = x0, cw[col] = w, cr[col] = 0;
+      }
+      ++cr[col];
+      hcol[nh] = col, hh[nh++] = (uint8_t)h;
+      // the column's second-to-last run (the leaf, or a PUSH whose next
+      // decision run is in another column): its forced rest follows
+      bool closes = dd == ld;
+      if (!closes) {
+        int nx0, nw, ny0, nhh;
+        decode(dd + 1 == ld ? leaf : path[dd + 1], nx0, nw, ny0, nhh);
+        closes = nx0 != x0;
+      }
+      if (closes) {
+        ++cr[col];
+        hcol[nh] = col, hh[nh++] = (uint8_t)(rows - y0 - h);
+      }
+    }
+  }
+  // columns by x; a column's runs keep their path order (top to bottom)
+  for (int i = 0; i < nc; ++i) cs[i] = i;
+  for (int i = 0; i < nc; ++i)
+    for (int j = i + 1; j < nc; ++j)
+      if (cx0[cs[j]] < cx0[cs[i]]) {
+        const int t = cs[i];
+        cs[i] = cs[j];
+        cs[j] = t;
+      }
+  int run = 0;
+  for (int i = 0; i < SC_MAX_COLS; ++i) {
+    snap[i] = (uint8_t)(i < nc ? cw[cs[i]] : 0);
+    snap[SC_MAX_COLS + i] = (uint8_t)(i < nc ? cr[cs[i]] : 0);
+    if (i < nc)
+      for (int q = 0; q < nh; ++q)
+        if (hcol[q] == cs[i]) snap[2 * SC_MAX_COLS + run++] = hh[q];
+  }
+  for (; run < SC_MAX_SLICES; ++run) snap[2 * SC_MAX_COLS + run] = 0;
+}
+
+// Sequential replay of one skeleton's ops (host emulator; the device uses a
+// warp-parallel replay in trace.cu): the candidate at position `which`.
 SCB_TR_HD bool trace_layout(const uint32_t* ops, uint64_t nops, uint64_t which, int cols, int rows,
                             int n, uint8_t* snap) {
   const int nyh = rows * (rows + 1) / 2;
@@ -265,15 +336,7 @@ SCB_TR_HD bool trace_layout(const uint32_t* ops, uint64_t nops, uint64_t which, 
   uint32_t fixes[SC_MAX_COLS];
   int nfix = 0, ld = 0;
   uint64_t seen = 0;
-  auto decode = [&](uint32_t idx, int& x0, int& w, int& y0, int& h) {
-    const int xw = (int)(idx / (uint32_t)nyh), yh = (int)(idx % (uint32_t)nyh);
-    x0 = 0;
-    while (tr_xw(cols, x0 + 1, 1) <= xw && x0 + 1 < cols) ++x0;
-    w = xw - tr_xw(cols, x0, 1) + 1;
-    y0 = 0;
-    while (tr_yh(rows, y0 + 1, 1) <= yh && y0 + 1 < rows) ++y0;
-    h = yh - tr_yh(rows, y0, 1) + 1;
-  };
+  (void)n;
   for (uint64_t p = 0; p < nops; ++p) {
     const uint32_t op = ops[p];
     const uint32_t code = op >> 30;
@@ -294,63 +357,8 @@ SCB_TR_HD bool trace_layout(const uint32_t* ops, uint64_t nops, uint64_t which, 
       seen += m;
       continue;
     }
-    // the candidate: columns from the one-run FIXes and the decision runs
-    int cx0[SC_MAX_COLS], cw[SC_MAX_COLS], cr[SC_MAX_COLS], nc = 0;
-    uint8_t ch[SC_MAX_COLS][SC_MAX_SLICES];
-    for (int i = 0; i < nfix; ++i) {
-      int x0, w, y0, h;
-      decode(fixes[i], x0, w, y0, h);
-      cx0[nc] = x0, cw[nc] = w, cr[nc] = 1, ch[nc][0] = (uint8_t)rows;
-      ++nc;
-    }
-    if (cnt) {
-      path[ld] = (op & kTrIdxMask) + (uint32_t)(which - seen);
-      for (int dd = 0; dd <= ld; ++dd) {
-        int x0, w, y0, h;
-        decode(path[dd], x0, w, y0, h);
-        int col = -1;
-        for (int i = 0; i < nc; ++i)
-          if (cx0[i] == x0) col = i;
-        if (col < 0) {
-          col = nc++;
-          cx0[col] = x0, cw[col] = w, cr[col] = 0;
-        }
-        ch[col][cr[col]++] = (uint8_t)h;
-        // the column's second-to-last run: the forced rest follows (the leaf
-        // always is one; a PUSH is one iff its next decision run starts a new
-        // column or it is the deepest PUSH before a leaf of another column)
-        bool closes = dd == ld;
-        if (!closes) {
-          int nx0, nw, ny0, nh;
-          decode(path[dd + 1], nx0, nw, ny0, nh);
-          closes = nx0 != x0;
-        }
-        if (closes) ch[col][cr[col]++] = (uint8_t)(rows - y0 - h);
-      }
-    }
-    // columns in x order
-    for (int i = 0; i < nc; ++i)
-      for (int j = i + 1; j < nc; ++j)
-        if (cx0[j] < cx0[i]) {
-          int t;
-          t = cx0[i], cx0[i] = cx0[j], cx0[j] = t;
-          t = cw[i], cw[i] = cw[j], cw[j] = t;
-          t = cr[i], cr[i] = cr[j], cr[j] = t;
-          for (int q = 0; q < SC_MAX_SLICES; ++q) {
-            const uint8_t u = ch[i][q];
-            ch[i][q] = ch[j][q];
-            ch[j][q] = u;
-          }
-        }
-    for (int i = 0; i < SC_MAX_COLS; ++i) {
-      snap[i] = (uint8_t)(i < nc ? cw[i] : 0);
-      snap[SC_MAX_COLS + i] = (uint8_t)(i < nc ? cr[i] : 0);
-    }
-    int run = 0;
-    for (int i = 0; i < nc; ++i)
-      for (int j = 0; j < cr[i]; ++j) snap[2 * SC_MAX_COLS + run++] = ch[i][j];
-    for (; run < SC_MAX_SLICES; ++run) snap[2 * SC_MAX_COLS + run] = 0;
-    (void)n;
+    trace_snapshot(fixes, nfix, path, ld, cnt ? (op & kTrIdxMask) + (uint32_t)(which - seen) : ~0u,
+                   cols, rows, snap);
     return true;
   }
   return false;
