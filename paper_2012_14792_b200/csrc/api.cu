@@ -486,7 +486,7 @@ void finish_schedule(Plan* p) {
 // Exhaustive step 1 through the candidate trace (trace.cuh): on by default
 // for families up to kTraceMaxCands candidates (the build runs the
 // enumeration once per plan); SLICECRAFT_B200_TRACE=0 keeps the DFS walk.
-constexpr double kTraceMaxCands = 2e9;
+constexpr double kTraceMaxCands = 2e9;  // < 2^31: 32-bit ordinals in the walk
 constexpr uint64_t kTraceMaxOps = 1ull << 28;  // 1 GiB of ops
 bool trace_enabled() {
   const char* v = getenv("SLICECRAFT_B200_TRACE");
@@ -551,7 +551,7 @@ void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan*
   if (step == 1 && !prune && trace_enabled() && ensure_trace(ctx, plan, g, cfg, st)) {
     const int depth_cap = std::max(cfg.n_slices, 2);
     const int blocks = ctx->sm_count * trace_blocks_per_sm(L.fpw, depth_cap);
-    const uint32_t n_lanes = (uint32_t)blocks * 256;
+    const uint32_t n_lanes = (uint32_t)blocks * 32;  // one record per block lane (trace.cu)
     const size_t lane_bytes = (size_t)n_lanes * 2 * sizeof(uint64_t);
     ctx->lanes.ensure(lane_bytes * L.groups);
     ctx->counter.ensure((size_t)L.groups * 8 * sizeof(uint64_t));

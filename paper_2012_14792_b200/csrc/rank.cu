@@ -20,6 +20,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace scb {
@@ -81,7 +83,8 @@ __global__ void k_rank_scatter(const uint64_t* __restrict__ sorted_bits,
 // bits_fm: [frames][nr] clamped time bits.  Outputs keys into the rt half of
 // [groups][2][nr][fpw] (the rts half is the split table; slots of frames >=
 // `frames` are left untouched), vals [frames][nr], nvals.
-void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
+// The original two-sort pipeline (SLICECRAFT_B200_RANK=sort64).
+void rank_times_sort64(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
                        uint32_t* keys, uint64_t* vals, uint32_t* nvals, cudaStream_t st) {
   const size_t total = nr * (size_t)frames;
   if (nr >= (1u << kRectBits) || frames >= (1 << (32 - kRectBits)))
@@ -121,6 +124,217 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   SCB_CUDA(cub::DeviceScan::InclusiveSum(ctx->rk_temp.p, b3, flags, scan, (int)total, st));
   k_rank_scatter<<<blocks, 256, 0, st>>>(sorted_bits, packed, pos, flags, scan, nr, frames, fpw,
                                          keys, vals, nvals);
+  SCB_CUDA(cudaGetLastError());
+}
+
+// ---- the 32-bit pipeline ---------------------------------------------------------
+// One 32-bit radix sort (4 passes) instead of a 64-bit one plus a frame sort:
+// key32 = frame << qb | q, where q is an order-preserving quantisation of the
+// time bits inside the frame's own range (0: +0.0, top: +inf, else
+// 1 + (bits - lo) >> s, s chosen so the frame's finite range fits).  Equal q
+// (a group) can still hold different times: groups are re-sorted by the full
+// bits -- small ones by their first thread, large ones (rare: a frame whose
+// times cluster far inside a huge range) by a counting rank in one block.
+// Then the same first-of-run flags, scan and scatter as before.  Exact: the
+// result (dense per-frame ranks, vals, nvals) equals the 64-bit sort's.
+constexpr int kSmallGroup = 16;
+
+__global__ void k_rank_range(const uint64_t* __restrict__ bits, size_t nr, uint64_t* lo,
+                             uint64_t* hi) {
+  const int f = blockIdx.y;
+  const uint64_t* b = bits + (size_t)f * nr;
+  uint64_t mn = ~0ull, mx = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nr;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t v = b[i];
+    if (v != 0 && v < 0x7ff0000000000000ull) {  // positive finite (clamped: no negatives)
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o), c = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = c > mx ? c : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mn != ~0ull) atomicMin((unsigned long long*)&lo[f], (unsigned long long)mn);
+    if (mx != 0) atomicMax((unsigned long long*)&hi[f], (unsigned long long)mx);
+  }
+}
+
+__global__ void k_rank_key32(const uint64_t* __restrict__ bits, size_t nr, int frames, int fbits,
+                             const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi,
+                             uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+  const int qb = 32 - fbits;
+  const uint32_t qmax = qb >= 32 ? 0xffffffffu : (1u << qb) - 1u;
+  const size_t total = nr * (size_t)frames;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int f = (int)(i / nr);
+    const uint64_t v = bits[i];
+    uint32_t q;
+    if (v == 0) {
+      q = 0;
+    } else if (v >= 0x7ff0000000000000ull) {
+      q = qmax;
+    } else {
+      const uint64_t l = lo[f], span = hi[f] - l;
+      const int need = span ? 64 - __clzll((long long)span) : 0;  // bits of the span
+      const int sh = need > qb - 2 ? need - (qb - 2) : 0;
+      q = 1u + (uint32_t)((v - l) >> sh);
+    }
+    key[i] = (fbits ? ((uint32_t)f << qb) : 0u) | q;
+    val[i] = (uint32_t)i;
+  }
+}
+
+__device__ __forceinline__ bool bits_less(uint64_t a, uint32_t ia, uint64_t b, uint32_t ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+// Group starts: small groups sorted in place by (bits, index); large ones
+// queued for k_rank_big.
+__global__ void k_rank_groups(const uint32_t* __restrict__ key, uint32_t* __restrict__ idx,
+                              const uint64_t* __restrict__ bits, size_t total,
+                              uint32_t* big_count, uint2* big_list) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t k = key[i];
+    if (i > 0 && key[i - 1] == k) continue;
+    size_t j = i + 1;
+    while (j < total && key[j] == k && j - i <= kSmallGroup) ++j;
+    if (j - i == 1) continue;
+    if (j - i > kSmallGroup) {
+      while (j < total && key[j] == k) ++j;
+      const uint32_t slot = atomicAdd(big_count, 1u);
+      big_list[slot] = make_uint2((uint32_t)i, (uint32_t)(j - i));
+      continue;
+    }
+    uint32_t gi[kSmallGroup];
+    uint64_t gb[kSmallGroup];
+    const int n = (int)(j - i);
+    for (int a = 0; a < n; ++a) {
+      uint32_t e = idx[i + a];
+      uint64_t be = bits[e];
+      int b = a - 1;
+      while (b >= 0 && bits_less(be, e, gb[b], gi[b])) {
+        gb[b + 1] = gb[b];
+        gi[b + 1] = gi[b];
+        --b;
+      }
+      gb[b + 1] = be;
+      gi[b + 1] = e;
+    }
+    for (int a = 0; a < n; ++a) idx[i + a] = gi[a];
+  }
+}
+
+// Large groups: the position of every element is the number of group
+// elements before it in (bits, index) order.  One block per group at a time.
+__global__ void k_rank_big(uint32_t* __restrict__ idx, const uint64_t* __restrict__ bits,
+                           const uint32_t* big_count, const uint2* __restrict__ big_list,
+                           uint32_t* __restrict__ tmp) {
+  for (uint32_t g = blockIdx.x; g < *big_count; g += gridDim.x) {
+    const uint2 gr = big_list[g];
+    for (uint32_t a = threadIdx.x; a < gr.y; a += blockDim.x) {
+      const uint32_t e = idx[gr.x + a];
+      const uint64_t be = bits[e];
+      uint32_t r = 0;
+      for (uint32_t c = 0; c < gr.y; ++c) {
+        const uint32_t o = idx[gr.x + c];
+        r += bits_less(bits[o], o, be, e) ? 1u : 0u;
+      }
+      tmp[gr.x + r] = e;
+    }
+    __syncthreads();
+    for (uint32_t a = threadIdx.x; a < gr.y; a += blockDim.x) idx[gr.x + a] = tmp[gr.x + a];
+    __syncthreads();
+  }
+}
+
+__global__ void k_rank_flags32(const uint32_t* __restrict__ idx, const uint64_t* __restrict__ bits,
+                               uint32_t* __restrict__ flags, size_t nr, size_t total) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x)
+    flags[i] = (i % nr == 0 || bits[idx[i]] != bits[idx[i - 1]]) ? 1u : 0u;
+}
+
+__global__ void k_rank_scatter32(const uint32_t* __restrict__ idx, const uint64_t* __restrict__ bits,
+                                 const uint32_t* __restrict__ flags,
+                                 const uint32_t* __restrict__ scan, size_t nr, int frames, int fpw,
+                                 uint32_t* __restrict__ keys, uint64_t* __restrict__ vals,
+                                 uint32_t* __restrict__ nvals) {
+  const size_t total = nr * (size_t)frames;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t f = i / nr;
+    const size_t start = f * nr;
+    const uint32_t key = scan[i] - scan[start];
+    const uint32_t e = idx[i];
+    const uint32_t rect = (uint32_t)(e - start);
+    const size_t g = f / fpw, slot = f % fpw;
+    keys[(g * 2 * nr + rect) * fpw + slot] = key;  // [group][rt | rts][rect][fpw]
+    if (flags[i]) vals[start + key] = bits[e];
+    if (i == start + nr - 1) nvals[f] = key + 1;
+  }
+}
+
+bool rank64_requested() {
+  const char* v = getenv("SLICECRAFT_B200_RANK");
+  return v && std::string(v) == "sort64";
+}
+
+void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
+                       uint32_t* keys, uint64_t* vals, uint32_t* nvals, cudaStream_t st) {
+  if (rank64_requested()) {
+    rank_times_sort64(ctx, bits_fm, nr, frames, fpw, keys, vals, nvals, st);
+    return;
+  }
+  const size_t total = nr * (size_t)frames;
+  if (total >= (1ull << 32) || frames > (1 << 10))
+    fail(SC_ERR_SIZE, "too many rectangles or frames for the time-key pipeline");
+  int fbits = 0;
+  while ((1 << fbits) < frames) ++fbits;
+  ctx->rk_idx.ensure(total * sizeof(uint32_t) * 6);
+  ctx->rk_flags.ensure(total * sizeof(uint32_t) * 2);
+  ctx->rk_sorted.ensure(((size_t)frames * 2 + 2) * sizeof(uint64_t) + (total / (kSmallGroup + 1) + 2) *
+                        sizeof(uint2));
+  uint32_t* key_in = ctx->rk_idx.as<uint32_t>();
+  uint32_t* key_out = key_in + total;
+  uint32_t* val_in = key_out + total;
+  uint32_t* idx = val_in + total;
+  uint32_t* tmp = idx + total;
+  uint32_t* flags = ctx->rk_flags.as<uint32_t>();
+  uint32_t* scan = flags + total;
+  uint64_t* lo = ctx->rk_sorted.as<uint64_t>();
+  uint64_t* hi = lo + frames;
+  uint32_t* big_count = reinterpret_cast<uint32_t*>(hi + frames);
+  uint2* big_list = reinterpret_cast<uint2*>(hi + frames + 2);
+  const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, (size_t)ctx->sm_count * 8);
+  SCB_CUDA(cudaMemsetAsync(lo, 0xff, (size_t)frames * sizeof(uint64_t), st));
+  SCB_CUDA(cudaMemsetAsync(hi, 0, (size_t)frames * sizeof(uint64_t) + 16, st));  // + big_count
+  const unsigned rb = (unsigned)std::max<size_t>(1, std::min<size_t>((nr + 255) / 256, 16));
+  k_rank_range<<<dim3(rb, frames), 256, 0, st>>>(bits_fm, nr, lo, hi);
+  SCB_CUDA(cudaGetLastError());
+  k_rank_key32<<<blocks, 256, 0, st>>>(bits_fm, nr, frames, fbits, lo, hi, key_in, val_in);
+  SCB_CUDA(cudaGetLastError());
+  size_t b1 = 0, b3 = 0;
+  SCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, key_in, key_out, val_in, idx, (int)total,
+                                           0, 32, st));
+  SCB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, b3, flags, scan, (int)total, st));
+  ctx->rk_temp.ensure(std::max(b1, b3));
+  SCB_CUDA(cub::DeviceRadixSort::SortPairs(ctx->rk_temp.p, b1, key_in, key_out, val_in, idx,
+                                           (int)total, 0, 32, st));
+  k_rank_groups<<<blocks, 256, 0, st>>>(key_out, idx, bits_fm, total, big_count, big_list);
+  SCB_CUDA(cudaGetLastError());
+  k_rank_big<<<ctx->sm_count, 256, 0, st>>>(idx, bits_fm, big_count, big_list, tmp);
+  SCB_CUDA(cudaGetLastError());
+  k_rank_flags32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, nr, total);
+  SCB_CUDA(cudaGetLastError());
+  SCB_CUDA(cub::DeviceScan::InclusiveSum(ctx->rk_temp.p, b3, flags, scan, (int)total, st));
+  k_rank_scatter32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, scan, nr, frames, fpw, keys, vals,
+                                           nvals);
   SCB_CUDA(cudaGetLastError());
 }
 

@@ -96,14 +96,18 @@ template <int FPW>
 __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
   constexpr int J = 32 / FPW;
   extern __shared__ uint32_t tr_sm[];
+  __shared__ uint32_t s_pos[256], s_hit[256];  // the best's LEAF op and height (rare writes)
+  __shared__ uint64_t s_red[2][256];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int f = lane % FPW, slot = lane / FPW;
   uint32_t* P = tr_sm + (size_t)wib * a.depth_cap * 32 + lane;  // P[d] at P[d * 32]
   const uint32_t* __restrict__ keys = a.keys + f;
   const uint32_t* __restrict__ rts = a.keys + (size_t)a.nr * FPW + f;
+  // lane state in registers: best key, its global ordinal (the trace holds
+  // < 2^31 candidates) and the tie threshold; the best's op position and
+  // height go to shared memory only when the best changes
   tkey best = kKeyInf;
-  uint64_t best_ord = ~0ull;
-  uint32_t best_skel = 0;
+  uint32_t best_ord = 0xffffffffu;
   while (true) {
     uint32_t k = 0;
     if (lane == 0) k = atomicAdd(a.counter, 1u);
@@ -113,12 +117,10 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
     const uint32_t s0 = a.chunk_skel[chunk], s1 = a.chunk_skel[chunk + 1];
     if (s0 >= s1) continue;
     const uint32_t b = a.skel_pos[s0], e = a.skel_pos[s1];
-    const uint64_t ord0 = a.skel_ord[s0];
-    uint32_t ord = 0;  // ordinal inside the chunk (< 2^21: <= 8192 ops x 255)
-    uint32_t skel = s0 - 1;  // current skeleton (the chunk starts with a SKEL op)
+    uint32_t ord = (uint32_t)a.skel_ord[s0];  // global ordinal of the next candidate
     // ties: a candidate of this chunk precedes the lane's best iff the best
     // comes from a later ordinal; inside the chunk ordinals only grow
-    tkey bcmp = (best != kKeyInf && best_ord > ord0) ? best + 1 : best;
+    tkey bcmp = (best != kKeyInf && best_ord > ord) ? best + 1 : best;
     int ld = 0;
     for (uint32_t p0 = b; p0 < e; p0 += 32) {
       const uint32_t mine = p0 + lane < e ? __ldg(a.ops + p0 + lane) : 0u;
@@ -138,8 +140,9 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
             if (slot == 0 && Pl < bcmp) {
               best = Pl;
               bcmp = Pl;
-              best_ord = ord0 + ord;
-              best_skel = skel;
+              best_ord = ord;
+              s_pos[threadIdx.x] = p0 + q;
+              s_hit[threadIdx.x] = 0;
             }
             ord += 1;
             continue;
@@ -168,8 +171,9 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
               }
             best = t;
             bcmp = t;
-            best_ord = ord0 + ord + (uint32_t)hit;
-            best_skel = skel;
+            best_ord = ord + (uint32_t)hit;
+            s_pos[threadIdx.x] = p0 + q;
+            s_hit[threadIdx.x] = (uint32_t)hit;
           }
           ord += (uint32_t)cnt;
         } else if ((op >> 29) & 1u) {  // FIX
@@ -177,15 +181,25 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
         } else {  // SKEL
           ld = (int)((op >> 23) & 63u);
           P[0] = 0;
-          ++skel;
         }
       }
     }
   }
-  const size_t gl = (size_t)(blockIdx.x * (blockDim.x >> 5) + wib) * 32 + lane;
-  // {time key << 32 | skeleton, ordinal}; all ones: no candidate
-  a.lanes[2 * gl] = best == kKeyInf ? ~0ull : ((uint64_t)best << 32) | best_skel;
-  a.lanes[2 * gl + 1] = best_ord;
+  // block-level reduction of the 8 warps' lanes with the same lane index
+  // (same frame and slot): {key << 32 | LEAF op, height << 32 | ordinal}
+  s_red[0][threadIdx.x] = best == kKeyInf ? ~0ull : ((uint64_t)best << 32) | s_pos[threadIdx.x];
+  s_red[1][threadIdx.x] = best == kKeyInf ? ~0ull : ((uint64_t)s_hit[threadIdx.x] << 32) | best_ord;
+  __syncthreads();
+  if (wib == 0) {
+    uint64_t k0 = s_red[0][lane], k1 = s_red[1][lane];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      const uint64_t a0 = s_red[0][w * 32 + lane], a1 = s_red[1][w * 32 + lane];
+      if ((a0 >> 32) < (k0 >> 32) || ((a0 >> 32) == (k0 >> 32) && (uint32_t)a1 < (uint32_t)k1))
+        k0 = a0, k1 = a1;
+    }
+    a.lanes[2 * ((size_t)blockIdx.x * 32 + lane)] = k0;
+    a.lanes[2 * ((size_t)blockIdx.x * 32 + lane) + 1] = k1;
+  }
 }
 
 __device__ __forceinline__ int64_t budget_key_t(const uint64_t* vals, uint32_t n, double b) {
@@ -200,17 +214,15 @@ __device__ __forceinline__ int64_t budget_key_t(const uint64_t* vals, uint32_t n
   return (int64_t)lo - 1;
 }
 
-// Per frame: min (key, ordinal) over the lanes of frame f; then warp 0
-// rebuilds the winner's layout from its skeleton's ops (the walk recorded the
-// skeleton): the LEAF holding the winning ordinal (warp scan of the leaf
-// counts), the last PUSH of every depth before it (lane d owns depths d and
-// d + 32) and the one-run columns (the FIX ops after the SKEL).  The step-2
-// budget as in k_finalize.
+// Per frame: min (key, ordinal) over the blocks' records of frame f; then
+// warp 0 rebuilds the winner's layout: its skeleton (32-ary search of the
+// skeleton starts for the LEAF op the walk recorded), the last PUSH of every
+// depth before that LEAF (lane d owns depths d and d + 32) and the one-run
+// columns (the FIX ops after the SKEL).  The step-2 budget as in k_finalize.
 __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
                                  const uint64_t* __restrict__ lanes, const uint32_t* __restrict__ ops,
-                                 const uint32_t* __restrict__ skel_pos,
-                                 const uint64_t* __restrict__ skel_ord, uint32_t nr, int cols,
-                                 int rows, uint64_t count, double lambda,
+                                 const uint32_t* __restrict__ skel_pos, uint32_t nskel, uint32_t nr,
+                                 int cols, int rows, uint64_t count, double lambda,
                                  const uint64_t* __restrict__ vals, const uint32_t* __restrict__ nvals,
                                  size_t nr_vals, FrameBest* __restrict__ out,
                                  int64_t* __restrict__ budget_out) {
@@ -221,7 +233,8 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
   uint64_t bk = ~0ull, bo = ~0ull;
   for (uint32_t li = threadIdx.x * fpw + f; li < n_lanes; li += blockDim.x * fpw) {
     const uint64_t k = lanes[2 * li], o = lanes[2 * li + 1];
-    if ((k >> 32) < (bk >> 32) || ((k >> 32) == (bk >> 32) && o < bo)) bk = k, bo = o;
+    if ((k >> 32) < (bk >> 32) || ((k >> 32) == (bk >> 32) && (uint32_t)o < (uint32_t)bo))
+      bk = k, bo = o;
   }
   skey[threadIdx.x] = bk;
   sord[threadIdx.x] = bo;
@@ -230,7 +243,7 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
     if (threadIdx.x < s) {
       const uint64_t k = skey[threadIdx.x + s], o = sord[threadIdx.x + s];
       if ((k >> 32) < (skey[threadIdx.x] >> 32) ||
-          ((k >> 32) == (skey[threadIdx.x] >> 32) && o < sord[threadIdx.x]))
+          ((k >> 32) == (skey[threadIdx.x] >> 32) && (uint32_t)o < (uint32_t)sord[threadIdx.x]))
         skey[threadIdx.x] = k, sord[threadIdx.x] = o;
     }
     __syncthreads();
@@ -246,41 +259,28 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
   if (lane == 0) {
     o->t = found ? fv[bk >> 32] : ~0ull;
     o->sse = __longlong_as_double(0x7ff0000000000000ll);
-    o->item = found ? bo : ~0ull;  // the global ordinal (shard merge orders by it)
+    o->item = found ? (uint32_t)bo : ~0ull;  // the global ordinal (shard merge orders by it)
     o->ord = 0;
     o->count = count;
     o->scored = count * (uint64_t)fpw;
     o->found = found ? 1 : 0;
   }
   if (!found) return;
-  const uint32_t sk = (uint32_t)bk;
-  const uint32_t b = skel_pos[sk], e = skel_pos[sk + 1];
-  const uint64_t which = bo - skel_ord[sk];
-  const int ld = (int)((ops[b] >> 23) & 63u);
-  // the LEAF holding candidate `which` of the skeleton
-  uint64_t seen = 0;
-  uint32_t leafpos = e, leafoff = 0;
-  for (uint32_t p0 = b; p0 < e; p0 += 32) {
-    const uint32_t p = p0 + lane;
-    const uint32_t op = p < e ? ops[p] : ~0u;
-    const bool isleaf = p < e && (op >> 30) == kOpLeaf;
-    const uint32_t c = isleaf ? (((op >> 22) & 255u) ? ((op >> 22) & 255u) : 1u) : 0u;
-    uint32_t incl = c;
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
-    const uint32_t excl = incl - c;
-    const bool hit = isleaf && which >= seen + excl && which < seen + incl;
-    const uint32_t m = __ballot_sync(0xffffffffu, hit);
-    if (m) {
-      const int L = __ffs(m) - 1;
-      leafpos = p0 + L;
-      leafoff = (uint32_t)(which - seen - __shfl_sync(0xffffffffu, excl, L));
-      break;
-    }
-    seen += __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t leafpos = (uint32_t)bk, leafoff = (uint32_t)(bo >> 32);
+  // the skeleton holding the LEAF: last start <= leafpos (32-ary search)
+  uint32_t lo = 0, hi = nskel;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t probe = lo + (uint32_t)lane * step;
+    const bool le = probe < hi && skel_pos[probe] <= leafpos;
+    const uint32_t m = __ballot_sync(0xffffffffu, le);
+    const int last = 31 - __clz(m);  // lane 0 always qualifies (skel_pos[lo] <= leafpos)
+    const uint32_t nlo = lo + (uint32_t)last * step;
+    hi = min(hi, nlo + step);
+    lo = nlo;
   }
+  const uint32_t b = skel_pos[lo];
+  const int ld = (int)((ops[b] >> 23) & 63u);
   // the decision path: the last PUSH of each depth before the leaf
   uint32_t my0 = ~0u, my1 = ~0u;
   for (uint32_t p0 = b; p0 < leafpos; p0 += 32) {
@@ -300,7 +300,7 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
   path[lane] = my0;
   path[lane + 32] = my1;
   // one-run columns: the FIX ops right after the SKEL
-  const uint32_t fop = b + 1 + lane < e && lane < SC_MAX_COLS ? ops[b + 1 + lane] : 0u;
+  const uint32_t fop = b + 1 + lane < leafpos && lane < SC_MAX_COLS ? ops[b + 1 + lane] : 0u;
   const bool isfix = (fop >> 29) == 7u;  // code 3 with the FIX bit
   const uint32_t fm = __ballot_sync(0xffffffffu, isfix);
   const int nfix = __ffs(~fm) - 1;       // consecutive FIXes from the start
@@ -444,10 +444,10 @@ void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const
                            double lambda, const uint64_t* vals,
                            const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
                            cudaStream_t st) {
-  (void)nskel;
+  (void)skel_ord;
   (void)n;
   k_trace_finalize<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
-                                                    skel_pos, skel_ord, (uint32_t)nr, cols, rows,
+                                                    skel_pos, nskel, (uint32_t)nr, cols, rows,
                                                     count, lambda, vals, nvals, nr, out,
                                                     budget_out);
   SCB_CUDA(cudaGetLastError());
