@@ -242,14 +242,14 @@ def run_ours(args):
     bps = w.bps
     pitch, fstride = w.width * bps, w.width * w.height * bps
     gc, cc = g.c(), cfg.c()
-    tim = (C.c_double * 5)()
+    tim = (C.c_double * 8)()
 
     def call(luma_ptr, est_ptr):
         check(lib().sc_partition_frames(part._h, C.byref(gc), C.byref(cc), C.c_void_p(luma_ptr),
                                         bps, pitch, fstride, C.c_void_p(est_ptr), F, None,
                                         C.cast(res, C.c_void_p)))
-        check(lib().sc_ctx_timings(part._h, tim))
-        return [tim[i] for i in range(5)]
+        check(lib().sc_ctx_timings_ex(part._h, 8, tim))
+        return [tim[i] for i in range(8)]
 
     def barrier():
         if world > 1:
@@ -285,7 +285,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    phase = np.zeros(5)
+    phase = np.zeros(8)
     e0.record(stream)
     for _ in range(args.steps):
         phase += np.array(call(luma_d.data_ptr(), est_d.data_ptr()))
@@ -380,7 +380,9 @@ def run_ours(args):
         "texture_gbs": tex_gbs,
         "phase_us": {"texture_k1": round(tex_us, 2), "tables_k2k3": round(tab_us, 2),
                      "step1": round(s1_us, 2), "step2": round(s2_us, 2),
-                     "call": round(phase[4], 2)},
+                     "call": round(phase[4], 2), "time_tables_main": round(phase[5], 2),
+                     "moment_tables_side": round(phase[6], 2),
+                     "postcheck_and_copies": round(phase[7], 2)},
         "roofline": issue,
         "roofline_texture": tex_roof,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": luma_bytes + F * g.cell_count() * 8,
@@ -396,6 +398,7 @@ def run_ours(args):
     }
     if rank == 0 and world == 1 and not args.no_extra and args.mode == 0:
         out["pruned"] = pruned_extras(part, stream, args, w, luma_d, est_d)
+        out["step2_lambda"] = lambda_extras(part, stream, w, luma_d, est_d)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_sample(w, threads=os.cpu_count() or 1)
     if rank == 0:
@@ -529,6 +532,54 @@ def run_candidates(args):
     part.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def lambda_extras(part, stream, w, luma_d, est_d):
+    """Step 2 where it matters: the headline workload at lambda
+    0.1 and 0.3 and the covering family at lambda 0.3, in the
+    exhaustive mode -- device time per phase, the step-2 leaves actually
+    scored, and the whole step."""
+    import ctypes as C
+
+    import torch
+    from paper_2012_14792_b200 import lib
+    from paper_2012_14792_b200._abi import SearchResult, check
+    F, g, bps = w.frames, w.grid(), w.bps
+    res = (SearchResult * F)()
+    tim = (C.c_double * 8)()
+    out = {}
+    for lam, cov in [(0.1, 0), (0.3, 0), (0.3, 1)]:
+        cc = w.cfg(mode=0, lambda_=lam, coverage=cov).c()
+        gc = g.c()
+
+        def call():
+            check(lib().sc_partition_frames(part._h, C.byref(gc), C.byref(cc),
+                                            C.c_void_p(luma_d.data_ptr()), bps, w.width * bps,
+                                            w.width * w.height * bps, C.c_void_p(est_d.data_ptr()),
+                                            F, None, C.cast(res, C.c_void_p)))
+            check(lib().sc_ctx_timings_ex(part._h, 8, tim))
+            return np.array([tim[i] for i in range(8)])
+        for _ in range(2):
+            call()
+        steps = 5
+        ph = np.zeros(8)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            ph += call()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ph /= steps
+        ms = e0.elapsed_time(e1) / steps
+        c1 = sum(r.candidates_step1 for r in res)
+        c2 = sum(r.candidates_step2 for r in res)
+        out[f"lambda{lam}_{'covering' if cov else 'reference'}"] = {
+            "ms_per_step": ms, "step1_us": round(ph[2], 2), "step2_us": round(ph[3], 2),
+            "candidates_per_frame_step": [c1 // F, c2 // F],
+            "step2_leaves_scored_per_frame": sum(r.leaves_scored_step2 for r in res) // F,
+            "candidates_resolved_per_s": (c1 + c2) / (ms / 1e3)}
+    return out
 
 
 def pruned_extras(part, stream, args, w3, luma3_d, est3_d):

@@ -186,6 +186,10 @@ sc_status sc_ctx_set_stream(sc_ctx* ctx, void* cuda_stream);
  * search call: [0] K1 texture, [1] K2/K3 tables, [2] step 1, [3] step 2,
  * [4] whole call (first to last event on the context's stream). */
 sc_status sc_ctx_timings(sc_ctx* ctx, double out[5]);
+/* The first n of: the five phases above, then [5] the time-table phase alone
+ * (main stream: est -> K2/K3 -> ranks -> split table), [6] the moment tables
+ * (side stream), [7] the device post-check and result copies. */
+sc_status sc_ctx_timings_ex(sc_ctx* ctx, int32_t n, double* out);
 
 /* ---- texture map (texture.cpp:145-169, ctu_stats) ------------------------ */
 /* K1: per-CTU exact moments over n_frames frames.  luma: bytes_per_sample

@@ -98,6 +98,7 @@ SIGNATURES = [
     ("sc_ctx_set_shard", C.c_int, [_P, C.c_int32, C.c_int32]),
     ("sc_ctx_set_stream", C.c_int, [_P, _P]),
     ("sc_ctx_timings", C.c_int, [_P, _P]),
+    ("sc_ctx_timings_ex", C.c_int, [_P, C.c_int32, _P]),
     ("sc_uniform_partition", C.c_int, [C.POINTER(Grid), C.c_int32, C.POINTER(PartitionC)]),
     ("sc_uniform_partition_n", C.c_int, [C.POINTER(Grid), C.c_int32, _P, C.POINTER(C.c_int32),
                                          _P, C.POINTER(C.c_int32), _P]),

@@ -895,7 +895,7 @@ void run_uniform(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int fr
   SCB_CUDA(cudaEventRecord(ev[9], s));
   SCB_CUDA(cudaEventSynchronize(ev[9]));
   const double us = 1000.0 * ev_ms(ev[0], ev[9]);
-  for (int i = 0; i < 5; ++i) ctx->timings[i] = 0.0;
+  for (int i = 0; i < 8; ++i) ctx->timings[i] = 0.0;
   ctx->timings[do1 ? 2 : 3] = us;
   ctx->timings[4] = us;
   ctx->last_best[0].clear();
@@ -1056,6 +1056,9 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   ctx->timings[2] = do1 ? 1000.0 * ev_ms(ev[1], ev[2]) : 0.0;
   ctx->timings[3] = do2 ? 1000.0 * ev_ms(ev[8], ev[3]) : 0.0;
   ctx->timings[4] = 1000.0 * ev_ms(ev[0], ev[9]);
+  ctx->timings[5] = 1000.0 * ev_ms(ev[0], ev[1]);                        // time tables (main)
+  ctx->timings[6] = need_moments ? 1000.0 * ev_ms(ev[5], ev[6]) : 0.0;   // moment tables (side)
+  ctx->timings[7] = 1000.0 * ev_ms(ev[3], ev[9]);                        // post-check + copies
   // results
   const FrameBest* hb = ctx->h_frame_best.as<FrameBest>();
   const FrameBest* b1 = hb;
@@ -1212,8 +1215,13 @@ sc_status sc_ctx_create(int32_t device, sc_ctx** out) {
     sc_ctx* c = new sc_ctx();
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
-    SCB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    SCB_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    // the side stream (K1 + moment tables, overlapping the time tables and
+    // step 1) runs at low priority: as SM slots free up the block scheduler
+    // prefers the critical-path kernels of the main stream
+    int prio_lo = 0, prio_hi = 0;
+    SCB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SCB_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
+    SCB_CUDA(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_lo));
     for (auto& e : c->ev) SCB_CUDA(cudaEventCreate(&e));
     *out = c;
   });
@@ -1256,6 +1264,13 @@ sc_status sc_ctx_timings(sc_ctx* ctx, double out[5]) {
   return guarded([&] {
     if (!ctx || !out) fail(SC_ERR_USAGE, "NULL argument");
     for (int i = 0; i < 5; ++i) out[i] = ctx->timings[i];
+  });
+}
+
+sc_status sc_ctx_timings_ex(sc_ctx* ctx, int32_t n, double* out) {
+  return guarded([&] {
+    if (!ctx || !out || n < 0) fail(SC_ERR_USAGE, "bad argument");
+    for (int i = 0; i < n; ++i) out[i] = i < 8 ? ctx->timings[i] : 0.0;
   });
 }
 

@@ -238,7 +238,7 @@ struct sc_ctx {
   cudaStream_t stream2 = nullptr;
   cudaStream_t user_stream = nullptr;
   cudaEvent_t ev[10] = {};
-  double timings[5] = {0, 0, 0, 0, 0};
+  double timings[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int shard_rank = 0, shard_world = 1;
   // staging / tables
   scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rs_search, usat;
