@@ -80,6 +80,19 @@ void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const
                            double lambda, const uint64_t* vals,
                            const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
                            cudaStream_t st);
+void trace_skips_device(const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
+                        uint32_t* skip, cudaStream_t st);
+int trace2_blocks_per_sm(int fpw, int depth_cap);
+void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skip,
+                        const uint32_t* skel_pos, const uint64_t* skel_ord,
+                        const uint32_t* chunk_skel, uint32_t n_chunks, uint32_t rank,
+                        uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
+                        const uint32_t* rest_of, const int64_t* budget, uint32_t nr, int depth_cap,
+                        uint64_t* lanes, cudaStream_t st);
+void trace_finalize2_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
+                            const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
+                            uint32_t nr, int cols, int rows, uint64_t count, const uint64_t* vals,
+                            FrameBest* out, cudaStream_t st);
 }  // namespace scb
 
 namespace scb {
@@ -304,6 +317,17 @@ const int16_t* decode_table(sc_ctx* ctx, const sc_grid& g) {
     }
   ctx->dec.ensure(dec.size() * sizeof(int16_t));
   SCB_CUDA(cudaMemcpy(ctx->dec.p, dec.data(), dec.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+  // the forced rest (x0, w, y0 + h, rows - y0 - h) of every run that leaves
+  // rows below it (step-2 trace walk)
+  std::vector<uint32_t> rest((size_t)nxw * nyh, 0);
+  for (int xw = 0; xw < nxw; ++xw)
+    for (int y0 = 0; y0 < g.rows; ++y0)
+      for (int h = 1; y0 + h < g.rows; ++h)
+        rest[(size_t)xw * nyh + yh_index(g.rows, y0, h)] =
+            (uint32_t)((size_t)xw * nyh + yh_index(g.rows, y0 + h, g.rows - y0 - h));
+  ctx->rest_of.ensure(rest.size() * sizeof(uint32_t));
+  SCB_CUDA(cudaMemcpy(ctx->rest_of.p, rest.data(), rest.size() * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice));
   ctx->dec_cols = g.cols;
   ctx->dec_rows = g.rows;
   return ctx->dec.as<int16_t>();
@@ -525,6 +549,24 @@ bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& c
   return true;
 }
 
+// Step 2 of the exhaustive mode through the trace (SLICECRAFT_B200_TRACE2=0:
+// the budget-bounded DFS walk).
+bool trace2_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_TRACE2");
+  return trace_enabled() && !(v && v[0] == '0');
+}
+
+// The plan's subtree-end table for the step-2 walk (built on first use).
+const uint32_t* ensure_skips(Plan* p, cudaStream_t st) {
+  if (!p->have_skip) {
+    p->tr_skip.ensure((size_t)p->trace_ops * sizeof(uint32_t) + 4);
+    trace_skips_device(p->tr_ops.as<uint32_t>(), p->tr_skel_pos.as<uint32_t>(), p->trace_nskel,
+                       p->tr_skip.as<uint32_t>(), st);
+    p->have_skip = true;
+  }
+  return p->tr_skip.as<uint32_t>();
+}
+
 // Candidates in the trace chunks of shard `rank` of `world` (all of them for
 // world 1), from the chunk and skeleton tables (once per shard layout).
 uint64_t trace_shard_count(Plan* p, int rank, int world) {
@@ -548,6 +590,41 @@ uint64_t trace_shard_count(Plan* p, int rank, int world) {
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
                   const Layouts& L, int step, bool compute_bounds, cudaStream_t st) {
   const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
+  if (step == 2 && cfg.mode == SC_MODE_EXHAUSTIVE && trace2_enabled() &&
+      ensure_trace(ctx, plan, g, cfg, st)) {
+    // step 2 through the trace; SLICECRAFT_B200_STEP2_BOUND=0 walks every op
+    // (no subtree skipping: the reference's full re-enumeration)
+    const uint32_t* skip = ensure_skips(plan, st);
+    const bool skipping = step2_bounded(cfg);
+    const int depth_cap = std::max(cfg.n_slices, 2);
+    const int blocks = ctx->sm_count * trace2_blocks_per_sm(L.fpw, depth_cap);
+    const uint32_t n_lanes = (uint32_t)blocks * 32;
+    const size_t lane_bytes = (size_t)n_lanes * 3 * sizeof(uint64_t);
+    ctx->lanes.ensure(lane_bytes * L.groups);
+    ctx->counter.ensure((size_t)L.groups * 8 * sizeof(uint64_t));
+    ctx->frame_best.ensure((size_t)2 * L.groups * L.fpw * sizeof(FrameBest));
+    FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)L.groups * L.fpw;
+    for (int gi = 0; gi < L.groups; ++gi) {
+      uint64_t* ctr = ctx->counter.as<uint64_t>() + 8 * gi + 4;
+      SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));
+      uint64_t* lanes = reinterpret_cast<uint64_t*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
+      trace_walk2_launch(L.fpw, blocks, plan->tr_ops.as<uint32_t>(), skipping ? skip : nullptr,
+                         plan->tr_skel_pos.as<uint32_t>(), plan->tr_skel_ord.as<uint64_t>(),
+                         plan->tr_chunk_skel.as<uint32_t>(), plan->trace_chunks,
+                         (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,
+                         reinterpret_cast<uint32_t*>(ctr), rt_of(ctx, L, gi),
+                         ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw,
+                         ctx->rest_of.as<uint32_t>(), ctx->budget.as<int64_t>() + (size_t)gi * L.fpw,
+                         (uint32_t)L.nr, depth_cap, lanes, st);
+      trace_finalize2_launch(L.fpw, std::min(L.fpw, L.frames - gi * L.fpw), n_lanes, lanes,
+                             plan->tr_ops.as<uint32_t>(), plan->tr_skel_pos.as<uint32_t>(),
+                             plan->trace_nskel, (uint32_t)L.nr, g.cols, g.rows,
+                             trace_shard_count(plan, ctx->shard_rank, ctx->shard_world),
+                             ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr,
+                             fb + (size_t)gi * L.fpw, st);
+    }
+    return;
+  }
   if (step == 1 && !prune && trace_enabled() && ensure_trace(ctx, plan, g, cfg, st)) {
     const int depth_cap = std::max(cfg.n_slices, 2);
     const int blocks = ctx->sm_count * trace_blocks_per_sm(L.fpw, depth_cap);
@@ -1135,7 +1212,7 @@ sc_ctx::~sc_ctx() {
                   &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc, &rt_bits, &vals, &nvals, &budget_f64, &rk_idx, &rk_sorted,
                   &rk_flags, &rk_offsets, &rk_temp, &sse_inc, &flt_idx, &flt_flag, &flt_list,
                   &flt_count, &flt_temp, &slice_maps, &owner, &vcheck, &val_in, &enum_out,
-                  &enum_temp})
+                  &enum_temp, &rest_of})
     b->release();
   h_vcheck.release();
   h_stage.release();
@@ -1150,7 +1227,8 @@ sc_ctx::~sc_ctx() {
     p->d_cost.release();
     p->d_enum_counts.release();
     p->d_enum_offsets.release();
-    for (auto* b : {&p->tr_ops, &p->tr_skel_pos, &p->tr_skel_ord, &p->tr_chunk_skel}) b->release();
+    for (auto* b : {&p->tr_ops, &p->tr_skel_pos, &p->tr_skel_ord, &p->tr_chunk_skel, &p->tr_skip})
+      b->release();
     delete p;
   }
   for (auto& e : ev)

@@ -154,6 +154,8 @@ struct Plan {
   uint32_t trace_nskel = 0, trace_chunks = 0;
   uint64_t trace_shard_key = ~0ull, trace_shard_cands = 0;  // candidates of one shard
   DevBuf tr_ops, tr_skel_pos, tr_skel_ord, tr_chunk_skel;
+  DevBuf tr_skip;         // step 2: subtree ends (trace.cu k_trace_skips)
+  bool have_skip = false;
   // candidate stream (enumerate.cu): per-item counts, their offsets, total
   DevBuf d_enum_counts, d_enum_offsets;
   bool have_enum = false;
@@ -255,6 +257,7 @@ struct sc_ctx {
   // device post-check of the returned partitions (validate.cu): CTU -> slice
   // id maps [2][frames][cells] of the last search, owner scratch, verdicts
   scb::DevBuf slice_maps, owner, vcheck, val_in, enum_out, enum_temp;
+  scb::DevBuf rest_of;  // [NR] forced rest of each run, per decode-table grid (step-2 trace)
   scb::HostBuf h_vcheck;
   int maps_frames[2] = {0, 0};
   size_t maps_cells = 0;

@@ -214,6 +214,60 @@ __device__ __forceinline__ int64_t budget_key_t(const uint64_t* vals, uint32_t n
   return (int64_t)lo - 1;
 }
 
+// Warp-cooperative rebuild of the layout of the candidate at height
+// `leafoff` of the LEAF op at `leafpos` (called by one full warp): its
+// skeleton (32-ary search of the skeleton starts), the last PUSH of every
+// depth before the LEAF (lane d owns depths d and d + 32) and the one-run
+// columns (the FIX ops after the SKEL); lane 0 writes the snapshot.
+__device__ void trace_rebuild(const uint32_t* __restrict__ ops, const uint32_t* __restrict__ skel_pos,
+                              uint32_t nskel, uint32_t nr, int cols, int rows, uint32_t leafpos,
+                              uint32_t leafoff, uint32_t* path, uint32_t* fixes, uint8_t* snap) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = nskel;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t probe = lo + (uint32_t)lane * step;
+    const bool le = probe < hi && skel_pos[probe] <= leafpos;
+    const uint32_t m = __ballot_sync(0xffffffffu, le);
+    const int last = 31 - __clz(m);  // lane 0 always qualifies (skel_pos[lo] <= leafpos)
+    const uint32_t nlo = lo + (uint32_t)last * step;
+    hi = min(hi, nlo + step);
+    lo = nlo;
+  }
+  const uint32_t b = skel_pos[lo];
+  const int ld = (int)((ops[b] >> 23) & 63u);
+  uint32_t my0 = ~0u, my1 = ~0u;
+  for (uint32_t p0 = b; p0 < leafpos; p0 += 32) {
+    const uint32_t mine = p0 + lane < leafpos ? ops[p0 + lane] : ~0u;
+    const int nb = (int)min(32u, leafpos - p0);
+    for (int q = 0; q < nb; ++q) {
+      const uint32_t op = __shfl_sync(0xffffffffu, mine, q);
+      if ((op >> 30) == kOpPush) {
+        const int d = (int)((op >> 24) & 63u);
+        const uint32_t kidx = op & kTrKeyMask;
+        const uint32_t idx = kidx >= nr ? kidx - nr : kidx;
+        if (d == lane) my0 = idx;
+        if (d == lane + 32) my1 = idx;
+      }
+    }
+  }
+  path[lane] = my0;
+  path[lane + 32] = my1;
+  const uint32_t fop = b + 1 + lane < leafpos && lane < SC_MAX_COLS ? ops[b + 1 + lane] : 0u;
+  const bool isfix = (fop >> 29) == 7u;  // code 3 with the FIX bit
+  const uint32_t fm = __ballot_sync(0xffffffffu, isfix);
+  const int nfix = __ffs(~fm) - 1;       // consecutive FIXes from the start
+  if (lane < nfix) fixes[lane] = fop & kTrIdxMask;
+  __syncwarp();
+  if (lane == 0) {
+    const uint32_t lop = ops[leafpos];
+    const uint32_t cnt = (lop >> 22) & 255u;
+    trace_snapshot(fixes, nfix, path, ld, cnt ? (lop & kTrIdxMask) + leafoff : ~0u, cols, rows,
+                   snap);
+  }
+  __syncwarp();
+}
+
 // Per frame: min (key, ordinal) over the blocks' records of frame f; then
 // warp 0 rebuilds the winner's layout: its skeleton (32-ary search of the
 // skeleton starts for the LEAF op the walk recorded), the last PUSH of every
@@ -267,55 +321,277 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
   }
   if (!found) return;
   const uint32_t leafpos = (uint32_t)bk, leafoff = (uint32_t)(bo >> 32);
-  // the skeleton holding the LEAF: last start <= leafpos (32-ary search)
-  uint32_t lo = 0, hi = nskel;  // answer in [lo, hi)
-  while (hi - lo > 1) {
-    const uint32_t step = (hi - lo + 31) / 32;
-    const uint32_t probe = lo + (uint32_t)lane * step;
-    const bool le = probe < hi && skel_pos[probe] <= leafpos;
-    const uint32_t m = __ballot_sync(0xffffffffu, le);
-    const int last = 31 - __clz(m);  // lane 0 always qualifies (skel_pos[lo] <= leafpos)
-    const uint32_t nlo = lo + (uint32_t)last * step;
-    hi = min(hi, nlo + step);
-    lo = nlo;
+  trace_rebuild(ops, skel_pos, nskel, nr, cols, rows, leafpos, leafoff, path, fixes, o->snap);
+  if (lane == 0 && budget_out) {
+    const double tmin = __longlong_as_double((long long)o->t);
+    budget_out[f] = budget_key_t(fv, nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, lambda)));
   }
-  const uint32_t b = skel_pos[lo];
-  const int ld = (int)((ops[b] >> 23) & 63u);
-  // the decision path: the last PUSH of each depth before the leaf
-  uint32_t my0 = ~0u, my1 = ~0u;
-  for (uint32_t p0 = b; p0 < leafpos; p0 += 32) {
-    const uint32_t mine = p0 + lane < leafpos ? ops[p0 + lane] : ~0u;
-    const int nb = (int)min(32u, leafpos - p0);
-    for (int q = 0; q < nb; ++q) {
-      const uint32_t op = __shfl_sync(0xffffffffu, mine, q);
-      if ((op >> 30) == kOpPush) {
-        const int d = (int)((op >> 24) & 63u);
-        const uint32_t kidx = op & kTrKeyMask;
-        const uint32_t idx = kidx >= nr ? kidx - nr : kidx;
-        if (d == lane) my0 = idx;
-        if (d == lane + 32) my1 = idx;
+}
+
+// ---- step 2 ---------------------------------------------------------------------
+// Subtree ends for the step-2 walk: skip[p] for a PUSH at p = the next op of
+// depth <= its own (or the skeleton's end); for a SKEL = the skeleton's end.
+// One thread per skeleton, a depth stack over its ops (once per plan).
+__global__ void k_trace_skips(const uint32_t* __restrict__ ops, const uint32_t* __restrict__ skel_pos,
+                              uint32_t nskel, uint32_t* __restrict__ skip) {
+  const uint32_t sk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sk >= nskel) return;
+  const uint32_t b = skel_pos[sk], e = skel_pos[sk + 1];
+  uint32_t open_pos[64];
+  int open_d[64], top = 0;
+  skip[b] = e;
+  for (uint32_t p = b + 1; p < e; ++p) {
+    const uint32_t op = ops[p];
+    if ((op >> 30) == kOpPush) {
+      const int d = (int)((op >> 24) & 63u);
+      while (top > 0 && open_d[top - 1] >= d) skip[open_pos[--top]] = p;
+      open_pos[top] = p;
+      open_d[top++] = d;
+    } else {
+      skip[p] = p + 1;
+    }
+  }
+  while (top > 0) skip[open_pos[--top]] = e;
+}
+
+struct Trace2Args {
+  const uint32_t* ops;
+  const uint32_t* skip;
+  const uint32_t* skel_pos;
+  const uint64_t* skel_ord;
+  const uint32_t* chunk_skel;
+  uint32_t n_chunks, chunk_offset, chunk_stride, n_mine;
+  uint32_t* counter;
+  const uint32_t* keys;      // [2][NR][FPW] time keys | split table of this frame group
+  const double* rs;          // [NR][FPW] slice SSEs of this frame group
+  const uint32_t* rest_of;   // [NR] the forced rest of a run (its column's last run)
+  const int64_t* budget;     // [FPW] largest key with time <= t_min * (1 + lambda), -1: none
+  uint32_t nr;
+  int depth_cap;
+  uint64_t* lanes;           // per block lane: {sse bits, key << 32 | op, height << 32 | ordinal}
+};
+
+// Step 2 (constrained_clustering_search, search.cpp:334-405) through the
+// trace: per lane (frame), the running maxima P and the SSE prefix S of the
+// current path (S folds the slices in slice order: leading one-run columns,
+// then each multi-run column's runs and forced rest followed by the one-run
+// columns right of it -- the FIX tags), and the (sse, t, ordinal) minimum
+// over the candidates with t <= budget.  A subtree whose fixed slices already
+// exceed every lane's budget is skipped through the skip table.
+template <int FPW>
+__global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
+  constexpr int J = 32 / FPW;
+  extern __shared__ __align__(16) uint8_t tr2_sm[];
+  __shared__ uint32_t s_pos[256], s_hit[256], s_fxi[8][SC_MAX_COLS], s_fxt[8][SC_MAX_COLS];
+  __shared__ int s_nfx[8];
+  __shared__ double s_rsse[256];
+  __shared__ uint64_t s_rk[256], s_ro[256];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int f = lane % FPW, slot = lane / FPW;
+  const size_t dstride = (size_t)a.depth_cap * 32;
+  double* S = reinterpret_cast<double*>(tr2_sm) + (size_t)wib * dstride + lane;
+  uint32_t* P = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(tr2_sm) + 8 * dstride) +
+                (size_t)wib * dstride + lane;
+  uint32_t* Cc = P + 8 * dstride;  // closed multi-run columns above each depth
+  const uint32_t* __restrict__ keys = a.keys + f;
+  const uint32_t* __restrict__ rts = a.keys + (size_t)a.nr * FPW + f;
+  const double* __restrict__ rs = a.rs + f;
+  const int64_t budget = a.budget[f];
+  double best_sse = __longlong_as_double(0x7ff0000000000000ll);
+  tkey best_t = kKeyInf;
+  uint32_t best_ord = 0xffffffffu;
+  auto offer = [&](tkey t, double sse, uint32_t o, uint32_t pos, int hit) {
+    if (sse < best_sse || (sse == best_sse && (t < best_t || (t == best_t && o < best_ord)))) {
+      best_sse = sse;
+      best_t = t;
+      best_ord = o;
+      s_pos[threadIdx.x] = pos;
+      s_hit[threadIdx.x] = (uint32_t)hit;
+    }
+  };
+  auto fold_fix = [&](double sv, uint32_t tag) {
+    const int nf = s_nfx[wib];
+    for (int j = 0; j < nf; ++j)
+      if (s_fxt[wib][j] == tag) sv = __dadd_rn(sv, __ldg(rs + (size_t)s_fxi[wib][j] * FPW));
+    return sv;
+  };
+  while (true) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(a.counter, 1u);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= a.n_mine) break;
+    const uint32_t chunk = a.chunk_offset + k * a.chunk_stride;
+    const uint32_t s0 = a.chunk_skel[chunk], s1 = a.chunk_skel[chunk + 1];
+    if (s0 >= s1) continue;
+    const uint32_t b = a.skel_pos[s0], e = a.skel_pos[s1];
+    uint32_t ord = (uint32_t)a.skel_ord[s0];
+    int ld = 0;
+    uint32_t base = 0xffffffffu, mine = 0;
+    uint32_t p = b;
+    while (p < e) {
+      if (base == 0xffffffffu || p - base >= 32) {
+        base = p;
+        mine = p + lane < e ? __ldg(a.ops + p + lane) : 0u;
       }
+      const uint32_t op = __shfl_sync(0xffffffffu, mine, p - base);
+      const uint32_t code = op >> 30;
+      uint32_t next = p + 1;
+      if (code == kOpPush) {
+        const uint32_t d = (op >> 24) & 63u;
+        const uint32_t kidx = op & kTrKeyMask;
+        const tkey Pn = kmax(P[d * 32], __ldg(keys + kidx * FPW));
+        P[(d + 1) * 32] = Pn;
+        const bool split = kidx >= a.nr;
+        const uint32_t c = Cc[d * 32] + (split ? 1u : 0u);
+        Cc[(d + 1) * 32] = c;
+        const bool live = (int64_t)Pn <= budget;
+        if (a.skip && __ballot_sync(0xffffffffu, live) == 0) {
+          next = __ldg(a.skip + p);  // no lane can meet its budget below: skip the subtree
+        } else if (live) {
+          const uint32_t idx = split ? kidx - a.nr : kidx;
+          double sv = __dadd_rn(S[d * 32], __ldg(rs + (size_t)idx * FPW));
+          if (split) {
+            sv = __dadd_rn(sv, __ldg(rs + (size_t)__ldg(a.rest_of + idx) * FPW));
+            sv = fold_fix(sv, c);
+          }
+          S[(d + 1) * 32] = sv;
+        }
+      } else if (code == kOpLeaf) {
+        const int cnt = (int)((op >> 22) & 255u);
+        const tkey Pl = P[ld * 32];
+        const bool live = (int64_t)Pl <= budget;
+        if (cnt == 0) {
+          if (slot == 0 && live) offer(Pl, S[ld * 32], ord, p, 0);
+          ord += 1;
+        } else {
+          if (__ballot_sync(0xffffffffu, live) != 0 && live) {
+            const uint32_t idx = op & kTrIdxMask;
+            const double Sl = S[ld * 32];
+            const uint32_t tag = Cc[ld * 32] + 1u;
+            for (int h = slot; h < cnt; h += J) {
+              const tkey t = kmax(Pl, __ldg(rts + (size_t)(idx + h) * FPW));
+              if ((int64_t)t > budget) continue;
+              double sv = __dadd_rn(Sl, __ldg(rs + (size_t)(idx + h) * FPW));
+              sv = __dadd_rn(sv, __ldg(rs + (size_t)__ldg(a.rest_of + idx + h) * FPW));
+              sv = fold_fix(sv, tag);
+              offer(t, sv, ord + (uint32_t)h, p, h);
+            }
+          }
+          ord += (uint32_t)cnt;
+        }
+      } else if ((op >> 29) & 1u) {  // FIX
+        const uint32_t idx = op & kTrIdxMask;
+        const uint32_t tag = (op >> 23) & 63u;
+        P[0] = kmax(P[0], __ldg(keys + idx * FPW));
+        if (tag == 0) {
+          S[0] = __dadd_rn(S[0], __ldg(rs + (size_t)idx * FPW));
+        } else {
+          const int nf = s_nfx[wib];
+          __syncwarp();
+          if (lane == 0) {
+            s_fxi[wib][nf] = idx;
+            s_fxt[wib][nf] = tag;
+            s_nfx[wib] = nf + 1;
+          }
+          __syncwarp();
+        }
+      } else {  // SKEL
+        ld = (int)((op >> 23) & 63u);
+        P[0] = 0;
+        S[0] = 0.0;
+        Cc[0] = 0;
+        __syncwarp();
+        if (lane == 0) s_nfx[wib] = 0;
+        __syncwarp();
+      }
+      p = next;
     }
   }
-  path[lane] = my0;
-  path[lane + 32] = my1;
-  // one-run columns: the FIX ops right after the SKEL
-  const uint32_t fop = b + 1 + lane < leafpos && lane < SC_MAX_COLS ? ops[b + 1 + lane] : 0u;
-  const bool isfix = (fop >> 29) == 7u;  // code 3 with the FIX bit
-  const uint32_t fm = __ballot_sync(0xffffffffu, isfix);
-  const int nfix = __ffs(~fm) - 1;       // consecutive FIXes from the start
-  if (lane < nfix) fixes[lane] = fop & kTrIdxMask;
-  __syncwarp();
+  // block-level reduction of the 8 warps' lanes with the same lane index
+  s_rsse[threadIdx.x] = best_sse;
+  s_rk[threadIdx.x] = best_t == kKeyInf ? ~0ull : ((uint64_t)best_t << 32) | s_pos[threadIdx.x];
+  s_ro[threadIdx.x] = best_t == kKeyInf ? ~0ull : ((uint64_t)s_hit[threadIdx.x] << 32) | best_ord;
+  __syncthreads();
+  if (wib == 0) {
+    double bs = s_rsse[lane];
+    uint64_t k0 = s_rk[lane], k1 = s_ro[lane];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      const double as = s_rsse[w * 32 + lane];
+      const uint64_t a0 = s_rk[w * 32 + lane], a1 = s_ro[w * 32 + lane];
+      if (a0 == ~0ull) continue;
+      if (k0 == ~0ull || as < bs ||
+          (as == bs && ((a0 >> 32) < (k0 >> 32) ||
+                        ((a0 >> 32) == (k0 >> 32) && (uint32_t)a1 < (uint32_t)k1))))
+        bs = as, k0 = a0, k1 = a1;
+    }
+    uint64_t* out = a.lanes + 3 * ((size_t)blockIdx.x * 32 + lane);
+    out[0] = (uint64_t)__double_as_longlong(bs);
+    out[1] = k0;
+    out[2] = k1;
+  }
+}
+
+// Per frame: min (sse, key, ordinal) over the blocks' records, then the
+// winner's layout (trace_rebuild).
+__global__ void k_trace_finalize2(int fpw, int frames_in_group, uint32_t n_lanes,
+                                  const uint64_t* __restrict__ lanes,
+                                  const uint32_t* __restrict__ ops,
+                                  const uint32_t* __restrict__ skel_pos, uint32_t nskel, uint32_t nr,
+                                  int cols, int rows, uint64_t count,
+                                  const uint64_t* __restrict__ vals, size_t nr_vals,
+                                  FrameBest* __restrict__ out) {
+  const int f = blockIdx.x;
+  if (f >= frames_in_group) return;
+  __shared__ double ssse[256];
+  __shared__ uint64_t skey[256], sord[256];
+  __shared__ uint32_t path[64], fixes[SC_MAX_COLS];
+  auto less = [](double as, uint64_t a0, uint64_t a1, double bs, uint64_t b0, uint64_t b1) {
+    if (a0 == ~0ull) return false;
+    if (b0 == ~0ull) return true;
+    if (as != bs) return as < bs;
+    if ((a0 >> 32) != (b0 >> 32)) return (a0 >> 32) < (b0 >> 32);
+    return (uint32_t)a1 < (uint32_t)b1;
+  };
+  double bs = 0.0;
+  uint64_t bk = ~0ull, bo = ~0ull;
+  for (uint32_t li = threadIdx.x * fpw + f; li < n_lanes; li += blockDim.x * fpw) {
+    const uint64_t* r = lanes + 3 * (size_t)li;
+    const double as = __longlong_as_double((long long)r[0]);
+    if (less(as, r[1], r[2], bs, bk, bo)) bs = as, bk = r[1], bo = r[2];
+  }
+  ssse[threadIdx.x] = bs;
+  skey[threadIdx.x] = bk;
+  sord[threadIdx.x] = bo;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s &&
+        less(ssse[threadIdx.x + s], skey[threadIdx.x + s], sord[threadIdx.x + s], ssse[threadIdx.x],
+             skey[threadIdx.x], sord[threadIdx.x])) {
+      ssse[threadIdx.x] = ssse[threadIdx.x + s];
+      skey[threadIdx.x] = skey[threadIdx.x + s];
+      sord[threadIdx.x] = sord[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  FrameBest* o = out + f;
+  bs = ssse[0];
+  bk = skey[0];
+  bo = sord[0];
+  const bool found = bk != ~0ull;
   if (lane == 0) {
-    const uint32_t lop = ops[leafpos];
-    const uint32_t cnt = (lop >> 22) & 255u;
-    trace_snapshot(fixes, nfix, path, ld, cnt ? (lop & kTrIdxMask) + leafoff : ~0u, cols, rows,
-                   o->snap);
-    if (budget_out) {
-      const double tmin = __longlong_as_double((long long)o->t);
-      budget_out[f] = budget_key_t(fv, nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, lambda)));
-    }
+    o->t = found ? vals[(size_t)f * nr_vals + (bk >> 32)] : ~0ull;
+    o->sse = bs;
+    o->item = found ? (uint32_t)bo : ~0ull;
+    o->ord = 0;
+    o->count = count;
+    o->scored = count * (uint64_t)fpw;
+    o->found = found ? 1 : 0;
   }
+  if (!found) return;
+  trace_rebuild(ops, skel_pos, nskel, nr, cols, rows, (uint32_t)bk, (uint32_t)(bo >> 32), path,
+                fixes, o->snap);
 }
 
 // ---- host side -------------------------------------------------------------------
@@ -450,6 +726,83 @@ void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const
                                                     skel_pos, nskel, (uint32_t)nr, cols, rows,
                                                     count, lambda, vals, nvals, nr, out,
                                                     budget_out);
+  SCB_CUDA(cudaGetLastError());
+}
+
+// ---- step 2 host side --------------------------------------------------------------
+void trace_skips_device(const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
+                        uint32_t* skip, cudaStream_t st) {
+  k_trace_skips<<<(nskel + 127) / 128, 128, 0, st>>>(ops, skel_pos, nskel, skip);
+  SCB_CUDA(cudaGetLastError());
+}
+
+size_t trace2_smem_bytes(int depth_cap) {
+  return (size_t)8 * depth_cap * 32 * (sizeof(double) + 2 * sizeof(uint32_t));
+}
+
+template <int F>
+static void trace2_attrs() {
+  once_per_device((const void*)k_trace_walk2<F>, [] {
+    SCB_CUDA(cudaFuncSetAttribute(k_trace_walk2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_dynamic_smem((const void*)k_trace_walk2<F>)));
+  });
+}
+
+int trace2_blocks_per_sm(int fpw, int depth_cap) {
+  int nb = 0;
+  const size_t smem = trace2_smem_bytes(depth_cap);
+#define OCC(F)                                                                                   \
+  if (fpw == F) {                                                                                \
+    trace2_attrs<F>();                                                                           \
+    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk2<F>, 256, smem));   \
+  }
+  OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
+#undef OCC
+  return nb < 1 ? 1 : nb;
+}
+
+void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skip,
+                        const uint32_t* skel_pos, const uint64_t* skel_ord,
+                        const uint32_t* chunk_skel, uint32_t n_chunks, uint32_t rank,
+                        uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
+                        const uint32_t* rest_of, const int64_t* budget, uint32_t nr, int depth_cap,
+                        uint64_t* lanes, cudaStream_t st) {
+  Trace2Args a;
+  a.ops = ops;
+  a.skip = skip;
+  a.skel_pos = skel_pos;
+  a.skel_ord = skel_ord;
+  a.chunk_skel = chunk_skel;
+  a.n_chunks = n_chunks;
+  a.chunk_offset = rank;
+  a.chunk_stride = world;
+  a.n_mine = n_chunks > rank ? (n_chunks - rank + world - 1) / world : 0;
+  a.counter = counter;
+  a.keys = keys;
+  a.rs = rs;
+  a.rest_of = rest_of;
+  a.budget = budget;
+  a.nr = nr;
+  a.depth_cap = depth_cap;
+  a.lanes = lanes;
+  const size_t smem = trace2_smem_bytes(depth_cap);
+  switch (fpw) {
+#define L(F) \
+  case F: k_trace_walk2<F><<<blocks, 256, smem, st>>>(a); break;
+    L(1) L(2) L(4) L(8) L(16) L(32)
+#undef L
+    default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
+  }
+  SCB_CUDA(cudaGetLastError());
+}
+
+void trace_finalize2_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
+                            const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
+                            uint32_t nr, int cols, int rows, uint64_t count, const uint64_t* vals,
+                            FrameBest* out, cudaStream_t st) {
+  k_trace_finalize2<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
+                                                     skel_pos, nskel, nr, cols, rows, count, vals,
+                                                     nr, out);
   SCB_CUDA(cudaGetLastError());
 }
 

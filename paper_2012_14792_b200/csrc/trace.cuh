@@ -11,7 +11,9 @@
 // interpreter that keeps one running maximum per DFS depth:
 //
 //   SKEL  ld        new skeleton (widths + runs): P[0] = 0, its leaf depth ld
-//   FIX   idx       P[0] = max(P[0], rt[idx])          a one-run column
+//   FIX   idx, tag  P[0] = max(P[0], rt[idx])          a one-run column (tag:
+//                   the multi-run columns left of it, its place in the slice
+//                   order for the step-2 SSE fold)
 //   PUSH  d, kidx   P[d+1] = max(P[d], keys[kidx])     a run of a multi-run
 //                   column; keys = rt | rts (the time keys, then the split
 //                   table: run + forced rest of its column), kidx = idx for
@@ -58,7 +60,11 @@ SCB_TR_HD uint32_t op_leaf(uint32_t idx, int cnt) {
   return (kOpLeaf << 30) | ((uint32_t)cnt << 22) | idx;
 }
 SCB_TR_HD uint32_t op_skel(int ld) { return (kOpSkel << 30) | ((uint32_t)ld << 23); }
-SCB_TR_HD uint32_t op_fix(uint32_t idx) { return (kOpSkel << 30) | (1u << 29) | idx; }
+// FIX: bits 28..23 = the number of multi-run columns left of the column (its
+// place in the slice order, for the step-2 SSE fold), 21..0 its rectangle
+SCB_TR_HD uint32_t op_fix(uint32_t idx, int tag) {
+  return (kOpSkel << 30) | (1u << 29) | ((uint32_t)tag << 23) | idx;
+}
 
 SCB_TR_HD int tr_xw(int cols, int x0, int w) { return x0 * cols - (x0 * (x0 - 1)) / 2 + (w - 1); }
 SCB_TR_HD int tr_yh(int rows, int y0, int h) { return y0 * rows - (y0 * (y0 - 1)) / 2 + (h - 1); }
@@ -67,7 +73,7 @@ SCB_TR_HD int tr_yh(int rows, int y0, int h) { return y0 * rows - (y0 * (y0 - 1)
 struct TraceCount {
   uint64_t ops = 0, cands = 0, skels = 0;
   SCB_TR_HD void skel(int) { ++ops; ++skels; }
-  SCB_TR_HD void fix(uint32_t) { ++ops; }
+  SCB_TR_HD void fix(uint32_t, int) { ++ops; }
   SCB_TR_HD void push(int, uint32_t) { ++ops; }
   SCB_TR_HD void leaf(uint32_t, int cnt) { ++ops; cands += cnt ? (uint64_t)cnt : 1u; }
 };
@@ -85,7 +91,7 @@ struct TraceWrite {
     ++nsk;
     ops[pos++] = op_skel(ld);
   }
-  SCB_TR_HD void fix(uint32_t idx) { ops[pos++] = op_fix(idx); }
+  SCB_TR_HD void fix(uint32_t idx, int tag) { ops[pos++] = op_fix(idx, tag); }
   SCB_TR_HD void push(int d, uint32_t kidx) { ops[pos++] = op_push(d, kidx); }
   SCB_TR_HD void leaf(uint32_t idx, int cnt) {
     ops[pos++] = op_leaf(idx, cnt);
@@ -110,6 +116,7 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
   int Dx0[SC_MAX_SLICES], Dw[SC_MAX_SLICES], Dleft[SC_MAX_SLICES];  // runs left incl. this
   int H[SC_MAX_SLICES], Y0[SC_MAX_SLICES], AMIN[SC_MAX_SLICES + 1], AMAX[SC_MAX_SLICES + 1];
   uint32_t FIXI[SC_MAX_COLS];
+  int FIXT[SC_MAX_COLS];  // multi-run columns left of each one-run column
   CL[0] = cols;
   for (int i = 0; i < d; ++i) {
     W[i] = wi.w[i];
@@ -158,7 +165,7 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
       }
       if (SL[c] != 0) continue;
       // ---- one skeleton: fixed one-run columns, then the decision runs
-      int amin = 0x7fffffff, amax = 0, nl = 0, nfix = 0, x0 = 0;
+      int amin = 0x7fffffff, amax = 0, nl = 0, nfix = 0, x0 = 0, nmulti = 0;
       bool ok = true;
       for (int i = 0; i < c; ++i) {
         if (R[i] == 1) {
@@ -166,6 +173,7 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
           amin = a < amin ? a : amin;
           amax = a > amax ? a : amax;
           ok = ok && (k * (double)amin > (double)amax);
+          FIXT[nfix] = nmulti;
           FIXI[nfix++] = (uint32_t)(tr_xw(cols, x0, W[i]) * nyh + tr_yh(rows, 0, rows));
         } else {
           for (int j = 0; j < R[i] - 1; ++j, ++nl) {
@@ -173,6 +181,7 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
             Dw[nl] = W[i];
             Dleft[nl] = R[i] - j;
           }
+          ++nmulti;
         }
         x0 += W[i];
       }
@@ -181,7 +190,7 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
       int emitted = 0;  // PUSH depths already written for the current path
       if (nl == 0) {    // the skeleton is one candidate
         out.skel(0);
-        for (int i = 0; i < nfix; ++i) out.fix(FIXI[i]);
+        for (int i = 0; i < nfix; ++i) out.fix(FIXI[i], FIXT[i]);
         out.leaf(0, 0);
         continue;
       }
@@ -234,7 +243,7 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
           if (h0 < 0) break;
           if (!skel_out) {
             out.skel(nl - 1);
-            for (int i = 0; i < nfix; ++i) out.fix(FIXI[i]);
+            for (int i = 0; i < nfix; ++i) out.fix(FIXI[i], FIXT[i]);
             skel_out = true;
             emitted = 0;
           }

@@ -40,6 +40,25 @@ class Emu:
         assert st == 0, st
         return t, cnt, ordn, snap, found, nops.value
 
+    def trace_step2(self, cols, rows, n, k, max_cols, coverage, rect_time, rect_sse, budget,
+                    item_target=16):
+        """Step 2 through the host build of the trace: (t, sse, ordinal,
+        snapshot, found)."""
+        rt = np.ascontiguousarray(rect_time, dtype=np.float64)
+        rs = np.ascontiguousarray(rect_sse, dtype=np.float64)
+        b = np.ascontiguousarray(budget, dtype=np.float64)
+        F = rt.shape[0]
+        t, sse = np.zeros(F), np.zeros(F)
+        ordn = np.zeros(F, dtype=np.uint64)
+        snap = np.zeros((F, 96), dtype=np.uint8)
+        found = np.zeros(F, dtype=np.int32)
+        I, D, P = C.c_int, C.c_double, C.c_void_p
+        self.L.emu_trace_step2.argtypes = [I, I, I, D, I, I, I, P, P, P, C.c_size_t, P, P, P, P, P]
+        st = self.L.emu_trace_step2(cols, rows, n, k, max_cols, coverage, F, _p(rt), _p(rs), _p(b),
+                                    item_target, _p(t), _p(sse), _p(ordn), _p(snap), _p(found))
+        assert st == 0, st
+        return t, sse, ordn, snap, found
+
     def search(self, cols, rows, n, k, max_cols, coverage, step, rect_time, rect_sse=None,
                budget=None, warps=3, item_target=16, offset=0, stride=1, full=False, prune=0,
                order=0, split=1, split_depth=1):

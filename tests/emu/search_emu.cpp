@@ -333,3 +333,140 @@ extern "C" int emu_trace_search(int cols, int rows, int n, double k, int max_til
   }
   return 0;
 }
+
+// Step 2 through the trace (scalar, one frame at a time): every candidate
+// with time <= budget gets its SSE folded in slice order -- leading one-run
+// columns at the skeleton start, each multi-run column's runs, its forced
+// rest, then the one-run columns after it (FIX tags) -- and the (sse, t,
+// order) minimum is kept.  Mirrors k_trace_walk2 (csrc/trace.cu).
+extern "C" int emu_trace_step2(int cols, int rows, int n, double k, int max_tile_cols,
+                               int coverage, int frames, const double* rect_time,
+                               const double* rect_sse, const double* budget, size_t item_target,
+                               double* out_t, double* out_sse, uint64_t* out_ord,
+                               uint8_t* out_snap, int* out_found) {
+  const int eff = max_tile_cols > 0 ? max_tile_cols : n;
+  const int maxc = std::min(std::min(n, eff), cols);
+  const std::vector<WorkItem> items = make_items(cols, maxc, coverage == 1, item_target);
+  std::vector<uint32_t> ops, skel_pos;
+  std::vector<uint64_t> skel_ord;
+  uint64_t cand = 0;
+  for (const WorkItem& wi : items) {
+    TraceCount c;
+    trace_item(wi, cols, rows, n, k, coverage, c);
+    const size_t o0 = ops.size(), s0 = skel_pos.size();
+    ops.resize(o0 + c.ops);
+    skel_pos.resize(s0 + c.skels);
+    skel_ord.resize(s0 + c.skels);
+    TraceWrite w;
+    w.ops = ops.data() + o0;
+    w.op_base = o0;
+    w.cand = cand;
+    w.skel_pos = skel_pos.data() + s0;
+    w.skel_ord = skel_ord.data() + s0;
+    trace_item(wi, cols, rows, n, k, coverage, w);
+    cand = w.cand;
+  }
+  skel_pos.push_back((uint32_t)ops.size());
+  skel_ord.push_back(cand);
+  const int nyh = rows * (rows + 1) / 2;
+  const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
+  auto rest_of = [&](uint32_t idx) {
+    const int xw = (int)(idx / (uint32_t)nyh), yh = (int)(idx % (uint32_t)nyh);
+    int y0 = 0;
+    while (y0 + 1 < rows && tr_yh(rows, y0 + 1, 1) <= yh) ++y0;
+    const int h = yh - tr_yh(rows, y0, 1) + 1;
+    return (uint32_t)(xw * nyh + tr_yh(rows, y0 + h, rows - y0 - h));
+  };
+  for (int f = 0; f < frames; ++f) {
+    const double* T = rect_time + (size_t)f * nr;
+    const double* S = rect_sse + (size_t)f * nr;
+    auto clamp = [](double t) { return t > 0.0 ? t : 0.0; };
+    auto tkey = [&](uint32_t idx, bool split) {
+      const double a = clamp(T[idx]);
+      if (!split) return a;
+      const double b = clamp(T[rest_of(idx)]);
+      return a > b ? a : b;
+    };
+    std::vector<double> P(n + 2, 0.0), SS(n + 2, 0.0);
+    std::vector<int> Cc(n + 2, 0);
+    uint32_t fxi[SC_MAX_COLS];
+    int fxt[SC_MAX_COLS], nfx = 0, ld = 0;
+    double bs = INFINITY, bt = INFINITY;
+    uint64_t bo = ~0ull, ord = 0;
+    size_t bpos = 0;
+    int bhit = 0;
+    const double B = budget[f];
+    auto fold_fix = [&](double s, int tag) {
+      for (int j = 0; j < nfx; ++j)
+        if (fxt[j] == tag) s = s + S[fxi[j]];
+      return s;
+    };
+    auto offer = [&](double t, double sse, uint64_t o, size_t pos, int hit) {
+      if (!(t <= B)) return;
+      if (sse < bs || (sse == bs && (t < bt || (t == bt && o < bo)))) {
+        bs = sse, bt = t, bo = o, bpos = pos, bhit = hit;
+      }
+    };
+    for (size_t p = 0; p < ops.size(); ++p) {
+      const uint32_t op = ops[p], code = op >> 30;
+      if (code == kOpPush) {
+        const int d = (int)((op >> 24) & 63u);
+        const uint32_t kidx = op & kTrKeyMask;
+        const bool split = kidx >= nr;
+        const uint32_t idx = split ? kidx - (uint32_t)nr : kidx;
+        const double v = tkey(idx, split);
+        P[d + 1] = P[d] > v ? P[d] : v;
+        double s = SS[d] + S[idx];
+        int c = Cc[d];
+        if (split) {
+          s = s + S[rest_of(idx)];
+          ++c;
+          s = fold_fix(s, c);
+        }
+        SS[d + 1] = s;
+        Cc[d + 1] = c;
+      } else if (code == kOpLeaf) {
+        const int cnt = (int)((op >> 22) & 255u);
+        if (cnt == 0) {
+          offer(P[ld], SS[ld], ord, p, 0);
+          ord += 1;
+          continue;
+        }
+        const uint32_t idx = op & kTrIdxMask;
+        for (int h = 0; h < cnt; ++h) {
+          const double v = tkey(idx + (uint32_t)h, true);
+          const double t = P[ld] > v ? P[ld] : v;
+          if (!(t <= B)) continue;
+          double s = SS[ld] + S[idx + (uint32_t)h];
+          s = s + S[rest_of(idx + (uint32_t)h)];
+          s = fold_fix(s, Cc[ld] + 1);
+          offer(t, s, ord + (uint64_t)h, p, h);
+        }
+        ord += (uint64_t)cnt;
+      } else if ((op >> 29) & 1u) {
+        const uint32_t idx = op & kTrIdxMask;
+        const int tag = (int)((op >> 23) & 63u);
+        const double v = clamp(T[idx]);
+        P[0] = P[0] > v ? P[0] : v;
+        if (tag == 0) SS[0] = SS[0] + S[idx];
+        else fxi[nfx] = idx, fxt[nfx] = tag, ++nfx;
+      } else {
+        ld = (int)((op >> 23) & 63u);
+        P[0] = 0.0, SS[0] = 0.0, Cc[0] = 0, nfx = 0;
+      }
+    }
+    out_found[f] = bo != ~0ull;
+    out_t[f] = bt;
+    out_sse[f] = bs;
+    out_ord[f] = bo;
+    if (bo != ~0ull) {
+      size_t s = std::upper_bound(skel_ord.begin(), skel_ord.end(), bo) - skel_ord.begin() - 1;
+      if (!trace_layout(ops.data() + skel_pos[s], skel_pos[s + 1] - skel_pos[s], bo - skel_ord[s],
+                        cols, rows, n, out_snap + (size_t)f * kSnap))
+        return 4;
+      (void)bpos;
+      (void)bhit;
+    }
+  }
+  return 0;
+}

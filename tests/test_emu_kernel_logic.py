@@ -245,3 +245,40 @@ def test_trace_cfg_grids_counts_and_size(emu, oracle):
                                                      item_target=4096)
         assert cnt[0] == want
         assert nops < 2 * want
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_trace_step2_matches_oracle(emu, oracle, seed):
+    """Step 2 through the candidate trace (host build): the SSE of every
+    feasible candidate folded in slice order from the FIX tags and the
+    decision path == the oracle's constrained clustering (t_best, sse_best
+    bit-exact, the chosen layout), both families, several lambdas."""
+    rng = np.random.default_rng(900 + seed)
+    for case in range(25):
+        cols, rows = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        n = int(rng.integers(1, min(9, cols * rows) + 1))
+        mc = int(rng.integers(0, 5))
+        k = float(rng.choice([3.0, 2.0, 1.5]))
+        cov = int(rng.integers(0, 2))
+        lam = float(rng.choice([0.0, 0.1, 0.3, 1.0, 5.0]))
+        F = 2
+        W, H = cols * 32, rows * 32
+        est = rng.lognormal(0, 0.7, (F, cols * rows))
+        est[1] = np.round(est[1])
+        rec = [oracle.ctu_stats(rng.integers(0, 1024, (H, W)).astype(np.uint16), 32)
+               for _ in range(F)]
+        rt = np.stack([oracle.rect_times(est[f], cols, rows) for f in range(F)])
+        rs = np.stack([oracle.rect_sse(W, H, 32, rec[f]) for f in range(F)])
+        exp = [oracle.search(W, H, 32, est[f], rec[f], n, lam, k, mc, cov, 3) for f in range(F)]
+        budget = np.array([e.t_min_us * (1.0 + lam) if st == 0 else -1.0 for st, e in exp])
+        t, sse, ordn, snap, found = emu.trace_step2(cols, rows, n, k, mc, cov, rt, rs, budget,
+                                                    item_target=int(rng.integers(1, 64)))
+        for f in range(F):
+            st, e = exp[f]
+            ctx = (cols, rows, n, mc, k, cov, lam, f)
+            if st != 0:
+                assert not found[f], ctx
+                continue
+            assert found[f], ctx
+            assert t[f] == e.t_best_us and sse[f] == e.sse_best, ctx
+            assert emu.slices(snap[f], n, rows) == e.best.slices(rows), ctx
