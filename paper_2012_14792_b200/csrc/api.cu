@@ -549,11 +549,18 @@ bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& c
   return true;
 }
 
-// Step 2 of the exhaustive mode through the trace (SLICECRAFT_B200_TRACE2=0:
-// the budget-bounded DFS walk).
-bool trace2_enabled() {
+// Step 2 of the exhaustive mode has two exact walks: the budget-bounded DFS
+// walk (per-lane pruning; fast when few candidates fit the budget, e.g. the
+// reference family at small lambda) and the trace interpreter (fast when
+// many do, e.g. the covering family at lambda 0.3, where the DFS walk's
+// per-lane divergence costs 10x).  The first call of a (plan, lambda) runs
+// both, timed with events, and later calls take the faster (results are
+// identical).  SLICECRAFT_B200_TRACE2=0 / =1 forces the DFS walk / the trace.
+int trace2_mode() {
   const char* v = getenv("SLICECRAFT_B200_TRACE2");
-  return trace_enabled() && !(v && v[0] == '0');
+  if (!trace_enabled() || (v && v[0] == '0')) return 1;
+  if (v && v[0] == '1') return 2;
+  return 0;
 }
 
 // The plan's subtree-end table for the step-2 walk (built on first use).
@@ -585,13 +592,42 @@ uint64_t trace_shard_count(Plan* p, int rank, int world) {
   return tot;
 }
 
+void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
+                        const Layouts& L, int step, bool compute_bounds, cudaStream_t st, int s2);
+
 // One search step over all frame groups; finalize writes FrameBest[step] and,
 // after step 1, the device budgets of step 2.  No host synchronisation.
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
                   const Layouts& L, int step, bool compute_bounds, cudaStream_t st) {
-  const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
-  if (step == 2 && cfg.mode == SC_MODE_EXHAUSTIVE && trace2_enabled() &&
+  int s2 = 1;  // step 2: 1 = DFS walk, 2 = trace, 3 = both (timed, first call)
+  if (step == 2 && cfg.mode == SC_MODE_EXHAUSTIVE && trace2_mode() != 1 &&
       ensure_trace(ctx, plan, g, cfg, st)) {
+    s2 = trace2_mode();
+    if (s2 == 0) {
+      s2 = 3;
+      for (const auto& c : plan->step2_choice)
+        if (c.first == cfg.lambda) s2 = c.second;
+    }
+  }
+  if (s2 == 3) {
+    SCB_CUDA(cudaEventRecord(ctx->ev_s2[0], st));
+    enqueue_step_walks(ctx, g, cfg, plan, L, step, compute_bounds, st, 1);
+    SCB_CUDA(cudaEventRecord(ctx->ev_s2[1], st));
+    enqueue_step_walks(ctx, g, cfg, plan, L, step, compute_bounds, st, 2);
+    SCB_CUDA(cudaEventRecord(ctx->ev_s2[2], st));
+    ctx->s2_pending = true;
+    ctx->s2_lambda = cfg.lambda;
+    ctx->s2_plan = plan;
+    return;
+  }
+  enqueue_step_walks(ctx, g, cfg, plan, L, step, compute_bounds, st, s2);
+}
+
+// The walks of one step (s2: step 2's walk, 1 = DFS, 2 = trace).
+void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
+                        const Layouts& L, int step, bool compute_bounds, cudaStream_t st, int s2) {
+  const bool prune = cfg.mode == SC_MODE_PRUNED || (step == 2 && step2_bounded(cfg));
+  if (step == 2 && s2 == 2) {
     // step 2 through the trace; SLICECRAFT_B200_STEP2_BOUND=0 walks every op
     // (no subtree skipping: the reference's full re-enumeration)
     const uint32_t* skip = ensure_skips(plan, st);
@@ -1105,6 +1141,11 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   SCB_CUDA(cudaEventRecord(ev[9], s));
   SCB_CUDA(cudaStreamSynchronize(s));
   finish_schedule(plan);
+  if (ctx->s2_pending) {  // first call of this (plan, lambda): keep the faster step-2 walk
+    const float dfs = ev_ms(ctx->ev_s2[0], ctx->ev_s2[1]), tr = ev_ms(ctx->ev_s2[1], ctx->ev_s2[2]);
+    ctx->s2_plan->step2_choice.push_back({ctx->s2_lambda, tr < dfs ? 2 : 1});
+    ctx->s2_pending = false;
+  }
   if (post) {
     const VCheck* vc = ctx->h_vcheck.as<VCheck>();
     for (int st = 1; st <= 2; ++st)
@@ -1233,6 +1274,8 @@ sc_ctx::~sc_ctx() {
   }
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ev_s2)
+    if (e) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);
   if (stream2) cudaStreamDestroy(stream2);
 }
@@ -1301,6 +1344,7 @@ sc_status sc_ctx_create(int32_t device, sc_ctx** out) {
     SCB_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi));
     SCB_CUDA(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_lo));
     for (auto& e : c->ev) SCB_CUDA(cudaEventCreate(&e));
+    for (auto& e : c->ev_s2) SCB_CUDA(cudaEventCreate(&e));
     *out = c;
   });
 }

@@ -156,6 +156,8 @@ struct Plan {
   DevBuf tr_ops, tr_skel_pos, tr_skel_ord, tr_chunk_skel;
   DevBuf tr_skip;         // step 2: subtree ends (trace.cu k_trace_skips)
   bool have_skip = false;
+  // step 2's walk per lambda, measured on the first call (api.cu enqueue_step)
+  std::vector<std::pair<double, int>> step2_choice;
   // candidate stream (enumerate.cu): per-item counts, their offsets, total
   DevBuf d_enum_counts, d_enum_offsets;
   bool have_enum = false;
@@ -240,6 +242,10 @@ struct sc_ctx {
   cudaStream_t stream2 = nullptr;
   cudaStream_t user_stream = nullptr;
   cudaEvent_t ev[10] = {};
+  cudaEvent_t ev_s2[3] = {};   // step-2 walk timing on the first call of a (plan, lambda)
+  bool s2_pending = false;
+  double s2_lambda = 0.0;
+  scb::Plan* s2_plan = nullptr;
   double timings[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int shard_rank = 0, shard_world = 1;
   // staging / tables

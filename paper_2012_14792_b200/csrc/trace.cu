@@ -732,6 +732,7 @@ void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const
 // ---- step 2 host side --------------------------------------------------------------
 void trace_skips_device(const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
                         uint32_t* skip, cudaStream_t st) {
+  if (nskel == 0) return;
   k_trace_skips<<<(nskel + 127) / 128, 128, 0, st>>>(ops, skel_pos, nskel, skip);
   SCB_CUDA(cudaGetLastError());
 }
