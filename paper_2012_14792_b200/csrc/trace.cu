@@ -389,10 +389,11 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int f = lane % FPW, slot = lane / FPW;
   const size_t dstride = (size_t)a.depth_cap * 32;
+  const int nw = blockDim.x >> 5;
   double* S = reinterpret_cast<double*>(tr2_sm) + (size_t)wib * dstride + lane;
-  uint32_t* P = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(tr2_sm) + 8 * dstride) +
+  uint32_t* P = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(tr2_sm) + nw * dstride) +
                 (size_t)wib * dstride + lane;
-  uint32_t* Cc = P + 8 * dstride;  // closed multi-run columns above each depth
+  uint32_t* Cc = P + nw * dstride;  // closed multi-run columns above each depth
   const uint32_t* __restrict__ keys = a.keys + f;
   const uint32_t* __restrict__ rts = a.keys + (size_t)a.nr * FPW + f;
   const double* __restrict__ rs = a.rs + f;
@@ -737,8 +738,17 @@ void trace_skips_device(const uint32_t* ops, const uint32_t* skel_pos, uint32_t 
   SCB_CUDA(cudaGetLastError());
 }
 
+// Per-warp stacks (S doubles, P and C words) of depth_cap entries x 32 lanes;
+// deep plans (n up to 64) run fewer warps per block to fit shared memory.
+size_t trace2_warp_bytes(int depth_cap) {
+  return (size_t)depth_cap * 32 * (sizeof(double) + 2 * sizeof(uint32_t));
+}
+int trace2_warps(int depth_cap) {
+  const int lim = max_dynamic_smem((const void*)k_trace_walk2<32>);
+  return std::max(1, std::min(8, (int)(lim / trace2_warp_bytes(depth_cap))));
+}
 size_t trace2_smem_bytes(int depth_cap) {
-  return (size_t)8 * depth_cap * 32 * (sizeof(double) + 2 * sizeof(uint32_t));
+  return (size_t)trace2_warps(depth_cap) * trace2_warp_bytes(depth_cap);
 }
 
 template <int F>
@@ -755,7 +765,8 @@ int trace2_blocks_per_sm(int fpw, int depth_cap) {
 #define OCC(F)                                                                                   \
   if (fpw == F) {                                                                                \
     trace2_attrs<F>();                                                                           \
-    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk2<F>, 256, smem));   \
+    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk2<F>,              \
+                                                           32 * trace2_warps(depth_cap), smem)); \
   }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
 #undef OCC
@@ -787,9 +798,10 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   a.depth_cap = depth_cap;
   a.lanes = lanes;
   const size_t smem = trace2_smem_bytes(depth_cap);
+  const int threads = 32 * trace2_warps(depth_cap);
   switch (fpw) {
 #define L(F) \
-  case F: k_trace_walk2<F><<<blocks, 256, smem, st>>>(a); break;
+  case F: k_trace_walk2<F><<<blocks, threads, smem, st>>>(a); break;
     L(1) L(2) L(4) L(8) L(16) L(32)
 #undef L
     default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
