@@ -229,7 +229,12 @@ def run_ours(args):
     w = wl.WORKLOADS[args.config]
     F = w.frames
     g = w.grid()
-    cfg = w.cfg(mode=args.mode)
+    over = {}
+    if args.lam is not None:
+        over["lambda_"] = args.lam
+    if args.coverage is not None:
+        over["coverage"] = args.coverage
+    cfg = w.cfg(mode=args.mode, **over)
     luma_h, est_h = make_inputs(w, rank, F)
     luma_d = luma_h.cuda()
     est_d = est_h.cuda()
@@ -780,6 +785,10 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--mode", type=int, default=0, choices=[0, 1],
                     help="0 exhaustive (every candidate scored), 1 exact branch-and-bound")
+    ap.add_argument("--lambda", dest="lam", type=float, default=None,
+                    help="profiling only: override the workload's lambda (0)")
+    ap.add_argument("--coverage", type=int, default=None, choices=[0, 1],
+                    help="profiling only: 1 = the covering family (SPEC.md:254)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the pruned-mode extras")
     ap.add_argument("--shard", default="frames", choices=["frames", "candidates"],

@@ -50,6 +50,9 @@ void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_w
                      const unsigned long long* count, const unsigned long long* scored,
                      double lambda, const uint64_t* vals, const uint32_t* nvals, size_t nr,
                      FrameBest* out, int64_t* budget_out, cudaStream_t st);
+bool small_tables_device(const double* d_est, int cols, int rows, int frames, int fpw,
+                         const int16_t* d_dec, uint32_t* keys, uint64_t* vals, uint32_t* nvals,
+                         cudaStream_t st);
 // device post-check and candidate stream (validate.cu, enumerate.cu)
 void validate_device(int n, const int* d_rects, int nbx, const int* d_bx, int nby, const int* d_by,
                      int cols, int rows, int* d_owner, int32_t* d_map, VCheck* d_out,
@@ -87,8 +90,8 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
                         const uint32_t* skel_pos, const uint64_t* skel_ord,
                         const uint32_t* chunk_skel, uint32_t n_chunks, uint32_t rank,
                         uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
-                        const uint32_t* rest_of, const int64_t* budget, uint32_t nr, int depth_cap,
-                        uint64_t* lanes, cudaStream_t st);
+                        const uint32_t* rest_of, double* rss, const int64_t* budget, uint32_t nr,
+                        int depth_cap, uint64_t* lanes, int sm_count, cudaStream_t st);
 void trace_finalize2_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
                             const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
                             uint32_t nr, int cols, int rows, uint64_t count, const uint64_t* vals,
@@ -402,6 +405,14 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
 
 void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
                               const int16_t* dec, cudaStream_t st) {
+  // small grids: the whole phase in one CTA per frame (small_tables.cu);
+  // SLICECRAFT_B200_SMALL_TABLES=0 keeps the general pipeline
+  const char* sv = getenv("SLICECRAFT_B200_SMALL_TABLES");
+  if (!raw && !(sv && sv[0] == '0') &&
+      small_tables_device(ctx->est.as<double>(), g.cols, g.rows, L.frames, L.fpw, dec,
+                          ctx->rt_search.as<uint32_t>(), ctx->vals.as<uint64_t>(),
+                          ctx->nvals.as<uint32_t>(), st))
+    return;
   grid_sat_device(ctx->est.as<double>(), nullptr, g.cols, g.rows, L.frames, ctx->sat.as<double>(),
                   nullptr, st);
   rect_tables_device(ctx->sat.as<double>(), nullptr, dec, g.cols, g.rows, L.frames, L.fpw,
@@ -633,13 +644,17 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
     const uint32_t* skip = ensure_skips(plan, st);
     const bool skipping = step2_bounded(cfg);
     const int depth_cap = std::max(cfg.n_slices, 2);
-    const int blocks = ctx->sm_count * trace2_blocks_per_sm(L.fpw, depth_cap);
+    // no more blocks than the shard has chunks for (small spaces: a few)
+    const int blocks = std::max(
+        1, (int)std::min<uint64_t>((uint64_t)ctx->sm_count * trace2_blocks_per_sm(L.fpw, depth_cap),
+                                   (plan->trace_chunks / ctx->shard_world + 8) / 2));
     const uint32_t n_lanes = (uint32_t)blocks * 32;  // one record per block lane
     const size_t lane_bytes = (size_t)n_lanes * 3 * sizeof(uint64_t);
     ctx->lanes.ensure(lane_bytes * L.groups);
     ctx->counter.ensure((size_t)L.groups * 8 * sizeof(uint64_t));
     ctx->frame_best.ensure((size_t)2 * L.groups * L.fpw * sizeof(FrameBest));
     FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)L.groups * L.fpw;
+    ctx->rss.ensure(L.nr * L.fpw * sizeof(double));
     for (int gi = 0; gi < L.groups; ++gi) {
       uint64_t* ctr = ctx->counter.as<uint64_t>() + 8 * gi + 4;
       SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));
@@ -650,8 +665,9 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
                          (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,
                          reinterpret_cast<uint32_t*>(ctr), rt_of(ctx, L, gi),
                          ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw,
-                         ctx->rest_of.as<uint32_t>(), ctx->budget.as<int64_t>() + (size_t)gi * L.fpw,
-                         (uint32_t)L.nr, depth_cap, lanes, st);
+                         ctx->rest_of.as<uint32_t>(), ctx->rss.as<double>(),
+                         ctx->budget.as<int64_t>() + (size_t)gi * L.fpw, (uint32_t)L.nr, depth_cap,
+                         lanes, ctx->sm_count, st);
       trace_finalize2_launch(L.fpw, std::min(L.fpw, L.frames - gi * L.fpw), n_lanes, lanes,
                              plan->tr_ops.as<uint32_t>(), plan->tr_skel_pos.as<uint32_t>(),
                              plan->trace_nskel, (uint32_t)L.nr, g.cols, g.rows,
@@ -663,7 +679,9 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
   }
   if (step == 1 && !prune && trace_enabled() && ensure_trace(ctx, plan, g, cfg, st)) {
     const int depth_cap = std::max(cfg.n_slices, 2);
-    const int blocks = ctx->sm_count * trace_blocks_per_sm(L.fpw, depth_cap);
+    const int blocks = std::max(
+        1, (int)std::min<uint64_t>((uint64_t)ctx->sm_count * trace_blocks_per_sm(L.fpw, depth_cap),
+                                   (plan->trace_chunks / ctx->shard_world + 8) / 2));
     const uint32_t n_lanes = (uint32_t)blocks * 32;  // one record per block lane (trace.cu)
     const size_t lane_bytes = (size_t)n_lanes * 2 * sizeof(uint64_t);
     ctx->lanes.ensure(lane_bytes * L.groups);
@@ -1260,7 +1278,7 @@ sc_ctx::~sc_ctx() {
                   &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc, &rt_bits, &vals, &nvals, &budget_f64, &rk_idx, &rk_sorted,
                   &rk_flags, &rk_offsets, &rk_temp, &sse_inc, &flt_idx, &flt_flag, &flt_list,
                   &flt_count, &flt_temp, &slice_maps, &owner, &vcheck, &val_in, &enum_out,
-                  &enum_temp, &rest_of})
+                  &enum_temp, &rest_of, &rss})
     b->release();
   h_vcheck.release();
   h_stage.release();

@@ -364,7 +364,7 @@ struct Trace2Args {
   uint32_t* counter;
   const uint32_t* keys;      // [2][NR][FPW] time keys | split table of this frame group
   const double* rs;          // [NR][FPW] slice SSEs of this frame group
-  const uint32_t* rest_of;   // [NR] the forced rest of a run (its column's last run)
+  const double* rss;         // [NR][FPW] SSE of each run's forced rest (gathered per call)
   const int64_t* budget;     // [FPW] largest key with time <= t_min * (1 + lambda), -1: none
   uint32_t nr;
   int depth_cap;
@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
   const uint32_t* __restrict__ keys = a.keys + f;
   const uint32_t* __restrict__ rts = a.keys + (size_t)a.nr * FPW + f;
   const double* __restrict__ rs = a.rs + f;
+  const double* __restrict__ rss = a.rss + f;
   const int64_t budget = a.budget[f];
   double best_sse = __longlong_as_double(0x7ff0000000000000ll);
   tkey best_t = kKeyInf;
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
           const uint32_t idx = split ? kidx - a.nr : kidx;
           double sv = __dadd_rn(S[d * 32], __ldg(rs + (size_t)idx * FPW));
           if (split) {
-            sv = __dadd_rn(sv, __ldg(rs + (size_t)__ldg(a.rest_of + idx) * FPW));
+            sv = __dadd_rn(sv, __ldg(rss + (size_t)idx * FPW));
             sv = fold_fix(sv, c);
           }
           S[(d + 1) * 32] = sv;
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
               const tkey t = kmax(Pl, __ldg(rts + (size_t)(idx + h) * FPW));
               if ((int64_t)t > budget) continue;
               double sv = __dadd_rn(Sl, __ldg(rs + (size_t)(idx + h) * FPW));
-              sv = __dadd_rn(sv, __ldg(rs + (size_t)__ldg(a.rest_of + idx + h) * FPW));
+              sv = __dadd_rn(sv, __ldg(rss + (size_t)(idx + h) * FPW));
               sv = fold_fix(sv, tag);
               offer(t, sv, ord + (uint32_t)h, p, h);
             }
@@ -529,6 +530,18 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
     out[0] = (uint64_t)__double_as_longlong(bs);
     out[1] = k0;
     out[2] = k1;
+  }
+}
+
+// rss[r][f] = rs[rest_of[r]][f]: the SSE of every run's forced rest next to
+// the run, so the step-2 walk adds it with one load instead of two dependent.
+__global__ void k_rest_sse(const double* __restrict__ rs, const uint32_t* __restrict__ rest_of,
+                           size_t nr, int fpw, double* __restrict__ rss) {
+  const size_t total = nr * (size_t)fpw;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / fpw, f = i % fpw;
+    rss[i] = rs[(size_t)rest_of[r] * fpw + f];
   }
 }
 
@@ -777,8 +790,14 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
                         const uint32_t* skel_pos, const uint64_t* skel_ord,
                         const uint32_t* chunk_skel, uint32_t n_chunks, uint32_t rank,
                         uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
-                        const uint32_t* rest_of, const int64_t* budget, uint32_t nr, int depth_cap,
-                        uint64_t* lanes, cudaStream_t st) {
+                        const uint32_t* rest_of, double* rss, const int64_t* budget, uint32_t nr,
+                        int depth_cap, uint64_t* lanes, int sm_count, cudaStream_t st) {
+  {
+    const size_t total = (size_t)nr * fpw;
+    const unsigned gb = (unsigned)std::min<size_t>((total + 255) / 256, (size_t)sm_count * 8);
+    k_rest_sse<<<gb, 256, 0, st>>>(rs, rest_of, nr, fpw, rss);
+    SCB_CUDA(cudaGetLastError());
+  }
   Trace2Args a;
   a.ops = ops;
   a.skip = skip;
@@ -792,7 +811,7 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   a.counter = counter;
   a.keys = keys;
   a.rs = rs;
-  a.rest_of = rest_of;
+  a.rss = rss;
   a.budget = budget;
   a.nr = nr;
   a.depth_cap = depth_cap;
