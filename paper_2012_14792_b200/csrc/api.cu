@@ -57,8 +57,9 @@ bool small_tables_device(const double* d_est, int cols, int rows, int frames, in
 void validate_device(int n, const int* d_rects, int nbx, const int* d_bx, int nby, const int* d_by,
                      int cols, int rows, int* d_owner, int32_t* d_map, VCheck* d_out,
                      cudaStream_t st);
-void result_maps_device(const FrameBest* d_fb, int frames, int n, int cols, int rows, int* d_owner,
-                        int32_t* d_maps, VCheck* d_out, cudaStream_t st);
+void result_maps_device(const FrameBest* d_fb, size_t fb_stride, int frames, int first_step,
+                        int steps, int n, int cols, int rows, int* d_owner, int32_t* d_maps,
+                        VCheck* d_out, cudaStream_t st);
 void enumerate_count_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
                             double k, int covering, uint64_t* d_counts, uint64_t* d_offsets,
                             DevBuf& temp, cudaStream_t st);
@@ -1132,18 +1133,15 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   // slice-id maps (sc_result_slice_maps)
   const bool post = postcheck_enabled();
   const size_t vb = (size_t)frames * sizeof(VCheck);
-  if (post) {
+  if (post) {  // both steps' partitions in one launch
     ctx->slice_maps.ensure((size_t)2 * frames * cells * sizeof(int32_t));
-    ctx->owner.ensure((size_t)frames * cells * sizeof(int));
+    ctx->owner.ensure((size_t)2 * frames * cells * sizeof(int));
     ctx->vcheck.ensure(2 * vb);
     ctx->h_vcheck.ensure(2 * vb);
-    for (int st = 1; st <= 2; ++st) {
-      if (st == 1 ? !do1 : !do2) continue;
-      result_maps_device(ctx->frame_best.as<FrameBest>() + (size_t)(st - 1) * L.groups * L.fpw,
-                         frames, cfg.n_slices, g.cols, g.rows, ctx->owner.as<int>(),
-                         ctx->slice_maps.as<int32_t>() + (size_t)(st - 1) * frames * cells,
-                         ctx->vcheck.as<VCheck>() + (size_t)(st - 1) * frames, s);
-    }
+    result_maps_device(ctx->frame_best.as<FrameBest>(), (size_t)L.groups * L.fpw, frames,
+                       do1 ? 1 : 2, (do1 ? 1 : 0) + (do2 ? 1 : 0), cfg.n_slices, g.cols, g.rows,
+                       ctx->owner.as<int>(), ctx->slice_maps.as<int32_t>(),
+                       ctx->vcheck.as<VCheck>(), s);
     SCB_CUDA(cudaMemcpyAsync(ctx->h_vcheck.p, ctx->vcheck.p, 2 * vb, cudaMemcpyDeviceToHost, s));
   }
   ctx->maps_cells = cells;

@@ -9,11 +9,11 @@
 //   1. the f64 SAT by the anti-diagonal wavefront (cost.cpp:97-112 order);
 //   2. every rectangle's time ((d - b) - c) + a, clamped to +0.0
 //      (search.cpp:77-83), as u64 bits;
-//   3. a block radix sort of (bits, rect), first-of-run flags and a block scan
-//      -> the exact per-frame ranks, vals[f][rank] and nvals[f] (rank.cu);
+//   3. a bitonic sort of (bits, rect) in shared memory, first-of-run flags
+//      and a block scan -> the exact per-frame ranks, vals[f][rank] and
+//      nvals[f] (rank.cu);
 //   4. the rt keys and the split table rts = max(run, forced rest) into the
 //      search layout [group][rt | rts][rect][fpw].
-#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -28,20 +28,19 @@ __global__ void __launch_bounds__(kSmallThreads)
     k_small_tables(const double* __restrict__ est, int cols, int rows, int frames, int fpw,
                    const int16_t* __restrict__ dec, uint32_t* __restrict__ keys,
                    uint64_t* __restrict__ vals, uint32_t* __restrict__ nvals) {
-  using Sort = cub::BlockRadixSort<uint64_t, kSmallThreads, kSmallItems, uint32_t>;
   using Scan = cub::BlockScan<uint32_t, kSmallThreads>;
   extern __shared__ __align__(16) uint8_t sm_small[];
-  union Temp {
-    typename Sort::TempStorage sort;
-    typename Scan::TempStorage scan;
-  };
-  Temp& temp = *reinterpret_cast<Temp*>(sm_small);
+  __shared__ typename Scan::TempStorage scan_tmp;
   const int f = blockIdx.x;
   const int nyh = rows * (rows + 1) / 2, nxw = cols * (cols + 1) / 2;
   const int nr = nxw * nyh;
+  int np = 1;  // sorted length: the next power of two
+  while (np < nr) np <<= 1;
   const int stride = cols + 1, nsat = stride * (rows + 1);
-  double* T = reinterpret_cast<double*>(sm_small + ((sizeof(Temp) + 15) & ~size_t(15)));
-  uint32_t* rank = reinterpret_cast<uint32_t*>(T + nsat);  // [nr] rank of each rectangle
+  uint64_t* sk = reinterpret_cast<uint64_t*>(sm_small);  // [np] time bits, then sorted
+  double* T = reinterpret_cast<double*>(sk + np);       // [nsat] SAT
+  uint32_t* sv = reinterpret_cast<uint32_t*>(T + nsat);  // [np] rectangle of each key
+  uint32_t* rank = sv + np;                              // [nr] rank of each rectangle
   const double* v = est + (size_t)f * cols * rows;
   // 1. f64 SAT, anti-diagonal wavefront: T = ((v + L) + U) - UL
   for (int i = threadIdx.x; i < nsat; i += blockDim.x) T[i] = 0.0;
@@ -57,51 +56,57 @@ __global__ void __launch_bounds__(kSmallThreads)
     }
     __syncthreads();
   }
-  // 2. clamped time bits of every rectangle, blocked: thread t holds
-  // rectangles t*ITEMS .. t*ITEMS + ITEMS - 1 (padding sorts last)
-  uint64_t kb[kSmallItems];
-  uint32_t kr[kSmallItems];
-  for (int j = 0; j < kSmallItems; ++j) {
-    const int rr = threadIdx.x * kSmallItems + j;
-    kr[j] = (uint32_t)rr;
-    kb[j] = ~0ull;
+  // 2. clamped time bits of every rectangle (padding sorts last)
+  for (int rr = threadIdx.x; rr < np; rr += blockDim.x) {
+    uint64_t b = ~0ull;
     if (rr < nr) {
       const int xw = rr / nyh, yh = rr % nyh;
       const int x0 = dec[xw], w = dec[nxw + xw], y0 = dec[2 * nxw + yh], h = dec[2 * nxw + nyh + yh];
       const int ia = y0 * stride + x0, ib = y0 * stride + x0 + w;
       const int ic = (y0 + h) * stride + x0, idd = (y0 + h) * stride + x0 + w;
       const double t = __dadd_rn(__dsub_rn(__dsub_rn(T[idd], T[ib]), T[ic]), T[ia]);
-      kb[j] = t > 0.0 ? (uint64_t)__double_as_longlong(t) : 0ull;
+      b = t > 0.0 ? (uint64_t)__double_as_longlong(t) : 0ull;
+    }
+    sk[rr] = b;
+    sv[rr] = (uint32_t)rr;
+  }
+  __syncthreads();
+  // 3. bitonic sort of (bits, rect) in shared memory
+  for (int size = 2; size <= np; size <<= 1) {
+    for (int half = size >> 1; half > 0; half >>= 1) {
+      for (int i = threadIdx.x; i < np / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (half - 1)), hi = lo + half;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = sk[lo], b = sk[hi];
+        const uint32_t va = sv[lo], vb = sv[hi];
+        const bool gt = a > b || (a == b && va > vb);
+        if (gt == up) {
+          sk[lo] = b, sk[hi] = a;
+          sv[lo] = vb, sv[hi] = va;
+        }
+      }
+      __syncthreads();
     }
   }
-  __syncthreads();
-  // 3. sort (bits, rect); ranks of the distinct values in order
-  Sort(temp.sort).Sort(kb, kr);
-  __syncthreads();
-  // first-of-run flags need the previous element: the last item of the
-  // previous thread, through shared memory
-  __shared__ uint64_t s_last[kSmallThreads];
-  s_last[threadIdx.x] = kb[kSmallItems - 1];
-  __syncthreads();
-  uint32_t flg[kSmallItems];
+  // first-of-run flags and their exclusive scan, kSmallItems positions per
+  // thread (blocked) -> the rank of each distinct value
+  const int p0 = threadIdx.x * kSmallItems;
   uint32_t cnt = 0;
   for (int j = 0; j < kSmallItems; ++j) {
-    const int pos = threadIdx.x * kSmallItems + j;
-    const uint64_t prev = j ? kb[j - 1] : (threadIdx.x ? s_last[threadIdx.x - 1] : 0ull);
-    flg[j] = (pos < nr && (pos == 0 || kb[j] != prev)) ? 1u : 0u;
-    cnt += flg[j];
+    const int pos = p0 + j;
+    cnt += (pos < nr && (pos == 0 || sk[pos] != sk[pos - 1])) ? 1u : 0u;
   }
-  uint32_t before = 0;
-  Scan(temp.scan).ExclusiveSum(cnt, before);
-  uint32_t run = before;  // distinct values before this thread's first item
+  uint32_t run = 0;
+  Scan(scan_tmp).ExclusiveSum(cnt, run);
   uint64_t* fv = vals + (size_t)f * nr;
   for (int j = 0; j < kSmallItems; ++j) {
-    const int pos = threadIdx.x * kSmallItems + j;
+    const int pos = p0 + j;
     if (pos >= nr) break;
-    run += flg[j];
+    const bool first = pos == 0 || sk[pos] != sk[pos - 1];
+    run += first ? 1u : 0u;
     const uint32_t key = run - 1;
-    rank[kr[j]] = key;
-    if (flg[j]) fv[key] = kb[j];
+    rank[sv[pos]] = key;
+    if (first) fv[key] = sk[pos];
     if (pos == nr - 1) nvals[f] = key + 1;
   }
   __syncthreads();
@@ -124,15 +129,11 @@ __global__ void __launch_bounds__(kSmallThreads)
 }
 
 size_t small_tables_smem(int cols, int rows) {
-  using Sort = cub::BlockRadixSort<uint64_t, kSmallThreads, kSmallItems, uint32_t>;
-  using Scan = cub::BlockScan<uint32_t, kSmallThreads>;
-  union Temp {
-    typename Sort::TempStorage sort;
-    typename Scan::TempStorage scan;
-  };
   const size_t nr = (size_t)cols * (cols + 1) / 2 * (rows * (rows + 1) / 2);
-  return ((sizeof(Temp) + 15) & ~size_t(15)) + (size_t)(cols + 1) * (rows + 1) * sizeof(double) +
-         nr * sizeof(uint32_t);
+  size_t np = 1;
+  while (np < nr) np <<= 1;
+  return np * (sizeof(uint64_t) + sizeof(uint32_t)) +
+         (size_t)(cols + 1) * (rows + 1) * sizeof(double) + nr * sizeof(uint32_t);
 }
 
 // true when the grid fits the one-CTA path (and it was launched)

@@ -656,10 +656,12 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
                            st));
   SCB_CUDA(cudaMemcpyAsync(skel_ord.as<uint64_t>() + tot_skel, &tot_cand, 8, cudaMemcpyHostToDevice,
                            st));
-  // ~128 chunks per SM (persistent warps take them dynamically), 256..8192 ops
+  // ~128 chunks per SM (persistent warps take them dynamically), 16..8192
+  // ops: small spaces get short chunks, so their few ops run on many warps
+  // instead of one warp's serial chain of dependent loads
   const uint64_t chunk_ops = std::min<uint64_t>(
-      8192, std::max<uint64_t>(256, (tot_ops + (uint64_t)sm_count * 128 - 1) /
-                                        ((uint64_t)sm_count * 128)));
+      8192, std::max<uint64_t>(16, (tot_ops + (uint64_t)sm_count * 128 - 1) /
+                                       ((uint64_t)sm_count * 128)));
   const uint32_t n_chunks = (uint32_t)std::max<uint64_t>(1, (tot_ops + chunk_ops - 1) / chunk_ops);
   chunk_skel.ensure(((size_t)n_chunks + 1) * sizeof(uint32_t));
   k_trace_chunks<<<(n_chunks + 1 + 255) / 256, 256, 0, st>>>(skel_pos.as<uint32_t>(),

@@ -118,9 +118,17 @@ __global__ void k_validate(int n, const int* rects, int nbx, const int* bx, int 
 // f's layout snapshot (W[16] R[16] H[64], FrameBest::snap) becomes the
 // layout_to_partition slices (search.cpp:63-75; tiles = widths x {rows}) and
 // goes through the same checks, restricted to the columns the widths span.
-__global__ void k_result_maps(const FrameBest* __restrict__ fb, int n, int cols, int rows,
-                              int* owner, int32_t* maps, VCheck* out) {
-  const int f = blockIdx.x;
+// blockIdx.y = step - 1 (both steps in one launch): the step's FrameBest,
+// maps and verdicts sit `fb_stride` / `frames` entries apart.
+__global__ void k_result_maps(const FrameBest* __restrict__ fb0, size_t fb_stride, int frames,
+                              int first_step, int n, int cols, int rows, int* owner0,
+                              int32_t* maps0, VCheck* out0) {
+  const int f = blockIdx.x, si = first_step - 1 + blockIdx.y;
+  const FrameBest* fb = fb0 + (size_t)si * fb_stride;
+  const size_t cells_ = (size_t)cols * rows;
+  int* owner = owner0 + (size_t)blockIdx.y * frames * cells_;
+  int32_t* maps = maps0 + (size_t)si * frames * cells_;
+  VCheck* out = out0 + (size_t)si * frames;
   __shared__ int rects[5 * SC_MAX_SLICES];
   __shared__ int bx[SC_MAX_COLS + 1], by[2];
   __shared__ int s_c, s_span;
@@ -171,9 +179,11 @@ void validate_device(int n, const int* d_rects, int nbx, const int* d_bx, int nb
   SCB_CUDA(cudaGetLastError());
 }
 
-void result_maps_device(const FrameBest* d_fb, int frames, int n, int cols, int rows, int* d_owner,
-                        int32_t* d_maps, VCheck* d_out, cudaStream_t st) {
-  k_result_maps<<<frames, 256, 0, st>>>(d_fb, n, cols, rows, d_owner, d_maps, d_out);
+void result_maps_device(const FrameBest* d_fb, size_t fb_stride, int frames, int first_step,
+                        int steps, int n, int cols, int rows, int* d_owner, int32_t* d_maps,
+                        VCheck* d_out, cudaStream_t st) {
+  k_result_maps<<<dim3(frames, steps), 256, 0, st>>>(d_fb, fb_stride, frames, first_step, n, cols,
+                                                     rows, d_owner, d_maps, d_out);
   SCB_CUDA(cudaGetLastError());
 }
 
