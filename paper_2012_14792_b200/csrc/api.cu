@@ -49,7 +49,7 @@ void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_w
                      const LaneBest* lanes, const uint8_t* snaps,
                      const unsigned long long* count, const unsigned long long* scored,
                      double lambda, const uint64_t* vals, const uint32_t* nvals, size_t nr,
-                     FrameBest* out, int64_t* budget_out, cudaStream_t st);
+                     FrameBest* out, int64_t* budget_out, DevBuf& scratch, cudaStream_t st);
 bool small_tables_device(const double* d_est, int cols, int rows, int frames, int fpw,
                          const int16_t* d_dec, uint32_t* keys, uint64_t* vals, uint32_t* nvals,
                          cudaStream_t st);
@@ -853,7 +853,8 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
                     ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr,
                     ctx->nvals.as<uint32_t>() + (size_t)gi * L.fpw, L.nr,
                     fb + (size_t)gi * L.fpw,
-                    step == 1 ? ctx->budget.as<int64_t>() + (size_t)gi * L.fpw : nullptr, st);
+                    step == 1 ? ctx->budget.as<int64_t>() + (size_t)gi * L.fpw : nullptr,
+                    ctx->fin_scratch, st);
   }
 }
 
@@ -1276,7 +1277,7 @@ sc_ctx::~sc_ctx() {
                   &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc, &rt_bits, &vals, &nvals, &budget_f64, &rk_idx, &rk_sorted,
                   &rk_flags, &rk_offsets, &rk_temp, &sse_inc, &flt_idx, &flt_flag, &flt_list,
                   &flt_count, &flt_temp, &slice_maps, &owner, &vcheck, &val_in, &enum_out,
-                  &enum_temp, &rest_of, &rss})
+                  &enum_temp, &rest_of, &rss, &fin_scratch})
     b->release();
   h_vcheck.release();
   h_stage.release();

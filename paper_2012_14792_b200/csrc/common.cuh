@@ -265,6 +265,7 @@ struct sc_ctx {
   scb::DevBuf slice_maps, owner, vcheck, val_in, enum_out, enum_temp;
   scb::DevBuf rest_of;  // [NR] forced rest of each run, per decode-table grid (step-2 trace)
   scb::DevBuf rss;      // [NR][FPW] SSE of each run's forced rest (step-2 trace, per group)
+  scb::DevBuf fin_scratch;  // two-level finalize partials (search.cu)
   scb::HostBuf h_vcheck;
   int maps_frames[2] = {0, 0};
   size_t maps_cells = 0;

@@ -333,26 +333,11 @@ __device__ __forceinline__ int64_t budget_key_f(const uint64_t* vals, uint32_t n
   return (int64_t)lo - 1;
 }
 
-__global__ void k_finalize(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
-                           const LaneBest* __restrict__ lanes, const uint8_t* __restrict__ snaps,
-                           const unsigned long long* count, const unsigned long long* scored,
-                           double lambda, const uint64_t* __restrict__ vals,
-                           const uint32_t* __restrict__ nvals, size_t nr,
-                           FrameBest* __restrict__ out, int64_t* __restrict__ budget_out) {
-  const int f = blockIdx.x;
-  if (f >= frames_in_group) return;
-  __shared__ LaneBest sb[256];
-  __shared__ uint32_t si[256];
-  LaneBest best;
-  best.t = ~0ull; best.sse = __longlong_as_double(0x7ff0000000000000ll);
-  best.item = ~0ull; best.ord = ~0ull;
-  uint32_t bi = 0xffffffffu;
-  const uint32_t n_lanes = n_warps * 32;
-  for (uint32_t li = threadIdx.x * fpw + f; li < n_lanes; li += blockDim.x * fpw) {
-    const LaneBest x = lanes[li];
-    if (x.item == ~0ull) continue;
-    if (bi == 0xffffffffu || lane_less(step, n, x, li, best, bi, snaps)) { best = x; bi = li; }
-  }
+// Block minimum (lane_less order) of the lanes a block's threads scanned;
+// thread 0 ends with it in sb[0] / si[0] (si: the lane, 0xffffffff: none).
+__device__ __forceinline__ void finalize_block_min(int step, int n, LaneBest best, uint32_t bi,
+                                                   const uint8_t* __restrict__ snaps,
+                                                   LaneBest* sb, uint32_t* si) {
   sb[threadIdx.x] = best;
   si[threadIdx.x] = bi;
   __syncthreads();
@@ -368,6 +353,59 @@ __global__ void k_finalize(int step, int n, int fpw, int frames_in_group, uint32
     }
     __syncthreads();
   }
+}
+
+// First level of the per-frame reduction: part p of frame f's lanes
+// (blockIdx = (p, f)) -> its minimum and that lane's index.  Spreads the
+// scan of the persistent grid's ~10^5 lanes over many blocks (one block per
+// frame took ~100 us).
+__global__ void k_finalize_part(int step, int n, int fpw, uint32_t n_warps,
+                                const LaneBest* __restrict__ lanes,
+                                const uint8_t* __restrict__ snaps, LaneBest* part_best,
+                                uint32_t* part_lane) {
+  const int f = blockIdx.y, parts = gridDim.x;
+  __shared__ LaneBest sb[256];
+  __shared__ uint32_t si[256];
+  LaneBest best;
+  best.t = ~0ull; best.sse = __longlong_as_double(0x7ff0000000000000ll);
+  best.item = ~0ull; best.ord = ~0ull;
+  uint32_t bi = 0xffffffffu;
+  const uint32_t n_lanes = n_warps * 32;
+  for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) * fpw + f; li < n_lanes;
+       li += (uint32_t)parts * blockDim.x * fpw) {
+    const LaneBest x = lanes[li];
+    if (x.item == ~0ull) continue;
+    if (bi == 0xffffffffu || lane_less(step, n, x, li, best, bi, snaps)) { best = x; bi = li; }
+  }
+  finalize_block_min(step, n, best, bi, snaps, sb, si);
+  if (threadIdx.x == 0) {
+    part_best[(size_t)f * parts + blockIdx.x] = sb[0];
+    part_lane[(size_t)f * parts + blockIdx.x] = si[0];
+  }
+}
+
+__global__ void k_finalize(int step, int n, int parts, int frames_in_group,
+                           const LaneBest* __restrict__ part_best,
+                           const uint32_t* __restrict__ part_lane, const uint8_t* __restrict__ snaps,
+                           const unsigned long long* count, const unsigned long long* scored,
+                           double lambda, const uint64_t* __restrict__ vals,
+                           const uint32_t* __restrict__ nvals, size_t nr,
+                           FrameBest* __restrict__ out, int64_t* __restrict__ budget_out) {
+  const int f = blockIdx.x;
+  if (f >= frames_in_group) return;
+  __shared__ LaneBest sb[256];
+  __shared__ uint32_t si[256];
+  LaneBest best;
+  best.t = ~0ull; best.sse = __longlong_as_double(0x7ff0000000000000ll);
+  best.item = ~0ull; best.ord = ~0ull;
+  uint32_t bi = 0xffffffffu;
+  for (int pi = threadIdx.x; pi < parts; pi += blockDim.x) {
+    const uint32_t li = part_lane[(size_t)f * parts + pi];
+    if (li == 0xffffffffu) continue;
+    const LaneBest x = part_best[(size_t)f * parts + pi];
+    if (bi == 0xffffffffu || lane_less(step, n, x, li, best, bi, snaps)) { best = x; bi = li; }
+  }
+  finalize_block_min(step, n, best, bi, snaps, sb, si);
   __shared__ uint32_t win;
   const uint64_t* fv = vals + (size_t)f * nr;  // this frame's key -> time bits
   if (threadIdx.x == 0) {
@@ -543,10 +581,17 @@ void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_w
                      const LaneBest* lanes, const uint8_t* snaps,
                      const unsigned long long* count, const unsigned long long* scored,
                      double lambda, const uint64_t* vals, const uint32_t* nvals, size_t nr,
-                     FrameBest* out, int64_t* budget_out, cudaStream_t st) {
-  k_finalize<<<frames_in_group, 256, 0, st>>>(step, n, fpw, frames_in_group, n_warps, lanes, snaps,
-                                              count, scored, lambda, vals, nvals, nr, out,
-                                              budget_out);
+                     FrameBest* out, int64_t* budget_out, DevBuf& scratch, cudaStream_t st) {
+  // ~2 blocks' worth of lanes per part
+  const int parts = (int)std::max<uint32_t>(1, std::min<uint32_t>(256, n_warps * 32 / fpw / 512));
+  scratch.ensure((size_t)frames_in_group * parts * (sizeof(LaneBest) + sizeof(uint32_t)));
+  LaneBest* pb = scratch.as<LaneBest>();
+  uint32_t* pl = reinterpret_cast<uint32_t*>(pb + (size_t)frames_in_group * parts);
+  k_finalize_part<<<dim3(parts, frames_in_group), 256, 0, st>>>(step, n, fpw, n_warps, lanes, snaps,
+                                                                pb, pl);
+  SCB_CUDA(cudaGetLastError());
+  k_finalize<<<frames_in_group, 256, 0, st>>>(step, n, parts, frames_in_group, pb, pl, snaps, count,
+                                              scored, lambda, vals, nvals, nr, out, budget_out);
   SCB_CUDA(cudaGetLastError());
 }
 

@@ -9,11 +9,12 @@
 //   1. the f64 SAT by the anti-diagonal wavefront (cost.cpp:97-112 order);
 //   2. every rectangle's time ((d - b) - c) + a, clamped to +0.0
 //      (search.cpp:77-83), as u64 bits;
-//   3. a bitonic sort of (bits, rect) in shared memory, first-of-run flags
-//      and a block scan -> the exact per-frame ranks, vals[f][rank] and
-//      nvals[f] (rank.cu);
+//   3. a 32-bit block radix sort of the range-quantised times (as rank.cu),
+//      equal-key groups re-sorted by the full bits, first-of-run flags and a
+//      block scan -> the exact per-frame ranks, vals[f][rank], nvals[f];
 //   4. the rt keys and the split table rts = max(run, forced rest) into the
 //      search layout [group][rt | rts][rect][fpw].
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -24,24 +25,31 @@ constexpr int kSmallThreads = 512;
 constexpr int kSmallItems = 16;
 constexpr int kSmallNR = kSmallThreads * kSmallItems;  // 8,192 rectangles
 
+using SmallSort = cub::BlockRadixSort<uint32_t, kSmallThreads, kSmallItems, uint32_t>;
+using SmallScan = cub::BlockScan<uint32_t, kSmallThreads>;
+union SmallTemp {
+  typename SmallSort::TempStorage sort;
+  typename SmallScan::TempStorage scan;
+};
+
 __global__ void __launch_bounds__(kSmallThreads)
     k_small_tables(const double* __restrict__ est, int cols, int rows, int frames, int fpw,
                    const int16_t* __restrict__ dec, uint32_t* __restrict__ keys,
                    uint64_t* __restrict__ vals, uint32_t* __restrict__ nvals) {
-  using Scan = cub::BlockScan<uint32_t, kSmallThreads>;
   extern __shared__ __align__(16) uint8_t sm_small[];
-  __shared__ typename Scan::TempStorage scan_tmp;
+  SmallTemp& temp = *reinterpret_cast<SmallTemp*>(sm_small);
+  __shared__ unsigned long long s_lo, s_hi;
   const int f = blockIdx.x;
   const int nyh = rows * (rows + 1) / 2, nxw = cols * (cols + 1) / 2;
   const int nr = nxw * nyh;
-  int np = 1;  // sorted length: the next power of two
-  while (np < nr) np <<= 1;
   const int stride = cols + 1, nsat = stride * (rows + 1);
-  uint64_t* sk = reinterpret_cast<uint64_t*>(sm_small);  // [np] time bits, then sorted
-  double* T = reinterpret_cast<double*>(sk + np);       // [nsat] SAT
-  uint32_t* sv = reinterpret_cast<uint32_t*>(T + nsat);  // [np] rectangle of each key
-  uint32_t* rank = sv + np;                              // [nr] rank of each rectangle
+  uint64_t* B = reinterpret_cast<uint64_t*>(sm_small + ((sizeof(SmallTemp) + 15) & ~size_t(15)));
+  double* T = reinterpret_cast<double*>(B + nr);    // [nsat] SAT
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(T + nsat);  // [kSmallNR] sorted rectangles
+  uint32_t* skey = sidx + kSmallNR;                  // [kSmallNR] sorted quantised keys
+  uint32_t* rank = skey + kSmallNR;                  // [nr] rank of each rectangle
   const double* v = est + (size_t)f * cols * rows;
+  if (threadIdx.x == 0) s_lo = ~0ull, s_hi = 0;
   // 1. f64 SAT, anti-diagonal wavefront: T = ((v + L) + U) - UL
   for (int i = threadIdx.x; i < nsat; i += blockDim.x) T[i] = 0.0;
   __syncthreads();
@@ -56,57 +64,84 @@ __global__ void __launch_bounds__(kSmallThreads)
     }
     __syncthreads();
   }
-  // 2. clamped time bits of every rectangle (padding sorts last)
-  for (int rr = threadIdx.x; rr < np; rr += blockDim.x) {
-    uint64_t b = ~0ull;
-    if (rr < nr) {
-      const int xw = rr / nyh, yh = rr % nyh;
-      const int x0 = dec[xw], w = dec[nxw + xw], y0 = dec[2 * nxw + yh], h = dec[2 * nxw + nyh + yh];
-      const int ia = y0 * stride + x0, ib = y0 * stride + x0 + w;
-      const int ic = (y0 + h) * stride + x0, idd = (y0 + h) * stride + x0 + w;
-      const double t = __dadd_rn(__dsub_rn(__dsub_rn(T[idd], T[ib]), T[ic]), T[ia]);
-      b = t > 0.0 ? (uint64_t)__double_as_longlong(t) : 0ull;
+  // 2. clamped time bits of every rectangle and their positive finite range
+  uint64_t mn = ~0ull, mx = 0;
+  for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+    const int xw = rr / nyh, yh = rr % nyh;
+    const int x0 = dec[xw], w = dec[nxw + xw], y0 = dec[2 * nxw + yh], h = dec[2 * nxw + nyh + yh];
+    const int ia = y0 * stride + x0, ib = y0 * stride + x0 + w;
+    const int ic = (y0 + h) * stride + x0, idd = (y0 + h) * stride + x0 + w;
+    const double t = __dadd_rn(__dsub_rn(__dsub_rn(T[idd], T[ib]), T[ic]), T[ia]);
+    const uint64_t b = t > 0.0 ? (uint64_t)__double_as_longlong(t) : 0ull;
+    B[rr] = b;
+    if (b != 0 && b < 0x7ff0000000000000ull) {
+      mn = b < mn ? b : mn;
+      mx = b > mx ? b : mx;
     }
-    sk[rr] = b;
-    sv[rr] = (uint32_t)rr;
+  }
+  atomicMin(&s_lo, (unsigned long long)mn);
+  atomicMax(&s_hi, (unsigned long long)mx);
+  __syncthreads();
+  // 3. 32-bit order-preserving quantisation inside the frame's range (as
+  //    rank.cu), a block radix sort, then equal-key groups re-sorted by the
+  //    full bits -> the exact order of (bits, rectangle)
+  const uint64_t lo = s_lo, span = s_hi > s_lo ? s_hi - s_lo : 0;
+  const int need = span ? 64 - __clzll((long long)span) : 0;
+  const int sh = need > 30 ? need - 30 : 0;
+  uint32_t kk[kSmallItems], ki[kSmallItems];
+  for (int j = 0; j < kSmallItems; ++j) {
+    const int rr = threadIdx.x * kSmallItems + j;
+    ki[j] = (uint32_t)rr;
+    kk[j] = 0xffffffffu;
+    if (rr < nr) {
+      const uint64_t b = B[rr];
+      kk[j] = b == 0 ? 0u : (b >= 0x7ff0000000000000ull ? 0xfffffffeu
+                                                        : 1u + (uint32_t)((b - lo) >> sh));
+    }
+  }
+  SmallSort(temp.sort).SortBlockedToStriped(kk, ki);
+  for (int j = 0; j < kSmallItems; ++j) {
+    const int pos = j * kSmallThreads + threadIdx.x;  // striped
+    skey[pos] = kk[j];
+    sidx[pos] = ki[j];
   }
   __syncthreads();
-  // 3. bitonic sort of (bits, rect) in shared memory
-  for (int size = 2; size <= np; size <<= 1) {
-    for (int half = size >> 1; half > 0; half >>= 1) {
-      for (int i = threadIdx.x; i < np / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (half - 1)), hi = lo + half;
-        const bool up = (lo & size) == 0;
-        const uint64_t a = sk[lo], b = sk[hi];
-        const uint32_t va = sv[lo], vb = sv[hi];
-        const bool gt = a > b || (a == b && va > vb);
-        if (gt == up) {
-          sk[lo] = b, sk[hi] = a;
-          sv[lo] = vb, sv[hi] = va;
-        }
+  for (int pos = threadIdx.x; pos < nr; pos += blockDim.x) {
+    if (pos > 0 && skey[pos - 1] == skey[pos]) continue;
+    int e = pos + 1;
+    while (e < nr && skey[e] == skey[pos]) ++e;
+    for (int a = pos + 1; a < e; ++a) {  // insertion sort by (bits, rectangle)
+      const uint32_t x = sidx[a];
+      const uint64_t bx = B[x];
+      int c = a - 1;
+      while (c >= pos && (B[sidx[c]] > bx || (B[sidx[c]] == bx && sidx[c] > x))) {
+        sidx[c + 1] = sidx[c];
+        --c;
       }
-      __syncthreads();
+      sidx[c + 1] = x;
     }
   }
+  __syncthreads();
   // first-of-run flags and their exclusive scan, kSmallItems positions per
   // thread (blocked) -> the rank of each distinct value
   const int p0 = threadIdx.x * kSmallItems;
   uint32_t cnt = 0;
   for (int j = 0; j < kSmallItems; ++j) {
     const int pos = p0 + j;
-    cnt += (pos < nr && (pos == 0 || sk[pos] != sk[pos - 1])) ? 1u : 0u;
+    cnt += (pos < nr && (pos == 0 || B[sidx[pos]] != B[sidx[pos - 1]])) ? 1u : 0u;
   }
   uint32_t run = 0;
-  Scan(scan_tmp).ExclusiveSum(cnt, run);
+  SmallScan(temp.scan).ExclusiveSum(cnt, run);
   uint64_t* fv = vals + (size_t)f * nr;
   for (int j = 0; j < kSmallItems; ++j) {
     const int pos = p0 + j;
     if (pos >= nr) break;
-    const bool first = pos == 0 || sk[pos] != sk[pos - 1];
+    const uint64_t b = B[sidx[pos]];
+    const bool first = pos == 0 || b != B[sidx[pos - 1]];
     run += first ? 1u : 0u;
     const uint32_t key = run - 1;
-    rank[sv[pos]] = key;
-    if (first) fv[key] = sk[pos];
+    rank[sidx[pos]] = key;
+    if (first) fv[key] = b;
     if (pos == nr - 1) nvals[f] = key + 1;
   }
   __syncthreads();
@@ -130,10 +165,9 @@ __global__ void __launch_bounds__(kSmallThreads)
 
 size_t small_tables_smem(int cols, int rows) {
   const size_t nr = (size_t)cols * (cols + 1) / 2 * (rows * (rows + 1) / 2);
-  size_t np = 1;
-  while (np < nr) np <<= 1;
-  return np * (sizeof(uint64_t) + sizeof(uint32_t)) +
-         (size_t)(cols + 1) * (rows + 1) * sizeof(double) + nr * sizeof(uint32_t);
+  return ((sizeof(SmallTemp) + 15) & ~size_t(15)) + nr * sizeof(uint64_t) +
+         (size_t)(cols + 1) * (rows + 1) * sizeof(double) + 2 * (size_t)kSmallNR * sizeof(uint32_t) +
+         nr * sizeof(uint32_t);
 }
 
 // true when the grid fits the one-CTA path (and it was launched)
