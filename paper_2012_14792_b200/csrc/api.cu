@@ -680,8 +680,12 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
   }
   if (step == 1 && !prune && trace_enabled() && ensure_trace(ctx, plan, g, cfg, st)) {
     const int depth_cap = std::max(cfg.n_slices, 2);
+    // blocks per SM: the occupancy limit, or SLICECRAFT_B200_TRACE_BPS (fewer
+    // leave room for the side stream's texture pass to run beside the walk)
+    int bps = trace_blocks_per_sm(L.fpw, depth_cap);
+    if (const char* v = getenv("SLICECRAFT_B200_TRACE_BPS")) bps = std::max(1, std::min(bps, atoi(v)));
     const int blocks = std::max(
-        1, (int)std::min<uint64_t>((uint64_t)ctx->sm_count * trace_blocks_per_sm(L.fpw, depth_cap),
+        1, (int)std::min<uint64_t>((uint64_t)ctx->sm_count * bps,
                                    (plan->trace_chunks / ctx->shard_world + 8) / 2));
     const uint32_t n_lanes = (uint32_t)blocks * 32;  // one record per block lane (trace.cu)
     const size_t lane_bytes = (size_t)n_lanes * 2 * sizeof(uint64_t);
@@ -1081,12 +1085,17 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   // fork the side stream from the caller's stream
   SCB_CUDA(cudaEventRecord(ev[7], s));
   SCB_CUDA(cudaStreamWaitEvent(s2, ev[7], 0));
-  // With a host luma batch, the main stream goes first: its small est upload
+  // The main stream goes first: with a host luma batch its small est upload
   // must not queue behind the luma copy on the copy engine, and step 1 then
-  // overlaps that copy.  Otherwise K1 goes first (it needs the SMs that the
-  // persistent step-1 walk would hold).
+  // overlaps that copy; with device luma the high-priority time tables take
+  // the SMs and K1 (low priority) fills the gaps.
   const bool need_moments = do2;
-  const bool main_first = need_moments && luma && !is_device_ptr(luma);
+  // (SLICECRAFT_B200_K1_LATE=0: K1 first for device luma -- measured 1.6 %
+  // slower on cfg3: with the main stream at high priority the time tables
+  // get the SMs first either way, and K1 fills the gaps)
+  const char* k1l = getenv("SLICECRAFT_B200_K1_LATE");
+  const bool main_first =
+      need_moments && luma && (!is_device_ptr(luma) || !(k1l && k1l[0] == '0'));
   auto enqueue_main = [&] {
     ctx->est.ensure((size_t)frames * cells * sizeof(double));
     SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),

@@ -164,9 +164,10 @@ __global__ void k_rank_range(const uint64_t* __restrict__ bits, size_t nr, uint6
 }
 
 __global__ void k_rank_key32(const uint64_t* __restrict__ bits, size_t nr, int frames, int fbits,
-                             const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi,
-                             uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
-  const int qb = 32 - fbits;
+                             int kbits, const uint64_t* __restrict__ lo,
+                             const uint64_t* __restrict__ hi, uint32_t* __restrict__ key,
+                             uint32_t* __restrict__ val) {
+  const int qb = kbits - fbits;
   const uint32_t qmax = qb >= 32 ? 0xffffffffu : (1u << qb) - 1u;
   const size_t total = nr * (size_t)frames;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
@@ -296,6 +297,10 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
     fail(SC_ERR_SIZE, "too many rectangles or frames for the time-key pipeline");
   int fbits = 0;
   while ((1 << fbits) < frames) ++fbits;
+  // key width: 24 bits (3 radix passes) leave >= 2^14 buckets per frame even
+  // at 1024 frames -- equal keys are re-sorted exactly by k_rank_groups --
+  // and 32 bits (4 passes) only when the frame index needs more room
+  const int kbits = fbits <= 10 ? 24 : 32;
   ctx->rk_idx.ensure(total * sizeof(uint32_t) * 6);
   ctx->rk_flags.ensure(total * sizeof(uint32_t) * 2);
   ctx->rk_sorted.ensure(((size_t)frames * 2 + 2) * sizeof(uint64_t) + (total / (kSmallGroup + 1) + 2) *
@@ -317,15 +322,15 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   const unsigned rb = (unsigned)std::max<size_t>(1, std::min<size_t>((nr + 255) / 256, 16));
   k_rank_range<<<dim3(rb, frames), 256, 0, st>>>(bits_fm, nr, lo, hi);
   SCB_CUDA(cudaGetLastError());
-  k_rank_key32<<<blocks, 256, 0, st>>>(bits_fm, nr, frames, fbits, lo, hi, key_in, val_in);
+  k_rank_key32<<<blocks, 256, 0, st>>>(bits_fm, nr, frames, fbits, kbits, lo, hi, key_in, val_in);
   SCB_CUDA(cudaGetLastError());
   size_t b1 = 0, b3 = 0;
   SCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, key_in, key_out, val_in, idx, (int)total,
-                                           0, 32, st));
+                                           0, kbits, st));
   SCB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, b3, flags, scan, (int)total, st));
   ctx->rk_temp.ensure(std::max(b1, b3));
   SCB_CUDA(cub::DeviceRadixSort::SortPairs(ctx->rk_temp.p, b1, key_in, key_out, val_in, idx,
-                                           (int)total, 0, 32, st));
+                                           (int)total, 0, kbits, st));
   k_rank_groups<<<blocks, 256, 0, st>>>(key_out, idx, bits_fm, total, big_count, big_list);
   SCB_CUDA(cudaGetLastError());
   k_rank_big<<<ctx->sm_count, 256, 0, st>>>(idx, bits_fm, big_count, big_list, tmp);
