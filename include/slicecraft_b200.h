@@ -356,7 +356,37 @@ sc_status sc_prefix_sum_table(const double* values, int64_t n_values, int32_t co
 /* split_even (grid.cpp:52-60). */
 sc_status sc_split_even(int32_t total, int32_t parts, int32_t* out);
 
-/* ---- multi-GPU shard merge --------------------------------------------- */
+/* ---- multi-GPU: the library owns the exchange between shards ---------- */
+/* With a communicator attached (rank r of world w, on the context's device),
+ * every search call shards the candidate space over the ranks (as
+ * sc_ctx_set_shard) AND exchanges what the shards need, returning the merged,
+ * global results on every rank: after step 1 the global t_min of each frame
+ * (a u64 all-reduce-min of the time bits, on the device) sets step 2's
+ * budget; in the pruned mode the frozen seed incumbents are all-reduced
+ * (min) between phase A and phase B, so every shard prunes with the global
+ * bound; at the end the per-frame shard bests are all-gathered and merged
+ * (first in enumeration order, counts summed).  Every rank must make the
+ * same calls in the same order.  Replaces the reference's per-flush
+ * std::thread pool (search.cpp:198-249). */
+#define SC_COMM_ID_BYTES 128
+/* An all-gather between the ranks: send `bytes` bytes, receive world * bytes
+ * in rank order into recv.  Returns 0 on success. */
+typedef int (*sc_allgather_fn)(void* user, const void* send, size_t bytes, void* recv);
+/* NCCL unique id (ncclGetUniqueId; SC_COMM_ID_BYTES bytes) for rank 0 to
+ * broadcast to the others by any means (the library loads libnccl.so.2 at
+ * run time). */
+sc_status sc_comm_unique_id(void* id_out);
+/* NCCL transport (ncclCommInitRank on the context's device; over NVLink /
+ * NVSwitch between the GPUs of one node). */
+sc_status sc_comm_init_nccl(sc_ctx* ctx, int32_t rank, int32_t world, const void* unique_id);
+/* Host transport: the library calls fn for every exchange (e.g. a gloo or MPI
+ * all-gather); the device waits for it. */
+sc_status sc_comm_init_callback(sc_ctx* ctx, int32_t rank, int32_t world, sc_allgather_fn fn,
+                                void* user);
+/* Detach (and destroy) the communicator; the context is a single shard again. */
+sc_status sc_comm_detach(sc_ctx* ctx);
+
+/* ---- multi-GPU shard merge (caller-owned exchange) ---------------------- */
 /* Opaque per-frame shard best, exchanged by an all-gather (NCCL or gloo). */
 typedef struct sc_shard_best {
   double key_sse;     /* step 2 key (inf in step 1) */

@@ -59,6 +59,9 @@ class SearchResult(C.Structure):
 
 
 SC_ORIGIN_PROPOSED, SC_ORIGIN_UNIFORM = 0, 1
+SC_COMM_ID_BYTES = 128
+# int (*)(void* user, const void* send, size_t bytes, void* recv)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 
 class Rect(C.Structure):
@@ -143,6 +146,10 @@ SIGNATURES = [
     ("sc_moments_sse", C.c_int, [C.POINTER(CtuRecord), C.POINTER(C.c_double)]),
     ("sc_prefix_sum_table", C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P]),
     ("sc_split_even", C.c_int, [C.c_int32, C.c_int32, _P]),
+    ("sc_comm_unique_id", C.c_int, [_P]),
+    ("sc_comm_init_nccl", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
+    ("sc_comm_init_callback", C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
+    ("sc_comm_detach", C.c_int, [_P]),
     ("sc_shard_export", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
     ("sc_shard_merge", C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P]),
 ]

@@ -3,6 +3,9 @@
 // Host work here is O(cells) or O(items) bookkeeping — geometry, validation,
 // the frame-independent work-item plan, the area-threshold table — plus the
 // CUDA launches.  No candidate is scored on the host.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -111,6 +114,90 @@ sc_status set_last_error(sc_status s, const char* msg) {
 using namespace scb;
 
 namespace {
+
+void export_shards(sc_ctx* ctx, int step, int frames, sc_shard_best* out);
+void merge_shards(int step, int world, int frames, const sc_shard_best* gathered,
+                  sc_search_result* inout);
+
+// ---- the library-owned exchange of candidate-space shards ---------------------
+// NCCL is opened at run time (dlopen), so the library has no link-time NCCL
+// dependency and shares the process's libnccl (e.g. torch's) when one is
+// loaded.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(h, "ncclAllReduce"));
+    a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(h, "ncclAllGather"));
+    a.errorString = reinterpret_cast<decltype(a.errorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.allReduce && a.allGather &&
+           a.errorString;
+    return a;
+  }();
+  if (!api.ok) fail(SC_ERR_CUDA, "NCCL (libnccl.so.2) is not available");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(SC_ERR_CUDA, std::string(what) + ": " + nccl().errorString(r));
+}
+
+bool has_comm(const sc_ctx* ctx) { return ctx->comm_kind != 0; }
+
+// Element-wise global minimum of n u64 on the device (in place, on st).
+void comm_min_u64(sc_ctx* ctx, uint64_t* d, size_t n, cudaStream_t st) {
+  if (ctx->comm_kind == 1) {
+    nccl_check(nccl().allReduce(d, d, n, ncclUint64, ncclMin, (ncclComm_t)ctx->nccl_comm, st),
+               "ncclAllReduce");
+    return;
+  }
+  // host transport: the caller's all-gather between the ranks
+  const int W = ctx->shard_world;
+  std::vector<uint64_t> mine(n), all(n * (size_t)W);
+  SCB_CUDA(cudaMemcpyAsync(mine.data(), d, n * 8, cudaMemcpyDeviceToHost, st));
+  SCB_CUDA(cudaStreamSynchronize(st));
+  if (ctx->comm_fn(ctx->comm_user, mine.data(), n * 8, all.data()) != 0)
+    fail(SC_ERR_INTERNAL, "the all-gather callback failed");
+  for (int r = 0; r < W; ++r)
+    for (size_t i = 0; i < n; ++i) mine[i] = std::min(mine[i], all[(size_t)r * n + i]);
+  SCB_CUDA(cudaMemcpyAsync(d, mine.data(), n * 8, cudaMemcpyHostToDevice, st));
+  SCB_CUDA(cudaStreamSynchronize(st));
+}
+
+// All-gather of `bytes` host bytes per rank into recv (world * bytes).
+void comm_allgather_host(sc_ctx* ctx, const void* send, size_t bytes, void* recv,
+                         cudaStream_t st) {
+  if (ctx->comm_kind == 1) {
+    const int W = ctx->shard_world;
+    ctx->comm_buf.ensure(bytes * (size_t)(W + 1));
+    uint8_t* d = ctx->comm_buf.as<uint8_t>();
+    SCB_CUDA(cudaMemcpyAsync(d, send, bytes, cudaMemcpyHostToDevice, st));
+    nccl_check(nccl().allGather(d, d + bytes, bytes, ncclUint8, (ncclComm_t)ctx->nccl_comm, st),
+               "ncclAllGather");
+    SCB_CUDA(cudaMemcpyAsync(recv, d + bytes, bytes * (size_t)W, cudaMemcpyDeviceToHost, st));
+    SCB_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  if (ctx->comm_fn(ctx->comm_user, send, bytes, recv) != 0)
+    fail(SC_ERR_INTERNAL, "the all-gather callback failed");
+}
 
 sc_status set_error(sc_status s, const std::string& m) {
   g_last_error = m;
@@ -831,6 +918,8 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
       uint64_t* frozen = ctx->seed_inc.as<uint64_t>() + (size_t)gi * L.fpw;
       SCB_CUDA(cudaMemcpyAsync(frozen, a.inc, L.fpw * sizeof(uint64_t),
                                cudaMemcpyDeviceToDevice, st));
+      // shards: every rank prunes phase B with the global seed incumbent
+      if (has_comm(ctx)) comm_min_u64(ctx, frozen, L.fpw, st);
       a.seed_inc = frozen;
       a.k_begin = seed_items * G;
       a.n_items = mine * G;
@@ -860,6 +949,35 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
                     step == 1 ? ctx->budget.as<int64_t>() + (size_t)gi * L.fpw : nullptr,
                     ctx->fin_scratch, st);
   }
+}
+
+// Shards: step 1's per-frame time bits (FrameBest::t, all ones when none)
+// gathered for the all-reduce, and step 2's budget keys from the global min.
+__global__ void k_tmin_gather(const FrameBest* __restrict__ fb, int frames, uint64_t* t) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < frames) t[f] = fb[f].found ? fb[f].t : ~0ull;
+}
+__global__ void k_budget_from_tmin(const uint64_t* __restrict__ t, int frames, double lambda,
+                                   const uint64_t* __restrict__ vals,
+                                   const uint32_t* __restrict__ nvals, size_t nr, int fpw,
+                                   int64_t* __restrict__ budget) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= frames) return;
+  const int g = f / fpw, slot = f % fpw;
+  int64_t key = -1;
+  if (t[f] != ~0ull) {
+    const double b = __dmul_rn(__longlong_as_double((long long)t[f]), __dadd_rn(1.0, lambda));
+    const uint64_t bits = (uint64_t)__double_as_longlong(b);
+    const uint64_t* fv = vals + ((size_t)g * fpw + slot) * nr;
+    uint32_t lo = 0, hi = nvals[f];
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (fv[mid] <= bits) lo = mid + 1;
+      else hi = mid;
+    }
+    key = b >= 0.0 ? (int64_t)lo - 1 : -1;
+  }
+  budget[(size_t)g * fpw + slot] = key;
 }
 
 // Device budget keys from caller t_min values (constrained_clustering with a
@@ -1102,8 +1220,22 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
                              cudaMemcpyDefault, s));
     enqueue_time_tables(ctx, g, L, false, s);
     SCB_CUDA(cudaEventRecord(ev[1], s));
-    if (do1) enqueue_step(ctx, g, cfg, plan, L, 1, true, s);
-    else upload_budgets(ctx, L, t_min_in, cfg.lambda, s);
+    if (do1) {
+      enqueue_step(ctx, g, cfg, plan, L, 1, true, s);
+      if (do2 && has_comm(ctx)) {  // step 2's budget from the global t_min
+        ctx->gtmin.ensure((size_t)frames * sizeof(uint64_t));
+        k_tmin_gather<<<(frames + 127) / 128, 128, 0, s>>>(ctx->frame_best.as<FrameBest>(), frames,
+                                                            ctx->gtmin.as<uint64_t>());
+        SCB_CUDA(cudaGetLastError());
+        comm_min_u64(ctx, ctx->gtmin.as<uint64_t>(), (size_t)frames, s);
+        k_budget_from_tmin<<<(frames + 127) / 128, 128, 0, s>>>(
+            ctx->gtmin.as<uint64_t>(), frames, cfg.lambda, ctx->vals.as<uint64_t>(),
+            ctx->nvals.as<uint32_t>(), L.nr, L.fpw, ctx->budget.as<int64_t>());
+        SCB_CUDA(cudaGetLastError());
+      }
+    } else {
+      upload_budgets(ctx, L, t_min_in, cfg.lambda, s);
+    }
     SCB_CUDA(cudaEventRecord(ev[2], s));
   };
   auto enqueue_side = [&] {
@@ -1276,6 +1408,16 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
     r.clustering_step_us = ctx->timings[3] / frames;
     r.search_time_us = (ctx->timings[2] + ctx->timings[3]) / frames;
   }
+  if (has_comm(ctx)) {  // the library's exchange: every rank returns the merged results
+    const int W = ctx->shard_world;
+    std::vector<sc_shard_best> mine(frames), all((size_t)W * frames);
+    for (int st = 1; st <= 2; ++st) {
+      if (st == 1 ? !do1 : !do2) continue;
+      export_shards(ctx, st, frames, mine.data());
+      comm_allgather_host(ctx, mine.data(), mine.size() * sizeof(sc_shard_best), all.data(), s);
+      merge_shards(st, W, frames, all.data(), out);
+    }
+  }
 }
 
 }  // namespace
@@ -1309,6 +1451,9 @@ sc_ctx::~sc_ctx() {
     if (e) cudaEventDestroy(e);
   for (auto& e : ev_s2)
     if (e) cudaEventDestroy(e);
+  if (comm_kind == 1 && nccl_comm) nccl().commDestroy((ncclComm_t)nccl_comm);
+  comm_buf.release();
+  gtmin.release();
   if (stream) cudaStreamDestroy(stream);
   if (stream2) cudaStreamDestroy(stream2);
 }
@@ -1728,6 +1873,15 @@ sc_status sc_shard_export(sc_ctx* ctx, int32_t step, int32_t frames, sc_shard_be
   return guarded([&] {
     if (!ctx || !out) fail(SC_ERR_USAGE, "NULL argument");
     if (step != 1 && step != 2) fail(SC_ERR_USAGE, "step must be 1 or 2");
+    export_shards(ctx, step, frames, out);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+void export_shards(sc_ctx* ctx, int step, int frames, sc_shard_best* out) {
+  {
     const auto& v = ctx->last_best[step - 1];
     if ((int)v.size() < frames) fail(SC_ERR_USAGE, "no step result for that many frames");
     for (int f = 0; f < frames; ++f) {
@@ -1745,6 +1899,64 @@ sc_status sc_shard_export(sc_ctx* ctx, int32_t step, int32_t frames, sc_shard_be
       s.leaves = b.scored / (uint64_t)ctx->last_fpw;
       layout_from_snap(b, SC_MAX_SLICES, &s.layout);
     }
+  }
+}
+}  // namespace
+
+extern "C" {
+
+sc_status sc_comm_unique_id(void* id_out) {
+  return guarded([&] {
+    if (!id_out) fail(SC_ERR_USAGE, "NULL argument");
+    static_assert(sizeof(ncclUniqueId) == SC_COMM_ID_BYTES, "NCCL unique id size");
+    ncclUniqueId id;
+    nccl_check(nccl().getUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+sc_status sc_comm_detach(sc_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) fail(SC_ERR_USAGE, "NULL argument");
+    if (ctx->comm_kind == 1 && ctx->nccl_comm) nccl().commDestroy((ncclComm_t)ctx->nccl_comm);
+    ctx->nccl_comm = nullptr;
+    ctx->comm_kind = 0;
+    ctx->comm_fn = nullptr;
+    ctx->comm_user = nullptr;
+    ctx->shard_rank = 0;
+    ctx->shard_world = 1;
+  });
+}
+
+sc_status sc_comm_init_nccl(sc_ctx* ctx, int32_t rank, int32_t world, const void* unique_id) {
+  return guarded([&] {
+    if (!ctx || !unique_id) fail(SC_ERR_USAGE, "NULL argument");
+    if (world < 1 || rank < 0 || rank >= world) fail(SC_ERR_CONFIG, "bad shard rank/world");
+    SCB_CUDA(cudaSetDevice(ctx->device));
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    nccl_check(nccl().commInitRank(&comm, world, id, rank), "ncclCommInitRank");
+    if (ctx->comm_kind == 1 && ctx->nccl_comm) nccl().commDestroy((ncclComm_t)ctx->nccl_comm);
+    ctx->nccl_comm = comm;
+    ctx->comm_kind = 1;
+    ctx->shard_rank = rank;
+    ctx->shard_world = world;
+  });
+}
+
+sc_status sc_comm_init_callback(sc_ctx* ctx, int32_t rank, int32_t world, sc_allgather_fn fn,
+                                void* user) {
+  return guarded([&] {
+    if (!ctx || !fn) fail(SC_ERR_USAGE, "NULL argument");
+    if (world < 1 || rank < 0 || rank >= world) fail(SC_ERR_CONFIG, "bad shard rank/world");
+    if (ctx->comm_kind == 1 && ctx->nccl_comm) nccl().commDestroy((ncclComm_t)ctx->nccl_comm);
+    ctx->nccl_comm = nullptr;
+    ctx->comm_kind = 2;
+    ctx->comm_fn = fn;
+    ctx->comm_user = user;
+    ctx->shard_rank = rank;
+    ctx->shard_world = world;
   });
 }
 
@@ -1752,6 +1964,18 @@ sc_status sc_shard_merge(int32_t step, int32_t world, int32_t frames,
                          const sc_shard_best* gathered, sc_search_result* inout) {
   return guarded([&] {
     if (!gathered || !inout) fail(SC_ERR_USAGE, "NULL argument");
+    merge_shards(step, world, frames, gathered, inout);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// The first-in-order winner of every frame over the ranks' records
+// (rank-major), counts summed; throws NoCandidateError when no rank has one.
+void merge_shards(int step, int world, int frames, const sc_shard_best* gathered,
+                  sc_search_result* inout) {
+  {
     for (int f = 0; f < frames; ++f) {
       int win = -1;
       unsigned __int128 total = 0;
@@ -1792,8 +2016,11 @@ sc_status sc_shard_merge(int32_t step, int32_t world, int32_t frames,
       }
       r.candidates_evaluated = r.candidates_step1 + r.candidates_step2;
     }
-  });
+  }
 }
+}  // namespace
+
+extern "C" {
 
 sc_status sc_validate_partition(sc_ctx* ctx, const sc_grid* grid, int32_t n_tile_cols,
                                 const int32_t* tile_col_widths, int32_t n_tile_rows,

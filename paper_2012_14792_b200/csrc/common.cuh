@@ -248,6 +248,13 @@ struct sc_ctx {
   scb::Plan* s2_plan = nullptr;
   double timings[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int shard_rank = 0, shard_world = 1;
+  // the exchange between shards when the library owns it (sc_comm_init_*):
+  // 0 none (per-shard results, merged by the caller), 1 NCCL, 2 host callback
+  int comm_kind = 0;
+  void* nccl_comm = nullptr;  // ncclComm_t
+  sc_allgather_fn comm_fn = nullptr;
+  void* comm_user = nullptr;
+  scb::DevBuf comm_buf, gtmin;
   // staging / tables
   scb::DevBuf luma, records, est, sat, rect_t, rect_s, rt_search, rs_search, usat;
   // rt_search: the time keys [groups][rt | rts][rect][fpw] (rank.cu, split table)

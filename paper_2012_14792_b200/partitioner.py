@@ -25,8 +25,9 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from ._abi import (SC_ORIGIN_UNIFORM, CtuRecord, Grid, Layout, PartitionC, PartitionStats, Rect,
-                   SearchCfg, SearchResult, ShardBest, SlicecraftError, check, lib)
+from ._abi import (ALLGATHER_FN, SC_COMM_ID_BYTES, SC_ORIGIN_UNIFORM, CtuRecord, Grid, Layout,
+                   PartitionC, PartitionStats, Rect, SearchCfg, SearchResult, ShardBest,
+                   SlicecraftError, check, lib)
 
 COLUMN_SPLIT, UNIFORM_ONLY = 0, 1
 COVERAGE_REFERENCE, COVERAGE_COVERING = 0, 1
@@ -294,6 +295,29 @@ class Partitioner:
     def set_shard(self, rank: int, world: int) -> None:
         check(lib().sc_ctx_set_shard(self._h, rank, world))
 
+    def comm_init_nccl(self, rank: int, world: int, unique_id: bytes) -> None:
+        """Shard over `world` GPUs with the library's own NCCL exchange
+        (sc_comm_init_nccl): every search call returns the merged results."""
+        buf = (C.c_uint8 * SC_COMM_ID_BYTES).from_buffer_copy(unique_id)
+        check(lib().sc_comm_init_nccl(self._h, rank, world, C.cast(buf, C.c_void_p)))
+
+    def comm_init_callback(self, rank: int, world: int, allgather) -> None:
+        """Shard with a host transport: allgather(send: bytes) -> bytes
+        (world * len(send), rank order), e.g. torch.distributed gloo."""
+        def fn(_user, send, nbytes, recv):
+            try:
+                got = allgather(C.string_at(send, nbytes))
+                C.memmove(recv, got, len(got))
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failure
+                return 1
+        self._comm_fn = ALLGATHER_FN(fn)  # keep the trampoline alive
+        check(lib().sc_comm_init_callback(self._h, rank, world, self._comm_fn, None))
+
+    def comm_detach(self) -> None:
+        check(lib().sc_comm_detach(self._h))
+
+
     # ---- texture map --------------------------------------------------------
     def timings(self) -> dict:
         """Device time (us, CUDA events) of the phases of the last search call."""
@@ -541,3 +565,10 @@ def read_yuv_luma(path: str, width: int, height: int, bit_depth: int, first_poc:
 def texture_validate(grid: CtuGrid, records: np.ndarray) -> None:
     rec = np.ascontiguousarray(records)
     check(lib().sc_texture_validate(C.byref(grid.c()), _ptr(rec)))
+
+
+def comm_unique_id() -> bytes:
+    """An NCCL unique id for sc_comm_init_nccl (rank 0 makes it, all ranks use it)."""
+    buf = (C.c_uint8 * SC_COMM_ID_BYTES)()
+    check(lib().sc_comm_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)

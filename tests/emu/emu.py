@@ -18,8 +18,9 @@ class Emu:
             raise RuntimeError(f"{SO} missing: make -C tests/emu")
         self.L = C.CDLL(SO)
         I, D, P = C.c_int, C.c_double, C.c_void_p
+        self.SEED_CB = C.CFUNCTYPE(None, C.POINTER(C.c_uint64), C.c_int)
         self.L.emu_search.argtypes = [I, I, I, D, I, I, I, I, I, P, P, P, I, C.c_size_t, I, I, P, P, P, P,
-                                      P, P, P, I, I, I]
+                                      P, P, P, I, I, I, self.SEED_CB]
 
     def trace_search(self, cols, rows, n, k, max_cols, coverage, rect_time, item_target=16):
         """Exhaustive step 1 through the host build of the candidate trace
@@ -61,7 +62,9 @@ class Emu:
 
     def search(self, cols, rows, n, k, max_cols, coverage, step, rect_time, rect_sse=None,
                budget=None, warps=3, item_target=16, offset=0, stride=1, full=False, prune=0,
-               order=0, split=1, split_depth=1):
+               order=0, split=1, split_depth=1, seed_allreduce=None):
+        """seed_allreduce(list[int]) -> list[int]: the shards' all-reduce-min
+        of the frozen seed incumbents (pruned step 1), or None."""
         rt = np.ascontiguousarray(rect_time, dtype=np.float64)
         F = rt.shape[0]
         rs = None if rect_sse is None else np.ascontiguousarray(rect_sse, dtype=np.float64)
@@ -77,11 +80,22 @@ class Emu:
                                _p(b),
                                warps, item_target, offset, stride, _p(t), _p(sse), _p(cnt),
                                _p(snap), _p(found), _p(item), _p(ordn), order, split,
-                               split_depth)
+                               split_depth, self._seed_cb(seed_allreduce))
         assert st == 0
         if full:
             return t, sse, cnt, snap, found, item, ordn
         return t, sse, cnt, snap, found
+
+    def _seed_cb(self, fn):
+        if fn is None:
+            return self.SEED_CB()
+
+        def cb(ptr, n):
+            vals = fn([ptr[i] for i in range(n)])
+            for i in range(n):
+                ptr[i] = vals[i]
+        self._cb_keep = self.SEED_CB(cb)
+        return self._cb_keep
 
     @staticmethod
     def slices(snap_row, n, rows):

@@ -21,7 +21,8 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
                           int warps, size_t item_target, int item_offset, int item_stride,
                           double* out_t, double* out_sse, uint64_t* out_count,
                           uint8_t* out_snap /*[F][96]*/, int* out_found, uint64_t* out_item,
-                          uint64_t* out_ord, int order_mode, int split_g, int split_depth) {
+                          uint64_t* out_ord, int order_mode, int split_g, int split_depth,
+                          void (*seed_allreduce)(uint64_t* inc, int n)) {
   // order_mode (exhaustive step 1 only, like api.cu's cost schedule): 0 the
   // enumeration order, 1 reversed, 2 a fixed pseudo-random permutation
   if (frames < 1 || frames > 32) return 1;
@@ -173,6 +174,8 @@ extern "C" int emu_search(int cols, int rows, int n, double k, int max_tile_cols
     const int part = (int)(su % (size_t)G);
     if (prune && step == 1 && kk == seed_local * (size_t)G && seed_local > 0) {  // phase B
       frozen = inc;
+      // shards (api.cu sc_comm_*): the frozen incumbent is the global minimum
+      if (seed_allreduce) seed_allreduce(frozen.data(), fpw);
       e.seed_inc = frozen.data();
     }
     const int wp = (int)(kk % (size_t)warps);

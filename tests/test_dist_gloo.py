@@ -1,11 +1,13 @@
-"""Multi-rank path on CPU (gloo, world_size 2).
+"""Multi-rank path on CPU (gloo, world_size 2, 4 and 8).
 
 Candidate-space sharding (cfg4/cfg5 style): rank r scores the work items
 r, r+w, r+2w, ...; each rank exports one shard-best record per frame
 (sc_shard_best), the records are all-gathered and sc_shard_merge picks the
 first-in-order winner and sums the counts.  Here each rank's shard is scored
 by the host emulator of the kernel walk (the GPU kernel is the same code);
-the merged result must equal the single-process oracle bit for bit.
+the merged result must equal the single-process oracle bit for bit.  In the
+pruned mode the frozen seed incumbents are all-reduced (min) between phase A
+and phase B, as the library's exchange does (api.cu sc_comm_*).
 
 Frame-batch sharding (bench.py's weak scaling) needs no collective beyond
 the barrier; it is covered by the per-frame independence check below.
@@ -58,9 +60,15 @@ def _worker(rank, world, port, step, prune, out_dir):
     if step == 2:
         budget = np.array([o.search(W, H, 64, est[f], recs[f], n, lam, k, mc, 0, 1)[1].t_min_us *
                            (1.0 + lam) for f in range(F)])
+    def seed_allreduce(vals):  # u64 min through an order-preserving i64 map
+        t = torch.tensor([(v ^ (1 << 63)) - (1 << 64) if v ^ (1 << 63) >= (1 << 63)
+                          else v ^ (1 << 63) for v in vals], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return [(int(x) & ((1 << 64) - 1)) ^ (1 << 63) for x in t.tolist()]
     t, sse, cnt, snap, found, item, ordn = e.search(cols, rows, n, k, mc, 0, step, rt, rs, budget,
                                                     item_target=64, offset=rank, stride=world,
-                                                    full=True, prune=prune)
+                                                    full=True, prune=prune,
+                                                    seed_allreduce=seed_allreduce if prune else None)
     mine = (ShardBest * F)()
     for f in range(F):
         s = mine[f]
@@ -114,11 +122,12 @@ def _worker(rank, world, port, step, prune, out_dir):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("prune", [0, 1])
 @pytest.mark.parametrize("step", [1, 2])
-def test_candidate_space_sharding_gloo(tmp_path, emu, step, prune):
+def test_candidate_space_sharding_gloo(tmp_path, emu, step, prune, world):
     port = _free_port()
-    mp.spawn(_worker, args=(2, port, step, prune, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, port, step, prune, str(tmp_path)), nprocs=world, join=True)
     res = open(tmp_path / f"step{step}_{prune}.txt").read().split("\n")
     assert len(res) == 4 and all(line.endswith(" 1") for line in res), res
 
