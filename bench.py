@@ -414,14 +414,15 @@ def run_ours(args):
 
 
 def run_candidates(args):
-    """--shard candidates: every rank holds the SAME frames and walks the work
-    items rank, rank + N, ... of each frame's candidate space
-    (sc_ctx_set_shard); after each step the ranks exchange one sc_shard_best
-    record per frame (all-gather, NCCL over NVLink) and sc_shard_merge picks
-    the first-in-order winner, so step 2 runs under the global t_min.  Total
-    work is fixed as N grows: strong scaling.  One step = K1 over the batch +
-    step 1 + exchange + step 2 + exchange, timed with CUDA events between
-    barriers, max over ranks."""
+    """--shard candidates: every rank holds the SAME frames and the library
+    shards each frame's candidate space over the ranks with its own exchange
+    (sc_comm_init_nccl: NCCL over NVLink; the gloo test backend uses the host
+    callback transport): after step 1 the global t_min (all-reduce min) sets
+    step 2's budget, pruned shards share their seed incumbents, and the shard
+    bests are all-gathered and merged inside the call, so every rank returns
+    the global result.  Total work is fixed as N grows: strong scaling.  One
+    step = one sc_partition_frames call (K1 + tables + both steps + the
+    exchanges), timed with CUDA events between barriers, max over ranks."""
     import ctypes as C
 
     import torch
@@ -429,7 +430,7 @@ def run_candidates(args):
     from paper_2012_14792_b200 import Partitioner, lib
     from paper_2012_14792_b200._abi import SearchResult, check
     from paper_2012_14792_b200 import workloads as wl
-    from paper_2012_14792_b200.partitioner import shard_merge
+    from paper_2012_14792_b200.partitioner import comm_unique_id
 
     rank, world, local = dist_env()
     backend = os.environ.get("SLICECRAFT_BENCH_BACKEND", "nccl")
@@ -446,60 +447,41 @@ def run_candidates(args):
     cfg = w.cfg(mode=args.mode)
     luma_h, est_h = make_inputs(w, 0, F)  # the same frames on every rank
     luma_d, est_d = luma_h.cuda(), est_h.cuda()
-    rec_d = torch.empty(F * g.cell_count() * 24, dtype=torch.uint8, device="cuda")
     part = Partitioner(local)
     stream = torch.cuda.current_stream()
     check(lib().sc_ctx_set_stream(part._h, C.c_void_p(stream.cuda_stream)))
-    part.set_shard(rank, world)
+    if world > 1:
+        if backend == "nccl":
+            box = [comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            part.comm_init_nccl(rank, world, box[0])
+        else:
+            def gather(blob: bytes) -> bytes:
+                t = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+                out = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(out, t)
+                return b"".join(x.numpy().tobytes() for x in out)
+            part.comm_init_callback(rank, world, gather)
     gc, cc = g.c(), cfg.c()
     pitch, fstride = w.width * bps, w.width * w.height * bps
-
-    def gather(blob: bytes) -> bytes:
-        if world == 1:
-            return blob
-        t = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
-        if backend == "nccl":
-            t = t.cuda()
-        out = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(out, t)
-        return b"".join(x.cpu().numpy().tobytes() for x in out)
-
-    def fresh():
-        r = (SearchResult * F)()
-        for f in range(F):
-            r[f].argmin.n_slices = w.n_slices
-            r[f].best.n_slices = w.n_slices
-        return r
+    res = (SearchResult * F)()
 
     def step():
-        check(lib().sc_texture_moments(part._h, C.c_void_p(luma_d.data_ptr()), bps, w.width,
-                                       w.height, pitch, fstride, w.ctu, F,
-                                       C.c_void_p(rec_d.data_ptr())))
-        r1 = fresh()
-        check(lib().sc_min_time_search(part._h, C.byref(gc), C.byref(cc),
-                                       C.c_void_p(est_d.data_ptr()), F, C.cast(r1, C.c_void_p)))
-        m1 = fresh()
-        shard_merge(1, world, F, gather(bytes(part.shard_export(1, F))), m1)
-        tmin = np.array([m1[f].t_min_us for f in range(F)], dtype=np.float64)
-        r2 = fresh()
-        check(lib().sc_constrained_clustering(part._h, C.byref(gc), C.byref(cc),
-                                              C.c_void_p(est_d.data_ptr()),
-                                              C.c_void_p(rec_d.data_ptr()),
-                                              C.c_void_p(tmin.ctypes.data), F,
-                                              C.cast(r2, C.c_void_p)))
-        m2 = fresh()
-        shard_merge(2, world, F, gather(bytes(part.shard_export(2, F))), m2)
-        return m1, m2
+        check(lib().sc_partition_frames(part._h, C.byref(gc), C.byref(cc),
+                                        C.c_void_p(luma_d.data_ptr()), bps, pitch, fstride,
+                                        C.c_void_p(est_d.data_ptr()), F, None,
+                                        C.cast(res, C.c_void_p)))
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     for _ in range(max(args.warmup, 1)):
-        m1, m2 = step()
-    cands = sum((m1[f].candidates_step1 | (m1[f].candidates_step1_hi << 64)) +
-                (m2[f].candidates_step2 | (m2[f].candidates_step2_hi << 64)) for f in range(F))
-    digest = hash(tuple((m2[f].t_best_us, m2[f].sse_best) for f in range(F)))
+        step()
+    c12 = [((r.candidates_step1 | (r.candidates_step1_hi << 64)),
+            (r.candidates_step2 | (r.candidates_step2_hi << 64))) for r in res]
+    cands = sum(a + b for a, b in c12)
+    digest = hash(tuple((r.t_best_us, r.sse_best) for r in res))
     clocks = Clocks(local)
     barrier()
     torch.cuda.synchronize()
@@ -521,13 +503,10 @@ def run_candidates(args):
         "metric": METRIC, "value": cands / (ms / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u64/f64", "data": "synthetic (seeded; SURVEY.md \u00a78d generator)",
-        "config": {"workload": w.name, "frames": F, "frame": f"{w.width}x{w.height}",
-                   "grid": f"{g.cols}x{g.rows}", "n_slices": w.n_slices,
-                   "max_tile_cols": w.max_tile_cols,
-                   "mode": "pruned" if args.mode else "exhaustive",
-                   "parallelism": f"candidate space sharded over {world} rank(s), "
-                                  "per-frame argmin all-gathered after each step"},
+        "dtype": "u64/f64", "data": DATA, "config": workload_config(w, sorted(set(c12))),
+        "parallelism": f"candidate space sharded over {world} rank(s), the library's own "
+                       "exchange (t_min all-reduce, shard bests all-gathered and merged)",
+        "search_mode": "pruned" if args.mode else "exhaustive",
         "frames_per_s": F / (ms / 1e3),
         "result_digest": digest,
         "clocks": ck,
