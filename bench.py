@@ -197,7 +197,7 @@ def kernel_src_sha():
     """Hash of the search-kernel sources an ncu instruction count belongs to."""
     import hashlib
     h = hashlib.sha256()
-    for f in ("search_walk.cuh", "search.cu", "rank.cu", "plan.h"):
+    for f in ("search_walk.cuh", "search.cu", "rank.cu", "plan.h", "trace.cuh", "trace.cu"):
         h.update(open(os.path.join(ROOT, "paper_2012_14792_b200", "csrc", f), "rb").read())
     return h.hexdigest()[:16]
 
@@ -345,10 +345,12 @@ def run_ours(args):
             clk = ck.get("sm_mhz") or p.get("sm_mhz_ncu") or 1965.0
             sms = torch.cuda.get_device_properties(local).multi_processor_count
             peak = sms * 4 * clk * 1e6 / 1e9  # G warp-instr / s at the measured clock
-            # dominant kernel: the step-1 walk (every candidate's time); the
-            # step-1 phase is that launch plus its few-us finalize
+            # dominant kernel: the step-1 trace walk (every candidate's time);
+            # the step-1 phase is that launch plus its finalize (~15 us)
             ach = p["warp_inst_step1"] / (s1_us * 1e-6) / 1e9
-            issue = {"bound": "alu", "kernel": "k_search_head<FPW> (exhaustive step-1 walk)",
+            issue = {"bound": "alu",
+                     "kernel": "k_trace_walk<FPW> (exhaustive step 1: the candidate-trace "
+                               "interpreter, trace.cu)",
                      "achieved": round(ach, 2), "peak": round(peak, 2),
                      "unit": "Gwarp-inst/s", "frac": round(ach / peak, 4),
                      "traffic": p.get("dram_bytes_per_launch"),

@@ -593,16 +593,20 @@ bool schedule_enabled() {
 
 // After a measuring call: items by decreasing measured walk cost (ties by
 // index), uploaded for the next calls.
+// (A shard orders its own items, rank, rank + world, ...: LPT per rank.)
 void finish_schedule(Plan* p) {
   if (p->order_state != 1) return;
   const size_t n = p->items.size();
-  std::vector<uint32_t> cost(n), order(n);
+  const uint32_t rank = p->order_rank, world = p->order_world;
+  std::vector<uint32_t> cost(n), order;
   SCB_CUDA(cudaMemcpy(cost.data(), p->d_cost.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  for (size_t i = 0; i < n; ++i) order[i] = (uint32_t)i;
+  for (size_t i = rank; i < n; i += world) order.push_back((uint32_t)i);
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
-  p->d_order.ensure(n * sizeof(uint32_t));
-  SCB_CUDA(cudaMemcpy(p->d_order.p, order.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  p->d_order.ensure(std::max<size_t>(1, order.size()) * sizeof(uint32_t));
+  if (!order.empty())
+    SCB_CUDA(cudaMemcpy(p->d_order.p, order.data(), order.size() * sizeof(uint32_t),
+                        cudaMemcpyHostToDevice));
   p->order_state = 2;
 }
 
@@ -823,10 +827,14 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
   const uint32_t rank = (uint32_t)ctx->shard_rank, world = (uint32_t)ctx->shard_world;
   const uint32_t mine = total > rank ? (total - rank + world - 1) / world : 0;
   FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)(step - 1) * L.groups * L.fpw;
-  const bool sched = step == 1 && !prune && world == 1 && schedule_enabled();
+  const bool sched = step == 1 && !prune && schedule_enabled();
+  if (sched && plan->order_state == 2 && (plan->order_rank != rank || plan->order_world != world))
+    plan->order_state = 0;  // another shard layout: measure again
   if (sched && plan->order_state != 2) {
     plan->d_cost.ensure(plan->items.size() * sizeof(uint32_t));
     plan->order_state = 1;
+    plan->order_rank = rank;
+    plan->order_world = world;
   }
   const int rstride = std::min(cfg.n_slices, g.rows) + 1;
   const size_t lb_per_group = (size_t)n_xw(g.cols) * rstride * L.fpw;

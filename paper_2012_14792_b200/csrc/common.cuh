@@ -143,6 +143,7 @@ struct Plan {
   // exhaustive step 1 schedule: the first call measures each item's walk
   // cost, later calls take the items in decreasing cost (shorter tail)
   int order_state = 0;        // 0: measure, 1: measured (copy pending), 2: ordered
+  uint32_t order_rank = 0, order_world = 1;  // the shard the order belongs to
   DevBuf d_order, d_cost;
   unsigned __int128 count = 0;
   DevBuf d_items, d_bmax;

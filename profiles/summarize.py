@@ -66,9 +66,12 @@ def main():
                 v, u, _ = m[k]
                 lines.append(f"- {k}: {v} {u}")
         lines.append("")
-        if "k_search" in kname:
-            mt = re.search(r"k_search<[^,]*,\s*(?:\(int\))?(\d)", kname)
-            step = mt.group(1) if mt else "1"
+        if "k_search" in kname or "k_trace_walk" in kname:
+            if "k_trace_walk" in kname:  # the trace interpreters: walk = step 1, walk2 = step 2
+                step = "2" if "k_trace_walk2" in kname else "1"
+            else:
+                mt = re.search(r"k_search<[^,]*,\s*(?:\(int\))?(\d)", kname)
+                step = mt.group(1) if mt else "1"
             try:
                 issue[f"warp_inst_step{step}"] = float(m["Executed Instructions"][0].replace(",", ""))
                 issue[f"issue_active_pct_step{step}"] = float(m["Issue Slots Busy"][0])
@@ -87,7 +90,7 @@ def main():
                 d = json.load(open(tj)) if os.path.exists(tj) else {}
                 d[os.environ.get("CFG", "cfg3")] = a + b
                 json.dump(d, open(tj, "w"), indent=1)
-            if "k_search" in k:
+            if "k_search" in k or "k_trace_walk" in k:
                 issue.setdefault("dram_bytes_per_launch", a + b)
     except Exception as e:  # raw page layout differs across ncu versions
         lines.append(f"(raw dram metrics unavailable: {e})")
