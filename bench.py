@@ -193,6 +193,34 @@ def make_inputs(w, rank, frames, pinned=True):
     return luma_t, est_t
 
 
+def count_kernel_launches(fn):
+    """Kernels launched by one untimed fn() call, counted from the CUDA
+    activity trace (CUPTI via torch.profiler sees every kernel of the process,
+    including the ones the C-ABI library launches on its own streams).
+    Returns (count, {name: n}) or (None, {}) when the profiler is unusable."""
+    import tempfile
+    from torch.profiler import ProfilerActivity, profile
+    try:
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "trace.json")
+            prof.export_chrome_trace(path)
+            ev = json.load(open(path)).get("traceEvents", [])
+        names = {}
+        for e in ev:
+            if e.get("cat") == "kernel":
+                n = e.get("name", "?")
+                n = n.split("(")[0].replace("void ", "")[:60]
+                names[n] = names.get(n, 0) + 1
+        total = sum(names.values())
+        return (total if total > 0 else None), names
+    except Exception:
+        return None, {}
+
+
 def kernel_src_sha():
     """Hash of the search-kernel sources an ncu instruction count belongs to."""
     import hashlib
@@ -313,6 +341,10 @@ def run_ours(args):
     barrier()
     ms_e2e = max_over_ranks(e2.elapsed_time(e3)) / args.steps
 
+    # launches per step, measured on one more (untimed) device-resident call
+    n_launch, launch_names = count_kernel_launches(lambda: call(luma_d.data_ptr(),
+                                                                 est_d.data_ptr()))
+
     total_cands = cands * world
     value = total_cands / (ms / 1e3)
     e2e = total_cands / (ms_e2e / 1e3)
@@ -394,13 +426,11 @@ def run_ours(args):
         "roofline_texture": tex_roof,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": luma_bytes + F * g.cell_count() * 8,
                 "d2h_bytes_per_step": 2 * 32 * ((F + 31) // 32) * 168, "ms_per_step": ms_e2e},
-        # per call (profiles/r01f_cfg3_launches.md, 33 launches): K1, 2x(K2 +
-        # K3), the rank pipeline (6 own + 13 CUB launches), split table; per
-        # frame group: column bounds, step-1 walk + finalize, item filter (own
-        # + 2 CUB select launches), step-2 walk + finalize; pruned mode adds the
-        # seed-phase walk and the phase-B item filter (+4); the device
-        # post-check of the returned partitions adds one launch per step
-        "gpu_launches": args.steps * (27 + (8 + 4 * args.mode) * ((F + 31) // 32)),
+        # kernels per step counted from the CUDA activity trace of one extra
+        # untimed call (every kernel is the library's own or a CUB kernel
+        # instantiated inside it), times the timed steps
+        "gpu_launches": (args.steps * n_launch) if n_launch else None,
+        "gpu_launches_per_step": launch_names or None,
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_extra and args.mode == 0:
