@@ -92,17 +92,52 @@ struct TraceArgs {
   uint64_t* lanes;            // [warps * 32] x {time key (u64), ordinal}
 };
 
+// keys + off as one IMAD.WIDE (off = an op's pre-scaled key offset)
+__device__ __forceinline__ const uint32_t* key_at(const uint32_t* base, uint32_t off) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(r) : "r"(off), "l"(base));
+  return reinterpret_cast<const uint32_t*>(r);
+}
+
+// min over `cnt` consecutive split-table keys of one lane (stride FPW words)
+template <int FPW>
+__device__ __forceinline__ tkey leaf_min(const uint32_t* __restrict__ pv, int cnt) {
+#define LD(i) __ldg(pv + (i) * FPW)
+  // most leaves hold <= 8 heights: a three-level branch tree (warp-uniform)
+  // into straight-line loads
+  if (cnt <= 4) {
+    if (cnt <= 2) {
+      if (cnt == 1) return LD(0);
+      return kmin(LD(0), LD(1));
+    }
+    if (cnt == 3) return umin3(LD(0), LD(1), LD(2));
+    return kmin(umin3(LD(0), LD(1), LD(2)), LD(3));
+  }
+  if (cnt <= 6) {
+    if (cnt == 5) return umin3(umin3(LD(0), LD(1), LD(2)), LD(3), LD(4));
+    return kmin(umin3(LD(0), LD(1), LD(2)), umin3(LD(3), LD(4), LD(5)));
+  }
+  if (cnt == 7) return umin3(umin3(LD(0), LD(1), LD(2)), umin3(LD(3), LD(4), LD(5)), LD(6));
+  tkey m = umin3(umin3(LD(0), LD(1), LD(2)), umin3(LD(3), LD(4), LD(5)), kmin(LD(6), LD(7)));
+#pragma unroll 1
+  for (int h = 8; h < cnt; ++h) m = kmin(m, LD(h));
+  return m;
+#undef LD
+}
+
 template <int FPW>
 __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
   constexpr int J = 32 / FPW;
+  constexpr int SH = FPW == 32 ? 0 : FPW == 16 ? 1 : FPW == 8 ? 2 : FPW == 4 ? 3 : FPW == 2 ? 4 : 5;
   extern __shared__ uint32_t tr_sm[];
   __shared__ uint32_t s_pos[256], s_hit[256];  // the best's LEAF op and height (rare writes)
   __shared__ uint64_t s_red[2][256];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int f = lane % FPW, slot = lane / FPW;
   uint32_t* P = tr_sm + (size_t)wib * a.depth_cap * 32 + lane;  // P[d] at P[d * 32]
+  // rt | rts of this lane's frame: an op's key is keys[(its offset field) >> SH]
   const uint32_t* __restrict__ keys = a.keys + f;
-  const uint32_t* __restrict__ rts = a.keys + (size_t)a.nr * FPW + f;
+  asm volatile("" : "+l"(keys));  // keep the per-lane base in registers (no re-derivation per op)
   // lane state in registers: best key, its global ordinal (the trace holds
   // < 2^31 candidates) and the tie threshold; the best's op position and
   // height go to shared memory only when the best changes
@@ -121,25 +156,33 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
     // ties: a candidate of this chunk precedes the lane's best iff the best
     // comes from a later ordinal; inside the chunk ordinals only grow
     tkey bcmp = (best != kKeyInf && best_ord > ord) ? best + 1 : best;
-    int ld = 0;
-    for (uint32_t p0 = b; p0 < e; p0 += 32) {
+    // P[0] and P[ld] of the current path live in registers (P0, Pt): a PUSHL
+    // reads P[ld - 1] (at Pl1) and leaves P[ld] in Pt for its LEAF(s)
+    tkey P0 = 0, Pt = 0;
+    const uint32_t* Pl1 = P;
+    int nbw = 32;
+    for (uint32_t p0 = b; p0 < e; p0 += (uint32_t)nbw) {
       const uint32_t mine = p0 + lane < e ? __ldg(a.ops + p0 + lane) : 0u;
-      const int nb = (int)min(32u, e - p0);
+      int nb = (int)min(32u, e - p0);
+      // a PUSHL and its LEAF (the next op) stay in one fetch: a window that
+      // would end on a PUSHL ends one op earlier
+      if (tr_code(__shfl_sync(0xffffffffu, mine, nb - 1)) == kOpPushL) --nb;
+      nbw = nb;
 #pragma unroll 1
       for (int q = 0; q < nb; ++q) {
-        const uint32_t op = __shfl_sync(0xffffffffu, mine, q);
-        const uint32_t code = op >> 30;
-        if (code == kOpPush) {
-          const uint32_t d = (op >> 24) & 63u;
-          const uint32_t v = __ldg(keys + (op & kTrKeyMask) * FPW);
-          P[(d + 1) * 32] = kmax(P[d * 32], v);
-        } else if (code == kOpLeaf) {
-          const int cnt = (int)((op >> 22) & 255u);
-          const tkey Pl = P[ld * 32];
+        uint32_t op = __shfl_sync(0xffffffffu, mine, q);
+        uint32_t code = tr_code(op);
+        if (__builtin_expect(code == kOpPushL, 1)) {
+          Pt = kmax(*Pl1, __ldg(key_at(keys, tr_koff32(op) >> SH)));
+          op = __shfl_sync(0xffffffffu, mine, ++q);  // a PUSHL's next op is its LEAF
+          code = kOpLeaf;
+        }
+        if (code == kOpLeaf) {
+          const int cnt = tr_leaf_cnt(op);
           if (cnt == 0) {  // the skeleton's single candidate
-            if (slot == 0 && Pl < bcmp) {
-              best = Pl;
-              bcmp = Pl;
+            if (slot == 0 && Pt < bcmp) {
+              best = Pt;
+              bcmp = Pt;
               best_ord = ord;
               s_pos[threadIdx.x] = p0 + q;
               s_hit[threadIdx.x] = 0;
@@ -147,25 +190,19 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
             ord += 1;
             continue;
           }
-          const uint32_t* pv = rts + (op & kTrIdxMask) * FPW;
+          const uint32_t* pv = key_at(keys, tr_koff32(op) >> SH);
           tkey m;
           if (J == 1) {
-            // most leaves hold <= 4 heights: predicated loads, then a loop
-            m = umin3(__ldg(pv), cnt > 1 ? __ldg(pv + FPW) : kKeyInf,
-                      cnt > 2 ? __ldg(pv + 2 * FPW) : kKeyInf);
-            m = cnt > 3 ? kmin(m, __ldg(pv + 3 * FPW)) : m;
-#pragma unroll 1
-            for (int h = 4; h < cnt; h += 2)
-              m = umin3(m, __ldg(pv + h * FPW), h + 1 < cnt ? __ldg(pv + (h + 1) * FPW) : kKeyInf);
+            m = leaf_min<FPW>(pv, cnt);
           } else {
             m = kKeyInf;
             for (int h = slot; h < cnt; h += J) m = kmin(m, __ldg(pv + h * FPW));
           }
-          if (kmax(Pl, m) < bcmp) {  // replay in order: the first minimum wins
-            const tkey t = kmax(Pl, m);
+          if (kmax(Pt, m) < bcmp) {  // replay in order: the first minimum wins
+            const tkey t = kmax(Pt, m);
             int hit = slot;
             for (int h = slot; h < cnt; h += J)
-              if (kmax(Pl, __ldg(pv + h * FPW)) == t) {
+              if (kmax(Pt, __ldg(pv + h * FPW)) == t) {
                 hit = h;
                 break;
               }
@@ -176,10 +213,18 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
             s_hit[threadIdx.x] = (uint32_t)hit;
           }
           ord += (uint32_t)cnt;
-        } else if ((op >> 29) & 1u) {  // FIX
-          P[0] = kmax(P[0], __ldg(keys + (op & kTrIdxMask) * FPW));
+        } else if (code == kOpPush) {
+          const uint32_t d = (uint32_t)tr_small_of(op);
+          P[(d + 1) * 32] = kmax(P[d * 32], __ldg(key_at(keys, tr_koff32(op) >> SH)));
+        } else if (tr_is_fix(op)) {
+          P0 = kmax(P0, __ldg(key_at(keys, tr_koff32(op) >> SH)));
+          Pt = P0;
+          P[0] = P0;
         } else {  // SKEL
-          ld = (int)((op >> 23) & 63u);
+          const int ld = tr_skel_ld(op);
+          Pl1 = P + (ld > 0 ? ld - 1 : 0) * 32;
+          P0 = 0;
+          Pt = 0;
           P[0] = 0;
         }
       }
@@ -235,16 +280,16 @@ __device__ void trace_rebuild(const uint32_t* __restrict__ ops, const uint32_t* 
     lo = nlo;
   }
   const uint32_t b = skel_pos[lo];
-  const int ld = (int)((ops[b] >> 23) & 63u);
+  const int ld = tr_skel_ld(ops[b]);
   uint32_t my0 = ~0u, my1 = ~0u;
   for (uint32_t p0 = b; p0 < leafpos; p0 += 32) {
     const uint32_t mine = p0 + lane < leafpos ? ops[p0 + lane] : ~0u;
     const int nb = (int)min(32u, leafpos - p0);
     for (int q = 0; q < nb; ++q) {
       const uint32_t op = __shfl_sync(0xffffffffu, mine, q);
-      if ((op >> 30) == kOpPush) {
-        const int d = (int)((op >> 24) & 63u);
-        const uint32_t kidx = op & kTrKeyMask;
+      if (tr_is_push(op)) {
+        const int d = tr_small_of(op);
+        const uint32_t kidx = tr_kidx(op);
         const uint32_t idx = kidx >= nr ? kidx - nr : kidx;
         if (d == lane) my0 = idx;
         if (d == lane + 32) my1 = idx;
@@ -254,15 +299,15 @@ __device__ void trace_rebuild(const uint32_t* __restrict__ ops, const uint32_t* 
   path[lane] = my0;
   path[lane + 32] = my1;
   const uint32_t fop = b + 1 + lane < leafpos && lane < SC_MAX_COLS ? ops[b + 1 + lane] : 0u;
-  const bool isfix = (fop >> 29) == 7u;  // code 3 with the FIX bit
+  const bool isfix = tr_is_fix(fop);
   const uint32_t fm = __ballot_sync(0xffffffffu, isfix);
   const int nfix = __ffs(~fm) - 1;       // consecutive FIXes from the start
-  if (lane < nfix) fixes[lane] = fop & kTrIdxMask;
+  if (lane < nfix) fixes[lane] = tr_kidx(fop);
   __syncwarp();
   if (lane == 0) {
     const uint32_t lop = ops[leafpos];
-    const uint32_t cnt = (lop >> 22) & 255u;
-    trace_snapshot(fixes, nfix, path, ld, cnt ? (lop & kTrIdxMask) + leafoff : ~0u, cols, rows,
+    const int cnt = tr_leaf_cnt(lop);
+    trace_snapshot(fixes, nfix, path, ld, cnt ? tr_kidx(lop) - nr + leafoff : ~0u, cols, rows,
                    snap);
   }
   __syncwarp();
@@ -342,8 +387,8 @@ __global__ void k_trace_skips(const uint32_t* __restrict__ ops, const uint32_t* 
   skip[b] = e;
   for (uint32_t p = b + 1; p < e; ++p) {
     const uint32_t op = ops[p];
-    if ((op >> 30) == kOpPush) {
-      const int d = (int)((op >> 24) & 63u);
+    if (tr_is_push(op)) {
+      const int d = tr_small_of(op);
       while (top > 0 && open_d[top - 1] >= d) skip[open_pos[--top]] = p;
       open_pos[top] = p;
       open_d[top++] = d;
@@ -436,11 +481,11 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
         mine = p + lane < e ? __ldg(a.ops + p + lane) : 0u;
       }
       const uint32_t op = __shfl_sync(0xffffffffu, mine, p - base);
-      const uint32_t code = op >> 30;
+      const uint32_t code = tr_code(op);
       uint32_t next = p + 1;
-      if (code == kOpPush) {
-        const uint32_t d = (op >> 24) & 63u;
-        const uint32_t kidx = op & kTrKeyMask;
+      if (tr_is_push(op)) {
+        const uint32_t d = (uint32_t)tr_small_of(op);
+        const uint32_t kidx = tr_kidx(op);
         const tkey Pn = kmax(P[d * 32], __ldg(keys + kidx * FPW));
         P[(d + 1) * 32] = Pn;
         const bool split = kidx >= a.nr;
@@ -459,7 +504,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
           S[(d + 1) * 32] = sv;
         }
       } else if (code == kOpLeaf) {
-        const int cnt = (int)((op >> 22) & 255u);
+        const int cnt = tr_leaf_cnt(op);
         const tkey Pl = P[ld * 32];
         const bool live = (int64_t)Pl <= budget;
         if (cnt == 0) {
@@ -467,7 +512,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
           ord += 1;
         } else {
           if (__ballot_sync(0xffffffffu, live) != 0 && live) {
-            const uint32_t idx = op & kTrIdxMask;
+            const uint32_t idx = tr_kidx(op) - a.nr;
             const double Sl = S[ld * 32];
             const uint32_t tag = Cc[ld * 32] + 1u;
             for (int h = slot; h < cnt; h += J) {
@@ -481,9 +526,9 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
           }
           ord += (uint32_t)cnt;
         }
-      } else if ((op >> 29) & 1u) {  // FIX
-        const uint32_t idx = op & kTrIdxMask;
-        const uint32_t tag = (op >> 23) & 63u;
+      } else if (tr_is_fix(op)) {
+        const uint32_t idx = tr_kidx(op);
+        const uint32_t tag = (uint32_t)tr_small_of(op);
         P[0] = kmax(P[0], __ldg(keys + idx * FPW));
         if (tag == 0) {
           S[0] = __dadd_rn(S[0], __ldg(rs + (size_t)idx * FPW));
@@ -498,7 +543,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
           __syncwarp();
         }
       } else {  // SKEL
-        ld = (int)((op >> 23) & 63u);
+        ld = tr_skel_ld(op);
         P[0] = 0;
         S[0] = 0.0;
         Cc[0] = 0;

@@ -18,9 +18,11 @@
 //                   column; keys = rt | rts (the time keys, then the split
 //                   table: run + forced rest of its column), kidx = idx for
 //                   rt and NR + idx for the column's second-to-last run
-//   LEAF  idx, cnt  candidates time max(P[ld], rts[idx + i]), i < cnt (<= 255): the
+//                   (PUSHL: the same op at depth ld - 1, right above a LEAF)
+//   LEAF  idx, cnt  candidates time max(P[ld], rts[idx + i]), i < cnt (<= 31): the
 //                   last decision run takes cnt consecutive heights (its
-//                   forced rest and any later one-run columns are in the key)
+//                   forced rest and any later one-run columns are in the key);
+//                   longer runs of heights are several LEAF ops
 //   LEAF  -, 0      the skeleton's single candidate (no decision run): P[ld]
 //
 // Only ops that lead to a candidate are emitted (a PUSH is written lazily,
@@ -47,24 +49,45 @@
 
 namespace scb {
 
-constexpr uint32_t kOpPush = 0u, kOpLeaf = 2u, kOpSkel = 3u;  // bits 31..30
+constexpr uint32_t kOpPush = 0u, kOpPushL = 1u, kOpLeaf = 2u, kOpSkel = 3u;  // bits 31..30
 constexpr int kTrIdxBits = 22;                                 // rectangle index
 constexpr uint32_t kTrIdxMask = (1u << kTrIdxBits) - 1u;
 constexpr uint32_t kTrKeyMask = (1u << (kTrIdxBits + 1)) - 1u;  // rt | rts key index
+constexpr int kTrLeafMax = 31;                                  // heights per LEAF op
 
-// PUSH: depth in bits 29..24, key index (rt | rts) in 22..0
-SCB_TR_HD uint32_t op_push(int d, uint32_t kidx) {
-  return (kOpPush << 30) | ((uint32_t)d << 24) | kidx;
+// Encoding.  Every op that reads a key holds its key index (rt | rts) in bits
+// 27..5, i.e. already multiplied by 32 -- the element offset of the key's line
+// in the [rect][32 frames] table -- so the interpreter's address is one AND
+// and one multiply-add.  The small field (a PUSH's depth, a FIX's tag, a
+// LEAF's count) is in bits 4..0 (+ bit 28 for depths / tags above 31).
+//   PUSH  (code 0)  depth d; PUSHL (code 1) the same with d == ld - 1: the
+//                   push right above a LEAF, which the step-1 interpreter
+//                   fuses with that LEAF (the next op) and keeps in a register
+//   LEAF  (code 2)  key index NR + idx (the split table), count 0..31
+//   SKEL  (code 3, bit 29 clear)  leaf depth in bits 5..0
+//   FIX   (code 3, bit 29 set)    rectangle idx, tag
+SCB_TR_HD uint32_t tr_small(int v) { return ((uint32_t)v & 31u) | (((uint32_t)v & 32u) << 23); }
+SCB_TR_HD uint32_t op_push(int d, uint32_t kidx, bool to_leaf) {
+  return ((to_leaf ? kOpPushL : kOpPush) << 30) | (kidx << 5) | tr_small(d);
 }
-SCB_TR_HD uint32_t op_leaf(uint32_t idx, int cnt) {
-  return (kOpLeaf << 30) | ((uint32_t)cnt << 22) | idx;
+SCB_TR_HD uint32_t op_leaf(uint32_t kidx, int cnt) {
+  return (kOpLeaf << 30) | (kidx << 5) | (uint32_t)cnt;
 }
-SCB_TR_HD uint32_t op_skel(int ld) { return (kOpSkel << 30) | ((uint32_t)ld << 23); }
-// FIX: bits 28..23 = the number of multi-run columns left of the column (its
-// place in the slice order, for the step-2 SSE fold), 21..0 its rectangle
+SCB_TR_HD uint32_t op_skel(int ld) { return (kOpSkel << 30) | (uint32_t)ld; }
+// FIX: tag = the number of multi-run columns left of the column (its place in
+// the slice order, for the step-2 SSE fold)
 SCB_TR_HD uint32_t op_fix(uint32_t idx, int tag) {
-  return (kOpSkel << 30) | (1u << 29) | ((uint32_t)tag << 23) | idx;
+  return (kOpSkel << 30) | (1u << 29) | (idx << 5) | tr_small(tag);
 }
+// decoders
+SCB_TR_HD uint32_t tr_code(uint32_t op) { return op >> 30; }
+SCB_TR_HD bool tr_is_push(uint32_t op) { return (op >> 31) == 0u; }  // PUSH or PUSHL
+SCB_TR_HD bool tr_is_fix(uint32_t op) { return (op >> 29) == 7u; }
+SCB_TR_HD uint32_t tr_kidx(uint32_t op) { return (op >> 5) & kTrKeyMask; }
+SCB_TR_HD uint32_t tr_koff32(uint32_t op) { return op & (kTrKeyMask << 5); }  // kidx * 32
+SCB_TR_HD int tr_small_of(uint32_t op) { return (int)((op & 31u) | ((op >> 23) & 32u)); }
+SCB_TR_HD int tr_leaf_cnt(uint32_t op) { return (int)(op & 31u); }
+SCB_TR_HD int tr_skel_ld(uint32_t op) { return (int)(op & 63u); }
 
 SCB_TR_HD int tr_xw(int cols, int x0, int w) { return x0 * cols - (x0 * (x0 - 1)) / 2 + (w - 1); }
 SCB_TR_HD int tr_yh(int rows, int y0, int h) { return y0 * rows - (y0 * (y0 - 1)) / 2 + (h - 1); }
@@ -74,7 +97,7 @@ struct TraceCount {
   uint64_t ops = 0, cands = 0, skels = 0;
   SCB_TR_HD void skel(int) { ++ops; ++skels; }
   SCB_TR_HD void fix(uint32_t, int) { ++ops; }
-  SCB_TR_HD void push(int, uint32_t) { ++ops; }
+  SCB_TR_HD void push(int, uint32_t, bool) { ++ops; }
   SCB_TR_HD void leaf(uint32_t, int cnt) { ++ops; cands += cnt ? (uint64_t)cnt : 1u; }
 };
 struct TraceWrite {
@@ -92,9 +115,9 @@ struct TraceWrite {
     ops[pos++] = op_skel(ld);
   }
   SCB_TR_HD void fix(uint32_t idx, int tag) { ops[pos++] = op_fix(idx, tag); }
-  SCB_TR_HD void push(int d, uint32_t kidx) { ops[pos++] = op_push(d, kidx); }
-  SCB_TR_HD void leaf(uint32_t idx, int cnt) {
-    ops[pos++] = op_leaf(idx, cnt);
+  SCB_TR_HD void push(int d, uint32_t kidx, bool to_leaf) { ops[pos++] = op_push(d, kidx, to_leaf); }
+  SCB_TR_HD void leaf(uint32_t kidx, int cnt) {
+    ops[pos++] = op_leaf(kidx, cnt);
     cand += cnt ? (uint64_t)cnt : 1u;
   }
 };
@@ -248,11 +271,17 @@ SCB_TR_HD void trace_item(const WorkItem& wi, int cols, int rows, int n, double 
             emitted = 0;
           }
           for (int dd = emitted; dd < nl - 1; ++dd)
-            out.push(dd, (Dleft[dd] == 2 ? nr : 0u) +
-                             (uint32_t)(tr_xw(cols, Dx0[dd], Dw[dd]) * nyh +
-                                        tr_yh(rows, Y0[dd], H[dd])));
+            out.push(dd,
+                     (Dleft[dd] == 2 ? nr : 0u) + (uint32_t)(tr_xw(cols, Dx0[dd], Dw[dd]) * nyh +
+                                                             tr_yh(rows, Y0[dd], H[dd])),
+                     dd == nl - 2);
           emitted = nl - 1;
-          out.leaf(base + (uint32_t)(h0 - 1), h - h0);  // h - h0 <= rows - 2 <= 253
+          // h - h0 <= rows - 2 <= 253 heights, kTrLeafMax per LEAF op
+          uint32_t lk = nr + base + (uint32_t)(h0 - 1);
+          int left_h = h - h0;
+          for (; left_h > kTrLeafMax; left_h -= kTrLeafMax, lk += kTrLeafMax)
+            out.leaf(lk, kTrLeafMax);
+          out.leaf(lk, left_h);
         }
         --t;
       }
@@ -348,25 +377,24 @@ SCB_TR_HD bool trace_layout(const uint32_t* ops, uint64_t nops, uint64_t which, 
   (void)n;
   for (uint64_t p = 0; p < nops; ++p) {
     const uint32_t op = ops[p];
-    const uint32_t code = op >> 30;
-    if (code == kOpSkel) {
-      if ((op >> 29) & 1u) fixes[nfix++] = op & kTrIdxMask;
-      else if (p == 0) ld = (int)((op >> 23) & 63u);
+    if (tr_code(op) == kOpSkel) {
+      if (tr_is_fix(op)) fixes[nfix++] = tr_kidx(op);
+      else if (p == 0) ld = tr_skel_ld(op);
       else return false;  // next skeleton: `which` was not in this one
       continue;
     }
-    if (code == kOpPush) {
-      const uint32_t kidx = op & kTrKeyMask;
-      path[(op >> 24) & 63u] = kidx >= nr ? kidx - nr : kidx;
+    if (tr_is_push(op)) {
+      const uint32_t kidx = tr_kidx(op);
+      path[tr_small_of(op)] = kidx >= nr ? kidx - nr : kidx;
       continue;
     }
-    const int cnt = (int)((op >> 22) & 255u);
+    const int cnt = tr_leaf_cnt(op);
     const uint64_t m = cnt ? (uint64_t)cnt : 1u;
     if (which >= seen + m) {
       seen += m;
       continue;
     }
-    trace_snapshot(fixes, nfix, path, ld, cnt ? (op & kTrIdxMask) + (uint32_t)(which - seen) : ~0u,
+    trace_snapshot(fixes, nfix, path, ld, cnt ? tr_kidx(op) - nr + (uint32_t)(which - seen) : ~0u,
                    cols, rows, snap);
     return true;
   }

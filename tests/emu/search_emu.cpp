@@ -296,30 +296,31 @@ extern "C" int emu_trace_search(int cols, int rows, int n, double k, int max_til
     uint64_t best_ord = ~0ull, ord = 0;
     int ld = 0;
     for (size_t p = 0; p < ops.size(); ++p) {
-      const uint32_t op = ops[p], code = op >> 30, idx = op & kTrIdxMask;
-      if (code == kOpPush) {
-        const int d = (int)((op >> 24) & 63u);
-        const uint32_t kidx = op & kTrKeyMask;
+      const uint32_t op = ops[p], code = tr_code(op);
+      if (tr_is_push(op)) {
+        const int d = tr_small_of(op);
+        const uint32_t kidx = tr_kidx(op);
         const double v = kidx >= nr ? tsplit(kidx - (uint32_t)nr) : clamp(T[kidx]);
         P[d + 1] = P[d] > v ? P[d] : v;
       } else if (code == kOpLeaf) {
-        const int cnt = (int)((op >> 22) & 255u);
+        const int cnt = tr_leaf_cnt(op);
         if (cnt == 0) {
           if (P[ld] < best) best = P[ld], best_ord = ord;
           ord += 1;
           continue;
         }
+        const uint32_t idx = tr_kidx(op) - (uint32_t)nr;
         for (int h = 0; h < cnt; ++h) {
           const double v = tsplit(idx + (uint32_t)h);
           const double t = P[ld] > v ? P[ld] : v;
           if (t < best) best = t, best_ord = ord + (uint64_t)h;
         }
         ord += (uint64_t)cnt;
-      } else if ((op >> 29) & 1u) {
-        const double v = clamp(T[idx]);
+      } else if (tr_is_fix(op)) {
+        const double v = clamp(T[tr_kidx(op)]);
         P[0] = P[0] > v ? P[0] : v;
       } else {
-        ld = (int)((op >> 23) & 63u);
+        ld = tr_skel_ld(op);
         P[0] = 0.0;
       }
     }
@@ -411,10 +412,10 @@ extern "C" int emu_trace_step2(int cols, int rows, int n, double k, int max_tile
       }
     };
     for (size_t p = 0; p < ops.size(); ++p) {
-      const uint32_t op = ops[p], code = op >> 30;
-      if (code == kOpPush) {
-        const int d = (int)((op >> 24) & 63u);
-        const uint32_t kidx = op & kTrKeyMask;
+      const uint32_t op = ops[p], code = tr_code(op);
+      if (tr_is_push(op)) {
+        const int d = tr_small_of(op);
+        const uint32_t kidx = tr_kidx(op);
         const bool split = kidx >= nr;
         const uint32_t idx = split ? kidx - (uint32_t)nr : kidx;
         const double v = tkey(idx, split);
@@ -429,13 +430,13 @@ extern "C" int emu_trace_step2(int cols, int rows, int n, double k, int max_tile
         SS[d + 1] = s;
         Cc[d + 1] = c;
       } else if (code == kOpLeaf) {
-        const int cnt = (int)((op >> 22) & 255u);
+        const int cnt = tr_leaf_cnt(op);
         if (cnt == 0) {
           offer(P[ld], SS[ld], ord, p, 0);
           ord += 1;
           continue;
         }
-        const uint32_t idx = op & kTrIdxMask;
+        const uint32_t idx = tr_kidx(op) - (uint32_t)nr;
         for (int h = 0; h < cnt; ++h) {
           const double v = tkey(idx + (uint32_t)h, true);
           const double t = P[ld] > v ? P[ld] : v;
@@ -446,15 +447,15 @@ extern "C" int emu_trace_step2(int cols, int rows, int n, double k, int max_tile
           offer(t, s, ord + (uint64_t)h, p, h);
         }
         ord += (uint64_t)cnt;
-      } else if ((op >> 29) & 1u) {
-        const uint32_t idx = op & kTrIdxMask;
-        const int tag = (int)((op >> 23) & 63u);
+      } else if (tr_is_fix(op)) {
+        const uint32_t idx = tr_kidx(op);
+        const int tag = tr_small_of(op);
         const double v = clamp(T[idx]);
         P[0] = P[0] > v ? P[0] : v;
         if (tag == 0) SS[0] = SS[0] + S[idx];
         else fxi[nfx] = idx, fxt[nfx] = tag, ++nfx;
       } else {
-        ld = (int)((op >> 23) & 63u);
+        ld = tr_skel_ld(op);
         P[0] = 0.0, SS[0] = 0.0, Cc[0] = 0, nfx = 0;
       }
     }
