@@ -161,6 +161,25 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
     tkey P0 = 0, Pt = 0;
     const uint32_t* Pl1 = P;
     int nbw = 32;
+    // a leaf's minimum against the lane's best; a winner is replayed in order
+    // (the first minimum wins)
+    auto leaf_tail = [&](tkey m, int cnt, const uint32_t* pv, uint32_t pos) {
+      const tkey t = kmax(Pt, m);
+      if (t < bcmp) {
+        int hit = slot;
+        for (int h = slot; h < cnt; h += J)
+          if (kmax(Pt, __ldg(pv + h * FPW)) == t) {
+            hit = h;
+            break;
+          }
+        best = t;
+        bcmp = t;
+        best_ord = ord + (uint32_t)hit;
+        s_pos[threadIdx.x] = pos;
+        s_hit[threadIdx.x] = (uint32_t)hit;
+      }
+      ord += (uint32_t)cnt;
+    };
     for (uint32_t p0 = b; p0 < e; p0 += (uint32_t)nbw) {
       const uint32_t mine = p0 + lane < e ? __ldg(a.ops + p0 + lane) : 0u;
       int nb = (int)min(32u, e - p0);
@@ -173,9 +192,23 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
         uint32_t op = __shfl_sync(0xffffffffu, mine, q);
         uint32_t code = tr_code(op);
         if (__builtin_expect(code == kOpPushL, 1)) {
-          Pt = kmax(*Pl1, __ldg(key_at(keys, tr_koff32(op) >> SH)));
-          op = __shfl_sync(0xffffffffu, mine, ++q);  // a PUSHL's next op is its LEAF
-          code = kOpLeaf;
+          // fused PUSHL + LEAF (the next op, in this fetch): the push's key
+          // and the leaf's keys are all requested before any is consumed
+          const tkey v = __ldg(key_at(keys, tr_koff32(op) >> SH));
+          const tkey pl = *Pl1;
+          op = __shfl_sync(0xffffffffu, mine, ++q);
+          const int cnt = tr_leaf_cnt(op);  // >= 1 below a PUSHL
+          const uint32_t* pv = key_at(keys, tr_koff32(op) >> SH);
+          tkey m;
+          if (J == 1) {
+            m = leaf_min<FPW>(pv, cnt);
+          } else {
+            m = kKeyInf;
+            for (int h = slot; h < cnt; h += J) m = kmin(m, __ldg(pv + h * FPW));
+          }
+          Pt = kmax(pl, v);
+          leaf_tail(m, cnt, pv, p0 + q);
+          continue;
         }
         if (code == kOpLeaf) {
           const int cnt = tr_leaf_cnt(op);
@@ -198,21 +231,7 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
             m = kKeyInf;
             for (int h = slot; h < cnt; h += J) m = kmin(m, __ldg(pv + h * FPW));
           }
-          if (kmax(Pt, m) < bcmp) {  // replay in order: the first minimum wins
-            const tkey t = kmax(Pt, m);
-            int hit = slot;
-            for (int h = slot; h < cnt; h += J)
-              if (kmax(Pt, __ldg(pv + h * FPW)) == t) {
-                hit = h;
-                break;
-              }
-            best = t;
-            bcmp = t;
-            best_ord = ord + (uint32_t)hit;
-            s_pos[threadIdx.x] = p0 + q;
-            s_hit[threadIdx.x] = (uint32_t)hit;
-          }
-          ord += (uint32_t)cnt;
+          leaf_tail(m, cnt, pv, p0 + q);
         } else if (code == kOpPush) {
           const uint32_t d = (uint32_t)tr_small_of(op);
           P[(d + 1) * 32] = kmax(P[d * 32], __ldg(key_at(keys, tr_koff32(op) >> SH)));
@@ -701,12 +720,13 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
                            st));
   SCB_CUDA(cudaMemcpyAsync(skel_ord.as<uint64_t>() + tot_skel, &tot_cand, 8, cudaMemcpyHostToDevice,
                            st));
-  // ~128 chunks per SM (persistent warps take them dynamically), 16..8192
+  // ~1024 chunks per SM (persistent warps take them dynamically: ~16 per
+  // warp, so the kernel's tail is a small share of a warp's work), 16..8192
   // ops: small spaces get short chunks, so their few ops run on many warps
   // instead of one warp's serial chain of dependent loads
   const uint64_t chunk_ops = std::min<uint64_t>(
-      8192, std::max<uint64_t>(16, (tot_ops + (uint64_t)sm_count * 128 - 1) /
-                                       ((uint64_t)sm_count * 128)));
+      8192, std::max<uint64_t>(16, (tot_ops + (uint64_t)sm_count * 1024 - 1) /
+                                       ((uint64_t)sm_count * 1024)));
   const uint32_t n_chunks = (uint32_t)std::max<uint64_t>(1, (tot_ops + chunk_ops - 1) / chunk_ops);
   chunk_skel.ensure(((size_t)n_chunks + 1) * sizeof(uint32_t));
   k_trace_chunks<<<(n_chunks + 1 + 255) / 256, 256, 0, st>>>(skel_pos.as<uint32_t>(),
