@@ -746,7 +746,7 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
     ctx->counter.ensure((size_t)L.groups * 8 * sizeof(uint64_t));
     ctx->frame_best.ensure((size_t)2 * L.groups * L.fpw * sizeof(FrameBest));
     FrameBest* fb = ctx->frame_best.as<FrameBest>() + (size_t)L.groups * L.fpw;
-    ctx->rss.ensure(L.nr * L.fpw * sizeof(double));
+    ctx->rss.ensure(L.nr * L.fpw * 2 * sizeof(double));  // {sse, rest sse} pairs
     for (int gi = 0; gi < L.groups; ++gi) {
       uint64_t* ctr = ctx->counter.as<uint64_t>() + 8 * gi + 4;
       SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));

@@ -427,8 +427,7 @@ struct Trace2Args {
   uint32_t n_chunks, chunk_offset, chunk_stride, n_mine;
   uint32_t* counter;
   const uint32_t* keys;      // [2][NR][FPW] time keys | split table of this frame group
-  const double* rs;          // [NR][FPW] slice SSEs of this frame group
-  const double* rss;         // [NR][FPW] SSE of each run's forced rest (gathered per call)
+  const double2* rsp;        // [NR][FPW] {slice SSE, SSE of the run's forced rest} (per call)
   const int64_t* budget;     // [FPW] largest key with time <= t_min * (1 + lambda), -1: none
   uint32_t nr;
   int depth_cap;
@@ -442,14 +441,22 @@ struct Trace2Args {
 // columns right of it -- the FIX tags), and the (sse, t, ordinal) minimum
 // over the candidates with t <= budget.  A subtree whose fixed slices already
 // exceed every lane's budget is skipped through the skip table.
+//
+// Like the step-1 walk, the top of the stacks (P[ld], S[ld]) lives in
+// registers and a PUSHL is processed together with its LEAF.  The tagged
+// one-run columns' SSEs sit at the top end of the S stack (the path needs
+// nl - 1 entries, the skeleton has n - nl - nmulti one-run columns: both fit
+// depth_cap = n), their tags in a 64-bit uniform register (4 bits each); a
+// candidate's loads ({key}, {sse, rest sse} as one 128-bit load) are issued
+// unconditionally, two heights at a time, so dead lanes only predicate the
+// offer.
 template <int FPW>
 __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
   constexpr int J = 32 / FPW;
+  constexpr int SH = FPW == 32 ? 0 : FPW == 16 ? 1 : FPW == 8 ? 2 : FPW == 4 ? 3 : FPW == 2 ? 4 : 5;
   extern __shared__ __align__(16) uint8_t tr2_sm[];
-  __shared__ uint32_t s_pos[256], s_hit[256], s_fxi[8][SC_MAX_COLS], s_fxt[8][SC_MAX_COLS];
-  __shared__ int s_nfx[8];
-  __shared__ double s_rsse[256];
-  __shared__ uint64_t s_rk[256], s_ro[256];
+  __shared__ uint32_t s_pos[256], s_hit[256];
+  __shared__ uint32_t s_cc[8][SC_MAX_SLICES];  // closed multi-run columns above each depth (uniform)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int f = lane % FPW, slot = lane / FPW;
   const size_t dstride = (size_t)a.depth_cap * 32;
@@ -457,12 +464,15 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
   double* S = reinterpret_cast<double*>(tr2_sm) + (size_t)wib * dstride + lane;
   uint32_t* P = reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(tr2_sm) + nw * dstride) +
                 (size_t)wib * dstride + lane;
-  uint32_t* Cc = P + nw * dstride;  // closed multi-run columns above each depth
+  double* Sfix = S + (size_t)(a.depth_cap - 1) * 32;  // tagged fix j at Sfix[-j * 32]
+  uint32_t* Cc = s_cc[wib];
   const uint32_t* __restrict__ keys = a.keys + f;
-  const uint32_t* __restrict__ rts = a.keys + (size_t)a.nr * FPW + f;
-  const double* __restrict__ rs = a.rs + f;
-  const double* __restrict__ rss = a.rss + f;
+  const double2* __restrict__ rsp = a.rsp + f;
+  asm volatile("" : "+l"(keys));
+  asm volatile("" : "+l"(rsp));
+  const uint32_t nrf = a.nr * FPW;  // element offset of the split table
   const int64_t budget = a.budget[f];
+  const uint32_t bp1 = budget < 0 ? 0u : (uint32_t)budget + 1u;  // live iff key < bp1
   double best_sse = __longlong_as_double(0x7ff0000000000000ll);
   tkey best_t = kKeyInf;
   uint32_t best_ord = 0xffffffffu;
@@ -475,12 +485,6 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
       s_hit[threadIdx.x] = (uint32_t)hit;
     }
   };
-  auto fold_fix = [&](double sv, uint32_t tag) {
-    const int nf = s_nfx[wib];
-    for (int j = 0; j < nf; ++j)
-      if (s_fxt[wib][j] == tag) sv = __dadd_rn(sv, __ldg(rs + (size_t)s_fxi[wib][j] * FPW));
-    return sv;
-  };
   while (true) {
     uint32_t k = 0;
     if (lane == 0) k = atomicAdd(a.counter, 1u);
@@ -491,89 +495,132 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
     if (s0 >= s1) continue;
     const uint32_t b = a.skel_pos[s0], e = a.skel_pos[s1];
     uint32_t ord = (uint32_t)a.skel_ord[s0];
+    // path state: P[0] / S[0] and the top P[ld] / S[ld] in registers
+    tkey P0 = 0, Pt = 0;
+    double S0 = 0.0, St = 0.0;
     int ld = 0;
-    uint32_t base = 0xffffffffu, mine = 0;
+    uint32_t ctop = 0;        // closed multi-run columns above the leaf depth
+    uint64_t fxt = 0;         // tags of the tagged one-run columns, 4 bits each
+    int nfx = 0, jl = 0;      // their number; first one with the highest tag so far
+    uint32_t lasttag = 0;
+    uint32_t base = b - 32u, mine = 0;
+    auto fetch = [&](uint32_t pp) {
+      if (pp - base >= 32u) {
+        base = pp;
+        mine = pp + lane < e ? __ldg(a.ops + pp + lane) : 0u;
+      }
+      return __shfl_sync(0xffffffffu, mine, pp - base);
+    };
+    auto fold_fix = [&](double sv, uint32_t tag) {
+      for (int j = 0; j < nfx; ++j)
+        if (((uint32_t)(fxt >> (4 * j)) & 15u) == tag) sv = __dadd_rn(sv, Sfix[-j * 32]);
+      return sv;
+    };
+    // the candidates of one LEAF op (cnt >= 1) under the path state above
+    auto leaf = [&](uint32_t op, uint32_t pos) {
+      const int cnt = tr_leaf_cnt(op);
+      if (__any_sync(0xffffffffu, Pt < bp1)) {
+        const uint32_t off = tr_koff32(op) >> SH;
+        const uint32_t* pk = key_at(keys, off);
+        const double2* pp = rsp + (off - nrf);
+        // the one-run columns right of the last multi-run column
+        const int j0 = lasttag == ctop + 1u ? jl : nfx;
+        for (int h = slot; h < cnt; h += 2 * J) {
+          const bool two = h + J < cnt;
+          const tkey k0 = __ldg(pk + h * FPW);
+          const double2 a0 = __ldg(pp + h * FPW);
+          const tkey k1 = two ? __ldg(pk + (h + J) * FPW) : kKeyInf;
+          const double2 a1 = two ? __ldg(pp + (h + J) * FPW) : make_double2(0.0, 0.0);
+          double sv0 = __dadd_rn(__dadd_rn(St, a0.x), a0.y);
+          double sv1 = __dadd_rn(__dadd_rn(St, a1.x), a1.y);
+          for (int j = j0; j < nfx; ++j) {
+            const double fv = Sfix[-j * 32];
+            sv0 = __dadd_rn(sv0, fv);
+            sv1 = __dadd_rn(sv1, fv);
+          }
+          const tkey t0 = kmax(Pt, k0), t1 = kmax(Pt, k1);
+          if (t0 < bp1 && sv0 <= best_sse) offer(t0, sv0, ord + (uint32_t)h, pos, h);
+          if (t1 < bp1 && sv1 <= best_sse) offer(t1, sv1, ord + (uint32_t)(h + J), pos, h + J);
+        }
+      }
+      ord += (uint32_t)cnt;
+    };
     uint32_t p = b;
     while (p < e) {
-      if (base == 0xffffffffu || p - base >= 32) {
-        base = p;
-        mine = p + lane < e ? __ldg(a.ops + p + lane) : 0u;
-      }
-      const uint32_t op = __shfl_sync(0xffffffffu, mine, p - base);
-      const uint32_t code = tr_code(op);
-      uint32_t next = p + 1;
+      const uint32_t op = fetch(p);
       if (tr_is_push(op)) {
         const uint32_t d = (uint32_t)tr_small_of(op);
-        const uint32_t kidx = tr_kidx(op);
-        const tkey Pn = kmax(P[d * 32], __ldg(keys + kidx * FPW));
-        P[(d + 1) * 32] = Pn;
-        const bool split = kidx >= a.nr;
-        const uint32_t c = Cc[d * 32] + (split ? 1u : 0u);
-        Cc[(d + 1) * 32] = c;
-        const bool live = (int64_t)Pn <= budget;
-        if (a.skip && __ballot_sync(0xffffffffu, live) == 0) {
-          next = __ldg(a.skip + p);  // no lane can meet its budget below: skip the subtree
-        } else if (live) {
-          const uint32_t idx = split ? kidx - a.nr : kidx;
-          double sv = __dadd_rn(S[d * 32], __ldg(rs + (size_t)idx * FPW));
-          if (split) {
-            sv = __dadd_rn(sv, __ldg(rss + (size_t)idx * FPW));
-            sv = fold_fix(sv, c);
-          }
-          S[(d + 1) * 32] = sv;
+        const uint32_t off = tr_koff32(op) >> SH;
+        const bool split = off >= nrf;  // the column's second-to-last run: its rest follows
+        const tkey v = __ldg(key_at(keys, off));
+        const double2* pr = rsp + (split ? off - nrf : off);
+        const double r0 = __ldg(&pr->x);
+        const double r1 = split ? __ldg(&pr->y) : 0.0;
+        const uint32_t c = Cc[d] + (split ? 1u : 0u);
+        const tkey Pn = kmax(P[d * 32], v);
+        double sv = __dadd_rn(S[d * 32], r0);
+        if (split) sv = fold_fix(__dadd_rn(sv, r1), c);
+        if (tr_code(op) == kOpPushL) {  // stays in registers; its LEAF is the next op
+          Pt = Pn;
+          St = sv;
+          ctop = c;
+          leaf(fetch(p + 1), p + 1);
+          p += 2;
+          continue;
         }
-      } else if (code == kOpLeaf) {
-        const int cnt = tr_leaf_cnt(op);
-        const tkey Pl = P[ld * 32];
-        const bool live = (int64_t)Pl <= budget;
-        if (cnt == 0) {
-          if (slot == 0 && live) offer(Pl, S[ld * 32], ord, p, 0);
+        P[(d + 1) * 32] = Pn;
+        S[(d + 1) * 32] = sv;
+        Cc[d + 1] = c;
+        // no lane can meet its budget below: skip the subtree
+        p = (a.skip && !__any_sync(0xffffffffu, Pn < bp1)) ? __ldg(a.skip + p) : p + 1;
+        continue;
+      }
+      if (tr_code(op) == kOpLeaf) {
+        if (tr_leaf_cnt(op) == 0) {  // the skeleton's single candidate
+          if (slot == 0 && Pt < bp1) offer(Pt, St, ord, p, 0);
           ord += 1;
         } else {
-          if (__ballot_sync(0xffffffffu, live) != 0 && live) {
-            const uint32_t idx = tr_kidx(op) - a.nr;
-            const double Sl = S[ld * 32];
-            const uint32_t tag = Cc[ld * 32] + 1u;
-            for (int h = slot; h < cnt; h += J) {
-              const tkey t = kmax(Pl, __ldg(rts + (size_t)(idx + h) * FPW));
-              if ((int64_t)t > budget) continue;
-              double sv = __dadd_rn(Sl, __ldg(rs + (size_t)(idx + h) * FPW));
-              sv = __dadd_rn(sv, __ldg(rss + (size_t)(idx + h) * FPW));
-              sv = fold_fix(sv, tag);
-              offer(t, sv, ord + (uint32_t)h, p, h);
-            }
-          }
-          ord += (uint32_t)cnt;
+          leaf(op, p);
         }
       } else if (tr_is_fix(op)) {
-        const uint32_t idx = tr_kidx(op);
+        const uint32_t off = tr_koff32(op) >> SH;
         const uint32_t tag = (uint32_t)tr_small_of(op);
-        P[0] = kmax(P[0], __ldg(keys + idx * FPW));
+        P0 = kmax(P0, __ldg(key_at(keys, off)));
+        const double r0 = __ldg(&(rsp + off)->x);
         if (tag == 0) {
-          S[0] = __dadd_rn(S[0], __ldg(rs + (size_t)idx * FPW));
+          S0 = __dadd_rn(S0, r0);
         } else {
-          const int nf = s_nfx[wib];
-          __syncwarp();
-          if (lane == 0) {
-            s_fxi[wib][nf] = idx;
-            s_fxt[wib][nf] = tag;
-            s_nfx[wib] = nf + 1;
-          }
-          __syncwarp();
+          Sfix[-nfx * 32] = r0;
+          fxt |= (uint64_t)tag << (4 * nfx);
+          if (tag != lasttag) jl = nfx, lasttag = tag;
+          ++nfx;
         }
+        P[0] = P0;
+        S[0] = S0;
+        Pt = P0;
+        St = S0;
       } else {  // SKEL
         ld = tr_skel_ld(op);
+        P0 = 0, Pt = 0;
+        S0 = 0.0, St = 0.0;
         P[0] = 0;
         S[0] = 0.0;
         Cc[0] = 0;
-        __syncwarp();
-        if (lane == 0) s_nfx[wib] = 0;
-        __syncwarp();
+        ctop = 0;
+        fxt = 0;
+        nfx = 0, jl = 0;
+        lasttag = 0;
       }
-      p = next;
+      ++p;
     }
+    (void)ld;
   }
-  // block-level reduction of the 8 warps' lanes with the same lane index
+  // block-level reduction of the warps' lanes with the same lane index (the
+  // stacks are dead: their shared memory holds the records)
+  __syncthreads();
+  double* s_rsse = reinterpret_cast<double*>(tr2_sm);
+  uint64_t* s_rk = reinterpret_cast<uint64_t*>(tr2_sm) + blockDim.x;
+  uint64_t* s_ro = s_rk + blockDim.x;
   s_rsse[threadIdx.x] = best_sse;
   s_rk[threadIdx.x] = best_t == kKeyInf ? ~0ull : ((uint64_t)best_t << 32) | s_pos[threadIdx.x];
   s_ro[threadIdx.x] = best_t == kKeyInf ? ~0ull : ((uint64_t)s_hit[threadIdx.x] << 32) | best_ord;
@@ -597,15 +644,15 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
   }
 }
 
-// rss[r][f] = rs[rest_of[r]][f]: the SSE of every run's forced rest next to
-// the run, so the step-2 walk adds it with one load instead of two dependent.
+// rsp[r][f] = {rs[r][f], rs[rest_of[r]][f]}: a run's SSE and the SSE of its
+// forced rest side by side, so the step-2 walk reads both with one load.
 __global__ void k_rest_sse(const double* __restrict__ rs, const uint32_t* __restrict__ rest_of,
-                           size_t nr, int fpw, double* __restrict__ rss) {
+                           size_t nr, int fpw, double2* __restrict__ rsp) {
   const size_t total = nr * (size_t)fpw;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const size_t r = i / fpw, f = i % fpw;
-    rss[i] = rs[(size_t)rest_of[r] * fpw + f];
+    rsp[i] = make_double2(rs[i], rs[(size_t)rest_of[r] * fpw + f]);
   }
 }
 
@@ -821,7 +868,7 @@ void trace_skips_device(const uint32_t* ops, const uint32_t* skel_pos, uint32_t 
 // Per-warp stacks (S doubles, P and C words) of depth_cap entries x 32 lanes;
 // deep plans (n up to 64) run fewer warps per block to fit shared memory.
 size_t trace2_warp_bytes(int depth_cap) {
-  return (size_t)depth_cap * 32 * (sizeof(double) + 2 * sizeof(uint32_t));
+  return (size_t)depth_cap * 32 * (sizeof(double) + sizeof(uint32_t));
 }
 int trace2_warps(int depth_cap) {
   const int lim = max_dynamic_smem((const void*)k_trace_walk2<32>);
@@ -862,7 +909,7 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   {
     const size_t total = (size_t)nr * fpw;
     const unsigned gb = (unsigned)std::min<size_t>((total + 255) / 256, (size_t)sm_count * 8);
-    k_rest_sse<<<gb, 256, 0, st>>>(rs, rest_of, nr, fpw, rss);
+    k_rest_sse<<<gb, 256, 0, st>>>(rs, rest_of, nr, fpw, reinterpret_cast<double2*>(rss));
     SCB_CUDA(cudaGetLastError());
   }
   Trace2Args a;
@@ -877,8 +924,7 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   a.n_mine = n_chunks > rank ? (n_chunks - rank + world - 1) / world : 0;
   a.counter = counter;
   a.keys = keys;
-  a.rs = rs;
-  a.rss = rss;
+  a.rsp = reinterpret_cast<const double2*>(rss);
   a.budget = budget;
   a.nr = nr;
   a.depth_cap = depth_cap;
