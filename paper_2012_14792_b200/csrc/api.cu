@@ -75,9 +75,11 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
                         double k, int covering, uint64_t max_ops, DevBuf& ops, DevBuf& skel_pos,
                         DevBuf& skel_ord, DevBuf& chunk_skel, DevBuf& scratch, DevBuf& temp,
                         int sm_count, TraceHost* out, cudaStream_t st);
-size_t trace_smem_bytes(int depth_cap);
-int trace_blocks_per_sm(int fpw, int depth_cap);
-void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skel_pos,
+size_t trace_smem_bytes(int depth_cap, int warps);
+int trace_warps(int depth_cap, uint64_t chunks, int sm_count);
+int trace_blocks_per_sm(int fpw, int depth_cap, int warps);
+void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint32_t* ops,
+                       const uint32_t* skel_pos,
                        const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
                        uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
                        uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st);
@@ -773,11 +775,13 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
     const int depth_cap = std::max(cfg.n_slices, 2);
     // blocks per SM: the occupancy limit, or SLICECRAFT_B200_TRACE_BPS (fewer
     // leave room for the side stream's texture pass to run beside the walk)
-    int bps = trace_blocks_per_sm(L.fpw, depth_cap);
+    const int warps = trace_warps(depth_cap, plan->trace_chunks / ctx->shard_world, ctx->sm_count);
+    int bps = trace_blocks_per_sm(L.fpw, depth_cap, warps);
     if (const char* v = getenv("SLICECRAFT_B200_TRACE_BPS")) bps = std::max(1, std::min(bps, atoi(v)));
+    // small spaces: no more warps than half the chunks
     const int blocks = std::max(
         1, (int)std::min<uint64_t>((uint64_t)ctx->sm_count * bps,
-                                   (plan->trace_chunks / ctx->shard_world + 8) / 2));
+                                   (plan->trace_chunks / ctx->shard_world * 8 / warps + 8) / 2));
     const uint32_t n_lanes = (uint32_t)blocks * 32;  // one record per block lane (trace.cu)
     const size_t lane_bytes = (size_t)n_lanes * 2 * sizeof(uint64_t);
     ctx->lanes.ensure(lane_bytes * L.groups);
@@ -788,7 +792,7 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
       uint64_t* ctr = ctx->counter.as<uint64_t>() + 8 * gi;
       SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));
       uint64_t* lanes = reinterpret_cast<uint64_t*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
-      trace_walk_launch(L.fpw, blocks, plan->tr_ops.as<uint32_t>(),
+      trace_walk_launch(L.fpw, blocks, warps, ctx->sm_count, plan->tr_ops.as<uint32_t>(),
                         plan->tr_skel_pos.as<uint32_t>(), plan->tr_skel_ord.as<uint64_t>(),
                         plan->tr_chunk_skel.as<uint32_t>(), plan->trace_chunks,
                         (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,

@@ -85,6 +85,11 @@ struct TraceArgs {
   uint32_t n_chunks;
   uint32_t chunk_offset, chunk_stride;  // shard: chunks offset, offset + stride, ...
   uint32_t n_mine;            // chunks of this shard
+  uint32_t groups_static;     // per block: groups of (warps per block) adjacent chunks taken in
+  uint32_t k_static;          // stripes (= groups_static * blocks * warps); the rest dynamically
+  uint32_t sm_major;
+  uint32_t sm_count;          // blocks b, b + sm_count, ... (one SM's, in the first wave) take
+                              // adjacent groups
   uint32_t* counter;
   const uint32_t* keys;       // [2][NR][FPW] time keys | split table of this frame group
   uint32_t nr;
@@ -125,16 +130,28 @@ __device__ __forceinline__ tkey leaf_min(const uint32_t* __restrict__ pv, int cn
 #undef LD
 }
 
+// Chunks reach the warps in two phases.  First each block walks its own
+// stripes of the chunk sequence -- groups of (warps per block) ADJACENT
+// chunks, handed to its warps through a shared-memory ticket: adjacent chunks
+// share their columns' rectangles, so the warps of an SM hit each other's key
+// lines in L1.  The last ~12 % of the chunks are taken one by one from a
+// global counter (the dynamic tail that evens out the blocks).
 template <int FPW>
-__global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
+__global__ void __launch_bounds__(1024, 2) k_trace_walk(TraceArgs a) {
   constexpr int J = 32 / FPW;
   constexpr int SH = FPW == 32 ? 0 : FPW == 16 ? 1 : FPW == 8 ? 2 : FPW == 4 ? 3 : FPW == 2 ? 4 : 5;
   extern __shared__ uint32_t tr_sm[];
-  __shared__ uint32_t s_pos[256], s_hit[256];  // the best's LEAF op and height (rare writes)
-  __shared__ uint64_t s_red[2][256];
+  __shared__ uint32_t s_ticket;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
   const int f = lane % FPW, slot = lane / FPW;
-  uint32_t* P = tr_sm + (size_t)wib * a.depth_cap * 32 + lane;  // P[d] at P[d * 32]
+  const int prow = a.depth_cap < 4 ? 4 : a.depth_cap;  // the records of the reduction fit
+  uint32_t* P = tr_sm + (size_t)wib * prow * 32 + lane;  // P[d] at P[d * 32]
+  // the best's LEAF op and height (rare writes)
+  uint32_t* s_pos = tr_sm + (size_t)nw * prow * 32;
+  uint32_t* s_hit = s_pos + blockDim.x;
+  if (threadIdx.x == 0) s_ticket = 0;
+  __syncthreads();
   // rt | rts of this lane's frame: an op's key is keys[(its offset field) >> SH]
   const uint32_t* __restrict__ keys = a.keys + f;
   asm volatile("" : "+l"(keys));  // keep the per-lane base in registers (no re-derivation per op)
@@ -145,7 +162,16 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
   uint32_t best_ord = 0xffffffffu;
   while (true) {
     uint32_t k = 0;
-    if (lane == 0) k = atomicAdd(a.counter, 1u);
+    if (lane == 0) {
+      const uint32_t t = atomicAdd(&s_ticket, 1u);
+      const uint32_t g = t / (uint32_t)nw;
+      // stripe position of this block: SM-major, so the blocks of one SM are neighbours
+      const uint32_t bps = (gridDim.x + a.sm_count - 1) / a.sm_count;
+      uint32_t bpos = (blockIdx.x % a.sm_count) * bps + blockIdx.x / a.sm_count;
+      if (gridDim.x % a.sm_count || a.sm_major == 0) bpos = blockIdx.x;  // partial waves: plain order
+      k = g < a.groups_static ? (g * gridDim.x + bpos) * (uint32_t)nw + t % (uint32_t)nw
+                              : a.k_static + atomicAdd(a.counter, 1u);
+    }
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= a.n_mine) break;
     const uint32_t chunk = a.chunk_offset + k * a.chunk_stride;
@@ -249,15 +275,19 @@ __global__ void __launch_bounds__(256) k_trace_walk(TraceArgs a) {
       }
     }
   }
-  // block-level reduction of the 8 warps' lanes with the same lane index
-  // (same frame and slot): {key << 32 | LEAF op, height << 32 | ordinal}
-  s_red[0][threadIdx.x] = best == kKeyInf ? ~0ull : ((uint64_t)best << 32) | s_pos[threadIdx.x];
-  s_red[1][threadIdx.x] = best == kKeyInf ? ~0ull : ((uint64_t)s_hit[threadIdx.x] << 32) | best_ord;
+  // block-level reduction of the warps' lanes with the same lane index (same
+  // frame and slot): {key << 32 | LEAF op, height << 32 | ordinal}; the
+  // records take the place of the (now dead) P stacks
+  __syncthreads();
+  uint64_t* s_red0 = reinterpret_cast<uint64_t*>(tr_sm);
+  uint64_t* s_red1 = s_red0 + blockDim.x;
+  s_red0[threadIdx.x] = best == kKeyInf ? ~0ull : ((uint64_t)best << 32) | s_pos[threadIdx.x];
+  s_red1[threadIdx.x] = best == kKeyInf ? ~0ull : ((uint64_t)s_hit[threadIdx.x] << 32) | best_ord;
   __syncthreads();
   if (wib == 0) {
-    uint64_t k0 = s_red[0][lane], k1 = s_red[1][lane];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      const uint64_t a0 = s_red[0][w * 32 + lane], a1 = s_red[1][w * 32 + lane];
+    uint64_t k0 = s_red0[lane], k1 = s_red1[lane];
+    for (int w = 1; w < nw; ++w) {
+      const uint64_t a0 = s_red0[w * 32 + lane], a1 = s_red1[w * 32 + lane];
       if ((a0 >> 32) < (k0 >> 32) || ((a0 >> 32) == (k0 >> 32) && (uint32_t)a1 < (uint32_t)k1))
         k0 = a0, k1 = a1;
     }
@@ -771,9 +801,11 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
   // warp, so the kernel's tail is a small share of a warp's work), 16..8192
   // ops: small spaces get short chunks, so their few ops run on many warps
   // instead of one warp's serial chain of dependent loads
+  uint64_t per_sm = 1024;
+  if (const char* v = getenv("SLICECRAFT_B200_TRACE_CHUNKS")) per_sm = std::max(1, atoi(v));
   const uint64_t chunk_ops = std::min<uint64_t>(
-      8192, std::max<uint64_t>(16, (tot_ops + (uint64_t)sm_count * 1024 - 1) /
-                                       ((uint64_t)sm_count * 1024)));
+      8192, std::max<uint64_t>(16, (tot_ops + (uint64_t)sm_count * per_sm - 1) /
+                                       ((uint64_t)sm_count * per_sm)));
   const uint32_t n_chunks = (uint32_t)std::max<uint64_t>(1, (tot_ops + chunk_ops - 1) / chunk_ops);
   chunk_skel.ensure(((size_t)n_chunks + 1) * sizeof(uint32_t));
   k_trace_chunks<<<(n_chunks + 1 + 255) / 256, 256, 0, st>>>(skel_pos.as<uint32_t>(),
@@ -789,7 +821,26 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
   return true;
 }
 
-size_t trace_smem_bytes(int depth_cap) { return (size_t)8 * depth_cap * 32 * sizeof(uint32_t); }
+// per warp: the P stack (>= 4 rows: the reduction's records reuse it) and the
+// best's position / height words
+size_t trace_smem_bytes(int depth_cap, int warps) {
+  return (size_t)warps * (std::max(depth_cap, 4) * 32 + 64) * sizeof(uint32_t);
+}
+
+// Warps per block of the step-1 walk: 32 when the space gives every SM a few
+// groups of 32 adjacent chunks (key lines shared in L1), else 8; fewer when
+// deep stacks would not fit shared memory.  SLICECRAFT_B200_TRACE_WARPS
+// overrides (A/B runs).
+int trace_warps(int depth_cap, uint64_t chunks, int sm_count) {
+  int nw = chunks >= (uint64_t)sm_count * 64 * 4 ? 32 : 8;
+  if (const char* v = getenv("SLICECRAFT_B200_TRACE_WARPS")) {
+    const int x = atoi(v);
+    if (x == 1 || x == 2 || x == 4 || x == 8 || x == 16 || x == 32) nw = x;
+  }
+  const size_t lim = (size_t)max_dynamic_smem((const void*)k_trace_walk<32>);
+  while (nw > 1 && trace_smem_bytes(depth_cap, nw) > lim) nw >>= 1;
+  return nw;
+}
 
 // deep skeletons (n up to 64) need more than the 48 KB default per block
 template <int F>
@@ -800,20 +851,22 @@ static void trace_attrs() {
   });
 }
 
-int trace_blocks_per_sm(int fpw, int depth_cap) {
+int trace_blocks_per_sm(int fpw, int depth_cap, int warps) {
   int nb = 0;
-  const size_t smem = trace_smem_bytes(depth_cap);
+  const size_t smem = trace_smem_bytes(depth_cap, warps);
 #define OCC(F)                                                                                  \
   if (fpw == F) {                                                                               \
     trace_attrs<F>();                                                                           \
-    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk<F>, 256, smem));   \
+    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk<F>, 32 * warps,    \
+                                                           smem));                              \
   }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
 #undef OCC
   return nb < 1 ? 1 : nb;
 }
 
-void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skel_pos,
+void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint32_t* ops,
+                       const uint32_t* skel_pos,
                        const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
                        uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
                        uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st) {
@@ -826,15 +879,24 @@ void trace_walk_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t*
   a.chunk_offset = rank;
   a.chunk_stride = world;
   a.n_mine = n_chunks > rank ? (n_chunks - rank + world - 1) / world : 0;
+  // striped groups for the first ~88 % of the chunks, the rest dynamically
+  const uint64_t per_round = (uint64_t)blocks * warps;
+  int pct = 88;
+  if (const char* v = getenv("SLICECRAFT_B200_TRACE_STATIC")) pct = std::max(0, std::min(100, atoi(v)));
+  a.sm_count = (uint32_t)sm_count;
+  a.sm_major = 0;
+  if (const char* v = getenv("SLICECRAFT_B200_TRACE_SMMAJOR")) a.sm_major = atoi(v);
+  a.groups_static = (uint32_t)((uint64_t)a.n_mine * pct / 100 / per_round);
+  a.k_static = (uint32_t)(a.groups_static * per_round);
   a.counter = counter;
   a.keys = keys;
   a.nr = nr;
   a.depth_cap = depth_cap;
   a.lanes = lanes;
-  const size_t smem = trace_smem_bytes(depth_cap);
+  const size_t smem = trace_smem_bytes(depth_cap, warps);
   switch (fpw) {
 #define L(F) \
-  case F: k_trace_walk<F><<<blocks, 256, smem, st>>>(a); break;
+  case F: k_trace_walk<F><<<blocks, 32 * warps, smem, st>>>(a); break;
     L(1) L(2) L(4) L(8) L(16) L(32)
 #undef L
     default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
