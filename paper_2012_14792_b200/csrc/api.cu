@@ -23,8 +23,11 @@ void texture_moments_device(const void* d_luma, int bps, int W, int H, size_t pi
                             sc_ctu_record* d_out, cudaStream_t st);
 void split_table_device(uint32_t* d_keys, int cols, int rows, int groups, int fpw, int sm_count,
                         cudaStream_t st);
+uint32_t trace_used_device(const uint32_t* ops, uint64_t nops, int rows, uint32_t nr, DevBuf& used,
+                           DevBuf& scratch, DevBuf& temp, int sm_count, cudaStream_t st);
 void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
-                       uint32_t* keys, uint64_t* vals, uint32_t* nvals, cudaStream_t st);
+                       uint32_t* keys, uint64_t* vals, uint32_t* nvals, const uint32_t* used,
+                       size_t nu, size_t groups, cudaStream_t st);
 void budget_keys_device(const double* d_budgets, const uint64_t* vals, const uint32_t* nvals,
                         size_t nr, int frames, int64_t* out, cudaStream_t st);
 void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, int rows,
@@ -433,23 +436,32 @@ bool graphs_enabled() {
 }
 
 void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
-                              const int16_t* dec, cudaStream_t st);
+                              const int16_t* dec, const uint32_t* used, size_t nu, cudaStream_t st);
+
+// SLICECRAFT_B200_RANK_USED=0: rank every rectangle even when the plan knows
+// which ones its candidates use
+bool rank_used_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_RANK_USED");
+  return !(v && v[0] == '0');
+}
 
 // K2 (f64 SAT) + K3 (time tables) from ctx->est.  The ~20 short launches of
 // this phase leave the device waiting on the host's launch rate, so when a
 // call repeats the previous call's shape and buffers (the steady state of a
 // frame pipeline) the phase is captured once into a CUDA graph and replayed.
 void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
-                         cudaStream_t st) {
+                         const uint32_t* used, size_t nu, cudaStream_t st) {
   const int16_t* dec = decode_table(ctx, g);
+  if (!rank_used_enabled() || nu == 0 || nu >= L.nr) used = nullptr, nu = 0;
   ctx->sat.ensure((size_t)L.frames * L.nsat * sizeof(double));
   ctx->rt_bits.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
   ctx->rt_search.ensure((size_t)L.groups * 2 * L.fpw * L.nr * sizeof(uint32_t));
   ctx->vals.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
   ctx->nvals.ensure((size_t)L.frames * sizeof(uint32_t));
   if (raw) ctx->rect_t.ensure((size_t)L.frames * L.nr * sizeof(double));
+  if (used) ctx->rk_bits_c.ensure(nu * (size_t)L.frames * sizeof(uint64_t));
   if (!graphs_enabled()) {
-    enqueue_time_tables_body(ctx, g, L, raw, dec, st);
+    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, st);
     return;
   }
   // everything a replay depends on: shape and every buffer address
@@ -460,7 +472,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
       (uintptr_t)ctx->rt_search.p, (uintptr_t)ctx->vals.p, (uintptr_t)ctx->nvals.p,
       (uintptr_t)ctx->rect_t.p, (uintptr_t)ctx->rk_idx.p,
       (uintptr_t)ctx->rk_sorted.p, (uintptr_t)ctx->rk_flags.p, (uintptr_t)ctx->rk_temp.p,
-      (uintptr_t)ctx->rk_temp.bytes};
+      (uintptr_t)ctx->rk_temp.bytes, (uintptr_t)used, (uintptr_t)nu, (uintptr_t)ctx->rk_bits_c.p};
   if (ctx->tt_exec && key == ctx->tt_key) {
     SCB_CUDA(cudaGraphLaunch(ctx->tt_exec, st));
     return;
@@ -471,7 +483,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   }
   if (key != ctx->tt_prev_key) {
     // first call of this shape: plain launches (they size the scratch buffers)
-    enqueue_time_tables_body(ctx, g, L, raw, dec, st);
+    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, st);
     ctx->tt_prev_key = key;
     return;
   }
@@ -479,7 +491,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   cudaGraph_t graph = nullptr;
   SCB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   try {
-    enqueue_time_tables_body(ctx, g, L, raw, dec, st);
+    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, st);
   } catch (...) {  // leave the stream out of capture mode before reporting
     cudaStreamEndCapture(st, &graph);
     if (graph) cudaGraphDestroy(graph);
@@ -494,7 +506,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
 }
 
 void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
-                              const int16_t* dec, cudaStream_t st) {
+                              const int16_t* dec, const uint32_t* used, size_t nu, cudaStream_t st) {
   // small grids: the whole phase in one CTA per frame (small_tables.cu);
   // SLICECRAFT_B200_SMALL_TABLES=0 keeps the general pipeline
   const char* sv = getenv("SLICECRAFT_B200_SMALL_TABLES");
@@ -511,7 +523,7 @@ void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, b
   // exact per-frame ranks of the times (rank.cu) -> 32-bit search keys
   rank_times_device(ctx, ctx->rt_bits.as<uint64_t>(), L.nr, L.frames, L.fpw,
                     ctx->rt_search.as<uint32_t>(), ctx->vals.as<uint64_t>(),
-                    ctx->nvals.as<uint32_t>(), st);
+                    ctx->nvals.as<uint32_t>(), used, nu, (size_t)L.groups, st);
   split_table_device(ctx->rt_search.as<uint32_t>(), g.cols, g.rows, L.groups, L.fpw, ctx->sm_count,
                      st);
 }
@@ -651,6 +663,14 @@ bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& c
   p->trace_nskel = th.nskel;
   p->trace_chunks = th.n_chunks;
   p->trace_state = 1;
+  {  // the rectangles the candidates use (later calls rank only these)
+    DevBuf sc2, tmp2;
+    p->n_used = trace_used_device(p->tr_ops.as<uint32_t>(), th.ops, g.rows,
+                                  (uint32_t)((size_t)n_xw(g.cols) * n_yh(g.rows)), p->tr_used, sc2,
+                                  tmp2, ctx->sm_count, st);
+    sc2.release();
+    tmp2.release();
+  }
   return true;
 }
 
@@ -1230,7 +1250,9 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
     ctx->est.ensure((size_t)frames * cells * sizeof(double));
     SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
                              cudaMemcpyDefault, s));
-    enqueue_time_tables(ctx, g, L, false, s);
+    // a plan that has its trace ranks only the rectangles its candidates use
+    enqueue_time_tables(ctx, g, L, false, plan->n_used ? plan->tr_used.as<uint32_t>() : nullptr,
+                        plan->n_used, s);
     SCB_CUDA(cudaEventRecord(ev[1], s));
     if (do1) {
       enqueue_step(ctx, g, cfg, plan, L, 1, true, s);
@@ -1438,7 +1460,7 @@ sc_ctx::~sc_ctx() {
   if (tt_exec) cudaGraphExecDestroy(tt_exec);
   for (auto* b : {&luma, &records, &est, &sat, &rect_t, &rect_s, &rt_search, &rs_search, &usat,
                   &lanes, &snaps, &frame_best, &counter, &budget, &scratch, &dec, &lbr, &lbm, &inc, &seed_inc, &rt_bits, &vals, &nvals, &budget_f64, &rk_idx, &rk_sorted,
-                  &rk_flags, &rk_offsets, &rk_temp, &sse_inc, &flt_idx, &flt_flag, &flt_list,
+                  &rk_flags, &rk_offsets, &rk_temp, &rk_bits_c, &sse_inc, &flt_idx, &flt_flag, &flt_list,
                   &flt_count, &flt_temp, &slice_maps, &owner, &vcheck, &val_in, &enum_out,
                   &enum_temp, &rest_of, &rss, &fin_scratch})
     b->release();
@@ -1455,7 +1477,8 @@ sc_ctx::~sc_ctx() {
     p->d_cost.release();
     p->d_enum_counts.release();
     p->d_enum_offsets.release();
-    for (auto* b : {&p->tr_ops, &p->tr_skel_pos, &p->tr_skel_ord, &p->tr_chunk_skel, &p->tr_skip})
+    for (auto* b : {&p->tr_ops, &p->tr_skel_pos, &p->tr_skel_ord, &p->tr_chunk_skel, &p->tr_skip,
+                    &p->tr_used})
       b->release();
     delete p;
   }
@@ -1636,7 +1659,7 @@ sc_status sc_grid_tables(sc_ctx* ctx, const sc_grid* grid, const double* est,
     ctx->est.ensure((size_t)frames * cells * sizeof(double));
     SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
                              cudaMemcpyDefault, s));
-    enqueue_time_tables(ctx, g, L, true, s);
+    enqueue_time_tables(ctx, g, L, true, nullptr, 0, s);
     if (records) {
       ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
       SCB_CUDA(cudaMemcpyAsync(ctx->records.p, records, cells * frames * sizeof(sc_ctu_record),

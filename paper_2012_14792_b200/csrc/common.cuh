@@ -156,6 +156,8 @@ struct Plan {
   uint64_t trace_shard_key = ~0ull, trace_shard_cands = 0;  // candidates of one shard
   DevBuf tr_ops, tr_skel_pos, tr_skel_ord, tr_chunk_skel;
   DevBuf tr_skip;         // step 2: subtree ends (trace.cu k_trace_skips)
+  DevBuf tr_used;         // ascending indices of the rectangles the candidates use
+  uint32_t n_used = 0;    // (0: unknown -- every rectangle is ranked)
   bool have_skip = false;
   // step 2's walk per lambda, measured on the first call (api.cu enqueue_step)
   std::vector<std::pair<double, int>> step2_choice;
@@ -266,7 +268,7 @@ struct sc_ctx {
   std::vector<uintptr_t> tt_key, tt_prev_key;
   cudaGraphExec_t tt_exec = nullptr;
   scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
-  scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp;       // rank.cu scratch
+  scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp, rk_bits_c;  // rank.cu scratch
   scb::DevBuf flt_idx, flt_flag, flt_list, flt_count, flt_temp;      // item filter (search.cu)
   // device post-check of the returned partitions (validate.cu): CTU -> slice
   // id maps [2][frames][cells] of the last search, owner scratch, verdicts

@@ -261,9 +261,12 @@ __global__ void k_rank_flags32(const uint32_t* __restrict__ idx, const uint64_t*
     flags[i] = (i % nr == 0 || bits[idx[i]] != bits[idx[i - 1]]) ? 1u : 0u;
 }
 
+// nr: ranked rectangles per frame; nr_full / used: the grid's rectangle count
+// and the ranked rectangles' indices (used == nullptr: all of them, in place)
 __global__ void k_rank_scatter32(const uint32_t* __restrict__ idx, const uint64_t* __restrict__ bits,
                                  const uint32_t* __restrict__ flags,
                                  const uint32_t* __restrict__ scan, size_t nr, int frames, int fpw,
+                                 size_t nr_full, const uint32_t* __restrict__ used,
                                  uint32_t* __restrict__ keys, uint64_t* __restrict__ vals,
                                  uint32_t* __restrict__ nvals) {
   const size_t total = nr * (size_t)frames;
@@ -273,11 +276,24 @@ __global__ void k_rank_scatter32(const uint32_t* __restrict__ idx, const uint64_
     const size_t start = f * nr;
     const uint32_t key = scan[i] - scan[start];
     const uint32_t e = idx[i];
-    const uint32_t rect = (uint32_t)(e - start);
+    uint32_t rect = (uint32_t)(e - start);
+    if (used) rect = used[rect];
     const size_t g = f / fpw, slot = f % fpw;
-    keys[(g * 2 * nr + rect) * fpw + slot] = key;  // [group][rt | rts][rect][fpw]
-    if (flags[i]) vals[start + key] = bits[e];
+    keys[(g * 2 * nr_full + rect) * fpw + slot] = key;  // [group][rt | rts][rect][fpw]
+    if (flags[i]) vals[f * nr_full + key] = bits[e];
     if (i == start + nr - 1) nvals[f] = key + 1;
+  }
+}
+
+// bits_c[f][u] = bits[f][used[u]]
+__global__ void k_rank_gather(const uint64_t* __restrict__ bits, size_t nr_full,
+                              const uint32_t* __restrict__ used, size_t nu, int frames,
+                              uint64_t* __restrict__ out) {
+  const size_t total = nu * (size_t)frames;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t f = i / nu, u = i % nu;
+    out[i] = bits[f * nr_full + used[u]];
   }
 }
 
@@ -286,11 +302,27 @@ bool rank64_requested() {
   return v && std::string(v) == "sort64";
 }
 
+// used / nu: rank only these rectangles (the ones the plan's candidates use,
+// trace.cu); every other rectangle gets the key "infinite" (all ones), which
+// bounds and walks treat as a slice no candidate can take.
 void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
-                       uint32_t* keys, uint64_t* vals, uint32_t* nvals, cudaStream_t st) {
+                       uint32_t* keys, uint64_t* vals, uint32_t* nvals, const uint32_t* used,
+                       size_t nu, size_t groups, cudaStream_t st) {
   if (rank64_requested()) {
     rank_times_sort64(ctx, bits_fm, nr, frames, fpw, keys, vals, nvals, st);
     return;
+  }
+  const size_t nr_full = nr;
+  if (used) {
+    ctx->rk_bits_c.ensure(nu * (size_t)frames * sizeof(uint64_t));
+    const unsigned gb =
+        (unsigned)std::min<size_t>((nu * frames + 255) / 256, (size_t)ctx->sm_count * 8);
+    k_rank_gather<<<gb, 256, 0, st>>>(bits_fm, nr_full, used, nu, frames,
+                                      ctx->rk_bits_c.as<uint64_t>());
+    SCB_CUDA(cudaGetLastError());
+    SCB_CUDA(cudaMemsetAsync(keys, 0xff, groups * 2 * nr_full * (size_t)fpw * sizeof(uint32_t), st));
+    bits_fm = ctx->rk_bits_c.as<uint64_t>();
+    nr = nu;
   }
   const size_t total = nr * (size_t)frames;
   if (total >= (1ull << 32) || frames > (1 << 10))
@@ -338,8 +370,8 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   k_rank_flags32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, nr, total);
   SCB_CUDA(cudaGetLastError());
   SCB_CUDA(cub::DeviceScan::InclusiveSum(ctx->rk_temp.p, b3, flags, scan, (int)total, st));
-  k_rank_scatter32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, scan, nr, frames, fpw, keys, vals,
-                                           nvals);
+  k_rank_scatter32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, scan, nr, frames, fpw, nr_full,
+                                           used, keys, vals, nvals);
   SCB_CUDA(cudaGetLastError());
 }
 

@@ -21,6 +21,8 @@
 // the lanes; the winner's layout is rebuilt from its skeleton's ops
 // (trace_layout) into the same FrameBest record the walk kernels produce.
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "common.cuh"
 #include "search_walk.cuh"
@@ -917,6 +919,69 @@ void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const
                                                     count, lambda, vals, nvals, nr, out,
                                                     budget_out);
   SCB_CUDA(cudaGetLastError());
+}
+
+// ---- the rectangles a plan's candidates use ---------------------------------------
+// Every rectangle that is a slice of some candidate: the keys the ops read
+// (rt entries directly; a split-table entry stands for the run and its forced
+// rest).  Under the area test most rectangles of a grid are never a slice
+// (cfg3: 32 % are), so the per-call time-key ranking (rank.cu) only ranks
+// these; the others keep the key "infinite", which no candidate reads.
+__global__ void k_trace_mark(const uint32_t* __restrict__ ops, uint64_t nops, uint32_t nr,
+                             uint8_t* __restrict__ used_rt, uint8_t* __restrict__ used_rts) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nops;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t op = ops[p];
+    const uint32_t kidx = tr_kidx(op);
+    if (tr_is_push(op)) {
+      if (kidx >= nr) used_rts[kidx - nr] = 1;
+      else used_rt[kidx] = 1;
+    } else if (tr_code(op) == kOpLeaf) {
+      const int cnt = tr_leaf_cnt(op);
+      for (int i = 0; i < cnt; ++i) used_rts[kidx - nr + i] = 1;
+    } else if (tr_is_fix(op)) {
+      used_rt[kidx] = 1;
+    }
+  }
+}
+
+__global__ void k_trace_used_close(int rows, uint32_t nr, uint8_t* __restrict__ used_rt,
+                                   const uint8_t* __restrict__ used_rts) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nr || !used_rts[idx]) return;
+  const int nyh = rows * (rows + 1) / 2;
+  const int xw = (int)(idx / (uint32_t)nyh), yh = (int)(idx % (uint32_t)nyh);
+  int y0 = 0;
+  while (y0 + 1 < rows && tr_yh(rows, y0 + 1, 1) <= yh) ++y0;
+  const int h = yh - tr_yh(rows, y0, 1) + 1;
+  used_rt[idx] = 1;
+  if (y0 + h < rows) used_rt[(uint32_t)(xw * nyh + tr_yh(rows, y0 + h, rows - y0 - h))] = 1;
+}
+
+// The ascending list of used rectangle indices (once per plan); returns its length.
+uint32_t trace_used_device(const uint32_t* ops, uint64_t nops, int rows, uint32_t nr, DevBuf& used,
+                           DevBuf& scratch, DevBuf& temp, int sm_count, cudaStream_t st) {
+  scratch.ensure((size_t)nr * 2 + 16);
+  uint8_t* f_rt = scratch.as<uint8_t>();
+  uint8_t* f_rts = f_rt + nr;
+  SCB_CUDA(cudaMemsetAsync(f_rt, 0, (size_t)nr * 2, st));
+  k_trace_mark<<<sm_count * 8, 256, 0, st>>>(ops, nops, nr, f_rt, f_rts);
+  SCB_CUDA(cudaGetLastError());
+  k_trace_used_close<<<(nr + 255) / 256, 256, 0, st>>>(rows, nr, f_rt, f_rts);
+  SCB_CUDA(cudaGetLastError());
+  used.ensure((size_t)nr * sizeof(uint32_t) + 16);
+  uint32_t* d_count = used.as<uint32_t>() + nr;
+  size_t tb = 0;
+  cub::CountingInputIterator<uint32_t> iota(0);
+  SCB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota, f_rt, used.as<uint32_t>(), d_count,
+                                      (int)nr, st));
+  temp.ensure(tb + 16);
+  SCB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota, f_rt, used.as<uint32_t>(), d_count,
+                                      (int)nr, st));
+  uint32_t n = 0;
+  SCB_CUDA(cudaMemcpyAsync(&n, d_count, 4, cudaMemcpyDeviceToHost, st));
+  SCB_CUDA(cudaStreamSynchronize(st));
+  return n;
 }
 
 // ---- step 2 host side --------------------------------------------------------------
