@@ -330,10 +330,13 @@ def run_ours(args):
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     phase = np.zeros(8)
+    lib().sc_kernel_launches.restype = C.c_uint64
+    launches0 = int(lib().sc_kernel_launches())
     e0.record(stream)
     for _ in range(args.steps):
         phase += np.array(call(luma_d.data_ptr(), est_d.data_ptr()))
     e1.record(stream)
+    launches_timed = int(lib().sc_kernel_launches()) - launches0
     torch.cuda.synchronize()
     barrier()
     ck = clocks.stop()
@@ -467,9 +470,15 @@ def run_ours(args):
         # kernels per step counted from the CUDA activity trace of one extra
         # untimed call (every kernel is the library's own or a CUB kernel
         # instantiated inside it), times the timed steps
-        "gpu_launches": (args.steps * n_launch) if n_launch else None,
-        "gpu_launches_per_step": launch_names or None,
-        "gpu_launches_source": launch_src,
+        # kernels launched inside the timed region: the library's own count
+        # (every launch goes through its SCB_LAUNCH macro; graph replays add
+        # their captured kernels); beside it the CUDA activity trace of one
+        # extra untimed call, when CUPTI delivers one
+        "gpu_launches": launches_timed,
+        "gpu_launches_source": "sc_kernel_launches() delta over the timed region",
+        "gpu_launches_per_step_traced": launch_names or None,
+        "gpu_launches_traced_total": (args.steps * n_launch) if n_launch else None,
+        "gpu_launches_trace_source": launch_src,
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_extra and args.mode == 0:

@@ -157,6 +157,12 @@ typedef struct sc_ctx sc_ctx;
 
 /* ---- errors / version --------------------------------------------------- */
 const char* sc_last_error(void);
+
+/* Kernels the library has launched in this process so far (its own kernels
+ * and the CUB kernels it instantiates; a CUDA-graph replay counts the kernels
+ * captured in it).  For launch accounting in benchmarks (bench.py's
+ * gpu_launches); no reference counterpart. */
+uint64_t sc_kernel_launches(void);
 int sc_abi_version(void);
 
 /* ---- geometry (grid.cpp:9-32, CtuGrid::make) ---------------------------- */

@@ -92,6 +92,7 @@ class ShardBest(C.Structure):
 _P = C.c_void_p
 SIGNATURES = [
     ("sc_last_error", C.c_char_p, []),
+    ("sc_kernel_launches", C.c_uint64, []),
     ("sc_abi_version", C.c_int, []),
     ("sc_grid_make", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(Grid)]),
     ("sc_temporal_layer", C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32)]),

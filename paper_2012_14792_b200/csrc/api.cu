@@ -17,6 +17,13 @@
 #include "common.cuh"
 
 namespace scb {
+uint64_t& launch_counter() {
+  static uint64_t n = 0;
+  return n;
+}
+}  // namespace scb
+
+namespace scb {
 // kernels (texture.cu, tables.cu, search.cu)
 void texture_moments_device(const void* d_luma, int bps, int W, int H, size_t pitch,
                             size_t fstride, int ctu, int frames, int cols, int rows,
@@ -475,6 +482,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
       (uintptr_t)ctx->rk_temp.bytes, (uintptr_t)used, (uintptr_t)nu, (uintptr_t)ctx->rk_bits_c.p};
   if (ctx->tt_exec && key == ctx->tt_key) {
     SCB_CUDA(cudaGraphLaunch(ctx->tt_exec, st));
+    count_launches(ctx->tt_launches);  // the kernels of the captured phase
     return;
   }
   if (ctx->tt_exec) {
@@ -489,6 +497,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   }
   // second call of the same shape: capture, instantiate, launch
   cudaGraph_t graph = nullptr;
+  const uint64_t launches_before = launch_counter();
   SCB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   try {
     enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, st);
@@ -502,6 +511,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   SCB_CUDA(cudaGraphInstantiate(&ctx->tt_exec, graph, 0));
   cudaGraphDestroy(graph);
   ctx->tt_key = key;
+  ctx->tt_launches = launch_counter() - launches_before;
   SCB_CUDA(cudaGraphLaunch(ctx->tt_exec, st));
 }
 
@@ -1258,13 +1268,13 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
       enqueue_step(ctx, g, cfg, plan, L, 1, true, s);
       if (do2 && has_comm(ctx)) {  // step 2's budget from the global t_min
         ctx->gtmin.ensure((size_t)frames * sizeof(uint64_t));
-        k_tmin_gather<<<(frames + 127) / 128, 128, 0, s>>>(ctx->frame_best.as<FrameBest>(), frames,
-                                                            ctx->gtmin.as<uint64_t>());
+        SCB_LAUNCH(k_tmin_gather<<<(frames + 127) / 128, 128, 0, s>>>(ctx->frame_best.as<FrameBest>(), frames,
+                                                            ctx->gtmin.as<uint64_t>()));
         SCB_CUDA(cudaGetLastError());
         comm_min_u64(ctx, ctx->gtmin.as<uint64_t>(), (size_t)frames, s);
-        k_budget_from_tmin<<<(frames + 127) / 128, 128, 0, s>>>(
+        SCB_LAUNCH(k_budget_from_tmin<<<(frames + 127) / 128, 128, 0, s>>>(
             ctx->gtmin.as<uint64_t>(), frames, cfg.lambda, ctx->vals.as<uint64_t>(),
-            ctx->nvals.as<uint32_t>(), L.nr, L.fpw, ctx->budget.as<int64_t>());
+            ctx->nvals.as<uint32_t>(), L.nr, L.fpw, ctx->budget.as<int64_t>()));
         SCB_CUDA(cudaGetLastError());
       }
     } else {
@@ -1506,6 +1516,8 @@ bool layout_less(const sc_layout& a, const sc_layout& b) {
 }
 
 extern "C" {
+
+uint64_t sc_kernel_launches(void) { return scb::launch_counter(); }
 
 const char* sc_last_error(void) { return g_last_error.c_str(); }
 int sc_abi_version(void) { return SC_ABI_VERSION; }

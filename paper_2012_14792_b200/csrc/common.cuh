@@ -32,6 +32,18 @@ struct Fail {
       ::scb::fail(SC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// ---- kernel-launch accounting ---------------------------------------------------
+// Every kernel launch of the library goes through SCB_LAUNCH, which counts it
+// (sc_kernel_launches).  CUB calls add their kernels by count_launches(n); a
+// CUDA-graph replay adds the launches counted while the graph was captured.
+uint64_t& launch_counter();  // process-wide (api.cu); host-side, one writer per stream of calls
+inline void count_launches(uint64_t n) { launch_counter() += n; }
+#define SCB_LAUNCH(...)          \
+  do {                           \
+    ::scb::count_launches(1);    \
+    __VA_ARGS__;                 \
+  } while (0)
+
 // ---- per-device kernel attributes ---------------------------------------------
 // cudaFuncSetAttribute acts on the current device only, so an opt-in (e.g. the
 // dynamic shared-memory limit) is applied once per (device, kernel), under a
@@ -267,6 +279,7 @@ struct sc_ctx {
   // CUDA graph, replayed while the call shape and buffers repeat (api.cu)
   std::vector<uintptr_t> tt_key, tt_prev_key;
   cudaGraphExec_t tt_exec = nullptr;
+  uint64_t tt_launches = 0;  // kernels in the captured time-table phase
   scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
   scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp, rk_bits_c;  // rank.cu scratch
   scb::DevBuf flt_idx, flt_flag, flt_list, flt_count, flt_temp;      // item filter (search.cu)

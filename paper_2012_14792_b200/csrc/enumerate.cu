@@ -142,13 +142,14 @@ void enumerate_count_device(const WorkItem* d_items, uint32_t n_items, int cols,
                             double k, int covering, uint64_t* d_counts, uint64_t* d_offsets,
                             DevBuf& temp, cudaStream_t st) {
   if (!n_items) return;
-  k_enumerate<false><<<(n_items + 127) / 128, 128, 0, st>>>(
-      d_items, n_items, cols, rows, n, k, covering, d_counts, nullptr, 0, 0, nullptr);
+  SCB_LAUNCH(k_enumerate<false><<<(n_items + 127) / 128, 128, 0, st>>>(
+      d_items, n_items, cols, rows, n, k, covering, d_counts, nullptr, 0, 0, nullptr));
   SCB_CUDA(cudaGetLastError());
   size_t tb = 0;
   SCB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, d_counts, d_offsets, (int)n_items, st));
   temp.ensure(tb + 16);
   SCB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, d_counts, d_offsets, (int)n_items, st));
+  count_launches(2);  // CUB scan: init + scan
 }
 
 void enumerate_emit_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
@@ -156,9 +157,9 @@ void enumerate_emit_device(const WorkItem* d_items, uint32_t n_items, int cols, 
                            const uint64_t* d_offsets, uint64_t first, uint64_t limit,
                            uint8_t* d_out, cudaStream_t st) {
   if (!n_items || !limit) return;
-  k_enumerate<true><<<(n_items + 127) / 128, 128, 0, st>>>(
+  SCB_LAUNCH(k_enumerate<true><<<(n_items + 127) / 128, 128, 0, st>>>(
       d_items, n_items, cols, rows, n, k, covering, const_cast<uint64_t*>(d_counts), d_offsets,
-      first, limit, d_out);
+      first, limit, d_out));
   SCB_CUDA(cudaGetLastError());
 }
 

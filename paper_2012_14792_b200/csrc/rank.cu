@@ -104,7 +104,7 @@ void rank_times_sort64(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   int fbits = 1;
   while ((1 << fbits) < frames) ++fbits;
   const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, (size_t)ctx->sm_count * 8);
-  k_rank_prepare<<<blocks, 256, 0, st>>>(packed_in, nr, frames);
+  SCB_LAUNCH(k_rank_prepare<<<blocks, 256, 0, st>>>(packed_in, nr, frames));
   SCB_CUDA(cudaGetLastError());
   size_t b1 = 0, b2 = 0, b3 = 0;
   SCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, bits_fm, sorted_bits, packed_in, packed,
@@ -115,15 +115,18 @@ void rank_times_sort64(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   ctx->rk_temp.ensure(std::max(b1, std::max(b2, b3)));
   SCB_CUDA(cub::DeviceRadixSort::SortPairs(ctx->rk_temp.p, b1, bits_fm, sorted_bits, packed_in,
                                            packed, (int)total, 0, 64, st));
-  k_rank_split<<<blocks, 256, 0, st>>>(packed, fkey_in, pos_in, total);
+  count_launches(10);  // CUB onesweep, 64-bit keys
+  SCB_LAUNCH(k_rank_split<<<blocks, 256, 0, st>>>(packed, fkey_in, pos_in, total));
   SCB_CUDA(cudaGetLastError());
   SCB_CUDA(cub::DeviceRadixSort::SortPairs(ctx->rk_temp.p, b2, fkey_in, fkey_out, pos_in, pos,
                                            (int)total, 0, fbits, st));
-  k_rank_flags<<<blocks, 256, 0, st>>>(sorted_bits, pos, flags, nr, frames);
+  count_launches(4);  // CUB onesweep (frame keys; at most two passes)
+  SCB_LAUNCH(k_rank_flags<<<blocks, 256, 0, st>>>(sorted_bits, pos, flags, nr, frames));
   SCB_CUDA(cudaGetLastError());
   SCB_CUDA(cub::DeviceScan::InclusiveSum(ctx->rk_temp.p, b3, flags, scan, (int)total, st));
-  k_rank_scatter<<<blocks, 256, 0, st>>>(sorted_bits, packed, pos, flags, scan, nr, frames, fpw,
-                                         keys, vals, nvals);
+  count_launches(2);  // CUB scan: init + scan
+  SCB_LAUNCH(k_rank_scatter<<<blocks, 256, 0, st>>>(sorted_bits, packed, pos, flags, scan, nr, frames, fpw,
+                                         keys, vals, nvals));
   SCB_CUDA(cudaGetLastError());
 }
 
@@ -317,8 +320,8 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
     ctx->rk_bits_c.ensure(nu * (size_t)frames * sizeof(uint64_t));
     const unsigned gb =
         (unsigned)std::min<size_t>((nu * frames + 255) / 256, (size_t)ctx->sm_count * 8);
-    k_rank_gather<<<gb, 256, 0, st>>>(bits_fm, nr_full, used, nu, frames,
-                                      ctx->rk_bits_c.as<uint64_t>());
+    SCB_LAUNCH(k_rank_gather<<<gb, 256, 0, st>>>(bits_fm, nr_full, used, nu, frames,
+                                      ctx->rk_bits_c.as<uint64_t>()));
     SCB_CUDA(cudaGetLastError());
     SCB_CUDA(cudaMemsetAsync(keys, 0xff, groups * 2 * nr_full * (size_t)fpw * sizeof(uint32_t), st));
     bits_fm = ctx->rk_bits_c.as<uint64_t>();
@@ -352,9 +355,9 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   SCB_CUDA(cudaMemsetAsync(lo, 0xff, (size_t)frames * sizeof(uint64_t), st));
   SCB_CUDA(cudaMemsetAsync(hi, 0, (size_t)frames * sizeof(uint64_t) + 16, st));  // + big_count
   const unsigned rb = (unsigned)std::max<size_t>(1, std::min<size_t>((nr + 255) / 256, 16));
-  k_rank_range<<<dim3(rb, frames), 256, 0, st>>>(bits_fm, nr, lo, hi);
+  SCB_LAUNCH(k_rank_range<<<dim3(rb, frames), 256, 0, st>>>(bits_fm, nr, lo, hi));
   SCB_CUDA(cudaGetLastError());
-  k_rank_key32<<<blocks, 256, 0, st>>>(bits_fm, nr, frames, fbits, kbits, lo, hi, key_in, val_in);
+  SCB_LAUNCH(k_rank_key32<<<blocks, 256, 0, st>>>(bits_fm, nr, frames, fbits, kbits, lo, hi, key_in, val_in));
   SCB_CUDA(cudaGetLastError());
   size_t b1 = 0, b3 = 0;
   SCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, key_in, key_out, val_in, idx, (int)total,
@@ -363,15 +366,17 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   ctx->rk_temp.ensure(std::max(b1, b3));
   SCB_CUDA(cub::DeviceRadixSort::SortPairs(ctx->rk_temp.p, b1, key_in, key_out, val_in, idx,
                                            (int)total, 0, kbits, st));
-  k_rank_groups<<<blocks, 256, 0, st>>>(key_out, idx, bits_fm, total, big_count, big_list);
+  count_launches(2 + (kbits + 7) / 8);  // CUB onesweep: histogram, exclusive sum, one kernel per 8-bit pass
+  SCB_LAUNCH(k_rank_groups<<<blocks, 256, 0, st>>>(key_out, idx, bits_fm, total, big_count, big_list));
   SCB_CUDA(cudaGetLastError());
-  k_rank_big<<<ctx->sm_count, 256, 0, st>>>(idx, bits_fm, big_count, big_list, tmp);
+  SCB_LAUNCH(k_rank_big<<<ctx->sm_count, 256, 0, st>>>(idx, bits_fm, big_count, big_list, tmp));
   SCB_CUDA(cudaGetLastError());
-  k_rank_flags32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, nr, total);
+  SCB_LAUNCH(k_rank_flags32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, nr, total));
   SCB_CUDA(cudaGetLastError());
   SCB_CUDA(cub::DeviceScan::InclusiveSum(ctx->rk_temp.p, b3, flags, scan, (int)total, st));
-  k_rank_scatter32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, scan, nr, frames, fpw, nr_full,
-                                           used, keys, vals, nvals);
+  count_launches(2);  // CUB scan: init + scan
+  SCB_LAUNCH(k_rank_scatter32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, scan, nr, frames, fpw, nr_full,
+                                           used, keys, vals, nvals));
   SCB_CUDA(cudaGetLastError());
 }
 
@@ -398,7 +403,7 @@ __global__ void k_budget_keys(const double* __restrict__ budgets, const uint64_t
 
 void budget_keys_device(const double* d_budgets, const uint64_t* vals, const uint32_t* nvals,
                         size_t nr, int frames, int64_t* out, cudaStream_t st) {
-  k_budget_keys<<<(frames + 127) / 128, 128, 0, st>>>(d_budgets, vals, nvals, nr, frames, out);
+  SCB_LAUNCH(k_budget_keys<<<(frames + 127) / 128, 128, 0, st>>>(d_budgets, vals, nvals, nr, frames, out));
   SCB_CUDA(cudaGetLastError());
 }
 

@@ -289,12 +289,12 @@ void column_bounds_launch(const uint32_t* rt, int fpw, int frames_in_group, int 
       SCB_CUDA(cudaFuncSetAttribute(k_column_bounds_blk,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     });
-    k_column_bounds_blk<<<nxw, 256, smem, st>>>(rt, fpw, frames_in_group, rows, rmax, rstride,
-                                                lbr, lbm);
+    SCB_LAUNCH(k_column_bounds_blk<<<nxw, 256, smem, st>>>(rt, fpw, frames_in_group, rows, rmax, rstride,
+                                                lbr, lbm));
   } else {  // tall grids: one thread per (column, frame)
     const int threads = 128, total = nxw * fpw;
-    k_column_bounds<<<(total + threads - 1) / threads, threads, 0, st>>>(
-        rt, fpw, frames_in_group, cols, rows, rmax, rstride, lbr, lbm);
+    SCB_LAUNCH(k_column_bounds<<<(total + threads - 1) / threads, threads, 0, st>>>(
+        rt, fpw, frames_in_group, cols, rows, rmax, rstride, lbr, lbm));
   }
   SCB_CUDA(cudaGetLastError());
 }
@@ -453,9 +453,9 @@ template <int FPW, int STEP>
 static void launch_fpw(const SearchArgs& a, int blocks, size_t smem, cudaStream_t st) {
   set_search_attrs<FPW, STEP>();
   if (a.prune)
-    search_kernel<FPW, STEP, true>()<<<blocks, SearchShape<STEP, true>::kBlock, smem, st>>>(a);
+    SCB_LAUNCH(search_kernel<FPW, STEP, true>()<<<blocks, SearchShape<STEP, true>::kBlock, smem, st>>>(a));
   else
-    search_kernel<FPW, STEP, false>()<<<blocks, SearchShape<STEP, false>::kBlock, smem, st>>>(a);
+    SCB_LAUNCH(search_kernel<FPW, STEP, false>()<<<blocks, SearchShape<STEP, false>::kBlock, smem, st>>>(a));
 }
 
 int search_blocks_per_sm(int fpw, int step, bool prune, size_t smem) {
@@ -563,10 +563,10 @@ void item_filter_launch(sc_ctx* ctx, const SearchArgs& a, uint32_t k0, uint32_t 
   ctx->flt_flag.ensure((size_t)(m + 1));
   const int rstride = std::min(a.n, a.rows) + 1;
   if (m) {
-    k_item_filter<<<(m + 255) / 256, 256, 0, st>>>(
+    SCB_LAUNCH(k_item_filter<<<(m + 255) / 256, 256, 0, st>>>(
         a.items, k0, k1, a.item_offset, a.item_stride, a.cols, a.rows, a.n, a.max_area, rstride,
         a.bmax, a.lbm, fpw, frames, step, a.inc, seed_inc, a.budget, ctx->flt_idx.as<uint32_t>(),
-        ctx->flt_flag.as<uint8_t>());
+        ctx->flt_flag.as<uint8_t>()));
     SCB_CUDA(cudaGetLastError());
   }
   size_t tb = 0;
@@ -575,6 +575,7 @@ void item_filter_launch(sc_ctx* ctx, const SearchArgs& a, uint32_t k0, uint32_t 
   ctx->flt_temp.ensure(tb + 16);
   SCB_CUDA(cub::DeviceSelect::Flagged(ctx->flt_temp.p, tb, ctx->flt_idx.as<uint32_t>(),
                                       ctx->flt_flag.as<uint8_t>(), list, count, (int)m, st));
+  count_launches(2);  // CUB select: init + sweep
 }
 
 void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_warps,
@@ -587,11 +588,11 @@ void finalize_launch(int step, int n, int fpw, int frames_in_group, uint32_t n_w
   scratch.ensure((size_t)frames_in_group * parts * (sizeof(LaneBest) + sizeof(uint32_t)));
   LaneBest* pb = scratch.as<LaneBest>();
   uint32_t* pl = reinterpret_cast<uint32_t*>(pb + (size_t)frames_in_group * parts);
-  k_finalize_part<<<dim3(parts, frames_in_group), 256, 0, st>>>(step, n, fpw, n_warps, lanes, snaps,
-                                                                pb, pl);
+  SCB_LAUNCH(k_finalize_part<<<dim3(parts, frames_in_group), 256, 0, st>>>(step, n, fpw, n_warps, lanes, snaps,
+                                                                pb, pl));
   SCB_CUDA(cudaGetLastError());
-  k_finalize<<<frames_in_group, 256, 0, st>>>(step, n, parts, frames_in_group, pb, pl, snaps, count,
-                                              scored, lambda, vals, nvals, nr, out, budget_out);
+  SCB_LAUNCH(k_finalize<<<frames_in_group, 256, 0, st>>>(step, n, parts, frames_in_group, pb, pl, snaps, count,
+                                              scored, lambda, vals, nvals, nr, out, budget_out));
   SCB_CUDA(cudaGetLastError());
 }
 

@@ -182,8 +182,8 @@ bool small_tables_device(const double* d_est, int cols, int rows, int frames, in
     SCB_CUDA(cudaFuncSetAttribute(k_small_tables, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   max_dynamic_smem((const void*)k_small_tables)));
   });
-  k_small_tables<<<frames, kSmallThreads, smem, st>>>(d_est, cols, rows, frames, fpw, d_dec, keys,
-                                                      vals, nvals);
+  SCB_LAUNCH(k_small_tables<<<frames, kSmallThreads, smem, st>>>(d_est, cols, rows, frames, fpw, d_dec, keys,
+                                                      vals, nvals));
   SCB_CUDA(cudaGetLastError());
   return true;
 }

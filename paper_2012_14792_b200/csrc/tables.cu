@@ -183,7 +183,7 @@ void split_table_device(uint32_t* d_keys, int cols, int rows, int groups, int fp
   const size_t cap = (size_t)sm_count * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_split_table<<<(unsigned)blocks, 256, 0, st>>>(d_keys, cols, rows, (size_t)groups * fpw, fpw);
+  SCB_LAUNCH(k_split_table<<<(unsigned)blocks, 256, 0, st>>>(d_keys, cols, rows, (size_t)groups * fpw, fpw));
   SCB_CUDA(cudaGetLastError());
 }
 
@@ -245,8 +245,8 @@ __global__ void k_partition_eval(const double* __restrict__ sat, const uint64_t*
 void partition_eval_device(const double* d_sat, const uint64_t* d_usat, const int* d_rects, int n,
                            int cols, int rows, int frames, sc_partition_stats* d_out,
                            double* d_slice_times, sc_ctu_record* d_slice_mom, cudaStream_t st) {
-  k_partition_eval<<<frames, 64, 0, st>>>(d_sat, d_usat, reinterpret_cast<const int4*>(d_rects),
-                                          n, cols, rows, d_out, d_slice_times, d_slice_mom);
+  SCB_LAUNCH(k_partition_eval<<<frames, 64, 0, st>>>(d_sat, d_usat, reinterpret_cast<const int4*>(d_rects),
+                                          n, cols, rows, d_out, d_slice_times, d_slice_mom));
   SCB_CUDA(cudaGetLastError());
 }
 
@@ -260,7 +260,7 @@ void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, 
                                   227 * 1024));
   });
   int threads = rows < 32 ? 32 : (rows > 1024 ? 1024 : ((rows + 31) / 32) * 32);
-  k_grid_sat<<<frames, threads, smem, st>>>(d_est, d_rec, cols, rows, d_sat, d_usat);
+  SCB_LAUNCH(k_grid_sat<<<frames, threads, smem, st>>>(d_est, d_rec, cols, rows, d_sat, d_usat));
   SCB_CUDA(cudaGetLastError());
 }
 
@@ -275,8 +275,8 @@ void rect_tables_device(const double* d_sat, const uint64_t* d_usat, const int16
   const size_t cap = (size_t)sm_count * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_rect_tables<<<(unsigned)blocks, 256, 0, st>>>(d_sat, d_usat, dec, cols, rows, frames, fpw,
-                                                  d_rect_t, d_rect_s, d_rt, d_rs);
+  SCB_LAUNCH(k_rect_tables<<<(unsigned)blocks, 256, 0, st>>>(d_sat, d_usat, dec, cols, rows, frames, fpw,
+                                                  d_rect_t, d_rect_s, d_rt, d_rs));
   SCB_CUDA(cudaGetLastError());
 }
 

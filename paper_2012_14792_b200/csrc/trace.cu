@@ -767,8 +767,8 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
   uint64_t* o_cand = o_ops + n_items;
   uint64_t* o_skel = o_cand + n_items;
   const unsigned blocks = (n_items + 127) / 128;
-  k_trace_count<<<blocks, 128, 0, st>>>(d_items, n_items, cols, rows, n, k, covering, c_ops, c_cand,
-                                        c_skel);
+  SCB_LAUNCH(k_trace_count<<<blocks, 128, 0, st>>>(d_items, n_items, cols, rows, n, k, covering, c_ops, c_cand,
+                                        c_skel));
   SCB_CUDA(cudaGetLastError());
   size_t tb = 0;
   SCB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c_ops, o_ops, (int)n_items, st));
@@ -776,6 +776,7 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
   for (int i = 0; i < 3; ++i)
     SCB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, c_ops + (size_t)i * n_items,
                                            o_ops + (size_t)i * n_items, (int)n_items, st));
+  count_launches(6);  // CUB scan: init + scan, three times
   uint64_t last[6];
   for (int i = 0; i < 3; ++i) {
     SCB_CUDA(cudaMemcpyAsync(&last[i], c_ops + (size_t)i * n_items + n_items - 1, 8,
@@ -790,9 +791,9 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
   ops.ensure(tot_ops * sizeof(uint32_t) + 128);
   skel_pos.ensure((tot_skel + 1) * sizeof(uint32_t));
   skel_ord.ensure((tot_skel + 1) * sizeof(uint64_t));
-  k_trace_emit<<<blocks, 128, 0, st>>>(d_items, n_items, cols, rows, n, k, covering, o_ops,
+  SCB_LAUNCH(k_trace_emit<<<blocks, 128, 0, st>>>(d_items, n_items, cols, rows, n, k, covering, o_ops,
                                        o_cand, o_skel, ops.as<uint32_t>(), skel_pos.as<uint32_t>(),
-                                       skel_ord.as<uint64_t>());
+                                       skel_ord.as<uint64_t>()));
   SCB_CUDA(cudaGetLastError());
   const uint32_t tail_pos = (uint32_t)tot_ops;
   SCB_CUDA(cudaMemcpyAsync(skel_pos.as<uint32_t>() + tot_skel, &tail_pos, 4, cudaMemcpyHostToDevice,
@@ -810,10 +811,10 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
                                        ((uint64_t)sm_count * per_sm)));
   const uint32_t n_chunks = (uint32_t)std::max<uint64_t>(1, (tot_ops + chunk_ops - 1) / chunk_ops);
   chunk_skel.ensure(((size_t)n_chunks + 1) * sizeof(uint32_t));
-  k_trace_chunks<<<(n_chunks + 1 + 255) / 256, 256, 0, st>>>(skel_pos.as<uint32_t>(),
+  SCB_LAUNCH(k_trace_chunks<<<(n_chunks + 1 + 255) / 256, 256, 0, st>>>(skel_pos.as<uint32_t>(),
                                                              (uint32_t)tot_skel, n_chunks,
                                                              (uint32_t)chunk_ops,
-                                                             chunk_skel.as<uint32_t>());
+                                                             chunk_skel.as<uint32_t>()));
   SCB_CUDA(cudaGetLastError());
   SCB_CUDA(cudaStreamSynchronize(st));  // tail_pos / tot_cand live on this stack frame
   out->ops = tot_ops;
@@ -898,7 +899,7 @@ void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint3
   const size_t smem = trace_smem_bytes(depth_cap, warps);
   switch (fpw) {
 #define L(F) \
-  case F: k_trace_walk<F><<<blocks, 32 * warps, smem, st>>>(a); break;
+  case F: SCB_LAUNCH(k_trace_walk<F><<<blocks, 32 * warps, smem, st>>>(a)); break;
     L(1) L(2) L(4) L(8) L(16) L(32)
 #undef L
     default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
@@ -914,10 +915,10 @@ void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const
                            cudaStream_t st) {
   (void)skel_ord;
   (void)n;
-  k_trace_finalize<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
+  SCB_LAUNCH(k_trace_finalize<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
                                                     skel_pos, nskel, (uint32_t)nr, cols, rows,
                                                     count, lambda, vals, nvals, nr, out,
-                                                    budget_out);
+                                                    budget_out));
   SCB_CUDA(cudaGetLastError());
 }
 
@@ -965,9 +966,9 @@ uint32_t trace_used_device(const uint32_t* ops, uint64_t nops, int rows, uint32_
   uint8_t* f_rt = scratch.as<uint8_t>();
   uint8_t* f_rts = f_rt + nr;
   SCB_CUDA(cudaMemsetAsync(f_rt, 0, (size_t)nr * 2, st));
-  k_trace_mark<<<sm_count * 8, 256, 0, st>>>(ops, nops, nr, f_rt, f_rts);
+  SCB_LAUNCH(k_trace_mark<<<sm_count * 8, 256, 0, st>>>(ops, nops, nr, f_rt, f_rts));
   SCB_CUDA(cudaGetLastError());
-  k_trace_used_close<<<(nr + 255) / 256, 256, 0, st>>>(rows, nr, f_rt, f_rts);
+  SCB_LAUNCH(k_trace_used_close<<<(nr + 255) / 256, 256, 0, st>>>(rows, nr, f_rt, f_rts));
   SCB_CUDA(cudaGetLastError());
   used.ensure((size_t)nr * sizeof(uint32_t) + 16);
   uint32_t* d_count = used.as<uint32_t>() + nr;
@@ -978,6 +979,7 @@ uint32_t trace_used_device(const uint32_t* ops, uint64_t nops, int rows, uint32_
   temp.ensure(tb + 16);
   SCB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota, f_rt, used.as<uint32_t>(), d_count,
                                       (int)nr, st));
+  count_launches(2);  // CUB select: init + sweep
   uint32_t n = 0;
   SCB_CUDA(cudaMemcpyAsync(&n, d_count, 4, cudaMemcpyDeviceToHost, st));
   SCB_CUDA(cudaStreamSynchronize(st));
@@ -988,7 +990,7 @@ uint32_t trace_used_device(const uint32_t* ops, uint64_t nops, int rows, uint32_
 void trace_skips_device(const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
                         uint32_t* skip, cudaStream_t st) {
   if (nskel == 0) return;
-  k_trace_skips<<<(nskel + 127) / 128, 128, 0, st>>>(ops, skel_pos, nskel, skip);
+  SCB_LAUNCH(k_trace_skips<<<(nskel + 127) / 128, 128, 0, st>>>(ops, skel_pos, nskel, skip));
   SCB_CUDA(cudaGetLastError());
 }
 
@@ -1036,7 +1038,7 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   {
     const size_t total = (size_t)nr * fpw;
     const unsigned gb = (unsigned)std::min<size_t>((total + 255) / 256, (size_t)sm_count * 8);
-    k_rest_sse<<<gb, 256, 0, st>>>(rs, rest_of, nr, fpw, reinterpret_cast<double2*>(rss));
+    SCB_LAUNCH(k_rest_sse<<<gb, 256, 0, st>>>(rs, rest_of, nr, fpw, reinterpret_cast<double2*>(rss)));
     SCB_CUDA(cudaGetLastError());
   }
   Trace2Args a;
@@ -1060,7 +1062,7 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   const int threads = 32 * trace2_warps(depth_cap);
   switch (fpw) {
 #define L(F) \
-  case F: k_trace_walk2<F><<<blocks, threads, smem, st>>>(a); break;
+  case F: SCB_LAUNCH(k_trace_walk2<F><<<blocks, threads, smem, st>>>(a)); break;
     L(1) L(2) L(4) L(8) L(16) L(32)
 #undef L
     default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
@@ -1072,9 +1074,9 @@ void trace_finalize2_launch(int fpw, int frames_in_group, uint32_t n_lanes, cons
                             const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
                             uint32_t nr, int cols, int rows, uint64_t count, const uint64_t* vals,
                             FrameBest* out, cudaStream_t st) {
-  k_trace_finalize2<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
+  SCB_LAUNCH(k_trace_finalize2<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
                                                      skel_pos, nskel, nr, cols, rows, count, vals,
-                                                     nr, out);
+                                                     nr, out));
   SCB_CUDA(cudaGetLastError());
 }
 

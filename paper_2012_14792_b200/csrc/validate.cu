@@ -174,16 +174,16 @@ __global__ void k_result_maps(const FrameBest* __restrict__ fb0, size_t fb_strid
 void validate_device(int n, const int* d_rects, int nbx, const int* d_bx, int nby, const int* d_by,
                      int cols, int rows, int* d_owner, int32_t* d_map, VCheck* d_out,
                      cudaStream_t st) {
-  k_validate<<<1, 256, 0, st>>>(n, d_rects, nbx, d_bx, nby, d_by, cols, rows, d_owner, d_map,
-                                d_out);
+  SCB_LAUNCH(k_validate<<<1, 256, 0, st>>>(n, d_rects, nbx, d_bx, nby, d_by, cols, rows, d_owner, d_map,
+                                d_out));
   SCB_CUDA(cudaGetLastError());
 }
 
 void result_maps_device(const FrameBest* d_fb, size_t fb_stride, int frames, int first_step,
                         int steps, int n, int cols, int rows, int* d_owner, int32_t* d_maps,
                         VCheck* d_out, cudaStream_t st) {
-  k_result_maps<<<dim3(frames, steps), 256, 0, st>>>(d_fb, fb_stride, frames, first_step, n, cols,
-                                                     rows, d_owner, d_maps, d_out);
+  SCB_LAUNCH(k_result_maps<<<dim3(frames, steps), 256, 0, st>>>(d_fb, fb_stride, frames, first_step, n, cols,
+                                                     rows, d_owner, d_maps, d_out));
   SCB_CUDA(cudaGetLastError());
 }
 

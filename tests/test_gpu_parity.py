@@ -41,6 +41,29 @@ def test_texture_matches_oracle(part, oracle, shape, depth):
         assert np.array_equal(g, exp), (shape, depth, f)
 
 
+@pytest.mark.parametrize("shape", [(1920, 1080, 128), (3840, 2160, 128), (129, 257, 128),
+                                   (7680, 4320, 128), (144, 128, 128)])
+@pytest.mark.parametrize("depth", [8, 10])
+@pytest.mark.parametrize("ctas", ["1", "2", "3"])
+def test_texture_tma_path_matches_oracle(part, oracle, shape, depth, ctas, monkeypatch):
+    """K1 through the TMA-staged kernel (SLICECRAFT_B200_K1=tma; the ring of 4 / 3 / 2
+    stages with 1 / 2 / 3 CTAs per SM): tensor-map zero fill handles the partial border
+    CTUs.  Same records as the oracle's ctu_stats (texture.cpp:145-169)."""
+    monkeypatch.setenv("SLICECRAFT_B200_K1", "tma")
+    monkeypatch.setenv("SLICECRAFT_B200_K1_CTAS", ctas)
+    W, H, ctu = shape
+    hi = (1 << depth)
+    dt = np.uint8 if depth == 8 else np.uint16
+    nf = 2 if W < 7680 else 1
+    frames = RNG.integers(0, hi, size=(nf, H, W)).astype(dt)
+    frames[nf - 1] = hi - 1
+    got = part.ctu_stats_batch(frames, ctu)
+    for f in range(nf):
+        exp = oracle.ctu_stats(frames[f], ctu)
+        g = np.stack([got[f]["count"], got[f]["sum"], got[f]["sumsq"]], axis=1)
+        assert np.array_equal(g, exp), (shape, depth, f)
+
+
 def test_texture_spec_kats(part):
     k = json.load(open(os.path.join(GOLDEN, "spec_kats.json")))
     c = k["constant_100"]
