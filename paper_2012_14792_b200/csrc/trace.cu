@@ -298,14 +298,28 @@ __global__ void __launch_bounds__(1024, 2) k_trace_walk(TraceArgs a) {
   }
 }
 
-__device__ __forceinline__ int64_t budget_key_t(const uint64_t* vals, uint32_t n, double b) {
+// Largest index with vals[i] <= bits(b), -1 when none: a warp-wide 32-ary
+// search (three rounds of independent loads instead of ~17 dependent ones).
+// Called by one full warp; every lane returns the result.
+__device__ __forceinline__ int64_t budget_key_warp(const uint64_t* __restrict__ vals, uint32_t n,
+                                                   double b) {
   if (!(b >= 0.0)) return -1;
+  const int lane = threadIdx.x & 31;
   const uint64_t bits = (uint64_t)__double_as_longlong(b);
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (vals[mid] <= bits) lo = mid + 1;
-    else hi = mid;
+  uint32_t lo = 0, hi = n;  // the first index with vals > bits lies in [lo, hi]
+  while (hi - lo > 0) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t probe = lo + (uint32_t)lane * step;
+    const bool le = probe < hi && vals[probe] <= bits;
+    const uint32_t m = __ballot_sync(0xffffffffu, le);
+    if (m == 0) {  // vals[lo] > bits
+      hi = lo;
+      break;
+    }
+    const int last = 31 - __clz(m);  // the last probe with vals <= bits
+    const uint32_t nlo = lo + (uint32_t)last * step + 1;
+    hi = min(hi, lo + (uint32_t)(last + 1) * step);
+    lo = nlo;
   }
   return (int64_t)lo - 1;
 }
@@ -398,14 +412,22 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
     }
     __syncthreads();
   }
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
+  if (threadIdx.x >= 64) return;
+  const int lane = threadIdx.x & 31;
   FrameBest* o = out + f;
   const uint64_t* fv = vals + (size_t)f * nr_vals;
   bk = skey[0];
   bo = sord[0];
   // step 1 keeps `t < best_t` from best_t = +inf (search.cpp:277-285)
   const bool found = bk != ~0ull && fv[bk >> 32] != 0x7ff0000000000000ull;
+  if (threadIdx.x >= 32) {  // warp 1: step 2's budget, beside warp 0's layout rebuild
+    if (found && budget_out) {
+      const double tmin = __longlong_as_double((long long)fv[bk >> 32]);
+      const int64_t bkey = budget_key_warp(fv, nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, lambda)));
+      if (lane == 0) budget_out[f] = bkey;
+    }
+    return;
+  }
   if (lane == 0) {
     o->t = found ? fv[bk >> 32] : ~0ull;
     o->sse = __longlong_as_double(0x7ff0000000000000ll);
@@ -418,10 +440,6 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
   if (!found) return;
   const uint32_t leafpos = (uint32_t)bk, leafoff = (uint32_t)(bo >> 32);
   trace_rebuild(ops, skel_pos, nskel, nr, cols, rows, leafpos, leafoff, path, fixes, o->snap);
-  if (lane == 0 && budget_out) {
-    const double tmin = __longlong_as_double((long long)o->t);
-    budget_out[f] = budget_key_t(fv, nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, lambda)));
-  }
 }
 
 // ---- step 2 ---------------------------------------------------------------------

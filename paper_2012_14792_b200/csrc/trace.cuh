@@ -36,6 +36,7 @@
 // on the host (tests/emu), together with a scalar reference interpreter.
 #pragma once
 
+#include <math.h>
 #include <stdint.h>
 
 #include "plan.h"
@@ -91,6 +92,19 @@ SCB_TR_HD int tr_skel_ld(uint32_t op) { return (int)(op & 63u); }
 
 SCB_TR_HD int tr_xw(int cols, int x0, int w) { return x0 * cols - (x0 * (x0 - 1)) / 2 + (w - 1); }
 SCB_TR_HD int tr_yh(int rows, int y0, int h) { return y0 * rows - (y0 * (y0 - 1)) / 2 + (h - 1); }
+// inverse of tr_xw / tr_yh: the origin a (largest with tr(n, a, 1) <= v) and
+// the extent v - tr(n, a, 1) + 1; closed form plus an exact fix-up
+SCB_TR_HD void tr_unrank(int n, int v, int& a, int& ext) {
+  const float b = (float)(2 * n + 1);
+  float disc = b * b - 8.0f * (float)v;
+  disc = disc > 0.0f ? disc : 0.0f;
+  int g = (int)((b - sqrtf(disc)) * 0.5f);
+  g = g < 0 ? 0 : (g > n - 1 ? n - 1 : g);
+  while (g + 1 < n && tr_xw(n, g + 1, 1) <= v) ++g;
+  while (g > 0 && tr_xw(n, g, 1) > v) --g;
+  a = g;
+  ext = v - tr_xw(n, g, 1) + 1;
+}
 
 // Counting sink (pass 1) and writing sink (pass 2) of the generator.
 struct TraceCount {
@@ -300,12 +314,8 @@ SCB_TR_HD void trace_snapshot(const uint32_t* fixes, int nfix, const uint32_t* p
   const int nyh = rows * (rows + 1) / 2;
   auto decode = [&](uint32_t idx, int& x0, int& w, int& y0, int& h) {
     const int xw = (int)(idx / (uint32_t)nyh), yh = (int)(idx % (uint32_t)nyh);
-    x0 = 0;
-    while (x0 + 1 < cols && tr_xw(cols, x0 + 1, 1) <= xw) ++x0;
-    w = xw - tr_xw(cols, x0, 1) + 1;
-    y0 = 0;
-    while (y0 + 1 < rows && tr_yh(rows, y0 + 1, 1) <= yh) ++y0;
-    h = yh - tr_yh(rows, y0, 1) + 1;
+    tr_unrank(cols, xw, x0, w);
+    tr_unrank(rows, yh, y0, h);
   };
   int cx0[SC_MAX_COLS], cw[SC_MAX_COLS], cr[SC_MAX_COLS], cs[SC_MAX_COLS], nc = 0;
   uint8_t hh[SC_MAX_SLICES];  // heights in path order, then re-ordered by column
