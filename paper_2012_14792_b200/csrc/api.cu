@@ -72,7 +72,7 @@ void validate_device(int n, const int* d_rects, int nbx, const int* d_bx, int nb
                      cudaStream_t st);
 void result_maps_device(const FrameBest* d_fb, size_t fb_stride, int frames, int first_step,
                         int steps, int n, int cols, int rows, int* d_owner, int32_t* d_maps,
-                        VCheck* d_out, cudaStream_t st);
+                        VCheck* d_out, FrameBest* h_fb, cudaStream_t st);
 void enumerate_count_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
                             double k, int covering, uint64_t* d_counts, uint64_t* d_offsets,
                             DevBuf& temp, cudaStream_t st);
@@ -1319,24 +1319,25 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   // slice-id maps (sc_result_slice_maps)
   const bool post = postcheck_enabled();
   const size_t vb = (size_t)frames * sizeof(VCheck);
+  const size_t nfb = (size_t)2 * L.groups * L.fpw;
+  ctx->h_frame_best.ensure(nfb * sizeof(FrameBest));
   if (post) {  // both steps' partitions in one launch
     ctx->slice_maps.ensure((size_t)2 * frames * cells * sizeof(int32_t));
     ctx->owner.ensure((size_t)2 * frames * cells * sizeof(int));
-    ctx->vcheck.ensure(2 * vb);
     ctx->h_vcheck.ensure(2 * vb);
+    // the kernel writes its verdicts and the FrameBest records straight into
+    // pinned host memory: no device-to-host copy on the call's critical path
     result_maps_device(ctx->frame_best.as<FrameBest>(), (size_t)L.groups * L.fpw, frames,
                        do1 ? 1 : 2, (do1 ? 1 : 0) + (do2 ? 1 : 0), cfg.n_slices, g.cols, g.rows,
                        ctx->owner.as<int>(), ctx->slice_maps.as<int32_t>(),
-                       ctx->vcheck.as<VCheck>(), s);
-    SCB_CUDA(cudaMemcpyAsync(ctx->h_vcheck.p, ctx->vcheck.p, 2 * vb, cudaMemcpyDeviceToHost, s));
+                       ctx->h_vcheck.as<VCheck>(), ctx->h_frame_best.as<FrameBest>(), s);
+  } else {
+    SCB_CUDA(cudaMemcpyAsync(ctx->h_frame_best.p, ctx->frame_best.p, nfb * sizeof(FrameBest),
+                             cudaMemcpyDeviceToHost, s));
   }
   ctx->maps_cells = cells;
   ctx->maps_frames[0] = post && do1 ? frames : 0;
   ctx->maps_frames[1] = post && do2 ? frames : 0;
-  const size_t nfb = (size_t)2 * L.groups * L.fpw;
-  ctx->h_frame_best.ensure(nfb * sizeof(FrameBest));
-  SCB_CUDA(cudaMemcpyAsync(ctx->h_frame_best.p, ctx->frame_best.p, nfb * sizeof(FrameBest),
-                           cudaMemcpyDeviceToHost, s));
   if (records_out && need_moments)
     SCB_CUDA(cudaMemcpyAsync(records_out, ctx->records.p, cells * frames * sizeof(sc_ctu_record),
                              cudaMemcpyDefault, s));

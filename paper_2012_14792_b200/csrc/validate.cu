@@ -120,11 +120,19 @@ __global__ void k_validate(int n, const int* rects, int nbx, const int* bx, int 
 // goes through the same checks, restricted to the columns the widths span.
 // blockIdx.y = step - 1 (both steps in one launch): the step's FrameBest,
 // maps and verdicts sit `fb_stride` / `frames` entries apart.
+// h_fb (optional): pinned host memory the block copies its FrameBest record
+// into, so the call needs no device-to-host copy after this kernel (out0 may
+// be pinned host memory as well).
 __global__ void k_result_maps(const FrameBest* __restrict__ fb0, size_t fb_stride, int frames,
                               int first_step, int n, int cols, int rows, int* owner0,
-                              int32_t* maps0, VCheck* out0) {
+                              int32_t* maps0, VCheck* out0, FrameBest* h_fb) {
   const int f = blockIdx.x, si = first_step - 1 + blockIdx.y;
   const FrameBest* fb = fb0 + (size_t)si * fb_stride;
+  if (h_fb && threadIdx.x < sizeof(FrameBest) / 8) {
+    static_assert(sizeof(FrameBest) % 8 == 0, "FrameBest is copied as 64-bit words");
+    reinterpret_cast<uint64_t*>(h_fb + (size_t)si * fb_stride + f)[threadIdx.x] =
+        reinterpret_cast<const uint64_t*>(fb + f)[threadIdx.x];
+  }
   const size_t cells_ = (size_t)cols * rows;
   int* owner = owner0 + (size_t)blockIdx.y * frames * cells_;
   int32_t* maps = maps0 + (size_t)si * frames * cells_;
@@ -181,9 +189,9 @@ void validate_device(int n, const int* d_rects, int nbx, const int* d_bx, int nb
 
 void result_maps_device(const FrameBest* d_fb, size_t fb_stride, int frames, int first_step,
                         int steps, int n, int cols, int rows, int* d_owner, int32_t* d_maps,
-                        VCheck* d_out, cudaStream_t st) {
+                        VCheck* d_out, FrameBest* h_fb, cudaStream_t st) {
   SCB_LAUNCH(k_result_maps<<<dim3(frames, steps), 256, 0, st>>>(d_fb, fb_stride, frames, first_step, n, cols,
-                                                     rows, d_owner, d_maps, d_out));
+                                                     rows, d_owner, d_maps, d_out, h_fb));
   SCB_CUDA(cudaGetLastError());
 }
 
