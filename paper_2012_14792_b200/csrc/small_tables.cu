@@ -53,16 +53,32 @@ __global__ void __launch_bounds__(kSmallThreads)
   // 1. f64 SAT, anti-diagonal wavefront: T = ((v + L) + U) - UL
   for (int i = threadIdx.x; i < nsat; i += blockDim.x) T[i] = 0.0;
   __syncthreads();
-  for (int s = 0; s <= cols + rows - 2; ++s) {
-    for (int y = threadIdx.x; y < rows; y += blockDim.x) {
-      const int x = s - y;
-      if (x >= 0 && x < cols) {
-        const int i = (y + 1) * stride + (x + 1);
-        T[i] = __dsub_rn(__dadd_rn(__dadd_rn(v[y * cols + x], T[i - 1]), T[i - stride]),
-                         T[i - stride - 1]);
+  if (rows <= 32) {  // one warp owns the wavefront: a warp barrier per anti-diagonal
+    if (threadIdx.x < 32) {
+      const int y = threadIdx.x;
+      for (int s = 0; s <= cols + rows - 2; ++s) {
+        const int x = s - y;
+        if (y < rows && x >= 0 && x < cols) {
+          const int i = (y + 1) * stride + (x + 1);
+          T[i] = __dsub_rn(__dadd_rn(__dadd_rn(v[y * cols + x], T[i - 1]), T[i - stride]),
+                           T[i - stride - 1]);
+        }
+        __syncwarp();
       }
     }
     __syncthreads();
+  } else {
+    for (int s = 0; s <= cols + rows - 2; ++s) {
+      for (int y = threadIdx.x; y < rows; y += blockDim.x) {
+        const int x = s - y;
+        if (x >= 0 && x < cols) {
+          const int i = (y + 1) * stride + (x + 1);
+          T[i] = __dsub_rn(__dadd_rn(__dadd_rn(v[y * cols + x], T[i - 1]), T[i - stride]),
+                           T[i - stride - 1]);
+        }
+      }
+      __syncthreads();
+    }
   }
   // 2. clamped time bits of every rectangle and their positive finite range
   uint64_t mn = ~0ull, mx = 0;
@@ -87,19 +103,22 @@ __global__ void __launch_bounds__(kSmallThreads)
   //    full bits -> the exact order of (bits, rectangle)
   const uint64_t lo = s_lo, span = s_hi > s_lo ? s_hi - s_lo : 0;
   const int need = span ? 64 - __clzll((long long)span) : 0;
-  const int sh = need > 30 ? need - 30 : 0;
+  // 20-bit keys (5 radix passes instead of 8): <= 2^18 + 1 quantised values,
+  // +inf and the padding above them; equal keys are re-sorted exactly below
+  constexpr int kQBits = 20;
+  const int sh = need > kQBits - 2 ? need - (kQBits - 2) : 0;
   uint32_t kk[kSmallItems], ki[kSmallItems];
   for (int j = 0; j < kSmallItems; ++j) {
     const int rr = threadIdx.x * kSmallItems + j;
     ki[j] = (uint32_t)rr;
-    kk[j] = 0xffffffffu;
+    kk[j] = (1u << kQBits) - 1u;
     if (rr < nr) {
       const uint64_t b = B[rr];
-      kk[j] = b == 0 ? 0u : (b >= 0x7ff0000000000000ull ? 0xfffffffeu
+      kk[j] = b == 0 ? 0u : (b >= 0x7ff0000000000000ull ? (1u << kQBits) - 2u
                                                         : 1u + (uint32_t)((b - lo) >> sh));
     }
   }
-  SmallSort(temp.sort).SortBlockedToStriped(kk, ki);
+  SmallSort(temp.sort).SortBlockedToStriped(kk, ki, 0, kQBits);
   for (int j = 0; j < kSmallItems; ++j) {
     const int pos = j * kSmallThreads + threadIdx.x;  // striped
     skey[pos] = kk[j];
