@@ -556,6 +556,12 @@ void enqueue_moment_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool
 // meet the budget.  Exact: a subtree whose fixed slices already exceed the
 // budget holds no feasible candidate, and step 1 evaluated the time of every
 // candidate of the family.  SLICECRAFT_B200_STEP2_BOUND=0 walks them all.
+// SLICECRAFT_B200_SIDE_BOUNDS=0: step 2 computes its column bounds itself
+bool side_bounds_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_SIDE_BOUNDS");
+  return !(v && v[0] == '0');
+}
+
 bool step2_bounded(const sc_search_cfg& cfg) {
   if (cfg.mode != SC_MODE_EXHAUSTIVE) return false;
   const char* v = getenv("SLICECRAFT_B200_STEP2_BOUND");
@@ -730,6 +736,22 @@ uint64_t trace_shard_count(Plan* p, int rank, int world) {
 void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
                         const Layouts& L, int step, bool compute_bounds, cudaStream_t st, int s2);
 
+// Per-frame column lower bounds (search.cu) from the time keys of every frame
+// group: they depend on the time tables only, so the exhaustive mode's
+// bounded step 2 can have them computed on the side stream while step 1 runs.
+void enqueue_column_bounds(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
+                           const Layouts& L, cudaStream_t st) {
+  const int rstride = std::min(cfg.n_slices, g.rows) + 1;
+  const size_t lb_per_group = (size_t)n_xw(g.cols) * rstride * L.fpw;
+  ctx->lbr.ensure(lb_per_group * L.groups * sizeof(uint32_t));
+  ctx->lbm.ensure(lb_per_group * L.groups * sizeof(uint32_t));
+  for (int gi = 0; gi < L.groups; ++gi)
+    column_bounds_launch(rt_of(ctx, L, gi), L.fpw, std::min(L.fpw, L.frames - gi * L.fpw), g.cols,
+                         g.rows, rstride - 1, rstride,
+                         ctx->lbr.as<uint32_t>() + gi * lb_per_group,
+                         ctx->lbm.as<uint32_t>() + gi * lb_per_group, st);
+}
+
 // One search step over all frame groups; finalize writes FrameBest[step] and,
 // after step 1, the device budgets of step 2.  No host synchronisation.
 void enqueue_step(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, Plan* plan,
@@ -875,16 +897,8 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
   if (prune) {
     ctx->inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
     ctx->seed_inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
-    if (compute_bounds) {
-      // column lower bounds from the time tables; shared incumbents to +inf
-      ctx->lbr.ensure(lb_per_group * L.groups * sizeof(uint32_t));
-      ctx->lbm.ensure(lb_per_group * L.groups * sizeof(uint32_t));
-      for (int gi = 0; gi < L.groups; ++gi)
-        column_bounds_launch(rt_of(ctx, L, gi), L.fpw,
-                             std::min(L.fpw, L.frames - gi * L.fpw), g.cols, g.rows,
-                             rstride - 1, rstride, ctx->lbr.as<uint32_t>() + gi * lb_per_group,
-                             ctx->lbm.as<uint32_t>() + gi * lb_per_group, st);
-    }
+    // column lower bounds from the time tables; shared incumbents to +inf
+    if (compute_bounds) enqueue_column_bounds(ctx, g, cfg, L, st);
     SCB_CUDA(cudaMemsetAsync(ctx->inc.p, 0xff, (size_t)L.groups * L.fpw * sizeof(uint64_t), st));
     if (step == 2) {  // shared SSE incumbents start at "none" (all-ones bits)
       ctx->sse_inc.ensure((size_t)L.groups * L.fpw * sizeof(uint64_t));
@@ -1256,6 +1270,12 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   const char* k1l = getenv("SLICECRAFT_B200_K1_LATE");
   const bool main_first =
       need_moments && luma && (!is_device_ptr(luma) || !(k1l && k1l[0] == '0'));
+  // exhaustive mode: step 1 runs the trace walk (no bounds), the bounded step
+  // 2 needs the column bounds -- computed on the side stream beside step 1
+  // (only when the main stream is enqueued first: the side stream waits for
+  // this call's time tables)
+  const bool bounds_on_side = main_first && do1 && do2 && cfg.mode == SC_MODE_EXHAUSTIVE &&
+                              step2_bounded(cfg) && side_bounds_enabled();
   auto enqueue_main = [&] {
     ctx->est.ensure((size_t)frames * cells * sizeof(double));
     SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
@@ -1302,6 +1322,11 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
     SCB_CUDA(cudaEventRecord(ev[5], s2));
     if (need_moments) enqueue_moment_tables(ctx, g, L, false, s2);
     SCB_CUDA(cudaEventRecord(ev[6], s2));
+    if (bounds_on_side) {  // after this call's time tables (ev[1], already recorded on s)
+      SCB_CUDA(cudaStreamWaitEvent(s2, ev[1], 0));
+      enqueue_column_bounds(ctx, g, cfg, L, s2);
+    }
+    SCB_CUDA(cudaEventRecord(ev[10], s2));
   };
   if (main_first) {
     enqueue_main();
@@ -1310,9 +1335,10 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
     enqueue_side();
     enqueue_main();
   }
-  SCB_CUDA(cudaStreamWaitEvent(s, ev[6], 0));  // join
+  SCB_CUDA(cudaStreamWaitEvent(s, ev[10], 0));  // join
   SCB_CUDA(cudaEventRecord(ev[8], s));
-  if (do2) enqueue_step(ctx, g, cfg, plan, L, 2, !do1 || step2_bounded(cfg), s);
+  if (do2)
+    enqueue_step(ctx, g, cfg, plan, L, 2, (!do1 || step2_bounded(cfg)) && !bounds_on_side, s);
   SCB_CUDA(cudaEventRecord(ev[3], s));
   // device post-check of the partitions this call returns (validate_partition,
   // grid.cpp:86-184, over the columns the layout spans) and their CTU ->

@@ -256,7 +256,7 @@ struct sc_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;
   cudaStream_t user_stream = nullptr;
-  cudaEvent_t ev[10] = {};
+  cudaEvent_t ev[11] = {};  // [10]: the side stream's join point
   cudaEvent_t ev_s2[3] = {};   // step-2 walk timing on the first call of a (plan, lambda)
   bool s2_pending = false;
   double s2_lambda = 0.0;
