@@ -466,7 +466,24 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   ctx->vals.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
   ctx->nvals.ensure((size_t)L.frames * sizeof(uint32_t));
   if (raw) ctx->rect_t.ensure((size_t)L.frames * L.nr * sizeof(double));
-  if (used) ctx->rk_bits_c.ensure(nu * (size_t)L.frames * sizeof(uint64_t));
+  if (used) {
+    ctx->rk_bits_c.ensure(nu * (size_t)L.frames * sizeof(uint64_t));
+    // the rectangles outside the used list keep the key "infinite": written
+    // once per (key table, used list) and outside the replayed graph -- later
+    // calls only rewrite the used entries, and the split table of an infinite
+    // key stays infinite
+    const size_t words = (size_t)L.groups * 2 * L.nr * L.fpw;
+    if (ctx->rk_inf_keys != ctx->rt_search.p || ctx->rk_inf_used != used ||
+        ctx->rk_inf_nu != nu || ctx->rk_inf_words != words) {
+      SCB_CUDA(cudaMemsetAsync(ctx->rt_search.p, 0xff, words * sizeof(uint32_t), st));
+      ctx->rk_inf_keys = ctx->rt_search.p;
+      ctx->rk_inf_used = used;
+      ctx->rk_inf_nu = nu;
+      ctx->rk_inf_words = words;
+    }
+  } else {
+    ctx->rk_inf_keys = nullptr;  // every entry is rewritten: no "infinite" filler left
+  }
   if (!graphs_enabled()) {
     enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, st);
     return;

@@ -280,6 +280,10 @@ struct sc_ctx {
   std::vector<uintptr_t> tt_key, tt_prev_key;
   cudaGraphExec_t tt_exec = nullptr;
   uint64_t tt_launches = 0;  // kernels in the captured time-table phase
+  // the key table whose unused rectangles currently hold the "infinite" key (rank.cu)
+  const void* rk_inf_keys = nullptr;
+  const void* rk_inf_used = nullptr;
+  size_t rk_inf_nu = 0, rk_inf_words = 0;
   scb::DevBuf rt_bits, vals, nvals, budget_f64;                       // time keys (rank.cu)
   scb::DevBuf rk_idx, rk_sorted, rk_flags, rk_offsets, rk_temp, rk_bits_c;  // rank.cu scratch
   scb::DevBuf flt_idx, flt_flag, flt_list, flt_count, flt_temp;      // item filter (search.cu)

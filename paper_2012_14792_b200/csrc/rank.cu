@@ -288,15 +288,32 @@ __global__ void k_rank_scatter32(const uint32_t* __restrict__ idx, const uint64_
   }
 }
 
-// bits_c[f][u] = bits[f][used[u]]
+// bits_c[f][u] = bits[f][used[u]], and the frame's positive finite range
+// (k_rank_range's job, in the same pass): blockIdx.y = frame
 __global__ void k_rank_gather(const uint64_t* __restrict__ bits, size_t nr_full,
-                              const uint32_t* __restrict__ used, size_t nu, int frames,
-                              uint64_t* __restrict__ out) {
-  const size_t total = nu * (size_t)frames;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const size_t f = i / nu, u = i % nu;
-    out[i] = bits[f * nr_full + used[u]];
+                              const uint32_t* __restrict__ used, size_t nu,
+                              uint64_t* __restrict__ out, uint64_t* lo, uint64_t* hi) {
+  const int f = blockIdx.y;
+  const uint64_t* b = bits + (size_t)f * nr_full;
+  uint64_t* o = out + (size_t)f * nu;
+  uint64_t mn = ~0ull, mx = 0;
+  for (size_t u = blockIdx.x * (size_t)blockDim.x + threadIdx.x; u < nu;
+       u += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t v = b[used[u]];
+    o[u] = v;
+    if (v != 0 && v < 0x7ff0000000000000ull) {
+      mn = v < mn ? v : mn;
+      mx = v > mx ? v : mx;
+    }
+  }
+  for (int s = 16; s > 0; s >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, s), c = __shfl_xor_sync(0xffffffffu, mx, s);
+    mn = a < mn ? a : mn;
+    mx = c > mx ? c : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mn != ~0ull) atomicMin((unsigned long long*)&lo[f], (unsigned long long)mn);
+    if (mx != 0) atomicMax((unsigned long long*)&hi[f], (unsigned long long)mx);
   }
 }
 
@@ -306,8 +323,10 @@ bool rank64_requested() {
 }
 
 // used / nu: rank only these rectangles (the ones the plan's candidates use,
-// trace.cu); every other rectangle gets the key "infinite" (all ones), which
-// bounds and walks treat as a slice no candidate can take.
+// trace.cu).  The caller keeps the other rectangles' keys "infinite" (all
+// ones: a slice no candidate takes -- api.cu enqueue_time_tables); whatever
+// they hold, no candidate reads them and a column bound (a minimum over
+// splits) stays a valid lower bound.
 void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
                        uint32_t* keys, uint64_t* vals, uint32_t* nvals, const uint32_t* used,
                        size_t nu, size_t groups, cudaStream_t st) {
@@ -316,14 +335,9 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
     return;
   }
   const size_t nr_full = nr;
+  const uint64_t* bits_full = bits_fm;
   if (used) {
     ctx->rk_bits_c.ensure(nu * (size_t)frames * sizeof(uint64_t));
-    const unsigned gb =
-        (unsigned)std::min<size_t>((nu * frames + 255) / 256, (size_t)ctx->sm_count * 8);
-    SCB_LAUNCH(k_rank_gather<<<gb, 256, 0, st>>>(bits_fm, nr_full, used, nu, frames,
-                                      ctx->rk_bits_c.as<uint64_t>()));
-    SCB_CUDA(cudaGetLastError());
-    SCB_CUDA(cudaMemsetAsync(keys, 0xff, groups * 2 * nr_full * (size_t)fpw * sizeof(uint32_t), st));
     bits_fm = ctx->rk_bits_c.as<uint64_t>();
     nr = nu;
   }
@@ -355,7 +369,11 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   SCB_CUDA(cudaMemsetAsync(lo, 0xff, (size_t)frames * sizeof(uint64_t), st));
   SCB_CUDA(cudaMemsetAsync(hi, 0, (size_t)frames * sizeof(uint64_t) + 16, st));  // + big_count
   const unsigned rb = (unsigned)std::max<size_t>(1, std::min<size_t>((nr + 255) / 256, 16));
-  SCB_LAUNCH(k_rank_range<<<dim3(rb, frames), 256, 0, st>>>(bits_fm, nr, lo, hi));
+  if (used)
+    SCB_LAUNCH(k_rank_gather<<<dim3(rb, frames), 256, 0, st>>>(
+        bits_full, nr_full, used, nu, ctx->rk_bits_c.as<uint64_t>(), lo, hi));
+  else
+    SCB_LAUNCH(k_rank_range<<<dim3(rb, frames), 256, 0, st>>>(bits_fm, nr, lo, hi));
   SCB_CUDA(cudaGetLastError());
   SCB_LAUNCH(k_rank_key32<<<blocks, 256, 0, st>>>(bits_fm, nr, frames, fbits, kbits, lo, hi, key_in, val_in));
   SCB_CUDA(cudaGetLastError());
