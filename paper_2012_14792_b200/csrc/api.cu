@@ -29,9 +29,10 @@ void texture_moments_device(const void* d_luma, int bps, int W, int H, size_t pi
                             size_t fstride, int ctu, int frames, int cols, int rows,
                             sc_ctu_record* d_out, cudaStream_t st);
 void split_table_device(uint32_t* d_keys, int cols, int rows, int groups, int fpw, int sm_count,
-                        cudaStream_t st);
+                        const uint32_t* list, size_t nl, cudaStream_t st);
 uint32_t trace_used_device(const uint32_t* ops, uint64_t nops, int rows, uint32_t nr, DevBuf& used,
-                           DevBuf& scratch, DevBuf& temp, int sm_count, cudaStream_t st);
+                           DevBuf& used_split, uint32_t* n_split, DevBuf& scratch, DevBuf& temp,
+                           int sm_count, cudaStream_t st);
 void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int frames, int fpw,
                        uint32_t* keys, uint64_t* vals, uint32_t* nvals, const uint32_t* used,
                        size_t nu, size_t groups, cudaStream_t st);
@@ -443,7 +444,8 @@ bool graphs_enabled() {
 }
 
 void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
-                              const int16_t* dec, const uint32_t* used, size_t nu, cudaStream_t st);
+                              const int16_t* dec, const uint32_t* used, size_t nu,
+                              const uint32_t* usplit, size_t nus, cudaStream_t st);
 
 // SLICECRAFT_B200_RANK_USED=0: rank every rectangle even when the plan knows
 // which ones its candidates use
@@ -457,9 +459,11 @@ bool rank_used_enabled() {
 // call repeats the previous call's shape and buffers (the steady state of a
 // frame pipeline) the phase is captured once into a CUDA graph and replayed.
 void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
-                         const uint32_t* used, size_t nu, cudaStream_t st) {
+                         const uint32_t* used, size_t nu, const uint32_t* usplit, size_t nus,
+                         cudaStream_t st) {
   const int16_t* dec = decode_table(ctx, g);
   if (!rank_used_enabled() || nu == 0 || nu >= L.nr) used = nullptr, nu = 0;
+  if (!used) usplit = nullptr, nus = 0;
   ctx->sat.ensure((size_t)L.frames * L.nsat * sizeof(double));
   ctx->rt_bits.ensure((size_t)L.frames * L.nr * sizeof(uint64_t));
   ctx->rt_search.ensure((size_t)L.groups * 2 * L.fpw * L.nr * sizeof(uint32_t));
@@ -485,7 +489,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
     ctx->rk_inf_keys = nullptr;  // every entry is rewritten: no "infinite" filler left
   }
   if (!graphs_enabled()) {
-    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, st);
+    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, usplit, nus, st);
     return;
   }
   // everything a replay depends on: shape and every buffer address
@@ -496,7 +500,8 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
       (uintptr_t)ctx->rt_search.p, (uintptr_t)ctx->vals.p, (uintptr_t)ctx->nvals.p,
       (uintptr_t)ctx->rect_t.p, (uintptr_t)ctx->rk_idx.p,
       (uintptr_t)ctx->rk_sorted.p, (uintptr_t)ctx->rk_flags.p, (uintptr_t)ctx->rk_temp.p,
-      (uintptr_t)ctx->rk_temp.bytes, (uintptr_t)used, (uintptr_t)nu, (uintptr_t)ctx->rk_bits_c.p};
+      (uintptr_t)ctx->rk_temp.bytes, (uintptr_t)used, (uintptr_t)nu, (uintptr_t)ctx->rk_bits_c.p,
+      (uintptr_t)usplit, (uintptr_t)nus};
   if (ctx->tt_exec && key == ctx->tt_key) {
     SCB_CUDA(cudaGraphLaunch(ctx->tt_exec, st));
     count_launches(ctx->tt_launches);  // the kernels of the captured phase
@@ -508,7 +513,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   }
   if (key != ctx->tt_prev_key) {
     // first call of this shape: plain launches (they size the scratch buffers)
-    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, st);
+    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, usplit, nus, st);
     ctx->tt_prev_key = key;
     return;
   }
@@ -517,7 +522,7 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
   const uint64_t launches_before = launch_counter();
   SCB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   try {
-    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, st);
+    enqueue_time_tables_body(ctx, g, L, raw, dec, used, nu, usplit, nus, st);
   } catch (...) {  // leave the stream out of capture mode before reporting
     cudaStreamEndCapture(st, &graph);
     if (graph) cudaGraphDestroy(graph);
@@ -533,7 +538,8 @@ void enqueue_time_tables(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool r
 }
 
 void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, bool raw,
-                              const int16_t* dec, const uint32_t* used, size_t nu, cudaStream_t st) {
+                              const int16_t* dec, const uint32_t* used, size_t nu,
+                              const uint32_t* usplit, size_t nus, cudaStream_t st) {
   // small grids: the whole phase in one CTA per frame (small_tables.cu);
   // SLICECRAFT_B200_SMALL_TABLES=0 keeps the general pipeline
   const char* sv = getenv("SLICECRAFT_B200_SMALL_TABLES");
@@ -552,7 +558,7 @@ void enqueue_time_tables_body(sc_ctx* ctx, const sc_grid& g, const Layouts& L, b
                     ctx->rt_search.as<uint32_t>(), ctx->vals.as<uint64_t>(),
                     ctx->nvals.as<uint32_t>(), used, nu, (size_t)L.groups, st);
   split_table_device(ctx->rt_search.as<uint32_t>(), g.cols, g.rows, L.groups, L.fpw, ctx->sm_count,
-                     st);
+                     usplit, nus, st);
 }
 
 // K2 (u64 SATs) + K3 (SSE tables) from ctx->records.
@@ -699,8 +705,9 @@ bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& c
   {  // the rectangles the candidates use (later calls rank only these)
     DevBuf sc2, tmp2;
     p->n_used = trace_used_device(p->tr_ops.as<uint32_t>(), th.ops, g.rows,
-                                  (uint32_t)((size_t)n_xw(g.cols) * n_yh(g.rows)), p->tr_used, sc2,
-                                  tmp2, ctx->sm_count, st);
+                                  (uint32_t)((size_t)n_xw(g.cols) * n_yh(g.rows)), p->tr_used,
+                                  p->tr_used_split, &p->n_used_split, sc2, tmp2, ctx->sm_count,
+                                  st);
     sc2.release();
     tmp2.release();
   }
@@ -1299,7 +1306,7 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
                              cudaMemcpyDefault, s));
     // a plan that has its trace ranks only the rectangles its candidates use
     enqueue_time_tables(ctx, g, L, false, plan->n_used ? plan->tr_used.as<uint32_t>() : nullptr,
-                        plan->n_used, s);
+                        plan->n_used, plan->tr_used_split.as<uint32_t>(), plan->n_used_split, s);
     SCB_CUDA(cudaEventRecord(ev[1], s));
     if (do1) {
       enqueue_step(ctx, g, cfg, plan, L, 1, true, s);
@@ -1532,7 +1539,7 @@ sc_ctx::~sc_ctx() {
     p->d_enum_counts.release();
     p->d_enum_offsets.release();
     for (auto* b : {&p->tr_ops, &p->tr_skel_pos, &p->tr_skel_ord, &p->tr_chunk_skel, &p->tr_skip,
-                    &p->tr_used})
+                    &p->tr_used, &p->tr_used_split})
       b->release();
     delete p;
   }
@@ -1715,7 +1722,7 @@ sc_status sc_grid_tables(sc_ctx* ctx, const sc_grid* grid, const double* est,
     ctx->est.ensure((size_t)frames * cells * sizeof(double));
     SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
                              cudaMemcpyDefault, s));
-    enqueue_time_tables(ctx, g, L, true, nullptr, 0, s);
+    enqueue_time_tables(ctx, g, L, true, nullptr, 0, nullptr, 0, s);
     if (records) {
       ctx->records.ensure(cells * frames * sizeof(sc_ctu_record));
       SCB_CUDA(cudaMemcpyAsync(ctx->records.p, records, cells * frames * sizeof(sc_ctu_record),

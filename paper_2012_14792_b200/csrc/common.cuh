@@ -170,6 +170,8 @@ struct Plan {
   DevBuf tr_skip;         // step 2: subtree ends (trace.cu k_trace_skips)
   DevBuf tr_used;         // ascending indices of the rectangles the candidates use
   uint32_t n_used = 0;    // (0: unknown -- every rectangle is ranked)
+  DevBuf tr_used_split;   // the rectangles whose split-table entry the candidates read
+  uint32_t n_used_split = 0;
   bool have_skip = false;
   // step 2's walk per lambda, measured on the first call (api.cu enqueue_step)
   std::vector<std::pair<double, int>> step2_choice;

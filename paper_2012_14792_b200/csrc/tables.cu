@@ -148,16 +148,21 @@ __global__ void k_rect_tables(const double* __restrict__ sat, const uint64_t* __
 // the forced remainder of its column, so the search scores a two-run split
 // with one load.  Same [group][rect][FPW] layout as the time table.
 // keys: [groups][2][nr][fpw] -- reads the rt half, writes the rts half
+// list / nl: only these rectangles' entries (the split entries a plan's
+// candidates read, trace.cu); nullptr: every rectangle
 __global__ void k_split_table(uint32_t* __restrict__ keys, int cols, int rows,
-                              size_t slots /* groups * fpw */, int fpw) {
+                              size_t slots /* groups * fpw */, int fpw,
+                              const uint32_t* __restrict__ list, size_t nl) {
   const int nyh = rows * (rows + 1) / 2;
   const size_t nr = (size_t)cols * (cols + 1) / 2 * nyh;
-  const size_t total = nr * slots;
+  const size_t per = list ? nl : nr;
+  const size_t total = per * slots;
   for (size_t id = blockIdx.x * (size_t)blockDim.x + threadIdx.x; id < total;
        id += (size_t)gridDim.x * blockDim.x) {
-    const size_t g = id / (nr * fpw);
-    const size_t rem = id % (nr * fpw);
-    const int rr = (int)(rem / fpw), slot = (int)(rem % fpw);
+    const size_t g = id / (per * fpw);
+    const size_t rem = id % (per * fpw);
+    const int slot = (int)(rem % fpw);
+    const int rr = list ? (int)list[rem / fpw] : (int)(rem / fpw);
     const int xw = rr / nyh, yh = rr % nyh;
     // decode (y0, h) from yh: y0 is the largest y with yh(y, 1) <= yh
     int y0 = 0;
@@ -177,13 +182,15 @@ __global__ void k_split_table(uint32_t* __restrict__ keys, int cols, int rows,
 }
 
 void split_table_device(uint32_t* d_keys, int cols, int rows, int groups, int fpw, int sm_count,
-                        cudaStream_t st) {
-  const size_t total = (size_t)cols * (cols + 1) / 2 * (rows * (rows + 1) / 2) * groups * fpw;
+                        const uint32_t* list, size_t nl, cudaStream_t st) {
+  const size_t total =
+      (list ? nl : (size_t)cols * (cols + 1) / 2 * (rows * (rows + 1) / 2)) * groups * fpw;
   size_t blocks = (total + 255) / 256;
   const size_t cap = (size_t)sm_count * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  SCB_LAUNCH(k_split_table<<<(unsigned)blocks, 256, 0, st>>>(d_keys, cols, rows, (size_t)groups * fpw, fpw));
+  SCB_LAUNCH(k_split_table<<<(unsigned)blocks, 256, 0, st>>>(d_keys, cols, rows, (size_t)groups * fpw, fpw,
+                                                  list, nl));
   SCB_CUDA(cudaGetLastError());
 }
 

@@ -977,9 +977,12 @@ __global__ void k_trace_used_close(int rows, uint32_t nr, uint8_t* __restrict__ 
   if (y0 + h < rows) used_rt[(uint32_t)(xw * nyh + tr_yh(rows, y0 + h, rows - y0 - h))] = 1;
 }
 
-// The ascending list of used rectangle indices (once per plan); returns its length.
+// The ascending lists of used rectangle indices and of the rectangles whose
+// split-table entry is read (once per plan); returns the first list's length,
+// the second's in *n_split.
 uint32_t trace_used_device(const uint32_t* ops, uint64_t nops, int rows, uint32_t nr, DevBuf& used,
-                           DevBuf& scratch, DevBuf& temp, int sm_count, cudaStream_t st) {
+                           DevBuf& used_split, uint32_t* n_split, DevBuf& scratch, DevBuf& temp,
+                           int sm_count, cudaStream_t st) {
   scratch.ensure((size_t)nr * 2 + 16);
   uint8_t* f_rt = scratch.as<uint8_t>();
   uint8_t* f_rts = f_rt + nr;
@@ -998,8 +1001,14 @@ uint32_t trace_used_device(const uint32_t* ops, uint64_t nops, int rows, uint32_
   SCB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota, f_rt, used.as<uint32_t>(), d_count,
                                       (int)nr, st));
   count_launches(2);  // CUB select: init + sweep
+  used_split.ensure((size_t)nr * sizeof(uint32_t) + 16);
+  uint32_t* d_count2 = used_split.as<uint32_t>() + nr;
+  SCB_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, iota, f_rts, used_split.as<uint32_t>(), d_count2,
+                                      (int)nr, st));
+  count_launches(2);
   uint32_t n = 0;
   SCB_CUDA(cudaMemcpyAsync(&n, d_count, 4, cudaMemcpyDeviceToHost, st));
+  SCB_CUDA(cudaMemcpyAsync(n_split, d_count2, 4, cudaMemcpyDeviceToHost, st));
   SCB_CUDA(cudaStreamSynchronize(st));
   return n;
 }
