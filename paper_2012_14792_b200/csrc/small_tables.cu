@@ -48,9 +48,13 @@ __global__ void __launch_bounds__(kSmallThreads)
   uint32_t* sidx = reinterpret_cast<uint32_t*>(T + nsat);  // [kSmallNR] sorted rectangles
   uint32_t* skey = sidx + kSmallNR;                  // [kSmallNR] sorted quantised keys
   uint32_t* rank = skey + kSmallNR;                  // [nr] rank of each rectangle
-  const double* v = est + (size_t)f * cols * rows;
+  const double* vg = est + (size_t)f * cols * rows;
   if (threadIdx.x == 0) s_lo = ~0ull, s_hi = 0;
-  // 1. f64 SAT, anti-diagonal wavefront: T = ((v + L) + U) - UL
+  // 1. f64 SAT, anti-diagonal wavefront: T = ((v + L) + U) - UL; the frame's
+  //    cells are staged in shared memory first (B is free until step 2), so
+  //    the chain of dependent steps holds no global load
+  double* v = reinterpret_cast<double*>(B);
+  for (int i = threadIdx.x; i < cols * rows; i += blockDim.x) v[i] = vg[i];
   for (int i = threadIdx.x; i < nsat; i += blockDim.x) T[i] = 0.0;
   __syncthreads();
   if (rows <= 32) {  // one warp owns the wavefront: a warp barrier per anti-diagonal

@@ -24,37 +24,63 @@ __global__ void k_grid_sat(const double* __restrict__ est, const sc_ctu_record* 
   extern __shared__ unsigned char smem[];
   const int stride = cols + 1;
   const int nsat = stride * (rows + 1);
+  const int cells = cols * rows;
   double* T = reinterpret_cast<double*>(smem);
   uint64_t* U = reinterpret_cast<uint64_t*>(T + nsat);  // 3 tables
+  // the frame's cells staged in shared memory first: the wavefront below is a
+  // chain of dependent steps, and a global load inside every step would set
+  // its pace
+  double* V = reinterpret_cast<double*>(U + 3 * nsat);        // [cells] (est)
+  uint64_t* R = reinterpret_cast<uint64_t*>(V + (est ? cells : 0));  // [3][cells] (records)
   const int f = blockIdx.x;
-  const double* v = est ? est + (size_t)f * cols * rows : nullptr;
-  const sc_ctu_record* r = rec ? rec + (size_t)f * cols * rows : nullptr;
+  const double* v = est ? est + (size_t)f * cells : nullptr;
+  const sc_ctu_record* r = rec ? rec + (size_t)f * cells : nullptr;
   for (int i = threadIdx.x; i < nsat; i += blockDim.x) {
     T[i] = 0.0;
     U[i] = 0;
     U[nsat + i] = 0;
     U[2 * nsat + i] = 0;
   }
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+    if (v) V[i] = v[i];
+    if (r) {
+      const sc_ctu_record c = r[i];
+      R[i] = c.count;
+      R[cells + i] = c.sum;
+      R[2 * cells + i] = c.sumsq;
+    }
+  }
   __syncthreads();
-  for (int s = 0; s <= cols + rows - 2; ++s) {
-    for (int y = threadIdx.x; y < rows; y += blockDim.x) {
-      const int x = s - y;
-      if (x >= 0 && x < cols) {
-        const int i = (y + 1) * stride + (x + 1);
-        if (v) {
-          const double val = v[y * cols + x];
-          T[i] = __dsub_rn(__dadd_rn(__dadd_rn(val, T[i - 1]), T[i - stride]), T[i - stride - 1]);
-        }
-        if (r) {
-          const sc_ctu_record c = r[y * cols + x];
-          U[i] = c.count + U[i - 1] + U[i - stride] - U[i - stride - 1];
-          U[nsat + i] = c.sum + U[nsat + i - 1] + U[nsat + i - stride] - U[nsat + i - stride - 1];
-          U[2 * nsat + i] =
-              c.sumsq + U[2 * nsat + i - 1] + U[2 * nsat + i - stride] - U[2 * nsat + i - stride - 1];
-        }
+  auto cell = [&](int y, int x) {
+    const int i = (y + 1) * stride + (x + 1), ci = y * cols + x;
+    if (v)
+      T[i] = __dsub_rn(__dadd_rn(__dadd_rn(V[ci], T[i - 1]), T[i - stride]), T[i - stride - 1]);
+    if (r) {
+      U[i] = R[ci] + U[i - 1] + U[i - stride] - U[i - stride - 1];
+      U[nsat + i] =
+          R[cells + ci] + U[nsat + i - 1] + U[nsat + i - stride] - U[nsat + i - stride - 1];
+      U[2 * nsat + i] = R[2 * cells + ci] + U[2 * nsat + i - 1] + U[2 * nsat + i - stride] -
+                        U[2 * nsat + i - stride - 1];
+    }
+  };
+  if (rows <= 32) {  // one warp owns the wavefront: a warp barrier per anti-diagonal
+    if (threadIdx.x < 32) {
+      const int y = threadIdx.x;
+      for (int s = 0; s <= cols + rows - 2; ++s) {
+        const int x = s - y;
+        if (y < rows && x >= 0 && x < cols) cell(y, x);
+        __syncwarp();
       }
     }
     __syncthreads();
+  } else {
+    for (int s = 0; s <= cols + rows - 2; ++s) {
+      for (int y = threadIdx.x; y < rows; y += blockDim.x) {
+        const int x = s - y;
+        if (x >= 0 && x < cols) cell(y, x);
+      }
+      __syncthreads();
+    }
   }
   for (int i = threadIdx.x; i < nsat; i += blockDim.x) {
     if (v) sat_out[(size_t)f * nsat + i] = T[i];
@@ -260,13 +286,14 @@ void partition_eval_device(const double* d_sat, const uint64_t* d_usat, const in
 void grid_sat_device(const double* d_est, const sc_ctu_record* d_rec, int cols, int rows,
                      int frames, double* d_sat, uint64_t* d_usat, cudaStream_t st) {
   const int nsat = (cols + 1) * (rows + 1);
-  const size_t smem = (size_t)nsat * (8 + 24);
+  const size_t smem = (size_t)nsat * (8 + 24) +
+                      (size_t)cols * rows * ((d_est ? 8 : 0) + (d_rec ? 24 : 0));
   if (smem > 227 * 1024) fail(SC_ERR_SIZE, "CTU grid too large for the shared-memory SAT");
   once_per_device((const void*)k_grid_sat, [] {
     SCB_CUDA(cudaFuncSetAttribute(k_grid_sat, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   227 * 1024));
   });
-  int threads = rows < 32 ? 32 : (rows > 1024 ? 1024 : ((rows + 31) / 32) * 32);
+  int threads = rows < 128 ? 128 : (rows > 1024 ? 1024 : ((rows + 31) / 32) * 32);
   SCB_LAUNCH(k_grid_sat<<<frames, threads, smem, st>>>(d_est, d_rec, cols, rows, d_sat, d_usat));
   SCB_CUDA(cudaGetLastError());
 }
