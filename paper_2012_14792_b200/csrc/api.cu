@@ -745,13 +745,12 @@ uint64_t trace_shard_count(Plan* p, int rank, int world) {
   if (world == 1) return p->trace_cands;
   const uint64_t key = ((uint64_t)rank << 32) | (uint32_t)world;
   if (p->trace_shard_key == key) return p->trace_shard_cands;
-  std::vector<uint32_t> cs(p->trace_chunks + 1);
+  // chunk records {first op, end op, SKEL op, first ordinal}; record n is the sentinel
+  std::vector<uint32_t> cs(((size_t)p->trace_chunks + 1) * 4);
   SCB_CUDA(cudaMemcpy(cs.data(), p->tr_chunk_skel.p, cs.size() * 4, cudaMemcpyDeviceToHost));
-  std::vector<uint64_t> so(p->trace_nskel + 1);
-  SCB_CUDA(cudaMemcpy(so.data(), p->tr_skel_ord.p, so.size() * 8, cudaMemcpyDeviceToHost));
   uint64_t tot = 0;
   for (uint32_t c = (uint32_t)rank; c < p->trace_chunks; c += (uint32_t)world)
-    tot += so[cs[c + 1]] - so[cs[c]];
+    tot += (uint64_t)(cs[4 * (size_t)(c + 1) + 3] - cs[4 * (size_t)c + 3]);
   p->trace_shard_key = key;
   p->trace_shard_cands = tot;
   return tot;

@@ -59,31 +59,62 @@ __global__ void k_trace_emit(const WorkItem* __restrict__ items, uint32_t n_item
   trace_item(items[it], cols, rows, n, k, covering, w);
 }
 
-// chunk c starts at the first skeleton whose first op is at or after c * size
-__global__ void k_trace_chunks(const uint32_t* __restrict__ skel_pos, uint32_t nskel,
-                               uint32_t n_chunks, uint32_t size, uint32_t* chunk_skel) {
+// Chunks may start at a skeleton's SKEL op or, inside a skeleton, at any push
+// of depth 0 (the path below it is empty: the state a walker needs there is
+// the skeleton's SKEL + FIX prologue and the candidate ordinal).  Long
+// skeletons (cfg3: up to 4,178 ops) are thus split over many warps instead of
+// setting a one-warp critical path.
+// cut[p] = 1 for a SKEL op or a depth-0 push; cnt[p] = candidates of a LEAF
+__global__ void k_trace_cuts(const uint32_t* __restrict__ ops, uint64_t nops,
+                             uint8_t* __restrict__ cut, uint32_t* __restrict__ cnt) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nops;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t op = ops[p];
+    const uint32_t code = tr_code(op);
+    cut[p] = (tr_is_push(op) && tr_small_of(op) == 0) || (code == kOpSkel && !tr_is_fix(op));
+    cnt[p] = code == kOpLeaf ? (tr_leaf_cnt(op) ? (uint32_t)tr_leaf_cnt(op) : 1u) : 0u;
+  }
+}
+
+// chunk c = {first op, end op, its skeleton's SKEL op, ordinal of its first
+// candidate}: it starts at the first cut at or after c * size; record
+// n_chunks is the sentinel {nops, nops, -, all candidates}
+__global__ void k_trace_chunks(const uint32_t* __restrict__ cutpos, uint32_t ncut,
+                               const uint32_t* __restrict__ ordp, const uint32_t* __restrict__ skel_pos,
+                               uint32_t nskel, uint32_t nops, uint32_t ncands, uint32_t n_chunks,
+                               uint32_t size, uint4* __restrict__ chunks) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c > n_chunks) return;
-  if (c == n_chunks) {
-    chunk_skel[c] = nskel;
-    return;
+  auto first_cut = [&](uint32_t cc) -> uint32_t {
+    if (cc >= n_chunks) return nops;
+    const uint64_t target = (uint64_t)cc * size;
+    uint32_t lo = 0, hi = ncut;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (cutpos[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo < ncut ? cutpos[lo] : nops;
+  };
+  const uint32_t start = first_cut(c), end = first_cut(c + 1);
+  uint4 r = make_uint4(start, end, start, ncands);
+  if (start < nops) {
+    uint32_t lo = 0, hi = nskel;  // the last skeleton starting at or before `start`
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (skel_pos[mid] <= start) lo = mid + 1;
+      else hi = mid;
+    }
+    r.z = skel_pos[lo - 1];
+    r.w = ordp[start];
   }
-  const uint64_t target = (uint64_t)c * size;
-  uint32_t lo = 0, hi = nskel;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (skel_pos[mid] < target) lo = mid + 1;
-    else hi = mid;
-  }
-  chunk_skel[c] = lo;
+  chunks[c] = r;
 }
 
 // ---- walk ------------------------------------------------------------------------
 struct TraceArgs {
   const uint32_t* ops;
-  const uint32_t* skel_pos;   // [nskel + 1] (last = total ops)
-  const uint64_t* skel_ord;   // [nskel + 1] (last = total candidates)
-  const uint32_t* chunk_skel; // [n_chunks + 1]
+  const uint4* chunks;        // [n_chunks + 1] {first op, end op, SKEL op, first ordinal}
   uint32_t n_chunks;
   uint32_t chunk_offset, chunk_stride;  // shard: chunks offset, offset + stride, ...
   uint32_t n_mine;            // chunks of this shard
@@ -176,11 +207,10 @@ __global__ void __launch_bounds__(1024, 2) k_trace_walk(TraceArgs a) {
     }
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= a.n_mine) break;
-    const uint32_t chunk = a.chunk_offset + k * a.chunk_stride;
-    const uint32_t s0 = a.chunk_skel[chunk], s1 = a.chunk_skel[chunk + 1];
-    if (s0 >= s1) continue;
-    const uint32_t b = a.skel_pos[s0], e = a.skel_pos[s1];
-    uint32_t ord = (uint32_t)a.skel_ord[s0];  // global ordinal of the next candidate
+    const uint4 rec = __ldg(a.chunks + a.chunk_offset + k * a.chunk_stride);
+    const uint32_t b = rec.x, e = rec.y;
+    if (b >= e) continue;
+    uint32_t ord = rec.w;  // global ordinal of the next candidate
     // ties: a candidate of this chunk precedes the lane's best iff the best
     // comes from a later ordinal; inside the chunk ordinals only grow
     tkey bcmp = (best != kKeyInf && best_ord > ord) ? best + 1 : best;
@@ -189,6 +219,18 @@ __global__ void __launch_bounds__(1024, 2) k_trace_walk(TraceArgs a) {
     tkey P0 = 0, Pt = 0;
     const uint32_t* Pl1 = P;
     int nbw = 32;
+    if (rec.z != b) {
+      // the chunk starts inside a skeleton (at a depth-0 push): its SKEL + FIX
+      // prologue (at most 1 + 16 ops) gives the leaf depth and P[0]
+      const uint32_t pro = __ldg(a.ops + rec.z + lane);
+      const int npro = __ffs(~__ballot_sync(0xffffffffu, tr_code(pro) == kOpSkel)) - 1;
+      const int ld = tr_skel_ld(__shfl_sync(0xffffffffu, pro, 0));
+      Pl1 = P + (ld > 0 ? ld - 1 : 0) * 32;
+      for (int q = 1; q < npro; ++q)
+        P0 = kmax(P0, __ldg(key_at(keys, tr_koff32(__shfl_sync(0xffffffffu, pro, q)) >> SH)));
+      Pt = P0;
+      P[0] = P0;
+    }
     // a leaf's minimum against the lane's best; a winner is replayed in order
     // (the first minimum wins)
     auto leaf_tail = [&](tkey m, int cnt, const uint32_t* pv, uint32_t pos) {
@@ -346,20 +388,28 @@ __device__ void trace_rebuild(const uint32_t* __restrict__ ops, const uint32_t* 
   }
   const uint32_t b = skel_pos[lo];
   const int ld = tr_skel_ld(ops[b]);
+  // The path's entry at depth d is the LAST push of depth d before the LEAF
+  // (a LEAF is only emitted after every shallower depth was pushed again), so
+  // the ops are scanned backwards from the LEAF, 32 at a time, until every
+  // depth below ld is found -- a few windows, however long the skeleton is.
   uint32_t my0 = ~0u, my1 = ~0u;
-  for (uint32_t p0 = b; p0 < leafpos; p0 += 32) {
-    const uint32_t mine = p0 + lane < leafpos ? ops[p0 + lane] : ~0u;
-    const int nb = (int)min(32u, leafpos - p0);
-    for (int q = 0; q < nb; ++q) {
+  bool f0 = lane >= ld, f1 = lane + 32 >= ld;  // depths this lane still looks for
+  for (uint32_t hi_p = leafpos; hi_p > b;) {
+    const uint32_t lo_p = hi_p - b > 32u ? hi_p - 32u : b;
+    const uint32_t mine = lo_p + lane < hi_p ? ops[lo_p + lane] : ~0u;
+    const int nb = (int)(hi_p - lo_p);
+    for (int q = nb - 1; q >= 0; --q) {
       const uint32_t op = __shfl_sync(0xffffffffu, mine, q);
       if (tr_is_push(op)) {
         const int d = tr_small_of(op);
         const uint32_t kidx = tr_kidx(op);
         const uint32_t idx = kidx >= nr ? kidx - nr : kidx;
-        if (d == lane) my0 = idx;
-        if (d == lane + 32) my1 = idx;
+        if (d == lane && !f0) my0 = idx, f0 = true;
+        if (d == lane + 32 && !f1) my1 = idx, f1 = true;
       }
     }
+    if (__all_sync(0xffffffffu, f0 && f1)) break;
+    hi_p = lo_p;
   }
   path[lane] = my0;
   path[lane + 32] = my1;
@@ -471,9 +521,7 @@ __global__ void k_trace_skips(const uint32_t* __restrict__ ops, const uint32_t* 
 struct Trace2Args {
   const uint32_t* ops;
   const uint32_t* skip;
-  const uint32_t* skel_pos;
-  const uint64_t* skel_ord;
-  const uint32_t* chunk_skel;
+  const uint4* chunks;       // [n_chunks + 1] {first op, end op, SKEL op, first ordinal}
   uint32_t n_chunks, chunk_offset, chunk_stride, n_mine;
   uint32_t* counter;
   const uint32_t* keys;      // [2][NR][FPW] time keys | split table of this frame group
@@ -540,11 +588,13 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
     if (lane == 0) k = atomicAdd(a.counter, 1u);
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= a.n_mine) break;
-    const uint32_t chunk = a.chunk_offset + k * a.chunk_stride;
-    const uint32_t s0 = a.chunk_skel[chunk], s1 = a.chunk_skel[chunk + 1];
-    if (s0 >= s1) continue;
-    const uint32_t b = a.skel_pos[s0], e = a.skel_pos[s1];
-    uint32_t ord = (uint32_t)a.skel_ord[s0];
+    const uint4 rec = __ldg(a.chunks + a.chunk_offset + k * a.chunk_stride);
+    const uint32_t b = rec.x, e = rec.y;
+    if (b >= e) continue;
+    uint32_t ord = rec.w;
+    // a chunk that starts inside a skeleton (at a depth-0 push) first runs the
+    // skeleton's SKEL + FIX prologue, then jumps to its first op
+    bool pro = rec.z != b;
     // path state: P[0] / S[0] and the top P[ld] / S[ld] in registers
     tkey P0 = 0, Pt = 0;
     double S0 = 0.0, St = 0.0;
@@ -553,7 +603,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
     uint64_t fxt = 0;         // tags of the tagged one-run columns, 4 bits each
     int nfx = 0, jl = 0;      // their number; first one with the highest tag so far
     uint32_t lasttag = 0;
-    uint32_t base = b - 32u, mine = 0;
+    uint32_t base = rec.z - 32u, mine = 0;
     auto fetch = [&](uint32_t pp) {
       if (pp - base >= 32u) {
         base = pp;
@@ -595,7 +645,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
       }
       ord += (uint32_t)cnt;
     };
-    uint32_t p = b;
+    uint32_t p = rec.z;
     while (p < e) {
       const uint32_t op = fetch(p);
       if (tr_is_push(op)) {
@@ -662,6 +712,10 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
         lasttag = 0;
       }
       ++p;
+      if (pro && tr_code(fetch(p)) != kOpSkel) {  // end of the prologue
+        p = b;
+        pro = false;
+      }
     }
     (void)ld;
   }
@@ -775,7 +829,7 @@ __global__ void k_trace_finalize2(int fpw, int frames_in_group, uint32_t n_lanes
 // nothing) when it would exceed `max_ops`.
 bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
                         double k, int covering, uint64_t max_ops, DevBuf& ops, DevBuf& skel_pos,
-                        DevBuf& skel_ord, DevBuf& chunk_skel, DevBuf& scratch, DevBuf& temp,
+                        DevBuf& skel_ord, DevBuf& chunks, DevBuf& scratch, DevBuf& temp,
                         int sm_count, TraceHost* out, cudaStream_t st) {
   scratch.ensure((size_t)n_items * 6 * sizeof(uint64_t) + 64);
   uint64_t* c_ops = scratch.as<uint64_t>();
@@ -828,12 +882,45 @@ bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int
       8192, std::max<uint64_t>(16, (tot_ops + (uint64_t)sm_count * per_sm - 1) /
                                        ((uint64_t)sm_count * per_sm)));
   const uint32_t n_chunks = (uint32_t)std::max<uint64_t>(1, (tot_ops + chunk_ops - 1) / chunk_ops);
-  chunk_skel.ensure(((size_t)n_chunks + 1) * sizeof(uint32_t));
-  SCB_LAUNCH(k_trace_chunks<<<(n_chunks + 1 + 255) / 256, 256, 0, st>>>(skel_pos.as<uint32_t>(),
-                                                             (uint32_t)tot_skel, n_chunks,
-                                                             (uint32_t)chunk_ops,
-                                                             chunk_skel.as<uint32_t>()));
-  SCB_CUDA(cudaGetLastError());
+  chunks.ensure(((size_t)n_chunks + 1) * sizeof(uint4));
+  {
+    // cut points (SKEL ops and depth-0 pushes), the ordinal of every op (a
+    // scan of the LEAF counts; the trace holds < 2^31 candidates), the chunks
+    DevBuf cutb, cntb, ordb, cutpos;
+    cutb.ensure(tot_ops + 16);
+    cntb.ensure(tot_ops * sizeof(uint32_t) + 16);
+    ordb.ensure(tot_ops * sizeof(uint32_t) + 16);
+    cutpos.ensure(tot_ops * sizeof(uint32_t) + 16);
+    SCB_LAUNCH(k_trace_cuts<<<sm_count * 8, 256, 0, st>>>(ops.as<uint32_t>(), tot_ops,
+                                                          cutb.as<uint8_t>(), cntb.as<uint32_t>()));
+    SCB_CUDA(cudaGetLastError());
+    size_t t1 = 0, t2 = 0;
+    cub::CountingInputIterator<uint32_t> iota(0);
+    uint32_t* d_ncut = cutpos.as<uint32_t>() + tot_ops;
+    SCB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, cntb.as<uint32_t>(), ordb.as<uint32_t>(),
+                                           (int)tot_ops, st));
+    SCB_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, iota, cutb.as<uint8_t>(),
+                                        cutpos.as<uint32_t>(), d_ncut, (int)tot_ops, st));
+    temp.ensure(std::max(t1, t2) + 16);
+    SCB_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, t1, cntb.as<uint32_t>(), ordb.as<uint32_t>(),
+                                           (int)tot_ops, st));
+    SCB_CUDA(cub::DeviceSelect::Flagged(temp.p, t2, iota, cutb.as<uint8_t>(),
+                                        cutpos.as<uint32_t>(), d_ncut, (int)tot_ops, st));
+    count_launches(4);
+    uint32_t ncut = 0;
+    SCB_CUDA(cudaMemcpyAsync(&ncut, d_ncut, 4, cudaMemcpyDeviceToHost, st));
+    SCB_CUDA(cudaStreamSynchronize(st));
+    SCB_LAUNCH(k_trace_chunks<<<(n_chunks + 1 + 255) / 256, 256, 0, st>>>(
+        cutpos.as<uint32_t>(), ncut, ordb.as<uint32_t>(), skel_pos.as<uint32_t>(),
+        (uint32_t)tot_skel, (uint32_t)tot_ops, (uint32_t)tot_cand, n_chunks, (uint32_t)chunk_ops,
+        chunks.as<uint4>()));
+    SCB_CUDA(cudaGetLastError());
+    SCB_CUDA(cudaStreamSynchronize(st));
+    cutb.release();
+    cntb.release();
+    ordb.release();
+    cutpos.release();
+  }
   SCB_CUDA(cudaStreamSynchronize(st));  // tail_pos / tot_cand live on this stack frame
   out->ops = tot_ops;
   out->cands = tot_cand;
@@ -887,15 +974,13 @@ int trace_blocks_per_sm(int fpw, int depth_cap, int warps) {
 }
 
 void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint32_t* ops,
-                       const uint32_t* skel_pos,
+                       const uint32_t* /*skel_pos*/,
                        const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
                        uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
                        uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st) {
   TraceArgs a;
   a.ops = ops;
-  a.skel_pos = skel_pos;
-  a.skel_ord = skel_ord;
-  a.chunk_skel = chunk_skel;
+  a.chunks = reinterpret_cast<const uint4*>(chunk_skel);
   a.n_chunks = n_chunks;
   a.chunk_offset = rank;
   a.chunk_stride = world;
@@ -1071,9 +1156,7 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   Trace2Args a;
   a.ops = ops;
   a.skip = skip;
-  a.skel_pos = skel_pos;
-  a.skel_ord = skel_ord;
-  a.chunk_skel = chunk_skel;
+  a.chunks = reinterpret_cast<const uint4*>(chunk_skel);
   a.n_chunks = n_chunks;
   a.chunk_offset = rank;
   a.chunk_stride = world;
