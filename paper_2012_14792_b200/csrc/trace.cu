@@ -167,7 +167,7 @@ __device__ __forceinline__ tkey leaf_min(const uint32_t* __restrict__ pv, int cn
 // stripes of the chunk sequence -- groups of (warps per block) ADJACENT
 // chunks, handed to its warps through a shared-memory ticket: adjacent chunks
 // share their columns' rectangles, so the warps of an SM hit each other's key
-// lines in L1.  The last ~12 % of the chunks are taken one by one from a
+// lines in L1.  The last ~40 % of the chunks are taken one by one from a
 // global counter (the dynamic tail that evens out the blocks).
 template <int FPW>
 __global__ void __launch_bounds__(1024, 2) k_trace_walk(TraceArgs a) {
@@ -985,9 +985,9 @@ void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint3
   a.chunk_offset = rank;
   a.chunk_stride = world;
   a.n_mine = n_chunks > rank ? (n_chunks - rank + world - 1) / world : 0;
-  // striped groups for the first ~88 % of the chunks, the rest dynamically
+  // striped groups for the first ~60 % of the chunks, the rest dynamically
   const uint64_t per_round = (uint64_t)blocks * warps;
-  int pct = 88;
+  int pct = 60;  // measured on cfg3 (profiles/ab_warps.sh): 88 -> 970 us, 70 -> 940, 60 -> 926, 50 -> 925
   if (const char* v = getenv("SLICECRAFT_B200_TRACE_STATIC")) pct = std::max(0, std::min(100, atoi(v)));
   a.sm_count = (uint32_t)sm_count;
   a.sm_major = 0;
