@@ -474,3 +474,47 @@ extern "C" int emu_trace_step2(int cols, int rows, int n, double k, int max_tile
   }
   return 0;
 }
+
+// tr_unrank (csrc/trace.cuh: closed form + fix-up) against the defining
+// search, for every (origin, extent) of an axis of n cells; returns the
+// number of mismatches.
+extern "C" int emu_unrank_check(int n) {
+  int bad = 0;
+  for (int a0 = 0; a0 < n; ++a0)
+    for (int e0 = 1; e0 <= n - a0; ++e0) {
+      const int v = tr_xw(n, a0, e0);
+      int a = -1, e = -1;
+      tr_unrank(n, v, a, e);
+      bad += (a != a0 || e != e0) ? 1 : 0;
+    }
+  return bad;
+}
+
+// Trace encoding round trip (csrc/trace.cuh): every field of every op kind.
+extern "C" int emu_trace_encoding_check() {
+  int bad = 0;
+  for (int d = 0; d < 64; ++d)
+    for (uint32_t kidx : {0u, 1u, 12345u, kTrKeyMask}) {
+      for (int tl = 0; tl < 2; ++tl) {
+        const uint32_t op = op_push(d, kidx, tl != 0);
+        bad += !(tr_is_push(op) && tr_code(op) == (tl ? kOpPushL : kOpPush) &&
+                 tr_small_of(op) == d && tr_kidx(op) == kidx && tr_koff32(op) == kidx * 32u);
+      }
+      if (kidx <= kTrIdxMask) {
+        const uint32_t fx = op_fix(kidx, d);
+        bad += !(tr_code(fx) == kOpSkel && tr_is_fix(fx) && !tr_is_push(fx) &&
+                 tr_small_of(fx) == d && tr_kidx(fx) == kidx);
+      }
+    }
+  for (int cnt = 0; cnt <= kTrLeafMax; ++cnt)
+    for (uint32_t kidx : {0u, 777u, kTrKeyMask}) {
+      const uint32_t op = op_leaf(kidx, cnt);
+      bad += !(tr_code(op) == kOpLeaf && !tr_is_push(op) && !tr_is_fix(op) &&
+               tr_leaf_cnt(op) == cnt && tr_kidx(op) == kidx);
+    }
+  for (int ld = 0; ld < 64; ++ld) {
+    const uint32_t op = op_skel(ld);
+    bad += !(tr_code(op) == kOpSkel && !tr_is_fix(op) && tr_skel_ld(op) == ld);
+  }
+  return bad;
+}

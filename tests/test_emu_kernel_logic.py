@@ -282,3 +282,12 @@ def test_trace_step2_matches_oracle(emu, oracle, seed):
             assert found[f], ctx
             assert t[f] == e.t_best_us and sse[f] == e.sse_best, ctx
             assert emu.slices(snap[f], n, rows) == e.best.slices(rows), ctx
+
+
+def test_trace_encoding_and_rect_decode(emu):
+    """The trace op encoding round-trips every field (csrc/trace.cuh), and the
+    closed-form rectangle decode used by the finalize kernels (tr_unrank)
+    inverts tr_xw / tr_yh for every (origin, extent) of every axis length."""
+    assert emu.L.emu_trace_encoding_check() == 0
+    for n in list(range(1, 70)) + [127, 128, 200, 255]:
+        assert emu.L.emu_unrank_check(n) == 0, n

@@ -415,6 +415,49 @@ def test_cost_ordered_schedule_keeps_first_in_order(part, oracle):
             assert out[f].candidates_step1 == e.candidates_step1
 
 
+@pytest.mark.parametrize("chunks", ["1", "64", "100000"])
+@pytest.mark.parametrize("coverage", [0, 1])
+def test_trace_chunk_cuts_inside_skeletons(oracle, chunks, coverage, monkeypatch):
+    """The trace is cut into chunks at SKEL ops and at depth-0 pushes (a chunk
+    that starts inside a skeleton replays its SKEL + FIX prologue).  Whatever
+    the chunk size (SLICECRAFT_B200_TRACE_CHUNKS, read when the plan's trace
+    is built: one chunk per SM ... 16-op chunks), both trace walks return the
+    oracle's results: t_min, argmin, (sse, t, first-in-order) winner, counts."""
+    from paper_2012_14792_b200 import CtuGrid, Partitioner, SearchConfig
+    monkeypatch.setenv("SLICECRAFT_B200_TRACE_CHUNKS", chunks)
+    monkeypatch.setenv("SLICECRAFT_B200_TRACE2", "1")
+    rng = np.random.default_rng(4178)
+    g = CtuGrid.make(14 * 64, 10 * 64, 64)
+    F = 5
+    # coarse values: many tied times and SSEs, so order decides
+    est = np.round(rng.lognormal(0, 0.4, size=(F, g.cell_count())) * 4) / 4
+    rec = np.zeros((F, g.cell_count(), 3), np.uint64)
+    rec[..., 0] = 64 * 64
+    mean = rng.integers(0, 64, size=(F, g.cell_count())).astype(np.uint64) * 16
+    rec[..., 1] = mean * 4096
+    rec[..., 2] = mean * mean * 4096 + rng.integers(0, 8, size=mean.shape).astype(np.uint64) * 4096
+    cfg = SearchConfig(n_slices=7, lambda_=0.25, k_area=3.0, max_tile_cols=0,
+                       coverage=coverage)
+    exp = [oracle.search(g.frame_width, g.frame_height, 64, est[f], rec[f], 7, 0.25, 3.0, 0,
+                         coverage, 3) for f in range(F)]
+    p = Partitioner(0)
+    try:
+        for call in range(2):
+            res = p.two_step_batch(g, est, rec, cfg)
+            for f in range(F):
+                st, e = exp[f]
+                assert st == 0
+                r = res[f]
+                assert r.t_min_us == e.t_min_us and r.t_best_us == e.t_best_us, (call, f)
+                assert r.sse_best == e.sse_best, (call, f)
+                assert r.candidates_step1 == e.candidates_step1
+                assert r.candidates_step2 == e.candidates_step2
+                assert r.best.rects() == e.best.slices(g.rows), (call, f)
+                assert r.argmin.rects() == e.argmin1.slices(g.rows), (call, f)
+    finally:
+        p.close()
+
+
 def test_cfg3_counts_all_frames(part):
     """Size-independent checks on the full cfg3 batch: counts, budget, feasibility."""
     w, tr, luma = _config_inputs(3, 32)
