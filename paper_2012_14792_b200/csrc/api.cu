@@ -103,12 +103,15 @@ void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const
 void trace_skips_device(const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
                         uint32_t* skip, cudaStream_t st);
 int trace2_blocks_per_sm(int fpw, int depth_cap);
+void rest_pairs_device(const double* rs, const uint32_t* rest_of, uint32_t nr, int fpw, double* rss,
+                       int sm_count, cudaStream_t st);
 void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skip,
                         const uint32_t* skel_pos, const uint64_t* skel_ord,
                         const uint32_t* chunk_skel, uint32_t n_chunks, uint32_t rank,
                         uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
                         const uint32_t* rest_of, double* rss, const int64_t* budget, uint32_t nr,
-                        int depth_cap, uint64_t* lanes, int sm_count, cudaStream_t st);
+                        int depth_cap, uint64_t* lanes, int sm_count, bool gather,
+                        cudaStream_t st);
 void trace_finalize2_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
                             const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
                             uint32_t nr, int cols, int rows, uint64_t count, const uint64_t* vals,
@@ -836,7 +839,7 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
                          ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw,
                          ctx->rest_of.as<uint32_t>(), ctx->rss.as<double>(),
                          ctx->budget.as<int64_t>() + (size_t)gi * L.fpw, (uint32_t)L.nr, depth_cap,
-                         lanes, ctx->sm_count, st);
+                         lanes, ctx->sm_count, !ctx->pairs_on_side, st);
       trace_finalize2_launch(L.fpw, std::min(L.fpw, L.frames - gi * L.fpw), n_lanes, lanes,
                              plan->tr_ops.as<uint32_t>(), plan->tr_skel_pos.as<uint32_t>(),
                              plan->trace_nskel, (uint32_t)L.nr, g.cols, g.rows,
@@ -1299,6 +1302,18 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
   // this call's time tables)
   const bool bounds_on_side = main_first && do1 && do2 && cfg.mode == SC_MODE_EXHAUSTIVE &&
                               step2_bounded(cfg) && side_bounds_enabled();
+  // the step-2 trace walk reads {sse, rest sse} pairs gathered per call: when
+  // it is known to be step 2's walk (the plan has its trace and this lambda's
+  // choice was measured) and there is one frame group, the side stream gathers
+  // them right after the moment tables
+  ctx->pairs_on_side = false;
+  if (do2 && need_moments && L.groups == 1 && cfg.mode == SC_MODE_EXHAUSTIVE &&
+      plan->trace_state == 1 && ctx->rest_of.p && trace2_mode() != 1) {
+    int choice = trace2_mode() == 2 ? 2 : 0;
+    for (const auto& c : plan->step2_choice)
+      if (c.first == cfg.lambda && choice == 0) choice = c.second;
+    ctx->pairs_on_side = choice == 2;
+  }
   auto enqueue_main = [&] {
     ctx->est.ensure((size_t)frames * cells * sizeof(double));
     SCB_CUDA(cudaMemcpyAsync(ctx->est.p, est, (size_t)frames * cells * sizeof(double),
@@ -1345,6 +1360,11 @@ void run_pipeline(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg, int m
     SCB_CUDA(cudaEventRecord(ev[5], s2));
     if (need_moments) enqueue_moment_tables(ctx, g, L, false, s2);
     SCB_CUDA(cudaEventRecord(ev[6], s2));
+    if (ctx->pairs_on_side) {  // the step-2 trace walk's {sse, rest sse} pairs, off the main stream
+      ctx->rss.ensure(L.nr * L.fpw * 2 * sizeof(double));
+      rest_pairs_device(ctx->rs_search.as<double>(), ctx->rest_of.as<uint32_t>(), (uint32_t)L.nr,
+                        L.fpw, ctx->rss.as<double>(), ctx->sm_count, s2);
+    }
     if (bounds_on_side) {  // after this call's time tables (ev[1], already recorded on s)
       SCB_CUDA(cudaStreamWaitEvent(s2, ev[1], 0));
       enqueue_column_bounds(ctx, g, cfg, L, s2);

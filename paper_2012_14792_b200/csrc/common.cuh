@@ -282,6 +282,7 @@ struct sc_ctx {
   std::vector<uintptr_t> tt_key, tt_prev_key;
   cudaGraphExec_t tt_exec = nullptr;
   uint64_t tt_launches = 0;  // kernels in the captured time-table phase
+  bool pairs_on_side = false;  // this call: the side stream gathers the step-2 trace walk's pairs
   // the key table whose unused rectangles currently hold the "infinite" key (rank.cu)
   const void* rk_inf_keys = nullptr;
   const void* rk_inf_used = nullptr;

@@ -1141,18 +1141,23 @@ int trace2_blocks_per_sm(int fpw, int depth_cap) {
   return nb < 1 ? 1 : nb;
 }
 
+// rss = {sse, sse of the forced rest} pairs of one frame group (k_rest_sse)
+void rest_pairs_device(const double* rs, const uint32_t* rest_of, uint32_t nr, int fpw, double* rss,
+                       int sm_count, cudaStream_t st) {
+  const size_t total = (size_t)nr * fpw;
+  const unsigned gb = (unsigned)std::min<size_t>((total + 255) / 256, (size_t)sm_count * 8);
+  SCB_LAUNCH(k_rest_sse<<<gb, 256, 0, st>>>(rs, rest_of, nr, fpw, reinterpret_cast<double2*>(rss)));
+  SCB_CUDA(cudaGetLastError());
+}
+
 void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skip,
                         const uint32_t* skel_pos, const uint64_t* skel_ord,
                         const uint32_t* chunk_skel, uint32_t n_chunks, uint32_t rank,
                         uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
                         const uint32_t* rest_of, double* rss, const int64_t* budget, uint32_t nr,
-                        int depth_cap, uint64_t* lanes, int sm_count, cudaStream_t st) {
-  {
-    const size_t total = (size_t)nr * fpw;
-    const unsigned gb = (unsigned)std::min<size_t>((total + 255) / 256, (size_t)sm_count * 8);
-    SCB_LAUNCH(k_rest_sse<<<gb, 256, 0, st>>>(rs, rest_of, nr, fpw, reinterpret_cast<double2*>(rss)));
-    SCB_CUDA(cudaGetLastError());
-  }
+                        int depth_cap, uint64_t* lanes, int sm_count, bool gather,
+                        cudaStream_t st) {
+  if (gather) rest_pairs_device(rs, rest_of, nr, fpw, rss, sm_count, st);
   Trace2Args a;
   a.ops = ops;
   a.skip = skip;
