@@ -21,8 +21,8 @@
 
 namespace scb {
 
-constexpr int kSmallThreads = 512;
-constexpr int kSmallItems = 16;
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallItems = 8;
 constexpr int kSmallNR = kSmallThreads * kSmallItems;  // 8,192 rectangles
 
 using SmallSort = cub::BlockRadixSort<uint32_t, kSmallThreads, kSmallItems, uint32_t>;
