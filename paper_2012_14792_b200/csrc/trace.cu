@@ -670,7 +670,8 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
         }
         P[(d + 1) * 32] = Pn;
         S[(d + 1) * 32] = sv;
-        Cc[d + 1] = c;
+        Cc[d + 1] = c;  // one word per warp: every lane writes the same value
+        __syncwarp();
         // no lane can meet its budget below: skip the subtree
         p = (a.skip && !__any_sync(0xffffffffu, Pn < bp1)) ? __ldg(a.skip + p) : p + 1;
         continue;
@@ -706,6 +707,7 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
         P[0] = 0;
         S[0] = 0.0;
         Cc[0] = 0;
+        __syncwarp();
         ctop = 0;
         fxt = 0;
         nfx = 0, jl = 0;
