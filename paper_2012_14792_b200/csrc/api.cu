@@ -84,14 +84,13 @@ void enumerate_emit_device(const WorkItem* d_items, uint32_t n_items, int cols, 
 // exhaustive step 1 as a trace interpreter (trace.cu)
 bool trace_build_device(const WorkItem* d_items, uint32_t n_items, int cols, int rows, int n,
                         double k, int covering, uint64_t max_ops, DevBuf& ops, DevBuf& skel_pos,
-                        DevBuf& skel_ord, DevBuf& chunk_skel, DevBuf& scratch, DevBuf& temp,
+                        DevBuf& skel_ord, DevBuf& chunks, DevBuf& scratch, DevBuf& temp,
                         int sm_count, TraceHost* out, cudaStream_t st);
 size_t trace_smem_bytes(int depth_cap, int warps);
 int trace_warps(int depth_cap, uint64_t chunks, int sm_count);
 int trace_blocks_per_sm(int fpw, int depth_cap, int warps);
 void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint32_t* ops,
-                       const uint32_t* skel_pos,
-                       const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
+                       const uint4* chunks, uint32_t n_chunks,
                        uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
                        uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st);
 void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
@@ -106,8 +105,7 @@ int trace2_blocks_per_sm(int fpw, int depth_cap);
 void rest_pairs_device(const double* rs, const uint32_t* rest_of, uint32_t nr, int fpw, double* rss,
                        int sm_count, cudaStream_t st);
 void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skip,
-                        const uint32_t* skel_pos, const uint64_t* skel_ord,
-                        const uint32_t* chunk_skel, uint32_t n_chunks, uint32_t rank,
+                        const uint4* chunks, uint32_t n_chunks, uint32_t rank,
                         uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
                         const uint32_t* rest_of, double* rss, const int64_t* budget, uint32_t nr,
                         int depth_cap, uint64_t* lanes, int sm_count, bool gather,
@@ -687,7 +685,7 @@ bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& c
   DevBuf scratch, temp;
   const bool ok = trace_build_device(p->d_items.as<WorkItem>(), (uint32_t)p->items.size(), g.cols,
                                      g.rows, cfg.n_slices, cfg.k_area, cfg.coverage, kTraceMaxOps,
-                                     p->tr_ops, p->tr_skel_pos, p->tr_skel_ord, p->tr_chunk_skel,
+                                     p->tr_ops, p->tr_skel_pos, p->tr_skel_ord, p->tr_chunks,
                                      scratch, temp, ctx->sm_count, &th, st);
   scratch.release();
   temp.release();
@@ -695,7 +693,7 @@ bool ensure_trace(sc_ctx* ctx, Plan* p, const sc_grid& g, const sc_search_cfg& c
     p->tr_ops.release();
     p->tr_skel_pos.release();
     p->tr_skel_ord.release();
-    p->tr_chunk_skel.release();
+    p->tr_chunks.release();
     return false;
   }
   if ((unsigned __int128)th.cands != plan_count(p, g, cfg))
@@ -750,7 +748,7 @@ uint64_t trace_shard_count(Plan* p, int rank, int world) {
   if (p->trace_shard_key == key) return p->trace_shard_cands;
   // chunk records {first op, end op, SKEL op, first ordinal}; record n is the sentinel
   std::vector<uint32_t> cs(((size_t)p->trace_chunks + 1) * 4);
-  SCB_CUDA(cudaMemcpy(cs.data(), p->tr_chunk_skel.p, cs.size() * 4, cudaMemcpyDeviceToHost));
+  SCB_CUDA(cudaMemcpy(cs.data(), p->tr_chunks.p, cs.size() * 4, cudaMemcpyDeviceToHost));
   uint64_t tot = 0;
   for (uint32_t c = (uint32_t)rank; c < p->trace_chunks; c += (uint32_t)world)
     tot += (uint64_t)(cs[4 * (size_t)(c + 1) + 3] - cs[4 * (size_t)c + 3]);
@@ -832,8 +830,7 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
       SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));
       uint64_t* lanes = reinterpret_cast<uint64_t*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
       trace_walk2_launch(L.fpw, blocks, plan->tr_ops.as<uint32_t>(), skipping ? skip : nullptr,
-                         plan->tr_skel_pos.as<uint32_t>(), plan->tr_skel_ord.as<uint64_t>(),
-                         plan->tr_chunk_skel.as<uint32_t>(), plan->trace_chunks,
+                         plan->tr_chunks.as<uint4>(), plan->trace_chunks,
                          (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,
                          reinterpret_cast<uint32_t*>(ctr), rt_of(ctx, L, gi),
                          ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw,
@@ -871,8 +868,7 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
       SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));
       uint64_t* lanes = reinterpret_cast<uint64_t*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
       trace_walk_launch(L.fpw, blocks, warps, ctx->sm_count, plan->tr_ops.as<uint32_t>(),
-                        plan->tr_skel_pos.as<uint32_t>(), plan->tr_skel_ord.as<uint64_t>(),
-                        plan->tr_chunk_skel.as<uint32_t>(), plan->trace_chunks,
+                        plan->tr_chunks.as<uint4>(), plan->trace_chunks,
                         (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,
                         reinterpret_cast<uint32_t*>(ctr),
                         rt_of(ctx, L, gi), (uint32_t)L.nr, depth_cap, lanes, st);
@@ -1557,7 +1553,7 @@ sc_ctx::~sc_ctx() {
     p->d_cost.release();
     p->d_enum_counts.release();
     p->d_enum_offsets.release();
-    for (auto* b : {&p->tr_ops, &p->tr_skel_pos, &p->tr_skel_ord, &p->tr_chunk_skel, &p->tr_skip,
+    for (auto* b : {&p->tr_ops, &p->tr_skel_pos, &p->tr_skel_ord, &p->tr_chunks, &p->tr_skip,
                     &p->tr_used, &p->tr_used_split})
       b->release();
     delete p;

@@ -166,7 +166,8 @@ struct Plan {
   uint64_t trace_ops = 0, trace_cands = 0;
   uint32_t trace_nskel = 0, trace_chunks = 0;
   uint64_t trace_shard_key = ~0ull, trace_shard_cands = 0;  // candidates of one shard
-  DevBuf tr_ops, tr_skel_pos, tr_skel_ord, tr_chunk_skel;
+  DevBuf tr_ops, tr_skel_pos, tr_skel_ord;
+  DevBuf tr_chunks;       // uint4 {first op, end op, SKEL op, first ordinal} per chunk + sentinel
   DevBuf tr_skip;         // step 2: subtree ends (trace.cu k_trace_skips)
   DevBuf tr_used;         // ascending indices of the rectangles the candidates use
   uint32_t n_used = 0;    // (0: unknown -- every rectangle is ranked)

@@ -4,18 +4,22 @@
 // Build (first call of a plan): one thread per work item runs the reference
 // enumeration below its width prefix twice -- counting ops, candidates and
 // skeletons, then writing them at scanned offsets -- and the trace is cut into
-// chunks of ~kChunkOps ops at skeleton starts (the interpreter's state resets
-// there), each with the global ordinal of its first candidate.
+// chunks at SKEL ops and depth-0 pushes (k_trace_cuts / k_trace_chunks), each
+// with the global ordinal of its first candidate; the rectangles the ops read
+// are listed for the per-call ranking (k_trace_mark).
 //
-// Walk (every call): persistent warps take chunks from an atomic counter; the
-// 32 lanes of a warp are frames (lanes = FPW frames x J slots), so every op is
+// Walk (every call): persistent 32-warp blocks take striped groups of
+// adjacent chunks, then single chunks from an atomic counter; the 32 lanes of
+// a warp are frames (lanes = FPW frames x J slots), so every op is
 // warp-uniform: a warp fetches 32 ops with one coalesced load and broadcasts
 // them with shuffles.  Per lane: the running maxima P[depth] (shared memory,
-// [depth][lane]), the best (time key, ordinal) and the tie threshold.  A LEAF
-// evaluates its candidates' times as one min-reduction over consecutive split-
-// table keys; only a leaf that beats the lane's best is replayed in order.
-// Every candidate's time key is loaded; the candidate set, order, ordinals and
-// first-in-order tie rule are the reference's (search.cpp:257-298).
+// [depth][lane]; P[0] and the stack top in registers), the best (time key,
+// ordinal) and the tie threshold.  A PUSHL is handled together with its LEAF;
+// a LEAF evaluates its candidates' times as one min-reduction over
+// consecutive split-table keys; only a leaf that beats the lane's best is
+// replayed in order.  Every candidate's time key is loaded; the candidate
+// set, order, ordinals and first-in-order tie rule are the reference's
+// (search.cpp:257-298).
 //
 // Finalize: per frame, the lexicographic minimum of (time key, ordinal) over
 // the lanes; the winner's layout is rebuilt from its skeleton's ops
@@ -976,13 +980,12 @@ int trace_blocks_per_sm(int fpw, int depth_cap, int warps) {
 }
 
 void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint32_t* ops,
-                       const uint32_t* /*skel_pos*/,
-                       const uint64_t* skel_ord, const uint32_t* chunk_skel, uint32_t n_chunks,
+                       const uint4* chunks, uint32_t n_chunks,
                        uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
                        uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st) {
   TraceArgs a;
   a.ops = ops;
-  a.chunks = reinterpret_cast<const uint4*>(chunk_skel);
+  a.chunks = chunks;
   a.n_chunks = n_chunks;
   a.chunk_offset = rank;
   a.chunk_stride = world;
@@ -1153,8 +1156,7 @@ void rest_pairs_device(const double* rs, const uint32_t* rest_of, uint32_t nr, i
 }
 
 void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t* skip,
-                        const uint32_t* skel_pos, const uint64_t* skel_ord,
-                        const uint32_t* chunk_skel, uint32_t n_chunks, uint32_t rank,
+                        const uint4* chunks, uint32_t n_chunks, uint32_t rank,
                         uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
                         const uint32_t* rest_of, double* rss, const int64_t* budget, uint32_t nr,
                         int depth_cap, uint64_t* lanes, int sm_count, bool gather,
@@ -1163,7 +1165,7 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   Trace2Args a;
   a.ops = ops;
   a.skip = skip;
-  a.chunks = reinterpret_cast<const uint4*>(chunk_skel);
+  a.chunks = chunks;
   a.n_chunks = n_chunks;
   a.chunk_offset = rank;
   a.chunk_stride = world;
