@@ -92,13 +92,9 @@ int trace_blocks_per_sm(int fpw, int depth_cap, int warps);
 void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint32_t* ops,
                        const uint4* chunks, uint32_t n_chunks,
                        uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
-                       uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st);
-void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
-                           const uint32_t* ops, const uint32_t* skel_pos, const uint64_t* skel_ord,
-                           uint32_t nskel, int cols, int rows, int n, uint64_t count,
-                           double lambda, const uint64_t* vals,
-                           const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
-                           cudaStream_t st);
+                       uint32_t nr, int depth_cap, uint64_t* lanes, const FinArgs* fin,
+                       uint32_t* done, cudaStream_t st);
+void trace_finalize_launch(const FinArgs& fa, cudaStream_t st);
 void trace_skips_device(const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
                         uint32_t* skip, cudaStream_t st);
 int trace2_blocks_per_sm(int fpw, int depth_cap);
@@ -109,11 +105,9 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
                         uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
                         const uint32_t* rest_of, double* rss, const int64_t* budget, uint32_t nr,
                         int depth_cap, uint64_t* lanes, int sm_count, bool gather,
-                        cudaStream_t st);
-void trace_finalize2_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
-                            const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
-                            uint32_t nr, int cols, int rows, uint64_t count, const uint64_t* vals,
-                            FrameBest* out, cudaStream_t st);
+                        const FinArgs* fin, uint32_t* done, cudaStream_t st);
+void trace_finalize2_launch(const FinArgs& fa, cudaStream_t st);
+bool trace_walk2_fuses(int fpw, int depth_cap);
 }  // namespace scb
 
 namespace scb {
@@ -586,6 +580,12 @@ bool side_bounds_enabled() {
   return !(v && v[0] == '0');
 }
 
+// SLICECRAFT_B200_FUSE_FIN=0: single-frame calls launch their finalize kernels separately
+bool fuse_finalize_enabled() {
+  const char* v = getenv("SLICECRAFT_B200_FUSE_FIN");
+  return !(v && v[0] == '0');
+}
+
 bool step2_bounded(const sc_search_cfg& cfg) {
   if (cfg.mode != SC_MODE_EXHAUSTIVE) return false;
   const char* v = getenv("SLICECRAFT_B200_STEP2_BOUND");
@@ -829,6 +829,23 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
       uint64_t* ctr = ctx->counter.as<uint64_t>() + 8 * gi + 4;
       SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));
       uint64_t* lanes = reinterpret_cast<uint64_t*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
+      const int fig = std::min(L.fpw, L.frames - gi * L.fpw);
+      FinArgs fa{};
+      fa.fpw = L.fpw;
+      fa.frames_in_group = fig;
+      fa.n_lanes = n_lanes;
+      fa.lanes = lanes;
+      fa.ops = plan->tr_ops.as<uint32_t>();
+      fa.skel_pos = plan->tr_skel_pos.as<uint32_t>();
+      fa.nskel = plan->trace_nskel;
+      fa.nr = (uint32_t)L.nr;
+      fa.cols = g.cols;
+      fa.rows = g.rows;
+      fa.count = trace_shard_count(plan, ctx->shard_rank, ctx->shard_world);
+      fa.vals = ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr;
+      fa.nr_vals = L.nr;
+      fa.out = fb + (size_t)gi * L.fpw;
+      const bool fuse = fig == 1 && trace_walk2_fuses(L.fpw, depth_cap) && fuse_finalize_enabled();
       trace_walk2_launch(L.fpw, blocks, plan->tr_ops.as<uint32_t>(), skipping ? skip : nullptr,
                          plan->tr_chunks.as<uint4>(), plan->trace_chunks,
                          (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,
@@ -836,13 +853,9 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
                          ctx->rs_search.as<double>() + (size_t)gi * L.nr * L.fpw,
                          ctx->rest_of.as<uint32_t>(), ctx->rss.as<double>(),
                          ctx->budget.as<int64_t>() + (size_t)gi * L.fpw, (uint32_t)L.nr, depth_cap,
-                         lanes, ctx->sm_count, !ctx->pairs_on_side, st);
-      trace_finalize2_launch(L.fpw, std::min(L.fpw, L.frames - gi * L.fpw), n_lanes, lanes,
-                             plan->tr_ops.as<uint32_t>(), plan->tr_skel_pos.as<uint32_t>(),
-                             plan->trace_nskel, (uint32_t)L.nr, g.cols, g.rows,
-                             trace_shard_count(plan, ctx->shard_rank, ctx->shard_world),
-                             ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr,
-                             fb + (size_t)gi * L.fpw, st);
+                         lanes, ctx->sm_count, !ctx->pairs_on_side, fuse ? &fa : nullptr,
+                         reinterpret_cast<uint32_t*>(ctr + 1), st);
+      if (!fuse) trace_finalize2_launch(fa, st);
     }
     return;
   }
@@ -867,20 +880,35 @@ void enqueue_step_walks(sc_ctx* ctx, const sc_grid& g, const sc_search_cfg& cfg,
       uint64_t* ctr = ctx->counter.as<uint64_t>() + 8 * gi;
       SCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * 4, st));
       uint64_t* lanes = reinterpret_cast<uint64_t*>(ctx->lanes.as<uint8_t>() + lane_bytes * gi);
+      const int fig = std::min(L.fpw, L.frames - gi * L.fpw);
+      FinArgs fa{};
+      fa.fpw = L.fpw;
+      fa.frames_in_group = fig;
+      fa.n_lanes = n_lanes;
+      fa.lanes = lanes;
+      fa.ops = plan->tr_ops.as<uint32_t>();
+      fa.skel_pos = plan->tr_skel_pos.as<uint32_t>();
+      fa.nskel = plan->trace_nskel;
+      fa.nr = (uint32_t)L.nr;
+      fa.cols = g.cols;
+      fa.rows = g.rows;
+      fa.count = trace_shard_count(plan, ctx->shard_rank, ctx->shard_world);
+      fa.lambda = cfg.lambda;
+      fa.vals = ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr;
+      fa.nvals = ctx->nvals.as<uint32_t>() + (size_t)gi * L.fpw;
+      fa.nr_vals = L.nr;
+      fa.out = ctx->frame_best.as<FrameBest>() + (size_t)gi * L.fpw;
+      fa.budget_out = ctx->budget.as<int64_t>() + (size_t)gi * L.fpw;
+      // a single-frame call with 256-thread blocks: the walk's last block
+      // finalizes (SLICECRAFT_B200_FUSE_FIN=0: separate launch)
+      const bool fuse = fig == 1 && L.fpw == 1 && warps == 8 && fuse_finalize_enabled();
       trace_walk_launch(L.fpw, blocks, warps, ctx->sm_count, plan->tr_ops.as<uint32_t>(),
                         plan->tr_chunks.as<uint4>(), plan->trace_chunks,
                         (uint32_t)ctx->shard_rank, (uint32_t)ctx->shard_world,
-                        reinterpret_cast<uint32_t*>(ctr),
-                        rt_of(ctx, L, gi), (uint32_t)L.nr, depth_cap, lanes, st);
-      trace_finalize_launch(L.fpw, std::min(L.fpw, L.frames - gi * L.fpw), n_lanes, lanes,
-                            plan->tr_ops.as<uint32_t>(), plan->tr_skel_pos.as<uint32_t>(),
-                            plan->tr_skel_ord.as<uint64_t>(), plan->trace_nskel, g.cols, g.rows,
-                            cfg.n_slices, trace_shard_count(plan, ctx->shard_rank,
-                                                            ctx->shard_world),
-                            cfg.lambda, ctx->vals.as<uint64_t>() + (size_t)gi * L.fpw * L.nr,
-                            ctx->nvals.as<uint32_t>() + (size_t)gi * L.fpw, L.nr,
-                            ctx->frame_best.as<FrameBest>() + (size_t)gi * L.fpw,
-                            ctx->budget.as<int64_t>() + (size_t)gi * L.fpw, st);
+                        reinterpret_cast<uint32_t*>(ctr), rt_of(ctx, L, gi), (uint32_t)L.nr,
+                        depth_cap, lanes, fuse ? &fa : nullptr,
+                        reinterpret_cast<uint32_t*>(ctr + 1), st);
+      if (!fuse) trace_finalize_launch(fa, st);
     }
     return;
   }

@@ -236,6 +236,24 @@ struct FrameBest {
   int32_t pad;
 };
 
+// What the per-frame finalize needs (k_trace_finalize); a single-frame call
+// runs it inside the walk kernel, in the last block to finish.
+struct FinArgs {
+  int fpw, frames_in_group;
+  uint32_t n_lanes;
+  const uint64_t* lanes;
+  const uint32_t* ops;
+  const uint32_t* skel_pos;
+  uint32_t nskel, nr;
+  int cols, rows;
+  uint64_t count;
+  double lambda;
+  const uint64_t* vals;
+  const uint32_t* nvals;
+  size_t nr_vals;
+  FrameBest* out;
+  int64_t* budget_out;
+};
 // Size of a plan's candidate trace (trace.cu).
 struct TraceHost {
   uint64_t ops = 0, cands = 0;

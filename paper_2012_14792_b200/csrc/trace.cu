@@ -116,6 +116,9 @@ __global__ void k_trace_chunks(const uint32_t* __restrict__ cutpos, uint32_t ncu
 }
 
 // ---- walk ------------------------------------------------------------------------
+__device__ __noinline__ void trace_finalize_frame(const FinArgs& a, int f);
+__device__ __noinline__ void trace_finalize2_frame(const FinArgs& a, int f);
+
 struct TraceArgs {
   const uint32_t* ops;
   const uint4* chunks;        // [n_chunks + 1] {first op, end op, SKEL op, first ordinal}
@@ -132,6 +135,8 @@ struct TraceArgs {
   uint32_t nr;
   int depth_cap;              // P stack entries per lane
   uint64_t* lanes;            // [warps * 32] x {time key (u64), ordinal}
+  uint32_t* done;             // fused finalize (one frame): blocks finished so far, or nullptr
+  FinArgs fin;
 };
 
 // keys + off as one IMAD.WIDE (off = an op's pre-scaled key offset)
@@ -173,7 +178,8 @@ __device__ __forceinline__ tkey leaf_min(const uint32_t* __restrict__ pv, int cn
 // share their columns' rectangles, so the warps of an SM hit each other's key
 // lines in L1.  The last ~40 % of the chunks are taken one by one from a
 // global counter (the dynamic tail that evens out the blocks).
-template <int FPW>
+// FUSE: a single-frame call (FPW 1) whose last block also finalizes.
+template <int FPW, bool FUSE>
 __global__ void __launch_bounds__(1024, 2) k_trace_walk(TraceArgs a) {
   constexpr int J = 32 / FPW;
   constexpr int SH = FPW == 32 ? 0 : FPW == 16 ? 1 : FPW == 8 ? 2 : FPW == 4 ? 3 : FPW == 2 ? 4 : 5;
@@ -342,6 +348,19 @@ __global__ void __launch_bounds__(1024, 2) k_trace_walk(TraceArgs a) {
     a.lanes[2 * ((size_t)blockIdx.x * 32 + lane)] = k0;
     a.lanes[2 * ((size_t)blockIdx.x * 32 + lane) + 1] = k1;
   }
+  if constexpr (FUSE) {
+    // single-frame call: the last block to finish reduces the blocks'
+    // records and rebuilds the winner (no separate finalize launch)
+    __shared__ uint32_t s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      trace_finalize_frame(a.fin, 0);
+    }
+  }
 }
 
 // Largest index with vals[i] <= bits(b), -1 when none: a warp-wide 32-ary
@@ -437,20 +456,14 @@ __device__ void trace_rebuild(const uint32_t* __restrict__ ops, const uint32_t* 
 // skeleton starts for the LEAF op the walk recorded), the last PUSH of every
 // depth before that LEAF (lane d owns depths d and d + 32) and the one-run
 // columns (the FIX ops after the SKEL).  The step-2 budget as in k_finalize.
-__global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
-                                 const uint64_t* __restrict__ lanes, const uint32_t* __restrict__ ops,
-                                 const uint32_t* __restrict__ skel_pos, uint32_t nskel, uint32_t nr,
-                                 int cols, int rows, uint64_t count, double lambda,
-                                 const uint64_t* __restrict__ vals, const uint32_t* __restrict__ nvals,
-                                 size_t nr_vals, FrameBest* __restrict__ out,
-                                 int64_t* __restrict__ budget_out) {
-  const int f = blockIdx.x;
-  if (f >= frames_in_group) return;
+__device__ __noinline__ void trace_finalize_frame(const FinArgs& a, int f) {
   __shared__ uint64_t skey[256], sord[256];
   __shared__ uint32_t path[64], fixes[SC_MAX_COLS];
+  const int fpw = a.fpw;
   uint64_t bk = ~0ull, bo = ~0ull;
-  for (uint32_t li = threadIdx.x * fpw + f; li < n_lanes; li += blockDim.x * fpw) {
-    const uint64_t k = lanes[2 * li], o = lanes[2 * li + 1];
+  // (__ldcg: inside the walk kernel the records were written by other blocks)
+  for (uint32_t li = threadIdx.x * fpw + f; li < a.n_lanes; li += blockDim.x * fpw) {
+    const uint64_t k = __ldcg(a.lanes + 2 * li), o = __ldcg(a.lanes + 2 * li + 1);
     if ((k >> 32) < (bk >> 32) || ((k >> 32) == (bk >> 32) && (uint32_t)o < (uint32_t)bo))
       bk = k, bo = o;
   }
@@ -468,17 +481,18 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
   }
   if (threadIdx.x >= 64) return;
   const int lane = threadIdx.x & 31;
-  FrameBest* o = out + f;
-  const uint64_t* fv = vals + (size_t)f * nr_vals;
+  FrameBest* o = a.out + f;
+  const uint64_t* fv = a.vals + (size_t)f * a.nr_vals;
   bk = skey[0];
   bo = sord[0];
   // step 1 keeps `t < best_t` from best_t = +inf (search.cpp:277-285)
   const bool found = bk != ~0ull && fv[bk >> 32] != 0x7ff0000000000000ull;
   if (threadIdx.x >= 32) {  // warp 1: step 2's budget, beside warp 0's layout rebuild
-    if (found && budget_out) {
+    if (found && a.budget_out) {
       const double tmin = __longlong_as_double((long long)fv[bk >> 32]);
-      const int64_t bkey = budget_key_warp(fv, nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, lambda)));
-      if (lane == 0) budget_out[f] = bkey;
+      const int64_t bkey =
+          budget_key_warp(fv, a.nvals[f], __dmul_rn(tmin, __dadd_rn(1.0, a.lambda)));
+      if (lane == 0) a.budget_out[f] = bkey;
     }
     return;
   }
@@ -487,13 +501,18 @@ __global__ void k_trace_finalize(int fpw, int frames_in_group, uint32_t n_lanes,
     o->sse = __longlong_as_double(0x7ff0000000000000ll);
     o->item = found ? (uint32_t)bo : ~0ull;  // the global ordinal (shard merge orders by it)
     o->ord = 0;
-    o->count = count;
-    o->scored = count * (uint64_t)fpw;
+    o->count = a.count;
+    o->scored = a.count * (uint64_t)fpw;
     o->found = found ? 1 : 0;
   }
   if (!found) return;
   const uint32_t leafpos = (uint32_t)bk, leafoff = (uint32_t)(bo >> 32);
-  trace_rebuild(ops, skel_pos, nskel, nr, cols, rows, leafpos, leafoff, path, fixes, o->snap);
+  trace_rebuild(a.ops, a.skel_pos, a.nskel, a.nr, a.cols, a.rows, leafpos, leafoff, path, fixes,
+                o->snap);
+}
+
+__global__ void k_trace_finalize(FinArgs a) {
+  if ((int)blockIdx.x < a.frames_in_group) trace_finalize_frame(a, (int)blockIdx.x);
 }
 
 // ---- step 2 ---------------------------------------------------------------------
@@ -534,6 +553,8 @@ struct Trace2Args {
   uint32_t nr;
   int depth_cap;
   uint64_t* lanes;           // per block lane: {sse bits, key << 32 | op, height << 32 | ordinal}
+  uint32_t* done;            // fused finalize (one frame): blocks finished so far
+  FinArgs fin;
 };
 
 // Step 2 (constrained_clustering_search, search.cpp:334-405) through the
@@ -552,7 +573,7 @@ struct Trace2Args {
 // candidate's loads ({key}, {sse, rest sse} as one 128-bit load) are issued
 // unconditionally, two heights at a time, so dead lanes only predicate the
 // offer.
-template <int FPW>
+template <int FPW, bool FUSE>
 __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
   constexpr int J = 32 / FPW;
   constexpr int SH = FPW == 32 ? 0 : FPW == 16 ? 1 : FPW == 8 ? 2 : FPW == 4 ? 3 : FPW == 2 ? 4 : 5;
@@ -752,6 +773,17 @@ __global__ void __launch_bounds__(256) k_trace_walk2(Trace2Args a) {
     out[1] = k0;
     out[2] = k1;
   }
+  if constexpr (FUSE) {  // single-frame call: the last block to finish also finalizes
+    __shared__ uint32_t s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      trace_finalize2_frame(a.fin, 0);
+    }
+  }
 }
 
 // rsp[r][f] = {rs[r][f], rs[rest_of[r]][f]}: a run's SSE and the SSE of its
@@ -768,18 +800,11 @@ __global__ void k_rest_sse(const double* __restrict__ rs, const uint32_t* __rest
 
 // Per frame: min (sse, key, ordinal) over the blocks' records, then the
 // winner's layout (trace_rebuild).
-__global__ void k_trace_finalize2(int fpw, int frames_in_group, uint32_t n_lanes,
-                                  const uint64_t* __restrict__ lanes,
-                                  const uint32_t* __restrict__ ops,
-                                  const uint32_t* __restrict__ skel_pos, uint32_t nskel, uint32_t nr,
-                                  int cols, int rows, uint64_t count,
-                                  const uint64_t* __restrict__ vals, size_t nr_vals,
-                                  FrameBest* __restrict__ out) {
-  const int f = blockIdx.x;
-  if (f >= frames_in_group) return;
+__device__ __noinline__ void trace_finalize2_frame(const FinArgs& a, int f) {
   __shared__ double ssse[256];
   __shared__ uint64_t skey[256], sord[256];
   __shared__ uint32_t path[64], fixes[SC_MAX_COLS];
+  const int fpw = a.fpw;
   auto less = [](double as, uint64_t a0, uint64_t a1, double bs, uint64_t b0, uint64_t b1) {
     if (a0 == ~0ull) return false;
     if (b0 == ~0ull) return true;
@@ -789,10 +814,12 @@ __global__ void k_trace_finalize2(int fpw, int frames_in_group, uint32_t n_lanes
   };
   double bs = 0.0;
   uint64_t bk = ~0ull, bo = ~0ull;
-  for (uint32_t li = threadIdx.x * fpw + f; li < n_lanes; li += blockDim.x * fpw) {
-    const uint64_t* r = lanes + 3 * (size_t)li;
-    const double as = __longlong_as_double((long long)r[0]);
-    if (less(as, r[1], r[2], bs, bk, bo)) bs = as, bk = r[1], bo = r[2];
+  // (__ldcg: inside the walk kernel the records were written by other blocks)
+  for (uint32_t li = threadIdx.x * fpw + f; li < a.n_lanes; li += blockDim.x * fpw) {
+    const uint64_t* r = a.lanes + 3 * (size_t)li;
+    const uint64_t r0 = __ldcg(r), r1 = __ldcg(r + 1), r2 = __ldcg(r + 2);
+    const double as = __longlong_as_double((long long)r0);
+    if (less(as, r1, r2, bs, bk, bo)) bs = as, bk = r1, bo = r2;
   }
   ssse[threadIdx.x] = bs;
   skey[threadIdx.x] = bk;
@@ -810,23 +837,27 @@ __global__ void k_trace_finalize2(int fpw, int frames_in_group, uint32_t n_lanes
   }
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
-  FrameBest* o = out + f;
+  FrameBest* o = a.out + f;
   bs = ssse[0];
   bk = skey[0];
   bo = sord[0];
   const bool found = bk != ~0ull;
   if (lane == 0) {
-    o->t = found ? vals[(size_t)f * nr_vals + (bk >> 32)] : ~0ull;
+    o->t = found ? a.vals[(size_t)f * a.nr_vals + (bk >> 32)] : ~0ull;
     o->sse = bs;
     o->item = found ? (uint32_t)bo : ~0ull;
     o->ord = 0;
-    o->count = count;
-    o->scored = count * (uint64_t)fpw;
+    o->count = a.count;
+    o->scored = a.count * (uint64_t)fpw;
     o->found = found ? 1 : 0;
   }
   if (!found) return;
-  trace_rebuild(ops, skel_pos, nskel, nr, cols, rows, (uint32_t)bk, (uint32_t)(bo >> 32), path,
-                fixes, o->snap);
+  trace_rebuild(a.ops, a.skel_pos, a.nskel, a.nr, a.cols, a.rows, (uint32_t)bk,
+                (uint32_t)(bo >> 32), path, fixes, o->snap);
+}
+
+__global__ void k_trace_finalize2(FinArgs a) {
+  if ((int)blockIdx.x < a.frames_in_group) trace_finalize2_frame(a, (int)blockIdx.x);
 }
 
 // ---- host side -------------------------------------------------------------------
@@ -951,7 +982,7 @@ int trace_warps(int depth_cap, uint64_t chunks, int sm_count) {
     const int x = atoi(v);
     if (x == 1 || x == 2 || x == 4 || x == 8 || x == 16 || x == 32) nw = x;
   }
-  const size_t lim = (size_t)max_dynamic_smem((const void*)k_trace_walk<32>);
+  const size_t lim = (size_t)max_dynamic_smem((const void*)k_trace_walk<32, false>);
   while (nw > 1 && trace_smem_bytes(depth_cap, nw) > lim) nw >>= 1;
   return nw;
 }
@@ -959,9 +990,9 @@ int trace_warps(int depth_cap, uint64_t chunks, int sm_count) {
 // deep skeletons (n up to 64) need more than the 48 KB default per block
 template <int F>
 static void trace_attrs() {
-  once_per_device((const void*)k_trace_walk<F>, [] {
-    SCB_CUDA(cudaFuncSetAttribute(k_trace_walk<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  max_dynamic_smem((const void*)k_trace_walk<F>)));
+  once_per_device((const void*)k_trace_walk<F, false>, [] {
+    SCB_CUDA(cudaFuncSetAttribute(k_trace_walk<F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_dynamic_smem((const void*)k_trace_walk<F, false>)));
   });
 }
 
@@ -971,7 +1002,7 @@ int trace_blocks_per_sm(int fpw, int depth_cap, int warps) {
 #define OCC(F)                                                                                  \
   if (fpw == F) {                                                                               \
     trace_attrs<F>();                                                                           \
-    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk<F>, 32 * warps,    \
+    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk<F, false>, 32 * warps,    \
                                                            smem));                              \
   }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
@@ -979,11 +1010,18 @@ int trace_blocks_per_sm(int fpw, int depth_cap, int warps) {
   return nb < 1 ? 1 : nb;
 }
 
+// fin / done: when given, the last block to finish runs the finalize of the
+// call's single frame (blocks of 256 threads only; *done zeroed by the caller)
 void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint32_t* ops,
                        const uint4* chunks, uint32_t n_chunks,
                        uint32_t rank, uint32_t world, uint32_t* counter, const uint32_t* keys,
-                       uint32_t nr, int depth_cap, uint64_t* lanes, cudaStream_t st) {
+                       uint32_t nr, int depth_cap, uint64_t* lanes, const FinArgs* fin,
+                       uint32_t* done, cudaStream_t st) {
   TraceArgs a;
+  if (fpw != 1 || warps != 8) fin = nullptr;  // the fused kernel: one frame, 256-thread blocks
+  a.done = fin ? done : nullptr;
+  if (fin) a.fin = *fin;
+  else a.fin = FinArgs{};
   a.ops = ops;
   a.chunks = chunks;
   a.n_chunks = n_chunks;
@@ -1007,26 +1045,28 @@ void trace_walk_launch(int fpw, int blocks, int warps, int sm_count, const uint3
   const size_t smem = trace_smem_bytes(depth_cap, warps);
   switch (fpw) {
 #define L(F) \
-  case F: SCB_LAUNCH(k_trace_walk<F><<<blocks, 32 * warps, smem, st>>>(a)); break;
-    L(1) L(2) L(4) L(8) L(16) L(32)
+  case F: SCB_LAUNCH(k_trace_walk<F, false><<<blocks, 32 * warps, smem, st>>>(a)); break;
+    L(2) L(4) L(8) L(16) L(32)
 #undef L
+    case 1:
+      if (a.done) {
+        once_per_device((const void*)k_trace_walk<1, true>, [] {
+          SCB_CUDA(cudaFuncSetAttribute(k_trace_walk<1, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        max_dynamic_smem((const void*)k_trace_walk<1, true>)));
+        });
+        SCB_LAUNCH(k_trace_walk<1, true><<<blocks, 32 * warps, smem, st>>>(a));
+      } else {
+        SCB_LAUNCH(k_trace_walk<1, false><<<blocks, 32 * warps, smem, st>>>(a));
+      }
+      break;
     default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
   }
   SCB_CUDA(cudaGetLastError());
 }
 
-void trace_finalize_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
-                           const uint32_t* ops, const uint32_t* skel_pos, const uint64_t* skel_ord,
-                           uint32_t nskel, int cols, int rows, int n, uint64_t count,
-                           double lambda, const uint64_t* vals,
-                           const uint32_t* nvals, size_t nr, FrameBest* out, int64_t* budget_out,
-                           cudaStream_t st) {
-  (void)skel_ord;
-  (void)n;
-  SCB_LAUNCH(k_trace_finalize<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
-                                                    skel_pos, nskel, (uint32_t)nr, cols, rows,
-                                                    count, lambda, vals, nvals, nr, out,
-                                                    budget_out));
+void trace_finalize_launch(const FinArgs& fa, cudaStream_t st) {
+  SCB_LAUNCH(k_trace_finalize<<<fa.frames_in_group, 256, 0, st>>>(fa));
   SCB_CUDA(cudaGetLastError());
 }
 
@@ -1117,7 +1157,7 @@ size_t trace2_warp_bytes(int depth_cap) {
   return (size_t)depth_cap * 32 * (sizeof(double) + sizeof(uint32_t));
 }
 int trace2_warps(int depth_cap) {
-  const int lim = max_dynamic_smem((const void*)k_trace_walk2<32>);
+  const int lim = max_dynamic_smem((const void*)k_trace_walk2<32, false>);
   return std::max(1, std::min(8, (int)(lim / trace2_warp_bytes(depth_cap))));
 }
 size_t trace2_smem_bytes(int depth_cap) {
@@ -1126,9 +1166,9 @@ size_t trace2_smem_bytes(int depth_cap) {
 
 template <int F>
 static void trace2_attrs() {
-  once_per_device((const void*)k_trace_walk2<F>, [] {
-    SCB_CUDA(cudaFuncSetAttribute(k_trace_walk2<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  max_dynamic_smem((const void*)k_trace_walk2<F>)));
+  once_per_device((const void*)k_trace_walk2<F, false>, [] {
+    SCB_CUDA(cudaFuncSetAttribute(k_trace_walk2<F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_dynamic_smem((const void*)k_trace_walk2<F, false>)));
   });
 }
 
@@ -1138,7 +1178,7 @@ int trace2_blocks_per_sm(int fpw, int depth_cap) {
 #define OCC(F)                                                                                   \
   if (fpw == F) {                                                                                \
     trace2_attrs<F>();                                                                           \
-    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk2<F>,              \
+    SCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_trace_walk2<F, false>,              \
                                                            32 * trace2_warps(depth_cap), smem)); \
   }
   OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
@@ -1160,7 +1200,7 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
                         uint32_t world, uint32_t* counter, const uint32_t* keys, const double* rs,
                         const uint32_t* rest_of, double* rss, const int64_t* budget, uint32_t nr,
                         int depth_cap, uint64_t* lanes, int sm_count, bool gather,
-                        cudaStream_t st) {
+                        const FinArgs* fin, uint32_t* done, cudaStream_t st) {
   if (gather) rest_pairs_device(rs, rest_of, nr, fpw, rss, sm_count, st);
   Trace2Args a;
   a.ops = ops;
@@ -1179,23 +1219,38 @@ void trace_walk2_launch(int fpw, int blocks, const uint32_t* ops, const uint32_t
   a.lanes = lanes;
   const size_t smem = trace2_smem_bytes(depth_cap);
   const int threads = 32 * trace2_warps(depth_cap);
+  if (fpw != 1 || threads != 256) fin = nullptr;  // the fused kernel: one frame, 256-thread blocks
+  a.done = fin ? done : nullptr;
+  a.fin = fin ? *fin : FinArgs{};
   switch (fpw) {
 #define L(F) \
-  case F: SCB_LAUNCH(k_trace_walk2<F><<<blocks, threads, smem, st>>>(a)); break;
-    L(1) L(2) L(4) L(8) L(16) L(32)
+  case F: SCB_LAUNCH(k_trace_walk2<F, false><<<blocks, threads, smem, st>>>(a)); break;
+    L(2) L(4) L(8) L(16) L(32)
 #undef L
+    case 1:
+      if (fin) {
+        once_per_device((const void*)k_trace_walk2<1, true>, [] {
+          SCB_CUDA(cudaFuncSetAttribute(k_trace_walk2<1, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        max_dynamic_smem((const void*)k_trace_walk2<1, true>)));
+        });
+        SCB_LAUNCH(k_trace_walk2<1, true><<<blocks, threads, smem, st>>>(a));
+      } else {
+        SCB_LAUNCH(k_trace_walk2<1, false><<<blocks, threads, smem, st>>>(a));
+      }
+      break;
     default: fail(SC_ERR_INTERNAL, "bad frames-per-warp");
   }
   SCB_CUDA(cudaGetLastError());
 }
 
-void trace_finalize2_launch(int fpw, int frames_in_group, uint32_t n_lanes, const uint64_t* lanes,
-                            const uint32_t* ops, const uint32_t* skel_pos, uint32_t nskel,
-                            uint32_t nr, int cols, int rows, uint64_t count, const uint64_t* vals,
-                            FrameBest* out, cudaStream_t st) {
-  SCB_LAUNCH(k_trace_finalize2<<<frames_in_group, 256, 0, st>>>(fpw, frames_in_group, n_lanes, lanes, ops,
-                                                     skel_pos, nskel, nr, cols, rows, count, vals,
-                                                     nr, out));
+// true when trace_walk2_launch will run the fused (walk + finalize) kernel
+bool trace_walk2_fuses(int fpw, int depth_cap) {
+  return fpw == 1 && 32 * trace2_warps(depth_cap) == 256;
+}
+
+void trace_finalize2_launch(const FinArgs& fa, cudaStream_t st) {
+  SCB_LAUNCH(k_trace_finalize2<<<fa.frames_in_group, 256, 0, st>>>(fa));
   SCB_CUDA(cudaGetLastError());
 }
 
