@@ -198,19 +198,33 @@ __device__ __forceinline__ bool bits_less(uint64_t a, uint32_t ia, uint64_t b, u
 }
 
 // Group starts: small groups sorted in place by (bits, index); large ones
-// queued for k_rank_big.
+// queued for k_rank_big.  The first-of-run flags come out of the same pass: a
+// group's first element always starts a run (a smaller q is a smaller time),
+// and inside a group the sorting thread compares neighbours; a group whose
+// bits are all equal (tied times: a uniform estimate map ties every rectangle
+// of the same area) needs no sorting at all.
 __global__ void k_rank_groups(const uint32_t* __restrict__ key, uint32_t* __restrict__ idx,
                               const uint64_t* __restrict__ bits, size_t total,
-                              uint32_t* big_count, uint2* big_list) {
+                              uint32_t* big_count, uint2* big_list,
+                              uint32_t* __restrict__ flags) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const uint32_t k = key[i];
     if (i > 0 && key[i - 1] == k) continue;
+    flags[i] = 1u;
+    if (i + 1 >= total || key[i + 1] != k) continue;  // a group of one
+    const uint64_t b0 = bits[idx[i]];
+    bool alleq = true;
     size_t j = i + 1;
-    while (j < total && key[j] == k && j - i <= kSmallGroup) ++j;
-    if (j - i == 1) continue;
-    if (j - i > kSmallGroup) {
-      while (j < total && key[j] == k) ++j;
+    while (j < total && key[j] == k) {
+      alleq = alleq && bits[idx[j]] == b0;
+      ++j;
+    }
+    if (alleq) {  // one run
+      for (size_t a = i + 1; a < j; ++a) flags[a] = 0u;
+      continue;
+    }
+    if (j - i > kSmallGroup) {  // k_rank_big sorts it and writes its flags
       const uint32_t slot = atomicAdd(big_count, 1u);
       big_list[slot] = make_uint2((uint32_t)i, (uint32_t)(j - i));
       continue;
@@ -230,15 +244,19 @@ __global__ void k_rank_groups(const uint32_t* __restrict__ key, uint32_t* __rest
       gb[b + 1] = be;
       gi[b + 1] = e;
     }
-    for (int a = 0; a < n; ++a) idx[i + a] = gi[a];
+    for (int a = 0; a < n; ++a) {
+      idx[i + a] = gi[a];
+      if (a > 0) flags[i + a] = gb[a] != gb[a - 1] ? 1u : 0u;
+    }
   }
 }
 
 // Large groups: the position of every element is the number of group
-// elements before it in (bits, index) order.  One block per group at a time.
+// elements before it in (bits, index) order.  One block per group at a time;
+// then the group's first-of-run flags (its first element's is already set).
 __global__ void k_rank_big(uint32_t* __restrict__ idx, const uint64_t* __restrict__ bits,
                            const uint32_t* big_count, const uint2* __restrict__ big_list,
-                           uint32_t* __restrict__ tmp) {
+                           uint32_t* __restrict__ tmp, uint32_t* __restrict__ flags) {
   for (uint32_t g = blockIdx.x; g < *big_count; g += gridDim.x) {
     const uint2 gr = big_list[g];
     for (uint32_t a = threadIdx.x; a < gr.y; a += blockDim.x) {
@@ -254,14 +272,10 @@ __global__ void k_rank_big(uint32_t* __restrict__ idx, const uint64_t* __restric
     __syncthreads();
     for (uint32_t a = threadIdx.x; a < gr.y; a += blockDim.x) idx[gr.x + a] = tmp[gr.x + a];
     __syncthreads();
+    for (uint32_t a = 1 + threadIdx.x; a < gr.y; a += blockDim.x)
+      flags[gr.x + a] = bits[idx[gr.x + a]] != bits[idx[gr.x + a - 1]] ? 1u : 0u;
+    __syncthreads();
   }
-}
-
-__global__ void k_rank_flags32(const uint32_t* __restrict__ idx, const uint64_t* __restrict__ bits,
-                               uint32_t* __restrict__ flags, size_t nr, size_t total) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x)
-    flags[i] = (i % nr == 0 || bits[idx[i]] != bits[idx[i - 1]]) ? 1u : 0u;
 }
 
 // nr: ranked rectangles per frame; nr_full / used: the grid's rectangle count
@@ -385,11 +399,10 @@ void rank_times_device(sc_ctx* ctx, const uint64_t* bits_fm, size_t nr, int fram
   SCB_CUDA(cub::DeviceRadixSort::SortPairs(ctx->rk_temp.p, b1, key_in, key_out, val_in, idx,
                                            (int)total, 0, kbits, st));
   count_launches(2 + (kbits + 7) / 8);  // CUB onesweep: histogram, exclusive sum, one kernel per 8-bit pass
-  SCB_LAUNCH(k_rank_groups<<<blocks, 256, 0, st>>>(key_out, idx, bits_fm, total, big_count, big_list));
+  SCB_LAUNCH(k_rank_groups<<<blocks, 256, 0, st>>>(key_out, idx, bits_fm, total, big_count, big_list,
+                                                flags));
   SCB_CUDA(cudaGetLastError());
-  SCB_LAUNCH(k_rank_big<<<ctx->sm_count, 256, 0, st>>>(idx, bits_fm, big_count, big_list, tmp));
-  SCB_CUDA(cudaGetLastError());
-  SCB_LAUNCH(k_rank_flags32<<<blocks, 256, 0, st>>>(idx, bits_fm, flags, nr, total));
+  SCB_LAUNCH(k_rank_big<<<ctx->sm_count, 256, 0, st>>>(idx, bits_fm, big_count, big_list, tmp, flags));
   SCB_CUDA(cudaGetLastError());
   SCB_CUDA(cub::DeviceScan::InclusiveSum(ctx->rk_temp.p, b3, flags, scan, (int)total, st));
   count_launches(2);  // CUB scan: init + scan
